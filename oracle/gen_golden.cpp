@@ -1,0 +1,123 @@
+// gen_golden.cpp — generates tests/golden/ref_toy.json by running the
+// REFERENCE's own code (compiled from /root/reference/proj/src by
+// oracle/Makefile into oracle/_ref/). TEST INFRASTRUCTURE ONLY.
+//
+// The fixture pins oracle/mrsp_oracle.c (the CPU restatement) and the B200
+// toy path to the reference bit for bit: shard plans (engine.cpp:15-29), pad
+// rows (engine.cpp:31-50), synthetic frames (mmseq.cpp:58-72), encoder and
+// policy init (policy.cpp:12-34, :56-61), encode_frame (policy.cpp:36-47),
+// serial_prefill/step_logits (engine.cpp:59-71, policy.cpp:85-119),
+// log_softmax (common.hpp:95-104) and cache/bench counters (engine.cpp:155-283).
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+
+#include "json.hpp"
+#include "lvrl/engine.hpp"
+
+using namespace lvrl;
+using json = nlohmann::ordered_json;
+
+int main(int argc, char** argv) {
+  const char* path = argc > 1 ? argv[1] : "ref_toy.json";
+  json j;
+
+  // plan_shards hand examples + the big token plans of the BASELINE configs.
+  json plans = json::array();
+  for (auto [n, k] : std::vector<std::pair<std::size_t, int>>{
+           {10, 3}, {2, 4}, {0, 3}, {7, 1}, {131104, 8}, {65568, 4}, {139301, 8}, {16421 + 8 * 1024, 2}}) {
+    auto p = mrsp::plan_shards(n, k);
+    json r = json::array();
+    for (auto [b, e] : p.ranges) r.push_back({b, e});
+    plans.push_back({{"n", n}, {"k", k}, {"ranges", r}});
+  }
+  j["plan_shards"] = plans;
+
+  {
+    std::vector<std::vector<TokenId>> rows = {{5, 6, 7}, {8}, {9, 10, 11, 12, 13}, {}};
+    auto b = mrsp::pad_batch(rows);
+    j["pad_batch"] = {{"rows_in", rows}, {"rows", b.rows}, {"lengths", b.lengths},
+                      {"max_len", b.max_len}};
+  }
+
+  {
+    Rng r = Rng::substream(7, "video");
+    j["substream_7_video_first"] = std::to_string(r.next_u64());
+    auto v = mmseq::gen_video(7, 2, 4);
+    json fr = json::array();
+    for (auto& f : v.frames) fr.push_back(f.features);
+    j["gen_video_7_2_4"] = {{"id", v.id}, {"frames", fr}};
+  }
+
+  // Encoder + encode of a small video.
+  {
+    auto enc = policy::EncoderParams::generate(1234, 8, 16);
+    auto v = mmseq::gen_video(9, 5, 16);
+    auto e = mrsp::serial_encode(enc, v);
+    j["encoder_1234_8_16"] = enc.w;
+    j["encode_v9f5"] = e;
+  }
+  // A bench-shaped encode (d 128, p 256) for 3 frames.
+  {
+    auto enc = policy::EncoderParams::generate(1234, 128, 256);
+    auto v = mmseq::gen_video(1234 + 64 * 100, 3, 256);
+    j["encode_bench_shape"] = mrsp::serial_encode(enc, v);
+  }
+
+  // Policy init + step_logits + log_softmax.
+  {
+    policy::PolicyDims dims{32, 8, 12, 16};
+    auto params = policy::PolicyParams::random(dims, 4, 0.4);
+    j["policy_32_8_12_seed4"] = params.theta;
+    Vec ctx(dims.d, 0.1);
+    auto logits = policy::step_logits(params, ctx, mmseq::Vocab::kEos);
+    j["step_logits_ctx01_eos"] = logits;
+    j["log_softmax_of_that"] = log_softmax(logits);
+
+    // serial_prefill on a ragged batch (one empty row included).
+    std::vector<std::vector<TokenId>> rows = {{5, 6, 7, 30}, {9}, {}, {11, 12, 13, 14, 15, 16}};
+    auto batch = mrsp::pad_batch(rows);
+    std::vector<Vec> contexts;
+    Rng rng(77);
+    for (std::size_t i = 0; i < rows.size(); ++i) {
+      Vec c(dims.d);
+      for (double& x : c) x = rng.normal();
+      contexts.push_back(c);
+    }
+    auto out = mrsp::serial_prefill(params, contexts, batch);
+    json o = json::array();
+    for (auto& r : out) o.push_back(r);
+    j["prefill"] = {{"rows", rows}, {"contexts", contexts}, {"logits", o}};
+
+    // context_vector over an encoded video + question template {10,11,12}.
+    auto enc = policy::EncoderParams::generate(2, 8, 16);
+    auto v = mmseq::gen_video(3, 4, 16);
+    mmseq::MultimodalSequence seq;
+    seq.frame_embeddings = mrsp::serial_encode(enc, v);
+    seq.text_tokens = {10, 11, 12};
+    j["context_vector"] = policy::context_vector(seq, params);
+  }
+
+  // Cache counter script (test_engine.cpp:189-221 shape) on the reference engine.
+  {
+    auto enc = policy::EncoderParams::generate(7, 8, 16);
+    mrsp::WorkerGroup group(2, enc);
+    mrsp::EmbeddingCache cache;
+    auto a = mmseq::gen_video(1, 6, 16), b = mmseq::gen_video(2, 6, 16);
+    auto plan = mrsp::plan_shards(6, 2);
+    json script = json::array();
+    for (auto* v : {&a, &a, &b, &a, &b}) {
+      bool hit = cache.get_or_encode(group, *v, plan).second;
+      script.push_back({{"video", v->id}, {"hit", hit},
+                        {"invocations", group.stats().encoder_invocations.load()},
+                        {"misses", group.stats().cache_misses.load()},
+                        {"hits", group.stats().cache_hits.load()},
+                        {"gather_bytes", group.stats().gather_bytes.load()}});
+    }
+    j["cache_script"] = script;
+  }
+
+  std::ofstream(path) << j.dump(1) << "\n";
+  std::cout << "wrote " << path << "\n";
+  return 0;
+}

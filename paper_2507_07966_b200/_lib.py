@@ -1,0 +1,117 @@
+"""ctypes binding of libmrsp_b200.so (include/mrsp_c.h).
+
+The library is built in-tree by ``paper_2507_07966_b200/csrc/Makefile`` (see
+``__graft_entry__.build``). There is no fallback: if the shared object is
+missing, importing the engine raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_lib" / "libmrsp_b200.so"
+
+c_u64p = ctypes.POINTER(ctypes.c_uint64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_f64p = ctypes.POINTER(ctypes.c_double)
+c_f32p = ctypes.POINTER(ctypes.c_float)
+
+STATUS = {
+    0: "MRSP_OK",
+    1: "MRSP_INVALID_ARGUMENT",
+    2: "MRSP_RUNTIME_ERROR",
+    3: "MRSP_OUT_OF_RANGE",
+    4: "MRSP_LOGIC_ERROR",
+    5: "MRSP_CUDA_ERROR",
+    6: "MRSP_NCCL_ERROR",
+    7: "MRSP_OUT_OF_MEMORY",
+    8: "MRSP_NO_DEVICE",
+}
+
+
+class MrspError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class InvalidArgument(MrspError, ValueError):
+    """Mirrors std::invalid_argument (engine.cpp:16, :32, :74, :80-83, :107-112)."""
+
+
+class GatherError(MrspError):
+    """Mirrors std::runtime_error from all_gather (engine.cpp:133-142)."""
+
+
+_lib = None
+
+# (name, restype, argtypes) for every symbol include/mrsp_c.h declares.
+SIGNATURES: dict = {}
+
+
+def _sig(name, argtypes, restype=ctypes.c_int):
+    SIGNATURES[name] = (restype, argtypes)
+
+
+_sig("mrsp_last_error", [], ctypes.c_char_p)
+_sig("mrsp_version", [], ctypes.c_char_p)
+_sig("mrsp_device_count", [], ctypes.c_int)
+_sig("mrsp_plan_shards", [ctypes.c_uint64, ctypes.c_int, c_u64p])
+_sig("mrsp_toy_encode", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, c_f64p, ctypes.c_uint64,
+                         c_u64p, c_f64p, c_u64p])
+_sig("mrsp_toy_prefill", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_f64p,
+                          c_i32p, c_u64p, ctypes.c_uint64, ctypes.c_uint64, c_u64p, c_f64p, c_u64p])
+
+
+def _register_more():
+    """Signatures for the transformer-path entry points (declared lazily so this
+    module stays importable while the header grows)."""
+    from . import _abi_ext  # noqa: F401  (populates SIGNATURES)
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (the B200 engine has no CPU fallback)")
+        # libcudart / libcuda come from the CUDA toolkit or torch's bundle.
+        l = ctypes.CDLL(str(LIB_PATH), mode=ctypes.RTLD_GLOBAL)
+        try:
+            _register_more()
+        except ImportError:
+            pass
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().mrsp_last_error().decode()
+    if status == 1:
+        raise InvalidArgument(status, msg)
+    if status == 2 and msg.startswith("all_gather"):
+        raise GatherError(status, msg)
+    raise MrspError(status, msg)
+
+
+def ptr(arr, ctype):
+    """Pointer to a C-contiguous numpy array's data."""
+    assert arr.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+    return arr.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def device_count() -> int:
+    return int(lib().mrsp_device_count())
+
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "LAZY")

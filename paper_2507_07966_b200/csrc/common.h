@@ -1,0 +1,61 @@
+// common.h — status plumbing shared by every translation unit of libmrsp_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "mrsp_c.h"
+
+namespace mrsp {
+
+// Exception carrying an mrsp_status; converted at the C-ABI edge.
+struct Error : std::runtime_error {
+  mrsp_status code;
+  Error(mrsp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+[[noreturn]] inline void fail(mrsp_status c, const std::string& m) { throw Error(c, m); }
+
+inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error in %s (%s:%d): %s", what, file, line,
+                  cudaGetErrorString(e));
+    fail(e == cudaErrorMemoryAllocation ? MRSP_OUT_OF_MEMORY : MRSP_CUDA_ERROR, buf);
+  }
+}
+
+// Runs f, mapping exceptions onto a status + thread-local message.
+template <typename F>
+mrsp_status guard(F&& f) {
+  try {
+    f();
+    set_last_error("");
+    return MRSP_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return MRSP_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return MRSP_RUNTIME_ERROR;
+  }
+}
+
+// Ensures a CUDA device exists; the product has no CPU fallback.
+void require_device();
+
+}  // namespace mrsp
+
+#define MRSP_CUDA(x) ::mrsp::check_cuda((x), #x, __FILE__, __LINE__)
+#define MRSP_REQUIRE(cond, code, msg) \
+  do {                                \
+    if (!(cond)) ::mrsp::fail(code, msg); \
+  } while (0)
