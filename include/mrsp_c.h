@@ -92,6 +92,46 @@ mrsp_status mrsp_toy_prefill(int sp_degree, const double* theta, int V, int d, i
                              const uint64_t* lengths, uint64_t n_rows, uint64_t max_len,
                              const uint64_t* ranges, double* out, uint64_t* pad_reads);
 
+/* ------------------------------------------------------------------------
+ * Device operators of the transformer-shaped path (dev pointers, async on
+ * `stream`). They are the building blocks the engine below chains; exported
+ * so the parity tests can check each kernel in isolation.
+ * ------------------------------------------------------------------------ */
+typedef enum {
+  GEMM_EPI_STORE_BF16 = 0,     /* C = A.B^T                                 */
+  GEMM_EPI_BIAS_BF16 = 1,      /* C = A.B^T + bias                          */
+  GEMM_EPI_BIAS_GELU_BF16 = 2, /* C = gelu_tanh(A.B^T + bias)               */
+  GEMM_EPI_RESID_F32 = 3,      /* resid(fp32) += A.B^T (+ bias)             */
+  GEMM_EPI_SWIGLU_BF16 = 4,    /* per 256-col tile [gate128|up128]:
+                                  C[:, tile*128 + j] = silu(g_j) * u_j      */
+  GEMM_EPI_STORE_F32 = 5       /* C(fp32) = A.B^T (+ bias)                  */
+} mrsp_gemm_epilogue;
+
+/* tcgen05 BF16 GEMM, fp32 accumulate: A[M][lda], B[N][ldb] (both K-major),
+ * C per epilogue. K, lda, ldb multiples of 8. Replaces the per-position
+ * scalar contractions of hidden_state/step_logits (policy.cpp:85-119) and
+ * encode_frame (policy.cpp:36-47) in the transformer-shaped model. */
+mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
+                              int ldb, int ldc, int epilogue, const float* bias, float* resid,
+                              int ldr, void* stream);
+
+typedef enum {
+  ATTN_CAUSAL_PREFIX = 0, /* k <= q && (k < Lp || row(k) == row(q)), row(x) = (x-Lp)/Lmax */
+  ATTN_BLOCK_DIAG = 1     /* q / blk == k / blk (bidirectional within a frame)          */
+} mrsp_attn_mask;
+
+/* tcgen05 flash-attention forward, head dim 128, bf16 in/out, fp32 softmax.
+ * Query head h reads Q columns [q_col0 + 128h, +128) and kv head h / q_per_kv
+ * of K/V; writes O columns [o_col0 + 128h, +128). L rows (tokens). The
+ * CAUSAL_PREFIX mask is the MR-SP packed GRPO group: the shared prompt prefix
+ * (video + question, Lp tokens) followed by G rollout rows padded to Lmax.
+ * Replaces the prefix pooling of context_vector (policy.cpp:63-80) that the
+ * reference shares across the G rows (grpo.cpp:53). */
+mrsp_status mrsp_op_attention(const void* Q, int ldq, int q_col0, const void* K, int ldk,
+                              int k_col0, const void* V, int ldv, int v_col0, void* O, int ldo,
+                              int o_col0, int L, int n_heads, int q_per_kv, float scale, int mode,
+                              int Lp, int Lmax, int blk, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

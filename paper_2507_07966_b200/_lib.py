@@ -64,6 +64,15 @@ _sig("mrsp_toy_encode", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, c_f64
                          c_u64p, c_f64p, c_u64p])
 _sig("mrsp_toy_prefill", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_f64p,
                           c_i32p, c_u64p, ctypes.c_uint64, ctypes.c_uint64, c_u64p, c_f64p, c_u64p])
+_sig("mrsp_op_gemm_bf16", [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                           ctypes.c_void_p])
+_sig("mrsp_op_attention", [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_float, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_void_p])
 
 
 def _register_more():

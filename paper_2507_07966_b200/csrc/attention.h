@@ -1,0 +1,26 @@
+// attention.h — internal interface of the tcgen05 flash-attention (csrc/attention.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mrsp_c.h"
+
+namespace mrsp {
+
+struct AttnParams {
+  const void* Q;  // [L][ldq] bf16; head h at columns q_col0 + 128 h
+  int ldq, q_col0;
+  const void* K;  // [L][ldk] bf16; kv head g at columns k_col0 + 128 g
+  int ldk, k_col0;
+  const void* V;
+  int ldv, v_col0;
+  void* O;  // [L][ldo] bf16; head h written at o_col0 + 128 h
+  int ldo, o_col0;
+  int L, n_heads, q_per_kv;
+  float scale;
+  int mode, Lp, Lmax, blk;
+};
+
+void attention_fwd(const AttnParams& p, cudaStream_t stream);
+
+}  // namespace mrsp

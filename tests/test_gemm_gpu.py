@@ -1,0 +1,62 @@
+"""GPU: tcgen05 GEMM (csrc/gemm.cu) vs a plain PyTorch fp32 reference."""
+import pytest
+import torch
+
+from paper_2507_07966_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def ref(A, B):
+    return A.float() @ B.float().T
+
+
+def rel_err(x, y):
+    return ((x.float() - y.float()).norm() / (y.float().norm() + 1e-12)).item()
+
+
+SHAPES = [(128, 256, 64), (256, 512, 128), (300, 700, 200), (1000, 1152, 1152), (77, 4608, 3584),
+          (4096, 4096, 4096), (515, 32, 256), (16384, 1152, 592)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_store(gpu, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    C = ops.gemm(A, B, ops.EPI_STORE_F32)
+    torch.cuda.synchronize()
+    assert rel_err(C, ref(A, B)) < 1e-5
+    Cb = ops.gemm(A, B)
+    assert rel_err(Cb, ref(A, B)) < 5e-3
+
+
+def test_gemm_epilogues(gpu):
+    M, N, K = 300, 512, 320
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    r = ref(A, B)
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_BF16, bias=bias), r + bias) < 5e-3
+    gelu = torch.nn.functional.gelu(r + bias, approximate="tanh")
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_GELU_BF16, bias=bias), gelu) < 5e-3
+    resid = torch.randn(M, N, device="cuda")
+    want = resid + r
+    ops.gemm(A, B, ops.EPI_RESID_F32, resid=resid)
+    assert rel_err(resid, want) < 1e-5
+    resid2 = torch.randn(M, N, device="cuda")
+    want2 = resid2 + r + bias
+    ops.gemm(A, B, ops.EPI_RESID_F32, resid=resid2, bias=bias)
+    assert rel_err(resid2, want2) < 1e-5
+    out = ops.gemm(A, B, ops.EPI_SWIGLU_BF16)
+    rr = r.view(M, N // 256, 2, 128)
+    sw = (torch.nn.functional.silu(rr[:, :, 0]) * rr[:, :, 1]).reshape(M, N // 2)
+    assert rel_err(out, sw) < 5e-3
+
+
+def test_gemm_strided_operands(gpu):
+    # A is a column slice of a wider buffer (e.g. one head of a packed QKV).
+    X = torch.randn(512, 1024, device="cuda").bfloat16()
+    A = X[:, 256:768]
+    B = torch.randn(384, 512, device="cuda").bfloat16()
+    assert rel_err(ops.gemm(A, B, ops.EPI_STORE_F32), ref(A, B)) < 1e-5
