@@ -57,6 +57,11 @@ int mrsp_device_count(void);
  * ------------------------------------------------------------------------ */
 mrsp_status mrsp_plan_shards(uint64_t n_items, int sp_degree, uint64_t* ranges);
 
+/* Synthetic video frames exactly as mmseq::gen_video (mmseq.cpp:58-72):
+ * frames*feature_dim values 2u-1, u from Rng::substream(seed, "video")
+ * (common.hpp:19-79), rounded to fp32. Host function. */
+mrsp_status mrsp_gen_video(uint64_t seed, int frames, int feature_dim, float* out);
+
 /* ------------------------------------------------------------------------
  * Toy-model path (the reference's own model, fp64, bit-exact to its CPU).
  * Ranks are CUDA streams on the current device; each rank runs exactly its
@@ -104,7 +109,8 @@ typedef enum {
   GEMM_EPI_RESID_F32 = 3,      /* resid(fp32) += A.B^T (+ bias)             */
   GEMM_EPI_SWIGLU_BF16 = 4,    /* per 256-col tile [gate128|up128]:
                                   C[:, tile*128 + j] = silu(g_j) * u_j      */
-  GEMM_EPI_STORE_F32 = 5       /* C(fp32) = A.B^T (+ bias)                  */
+  GEMM_EPI_STORE_F32 = 5,      /* C(fp32) = A.B^T (+ bias)                  */
+  GEMM_EPI_LOGPROB_PARTIAL = 6 /* internal: LM-head tile (max, sumexp, target) */
 } mrsp_gemm_epilogue;
 
 /* tcgen05 BF16 GEMM, fp32 accumulate: A[M][lda], B[N][ldb] (both K-major),
@@ -114,6 +120,45 @@ typedef enum {
 mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                               int ldb, int ldc, int epilogue, const float* bias, float* resid,
                               int ldr, void* stream);
+
+/* Fused vocabulary projection + log-softmax + gather (north-star item 5):
+ *   logprob[i] = log_softmax(X[i] . W^T)[targets[i]],  lse[i] = logsumexp(X[i] . W^T)
+ * X [M][ldx] bf16 (final-normed hidden at scored positions), W [V][K] bf16.
+ * The [M x V] logits are never written to memory: each 128x256 tile's
+ * (max, sum exp) and the target logit are reduced in the GEMM epilogue, then
+ * combined across vocab tiles. lse may be NULL. Replaces log_softmax
+ * (common.hpp:95-104) + the gather lp[y] (grpo.cpp:82-85, policy.cpp:159-174)
+ * over materialised logits (engine.hpp:88-94). Workspace from
+ * mrsp_lmhead_workspace_bytes(M, V). */
+size_t mrsp_lmhead_workspace_bytes(int M, int V);
+mrsp_status mrsp_op_lmhead_logprob(const void* X, int ldx, const void* W, int M, int V, int K,
+                                   const int32_t* targets, float* logprob, float* lse,
+                                   void* workspace, size_t ws_bytes, void* stream);
+
+/* RMSNorm (Qwen2): out[i] = bf16(w * x[rows ? rows[i] : i] * rsqrt(mean(x^2) + eps)),
+ * x fp32 [.][ldx], out bf16 [n][ldo]. */
+mrsp_status mrsp_op_rmsnorm(const float* x, int ldx, const float* w, void* out, int ldo, int n,
+                            int d, float eps, const int32_t* rows, void* stream);
+/* LayerNorm (SigLIP): out = bf16((x - mean) * rsqrt(var + eps) * w + b). */
+mrsp_status mrsp_op_layernorm(const float* x, int ldx, const float* w, const float* b, void* out,
+                              int ldo, int n, int d, float eps, void* stream);
+/* Rotate-half RoPE in place on n_heads 128-dim heads starting at column col0
+ * of bf16 rows, angle = fp32(pos) * fp32(theta^(-2i/128)). */
+mrsp_status mrsp_op_rope(void* qkv, int ld, int col0, int n_heads, const int32_t* pos, int n,
+                         float theta, void* stream);
+/* Pixels [F][3][H][W] fp32 -> patch rows bf16 [F*(H/P)*(W/P)][kpad], zero padded. */
+mrsp_status mrsp_op_patchify(const float* pixels, void* out, int F, int H, int W, int P, int kpad,
+                             void* stream);
+/* MR-SP packed-sequence builder for global positions [p0, p0 + n): hidden fp32
+ * rows gathered from frame embeddings / the token embedding table, position
+ * ids and the pad mask. Layout: [n_frame_tok frame tokens | n_q question |
+ * G rows x Lmax], row g = [EOS, resp[g][0 .. len_g - 2], PAD ...]
+ * (pad_batch, engine.cpp:31-43; prev = EOS at t = 0, engine.cpp:124). */
+mrsp_status mrsp_op_pack_sequence(const void* frame_emb, int n_frame_tok, const int32_t* question,
+                                  int n_q, const int32_t* resp, const int32_t* lengths, int Lmax,
+                                  const void* embed, int d, int64_t p0, int n, float* hidden,
+                                  int32_t* pos_ids, uint8_t* pad_mask, int32_t* tokens,
+                                  void* stream);
 
 typedef enum {
   ATTN_CAUSAL_PREFIX = 0, /* k <= q && (k < Lp || row(k) == row(q)), row(x) = (x-Lp)/Lmax */
@@ -131,6 +176,99 @@ mrsp_status mrsp_op_attention(const void* Q, int ldq, int q_col0, const void* K,
                               int k_col0, const void* V, int ldv, int v_col0, void* O, int ldo,
                               int o_col0, int L, int n_heads, int q_per_kv, float scale, int mode,
                               int Lp, int Lmax, int blk, void* stream);
+
+/* ------------------------------------------------------------------------
+ * The MR-SP engine (transformer-shaped model; BASELINE.json configs c1..c5).
+ *
+ * Stage 1 — replaces WorkerGroup::parallel_encode + all_gather +
+ *   EmbeddingCache::get_or_encode (engine.cpp:78-101, :132-197): frames are
+ *   sharded with plan_shards(F, sp), each rank runs the SigLIP-shaped tower +
+ *   projector on its frames (tcgen05 GEMMs, block-diagonal attention), the
+ *   embeddings are all-gathered (NCCL over NVLink, or in-process) into a
+ *   device-resident cache keyed by video id with the reference's exactly-once
+ *   fill protocol and counters.
+ * Stage 2 — replaces pad_batch + plan_shards(max_len) + parallel_prefill +
+ *   log_softmax/gather (engine.cpp:31-43, :103-130; grpo.cpp:44-55, :82-85):
+ *   the GRPO group is packed as [video | question | G rows padded to Lmax],
+ *   sharded with plan_shards(L_total, sp), and prefilled through a
+ *   Qwen2.5-shaped decoder with Ulysses all-to-all around the attention; the
+ *   fused LM head returns per-token log-probs of the response tokens.
+ *
+ * Ranks: sp_degree = n_procs x local ranks. n_procs == 1 runs sp_degree
+ * virtual ranks on the current device (loopback collectives); n_procs > 1
+ * requires sp_degree == n_procs, one process per GPU, and a NCCL unique id
+ * broadcast by the launcher (mrsp_nccl_unique_id on rank 0).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int image_size;  /* 224 (c2..c5) / 64 (c1)                     */
+  int patch;       /* 14 / 8  -> tokens per frame (image/patch)^2   */
+  int v_dim;       /* 1152 / 256                                    */
+  int v_heads;     /* 16 / 4                                        */
+  int v_head_dim;  /* 72 / 64 (<= 128; padded to 128 on device)     */
+  int v_mlp;       /* 4304 / 1024                                   */
+  int v_layers;    /* 27 / 2                                        */
+  int dim;         /* 3584 / 256                                    */
+  int n_q_heads;   /* 28 / 4                                        */
+  int n_kv_heads;  /* 4 / 2                                         */
+  int head_dim;    /* 128 (the only supported value)                */
+  int mlp;         /* 18944 / 1024 (multiple of 128)                */
+  int layers;      /* 28 (c3..c5) / 4 (c2) / 2 (c1)                 */
+  int vocab;       /* 152064 / 32                                   */
+  float rope_theta;
+  float rms_eps;
+  float ln_eps;
+} mrsp_model_config;
+
+typedef struct mrsp_engine mrsp_engine;
+
+/* Fills the 128-byte NCCL unique id (call on rank 0, broadcast to all). */
+mrsp_status mrsp_nccl_unique_id(void* out128);
+
+/* Creates the engine on the current device and initialises synthetic weights
+ * (counter-based uniform init, see oracle/transformer.py). with_ref = 0 makes
+ * the reference model alias the policy (the reference bench's behaviour,
+ * engine.cpp:218-219). */
+mrsp_status mrsp_engine_create(const mrsp_model_config* cfg, int sp_degree, int proc_rank,
+                               int n_procs, uint64_t vision_seed, uint64_t policy_seed,
+                               uint64_t ref_seed, int with_ref, const void* nccl_id,
+                               mrsp_engine** out);
+mrsp_status mrsp_engine_destroy(mrsp_engine* e);
+
+/* Stage 1: encode + gather the video into the cache (or hit it).
+ * pixels: F x 3 x S x S fp32, host or device (pixels_on_device). hit: 0/1.
+ * use_cache = 0 encodes without touching the cache (cache-off bench cell). */
+mrsp_status mrsp_engine_encode(mrsp_engine* e, const char* video_id, const float* pixels, int F,
+                               int pixels_on_device, int use_cache, int* hit);
+
+/* Stage 2: per-token log-probs of G rollouts against the cached video
+ * `video_id`. resp: G x Lmax token ids (row g valid below lengths[g]);
+ * model 0 = policy, 1 = reference. logprob/lse: sum(lengths) floats in
+ * row-major (rollout, position) order; host memory unless out_on_device. */
+mrsp_status mrsp_engine_prefill_logprobs(mrsp_engine* e, const char* video_id,
+                                         const int32_t* question, int n_q, const int32_t* resp,
+                                         const int32_t* lengths, int G, int Lmax, int model,
+                                         float* logprob, float* lse, int out_on_device);
+
+/* One MR-SP step (engine.cpp:203-225 contract): G embedding fetches (cache
+ * on: 1 miss + G-1 hits), then policy and reference prefill + log-probs. */
+mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, const float* pixels, int F,
+                             int pixels_on_device, int use_cache, const int32_t* question,
+                             int n_q, const int32_t* resp, const int32_t* lengths, int G,
+                             int Lmax, float* logprob_policy, float* logprob_ref,
+                             int out_on_device);
+
+/* Counters: [encoder_invocations, cache_hits, cache_misses, gather_bytes,
+ * pad_reads, a2a_bytes] (EngineStats, engine.hpp:27-41, plus a2a bytes). */
+mrsp_status mrsp_engine_stats(mrsp_engine* e, uint64_t* out6, int reset);
+mrsp_status mrsp_engine_cache(mrsp_engine* e, int op /*0 size,1 clear,2 set capacity*/, int arg,
+                              uint64_t* size_out);
+/* Copies the cached [F*T][dim] bf16 embeddings of video_id to host. */
+mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* video_id, void* host_out);
+/* Per-kernel-class CUDA-event timing: cls 0 LLM attention, 1 LLM GEMMs,
+ * 2 vision tower, 3 LM head, 4 collectives, 5 norms/rope/pack. */
+mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, double* ms, int64_t* launches);
+/* The stream the engine launches on (cudaStream_t). */
+void* mrsp_engine_stream(mrsp_engine* e);
 
 #ifdef __cplusplus
 }

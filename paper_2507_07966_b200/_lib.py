@@ -73,12 +73,26 @@ _sig("mrsp_op_attention", [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c
                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                            ctypes.c_float, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                            ctypes.c_void_p])
-
-
-def _register_more():
-    """Signatures for the transformer-path entry points (declared lazily so this
-    module stays importable while the header grows)."""
-    from . import _abi_ext  # noqa: F401  (populates SIGNATURES)
+_V, _I, _F, _U64, _I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_uint64, ctypes.c_int64
+_sig("mrsp_gen_video", [_U64, _I, _I, c_f32p])
+_sig("mrsp_lmhead_workspace_bytes", [_I, _I], ctypes.c_size_t)
+_sig("mrsp_op_lmhead_logprob", [_V, _I, _V, _I, _I, _I, _V, _V, _V, _V, ctypes.c_size_t, _V])
+_sig("mrsp_op_rmsnorm", [_V, _I, _V, _V, _I, _I, _I, _F, _V, _V])
+_sig("mrsp_op_layernorm", [_V, _I, _V, _V, _V, _I, _I, _I, _F, _V])
+_sig("mrsp_op_rope", [_V, _I, _I, _I, _V, _I, _F, _V])
+_sig("mrsp_op_patchify", [_V, _V, _I, _I, _I, _I, _I, _V])
+_sig("mrsp_op_pack_sequence", [_V, _I, _V, _I, _V, _V, _I, _V, _I, _I64, _I, _V, _V, _V, _V, _V])
+_sig("mrsp_nccl_unique_id", [_V])
+_sig("mrsp_engine_create", [_V, _I, _I, _I, _U64, _U64, _U64, _I, _V, _V])
+_sig("mrsp_engine_destroy", [_V])
+_sig("mrsp_engine_encode", [_V, ctypes.c_char_p, _V, _I, _I, _I, _V])
+_sig("mrsp_engine_prefill_logprobs", [_V, ctypes.c_char_p, _V, _I, _V, _V, _I, _I, _I, _V, _V, _I])
+_sig("mrsp_engine_step", [_V, ctypes.c_char_p, _V, _I, _I, _I, _V, _I, _V, _V, _I, _I, _V, _V, _I])
+_sig("mrsp_engine_stats", [_V, _V, _I])
+_sig("mrsp_engine_cache", [_V, _I, _I, _V])
+_sig("mrsp_engine_get_embeddings", [_V, ctypes.c_char_p, _V])
+_sig("mrsp_engine_profile", [_V, _I, _I, _V, _V])
+_sig("mrsp_engine_stream", [_V], ctypes.c_void_p)
 
 
 def lib() -> ctypes.CDLL:
@@ -90,10 +104,6 @@ def lib() -> ctypes.CDLL:
                 " (the B200 engine has no CPU fallback)")
         # libcudart / libcuda come from the CUDA toolkit or torch's bundle.
         l = ctypes.CDLL(str(LIB_PATH), mode=ctypes.RTLD_GLOBAL)
-        try:
-            _register_more()
-        except ImportError:
-            pass
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(l, name)
             fn.restype = res

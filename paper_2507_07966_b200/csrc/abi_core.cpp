@@ -55,3 +55,36 @@ mrsp_status mrsp_plan_shards(uint64_t n_items, int sp_degree, uint64_t* ranges) 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic inputs (mmseq.cpp:58-72, common.hpp:19-79): frames U[-1,1) from
+// mt19937_64 seeded by Rng::substream(seed, "video"); delivered as fp32.
+#include <random>
+
+namespace {
+uint64_t substream_seed(uint64_t base, const char* tag) {
+  uint64_t h = 1469598103934665603ull;
+  for (const unsigned char* c = reinterpret_cast<const unsigned char*>(tag); *c; ++c) {
+    h ^= *c;
+    h *= 1099511628211ull;
+  }
+  uint64_t z = base ^ h;
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+}  // namespace
+
+extern "C" mrsp_status mrsp_gen_video(uint64_t seed, int frames, int feature_dim, float* out) {
+  return mrsp::guard([&] {
+    MRSP_REQUIRE(frames >= 1, MRSP_INVALID_ARGUMENT, "gen_video: num_frames must be >= 1");
+    MRSP_REQUIRE(feature_dim >= 4, MRSP_INVALID_ARGUMENT, "gen_video: feature_dim must be >= 4");
+    std::mt19937_64 g(substream_seed(seed, "video"));
+    const size_t n = static_cast<size_t>(frames) * static_cast<size_t>(feature_dim);
+    for (size_t i = 0; i < n; ++i) {
+      const double u = static_cast<double>(g() >> 11) * 0x1.0p-53;
+      out[i] = static_cast<float>(2.0 * u - 1.0);
+    }
+  });
+}

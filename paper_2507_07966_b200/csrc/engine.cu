@@ -1,0 +1,1033 @@
+// engine.cu — B200 MR-SP engine: Stage 1 (sharded vision encode -> all-gather
+// -> device-resident exactly-once cache) and Stage 2 (packed, sequence-sharded
+// Ulysses prefill of policy and reference -> fused LM-head log-probs).
+//
+// Reference anchors (paths under /root/reference/proj):
+//   plan_shards            engine.cpp:15-29   (frame plan and token plan)
+//   parallel_encode        engine.cpp:78-101  -> encode_rank() per SP rank
+//   all_gather             engine.cpp:132-153 -> NCCL all-gather / in-process
+//   EmbeddingCache         engine.cpp:155-197 -> get_or_encode() (same protocol)
+//   pad_batch + prefill    engine.cpp:31-43, :103-130, grpo.cpp:44-55
+//                          -> packed [video | question | G x Lmax] sequence
+//   log_softmax + lp[y]    common.hpp:95-104, grpo.cpp:82-85 -> fused LM head
+//   run_step               engine.cpp:203-225 -> mrsp_engine_step
+#include "engine.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "attention.h"
+#include "common.h"
+#include "gemm.h"
+#include "misc.h"
+
+namespace mrsp {
+
+// ---------------------------------------------------------------------------
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+void* DevBuf::ensure(size_t b) {
+  if (b <= bytes && p) return p;
+  release();
+  const size_t nb = std::max<size_t>((b + 255) & ~size_t(255), 256);
+  MRSP_CUDA(cudaMalloc(&p, nb));
+  bytes = nb;
+  return p;
+}
+
+namespace {
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+uint64_t splitmix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+uint64_t tensor_key(uint64_t seed, const std::string& name) { return splitmix(seed ^ fnv1a(name)); }
+
+std::vector<std::pair<long, long>> plan(long n, int k) {
+  std::vector<std::pair<long, long>> r(k);
+  const long base = n / k, extra = n % k;
+  long pos = 0;
+  for (int w = 0; w < k; ++w) {
+    const long len = base + (w < extra ? 1 : 0);
+    r[w] = {pos, pos + len};
+    pos += len;
+  }
+  return r;
+}
+
+__global__ void scatter_f32_kernel(const float* __restrict__ src, const int* __restrict__ slot,
+                                   int n, float* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[slot[i]] = src[i];
+}
+
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += (n * sizeof(T) + 255) & ~size_t(255);
+    return p;
+  }
+};
+
+}  // namespace
+
+// Ulysses head split for SP rank r of k: contiguous head blocks
+// when k <= n_kv; otherwise k / n_kv ranks share one kv head (replicated) and
+// split its query-head group with plan_shards (28/4 at SP=8 -> 4+3 heads).
+HeadSplit head_split(int nq, int nkv, int k, int r) {
+  HeadSplit h{};
+  if (k <= nkv) {
+    MRSP_REQUIRE(nkv % k == 0 && nq % k == 0, MRSP_INVALID_ARGUMENT,
+                 "ulysses: heads must divide evenly across SP ranks");
+    h.q_lo = r * nq / k;
+    h.q_hi = (r + 1) * nq / k;
+    h.kv_lo = r * nkv / k;
+    h.kv_hi = (r + 1) * nkv / k;
+    h.q_per_kv = nq / nkv;
+  } else {
+    MRSP_REQUIRE(k % nkv == 0, MRSP_INVALID_ARGUMENT,
+                 "ulysses: SP degree must be a multiple of the kv head count");
+    const int m = k / nkv, g = r / m, j = r % m, qpk = nq / nkv;
+    const auto p = plan(qpk, m)[j];
+    h.q_lo = g * qpk + static_cast<int>(p.first);
+    h.q_hi = g * qpk + static_cast<int>(p.second);
+    h.kv_lo = g;
+    h.kv_hi = g + 1;
+    h.q_per_kv = std::max(1, h.q_hi - h.q_lo);
+  }
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n_procs,
+               uint64_t vision_seed, uint64_t policy_seed, uint64_t ref_seed, int with_ref,
+               const void* nccl_id)
+    : cfg_(cfg), k_(sp_degree), proc_rank_(proc_rank), n_procs_(n_procs) {
+  MRSP_REQUIRE(sp_degree >= 1, MRSP_INVALID_ARGUMENT, "WorkerGroup: sp_degree must be >= 1");
+  MRSP_REQUIRE(n_procs >= 1 && (n_procs == 1 || n_procs == sp_degree), MRSP_INVALID_ARGUMENT,
+               "engine: n_procs must be 1 (virtual ranks) or equal to sp_degree");
+  MRSP_REQUIRE(cfg.head_dim == 128, MRSP_INVALID_ARGUMENT, "engine: head_dim must be 128");
+  MRSP_REQUIRE(cfg.v_head_dim <= 128 && cfg.v_head_dim * cfg.v_heads == cfg.v_dim,
+               MRSP_INVALID_ARGUMENT, "engine: bad vision head geometry");
+  MRSP_REQUIRE(cfg.mlp % 128 == 0, MRSP_INVALID_ARGUMENT, "engine: mlp must be a multiple of 128");
+  MRSP_REQUIRE(cfg.dim % 8 == 0 && cfg.v_dim % 8 == 0 && cfg.v_mlp % 8 == 0, MRSP_INVALID_ARGUMENT,
+               "engine: model dims must be multiples of 8");
+  MRSP_REQUIRE(cfg.image_size % cfg.patch == 0, MRSP_INVALID_ARGUMENT,
+               "engine: image size must be a multiple of the patch");
+  require_device();
+  MRSP_CUDA(cudaGetDevice(&device_));
+  MRSP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (n_procs > 1) {
+    MRSP_REQUIRE(nccl_id != nullptr, MRSP_INVALID_ARGUMENT, "engine: NCCL id required");
+    nccl_ = std::make_unique<Nccl>(n_procs, proc_rank, nccl_id, device_);
+  }
+  const int local = n_procs > 1 ? 1 : k_;
+  ranks_.resize(local);
+  for (int i = 0; i < local; ++i) {
+    ranks_[i].g = n_procs > 1 ? proc_rank : i;
+    ranks_[i].hs = head_split(cfg.n_q_heads, cfg.n_kv_heads, k_, ranks_[i].g);
+  }
+  float inv[64];
+  for (int i = 0; i < 64; ++i)
+    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(cfg.rope_theta), (2.0 * i) / 128.0));
+  set_rope_inv_freq(inv, stream_);
+  init_weights(vision_seed, policy_seed, ref_seed, with_ref);
+  MRSP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Engine::~Engine() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& e : ev_pending_) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  ranks_.clear();
+  cache_.clear();
+  nccl_.reset();
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+// Synthetic weights: w = bf16(a * (2u - 1)), u from splitmix64(key + i) (24-bit),
+// key = splitmix64(seed ^ fnv1a(name)); restated in oracle/transformer.py.
+void Engine::init_weights(uint64_t vseed, uint64_t pseed, uint64_t rseed, int with_ref) {
+  const auto& c = cfg_;
+  const int T = tokens_per_frame(), kreal = 3 * c.patch * c.patch, kpad = (kreal + 7) / 8 * 8;
+  const int vd = c.v_dim, vh = c.v_heads, vhd = c.v_head_dim, vq = vh * 128;
+  const int d = c.dim, qkv_rows = (c.n_q_heads + 2 * c.n_kv_heads) * 128;
+  has_ref_ = with_ref != 0;
+  // size the single weight allocation
+  size_t total = 0;
+  auto add = [&](size_t n, size_t es) { total += (n * es + 255) & ~size_t(255); };
+  add(static_cast<size_t>(vd) * kpad, 2);
+  add(vd, 4);
+  add(static_cast<size_t>(T) * vd, 4);
+  for (int l = 0; l < c.v_layers; ++l) {
+    add(vd, 4); add(vd, 4); add(static_cast<size_t>(3) * vq * vd, 2); add(3 * vq, 4);
+    add(static_cast<size_t>(vd) * vq, 2); add(vd, 4); add(vd, 4); add(vd, 4);
+    add(static_cast<size_t>(c.v_mlp) * vd, 2); add(c.v_mlp, 4);
+    add(static_cast<size_t>(vd) * c.v_mlp, 2); add(vd, 4);
+  }
+  add(vd, 4); add(vd, 4);
+  add(static_cast<size_t>(d) * vd, 2); add(d, 4); add(static_cast<size_t>(d) * d, 2); add(d, 4);
+  const int n_llm = has_ref_ ? 2 : 1;
+  for (int m = 0; m < n_llm; ++m) {
+    add(static_cast<size_t>(c.vocab) * d, 2);
+    for (int l = 0; l < c.layers; ++l) {
+      add(d, 4); add(static_cast<size_t>(qkv_rows) * d, 2); add(qkv_rows, 4);
+      add(static_cast<size_t>(d) * c.n_q_heads * 128, 2); add(d, 4);
+      add(static_cast<size_t>(2) * c.mlp * d, 2); add(static_cast<size_t>(d) * c.mlp, 2);
+    }
+    add(d, 4);
+    add(static_cast<size_t>(c.vocab) * d, 2);
+  }
+  wbuf_.ensure(total);
+  MRSP_CUDA(cudaMemsetAsync(wbuf_.p, 0, total, stream_));
+  Carver cv{static_cast<uint8_t*>(wbuf_.p)};
+  cudaStream_t s = stream_;
+  auto wscale = [](int fan_in) { return static_cast<float>(std::sqrt(3.0 / fan_in)); };
+  const float kBias = 0.03f, kNorm = 0.1f, kPos = 0.1f, kEmbed = static_cast<float>(std::sqrt(3.0));
+  auto bf = [&](bf16* dst, size_t n, uint64_t seed, const std::string& name, float a) {
+    init_uniform_bf16(dst, n, tensor_key(seed, name), a, s);
+  };
+  auto f32 = [&](float* dst, size_t n, uint64_t seed, const std::string& name, float a, float off) {
+    init_uniform_f32(dst, n, tensor_key(seed, name), a, off, s);
+  };
+  DevBuf tmp;
+  // ---- vision tower
+  vis_.patch_w = cv.take<bf16>(static_cast<size_t>(vd) * kpad);
+  {
+    bf16* t = static_cast<bf16*>(tmp.ensure(static_cast<size_t>(vd) * kreal * 2));
+    bf(t, static_cast<size_t>(vd) * kreal, vseed, "vision.patch_w", wscale(kreal));
+    MRSP_CUDA(cudaMemcpy2DAsync(vis_.patch_w, kpad * 2, t, kreal * 2, kreal * 2, vd,
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  vis_.patch_b = cv.take<float>(vd);
+  f32(vis_.patch_b, vd, vseed, "vision.patch_b", kBias, 0.f);
+  vis_.pos = cv.take<float>(static_cast<size_t>(T) * vd);
+  f32(vis_.pos, static_cast<size_t>(T) * vd, vseed, "vision.pos", kPos, 0.f);
+  vis_.layers.resize(c.v_layers);
+  for (int l = 0; l < c.v_layers; ++l) {
+    auto& L = vis_.layers[l];
+    const std::string p = "vision." + std::to_string(l) + ".";
+    L.ln1_w = cv.take<float>(vd); f32(L.ln1_w, vd, vseed, p + "ln1_w", kNorm, 1.f);
+    L.ln1_b = cv.take<float>(vd); f32(L.ln1_b, vd, vseed, p + "ln1_b", kBias, 0.f);
+    // QKV / O with heads padded 72 -> 128 (zero rows / columns)
+    L.wqkv = cv.take<bf16>(static_cast<size_t>(3) * vq * vd);
+    {
+      bf16* t = static_cast<bf16*>(tmp.ensure(static_cast<size_t>(3) * vd * vd * 2));
+      bf(t, static_cast<size_t>(3) * vd * vd, vseed, p + "wqkv", wscale(vd));
+      for (int part = 0; part < 3; ++part)
+        for (int h = 0; h < vh; ++h)
+          MRSP_CUDA(cudaMemcpyAsync(L.wqkv + (static_cast<size_t>(part) * vq + h * 128) * vd,
+                                    t + (static_cast<size_t>(part) * vd + h * vhd) * vd,
+                                    static_cast<size_t>(vhd) * vd * 2, cudaMemcpyDeviceToDevice, s));
+    }
+    L.bqkv = cv.take<float>(3 * vq);
+    {
+      float* t = static_cast<float*>(tmp.ensure(static_cast<size_t>(3) * vd * 4));
+      f32(t, 3 * vd, vseed, p + "bqkv", kBias, 0.f);
+      for (int part = 0; part < 3; ++part)
+        for (int h = 0; h < vh; ++h)
+          MRSP_CUDA(cudaMemcpyAsync(L.bqkv + part * vq + h * 128, t + part * vd + h * vhd, vhd * 4,
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+    L.wo = cv.take<bf16>(static_cast<size_t>(vd) * vq);
+    {
+      bf16* t = static_cast<bf16*>(tmp.ensure(static_cast<size_t>(vd) * vd * 2));
+      bf(t, static_cast<size_t>(vd) * vd, vseed, p + "wo", wscale(vd));
+      for (int h = 0; h < vh; ++h)
+        MRSP_CUDA(cudaMemcpy2DAsync(L.wo + h * 128, static_cast<size_t>(vq) * 2, t + h * vhd,
+                                    static_cast<size_t>(vd) * 2, vhd * 2, vd,
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+    L.bo = cv.take<float>(vd); f32(L.bo, vd, vseed, p + "bo", kBias, 0.f);
+    L.ln2_w = cv.take<float>(vd); f32(L.ln2_w, vd, vseed, p + "ln2_w", kNorm, 1.f);
+    L.ln2_b = cv.take<float>(vd); f32(L.ln2_b, vd, vseed, p + "ln2_b", kBias, 0.f);
+    L.w1 = cv.take<bf16>(static_cast<size_t>(c.v_mlp) * vd);
+    bf(L.w1, static_cast<size_t>(c.v_mlp) * vd, vseed, p + "w1", wscale(vd));
+    L.b1 = cv.take<float>(c.v_mlp); f32(L.b1, c.v_mlp, vseed, p + "b1", kBias, 0.f);
+    L.w2 = cv.take<bf16>(static_cast<size_t>(vd) * c.v_mlp);
+    bf(L.w2, static_cast<size_t>(vd) * c.v_mlp, vseed, p + "w2", wscale(c.v_mlp));
+    L.b2 = cv.take<float>(vd); f32(L.b2, vd, vseed, p + "b2", kBias, 0.f);
+  }
+  vis_.post_w = cv.take<float>(vd); f32(vis_.post_w, vd, vseed, "vision.post_w", kNorm, 1.f);
+  vis_.post_b = cv.take<float>(vd); f32(vis_.post_b, vd, vseed, "vision.post_b", kBias, 0.f);
+  vis_.p1_w = cv.take<bf16>(static_cast<size_t>(d) * vd);
+  bf(vis_.p1_w, static_cast<size_t>(d) * vd, vseed, "proj.w1", wscale(vd));
+  vis_.p1_b = cv.take<float>(d); f32(vis_.p1_b, d, vseed, "proj.b1", kBias, 0.f);
+  vis_.p2_w = cv.take<bf16>(static_cast<size_t>(d) * d);
+  bf(vis_.p2_w, static_cast<size_t>(d) * d, vseed, "proj.w2", wscale(d));
+  vis_.p2_b = cv.take<float>(d); f32(vis_.p2_b, d, vseed, "proj.b2", kBias, 0.f);
+  // ---- LLMs
+  for (int m = 0; m < n_llm; ++m) {
+    auto& W = llm_[m];
+    const uint64_t seed = m == 0 ? pseed : rseed;
+    const std::string pre = m == 0 ? "policy." : "ref.";
+    W.embed = cv.take<bf16>(static_cast<size_t>(c.vocab) * d);
+    bf(W.embed, static_cast<size_t>(c.vocab) * d, seed, pre + "embed", kEmbed);
+    W.layers.resize(c.layers);
+    for (int l = 0; l < c.layers; ++l) {
+      auto& L = W.layers[l];
+      const std::string p = pre + std::to_string(l) + ".";
+      L.attn_norm = cv.take<float>(d); f32(L.attn_norm, d, seed, p + "attn_norm", kNorm, 1.f);
+      L.wqkv = cv.take<bf16>(static_cast<size_t>(qkv_rows) * d);
+      bf(L.wqkv, static_cast<size_t>(qkv_rows) * d, seed, p + "wqkv", wscale(d));
+      L.bqkv = cv.take<float>(qkv_rows); f32(L.bqkv, qkv_rows, seed, p + "bqkv", kBias, 0.f);
+      L.wo = cv.take<bf16>(static_cast<size_t>(d) * c.n_q_heads * 128);
+      bf(L.wo, static_cast<size_t>(d) * c.n_q_heads * 128, seed, p + "wo", wscale(c.n_q_heads * 128));
+      L.mlp_norm = cv.take<float>(d); f32(L.mlp_norm, d, seed, p + "mlp_norm", kNorm, 1.f);
+      L.wgu = cv.take<bf16>(static_cast<size_t>(2) * c.mlp * d);
+      {
+        // interleave [gate | up] in 128-row blocks for the SwiGLU epilogue
+        const size_t n1 = static_cast<size_t>(c.mlp) * d;
+        bf16* t = static_cast<bf16*>(tmp.ensure(n1 * 2));
+        bf(t, n1, seed, p + "w_gate", wscale(d));
+        MRSP_CUDA(cudaMemcpy2DAsync(L.wgu, static_cast<size_t>(256) * d * 2, t,
+                                    static_cast<size_t>(128) * d * 2, static_cast<size_t>(128) * d * 2,
+                                    c.mlp / 128, cudaMemcpyDeviceToDevice, s));
+        MRSP_CUDA(cudaStreamSynchronize(s));
+        bf(t, n1, seed, p + "w_up", wscale(d));
+        MRSP_CUDA(cudaMemcpy2DAsync(L.wgu + static_cast<size_t>(128) * d,
+                                    static_cast<size_t>(256) * d * 2, t,
+                                    static_cast<size_t>(128) * d * 2, static_cast<size_t>(128) * d * 2,
+                                    c.mlp / 128, cudaMemcpyDeviceToDevice, s));
+        MRSP_CUDA(cudaStreamSynchronize(s));
+      }
+      L.wdown = cv.take<bf16>(static_cast<size_t>(d) * c.mlp);
+      bf(L.wdown, static_cast<size_t>(d) * c.mlp, seed, p + "w_down", wscale(c.mlp));
+    }
+    W.final_norm = cv.take<float>(d); f32(W.final_norm, d, seed, pre + "final_norm", kNorm, 1.f);
+    W.lm_head = cv.take<bf16>(static_cast<size_t>(c.vocab) * d);
+    bf(W.lm_head, static_cast<size_t>(c.vocab) * d, seed, pre + "lm_head", wscale(d));
+  }
+  if (!has_ref_) llm_[1] = llm_[0];
+  MRSP_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+void Engine::prof_begin(int cls, cudaEvent_t* a) {
+  (void)cls;
+  if (!prof_) return;
+  if (ev_pool_.empty()) {
+    cudaEvent_t e;
+    MRSP_CUDA(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  *a = ev_pool_.back();
+  ev_pool_.pop_back();
+  MRSP_CUDA(cudaEventRecord(*a, stream_));
+}
+void Engine::prof_end(int cls, cudaEvent_t a) {
+  if (!prof_) return;
+  cudaEvent_t b;
+  if (ev_pool_.empty()) {
+    MRSP_CUDA(cudaEventCreate(&b));
+  } else {
+    b = ev_pool_.back();
+    ev_pool_.pop_back();
+  }
+  MRSP_CUDA(cudaEventRecord(b, stream_));
+  ev_pending_.push_back({cls, a, b});
+}
+void Engine::prof_collect() {
+  if (ev_pending_.empty()) return;
+  MRSP_CUDA(cudaStreamSynchronize(stream_));
+  for (auto& e : ev_pending_) {
+    float ms = 0;
+    MRSP_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+    prof_ms_[e.cls] += ms;
+    prof_n_[e.cls] += 1;
+    ev_pool_.push_back(e.a);
+    ev_pool_.push_back(e.b);
+  }
+  ev_pending_.clear();
+}
+void Engine::set_profiling(bool on) {
+  prof_collect();
+  prof_ = on;
+  for (int i = 0; i < 8; ++i) {
+    prof_ms_[i] = 0;
+    prof_n_[i] = 0;
+  }
+}
+void Engine::profile_read(int cls, double* ms, long* launches) {
+  prof_collect();
+  *ms = prof_ms_[cls];
+  *launches = prof_n_[cls];
+}
+
+// RAII timing scope for one kernel class.
+struct Prof {
+  Engine& e;
+  int cls;
+  cudaEvent_t a = nullptr;
+  Prof(Engine& en, int c) : e(en), cls(c) { e.prof_begin(cls, &a); }
+  ~Prof() {
+    if (a) e.prof_end(cls, a);
+  }
+};
+
+enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5 };
+
+// ---------------------------------------------------------------------------
+// Stage 1 for one SP rank: frames [fb, fe) -> projector output rows.
+void Engine::encode_rank(RankCtx& R, const float* pixels, bool on_device, int F, long fb, long fe,
+                         bf16* out) {
+  (void)F;
+  const auto& c = cfg_;
+  const int nf = static_cast<int>(fe - fb);
+  if (nf <= 0) return;
+  const int T = tokens_per_frame(), S = c.image_size, P = c.patch;
+  const int kreal = 3 * P * P, kpad = (kreal + 7) / 8 * 8;
+  const int vd = c.v_dim, vq = c.v_heads * 128, ntok = nf * T;
+  cudaStream_t s = stream_;
+  const size_t frame_px = static_cast<size_t>(3) * S * S;
+  Prof pv(*this, P_VISION);
+  float* pix = static_cast<float*>(R.pix.ensure(static_cast<size_t>(nf) * frame_px * 4));
+  MRSP_CUDA(cudaMemcpyAsync(pix, pixels + static_cast<size_t>(fb) * frame_px,
+                            static_cast<size_t>(nf) * frame_px * 4,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  bf16* patches = static_cast<bf16*>(R.patches.ensure(static_cast<size_t>(ntok) * kpad * 2));
+  patchify(pix, patches, nf, S, S, P, kpad, s);
+  float* vh = static_cast<float*>(R.vh.ensure(static_cast<size_t>(ntok) * vd * 4));
+  bf16* xn = static_cast<bf16*>(R.vxn.ensure(static_cast<size_t>(ntok) * vd * 2));
+  bf16* qkv = static_cast<bf16*>(R.vqkv.ensure(static_cast<size_t>(ntok) * 3 * vq * 2));
+  bf16* o = static_cast<bf16*>(R.vo.ensure(static_cast<size_t>(ntok) * vq * 2));
+  bf16* mid = static_cast<bf16*>(
+      R.vmid.ensure(static_cast<size_t>(ntok) * std::max(c.v_mlp, c.dim) * 2));
+  broadcast_rows(vis_.pos, vh, ntok, T, vd, s);
+  gemm_bf16({patches, vis_.patch_w, nullptr, ntok, vd, kpad, kpad, kpad, 0, GEMM_EPI_RESID_F32,
+             vis_.patch_b, vh, vd},
+            s);
+  const float vscale = 1.0f / std::sqrt(static_cast<float>(c.v_head_dim));
+  for (const auto& L : vis_.layers) {
+    layernorm(vh, vd, L.ln1_w, L.ln1_b, xn, vd, ntok, vd, c.ln_eps, s);
+    gemm_bf16({xn, L.wqkv, qkv, ntok, 3 * vq, vd, vd, vd, 3 * vq, GEMM_EPI_BIAS_BF16, L.bqkv,
+               nullptr, 0},
+              s);
+    attention_fwd({qkv, 3 * vq, 0, qkv, 3 * vq, vq, qkv, 3 * vq, 2 * vq, o, vq, 0, ntok,
+                   c.v_heads, 1, vscale, ATTN_BLOCK_DIAG, 0, 0, T},
+                  s);
+    gemm_bf16({o, L.wo, nullptr, ntok, vd, vq, vq, vq, 0, GEMM_EPI_RESID_F32, L.bo, vh, vd}, s);
+    layernorm(vh, vd, L.ln2_w, L.ln2_b, xn, vd, ntok, vd, c.ln_eps, s);
+    gemm_bf16({xn, L.w1, mid, ntok, c.v_mlp, vd, vd, vd, c.v_mlp, GEMM_EPI_BIAS_GELU_BF16, L.b1,
+               nullptr, 0},
+              s);
+    gemm_bf16({mid, L.w2, nullptr, ntok, vd, c.v_mlp, c.v_mlp, c.v_mlp, 0, GEMM_EPI_RESID_F32,
+               L.b2, vh, vd},
+              s);
+  }
+  layernorm(vh, vd, vis_.post_w, vis_.post_b, xn, vd, ntok, vd, c.ln_eps, s);
+  gemm_bf16({xn, vis_.p1_w, mid, ntok, c.dim, vd, vd, vd, c.dim, GEMM_EPI_BIAS_GELU_BF16,
+             vis_.p1_b, nullptr, 0},
+            s);
+  gemm_bf16({mid, vis_.p2_w, out, ntok, c.dim, c.dim, c.dim, c.dim, c.dim, GEMM_EPI_BIAS_BF16,
+             vis_.p2_b, nullptr, 0},
+            s);
+  encoder_invocations.fetch_add(static_cast<uint64_t>(nf), std::memory_order_relaxed);
+}
+
+std::shared_ptr<CacheEntry> Engine::get_or_encode(const std::string& id, const float* pixels,
+                                                  int F, bool on_device, bool use_cache,
+                                                  bool* hit) {
+  MRSP_REQUIRE(F >= 1, MRSP_INVALID_ARGUMENT, "gen_video: num_frames must be >= 1");
+  std::shared_ptr<CacheEntry> entry;
+  bool filler = true;
+  if (use_cache) {
+    std::lock_guard<std::mutex> lock(cache_mu_);
+    auto it = cache_.find(id);
+    if (it == cache_.end()) {
+      entry = std::make_shared<CacheEntry>();
+      entry->seq = ++cache_seq_;
+      cache_.emplace(id, entry);
+      cache_misses.fetch_add(1, std::memory_order_relaxed);
+      if (cache_capacity > 0) {
+        while (static_cast<int>(cache_.size()) > cache_capacity) {
+          auto oldest = std::min_element(cache_.begin(), cache_.end(), [](auto& a, auto& b) {
+            return a.second->seq < b.second->seq;
+          });
+          cache_.erase(oldest);
+        }
+      }
+    } else {
+      entry = it->second;
+      filler = false;
+      cache_hits.fetch_add(1, std::memory_order_relaxed);
+    }
+  } else {
+    entry = std::make_shared<CacheEntry>();
+  }
+  *hit = !filler;
+  if (!filler) {
+    std::unique_lock<std::mutex> lock(entry->m);
+    entry->cv.wait(lock, [&] { return entry->ready; });
+    if (entry->failed) fail(MRSP_RUNTIME_ERROR, entry->error);
+    return entry;
+  }
+  try {
+    std::lock_guard<std::mutex> run(run_mu_);
+    const int T = tokens_per_frame(), d = cfg_.dim;
+    const auto fplan = plan(F, k_);
+    auto emb = std::make_shared<DevBuf>();
+    const size_t row_bytes = static_cast<size_t>(T) * d * 2;  // one frame's embeddings
+    bf16* full = static_cast<bf16*>(emb->ensure(static_cast<size_t>(F) * row_bytes));
+    if (!nccl_) {
+      // virtual ranks share this device: each rank's projector writes its
+      // slice of the gathered buffer directly (the in-process all-gather)
+      for (auto& R : ranks_) {
+        const auto [fb, fe] = fplan[R.g];
+        encode_rank(R, pixels, on_device, F, fb, fe, full + static_cast<size_t>(fb) * T * d);
+      }
+    } else {
+      RankCtx& R = ranks_[0];
+      const auto [fb, fe] = fplan[R.g];
+      const long chunk_frames = (F + k_ - 1) / k_;
+      const size_t chunk = chunk_frames * row_bytes;
+      uint8_t* sendb = static_cast<uint8_t*>(R.send.ensure(chunk));
+      uint8_t* recvb = static_cast<uint8_t*>(R.recv.ensure(chunk * k_));
+      encode_rank(R, pixels, on_device, F, fb, fe, reinterpret_cast<bf16*>(sendb));
+      {
+        Prof pc(*this, P_COMM);
+        nccl_->all_gather(sendb, recvb, chunk, stream_);
+      }
+      for (int w = 0; w < k_; ++w) {
+        const auto [b, e] = fplan[w];
+        if (e > b)
+          MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(full) + b * row_bytes,
+                                    recvb + w * chunk, (e - b) * row_bytes,
+                                    cudaMemcpyDeviceToDevice, stream_));
+      }
+    }
+    // reference accounting: values x (sp - 1) x bytes per value (engine.cpp:149-151)
+    gather_bytes.fetch_add(static_cast<uint64_t>(F) * T * d * (k_ - 1) * 2,
+                           std::memory_order_relaxed);
+    MRSP_CUDA(cudaStreamSynchronize(stream_));
+    prof_collect();
+    {
+      std::lock_guard<std::mutex> lock(entry->m);
+      entry->emb = emb;
+      entry->n_frames = F;
+      entry->ready = true;
+    }
+    entry->cv.notify_all();
+  } catch (const std::exception& ex) {
+    {
+      std::lock_guard<std::mutex> lock(entry->m);
+      entry->failed = true;
+      entry->error = ex.what();
+      entry->ready = true;
+    }
+    entry->cv.notify_all();
+    if (use_cache) {
+      std::lock_guard<std::mutex> lock(cache_mu_);
+      auto it = cache_.find(id);
+      if (it != cache_.end() && it->second == entry) cache_.erase(it);
+    }
+    throw;
+  }
+  return entry;
+}
+
+// ---------------------------------------------------------------------------
+// Ulysses all-to-all: sequence shards [n_r, Cqkv] -> head shards [L, C_r].
+void Engine::a2a_forward(int L) {
+  (void)L;
+  const auto& c = cfg_;
+  const int nq = c.n_q_heads, nkv = c.n_kv_heads, Cqkv = (nq + 2 * nkv) * 128;
+  Prof pc(*this, P_COMM);
+  auto col_blocks = [&](const HeadSplit& hs) {
+    // (src col, dst col, width) for Q, K, V of the destination's heads
+    const int Cr_q = hs.nq() * 128, Cr_kv = hs.nkv() * 128;
+    return std::array<std::array<int, 3>, 3>{
+        std::array<int, 3>{hs.q_lo * 128, 0, Cr_q},
+        std::array<int, 3>{nq * 128 + hs.kv_lo * 128, Cr_q, Cr_kv},
+        std::array<int, 3>{(nq + nkv) * 128 + hs.kv_lo * 128, Cr_q + Cr_kv, Cr_kv}};
+  };
+  if (!nccl_) {
+    for (auto& dst : ranks_) {
+      const int Cr = (dst.hs.nq() + 2 * dst.hs.nkv()) * 128;
+      bf16* qh = dst.qh.as<bf16>();
+      for (auto& src : ranks_) {
+        const long n = src.e - src.b;
+        if (n <= 0) continue;
+        for (auto& blk : col_blocks(dst.hs)) {
+          if (blk[2] == 0) continue;
+          MRSP_CUDA(cudaMemcpy2DAsync(qh + static_cast<size_t>(src.b) * Cr + blk[1],
+                                      static_cast<size_t>(Cr) * 2,
+                                      src.qkv.as<bf16>() + blk[0], static_cast<size_t>(Cqkv) * 2,
+                                      static_cast<size_t>(blk[2]) * 2, n, cudaMemcpyDeviceToDevice,
+                                      stream_));
+          if (&src != &dst) a2a_bytes.fetch_add(static_cast<uint64_t>(n) * blk[2] * 2);
+        }
+      }
+    }
+    return;
+  }
+  RankCtx& me = ranks_[0];
+  const long n_me = me.e - me.b;
+  const int Cme = (me.hs.nq() + 2 * me.hs.nkv()) * 128;
+  // pack per-peer send blocks [n_me, C_peer]
+  std::vector<size_t> soff(k_ + 1, 0);
+  std::vector<HeadSplit> hs(k_);
+  for (int p = 0; p < k_; ++p) {
+    hs[p] = head_split(nq, nkv, k_, p);
+    soff[p + 1] = soff[p] + static_cast<size_t>(n_me) * (hs[p].nq() + 2 * hs[p].nkv()) * 128;
+  }
+  bf16* sendb = static_cast<bf16*>(me.send.ensure(std::max<size_t>(soff[k_], 1) * 2));
+  for (int p = 0; p < k_; ++p) {
+    const int Cp = (hs[p].nq() + 2 * hs[p].nkv()) * 128;
+    for (auto& blk : col_blocks(hs[p])) {
+      if (blk[2] == 0 || n_me == 0) continue;
+      bf16* dst = p == me.g ? me.qh.as<bf16>() + static_cast<size_t>(me.b) * Cme + blk[1]
+                            : sendb + soff[p] + blk[1];
+      MRSP_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(Cp) * 2, me.qkv.as<bf16>() + blk[0],
+                                  static_cast<size_t>(Cqkv) * 2, static_cast<size_t>(blk[2]) * 2,
+                                  n_me, cudaMemcpyDeviceToDevice, stream_));
+    }
+  }
+  nccl_->group_start();
+  for (int p = 0; p < k_; ++p) {
+    if (p == me.g) continue;
+    const size_t sb = (soff[p + 1] - soff[p]) * 2;
+    if (sb) nccl_->send(sendb + soff[p], sb, p, stream_);
+    const long b = token_b_[p], e = token_e_[p];
+    const size_t rb = static_cast<size_t>(e - b) * Cme * 2;
+    if (rb) nccl_->recv(me.qh.as<bf16>() + static_cast<size_t>(b) * Cme, rb, p, stream_);
+    a2a_bytes.fetch_add(sb);
+  }
+  nccl_->group_end();
+}
+
+// Head shards [L, nq_r*128] -> sequence shards [n_r, nq*128].
+void Engine::a2a_backward(int L) {
+  (void)L;
+  const int nq = cfg_.n_q_heads, Cq = nq * 128;
+  Prof pc(*this, P_COMM);
+  if (!nccl_) {
+    for (auto& src : ranks_) {
+      const int Cs = src.hs.nq() * 128;
+      if (Cs == 0) continue;
+      for (auto& dst : ranks_) {
+        const long n = dst.e - dst.b;
+        if (n <= 0) continue;
+        MRSP_CUDA(cudaMemcpy2DAsync(dst.ol.as<bf16>() + src.hs.q_lo * 128,
+                                    static_cast<size_t>(Cq) * 2,
+                                    src.oh.as<bf16>() + static_cast<size_t>(dst.b) * Cs,
+                                    static_cast<size_t>(Cs) * 2, static_cast<size_t>(Cs) * 2, n,
+                                    cudaMemcpyDeviceToDevice, stream_));
+        if (&src != &dst) a2a_bytes.fetch_add(static_cast<uint64_t>(n) * Cs * 2);
+      }
+    }
+    return;
+  }
+  RankCtx& me = ranks_[0];
+  const long n_me = me.e - me.b;
+  const int Cme = me.hs.nq() * 128;
+  std::vector<HeadSplit> hs(k_);
+  std::vector<size_t> roff(k_ + 1, 0);
+  for (int p = 0; p < k_; ++p) {
+    hs[p] = head_split(nq, cfg_.n_kv_heads, k_, p);
+    roff[p + 1] = roff[p] + static_cast<size_t>(n_me) * hs[p].nq() * 128;
+  }
+  bf16* recvb = static_cast<bf16*>(me.recv.ensure(std::max<size_t>(roff[k_], 1) * 2));
+  nccl_->group_start();
+  for (int p = 0; p < k_; ++p) {
+    if (p == me.g) continue;
+    const long b = token_b_[p], e = token_e_[p];
+    const size_t sb = static_cast<size_t>(e - b) * Cme * 2;
+    if (sb) nccl_->send(me.oh.as<bf16>() + static_cast<size_t>(b) * Cme, sb, p, stream_);
+    const size_t rb = (roff[p + 1] - roff[p]) * 2;
+    if (rb) nccl_->recv(recvb + roff[p], rb, p, stream_);
+    a2a_bytes.fetch_add(sb);
+  }
+  nccl_->group_end();
+  for (int p = 0; p < k_; ++p) {
+    const int Cp = hs[p].nq() * 128;
+    if (Cp == 0 || n_me == 0) continue;
+    const bf16* src = p == me.g ? me.oh.as<bf16>() + static_cast<size_t>(me.b) * Cme : recvb + roff[p];
+    MRSP_CUDA(cudaMemcpy2DAsync(me.ol.as<bf16>() + hs[p].q_lo * 128, static_cast<size_t>(Cq) * 2,
+                                src, static_cast<size_t>(Cp) * 2, static_cast<size_t>(Cp) * 2, n_me,
+                                cudaMemcpyDeviceToDevice, stream_));
+  }
+}
+
+// ---------------------------------------------------------------------------
+void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
+                              const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                              int model, float* lp_out, float* lse_out, bool out_on_device) {
+  const auto& c = cfg_;
+  MRSP_REQUIRE(model == 0 || model == 1, MRSP_INVALID_ARGUMENT, "prefill: model must be 0 or 1");
+  MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "pad_batch: empty batch");
+  MRSP_REQUIRE(Lmax >= 1 && n_q >= 0, MRSP_INVALID_ARGUMENT, "prefill: bad lengths");
+  std::lock_guard<std::mutex> run(run_mu_);
+  const LlmW& W = llm_[model];
+  const int T = tokens_per_frame(), d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads;
+  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128;
+  const long n_frame_tok = static_cast<long>(emb.n_frames) * T;
+  const long Lp = n_frame_tok + n_q;
+  const long Ltot = Lp + static_cast<long>(G) * Lmax;
+  MRSP_REQUIRE(Ltot < (1L << 31), MRSP_INVALID_ARGUMENT, "prefill: sequence too long");
+  // host-side pad_batch semantics: validate rows, scored positions per rank
+  std::vector<long> row_off(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    MRSP_REQUIRE(lengths[g] >= 0 && lengths[g] <= Lmax, MRSP_INVALID_ARGUMENT,
+                 "prefill: row longer than Lmax");
+    row_off[g + 1] = row_off[g] + lengths[g];
+    for (int j = 0; j < lengths[g]; ++j)
+      MRSP_REQUIRE(resp[static_cast<size_t>(g) * Lmax + j] >= 0 &&
+                       resp[static_cast<size_t>(g) * Lmax + j] < c.vocab,
+                   MRSP_INVALID_ARGUMENT, "step_logits: prev token out of range");
+  }
+  for (int i = 0; i < n_q; ++i)
+    MRSP_REQUIRE(question[i] >= 0 && question[i] < c.vocab, MRSP_INVALID_ARGUMENT,
+                 "context_vector: token out of range");
+  const long total_scored = row_off[G];
+  const auto tplan = plan(Ltot, k_);
+  token_b_.resize(k_);
+  token_e_.resize(k_);
+  for (int w = 0; w < k_; ++w) {
+    token_b_[w] = tplan[w].first;
+    token_e_[w] = tplan[w].second;
+  }
+  cudaStream_t s = stream_;
+  // upload the group's tokens once (shared by all local ranks)
+  const size_t tok_ints = static_cast<size_t>(n_q) + static_cast<size_t>(G) * Lmax + G;
+  int32_t* dtok = static_cast<int32_t*>(io_.ensure(tok_ints * 4 + (total_scored + 64) * 8));
+  MRSP_CUDA(cudaMemcpyAsync(dtok, question, static_cast<size_t>(n_q) * 4, cudaMemcpyHostToDevice, s));
+  MRSP_CUDA(cudaMemcpyAsync(dtok + n_q, resp, static_cast<size_t>(G) * Lmax * 4,
+                            cudaMemcpyHostToDevice, s));
+  MRSP_CUDA(cudaMemcpyAsync(dtok + n_q + static_cast<size_t>(G) * Lmax, lengths,
+                            static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
+  float* dlp_full = reinterpret_cast<float*>(dtok + tok_ints);
+  float* dlse_full = dlp_full + total_scored + 16;
+  MRSP_CUDA(cudaMemsetAsync(dlp_full, 0, (2 * total_scored + 32) * 4, s));
+  const int32_t* d_question = dtok;
+  const int32_t* d_resp = dtok + n_q;
+  const int32_t* d_len = dtok + n_q + static_cast<size_t>(G) * Lmax;
+
+  for (auto& R : ranks_) {
+    R.b = tplan[R.g].first;
+    R.e = tplan[R.g].second;
+    const long n = R.e - R.b;
+    // scored positions of this shard: row region, j < len (never a pad: the
+    // prev token of position j is read only for j < len, engine.cpp:124)
+    std::vector<int32_t> idx, tgt, slot;
+    const long r0 = std::max(R.b, Lp);
+    for (long p = r0; p < R.e; ++p) {
+      const long q = p - Lp;
+      const int g = static_cast<int>(q / Lmax), j = static_cast<int>(q % Lmax);
+      if (j < lengths[g]) {
+        idx.push_back(static_cast<int32_t>(p - R.b));
+        tgt.push_back(resp[static_cast<size_t>(g) * Lmax + j]);
+        slot.push_back(static_cast<int32_t>(row_off[g] + j));
+      }
+    }
+    R.n_scored = static_cast<int>(idx.size());
+    int32_t* di = static_cast<int32_t*>(R.scored_idx.ensure((idx.size() + 1) * 4 * 3));
+    if (!idx.empty()) {
+      MRSP_CUDA(cudaMemcpyAsync(di, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
+      MRSP_CUDA(cudaMemcpyAsync(di + idx.size(), tgt.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
+      MRSP_CUDA(cudaMemcpyAsync(di + 2 * idx.size(), slot.data(), idx.size() * 4,
+                                cudaMemcpyHostToDevice, s));
+      MRSP_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    }
+    // activations
+    R.h.ensure(static_cast<size_t>(std::max(n, 1L)) * d * 4);
+    R.xn.ensure(static_cast<size_t>(std::max(n, 1L)) * d * 2);
+    R.qkv.ensure(static_cast<size_t>(std::max(n, 1L)) * Cqkv * 2);
+    R.ol.ensure(static_cast<size_t>(std::max(n, 1L)) * Cq * 2);
+    R.act.ensure(static_cast<size_t>(std::max(n, 1L)) * c.mlp * 2);
+    R.pos.ensure(static_cast<size_t>(std::max(n, 1L)) * 4);
+    R.pad.ensure(static_cast<size_t>(std::max(n, 1L)));
+    if (k_ > 1) {
+      R.qh.ensure(static_cast<size_t>(Ltot) * (R.hs.nq() + 2 * R.hs.nkv()) * 128 * 2);
+      R.oh.ensure(static_cast<size_t>(Ltot) * std::max(R.hs.nq(), 1) * 128 * 2);
+    }
+    {
+      Prof pm(*this, P_MISC);
+      pack_sequence(emb.emb->as<bf16>(), static_cast<int>(n_frame_tok), d_question, n_q, d_resp,
+                    d_len, Lmax, W.embed, d, R.b, static_cast<int>(n), R.h.as<float>(),
+                    R.pos.as<int>(), R.pad.as<unsigned char>(), nullptr, s);
+    }
+  }
+  const float scale = 1.0f / std::sqrt(128.0f);
+  for (const auto& Lw : W.layers) {
+    for (auto& R : ranks_) {
+      const int n = static_cast<int>(R.e - R.b);
+      if (n <= 0) continue;
+      {
+        Prof pm(*this, P_MISC);
+        rmsnorm(R.h.as<float>(), d, Lw.attn_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
+      }
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({R.xn.p, Lw.wqkv, R.qkv.p, n, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv,
+                   nullptr, 0},
+                  s);
+      }
+      {
+        Prof pm(*this, P_MISC);
+        rope(R.qkv.as<bf16>(), Cqkv, 0, nq + nkv, R.pos.as<int>(), n, s);
+      }
+    }
+    if (k_ > 1) a2a_forward(static_cast<int>(Ltot));
+    for (auto& R : ranks_) {
+      const int nqr = R.hs.nq();
+      if (nqr == 0) continue;
+      Prof pa(*this, P_ATTN);
+      if (k_ == 1) {
+        attention_fwd({R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
+                       R.ol.p, Cq, 0, static_cast<int>(Ltot), nq, nq / nkv, scale,
+                       ATTN_CAUSAL_PREFIX, static_cast<int>(Lp), Lmax, 0},
+                      s);
+      } else {
+        const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
+        attention_fwd({R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr,
+                       (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(Ltot), nqr,
+                       R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(Lp), Lmax, 0},
+                      s);
+      }
+    }
+    if (k_ > 1) a2a_backward(static_cast<int>(Ltot));
+    for (auto& R : ranks_) {
+      const int n = static_cast<int>(R.e - R.b);
+      if (n <= 0) continue;
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr,
+                   R.h.as<float>(), d},
+                  s);
+      }
+      {
+        Prof pm(*this, P_MISC);
+        rmsnorm(R.h.as<float>(), d, Lw.mlp_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
+      }
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({R.xn.p, Lw.wgu, R.act.p, n, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16,
+                   nullptr, nullptr, 0},
+                  s);
+        gemm_bf16({R.act.p, Lw.wdown, nullptr, n, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
+                   nullptr, R.h.as<float>(), d},
+                  s);
+      }
+    }
+  }
+  // final norm + fused LM head at the scored positions of each shard
+  for (auto& R : ranks_) {
+    const int ns = R.n_scored;
+    if (ns == 0) continue;
+    const int32_t* di = R.scored_idx.as<int32_t>();
+    bf16* xs = static_cast<bf16*>(R.xs.ensure(static_cast<size_t>(ns) * d * 2));
+    float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 8));
+    rmsnorm(R.h.as<float>(), d, W.final_norm, xs, d, ns, d, c.rms_eps, di, s);
+    const size_t wsb = lmhead_workspace_bytes(ns, c.vocab);
+    void* ws = R.ws.ensure(wsb);
+    {
+      Prof pl(*this, P_LMHEAD);
+      lmhead_logprob(xs, d, W.lm_head, ns, c.vocab, d, di + ns, lp, lp + ns, ws, wsb, s);
+    }
+    scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp, di + 2 * ns, ns, dlp_full);
+    scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp + ns, di + 2 * ns, ns, dlse_full);
+    MRSP_CUDA(cudaGetLastError());
+  }
+  if (nccl_) {
+    Prof pc(*this, P_COMM);
+    nccl_->all_reduce_sum_f32(dlp_full, dlp_full, static_cast<size_t>(2 * total_scored + 32), s);
+  }
+  const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (total_scored) {
+    MRSP_CUDA(cudaMemcpyAsync(lp_out, dlp_full, total_scored * 4, kind, s));
+    if (lse_out) MRSP_CUDA(cudaMemcpyAsync(lse_out, dlse_full, total_scored * 4, kind, s));
+  }
+  MRSP_CUDA(cudaStreamSynchronize(s));
+  prof_collect();
+}
+
+size_t Engine::cache_size() {
+  std::lock_guard<std::mutex> lock(cache_mu_);
+  return cache_.size();
+}
+void Engine::cache_clear() {
+  std::lock_guard<std::mutex> lock(cache_mu_);
+  cache_.clear();
+}
+void Engine::copy_embeddings(const CacheEntry& e, void* host_out) {
+  MRSP_CUDA(cudaMemcpy(host_out, e.emb->p,
+                       static_cast<size_t>(e.n_frames) * tokens_per_frame() * cfg_.dim * 2,
+                       cudaMemcpyDeviceToHost));
+}
+
+}  // namespace mrsp
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+struct mrsp_engine {
+  std::unique_ptr<mrsp::Engine> impl;
+  std::mutex mu;
+  std::map<std::string, std::shared_ptr<mrsp::CacheEntry>> last;  // pins for prefill
+};
+
+using namespace mrsp;
+
+extern "C" mrsp_status mrsp_nccl_unique_id(void* out128) {
+  return guard([&] { Nccl::unique_id(out128); });
+}
+
+extern "C" mrsp_status mrsp_engine_create(const mrsp_model_config* cfg, int sp_degree,
+                                          int proc_rank, int n_procs, uint64_t vision_seed,
+                                          uint64_t policy_seed, uint64_t ref_seed, int with_ref,
+                                          const void* nccl_id, mrsp_engine** out) {
+  return guard([&] {
+    MRSP_REQUIRE(cfg && out, MRSP_INVALID_ARGUMENT, "engine: null argument");
+    auto e = std::make_unique<mrsp_engine>();
+    e->impl = std::make_unique<Engine>(*cfg, sp_degree, proc_rank, n_procs, vision_seed,
+                                       policy_seed, ref_seed, with_ref, nccl_id);
+    *out = e.release();
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_destroy(mrsp_engine* e) {
+  return guard([&] { delete e; });
+}
+
+static std::shared_ptr<CacheEntry> lookup(mrsp_engine* e, const char* id) {
+  std::lock_guard<std::mutex> lock(e->mu);
+  auto it = e->last.find(id);
+  MRSP_REQUIRE(it != e->last.end(), MRSP_INVALID_ARGUMENT,
+               std::string("prefill: video not encoded: ") + id);
+  return it->second;
+}
+
+extern "C" mrsp_status mrsp_engine_encode(mrsp_engine* e, const char* video_id,
+                                          const float* pixels, int F, int pixels_on_device,
+                                          int use_cache, int* hit) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && pixels, MRSP_INVALID_ARGUMENT, "encode: null argument");
+    bool h = false;
+    auto entry = e->impl->get_or_encode(video_id, pixels, F, pixels_on_device != 0, use_cache != 0, &h);
+    {
+      std::lock_guard<std::mutex> lock(e->mu);
+      e->last[video_id] = entry;
+      while (e->last.size() > 4) {
+        auto oldest = std::min_element(e->last.begin(), e->last.end(),
+                                       [](auto& a, auto& b) { return a.second->seq < b.second->seq; });
+        if (oldest->first == video_id) break;
+        e->last.erase(oldest);
+      }
+    }
+    if (hit) *hit = h ? 1 : 0;
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_prefill_logprobs(mrsp_engine* e, const char* video_id,
+                                                    const int32_t* question, int n_q,
+                                                    const int32_t* resp, const int32_t* lengths,
+                                                    int G, int Lmax, int model, float* logprob,
+                                                    float* lse, int out_on_device) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && resp && lengths && logprob, MRSP_INVALID_ARGUMENT,
+                 "prefill: null argument");
+    auto entry = lookup(e, video_id);
+    e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, model, logprob, lse,
+                              out_on_device != 0);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, const float* pixels,
+                                        int F, int pixels_on_device, int use_cache,
+                                        const int32_t* question, int n_q, const int32_t* resp,
+                                        const int32_t* lengths, int G, int Lmax,
+                                        float* logprob_policy, float* logprob_ref,
+                                        int out_on_device) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && pixels, MRSP_INVALID_ARGUMENT, "step: null argument");
+    std::shared_ptr<CacheEntry> entry;
+    for (int g = 0; g < G; ++g) {  // one embedding fetch per rollout (grpo.cpp:376-379)
+      bool h = false;
+      entry = e->impl->get_or_encode(video_id, pixels, F, pixels_on_device != 0, use_cache != 0, &h);
+    }
+    e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, 0, logprob_policy,
+                              nullptr, out_on_device != 0);
+    e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, 1, logprob_ref,
+                              nullptr, out_on_device != 0);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_stats(mrsp_engine* e, uint64_t* out6, int reset) {
+  return guard([&] {
+    Engine& x = *e->impl;
+    out6[0] = x.encoder_invocations.load();
+    out6[1] = x.cache_hits.load();
+    out6[2] = x.cache_misses.load();
+    out6[3] = x.gather_bytes.load();
+    out6[4] = x.pad_reads.load();
+    out6[5] = x.a2a_bytes.load();
+    if (reset) {
+      x.encoder_invocations = 0;
+      x.cache_hits = 0;
+      x.cache_misses = 0;
+      x.gather_bytes = 0;
+      x.pad_reads = 0;
+      x.a2a_bytes = 0;
+    }
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_cache(mrsp_engine* e, int op, int arg, uint64_t* size_out) {
+  return guard([&] {
+    if (op == 1) {
+      e->impl->cache_clear();
+      std::lock_guard<std::mutex> lock(e->mu);
+      e->last.clear();
+    } else if (op == 2) {
+      e->impl->cache_capacity = arg;
+    }
+    if (size_out) *size_out = e->impl->cache_size();
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* video_id,
+                                                  void* host_out) {
+  return guard([&] {
+    auto entry = lookup(e, video_id);
+    e->impl->copy_embeddings(*entry, host_out);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, double* ms,
+                                           int64_t* launches) {
+  return guard([&] {
+    if (enable >= 0) e->impl->set_profiling(enable != 0);
+    if (ms && launches) {
+      long n = 0;
+      e->impl->profile_read(cls, ms, &n);
+      *launches = n;
+    }
+  });
+}
+
+extern "C" void* mrsp_engine_stream(mrsp_engine* e) { return e ? e->impl->stream() : nullptr; }

@@ -1,0 +1,179 @@
+// engine.h — the transformer-shaped MR-SP engine (csrc/engine.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "mrsp_c.h"
+
+namespace mrsp {
+
+using bf16 = __nv_bfloat16;
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release();
+  void* ensure(size_t b);
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct VisionLayerW {
+  float *ln1_w, *ln1_b, *bqkv, *bo, *ln2_w, *ln2_b, *b1, *b2;
+  bf16 *wqkv, *wo, *w1, *w2;
+};
+struct VisionW {
+  bf16* patch_w;
+  float *patch_b, *pos;
+  std::vector<VisionLayerW> layers;
+  float *post_w, *post_b, *p1_b, *p2_b;
+  bf16 *p1_w, *p2_w;
+};
+struct LlmLayerW {
+  float *attn_norm, *bqkv, *mlp_norm;
+  bf16 *wqkv, *wo, *wgu, *wdown;
+};
+struct LlmW {
+  bf16* embed;
+  std::vector<LlmLayerW> layers;
+  float* final_norm;
+  bf16* lm_head;
+};
+
+struct HeadSplit {
+  int q_lo, q_hi, kv_lo, kv_hi, q_per_kv;
+  int nq() const { return q_hi - q_lo; }
+  int nkv() const { return kv_hi - kv_lo; }
+};
+
+// One SP rank living in this process (k of them in loopback mode, 1 with NCCL).
+struct RankCtx {
+  int g = 0;  // global SP rank
+  HeadSplit hs{};
+  // stage 1
+  DevBuf pix, patches, vh, vxn, vqkv, vo, vmid, pout;
+  // stage 2
+  DevBuf h, xn, qkv, qh, oh, ol, act, pos, pad, scored_idx, scored_tgt, scored_slot, xs, lp, ws,
+      send, recv;
+  long b = 0, e = 0;  // token range
+  int n_scored = 0;
+};
+
+struct CacheEntry {
+  std::mutex m;
+  std::condition_variable cv;
+  bool ready = false;
+  bool failed = false;
+  std::string error;
+  std::shared_ptr<DevBuf> emb;  // [F*T][dim] bf16, all frames (gathered)
+  int n_frames = 0;
+  uint64_t seq = 0;
+};
+
+class Engine {
+ public:
+  Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n_procs,
+         uint64_t vision_seed, uint64_t policy_seed, uint64_t ref_seed, int with_ref,
+         const void* nccl_id);
+  ~Engine();
+
+  // Stage 1 with the exactly-once cache (engine.cpp:155-197 protocol).
+  std::shared_ptr<CacheEntry> get_or_encode(const std::string& id, const float* pixels, int F,
+                                            bool on_device, bool use_cache, bool* hit);
+  // Stage 2 for one model over the packed GRPO group; lp_out has sum(lengths)
+  // entries (host or device per lp_on_device).
+  void prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
+                        const int32_t* resp, const int32_t* lengths, int G, int Lmax, int model,
+                        float* lp_out, float* lse_out, bool out_on_device);
+
+  const mrsp_model_config& cfg() const { return cfg_; }
+  int tokens_per_frame() const { return (cfg_.image_size / cfg_.patch) * (cfg_.image_size / cfg_.patch); }
+  int sp() const { return k_; }
+  cudaStream_t stream() const { return stream_; }
+  std::vector<RankCtx>& ranks() { return ranks_; }
+
+  // counters (EngineStats, engine.hpp:27-41, plus device traffic)
+  std::atomic<uint64_t> encoder_invocations{0}, cache_hits{0}, cache_misses{0}, gather_bytes{0},
+      pad_reads{0}, a2a_bytes{0};
+  size_t cache_size();
+  void cache_clear();
+  int cache_capacity = 0;  // 0 = unbounded
+
+  // profiling: CUDA-event time per kernel class
+  void set_profiling(bool on);
+  void profile_read(int cls, double* ms, long* launches);
+  void copy_embeddings(const CacheEntry& e, void* host_out);
+
+ private:
+  friend struct Prof;
+  void init_weights(uint64_t vision_seed, uint64_t policy_seed, uint64_t ref_seed, int with_ref);
+  void encode_rank(RankCtx& R, const float* pixels, bool on_device, int F, long fb, long fe,
+                   bf16* out);
+  void a2a_forward(int L);
+  void a2a_backward(int L);
+
+  mrsp_model_config cfg_;
+  int k_, proc_rank_, n_procs_, device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::unique_ptr<Nccl> nccl_;
+  std::vector<RankCtx> ranks_;
+  DevBuf wbuf_;  // all weights
+  VisionW vis_{};
+  LlmW llm_[2]{};
+  bool has_ref_ = false;
+  int vhd_pad_ = 128;
+  std::vector<long> token_b_, token_e_;  // current stage-2 plan
+  std::mutex cache_mu_;
+  std::map<std::string, std::shared_ptr<CacheEntry>> cache_;
+  uint64_t cache_seq_ = 0;
+  std::mutex run_mu_;  // one stage at a time per engine
+  // profiling
+  bool prof_ = false;
+  struct Ev {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> ev_pending_;
+  std::vector<cudaEvent_t> ev_pool_;
+  double prof_ms_[8] = {0};
+  long prof_n_[8] = {0};
+  void prof_begin(int cls, cudaEvent_t* a);
+  void prof_end(int cls, cudaEvent_t a);
+  void prof_collect();
+
+ public:
+  DevBuf io_;  // step I/O staging
+};
+
+HeadSplit head_split(int nq, int nkv, int k, int r);
+
+}  // namespace mrsp

@@ -22,6 +22,7 @@
 
 #include "common.h"
 #include "gemm.h"
+#include "misc.h"
 #include "sm100.cuh"
 #include "tma.h"
 
@@ -45,6 +46,9 @@ struct EpiArgs {
   const float* bias;
   float* resid;
   int ldr;
+  const int* targets;  // LOGPROB: target id per row
+  float2* part;        // LOGPROB: [M][n_tiles] (tile max, sum exp(x - max))
+  float* tgt_logit;    // LOGPROB: logit of the target per row
 };
 
 // Grouped raster: consecutive tiles sweep a GROUP_M-tall band of m-tiles with
@@ -161,7 +165,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = mt * BM + ew * 32 + lane_id();
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      if (args.epi == GEMM_EPI_SWIGLU_BF16) {
+      if (args.epi == GEMM_EPI_LOGPROB_PARTIAL) {
+        // Fused vocabulary projection + log-softmax pieces: this 256-wide vocab
+        // tile's (max, sum exp) per row and the target logit if it lies here.
+        // Logits never leave TMEM/registers.
+        const int tgt = row_ok ? args.targets[row] : -1;
+        float m = -INFINITY, ssum = 0.f;
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c, r);
+          tmem_ld_wait();
+          const int col = nt * BN + c;
+          float cm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col + j < args.N) cm = fmaxf(cm, __uint_as_float(r[j]));
+          const float mn = fmaxf(m, cm);
+          float acc_s = (m == -INFINITY) ? 0.f : ssum * __expf(m - mn);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(r[j]);
+            if (col + j < args.N) acc_s += __expf(x - mn);
+            if (col + j == tgt) args.tgt_logit[row] = x;
+          }
+          m = mn;
+          ssum = acc_s;
+        }
+        if (row_ok) args.part[static_cast<size_t>(row) * n_tiles + nt] = make_float2(m, ssum);
+      } else if (args.epi == GEMM_EPI_SWIGLU_BF16) {
         // columns [0,128) are gate, [128,256) the matching up projections
         __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
         for (int c = 0; c < BN / 2; c += 32) {
@@ -296,11 +327,38 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   const int ld_out = g.epi == GEMM_EPI_RESID_F32 ? g.ldr : g.ldc;
   const int elem_per_16b = (f32_out || g.epi == GEMM_EPI_RESID_F32) ? 4 : 8;
   const int vec_ok = (out_addr % 16 == 0) && (ld_out % elem_per_16b == 0);
-  EpiArgs e{g.M, g.N, g.K, g.epi, vec_ok, g.C, g.ldc, g.bias, g.resid, g.ldr};
+  EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     g.C,        g.ldc,
+            g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit};
+  if (g.epi == GEMM_EPI_LOGPROB_PARTIAL)
+    MRSP_REQUIRE(g.targets && g.part && g.tgt_logit, MRSP_INVALID_ARGUMENT,
+                 "gemm logprob: null targets/partials");
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = std::min(tiles, num_sms());
   gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, e);
   MRSP_CUDA(cudaGetLastError());
+}
+
+size_t lmhead_workspace_bytes(int M, int V) {
+  const size_t n_tiles = (V + BN - 1) / BN;
+  return (static_cast<size_t>(M) * n_tiles * sizeof(float2) + static_cast<size_t>(M) * 4 + 255) &
+         ~size_t(255);
+}
+
+void lmhead_logprob(const void* X, int ldx, const void* W, int M, int V, int K,
+                    const int32_t* targets, float* logprob, float* lse, void* ws, size_t ws_bytes,
+                    cudaStream_t stream) {
+  if (M <= 0) return;
+  MRSP_REQUIRE(ws_bytes >= lmhead_workspace_bytes(M, V), MRSP_INVALID_ARGUMENT,
+               "lmhead_logprob: workspace too small");
+  const int n_tiles = (V + BN - 1) / BN;
+  float2* part = static_cast<float2*>(ws);
+  float* tgt = reinterpret_cast<float*>(part + static_cast<size_t>(M) * n_tiles);
+  GemmArgs g{X, W, nullptr, M, V, K, ldx, K, 0, GEMM_EPI_LOGPROB_PARTIAL, nullptr, nullptr, 0};
+  g.targets = targets;
+  g.part = part;
+  g.tgt_logit = tgt;
+  gemm_bf16(g, stream);
+  logprob_combine(part, n_tiles, tgt, M, logprob, lse, stream);
 }
 
 }  // namespace mrsp
@@ -313,4 +371,19 @@ extern "C" mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, 
     mrsp::GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, epilogue, bias, resid, ldr};
     mrsp::gemm_bf16(g, static_cast<cudaStream_t>(stream));
   });
+}
+
+extern "C" mrsp_status mrsp_op_lmhead_logprob(const void* X, int ldx, const void* W, int M, int V,
+                                              int K, const int32_t* targets, float* logprob,
+                                              float* lse, void* workspace, size_t ws_bytes,
+                                              void* stream) {
+  return mrsp::guard([&] {
+    mrsp::require_device();
+    mrsp::lmhead_logprob(X, ldx, W, M, V, K, targets, logprob, lse, workspace, ws_bytes,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" size_t mrsp_lmhead_workspace_bytes(int M, int V) {
+  return mrsp::lmhead_workspace_bytes(M, V);
 }

@@ -17,8 +17,18 @@ struct GemmArgs {
   const float* bias;    // [N] fp32 or null
   float* resid;         // fp32 residual for GEMM_EPI_RESID_F32
   int ldr;
+  const int* targets = nullptr;  // GEMM_EPI_LOGPROB_PARTIAL
+  float2* part = nullptr;
+  float* tgt_logit = nullptr;
 };
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
+
+// Fused LM head: per row, log softmax(X W^T)[target] and the log-partition,
+// never materialising the [M x V] logits.
+size_t lmhead_workspace_bytes(int M, int V);
+void lmhead_logprob(const void* X, int ldx, const void* W, int M, int V, int K,
+                    const int32_t* targets, float* logprob, float* lse, void* ws, size_t ws_bytes,
+                    cudaStream_t stream);
 
 }  // namespace mrsp

@@ -1,0 +1,30 @@
+// misc.h — HBM-bound kernels around the tensor-core work (csrc/kernels_misc.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mrsp {
+
+void rmsnorm(const float* x, int ldx, const float* w, __nv_bfloat16* out, int ldo, int n, int d,
+             float eps, const int* rows, cudaStream_t s);
+void layernorm(const float* x, int ldx, const float* w, const float* b, __nv_bfloat16* out,
+               int ldo, int n, int d, float eps, cudaStream_t s);
+void set_rope_inv_freq(const float* inv_freq64, cudaStream_t s);
+void rope(__nv_bfloat16* qkv, int ld, int col0, int n_heads, const int* pos, int n, cudaStream_t s);
+void patchify(const float* pix, __nv_bfloat16* out, int F, int H, int W, int P, int kpad,
+              cudaStream_t s);
+void broadcast_rows(const float* src, float* dst, int n, int period, int d, cudaStream_t s);
+void pack_sequence(const __nv_bfloat16* frame_emb, int n_frame_tok, const int* question, int n_q,
+                   const int* resp, const int* lengths, int Lmax, const __nv_bfloat16* embed,
+                   int d, long p0, int n, float* hidden, int* pos_ids, unsigned char* pad_mask,
+                   int* tok_out, cudaStream_t s);
+void logprob_combine(const float2* part, int n_tiles, const float* tgt_logit, int n, float* lp,
+                     float* lse, cudaStream_t s);
+void init_uniform_bf16(__nv_bfloat16* w, size_t n, uint64_t key, float scale, cudaStream_t s);
+void init_uniform_f32(float* w, size_t n, uint64_t key, float scale, float offset, cudaStream_t s);
+void convert_bf16_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s);
+
+}  // namespace mrsp

@@ -1,0 +1,245 @@
+"""Host-side front-end of the MR-SP engine (include/mrsp_c.h, csrc/engine.cu).
+
+Mirrors the reference's two-stage call sites: ``encode`` is the Stage-1
+fetch_embeddings / EmbeddingCache::get_or_encode (grpo.cpp:289-295,
+engine.cpp:155-197); ``prefill_logprobs`` is engine_group_logits + the
+log-softmax/gather (grpo.cpp:44-55, :82-85); ``step`` is run_step
+(engine.cpp:203-225). All compute runs in libmrsp_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import asdict, dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+K_PAD, K_EOS, K_CONTENT_BASE = 0, 1, 10  # mmseq.hpp:15-23
+
+
+class ModelConfig(ctypes.Structure):
+    """mrsp_model_config."""
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "image_size", "patch", "v_dim", "v_heads", "v_head_dim", "v_mlp", "v_layers", "dim",
+        "n_q_heads", "n_kv_heads", "head_dim", "mlp", "layers", "vocab")] + [
+        ("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("ln_eps", ctypes.c_float)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+    @property
+    def tokens_per_frame(self) -> int:
+        return (self.image_size // self.patch) ** 2
+
+
+def _cfg(**kw) -> ModelConfig:
+    base = dict(rope_theta=1e6, rms_eps=1e-6, ln_eps=1e-6, head_dim=128)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+SIGLIP = dict(image_size=224, patch=14, v_dim=1152, v_heads=16, v_head_dim=72, v_mlp=4304,
+              v_layers=27)
+QWEN7B = dict(dim=3584, n_q_heads=28, n_kv_heads=4, mlp=18944, layers=28, vocab=152064)
+
+
+@dataclass
+class Workload:
+    """One BASELINE.json configuration: model shape + the synthetic GRPO group."""
+    name: str
+    cfg: ModelConfig
+    frames: int
+    sp: int
+    G: int
+    n_question: int
+    len_lo: int
+    len_hi: int
+    desc: str = ""
+
+
+def workloads():
+    """BASELINE.json configs c1..c5."""
+    c1 = _cfg(image_size=64, patch=8, v_dim=256, v_heads=4, v_head_dim=64, v_mlp=1024, v_layers=2,
+              dim=256, n_q_heads=4, n_kv_heads=2, mlp=1024, layers=2, vocab=32)
+    c2 = _cfg(**SIGLIP, **{**QWEN7B, "layers": 4})
+    c3 = _cfg(**SIGLIP, **QWEN7B)
+    return {
+        "c1": Workload("c1", c1, 8, 1, 4, 3, 6, 12,
+                       "tiny synthetic MR-SP step: 8 frames x 64 tokens, 2-layer vision + 2-layer "
+                       "LLM (d=256), SP=1, 4 rollouts"),
+        "c2": Workload("c2", c2, 64, 2, 8, 37, 512, 1024,
+                       "64 frames x 256 tokens, SigLIP-shaped tower + 4-layer Qwen2.5-7B-shaped LLM, SP=2"),
+        "c3": Workload("c3", c3, 256, 4, 8, 37, 512, 1024,
+                       "256 frames x 256 tokens, 28-layer Qwen2.5-7B-shaped prefill, SP=4, G=8"),
+        "c4": Workload("c4", c3, 512, 8, 8, 37, 512, 1024,
+                       "512 frames x 256 tokens (~131K tokens), 7B-shaped encode+prefill, SP=8"),
+        "c5": Workload("c5", c3, 1024, 8, 8, 37, 512, 1024,
+                       "1024 frames (~262K tokens), 7B-shaped prefill, policy + reference, SP=8"),
+    }
+
+
+@dataclass
+class Group:
+    """A GRPO group's token data: question + G responses padded to Lmax."""
+    question: np.ndarray  # int32 [n_q]
+    resp: np.ndarray      # int32 [G, Lmax] (PAD past lengths)
+    lengths: np.ndarray   # int32 [G]
+
+    @property
+    def Lmax(self) -> int:
+        return int(self.resp.shape[1])
+
+    @property
+    def scored(self) -> int:
+        return int(self.lengths.sum())
+
+
+def make_group(w: Workload, seed: int = 3) -> Group:
+    """Seeded synthetic group: content tokens U[kContentBase, V), lengths
+    U[len_lo, len_hi] (SURVEY §8d value distributions)."""
+    rng = np.random.default_rng(seed)
+    V = w.cfg.vocab
+    q = rng.integers(K_CONTENT_BASE, V, size=w.n_question, dtype=np.int64).astype(np.int32)
+    lengths = rng.integers(w.len_lo, w.len_hi + 1, size=w.G).astype(np.int32)
+    Lmax = int(lengths.max())
+    resp = np.full((w.G, Lmax), K_PAD, dtype=np.int32)
+    for g in range(w.G):
+        resp[g, : lengths[g]] = rng.integers(K_CONTENT_BASE, V, size=int(lengths[g]))
+    return Group(q, resp, lengths)
+
+
+def gen_video(seed: int, frames: int, feature_dim: int) -> np.ndarray:
+    """mmseq::gen_video as fp32 (mrsp_gen_video)."""
+    out = np.empty((frames, feature_dim), dtype=np.float32)
+    check(_lib.lib().mrsp_gen_video(seed, frames, feature_dim,
+                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+    return out
+
+
+def video_id(seed: int, frames: int) -> str:
+    return f"v{seed}f{frames}"  # mmseq.cpp:64
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(_lib.lib().mrsp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _ptr(a, t=ctypes.c_int32):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.cast(ctypes.c_void_p(a.data_ptr()), ctypes.POINTER(t))
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+class Engine:
+    """One process's share of an SP group (sp virtual ranks when n_procs == 1)."""
+
+    def __init__(self, cfg: ModelConfig, sp: int = 1, rank: int = 0, n_procs: int = 1,
+                 vision_seed: int = 2, policy_seed: int = 3, ref_seed: int = 4,
+                 with_ref: bool = True, nccl_id: Optional[bytes] = None):
+        self.cfg = cfg
+        self.sp = sp
+        self._h = ctypes.c_void_p()
+        idb = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        check(_lib.lib().mrsp_engine_create(ctypes.byref(cfg), sp, rank, n_procs, vision_seed,
+                                            policy_seed, ref_seed, int(with_ref), idb,
+                                            ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            check(_lib.lib().mrsp_engine_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(_lib.lib().mrsp_engine_stream(self._h) or 0)
+
+    def encode(self, vid: str, pixels, use_cache: bool = True) -> bool:
+        """Stage 1; pixels [F, 3*S*S] fp32 numpy (host) or torch CUDA tensor."""
+        on_dev = hasattr(pixels, "is_cuda") and pixels.is_cuda
+        F = int(pixels.shape[0])
+        hit = ctypes.c_int(0)
+        check(_lib.lib().mrsp_engine_encode(self._h, vid.encode(), _ptr(pixels, ctypes.c_float), F,
+                                            int(on_dev), int(use_cache), ctypes.byref(hit)))
+        return bool(hit.value)
+
+    def prefill_logprobs(self, vid: str, group: Group, model: int = 0, with_lse: bool = False):
+        n = group.scored
+        lp = np.zeros(n, dtype=np.float32)
+        lse = np.zeros(n, dtype=np.float32) if with_lse else None
+        check(_lib.lib().mrsp_engine_prefill_logprobs(
+            self._h, vid.encode(), _ptr(np.ascontiguousarray(group.question)), len(group.question),
+            _ptr(np.ascontiguousarray(group.resp)), _ptr(np.ascontiguousarray(group.lengths)),
+            int(group.resp.shape[0]), group.Lmax, model, _ptr(lp, ctypes.c_float),
+            _ptr(lse, ctypes.c_float), 0))
+        return (lp, lse) if with_lse else lp
+
+    def step(self, vid: str, pixels, group: Group, use_cache: bool = True, out=None):
+        """run_step: G fetches + policy and reference log-probs. `out` = optional
+        pair of device tensors to receive the log-probs without a D2H copy."""
+        on_dev = hasattr(pixels, "is_cuda") and pixels.is_cuda
+        n = group.scored
+        if out is None:
+            lp_p = np.zeros(n, dtype=np.float32)
+            lp_r = np.zeros(n, dtype=np.float32)
+            out_dev = 0
+        else:
+            lp_p, lp_r = out
+            out_dev = 1
+        check(_lib.lib().mrsp_engine_step(
+            self._h, vid.encode(), _ptr(pixels, ctypes.c_float), int(pixels.shape[0]), int(on_dev),
+            int(use_cache), _ptr(np.ascontiguousarray(group.question)), len(group.question),
+            _ptr(np.ascontiguousarray(group.resp)), _ptr(np.ascontiguousarray(group.lengths)),
+            int(group.resp.shape[0]), group.Lmax, _ptr(lp_p, ctypes.c_float),
+            _ptr(lp_r, ctypes.c_float), out_dev))
+        return lp_p, lp_r
+
+    def stats(self, reset: bool = False) -> dict:
+        out = (ctypes.c_uint64 * 6)()
+        check(_lib.lib().mrsp_engine_stats(self._h, out, int(reset)))
+        return dict(zip(["encoder_invocations", "cache_hits", "cache_misses", "gather_bytes",
+                         "pad_reads", "a2a_bytes"], [int(x) for x in out]))
+
+    def cache_size(self) -> int:
+        n = ctypes.c_uint64()
+        check(_lib.lib().mrsp_engine_cache(self._h, 0, 0, ctypes.byref(n)))
+        return int(n.value)
+
+    def cache_clear(self):
+        check(_lib.lib().mrsp_engine_cache(self._h, 1, 0, None))
+
+    def cache_capacity(self, n: int):
+        check(_lib.lib().mrsp_engine_cache(self._h, 2, n, None))
+
+    def embeddings(self, vid: str, frames: int) -> np.ndarray:
+        """Cached [F*T, dim] embeddings as float32 (from bf16)."""
+        T = self.cfg.tokens_per_frame
+        raw = np.empty((frames * T, self.cfg.dim), dtype=np.uint16)
+        check(_lib.lib().mrsp_engine_get_embeddings(self._h, vid.encode(),
+                                                    raw.ctypes.data_as(ctypes.c_void_p)))
+        return (raw.astype(np.uint32) << 16).view(np.float32)
+
+    PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc"]
+
+    def profile(self, enable: Optional[bool] = None) -> dict:
+        en = -1 if enable is None else int(enable)
+        check(_lib.lib().mrsp_engine_profile(self._h, en, 0, None, None))
+        out = {}
+        for i, name in enumerate(self.PROFILE_CLASSES):
+            ms = ctypes.c_double()
+            n = ctypes.c_int64()
+            check(_lib.lib().mrsp_engine_profile(self._h, -1, i, ctypes.byref(ms), ctypes.byref(n)))
+            out[name] = (ms.value, n.value)
+        return out

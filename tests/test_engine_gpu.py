@@ -1,0 +1,127 @@
+"""GPU: the MR-SP engine (csrc/engine.cu) through the C-ABI vs the CPU oracle
+(oracle/transformer.py) on c1, SP invariance (loopback virtual ranks), the
+exactly-once cache counters and the pack kernel's bit-exact layout."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import transformer as T
+from paper_2507_07966_b200 import _lib, engine as E
+
+pytestmark = pytest.mark.gpu
+
+W1 = E.workloads()["c1"]
+VSEED, PSEED, RSEED = 2, 3, 4
+
+
+@pytest.fixture(scope="module")
+def c1_oracle():
+    c = T.Cfg.from_any(W1.cfg)
+    pix = E.gen_video(1, W1.frames, 3 * c.image_size ** 2)
+    grp = E.make_group(W1, seed=3)
+    emb = T.vision_forward(c, T.vision_weights(c, VSEED), pix)
+    lp_p, lse_p = T.llm_logprobs(c, T.llm_weights(c, PSEED, "policy."), emb, grp.question,
+                                 grp.resp, grp.lengths)
+    lp_r, _ = T.llm_logprobs(c, T.llm_weights(c, RSEED, "ref."), emb, grp.question, grp.resp,
+                             grp.lengths)
+    return dict(pix=pix, grp=grp, emb=emb, lp_p=lp_p, lse_p=lse_p, lp_r=lp_r)
+
+
+def run_engine(sp, pix, grp):
+    eng = E.Engine(W1.cfg, sp=sp, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    vid = E.video_id(1, W1.frames)
+    assert eng.encode(vid, pix) is False
+    emb = eng.embeddings(vid, W1.frames)
+    lp_p, lse_p = eng.prefill_logprobs(vid, grp, 0, with_lse=True)
+    lp_r = eng.prefill_logprobs(vid, grp, 1)
+    st = eng.stats()
+    eng.close()
+    return emb, lp_p, lse_p, lp_r, st
+
+
+def test_c1_embeddings_vs_oracle(gpu, c1_oracle):
+    emb, *_ = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
+    want = c1_oracle["emb"]
+    rel = np.linalg.norm(emb - want, axis=1) / np.linalg.norm(want, axis=1)
+    cos = (emb * want).sum(1) / (np.linalg.norm(emb, axis=1) * np.linalg.norm(want, axis=1))
+    assert rel.max() <= 1e-2, rel.max()
+    assert cos.min() >= 0.9995, cos.min()
+
+
+def test_c1_logprobs_vs_oracle(gpu, c1_oracle):
+    _, lp_p, lse_p, lp_r, st = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
+    for got, want in ((lp_p, c1_oracle["lp_p"]), (lp_r, c1_oracle["lp_r"])):
+        d = np.abs(got - want)
+        assert d.max() <= 5e-2 and d.mean() <= 5e-3, (d.max(), d.mean())
+    assert np.abs(lse_p - c1_oracle["lse_p"]).max() <= 5e-2
+    assert not np.array_equal(lp_p, lp_r)  # policy != reference weights
+    assert st["encoder_invocations"] == W1.frames and st["cache_misses"] == 1
+
+
+@pytest.mark.parametrize("sp", [2, 4])
+def test_sp_invariance_bit_exact(gpu, c1_oracle, sp):
+    """GPU SP=k outputs are bit-identical to SP=1 (acceptance C4 analogue)."""
+    base = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
+    got = run_engine(sp, c1_oracle["pix"], c1_oracle["grp"])
+    assert np.array_equal(base[0], got[0]), "embeddings differ across SP"
+    assert np.array_equal(base[1], got[1]) and np.array_equal(base[3], got[3]), "log-probs differ"
+    T_ = W1.cfg.tokens_per_frame
+    assert got[4]["gather_bytes"] == W1.frames * T_ * W1.cfg.dim * (sp - 1) * 2
+    assert got[4]["a2a_bytes"] > 0
+
+
+def test_sp8_uneven_heads_close(gpu, c1_oracle):
+    # SP=8 > n_kv: replicated kv heads, some ranks with no query heads.
+    base = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
+    got = run_engine(8, c1_oracle["pix"], c1_oracle["grp"])
+    assert np.abs(base[1] - got[1]).max() < 1e-2
+
+
+def test_step_cache_counters(gpu, c1_oracle):
+    """run_step (engine.cpp:203-225): cache on -> 1 miss + (G-1) hits and F
+    invocations; cache off -> G x F invocations (acceptance.cpp:442-444)."""
+    eng = E.Engine(W1.cfg, sp=2, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    pix, grp = c1_oracle["pix"], c1_oracle["grp"]
+    lp_p, lp_r = eng.step("vA", pix, grp, use_cache=True)
+    st = eng.stats(reset=True)
+    assert st["cache_misses"] == 1 and st["cache_hits"] == W1.G - 1
+    assert st["encoder_invocations"] == W1.frames
+    assert np.abs(lp_p - c1_oracle["lp_p"]).max() <= 5e-2
+    eng.step("vB", pix, grp, use_cache=False)
+    st = eng.stats(reset=True)
+    assert st["encoder_invocations"] == W1.G * W1.frames and st["cache_misses"] == 0
+    assert eng.cache_size() == 1
+    # device-resident input path gives the same answer
+    dpix = torch.from_numpy(pix).cuda()
+    lp_p2, _ = eng.step("vC", dpix, grp)
+    assert np.array_equal(lp_p, lp_p2)
+    eng.close()
+
+
+def test_pack_kernel_bit_exact(gpu):
+    """Pad mask, position ids and the token gather map are bit-exact vs the oracle."""
+    grp = E.make_group(W1, seed=11)
+    n_frame_tok, d, V = 100, 16, 32
+    tok, pos, pad, Lp, L = T.pack(n_frame_tok, grp.question, grp.resp, grp.lengths)
+    emb = torch.randn(n_frame_tok, d, device="cuda").bfloat16()
+    table = torch.randn(V, d, device="cuda").bfloat16()
+    q = torch.from_numpy(grp.question).cuda()
+    resp = torch.from_numpy(grp.resp).cuda()
+    lens = torch.from_numpy(grp.lengths).cuda()
+    for p0, n in ((0, L), (37, L - 50), (Lp, L - Lp)):
+        hid = torch.empty(n, d, device="cuda")
+        posd = torch.empty(n, dtype=torch.int32, device="cuda")
+        padd = torch.empty(n, dtype=torch.uint8, device="cuda")
+        tokd = torch.empty(n, dtype=torch.int32, device="cuda")
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        _lib.check(_lib.lib().mrsp_op_pack_sequence(
+            vp(emb), n_frame_tok, vp(q), len(grp.question), vp(resp), vp(lens), grp.Lmax,
+            vp(table), d, p0, n, vp(hid), vp(posd), vp(padd), vp(tokd), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(posd.cpu().numpy(), pos[p0:p0 + n])
+        assert np.array_equal(padd.cpu().numpy(), pad[p0:p0 + n])
+        assert np.array_equal(tokd.cpu().numpy(), tok[p0:p0 + n])
+        src = torch.cat([emb.float(), table.float()[torch.from_numpy(np.maximum(tok[n_frame_tok:], 0)).cuda()]])
+        assert torch.equal(hid, src[p0:p0 + n])

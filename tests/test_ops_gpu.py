@@ -1,0 +1,86 @@
+"""GPU: HBM-bound device operators and the fused LM-head log-prob vs plain
+PyTorch fp32 references (through the C-ABI)."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import transformer as T
+from paper_2507_07966_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@pytest.mark.parametrize("M,V,K", [(77, 32, 256), (300, 152064, 512), (1030, 5000, 3584)])
+def test_lmhead_logprob(gpu, M, V, K):
+    g = torch.Generator(device="cuda").manual_seed(M + V)
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(V, K, device="cuda", generator=g) / K ** 0.5 * 3).bfloat16()
+    tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32, generator=g)
+    lp = torch.empty(M, device="cuda")
+    lse = torch.empty(M, device="cuda")
+    wsb = _lib.lib().mrsp_lmhead_workspace_bytes(M, V)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().mrsp_op_lmhead_logprob(vp(X), K, vp(W), M, V, K, vp(tgt), vp(lp), vp(lse),
+                                                 vp(ws), wsb, None))
+    logits = X.double() @ W.double().T
+    want = torch.log_softmax(logits, -1).gather(1, tgt.long()[:, None])[:, 0]
+    torch.cuda.synchronize()
+    assert (lp.double() - want).abs().max().item() < 2e-3
+    assert (lse.double() - torch.logsumexp(logits, -1)).abs().max().item() < 2e-3
+
+
+def test_rmsnorm_and_gather(gpu):
+    n, d = 333, 3584
+    x = torch.randn(n, d, device="cuda") * 3
+    w = 1 + 0.1 * torch.randn(d, device="cuda")
+    out = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_rmsnorm(vp(x), d, vp(w), vp(out), d, n, d, 1e-6, None, None))
+    want = w * (x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6))
+    assert ((out.float() - want).abs() / (want.abs() + 1e-2)).max().item() < 1e-2
+    rows = torch.tensor([5, 0, 332, 17], device="cuda", dtype=torch.int32)
+    out2 = torch.empty(4, d, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_rmsnorm(vp(x), d, vp(w), vp(out2), d, 4, d, 1e-6, vp(rows), None))
+    assert torch.equal(out2, out[rows.long()])
+
+
+def test_layernorm(gpu):
+    n, d = 257, 1152
+    x = torch.randn(n, d, device="cuda") * 2 + 0.5
+    w = 1 + 0.1 * torch.randn(d, device="cuda")
+    b = 0.1 * torch.randn(d, device="cuda")
+    out = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_layernorm(vp(x), d, vp(w), vp(b), vp(out), d, n, d, 1e-6, None))
+    want = torch.nn.functional.layer_norm(x, (d,), w, b, 1e-6)
+    assert (out.float() - want).abs().max().item() < 3e-2
+
+
+def test_rope_matches_oracle(gpu):
+    n, H = 300, 6
+    x = torch.randn(n, H * 128, device="cuda").bfloat16()
+    pos = torch.randint(0, 262144, (n,), device="cuda", dtype=torch.int32)
+    y = x.clone()
+    _lib.check(_lib.lib().mrsp_op_rope(vp(y), H * 128, 0, H, vp(pos), n, 1e6, None))
+    c = T.Cfg(64, 8, 8, 1, 8, 8, 1, 8, 1, 1, 128, 128, 1, 8)
+    cos, sin = T.rope_tables(c, pos.cpu().numpy())
+    want = T.apply_rope(x.float().cpu().numpy().reshape(n, H, 128), cos, sin).reshape(n, H * 128)
+    got = y.float().cpu().numpy()
+    assert np.abs(got - want).max() <= 2 ** -6 * np.abs(want).max()
+    assert (got == want).mean() > 0.97
+
+
+def test_patchify_matches_oracle(gpu):
+    F, S, P = 3, 224, 14
+    pix = torch.rand(F, 3 * S * S, device="cuda") * 2 - 1
+    kpad = 592
+    out = torch.empty(F * (S // P) ** 2, kpad, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_patchify(vp(pix), vp(out), F, S, S, P, kpad, None))
+    want = T.patchify(pix.cpu().numpy(), S, P)
+    got = out.float().cpu().numpy()
+    assert np.array_equal(got[:, :588], want) and (got[:, 588:] == 0).all()
