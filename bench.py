@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""MR-SP encode+prefill benchmark (BASELINE.json metric) on 1..8 B200.
+
+One step = Stage 1 (a fresh video: sharded SigLIP-shaped encode + all-gather
+into the device cache; the G rollout fetches then hit the cache) + Stage 2
+(policy and reference Ulysses prefill of the packed GRPO group + fused LM-head
+log-probs). Workload c4 of BASELINE.json (512 frames x 256 tokens, 28-layer
+Qwen2.5-7B-shaped LLM, G = 8) split over N GPUs as SP = N (strong scaling).
+
+  python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload c4]
+
+Prints ONE JSON line on rank 0. Multi-GPU: launched by torch.distributed.run,
+one process per GPU; the engine's collectives run over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MR-SP step tokens/s (encode+prefill), 512 frames, 1/2/4/8 B200; % roofline"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi equivalent via NVML, sampled during the timed region."""
+
+    def __init__(self, device_index: int, period: float = 0.2):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.dev, self._stop = period, device_index, threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for n, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        load = [s for s in self.samples if s > 300] or self.samples
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------- CPU baseline
+def cpu_port_timing(w, group, budget_s: float = 20.0):
+    """Time the CPU port (oracle/transformer.py, fp64 numpy over bf16-valued
+    tensors, all host threads via BLAS) on a bounded sample of the same
+    workload and extrapolate to one step with the algorithmic FLOP table."""
+    import numpy as np
+    from oracle import transformer as T
+    c = T.Cfg.from_any(w.cfg)
+    fl = T.step_flops(c, w.frames, w.n_question, group.lengths)
+    rng = np.random.default_rng(0)
+    timings = {}
+    # (1) one SigLIP-shaped frame through the full tower + projector
+    # weight VALUES do not change the port's arithmetic cost: fast random tensors
+    # of the exact SigLIP-shaped shapes stand in for the counter-based init
+    Wv = {}
+    for k_, v_ in vision_shapes(c).items():
+        Wv[k_] = (rng.random(v_, dtype=np.float32) - np.float32(0.5)) * np.float32(0.05)
+        if k_.endswith("_w") and len(v_) == 1:
+            Wv[k_] += np.float32(1.0)
+    pix = rng.uniform(-1, 1, size=(1, 3 * c.image_size ** 2)).astype(np.float32)
+    t = time.perf_counter()
+    T.vision_forward(c, Wv, pix)
+    timings["vision_frame_s"] = time.perf_counter() - t
+    del Wv
+    # (2) one 7B-shaped decoder layer (linear part) over a 512-token slice
+    n = 512
+    d, hd, nq, nkv = c.dim, c.head_dim, c.n_q_heads, c.n_kv_heads
+    rnd = lambda *shape: rng.random(shape, dtype=np.float32) - np.float32(0.5)
+    x = rnd(n, d)
+    wq, wo = rnd((nq + 2 * nkv) * hd, d), rnd(d, nq * hd)
+    wg, wu, wd = rnd(c.mlp, d), rnd(c.mlp, d), rnd(d, c.mlp)
+    t = time.perf_counter()
+    xn = T.rmsnorm(x, np.ones(d, np.float32), 1e-6)
+    T.linear(xn, wq)
+    h = x + T.linear(T.bf16_round(rnd(n, nq * hd)), wo)
+    xn = T.rmsnorm(h, np.ones(d, np.float32), 1e-6)
+    act = T.bf16_round((T.silu(T.linear(xn, wg)) * T.linear(xn, wu)).astype(np.float32))
+    T.linear(act, wd)
+    timings["layer_linear_512tok_s"] = time.perf_counter() - t
+    lin_flops = 2 * (d * (nq + 2 * nkv) * hd + nq * hd * d + 3 * d * c.mlp) * n
+    del wq, wo, wg, wu, wd
+    # (3) attention: 28 heads, 256 queries x 4096 keys
+    q = rng.standard_normal((nq, 256, hd))
+    k = rng.standard_normal((nkv, 4096, hd))
+    mask = np.ones((256, 4096), dtype=bool)
+    t = time.perf_counter()
+    T.attention(q, k, k, mask, 1 / np.sqrt(hd))
+    timings["attention_28h_256x4096_s"] = time.perf_counter() - t
+    attn_flops = 4 * nq * 256 * 4096 * hd
+    # (4) LM head block: 32 tokens x V
+    xs = T.bf16_round(rnd(32, d))
+    wl = rnd(c.vocab, d)
+    t = time.perf_counter()
+    T.linear(xs, wl)
+    timings["lm_head_32tok_s"] = time.perf_counter() - t
+    lm_flops = 2 * 32 * d * c.vocab
+    del wl
+    vis_per_flop = timings["vision_frame_s"] / (fl["encode"] / w.frames)
+    lin_per_flop = timings["layer_linear_512tok_s"] / lin_flops
+    attn_per_flop = timings["attention_28h_256x4096_s"] / attn_flops
+    lm_per_flop = timings["lm_head_32tok_s"] / lm_flops
+    step_s = (fl["encode"] * vis_per_flop + 2 * fl["linear"] * lin_per_flop
+              + 2 * (fl["attn_prefix"] + fl["attn_resp"]) * attn_per_flop
+              + 2 * fl["lm_head"] * lm_per_flop)
+    cores = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max((i.get("num_threads") or 0) for i in threadpool_info()) or cores
+    except Exception:
+        pass
+    return {
+        "value": fl["tokens"] / step_s, "unit": "tokens/s", "cores": cores, "kind": "port",
+        "sample": ("oracle/transformer.py (fp64 numpy over bf16 tensors): 1 SigLIP-shaped frame "
+                   "(27 layers + projector), 1 Qwen2.5-7B-shaped decoder layer (linear) on 512 "
+                   "tokens, attention 28 heads x 256 q x 4096 k, LM head 32 tokens; extrapolated "
+                   "to the full step by the SURVEY §8d FLOP table"),
+        "extrapolated_step_s": step_s, "timings_s": timings,
+    }
+
+
+def vision_shapes(c):
+    vd, kreal = c.v_dim, 3 * c.patch * c.patch
+    sh = {"patch_w": (vd, kreal), "patch_b": (vd,), "pos": (c.T, vd), "post_w": (vd,),
+          "post_b": (vd,), "p1_w": (c.dim, vd), "p1_b": (c.dim,), "p2_w": (c.dim, c.dim),
+          "p2_b": (c.dim,)}
+    for l in range(c.v_layers):
+        p = f"vision.{l}."
+        sh.update({p + "ln1_w": (vd,), p + "ln1_b": (vd,), p + "wqkv": (3 * vd, vd),
+                   p + "bqkv": (3 * vd,), p + "wo": (vd, vd), p + "bo": (vd,), p + "ln2_w": (vd,),
+                   p + "ln2_b": (vd,), p + "w1": (c.v_mlp, vd), p + "b1": (c.v_mlp,),
+                   p + "w2": (vd, c.v_mlp), p + "b2": (vd,)})
+    return sh
+
+
+def reference_toy_engine():
+    """The literal reference CPU engine (lvrl mrsp::bench, toy model) if built."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "512", "8", "1", "5", "2"], capture_output=True, text=True,
+                             timeout=120, env={**os.environ, "OMP_NUM_THREADS": "8"})
+        cell = json.loads(out.stdout.strip().splitlines()[-1])
+        cell["note"] = ("reference lvrl mrsp::bench, toy model (1 token/frame, d 128), "
+                        "512 frames sp 8 cache on, OpenMP threads = sp")
+        return cell
+    except Exception as e:  # informational only
+        return {"error": str(e)}
+
+
+# -------------------------------------------------------------- the bench
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    from paper_2507_07966_b200 import engine as E
+    from oracle import transformer as T  # FLOP accounting (the algorithmic numerator)
+
+    w = E.workloads()[args.workload]
+    group = E.make_group(w, seed=3)
+    fl = T.step_flops(T.Cfg.from_any(w.cfg), w.frames, w.n_question, group.lengths)
+    peaks, peak_src = load_peaks()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        t0 = time.perf_counter()
+        base = cpu_port_timing(w, group)
+        times = [base["extrapolated_step_s"]]
+        for _ in range(max(args.steps - 1, 0)):
+            times.append(cpu_port_timing(w, group)["extrapolated_step_s"])
+        step_s = statistics.median(times)
+        val = fl["tokens"] / step_s
+        base["value"] = val
+        line = {
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (over bf16-valued tensors)",
+            "data": "synthetic", "config": workload_config(w, group, fl, args.gpus),
+            "cpu_baseline": base,
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "reference_toy_engine": reference_toy_engine(),
+            "wall_s": time.perf_counter() - t0,
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [E.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    from paper_2507_07966_b200 import _lib
+    eng = E.Engine(w.cfg, sp=world, rank=rank, n_procs=world, vision_seed=2, policy_seed=3,
+                   ref_seed=4, with_ref=True, nccl_id=nccl_id)
+    eng.cache_capacity(2)
+    S = w.cfg.image_size
+    pix_host = torch.from_numpy(E.gen_video(1, w.frames, 3 * S * S)).pin_memory()
+    pix = pix_host.cuda()
+    n_scored = group.scored
+    lp_dev = (torch.empty(n_scored, device="cuda"), torch.empty(n_scored, device="cuda"))
+    stream = torch.cuda.ExternalStream(eng.stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step_no = [0]
+
+    def one_step(dev_inputs=True):
+        vid = E.video_id(1000 + step_no[0], w.frames)  # fresh video -> Stage 1 runs every step
+        step_no[0] += 1
+        if dev_inputs:
+            eng.step(vid, pix, group, out=lp_dev)
+            return None
+        return eng.step(vid, pix_host.numpy(), group)  # host pixels in, host log-probs out
+
+    for _ in range(args.warmup):
+        one_step()
+    eng.stats(reset=True)
+
+    # ---- device-resident timed region
+    barrier()
+    launches0 = int(_lib.lib().mrsp_launch_count())
+    eng.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_step(True)
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    prof = eng.profile(False)
+    launches = int(_lib.lib().mrsp_launch_count()) - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    stats = eng.stats(reset=True)
+    value = fl["tokens"] / (ms / 1e3)
+
+    # ---- end to end: host pixels (pinned) in, host log-probs out, copies timed
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_wall = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            lp_p, lp_r = one_step(False)
+        e1.record(stream)
+        e1.synchronize()
+        wall = (time.perf_counter() - t_wall) / args.steps * 1e3
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall))
+        frame_bytes = 3 * S * S * 4
+        tok_bytes = 4 * (len(group.question) + group.resp.size + group.lengths.size)
+        e2e = {"value": fl["tokens"] / (e2e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": w.frames * frame_bytes + 2 * world * tok_bytes,
+               "d2h_bytes_per_step": 2 * world * n_scored * 4,
+               "ms_per_step": e2e_ms,
+               "note": "mrsp_engine_step with pinned host pixels and host log-prob buffers"}
+
+    # ---- roofline of the dominant kernel (LLM attention), live CUDA events
+    attn_ms, attn_n = prof["llm_attention"]
+    attn_flops_total = args.steps * 2 * (fl["attn_prefix"] + fl["attn_resp"]) / world
+    per_launch_flops = attn_flops_total / max(attn_n, 1)
+    achieved = per_launch_flops / (attn_ms / max(attn_n, 1) / 1e3) / 1e12 if attn_n else 0.0
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attention_dram_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "attn_fwd_tcgen05 (LLM layer attention)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": f"{peak_src} bf16_tflops_sustained",
+                "launches": attn_n, "avg_launch_ms": attn_ms / max(attn_n, 1),
+                "algorithmic_flops_per_launch": per_launch_flops,
+                "share_of_step": attn_ms / (ms * args.steps)}
+    step_tflops = fl["step"] / (ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(w, group, fl, world),
+        "roofline": roofline,
+        "step_roofline": {"flops_per_step": fl["step"], "achieved_tflops": step_tflops,
+                          "frac_of_sustained": step_tflops / world / peak},
+        "kernel_ms": {k: round(v[0] / args.steps, 2) for k, v in prof.items()},
+        "kernel_launches": {k: v[1] for k, v in prof.items()},
+        "e2e": e2e, "gpu_launches": launches, "counters_per_step":
+            {k: v // args.steps for k, v in stats.items()},
+    }
+    if rank == 0:
+        clocks = clk.summary()
+        line["clocks"] = clocks
+        if world == 1 and not args.no_cpu:
+            try:
+                line["cpu_baseline"] = cpu_port_timing(w, group)
+            except Exception as e:
+                line["cpu_baseline"] = {"error": str(e)}
+        line["reference_toy_engine"] = reference_toy_engine() if world == 1 else None
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def workload_config(w, group, fl, n):
+    return {"workload": f"{w.name}: {w.desc}", "frames": w.frames,
+            "tokens_per_frame": w.cfg.tokens_per_frame, "prefix_tokens": fl["Lp"],
+            "G": w.G, "scored_tokens": int(group.scored), "Lmax": group.Lmax,
+            "total_tokens": fl["tokens"], "sp_degree": n, "parallelism": f"sp{n} (Ulysses)",
+            "model": "SigLIP-shaped 27L tower + 2-layer projector; Qwen2.5-7B-shaped 28L LLM "
+                     "(policy + reference, V 152064)",
+            "l2": "inputs larger than L2 (~31 GB of weights streamed per step)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -46,6 +46,8 @@ typedef enum {
 const char* mrsp_last_error(void);
 /* Library version string and the sm arch it was built for ("sm_100a"). */
 const char* mrsp_version(void);
+/* Kernels launched by this library since load (all entry points). */
+uint64_t mrsp_launch_count(void);
 /* Number of visible CUDA devices (0 when none); never fails. */
 int mrsp_device_count(void);
 

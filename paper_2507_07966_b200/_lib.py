@@ -59,6 +59,7 @@ def _sig(name, argtypes, restype=ctypes.c_int):
 _sig("mrsp_last_error", [], ctypes.c_char_p)
 _sig("mrsp_version", [], ctypes.c_char_p)
 _sig("mrsp_device_count", [], ctypes.c_int)
+_sig("mrsp_launch_count", [], ctypes.c_uint64)
 _sig("mrsp_plan_shards", [ctypes.c_uint64, ctypes.c_int, c_u64p])
 _sig("mrsp_toy_encode", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, c_f64p, ctypes.c_uint64,
                          c_u64p, c_f64p, c_u64p])

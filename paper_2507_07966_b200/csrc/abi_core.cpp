@@ -1,4 +1,5 @@
 // abi_core.cpp — error plumbing, device probe and shard planning.
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -7,6 +8,9 @@
 namespace mrsp {
 
 static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -27,6 +31,8 @@ extern "C" {
 const char* mrsp_last_error(void) { return mrsp::g_last_error.c_str(); }
 
 const char* mrsp_version(void) { return "mrsp_b200 0.1 (sm_100a)"; }
+
+uint64_t mrsp_launch_count(void) { return mrsp::g_launches.load(); }
 
 int mrsp_device_count(void) {
   int n = 0;

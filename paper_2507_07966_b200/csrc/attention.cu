@@ -291,23 +291,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       // P buffer and O are free once the previous P.V has completed.
       if (it > 0) mbar_wait(pv_done, (it - 1) & 1);
       tc_fence_after();
-      if (mt > m_run + RESCALE_THRESHOLD) {
-        if (it > 0 && m_run != -INFINITY) {
-          const float alpha = exp2f(m_run - mt);
-          l_run *= alpha;
+      // Lazy rescale: a row moves its reference max only when the tile max
+      // exceeds it by 2^8. tcgen05.ld/st are warp-collective (.sync.aligned),
+      // so the TMEM round trip runs for the whole warp when any lane needs it
+      // (alpha = 1 for the others).
+      const bool need = mt > m_run + RESCALE_THRESHOLD;
+      if (__any_sync(0xffffffffu, need) && it > 0) {
+        const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
+        if (need) l_run *= alpha;
 #pragma unroll 1
-          for (int c = 0; c < HD; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + c, o);
-            tmem_ld_wait();
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tO + lane_off + c, o);
+          tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-            tmem_st32(tO + lane_off + c, o);
-          }
-          tmem_st_wait();
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st32(tO + lane_off + c, o);
         }
-        m_run = mt;
+        tmem_st_wait();
       }
+      if (need) m_run = mt;
       const float m_use = m_run == -INFINITY ? 0.f : m_run;
       float lsum = 0.f;
 #pragma unroll
@@ -391,6 +394,7 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.mask = MaskDev{p.mode, p.L, p.Lp, p.Lmax > 0 ? p.Lmax : 1, p.blk > 0 ? p.blk : 1};
   const int grid = a.n_q_tiles * a.n_heads;
   attn_fwd_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 

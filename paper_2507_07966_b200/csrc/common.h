@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -51,6 +53,9 @@ mrsp_status guard(F&& f) {
 
 // Ensures a CUDA device exists; the product has no CPU fallback.
 void require_device();
+
+// Count of kernels this library has launched (evidence for bench.py's gpu_launches).
+void count_launch(uint64_t n = 1);
 
 }  // namespace mrsp
 

@@ -367,9 +367,11 @@ void Engine::prof_collect() {
 void Engine::set_profiling(bool on) {
   prof_collect();
   prof_ = on;
-  for (int i = 0; i < 8; ++i) {
-    prof_ms_[i] = 0;
-    prof_n_[i] = 0;
+  if (on) {
+    for (int i = 0; i < 8; ++i) {
+      prof_ms_[i] = 0;
+      prof_n_[i] = 0;
+    }
   }
 }
 void Engine::profile_read(int cls, double* ms, long* launches) {
@@ -850,7 +852,9 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
       lmhead_logprob(xs, d, W.lm_head, ns, c.vocab, d, di + ns, lp, lp + ns, ws, wsb, s);
     }
     scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp, di + 2 * ns, ns, dlp_full);
+    count_launch();
     scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp + ns, di + 2 * ns, ns, dlse_full);
+    count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
   if (nccl_) {

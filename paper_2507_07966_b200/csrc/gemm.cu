@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_ld32(t_row + c, r);
           tmem_ld_wait();
           const int col = nt * BN + c;
-          if (!row_ok || col >= args.N) continue;
+          if (row_ok && col < args.N) {  // stores only; the TMEM load above is warp-wide
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
               for (int j = 0; j < 32 && col + j < args.N; ++j) Cb[j] = ob[j];
             }
+          }
           }
         }
       }
@@ -335,6 +336,7 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = std::min(tiles, num_sms());
   gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, e);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 

@@ -251,6 +251,7 @@ void rmsnorm(const float* x, int ldx, const float* w, __nv_bfloat16* out, int ld
   MRSP_REQUIRE(d % 4 == 0 && ldx % 4 == 0, MRSP_INVALID_ARGUMENT, "rmsnorm: d % 4");
   if (n <= 0) return;
   rmsnorm_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, ldx, w, out, ldo, n, d, eps, rows);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -259,6 +260,7 @@ void layernorm(const float* x, int ldx, const float* w, const float* b, __nv_bfl
   MRSP_REQUIRE(d % 4 == 0 && ldx % 4 == 0, MRSP_INVALID_ARGUMENT, "layernorm: d % 4");
   if (n <= 0) return;
   layernorm_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, ldx, w, b, out, ldo, n, d, eps);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -272,6 +274,7 @@ void rope(__nv_bfloat16* qkv, int ld, int col0, int n_heads, const int* pos, int
   if (n <= 0 || n_heads <= 0) return;
   const int work = n * 64;
   rope_kernel<<<(work + 255) / 256, 256, 0, s>>>(qkv, ld, col0, n_heads, pos, n);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -280,6 +283,7 @@ void patchify(const float* pix, __nv_bfloat16* out, int F, int H, int W, int P, 
   const size_t total = static_cast<size_t>(F) * (H / P) * (W / P) * kpad;
   if (!total) return;
   patchify_kernel<<<grid_for(total, 256), 256, 0, s>>>(pix, out, F, H, W, P, kpad);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -288,6 +292,7 @@ void broadcast_rows(const float* src, float* dst, int n, int period, int d, cuda
   const size_t total = static_cast<size_t>(n) * d / 4;
   if (!total) return;
   broadcast_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, dst, n, period, d);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -300,6 +305,7 @@ void pack_sequence(const __nv_bfloat16* frame_emb, int n_frame_tok, const int* q
   pack_kernel<<<std::min(n, 148 * 8), 256, 0, s>>>(frame_emb, n_frame_tok, question, n_q, resp,
                                                    lengths, Lmax, embed, d, p0, n, hidden, pos_ids,
                                                    pad_mask, tok_out);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
@@ -307,24 +313,28 @@ void logprob_combine(const float2* part, int n_tiles, const float* tgt_logit, in
                      float* lse, cudaStream_t s) {
   if (n <= 0) return;
   logprob_combine_kernel<<<(n + 7) / 8, 256, 0, s>>>(part, n_tiles, tgt_logit, n, lp, lse);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
 void init_uniform_bf16(__nv_bfloat16* w, size_t n, uint64_t key, float scale, cudaStream_t s) {
   if (!n) return;
   init_uniform_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, n, key, scale);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
 void init_uniform_f32(float* w, size_t n, uint64_t key, float scale, float offset, cudaStream_t s) {
   if (!n) return;
   init_uniform_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, n, key, scale, offset);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 
 void convert_bf16_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s) {
   if (!n) return;
   convert_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
+  count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
 

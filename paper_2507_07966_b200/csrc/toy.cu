@@ -153,6 +153,7 @@ extern "C" mrsp_status mrsp_toy_encode(int sp_degree, const double* enc_w, int d
       MRSP_CUDA(cudaStreamWaitEvent(streams[w], ready, 0));
       toy_encode_kernel<<<static_cast<unsigned>(e - b), threads, sizeof(double) * p, streams[w]>>>(
           dw.p, dx.p, dout.p, d, p, b);
+      count_launch();
       MRSP_CUDA(cudaGetLastError());
       // each rank's slice lands in its own range of the gathered buffer
       MRSP_CUDA(cudaMemcpyAsync(out + b * d, dout.p + b * d, sizeof(double) * (e - b) * d,
@@ -229,6 +230,7 @@ extern "C" mrsp_status mrsp_toy_prefill(int sp_degree, const double* theta, int 
       MRSP_CUDA(cudaStreamWaitEvent(streams[w], ready, 0));
       toy_prefill_kernel<<<static_cast<unsigned>(plist[w].size()), threads, smem, streams[w]>>>(
           dtheta.p, dctx.p, dpos.p + pos_off[w], dout.p, V, d, h);
+      count_launch();
       MRSP_CUDA(cudaGetLastError());
     }
     for (int w = 0; w < sp_degree; ++w) MRSP_CUDA(cudaStreamSynchronize(streams[w]));
