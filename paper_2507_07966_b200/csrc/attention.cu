@@ -1,15 +1,23 @@
 // attention.cu — tcgen05 flash-attention forward for sm_100a (head dim 128).
 //
-// One CTA = one 128-query tile x one query head. K/V tiles of 128 keys stream
-// through a 2-stage TMA ring; S = Q.K^T and O += P.V run on the tensor cores
-// with fp32 accumulators in TMEM (S double-buffered, O resident for the
-// whole KV sweep); the softmax warpgroup reads S with tcgen05.ld, keeps the
-// running max / sum in registers, writes P (bf16) into swizzled smem for the
-// P.V MMA and rescales O in TMEM only when the running max grows by > 2^8
-// (lazy rescale; exact after the final 1/l normalisation).
+// One CTA = TWO 128-query tiles of one query head, sharing every K/V tile.
+// The tensor core (one elected thread of warp 1) alternates between the tiles:
+//     ... P.V(t0, j-1) | S(t0, j) = Q0.K_j^T | P.V(t1, j-1) | S(t1, j) ...
+// so while softmax warpgroup 0 turns S(t0) into P(t0) the tensor core works on
+// tile 1 and vice versa (ping-pong). S and O accumulate in TMEM
+// (S0 | S1 | O0 | O1 = 512 columns); K and V stream through a 3-slot TMA ring
+// (K_j, V_j alternate); P goes through swizzled smem to the P.V MMA.
 //
-// Roles (256 threads): warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator,
-// warps 4-7 softmax / correction / epilogue (thread = query row).
+// Softmax (thread = query row): tcgen05.ld of the 128 scores, row max on the
+// raw scores, p = exp2(s*scale - m) with one FFMA per element; 1 in 4
+// exponentials runs as a degree-3 polynomial on the FMA pipe instead of
+// MUFU.EX2 (balances the two pipes); O is rescaled in TMEM only when the
+// running max grows by > 2^8 (lazy rescale, warp-uniform because tcgen05.ld/st
+// are warp-collective). Registers rebalanced with setmaxnreg (TMA/MMA
+// warpgroup 56, softmax warpgroups 200).
+//
+// Roles (384 threads): warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warps 4-7 softmax of tile 0, warps 8-11 softmax of tile 1.
 //
 // Masks (MR-SP packed sequence):
 //   ATTN_CAUSAL_PREFIX: sequence = [prefix (Lp) | G rows of Lmax]; query q sees
@@ -17,8 +25,8 @@
 //     attends to the shared prompt prefix and causally to itself only.
 //   ATTN_BLOCK_DIAG: bidirectional inside blocks of `blk` tokens (one video
 //     frame of the vision tower), nothing across blocks.
-// KV tiles with no visible (q,k) pair are skipped entirely; tiles that are
-// fully visible skip the per-element mask.
+// Per (query tile, KV tile): skipped (no visible pair: no MMA, no softmax),
+// full (no element mask) or partial (element mask).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -37,19 +45,16 @@ namespace {
 using namespace sm100;
 
 constexpr int TQ = 128, TK = 128, HD = 128;
-constexpr int CHUNK = 128 * 64 * 2;       // one 128-row x 64-col bf16 SW128 block (16 KB)
-constexpr int Q_BYTES = 2 * CHUNK;        // 32 KB
-constexpr int KV_BYTES = 2 * CHUNK;       // 32 KB per K or V stage
-constexpr int KV_STAGES = 2;
-constexpr int P_BYTES = 2 * CHUNK;        // 32 KB
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + Q_BYTES;
-constexpr int OFF_V = OFF_K + KV_STAGES * KV_BYTES;
-constexpr int OFF_P = OFF_V + KV_STAGES * KV_BYTES;
-constexpr int OFF_BAR = OFF_P + P_BYTES;
+constexpr int CHUNK = 128 * 64 * 2;  // one 128-row x 64-col bf16 SW128 block (16 KB)
+constexpr int TILE = 2 * CHUNK;      // a 128 x 128 bf16 operand (32 KB)
+constexpr int RING = 3;              // K/V ring slots
+constexpr int OFF_Q = 0;                       // Q0, Q1
+constexpr int OFF_RING = OFF_Q + 2 * TILE;     // 3 slots
+constexpr int OFF_P = OFF_RING + RING * TILE;  // P0, P1
+constexpr int OFF_BAR = OFF_P + 2 * TILE;
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
-constexpr int THREADS = 256;
-constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O [256,384)
+constexpr int THREADS = 384;
+constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 
 struct MaskDev {
@@ -68,7 +73,7 @@ __device__ __forceinline__ bool visible(int q, int k, const MaskDev& m) {
 // 0 = skip, 1 = fully visible, 2 = needs the element mask.
 __device__ __forceinline__ int tile_class(int q0, int kt, const MaskDev& m) {
   const int k0 = kt * TK, klast = k0 + TK - 1, qlast = q0 + TQ - 1;
-  if (k0 >= m.L) return 0;
+  if (k0 >= m.L || q0 >= m.L) return 0;
   if (m.mode == ATTN_BLOCK_DIAG) {
     const int kb0 = k0 / m.blk, kb1 = min(klast, m.L - 1) / m.blk;
     const int qb0 = q0 / m.blk, qb1 = qlast / m.blk;
@@ -86,8 +91,9 @@ __device__ __forceinline__ int tile_class(int q0, int kt, const MaskDev& m) {
   return (sk0 == sk1 && qs0 == qs1 && sk0 == qs0 && q0 >= m.Lp && klast <= q0) ? 1 : 2;
 }
 
+// KV tile range covering both query tiles [q0, q0 + 256).
 __device__ __forceinline__ void kt_range(int q0, const MaskDev& m, int n_kt, int& lo, int& hi) {
-  const int qlast = q0 + TQ - 1;
+  const int qlast = q0 + 2 * TQ - 1;
   if (m.mode == ATTN_BLOCK_DIAG) {
     lo = (q0 / m.blk) * m.blk / TK;
     hi = min(n_kt, ((qlast / m.blk + 1) * m.blk + TK - 1) / TK);
@@ -97,23 +103,53 @@ __device__ __forceinline__ void kt_range(int q0, const MaskDev& m, int n_kt, int
   }
 }
 
-// Advances kt to the next non-skipped tile in [kt, hi); returns its class or 0.
+// Next KV tile in [kt, hi) visible to either query tile; returns the two
+// classes packed as c0 | c1 << 2 (0 when exhausted).
 __device__ __forceinline__ int next_tile(int q0, int& kt, int hi, const MaskDev& m) {
   for (; kt < hi; ++kt) {
-    const int c = tile_class(q0, kt, m);
-    if (c) return c;
+    const int c0 = tile_class(q0, kt, m), c1 = tile_class(q0 + TQ, kt, m);
+    if (c0 | c1) return c0 | (c1 << 2);
   }
   return 0;
 }
 
 struct AttnArgs {
-  int n_q_tiles, n_heads, q_per_kv;
+  int n_pairs, n_heads, q_per_kv;
   int q_col0, k_col0, v_col0, o_col0;
   __nv_bfloat16* O;
   int ldo;
   float scale_log2;
   MaskDev mask;
 };
+
+// 2^x on the FMA/ALU pipes (x <= ~8): round-to-nearest split x = j + f,
+// f in [-0.5, 0.5], degree-3 polynomial (max rel. error 7.7e-5), exponent add.
+__device__ __forceinline__ float exp2_poly(float x) {
+  const float xc = fmaxf(x, -126.0f);  // keeps the exponent field positive
+  const float r = xc + 12582912.0f;    // 1.5 * 2^23: low mantissa bits = round(x)
+  const int j = __float_as_int(r) - 0x4B400000;
+  const float f = xc - (r - 12582912.0f);
+  float p = fmaf(f, 0.05508868396282196f, 0.24260404706001282f);
+  p = fmaf(f, p, 0.6932762265205383f);
+  p = fmaf(f, p, 0.9999289512634277f);
+  const float y = __int_as_float(__float_as_int(p) + (j << 23));
+  return x < -126.0f ? 0.0f : y;  // masked scores (-inf) give exactly 0, as MUFU.EX2 does
+}
+
+__device__ __forceinline__ float exp2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -123,21 +159,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* s_free = bars + 11;  // [2]
-  uint64_t* p_full = bars + 13;
-  uint64_t* pv_done = bars + 14;
+  uint64_t* r_full = bars + 1;    // [3]
+  uint64_t* r_empty = bars + 4;   // [3]
+  uint64_t* s_full = bars + 7;    // [2] per query tile
+  uint64_t* s_free = bars + 9;    // [2]
+  uint64_t* p_full = bars + 11;   // [2]
+  uint64_t* pv_done = bars + 13;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id();
-  const int qt = a.n_q_tiles - 1 - static_cast<int>(blockIdx.x) / a.n_heads;  // heavy tiles first
+  const int pair = a.n_pairs - 1 - static_cast<int>(blockIdx.x) / a.n_heads;  // heavy first
   const int h = static_cast<int>(blockIdx.x) % a.n_heads;
   const int kvh = h / a.q_per_kv;
-  const int q0 = qt * TQ;
+  const int q0 = pair * 2 * TQ;
   const int n_kt = (a.mask.L + TK - 1) / TK;
   int kt_lo, kt_hi;
   kt_range(q0, a.mask, n_kt, kt_lo, kt_hi);
@@ -147,16 +181,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 128);
+    for (int s = 0; s < RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&s_free[t], 128);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&pv_done[t], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -164,104 +198,130 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 256;
 
-  if (warp == 0) {
-    if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, Q_BYTES);
-      tma_load_2d(smem + OFF_Q, &tmQ, q_full, a.q_col0 + h * HD, q0);
-      tma_load_2d(smem + OFF_Q + CHUNK, &tmQ, q_full, a.q_col0 + h * HD + 64, q0);
-      int st = 0;
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        // Q0, Q1 (rows past L are zero-filled by TMA)
+        mbar_arrive_expect_tx(q_full, 2 * TILE);
+        for (int t = 0; t < 2; ++t)
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(smem + OFF_Q + t * TILE + c * CHUNK, &tmQ, q_full,
+                        a.q_col0 + h * HD + c * 64, q0 + t * TQ);
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int kt = kt_lo; next_tile(q0, kt, kt_hi, a.mask); ++kt) {
+          const int k0 = kt * TK;
+          for (int kv = 0; kv < 2; ++kv) {  // K_j then V_j
+            mbar_wait(&r_empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&r_full[slot], TILE);
+            uint8_t* dst = smem + OFF_RING + slot * TILE;
+            const CUtensorMap* tm = kv ? &tmV : &tmK;
+            const int col = (kv ? a.v_col0 : a.k_col0) + kvh * HD;
+            tma_load_2d(dst, tm, &r_full[slot], col, k0);
+            tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, k0);
+            if (++slot == RING) { slot = 0; ph ^= 1; }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TQ, TK);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
+      const uint32_t q_addr = smem_u32(smem + OFF_Q);
+      const uint32_t p_addr = smem_u32(smem + OFF_P);
+      const uint32_t ring_addr = smem_u32(smem + OFF_RING);
+      mbar_wait(q_full, 0);
+      int slot = 0;
       uint32_t ph = 0;
-      for (int kt = kt_lo; next_tile(q0, kt, kt_hi, a.mask); ++kt) {
-        const int k0 = kt * TK;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], KV_BYTES);
-        uint8_t* kd = smem + OFF_K + st * KV_BYTES;
-        tma_load_2d(kd, &tmK, &k_full[st], a.k_col0 + kvh * HD, k0);
-        tma_load_2d(kd + CHUNK, &tmK, &k_full[st], a.k_col0 + kvh * HD + 64, k0);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&v_full[st], KV_BYTES);
-        uint8_t* vd = smem + OFF_V + st * KV_BYTES;
-        tma_load_2d(vd, &tmV, &v_full[st], a.v_col0 + kvh * HD, k0);
-        tma_load_2d(vd + CHUNK, &tmV, &v_full[st], a.v_col0 + kvh * HD + 64, k0);
-        if (++st == KV_STAGES) { st = 0; ph ^= 1; }
+      int n_s[2] = {0, 0}, n_pv[2] = {0, 0};  // MMAs issued per query tile
+      int pend_slot = -1;                     // ring slot of V_{j-1} (pending P.V)
+      int pend_cls = 0;
+      auto issue_s = [&](int t, uint32_t k_addr) {
+        mbar_wait(&s_free[t], (n_s[t] & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk / 4) * CHUNK + (kk % 4) * 32;
+            mma_bf16_ss(tmem + t * 128, sdesc_sw128(q_addr + t * TILE + off),
+                        sdesc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[t]);
+        }
+        __syncwarp();
+        ++n_s[t];
+      };
+      auto issue_pv = [&](int t, uint32_t v_addr) {
+        mbar_wait(&p_full[t], n_pv[t] & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < TK / 16; ++kk) {
+            const uint64_t ad = sdesc_sw128(p_addr + t * TILE + (kk / 4) * CHUNK + (kk % 4) * 32);
+            const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
+            mma_bf16_ss(tmem + 256 + t * 128, ad, bd, idesc_o, (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&pv_done[t]);
+        }
+        __syncwarp();
+        ++n_pv[t];
+      };
+      auto release = [&](int s) {
+        if (elect_one()) mma_commit(&r_empty[s]);
+        __syncwarp();
+      };
+      for (int kt = kt_lo;; ++kt) {
+        const int cls = next_tile(q0, kt, kt_hi, a.mask);
+        int k_slot = -1;
+        if (cls) {  // K_j
+          mbar_wait(&r_full[slot], ph);
+          k_slot = slot;
+          if (++slot == RING) { slot = 0; ph ^= 1; }
+        }
+        const uint32_t k_addr = ring_addr + (k_slot < 0 ? 0 : k_slot) * TILE;
+        const uint32_t v_addr = ring_addr + (pend_slot < 0 ? 0 : pend_slot) * TILE;
+        // P.V(t0, j-1), S(t0, j), P.V(t1, j-1), S(t1, j)
+        if (pend_slot >= 0 && (pend_cls & 3)) issue_pv(0, v_addr);
+        if (cls & 3) issue_s(0, k_addr);
+        if (pend_slot >= 0 && (pend_cls >> 2)) issue_pv(1, v_addr);
+        if (cls >> 2) issue_s(1, k_addr);
+        if (pend_slot >= 0) release(pend_slot);  // V_{j-1}: both P.V issued
+        if (k_slot >= 0) release(k_slot);        // K_j: both S issued
+        if (!cls) break;
+        mbar_wait(&r_full[slot], ph);  // V_j becomes the pending P.V operand
+        pend_slot = slot;
+        pend_cls = cls;
+        if (++slot == RING) { slot = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 1) {
-    const uint32_t idesc_s = idesc_bf16_f32(TQ, TK);
-    const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
-    const uint32_t q_addr = smem_u32(smem + OFF_Q);
-    const uint32_t p_addr = smem_u32(smem + OFF_P);
-    mbar_wait(q_full, 0);
-    int it = 0;
-    int st = 0;
-    uint32_t ph = 0;
-    int pst = 0;          // stage of the tile whose P.V is pending
-    uint32_t pph = 0;
-    bool pending = false;
-    auto issue_pv = [&](int j) {
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[pst], pph);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t v_addr = smem_u32(smem + OFF_V + pst * KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk) {
-          const uint64_t ad = sdesc_sw128(p_addr + (kk / 4) * CHUNK + (kk % 4) * 32);
-          const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
-          mma_bf16_ss(tO, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(pv_done);
-        mma_commit(&v_empty[pst]);
-      }
-      __syncwarp();
-      if (++pst == KV_STAGES) { pst = 0; pph ^= 1; }
-    };
-    for (int kt = kt_lo; next_tile(q0, kt, kt_hi, a.mask); ++kt, ++it) {
-      const int b = it & 1;
-      mbar_wait(&k_full[st], ph);
-      mbar_wait(&s_free[b], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t k_addr = smem_u32(smem + OFF_K + st * KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk / 4) * CHUNK + (kk % 4) * 32;
-          mma_bf16_ss(tmem + b * 128, sdesc_sw128(q_addr + off), sdesc_sw128(k_addr + off),
-                      idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&s_full[b]);
-        mma_commit(&k_empty[st]);
-      }
-      __syncwarp();
-      if (++st == KV_STAGES) { st = 0; ph ^= 1; }
-      if (pending) issue_pv(it - 1);
-      pending = true;
-    }
-    if (pending) issue_pv(it - 1);
-  } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int r = ew * 32 + lane_id();  // query row in tile == TMEM lane
-    const int q = q0 + r;
+  } else {
+    reg_alloc<200>();
+    const int t = (warp - 4) >> 2;      // query tile of this warpgroup
+    const int ew = (warp - 4) & 3;      // TMEM lane quarter
+    const int r = ew * 32 + lane_id();  // query row in the tile
+    const int q = q0 + t * TQ + r;
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
-    uint8_t* p_smem = smem + OFF_P;
-    float m_run = -INFINITY, l_run = 0.f;
-    int it = 0;
-    for (int kt = kt_lo;; ++kt, ++it) {
-      const int cls = next_tile(q0, kt, kt_hi, a.mask);
-      if (!cls) break;
-      const int b = it & 1;
-      mbar_wait(&s_full[b], (it >> 1) & 1);
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    uint8_t* p_smem = smem + OFF_P + t * TILE;
+    const float sl2 = a.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;  // m_run in scaled log2 units
+    int it = 0;                            // KV tiles processed by this warpgroup
+    for (int kt = kt_lo;; ++kt) {
+      const int both = next_tile(q0, kt, kt_hi, a.mask);
+      if (!both) break;
+      const int cls = (both >> (2 * t)) & 3;
+      if (!cls) continue;
+      mbar_wait(&s_full[t], it & 1);
       tc_fence_after();
       float s[TK];
       {
         uint32_t r0[32], r1[32], r2[32], r3[32];
-        const uint32_t base = tmem + lane_off + b * 128;
-        tmem_ld32(base + 0, r0);
-        tmem_ld32(base + 32, r1);
-        tmem_ld32(base + 64, r2);
-        tmem_ld32(base + 96, r3);
+        tmem_ld32(tS + 0, r0);
+        tmem_ld32(tS + 32, r1);
+        tmem_ld32(tS + 64, r2);
+        tmem_ld32(tS + 96, r3);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -272,29 +332,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&s_free[b]);
+      mbar_arrive(&s_free[t]);
       const int k0 = kt * TK;
-      float mt = -INFINITY;
+      float mx = -INFINITY;
       if (cls == 2) {
 #pragma unroll
         for (int j = 0; j < TK; ++j) {
-          s[j] = visible(q, k0 + j, a.mask) ? s[j] * a.scale_log2 : -INFINITY;
-          mt = fmaxf(mt, s[j]);
+          if (!visible(q, k0 + j, a.mask)) s[j] = -INFINITY;
+          mx = fmaxf(mx, s[j]);
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < TK; ++j) {
-          s[j] *= a.scale_log2;
-          mt = fmaxf(mt, s[j]);
-        }
+        for (int j = 0; j < TK; ++j) mx = fmaxf(mx, s[j]);
       }
-      // P buffer and O are free once the previous P.V has completed.
-      if (it > 0) mbar_wait(pv_done, (it - 1) & 1);
+      const float mt = mx * sl2;  // -inf stays -inf
+      // P buffer and O are free once this tile's previous P.V has completed.
+      if (it > 0) mbar_wait(&pv_done[t], (it - 1) & 1);
       tc_fence_after();
-      // Lazy rescale: a row moves its reference max only when the tile max
-      // exceeds it by 2^8. tcgen05.ld/st are warp-collective (.sync.aligned),
-      // so the TMEM round trip runs for the whole warp when any lane needs it
-      // (alpha = 1 for the others).
       const bool need = mt > m_run + RESCALE_THRESHOLD;
       if (__any_sync(0xffffffffu, need) && it > 0) {
         const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
@@ -302,16 +356,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
         for (int c = 0; c < HD; c += 32) {
           uint32_t o[32];
-          tmem_ld32(tO + lane_off + c, o);
+          tmem_ld32(tO + c, o);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + lane_off + c, o);
+          tmem_st32(tO + c, o);
         }
         tmem_st_wait();
       }
       if (need) m_run = mt;
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
       float lsum = 0.f;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -320,8 +374,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float p0 = exp2f(s[c * 64 + u * 8 + 2 * e] - m_use);
-            const float p1 = exp2f(s[c * 64 + u * 8 + 2 * e + 1] - m_use);
+            const int j = c * 64 + u * 8 + 2 * e;
+            const float x0 = fmaf(s[j], sl2, neg_m), x1 = fmaf(s[j + 1], sl2, neg_m);
+            const float p0 = exp2_mufu(x0);
+            const float p1 = (e & 1) ? exp2_poly(x1) : exp2_mufu(x1);
             lsum += p0 + p1;
             w[e] = pack_bf16(p0, p1);
           }
@@ -332,28 +388,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       l_run += lsum;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[t]);
+      ++it;
     }
     // epilogue: O / l -> bf16 global
-    if (it > 0) mbar_wait(pv_done, (it - 1) & 1);
-    tc_fence_after();
-    const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
     const bool row_ok = q < a.mask.L;
     __nv_bfloat16* orow = a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD;
+    if (it > 0) {
+      mbar_wait(&pv_done[t], (it - 1) & 1);
+      tc_fence_after();
+      const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t o[32];
-      tmem_ld32(tO + lane_off + c, o);
-      tmem_ld_wait();
-      if (row_ok) {
-        uint32_t pk[16];
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + c, o);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * inv_l, __uint_as_float(o[2 * j + 1]) * inv_l);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c);
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * inv_l, __uint_as_float(o[2 * j + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
       }
+    } else if (row_ok) {  // no visible key (only possible for rows past L)
+      for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
     }
   }
   tc_fence_before();
@@ -381,7 +443,8 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   CUtensorMap tk = make_tmap_bf16_2d(p.K, p.L, p.ldk, p.ldk, TK, 64);
   CUtensorMap tv = make_tmap_bf16_2d(p.V, p.L, p.ldv, p.ldv, TK, 64);
   AttnArgs a;
-  a.n_q_tiles = (p.L + TQ - 1) / TQ;
+  const int n_q_tiles = (p.L + TQ - 1) / TQ;
+  a.n_pairs = (n_q_tiles + 1) / 2;
   a.n_heads = p.n_heads;
   a.q_per_kv = p.q_per_kv;
   a.q_col0 = p.q_col0;
@@ -392,7 +455,7 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.ldo = p.ldo;
   a.scale_log2 = p.scale * 1.4426950408889634f;
   a.mask = MaskDev{p.mode, p.L, p.Lp, p.Lmax > 0 ? p.Lmax : 1, p.blk > 0 ? p.blk : 1};
-  const int grid = a.n_q_tiles * a.n_heads;
+  const int grid = a.n_pairs * a.n_heads;
   attn_fwd_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
