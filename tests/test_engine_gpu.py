@@ -125,3 +125,33 @@ def test_pack_kernel_bit_exact(gpu):
         assert np.array_equal(tokd.cpu().numpy(), tok[p0:p0 + n])
         src = torch.cat([emb.float(), table.float()[torch.from_numpy(np.maximum(tok[n_frame_tok:], 0)).cuda()]])
         assert torch.equal(hid, src[p0:p0 + n])
+
+
+def test_full_width_shapes_vs_oracle(gpu):
+    """Production shapes (SigLIP-shaped 27-layer tower + projector, one
+    Qwen2.5-7B-shaped decoder layer, V = 152064) on a short sequence: every
+    kernel at its c4 dimensions, compared with the fp64 oracle."""
+    from paper_2507_07966_b200.engine import ModelConfig
+    w4 = E.workloads()["c4"]
+    cfgd = w4.cfg.as_dict()
+    cfgd["layers"] = 1
+    cfg = ModelConfig(**cfgd)
+    c = T.Cfg.from_any(cfg)
+    frames = 1
+    pix = E.gen_video(5, frames, 3 * c.image_size ** 2)
+    wl = E.Workload("full-width", cfg, frames, 1, 2, 37, 20, 40)
+    grp = E.make_group(wl, seed=9)
+    eng = E.Engine(cfg, sp=1, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED, with_ref=False)
+    vid = E.video_id(5, frames)
+    eng.encode(vid, pix)
+    emb = eng.embeddings(vid, frames)
+    lp, lse = eng.prefill_logprobs(vid, grp, 0, with_lse=True)
+    eng.close()
+    want_emb = T.vision_forward(c, T.vision_weights(c, VSEED), pix)
+    rel = np.linalg.norm(emb - want_emb, axis=1) / np.linalg.norm(want_emb, axis=1)
+    assert rel.max() <= 2e-2 and rel.mean() <= 1e-2, (rel.max(), rel.mean())
+    want_lp, want_lse = T.llm_logprobs(c, T.llm_weights(c, PSEED, "policy."), emb, grp.question,
+                                       grp.resp, grp.lengths)
+    d = np.abs(lp - want_lp)
+    assert d.max() <= 5e-2 and d.mean() <= 5e-3, (d.max(), d.mean())
+    assert np.abs(lse - want_lse).max() <= 5e-2
