@@ -223,6 +223,13 @@ typedef struct {
 
 typedef struct mrsp_engine mrsp_engine;
 
+/* Ulysses plan of SP rank `rank` (host function; the engine's all-to-all uses
+ * exactly this): out14 = [q_lo, q_hi, kv_lo, kv_hi, q_per_kv, then for Q, K, V
+ * the (src col, dst col, width) block a sequence shard sends this rank]. For
+ * sp <= n_kv heads split contiguously; for sp > n_kv each kv head is replicated
+ * to sp/n_kv ranks that split its query-head group with plan_shards. */
+mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
+
 /* Fills the 128-byte NCCL unique id (call on rank 0, broadcast to all). */
 mrsp_status mrsp_nccl_unique_id(void* out128);
 

@@ -119,6 +119,16 @@ HeadSplit head_split(int nq, int nkv, int k, int r) {
   return h;
 }
 
+// Column blocks of a sequence-shard QKV row [Q heads | K heads | V heads] that
+// the destination rank of `hs` owns, as (src col, dst col, width) for Q, K, V;
+// the destination stores them as [its Q | its K | its V].
+std::array<std::array<int, 3>, 3> ulysses_blocks(int nq, int nkv, const HeadSplit& hs) {
+  const int Cq = hs.nq() * 128, Ckv = hs.nkv() * 128;
+  return {std::array<int, 3>{hs.q_lo * 128, 0, Cq},
+          std::array<int, 3>{nq * 128 + hs.kv_lo * 128, Cq, Ckv},
+          std::array<int, 3>{(nq + nkv) * 128 + hs.kv_lo * 128, Cq + Ckv, Ckv}};
+}
+
 // ---------------------------------------------------------------------------
 Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n_procs,
                uint64_t vision_seed, uint64_t policy_seed, uint64_t ref_seed, int with_ref,
@@ -559,14 +569,7 @@ void Engine::a2a_forward(int L) {
   const auto& c = cfg_;
   const int nq = c.n_q_heads, nkv = c.n_kv_heads, Cqkv = (nq + 2 * nkv) * 128;
   Prof pc(*this, P_COMM);
-  auto col_blocks = [&](const HeadSplit& hs) {
-    // (src col, dst col, width) for Q, K, V of the destination's heads
-    const int Cr_q = hs.nq() * 128, Cr_kv = hs.nkv() * 128;
-    return std::array<std::array<int, 3>, 3>{
-        std::array<int, 3>{hs.q_lo * 128, 0, Cr_q},
-        std::array<int, 3>{nq * 128 + hs.kv_lo * 128, Cr_q, Cr_kv},
-        std::array<int, 3>{(nq + nkv) * 128 + hs.kv_lo * 128, Cr_q + Cr_kv, Cr_kv}};
-  };
+  auto col_blocks = [&](const HeadSplit& hs) { return ulysses_blocks(nq, nkv, hs); };
   if (!nccl_) {
     for (auto& dst : ranks_) {
       const int Cr = (dst.hs.nq() + 2 * dst.hs.nkv()) * 128;
@@ -896,6 +899,21 @@ struct mrsp_engine {
 };
 
 using namespace mrsp;
+
+extern "C" mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14) {
+  return guard([&] {
+    MRSP_REQUIRE(sp >= 1 && rank >= 0 && rank < sp, MRSP_INVALID_ARGUMENT, "ulysses: bad rank");
+    const HeadSplit hs = head_split(n_q, n_kv, sp, rank);
+    out14[0] = hs.q_lo;
+    out14[1] = hs.q_hi;
+    out14[2] = hs.kv_lo;
+    out14[3] = hs.kv_hi;
+    out14[4] = hs.q_per_kv;
+    const auto b = ulysses_blocks(n_q, n_kv, hs);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) out14[5 + 3 * i + j] = b[i][j];
+  });
+}
 
 extern "C" mrsp_status mrsp_nccl_unique_id(void* out128) {
   return guard([&] { Nccl::unique_id(out128); });

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <map>
@@ -175,5 +176,6 @@ class Engine {
 };
 
 HeadSplit head_split(int nq, int nkv, int k, int r);
+std::array<std::array<int, 3>, 3> ulysses_blocks(int nq, int nkv, const HeadSplit& hs);
 
 }  // namespace mrsp

@@ -123,6 +123,15 @@ def video_id(seed: int, frames: int) -> str:
     return f"v{seed}f{frames}"  # mmseq.cpp:64
 
 
+def ulysses_plan(n_q: int, n_kv: int, sp: int, rank: int) -> dict:
+    """Head split + all-to-all column blocks of one SP rank (mrsp_ulysses_plan)."""
+    out = (ctypes.c_int32 * 14)()
+    check(_lib.lib().mrsp_ulysses_plan(n_q, n_kv, sp, rank, out))
+    v = list(out)
+    return {"q": (v[0], v[1]), "kv": (v[2], v[3]), "q_per_kv": v[4],
+            "blocks": [tuple(v[5 + 3 * i: 8 + 3 * i]) for i in range(3)]}
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     check(_lib.lib().mrsp_nccl_unique_id(buf))
