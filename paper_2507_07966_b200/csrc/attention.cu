@@ -5,13 +5,15 @@
 //     ... P.V(t0, j-1) | S(t0, j) = Q0.K_j^T | P.V(t1, j-1) | S(t1, j) ...
 // so while softmax warpgroup 0 turns S(t0) into P(t0) the tensor core works on
 // tile 1 and vice versa (ping-pong). S and O accumulate in TMEM
-// (S0 | S1 | O0 | O1 = 512 columns); K and V stream through a 3-slot TMA ring
-// (K_j, V_j alternate); P goes through swizzled smem to the P.V MMA.
+// (S0 | S1 | O0 | O1 = 512 columns); K and V stream through a 5-slot TMA ring
+// (K_j, V_j alternate). P never touches shared memory: the softmax writes it
+// as packed bf16 over the first 64 columns of its S buffer (tcgen05.st) and
+// the P.V MMA takes its A operand straight from TMEM.
 //
 // Softmax (thread = query row): tcgen05.ld of the 128 scores, row max on the
-// raw scores, p = exp2(s*scale - m) with one FFMA per element; 1 in 4
-// exponentials runs as a degree-3 polynomial on the FMA pipe instead of
-// MUFU.EX2 (balances the two pipes); O is rescaled in TMEM only when the
+// raw scores (8 independent chains), p = exp2(s*scale - m) with packed
+// FFMA2 / FADD2 (fp32x2) arithmetic and MUFU.EX2 (a degree-3 FMA-pipe exp2 is
+// available as kPoly but measured slower here); O is rescaled in TMEM only when the
 // running max grows by > 2^8 (lazy rescale, warp-uniform because tcgen05.ld/st
 // are warp-collective). Registers rebalanced with setmaxnreg (TMA/MMA
 // warpgroup 56, softmax warpgroups 200).
@@ -33,6 +35,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "attention.h"
 #include "common.h"
@@ -47,11 +50,10 @@ using namespace sm100;
 constexpr int TQ = 128, TK = 128, HD = 128;
 constexpr int CHUNK = 128 * 64 * 2;  // one 128-row x 64-col bf16 SW128 block (16 KB)
 constexpr int TILE = 2 * CHUNK;      // a 128 x 128 bf16 operand (32 KB)
-constexpr int RING = 3;              // K/V ring slots
+constexpr int RING = 5;              // K/V ring slots
 constexpr int OFF_Q = 0;                       // Q0, Q1
-constexpr int OFF_RING = OFF_Q + 2 * TILE;     // 3 slots
-constexpr int OFF_P = OFF_RING + RING * TILE;  // P0, P1
-constexpr int OFF_BAR = OFF_P + 2 * TILE;
+constexpr int OFF_RING = OFF_Q + 2 * TILE;     // 5 slots
+constexpr int OFF_BAR = OFF_RING + RING * TILE;
 constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
 constexpr int THREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512)
@@ -62,13 +64,6 @@ struct MaskDev {
 };
 
 __device__ __forceinline__ int seg_of(int x, const MaskDev& m) { return (x - m.Lp) / m.Lmax; }
-
-__device__ __forceinline__ bool visible(int q, int k, const MaskDev& m) {
-  if (k >= m.L) return false;
-  if (m.mode == ATTN_BLOCK_DIAG) return q / m.blk == k / m.blk;
-  if (k > q) return false;
-  return k < m.Lp || seg_of(k, m) == seg_of(q, m);
-}
 
 // 0 = skip, 1 = fully visible, 2 = needs the element mask.
 __device__ __forceinline__ int tile_class(int q0, int kt, const MaskDev& m) {
@@ -122,18 +117,36 @@ struct AttnArgs {
   MaskDev mask;
 };
 
-// 2^x on the FMA/ALU pipes (x <= ~8): round-to-nearest split x = j + f,
-// f in [-0.5, 0.5], degree-3 polynomial (max rel. error 7.7e-5), exponent add.
+// 2^x on the FMA/ALU pipes: round-to-nearest split x = j + f, f in
+// [-0.5, 0.5], degree-3 polynomial (max rel. error 7.7e-5, far below bf16's
+// 3.9e-3), exponent add. Inputs below -126 clamp to 2^-126 (~1e-38, i.e. 0
+// after the P.V product).
 __device__ __forceinline__ float exp2_poly(float x) {
-  const float xc = fmaxf(x, -126.0f);  // keeps the exponent field positive
-  const float r = xc + 12582912.0f;    // 1.5 * 2^23: low mantissa bits = round(x)
+  x = fmaxf(x, -126.0f);
+  const float r = x + 12582912.0f;  // 1.5 * 2^23: low mantissa bits = round(x)
   const int j = __float_as_int(r) - 0x4B400000;
-  const float f = xc - (r - 12582912.0f);
+  const float f = x - (r - 12582912.0f);
   float p = fmaf(f, 0.05508868396282196f, 0.24260404706001282f);
   p = fmaf(f, p, 0.6932762265205383f);
   p = fmaf(f, p, 0.9999289512634277f);
-  const float y = __int_as_float(__float_as_int(p) + (j << 23));
-  return x < -126.0f ? 0.0f : y;  // masked scores (-inf) give exactly 0, as MUFU.EX2 does
+  return __int_as_float(__float_as_int(p) + (j << 23));
+}
+
+// Packed fp32x2 FMA / add (FFMA2 / FADD2 on sm_100a): half the issue slots.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                      float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1) {
+  asm("{\n\t.reg .b64 ra, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rd, {%0, %1};\n\t"
+      "add.rn.f32x2 rd, rd, ra;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1));
 }
 
 __device__ __forceinline__ float exp2_mufu(float x) {
@@ -151,6 +164,9 @@ __device__ __forceinline__ void reg_dealloc() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
+// kPoly: one element in kPoly (per packed pair slot) uses the FMA-pipe exp2
+// (0 = all MUFU).
+template <int kPoly>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
@@ -159,13 +175,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* r_full = bars + 1;    // [3]
-  uint64_t* r_empty = bars + 4;   // [3]
-  uint64_t* s_full = bars + 7;    // [2] per query tile
-  uint64_t* s_free = bars + 9;    // [2]
-  uint64_t* p_full = bars + 11;   // [2]
-  uint64_t* pv_done = bars + 13;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* r_full = bars + 1;    // [RING]
+  uint64_t* r_empty = bars + 6;   // [RING]
+  uint64_t* s_full = bars + 11;   // [2] per query tile
+  uint64_t* s_free = bars + 13;   // [2]
+  uint64_t* p_full = bars + 15;   // [2]
+  uint64_t* pv_done = bars + 17;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = warp_id();
   const int pair = a.n_pairs - 1 - static_cast<int>(blockIdx.x) / a.n_heads;  // heavy first
@@ -229,7 +245,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t idesc_s = idesc_bf16_f32(TQ, TK);
       const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
       const uint32_t q_addr = smem_u32(smem + OFF_Q);
-      const uint32_t p_addr = smem_u32(smem + OFF_P);
       const uint32_t ring_addr = smem_u32(smem + OFF_RING);
       mbar_wait(q_full, 0);
       int slot = 0;
@@ -258,9 +273,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < TK / 16; ++kk) {
-            const uint64_t ad = sdesc_sw128(p_addr + t * TILE + (kk / 4) * CHUNK + (kk % 4) * 32);
+            // A = P from TMEM (packed bf16 pairs over S(t)'s first 64 columns)
             const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
-            mma_bf16_ss(tmem + 256 + t * 128, ad, bd, idesc_o, (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o,
+                        (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&pv_done[t]);
         }
@@ -304,8 +320,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
     const uint32_t tS = tmem + t * 128 + lane_off;
     const uint32_t tO = tmem + 256 + t * 128 + lane_off;
-    uint8_t* p_smem = smem + OFF_P + t * TILE;
     const float sl2 = a.scale_log2;
+    // this row's visible key set, computed once: k < k_end and
+    // (k < k_mid or k >= k_lo)   [k_mid = Lp, k_lo = start of the row's segment]
+    int k_end, k_mid, k_lo;
+    if (a.mask.mode == ATTN_BLOCK_DIAG) {
+      k_lo = (q / a.mask.blk) * a.mask.blk;
+      k_mid = 0;
+      k_end = min(k_lo + a.mask.blk, a.mask.L);
+    } else {
+      k_end = min(q + 1, a.mask.L);
+      k_mid = a.mask.Lp;
+      k_lo = q >= a.mask.Lp ? a.mask.Lp + seg_of(q, a.mask) * a.mask.Lmax : 0;
+    }
     float m_run = -INFINITY, l_run = 0.f;  // m_run in scaled log2 units
     int it = 0;                            // KV tiles processed by this warpgroup
     for (int kt = kt_lo;; ++kt) {
@@ -334,16 +361,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       mbar_arrive(&s_free[t]);
       const int k0 = kt * TK;
-      float mx = -INFINITY;
       if (cls == 2) {
 #pragma unroll
         for (int j = 0; j < TK; ++j) {
-          if (!visible(q, k0 + j, a.mask)) s[j] = -INFINITY;
-          mx = fmaxf(mx, s[j]);
+          const int k = k0 + j;
+          if (!(k < k_end && (k < k_mid || k >= k_lo))) s[j] = -INFINITY;
         }
-      } else {
+      }
+      float mx;
+      {  // 8 independent max chains (FMNMX3) instead of one 128-deep chain
+        float m8[8];
 #pragma unroll
-        for (int j = 0; j < TK; ++j) mx = fmaxf(mx, s[j]);
+        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(s[i], s[i + 8]);
+#pragma unroll
+        for (int j = 16; j < TK; j += 16)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], fmaxf(s[j + i], s[j + i + 8]));
+        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       }
       const float mt = mx * sl2;  // -inf stays -inf
       // P buffer and O are free once this tile's previous P.V has completed.
@@ -366,27 +401,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (need) m_run = mt;
       const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      float lsum = 0.f;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 4 packed partial sums
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+        uint32_t w[32];  // 64 keys as 32 packed bf16 pairs -> TMEM columns [32c, 32c + 32)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = c * 64 + u * 8 + 2 * e;
-            const float x0 = fmaf(s[j], sl2, neg_m), x1 = fmaf(s[j + 1], sl2, neg_m);
-            const float p0 = exp2_mufu(x0);
-            const float p1 = (e & 1) ? exp2_poly(x1) : exp2_mufu(x1);
-            lsum += p0 + p1;
-            w[e] = pack_bf16(p0, p1);
-          }
-          uint8_t* dst = p_smem + c * CHUNK + (r >> 3) * 1024 + (r & 7) * 128 + ((u ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int i = 0; i < 32; ++i) {
+          const int j = c * 64 + 2 * i;
+          float x0, x1;
+          ffma2(x0, x1, s[j], s[j + 1], sl2, sl2, neg_m, neg_m);
+          const float p0 = exp2_mufu(x0);
+          const bool poly = kPoly > 0 && ((c * 32 + i) % (kPoly / 2)) == (kPoly / 2 - 1);
+          const float p1 = poly ? exp2_poly(x1) : exp2_mufu(x1);
+          fadd2(acc[2 * (i & 3)], acc[2 * (i & 3) + 1], p0, p1);
+          w[i] = pack_bf16(p0, p1);
         }
+        tmem_st32(tS + c * 32, w);
       }
+      tmem_st_wait();
+      const float lsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       l_run += lsum;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&p_full[t]);
       ++it;
@@ -433,9 +467,14 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
                MRSP_INVALID_ARGUMENT, "attention: leading dims must be multiples of 8");
   MRSP_REQUIRE(p.mode == ATTN_BLOCK_DIAG ? p.blk > 0 : (p.Lmax > 0 || p.Lp >= p.L),
                MRSP_INVALID_ARGUMENT, "attention: bad mask parameters");
+  // Measured on B200 (profiles/r1_summary.md): with P in TMEM the softmax is
+  // not MUFU-bound, so the FMA-pipe exp2 share that FA4 uses does not pay here
+  // (0: 1122 TFLOP/s at c4 shape vs 1100 with 1 in 16); kPoly = 0.
+  constexpr int kPolyChoice = 0;
   static bool attr = false;
   if (!attr) {
-    MRSP_CUDA(cudaFuncSetAttribute(attn_fwd_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MRSP_CUDA(cudaFuncSetAttribute(attn_fwd_tcgen05<kPolyChoice>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM_BYTES)));
     attr = true;
   }
@@ -456,7 +495,7 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.scale_log2 = p.scale * 1.4426950408889634f;
   a.mask = MaskDev{p.mode, p.L, p.Lp, p.Lmax > 0 ? p.Lmax : 1, p.blk > 0 ? p.blk : 1};
   const int grid = a.n_pairs * a.n_heads;
-  attn_fwd_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
+  attn_fwd_tcgen05<kPolyChoice><<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

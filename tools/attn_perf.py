@@ -23,3 +23,4 @@ if __name__ == "__main__":
     print(json.dumps(bench(16384, 28, 4)), flush=True)
     print(json.dumps(bench(32768, 28, 4)), flush=True)
     print(json.dumps(bench(16421 + 8 * 1024, 28, 4, 16421, 1024)), flush=True)
+    print(json.dumps(bench(131109 + 8 * 1011, 28, 4, 131109, 1011, iters=2)), flush=True)
