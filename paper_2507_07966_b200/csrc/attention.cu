@@ -179,9 +179,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* r_empty = bars + 6;   // [RING]
   uint64_t* s_full = bars + 11;   // [2] per query tile
   uint64_t* s_free = bars + 13;   // [2]
-  uint64_t* p_full = bars + 15;   // [2]
-  uint64_t* pv_done = bars + 17;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* p_full = bars + 15;   // [2][2]: per query tile, per 64-key half of P
+  uint64_t* pv_done = bars + 19;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const int warp = warp_id();
   const int pair = a.n_pairs - 1 - static_cast<int>(blockIdx.x) / a.n_heads;  // heavy first
@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&s_free[t], 128);
-      mbar_init(&p_full[t], 128);
+      mbar_init(&p_full[2 * t], 128);
+      mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&pv_done[t], 1);
     }
     fence_barrier_init();
@@ -268,19 +269,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         ++n_s[t];
       };
       auto issue_pv = [&](int t, uint32_t v_addr) {
-        mbar_wait(&p_full[t], n_pv[t] & 1);
-        tc_fence_after();
-        if (elect_one()) {
+        // two halves of 64 keys: the first half's MMAs start while the softmax
+        // is still exponentiating the second half
 #pragma unroll
-          for (int kk = 0; kk < TK / 16; ++kk) {
-            // A = P from TMEM (packed bf16 pairs over S(t)'s first 64 columns)
-            const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
-            mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o,
-                        (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(&p_full[2 * t + half], n_pv[t] & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int kk = half * 4 + k4;
+              // A = P from TMEM (packed bf16 pairs over S(t)'s first 64 columns)
+              const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
+              mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o,
+                          (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (half == 1) mma_commit(&pv_done[t]);
           }
-          mma_commit(&pv_done[t]);
+          __syncwarp();
         }
-        __syncwarp();
         ++n_pv[t];
       };
       auto release = [&](int s) {
@@ -417,12 +424,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           w[i] = pack_bf16(p0, p1);
         }
         tmem_st32(tS + c * 32, w);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * t + c]);  // this half of P is ready for the MMA
       }
-      tmem_st_wait();
-      const float lsum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      l_run += lsum;
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      l_run += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       ++it;
     }
     // epilogue: O / l -> bf16 global
