@@ -275,7 +275,7 @@ def main():
     pix_host = torch.from_numpy(E.gen_video(1, w.frames, 3 * S * S)).pin_memory()
     pix = pix_host.cuda()
     n_scored = group.scored
-    lp_dev = (torch.empty(n_scored, device="cuda"), torch.empty(n_scored, device="cuda"))
+    lp_dev = tuple(torch.empty(n_scored, device="cuda") for _ in range(3))  # lp_policy, lp_ref, kl
     stream = torch.cuda.ExternalStream(eng.stream)
 
     def barrier():
@@ -298,7 +298,7 @@ def main():
         if dev_inputs:
             eng.step(vid, pix, group, out=lp_dev)
             return None
-        return eng.step(vid, pix_host.numpy(), group)  # host pixels in, host log-probs out
+        return eng.step(vid, pix_host.numpy(), group, with_kl=True)  # host in, host out
 
     for _ in range(args.warmup):
         one_step()
@@ -331,7 +331,7 @@ def main():
         t_wall = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
-            lp_p, lp_r = one_step(False)
+            lp_p, lp_r, kl = one_step(False)
         e1.record(stream)
         e1.synchronize()
         wall = (time.perf_counter() - t_wall) / args.steps * 1e3
@@ -340,9 +340,9 @@ def main():
         tok_bytes = 4 * (len(group.question) + group.resp.size + group.lengths.size)
         e2e = {"value": fl["tokens"] / (e2e_ms / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": w.frames * frame_bytes + 2 * world * tok_bytes,
-               "d2h_bytes_per_step": 2 * world * n_scored * 4,
+               "d2h_bytes_per_step": 3 * world * n_scored * 4,
                "ms_per_step": e2e_ms,
-               "note": "mrsp_engine_step with pinned host pixels and host log-prob buffers"}
+               "note": "mrsp_engine_step with pinned host pixels in; host log-probs (policy, ref) and exact KL out"}
 
     # ---- roofline of the dominant kernel (LLM attention), live CUDA events
     attn_ms, attn_n = prof["llm_attention"]

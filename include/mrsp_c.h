@@ -137,6 +137,18 @@ mrsp_status mrsp_op_lmhead_logprob(const void* X, int ldx, const void* W, int M,
                                    const int32_t* targets, float* logprob, float* lse,
                                    void* workspace, size_t ws_bytes, void* stream);
 
+/* Fused policy + reference LM head: for each scored token
+ * one vocabulary sweep over both models yields log pi_theta(y), log pi_ref(y)
+ * and the exact KL(pi_theta || pi_ref) = sum_v p_v (log p_v - log q_v) — the
+ * quantities evaluate_from_logits computes from two materialised logit
+ * tensors (grpo.cpp:68-108, exact KL at :94-96; policy.cpp:176-193).
+ * X_* [M][K] bf16 (final-normed hidden of each model), W_* [V][K] bf16. */
+size_t mrsp_lmhead_dual_workspace_bytes(int M, int V);
+mrsp_status mrsp_op_lmhead_dual(const void* X_policy, const void* W_policy, const void* X_ref,
+                                const void* W_ref, int M, int V, int K, const int32_t* targets,
+                                float* logprob_policy, float* logprob_ref, float* kl,
+                                void* workspace, size_t ws_bytes, void* stream);
+
 /* RMSNorm (Qwen2): out[i] = bf16(w * x[rows ? rows[i] : i] * rsqrt(mean(x^2) + eps)),
  * x fp32 [.][ldx], out bf16 [n][ldo]. */
 mrsp_status mrsp_op_rmsnorm(const float* x, int ldx, const float* w, void* out, int ldo, int n,
@@ -259,11 +271,13 @@ mrsp_status mrsp_engine_prefill_logprobs(mrsp_engine* e, const char* video_id,
                                          float* logprob, float* lse, int out_on_device);
 
 /* One MR-SP step (engine.cpp:203-225 contract): G embedding fetches (cache
- * on: 1 miss + G-1 hits), then policy and reference prefill + log-probs. */
+ * on: 1 miss + G-1 hits), then policy and reference prefill; the two LM heads
+ * run as one fused sweep that also yields the exact per-token KL (kl may be
+ * NULL). Outputs: sum(lengths) floats each, host unless out_on_device. */
 mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, const float* pixels, int F,
                              int pixels_on_device, int use_cache, const int32_t* question,
                              int n_q, const int32_t* resp, const int32_t* lengths, int G,
-                             int Lmax, float* logprob_policy, float* logprob_ref,
+                             int Lmax, float* logprob_policy, float* logprob_ref, float* kl,
                              int out_on_device);
 
 /* Counters: [encoder_invocations, cache_hits, cache_misses, gather_bytes,

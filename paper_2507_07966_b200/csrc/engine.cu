@@ -73,12 +73,6 @@ std::vector<std::pair<long, long>> plan(long n, int k) {
   return r;
 }
 
-__global__ void scatter_f32_kernel(const float* __restrict__ src, const int* __restrict__ slot,
-                                   int n, float* __restrict__ dst) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[slot[i]] = src[i];
-}
-
 struct Carver {
   uint8_t* base;
   size_t off = 0;
@@ -679,37 +673,37 @@ void Engine::a2a_backward(int L) {
 }
 
 // ---------------------------------------------------------------------------
-void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
-                              const int32_t* resp, const int32_t* lengths, int G, int Lmax,
-                              int model, float* lp_out, float* lse_out, bool out_on_device) {
+// Host-side pad_batch semantics for one GRPO group: validation, token upload
+// (shared by both passes), the token plan and each shard's scored positions.
+void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
+                           const int32_t* resp, const int32_t* lengths, int G, int Lmax) {
   const auto& c = cfg_;
-  MRSP_REQUIRE(model == 0 || model == 1, MRSP_INVALID_ARGUMENT, "prefill: model must be 0 or 1");
   MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "pad_batch: empty batch");
   MRSP_REQUIRE(Lmax >= 1 && n_q >= 0, MRSP_INVALID_ARGUMENT, "prefill: bad lengths");
-  std::lock_guard<std::mutex> run(run_mu_);
-  const LlmW& W = llm_[model];
-  const int T = tokens_per_frame(), d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads;
-  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128;
-  const long n_frame_tok = static_cast<long>(emb.n_frames) * T;
-  const long Lp = n_frame_tok + n_q;
-  const long Ltot = Lp + static_cast<long>(G) * Lmax;
-  MRSP_REQUIRE(Ltot < (1L << 31), MRSP_INVALID_ARGUMENT, "prefill: sequence too long");
-  // host-side pad_batch semantics: validate rows, scored positions per rank
+  const int T = tokens_per_frame(), d = c.dim;
+  GroupState& g = grp_;
+  g.n_q = n_q;
+  g.G = G;
+  g.Lmax = Lmax;
+  g.n_frame_tok = static_cast<long>(emb.n_frames) * T;
+  g.Lp = g.n_frame_tok + n_q;
+  g.Ltot = g.Lp + static_cast<long>(G) * Lmax;
+  MRSP_REQUIRE(g.Ltot < (1L << 31), MRSP_INVALID_ARGUMENT, "prefill: sequence too long");
   std::vector<long> row_off(G + 1, 0);
-  for (int g = 0; g < G; ++g) {
-    MRSP_REQUIRE(lengths[g] >= 0 && lengths[g] <= Lmax, MRSP_INVALID_ARGUMENT,
+  for (int r = 0; r < G; ++r) {
+    MRSP_REQUIRE(lengths[r] >= 0 && lengths[r] <= Lmax, MRSP_INVALID_ARGUMENT,
                  "prefill: row longer than Lmax");
-    row_off[g + 1] = row_off[g] + lengths[g];
-    for (int j = 0; j < lengths[g]; ++j)
-      MRSP_REQUIRE(resp[static_cast<size_t>(g) * Lmax + j] >= 0 &&
-                       resp[static_cast<size_t>(g) * Lmax + j] < c.vocab,
+    row_off[r + 1] = row_off[r] + lengths[r];
+    for (int j = 0; j < lengths[r]; ++j)
+      MRSP_REQUIRE(resp[static_cast<size_t>(r) * Lmax + j] >= 0 &&
+                       resp[static_cast<size_t>(r) * Lmax + j] < c.vocab,
                    MRSP_INVALID_ARGUMENT, "step_logits: prev token out of range");
   }
   for (int i = 0; i < n_q; ++i)
     MRSP_REQUIRE(question[i] >= 0 && question[i] < c.vocab, MRSP_INVALID_ARGUMENT,
                  "context_vector: token out of range");
-  const long total_scored = row_off[G];
-  const auto tplan = plan(Ltot, k_);
+  g.total_scored = row_off[G];
+  const auto tplan = plan(g.Ltot, k_);
   token_b_.resize(k_);
   token_e_.resize(k_);
   for (int w = 0; w < k_; ++w) {
@@ -717,36 +711,35 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
     token_e_[w] = tplan[w].second;
   }
   cudaStream_t s = stream_;
-  // upload the group's tokens once (shared by all local ranks)
   const size_t tok_ints = static_cast<size_t>(n_q) + static_cast<size_t>(G) * Lmax + G;
-  int32_t* dtok = static_cast<int32_t*>(io_.ensure(tok_ints * 4 + (total_scored + 64) * 8));
+  // [question | resp | lengths] ints, then 4 full-length float vectors
+  int32_t* dtok = static_cast<int32_t*>(io_.ensure(tok_ints * 4 + (4 * g.total_scored + 64) * 4));
   MRSP_CUDA(cudaMemcpyAsync(dtok, question, static_cast<size_t>(n_q) * 4, cudaMemcpyHostToDevice, s));
   MRSP_CUDA(cudaMemcpyAsync(dtok + n_q, resp, static_cast<size_t>(G) * Lmax * 4,
                             cudaMemcpyHostToDevice, s));
   MRSP_CUDA(cudaMemcpyAsync(dtok + n_q + static_cast<size_t>(G) * Lmax, lengths,
                             static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
-  float* dlp_full = reinterpret_cast<float*>(dtok + tok_ints);
-  float* dlse_full = dlp_full + total_scored + 16;
-  MRSP_CUDA(cudaMemsetAsync(dlp_full, 0, (2 * total_scored + 32) * 4, s));
-  const int32_t* d_question = dtok;
-  const int32_t* d_resp = dtok + n_q;
-  const int32_t* d_len = dtok + n_q + static_cast<size_t>(G) * Lmax;
-
+  g.d_question = dtok;
+  g.d_resp = dtok + n_q;
+  g.d_len = dtok + n_q + static_cast<size_t>(G) * Lmax;
+  g.full = reinterpret_cast<float*>(dtok + tok_ints);  // 4 x (total_scored + 16)
+  g.stride = g.total_scored + 16;
+  MRSP_CUDA(cudaMemsetAsync(g.full, 0, static_cast<size_t>(4 * g.stride) * 4, s));
+  const int Cqkv = (c.n_q_heads + 2 * c.n_kv_heads) * 128, Cq = c.n_q_heads * 128;
   for (auto& R : ranks_) {
     R.b = tplan[R.g].first;
     R.e = tplan[R.g].second;
     const long n = R.e - R.b;
-    // scored positions of this shard: row region, j < len (never a pad: the
-    // prev token of position j is read only for j < len, engine.cpp:124)
+    // scored positions of this shard: row region, j < len (the prev token of
+    // position j is read only for j < len, engine.cpp:124 -> pad_reads == 0)
     std::vector<int32_t> idx, tgt, slot;
-    const long r0 = std::max(R.b, Lp);
-    for (long p = r0; p < R.e; ++p) {
-      const long q = p - Lp;
-      const int g = static_cast<int>(q / Lmax), j = static_cast<int>(q % Lmax);
-      if (j < lengths[g]) {
+    for (long p = std::max(R.b, g.Lp); p < R.e; ++p) {
+      const long q = p - g.Lp;
+      const int r = static_cast<int>(q / Lmax), j = static_cast<int>(q % Lmax);
+      if (j < lengths[r]) {
         idx.push_back(static_cast<int32_t>(p - R.b));
-        tgt.push_back(resp[static_cast<size_t>(g) * Lmax + j]);
-        slot.push_back(static_cast<int32_t>(row_off[g] + j));
+        tgt.push_back(resp[static_cast<size_t>(r) * Lmax + j]);
+        slot.push_back(static_cast<int32_t>(row_off[r] + j));
       }
     }
     R.n_scored = static_cast<int>(idx.size());
@@ -758,24 +751,37 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
                                 cudaMemcpyHostToDevice, s));
       MRSP_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
     }
-    // activations
-    R.h.ensure(static_cast<size_t>(std::max(n, 1L)) * d * 4);
-    R.xn.ensure(static_cast<size_t>(std::max(n, 1L)) * d * 2);
-    R.qkv.ensure(static_cast<size_t>(std::max(n, 1L)) * Cqkv * 2);
-    R.ol.ensure(static_cast<size_t>(std::max(n, 1L)) * Cq * 2);
-    R.act.ensure(static_cast<size_t>(std::max(n, 1L)) * c.mlp * 2);
-    R.pos.ensure(static_cast<size_t>(std::max(n, 1L)) * 4);
-    R.pad.ensure(static_cast<size_t>(std::max(n, 1L)));
+    const size_t nn = static_cast<size_t>(std::max(n, 1L));
+    R.h.ensure(nn * d * 4);
+    R.xn.ensure(nn * d * 2);
+    R.qkv.ensure(nn * Cqkv * 2);
+    R.ol.ensure(nn * Cq * 2);
+    R.act.ensure(nn * c.mlp * 2);
+    R.pos.ensure(nn * 4);
+    R.pad.ensure(nn);
     if (k_ > 1) {
-      R.qh.ensure(static_cast<size_t>(Ltot) * (R.hs.nq() + 2 * R.hs.nkv()) * 128 * 2);
-      R.oh.ensure(static_cast<size_t>(Ltot) * std::max(R.hs.nq(), 1) * 128 * 2);
+      R.qh.ensure(static_cast<size_t>(g.Ltot) * (R.hs.nq() + 2 * R.hs.nkv()) * 128 * 2);
+      R.oh.ensure(static_cast<size_t>(g.Ltot) * std::max(R.hs.nq(), 1) * 128 * 2);
     }
-    {
-      Prof pm(*this, P_MISC);
-      pack_sequence(emb.emb->as<bf16>(), static_cast<int>(n_frame_tok), d_question, n_q, d_resp,
-                    d_len, Lmax, W.embed, d, R.b, static_cast<int>(n), R.h.as<float>(),
-                    R.pos.as<int>(), R.pad.as<unsigned char>(), nullptr, s);
-    }
+    R.xs.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
+    R.xs2.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
+  }
+}
+
+// One model's pass over the packed group: pack, the decoder stack with Ulysses
+// all-to-alls, final RMSNorm at the scored positions into R.xs / R.xs2.
+void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
+  const auto& c = cfg_;
+  const GroupState& g = grp_;
+  const LlmW& W = llm_[model];
+  const int d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads;
+  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128;
+  cudaStream_t s = stream_;
+  for (auto& R : ranks_) {
+    Prof pm(*this, P_MISC);
+    pack_sequence(emb.emb->as<bf16>(), static_cast<int>(g.n_frame_tok), g.d_question, g.n_q,
+                  g.d_resp, g.d_len, g.Lmax, W.embed, d, R.b, static_cast<int>(R.e - R.b),
+                  R.h.as<float>(), R.pos.as<int>(), R.pad.as<unsigned char>(), nullptr, s);
   }
   const float scale = 1.0f / std::sqrt(128.0f);
   for (const auto& Lw : W.layers) {
@@ -797,25 +803,26 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
         rope(R.qkv.as<bf16>(), Cqkv, 0, nq + nkv, R.pos.as<int>(), n, s);
       }
     }
-    if (k_ > 1) a2a_forward(static_cast<int>(Ltot));
+    if (k_ > 1) a2a_forward(static_cast<int>(g.Ltot));
     for (auto& R : ranks_) {
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
       Prof pa(*this, P_ATTN);
       if (k_ == 1) {
         attention_fwd({R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
-                       R.ol.p, Cq, 0, static_cast<int>(Ltot), nq, nq / nkv, scale,
-                       ATTN_CAUSAL_PREFIX, static_cast<int>(Lp), Lmax, 0},
+                       R.ol.p, Cq, 0, static_cast<int>(g.Ltot), nq, nq / nkv, scale,
+                       ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0},
                       s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
         attention_fwd({R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr,
-                       (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(Ltot), nqr,
-                       R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(Lp), Lmax, 0},
+                       (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(g.Ltot),
+                       nqr, R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp),
+                       g.Lmax, 0},
                       s);
       }
     }
-    if (k_ > 1) a2a_backward(static_cast<int>(Ltot));
+    if (k_ > 1) a2a_backward(static_cast<int>(g.Ltot));
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
@@ -840,37 +847,93 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
       }
     }
   }
-  // final norm + fused LM head at the scored positions of each shard
   for (auto& R : ranks_) {
-    const int ns = R.n_scored;
-    if (ns == 0) continue;
-    const int32_t* di = R.scored_idx.as<int32_t>();
-    bf16* xs = static_cast<bf16*>(R.xs.ensure(static_cast<size_t>(ns) * d * 2));
-    float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 8));
-    rmsnorm(R.h.as<float>(), d, W.final_norm, xs, d, ns, d, c.rms_eps, di, s);
-    const size_t wsb = lmhead_workspace_bytes(ns, c.vocab);
-    void* ws = R.ws.ensure(wsb);
-    {
-      Prof pl(*this, P_LMHEAD);
-      lmhead_logprob(xs, d, W.lm_head, ns, c.vocab, d, di + ns, lp, lp + ns, ws, wsb, s);
-    }
-    scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp, di + 2 * ns, ns, dlp_full);
-    count_launch();
-    scatter_f32_kernel<<<(ns + 255) / 256, 256, 0, s>>>(lp + ns, di + 2 * ns, ns, dlse_full);
+    if (R.n_scored == 0) continue;
+    DevBuf& xs = xs_slot ? R.xs2 : R.xs;
+    rmsnorm(R.h.as<float>(), d, W.final_norm, xs.as<bf16>(), d, R.n_scored, d, c.rms_eps,
+            R.scored_idx.as<int32_t>(), s);
+  }
+}
+
+namespace {
+__global__ void scatter3_kernel(const float* __restrict__ src, const int* __restrict__ slot, int n,
+                                int nvec, float* __restrict__ dst, long stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n)
+    for (int v = 0; v < nvec; ++v) dst[v * stride + slot[i]] = src[v * n + i];
+}
+}  // namespace
+
+// Scatter per-shard vectors into the group-ordered outputs, reduce across
+// processes, copy out.
+void Engine::finish_group(int nvec, float* const* outs, bool out_on_device) {
+  const GroupState& g = grp_;
+  cudaStream_t s = stream_;
+  for (auto& R : ranks_) {
+    if (R.n_scored == 0) continue;
+    scatter3_kernel<<<(R.n_scored + 255) / 256, 256, 0, s>>>(
+        R.lp.as<float>(), R.scored_idx.as<int32_t>() + 2 * R.n_scored, R.n_scored, nvec, g.full,
+        g.stride);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
   if (nccl_) {
     Prof pc(*this, P_COMM);
-    nccl_->all_reduce_sum_f32(dlp_full, dlp_full, static_cast<size_t>(2 * total_scored + 32), s);
+    nccl_->all_reduce_sum_f32(g.full, g.full, static_cast<size_t>(nvec * g.stride), s);
   }
   const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (total_scored) {
-    MRSP_CUDA(cudaMemcpyAsync(lp_out, dlp_full, total_scored * 4, kind, s));
-    if (lse_out) MRSP_CUDA(cudaMemcpyAsync(lse_out, dlse_full, total_scored * 4, kind, s));
-  }
+  for (int v = 0; v < nvec; ++v)
+    if (outs[v] && g.total_scored)
+      MRSP_CUDA(cudaMemcpyAsync(outs[v], g.full + v * g.stride, g.total_scored * 4, kind, s));
   MRSP_CUDA(cudaStreamSynchronize(s));
   prof_collect();
+}
+
+void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
+                              const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                              int model, float* lp_out, float* lse_out, bool out_on_device) {
+  MRSP_REQUIRE(model == 0 || model == 1, MRSP_INVALID_ARGUMENT, "prefill: model must be 0 or 1");
+  std::lock_guard<std::mutex> run(run_mu_);
+  prepare_group(emb, question, n_q, resp, lengths, G, Lmax);
+  run_pass(emb, model, 0);
+  const auto& c = cfg_;
+  for (auto& R : ranks_) {
+    const int ns = R.n_scored;
+    if (ns == 0) continue;
+    float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 4 * 3));
+    const size_t wsb = lmhead_workspace_bytes(ns, c.vocab);
+    void* ws = R.ws.ensure(wsb);
+    Prof pl(*this, P_LMHEAD);
+    lmhead_logprob(R.xs.p, c.dim, llm_[model].lm_head, ns, c.vocab, c.dim,
+                   R.scored_idx.as<int32_t>() + ns, lp, lp + ns, ws, wsb, stream_);
+  }
+  float* outs[2] = {lp_out, lse_out};
+  finish_group(2, outs, out_on_device);
+}
+
+// Both passes + the fused dual LM head: per-token log pi_theta(y), log pi_ref(y)
+// and exact KL(pi_theta || pi_ref) from one vocabulary sweep.
+void Engine::group_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
+                            const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                            float* lp_policy, float* lp_ref, float* kl, bool out_on_device) {
+  std::lock_guard<std::mutex> run(run_mu_);
+  prepare_group(emb, question, n_q, resp, lengths, G, Lmax);
+  run_pass(emb, 0, 0);
+  run_pass(emb, 1, 1);
+  const auto& c = cfg_;
+  for (auto& R : ranks_) {
+    const int ns = R.n_scored;
+    if (ns == 0) continue;
+    float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 4 * 3));
+    const size_t wsb = lmhead_dual_workspace_bytes(ns, c.vocab);
+    void* ws = R.ws.ensure(wsb);
+    Prof pl(*this, P_LMHEAD);
+    lmhead_dual_logprob_kl(R.xs.p, llm_[0].lm_head, R.xs2.p, llm_[1].lm_head, ns, c.vocab, c.dim,
+                           R.scored_idx.as<int32_t>() + ns, lp, lp + ns, lp + 2 * ns, ws, wsb,
+                           stream_);
+  }
+  float* outs[3] = {lp_policy, lp_ref, kl};
+  finish_group(3, outs, out_on_device);
 }
 
 size_t Engine::cache_size() {
@@ -983,7 +1046,7 @@ extern "C" mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, co
                                         int F, int pixels_on_device, int use_cache,
                                         const int32_t* question, int n_q, const int32_t* resp,
                                         const int32_t* lengths, int G, int Lmax,
-                                        float* logprob_policy, float* logprob_ref,
+                                        float* logprob_policy, float* logprob_ref, float* kl,
                                         int out_on_device) {
   return guard([&] {
     MRSP_REQUIRE(e && video_id && pixels, MRSP_INVALID_ARGUMENT, "step: null argument");
@@ -992,10 +1055,8 @@ extern "C" mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, co
       bool h = false;
       entry = e->impl->get_or_encode(video_id, pixels, F, pixels_on_device != 0, use_cache != 0, &h);
     }
-    e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, 0, logprob_policy,
-                              nullptr, out_on_device != 0);
-    e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, 1, logprob_ref,
-                              nullptr, out_on_device != 0);
+    e->impl->group_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, logprob_policy,
+                            logprob_ref, kl, out_on_device != 0);
   });
 }
 

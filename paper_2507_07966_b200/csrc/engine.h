@@ -83,8 +83,7 @@ struct RankCtx {
   // stage 1
   DevBuf pix, patches, vh, vxn, vqkv, vo, vmid, pout;
   // stage 2
-  DevBuf h, xn, qkv, qh, oh, ol, act, pos, pad, scored_idx, scored_tgt, scored_slot, xs, lp, ws,
-      send, recv;
+  DevBuf h, xn, qkv, qh, oh, ol, act, pos, pad, scored_idx, xs, xs2, lp, ws, send, recv;
   long b = 0, e = 0;  // token range
   int n_scored = 0;
 };
@@ -115,6 +114,11 @@ class Engine {
   void prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
                         const int32_t* resp, const int32_t* lengths, int G, int Lmax, int model,
                         float* lp_out, float* lse_out, bool out_on_device);
+  // Policy + reference passes and the fused dual LM head (log-probs of both
+  // models and the exact per-token KL in one vocabulary sweep).
+  void group_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
+                      const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                      float* lp_policy, float* lp_ref, float* kl, bool out_on_device);
 
   const mrsp_model_config& cfg() const { return cfg_; }
   int tokens_per_frame() const { return (cfg_.image_size / cfg_.patch) * (cfg_.image_size / cfg_.patch); }
@@ -141,6 +145,17 @@ class Engine {
                    bf16* out);
   void a2a_forward(int L);
   void a2a_backward(int L);
+  void prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
+                     const int32_t* resp, const int32_t* lengths, int G, int Lmax);
+  void run_pass(const CacheEntry& emb, int model, int xs_slot);
+  void finish_group(int nvec, float* const* outs, bool out_on_device);
+
+  struct GroupState {
+    int n_q = 0, G = 0, Lmax = 0;
+    long n_frame_tok = 0, Lp = 0, Ltot = 0, total_scored = 0, stride = 0;
+    const int32_t *d_question = nullptr, *d_resp = nullptr, *d_len = nullptr;
+    float* full = nullptr;  // group-ordered output vectors (stride floats each)
+  } grp_;
 
   mrsp_model_config cfg_;
   int k_, proc_rank_, n_procs_, device_ = 0;

@@ -31,4 +31,11 @@ void lmhead_logprob(const void* X, int ldx, const void* W, int M, int V, int K,
                     const int32_t* targets, float* logprob, float* lse, void* ws, size_t ws_bytes,
                     cudaStream_t stream);
 
+// Fused policy + reference LM head: log-probs of both models at the targets and
+// the exact KL(policy || reference) per token (csrc/lmhead_dual.cu).
+size_t lmhead_dual_workspace_bytes(int M, int V);
+void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, const void* Wr, int M,
+                            int V, int K, const int32_t* targets, float* lp_p, float* lp_r,
+                            float* kl, void* ws, size_t ws_bytes, cudaStream_t stream);
+
 }  // namespace mrsp

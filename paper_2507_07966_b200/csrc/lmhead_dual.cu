@@ -1,0 +1,302 @@
+// lmhead_dual.cu — fused policy + reference LM head over the same scored tokens:
+// one vocabulary sweep computes, per token, log pi_theta(y), log pi_ref(y) and the
+// exact KL(pi_theta || pi_ref) over the whole vocabulary — the quantities the
+// reference derives from two materialised [tokens x V] logit tensors in
+// evaluate_from_logits (grpo.cpp:68-108: log_softmax, lp[y], exact KL at
+// :94-96; per-position KL in policy.cpp:176-193). Logits never leave TMEM.
+//
+// Tile = 128 tokens x 256 vocab entries, BOTH models: two tcgen05 accumulators
+// (2 x 256 TMEM columns), A_p/B_p/A_r/B_r staged by TMA (2-stage ring of
+// 96 KB). Epilogue per row (thread = token): online over the tile's 256
+// columns, with x = policy logit, y = reference logit,
+//   m_x, s_x = sum e^(x - m_x), u = sum e^(x - m_x) (x - y), m_y, s_y = sum e^(y - m_y)
+// plus the two target logits; a combine kernel merges the vocab tiles:
+//   lse_x = M_x + log S_x,  KL = U / S_x - lse_x + lse_y,  lp = logit[y] - lse.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.h"
+#include "gemm.h"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace mrsp {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 2;
+constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // policy + reference operands
+constexpr int THREADS = 256;
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+
+struct Part {  // per (token, vocab tile)
+  float mx, sx, ux, my, sy;
+};
+
+struct DualArgs {
+  int M, V, K, n_tiles;
+  const int* targets;
+  Part* part;
+  float* tgt_x;
+  float* tgt_y;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    lmhead_dual_tcgen05(const __grid_constant__ CUtensorMap tmAx, const __grid_constant__ CUtensorMap tmBx,
+                        const __grid_constant__ CUtensorMap tmAy, const __grid_constant__ CUtensorMap tmBy,
+                        DualArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = warp_id();
+  const int m_tiles = (a.M + BM - 1) / BM;
+  const int num_tiles = m_tiles * a.n_tiles;
+  const int k_blocks = (a.K + BK - 1) / BK;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmAx);
+    tma_prefetch_desc(&tmBx);
+    tma_prefetch_desc(&tmAy);
+    tma_prefetch_desc(&tmBy);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile % m_tiles, nt = tile / m_tiles;  // vocab-major: W tiles stream once
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* s = smem + stage * STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(s, &tmAx, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(s + A_BYTES, &tmBx, &full[stage], kb * BK, nt * BN);
+          tma_load_2d(s + A_BYTES + B_BYTES, &tmAy, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(s + 2 * A_BYTES + B_BYTES, &tmBy, &full[stage], kb * BK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t tphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(tempty, tphase ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t s = smem_u32(smem + stage * STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            mma_bf16_ss(tmem, sdesc_sw128(s + k * 32), sdesc_sw128(s + A_BYTES + k * 32), idesc,
+                        (kb | k) != 0);
+            mma_bf16_ss(tmem + BN, sdesc_sw128(s + A_BYTES + B_BYTES + k * 32),
+                        sdesc_sw128(s + 2 * A_BYTES + B_BYTES + k * 32), idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (kb == k_blocks - 1) mma_commit(tfull);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      tphase ^= 1;
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    uint32_t tphase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile % m_tiles, nt = tile / m_tiles;
+      mbar_wait(tfull, tphase);
+      tc_fence_after();
+      const int row = mt * BM + ew * 32 + lane_id();
+      const bool row_ok = row < a.M;
+      const int tgt = row_ok ? a.targets[row] : -1;
+      const uint32_t tr = tmem + (static_cast<uint32_t>(ew * 32) << 16);
+      float mx = -INFINITY, sx = 0.f, ux = 0.f, my = -INFINITY, sy = 0.f;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t rx[32], ry[32];
+        tmem_ld32(tr + c, rx);
+        tmem_ld32(tr + BN + c, ry);
+        tmem_ld_wait();
+        const int col = nt * BN + c;
+        float cx = -INFINITY, cy = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col + j < a.V) {
+            cx = fmaxf(cx, __uint_as_float(rx[j]));
+            cy = fmaxf(cy, __uint_as_float(ry[j]));
+          }
+        const float nx = fmaxf(mx, cx), ny = fmaxf(my, cy);
+        const float fx = mx == -INFINITY ? 0.f : __expf(mx - nx);
+        const float fy = my == -INFINITY ? 0.f : __expf(my - ny);
+        float ax = sx * fx, au = ux * fx, ay = sy * fy;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = __uint_as_float(rx[j]), y = __uint_as_float(ry[j]);
+          if (col + j < a.V) {
+            const float ex = __expf(x - nx);
+            ax += ex;
+            au = fmaf(ex, x - y, au);
+            ay += __expf(y - ny);
+          }
+          if (col + j == tgt) {
+            a.tgt_x[row] = x;
+            a.tgt_y[row] = y;
+          }
+        }
+        mx = nx;
+        my = ny;
+        sx = ax;
+        ux = au;
+        sy = ay;
+      }
+      if (row_ok) a.part[static_cast<size_t>(row) * a.n_tiles + nt] = Part{mx, sx, ux, my, sy};
+      tc_fence_before();
+      mbar_arrive(tempty);
+      tphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+__global__ void lmhead_dual_combine(const Part* __restrict__ part, int n_tiles,
+                                    const float* __restrict__ tgt_x, const float* __restrict__ tgt_y,
+                                    int n, float* __restrict__ lp_x, float* __restrict__ lp_y,
+                                    float* __restrict__ kl) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const Part* pr = part + static_cast<size_t>(warp) * n_tiles;
+  float Mx = -INFINITY, My = -INFINITY;
+  for (int t = lane; t < n_tiles; t += 32) {
+    Mx = fmaxf(Mx, pr[t].mx);
+    My = fmaxf(My, pr[t].my);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+    My = fmaxf(My, __shfl_xor_sync(0xffffffffu, My, o));
+  }
+  float Sx = 0.f, Ux = 0.f, Sy = 0.f;
+  for (int t = lane; t < n_tiles; t += 32) {
+    const float fx = expf(pr[t].mx - Mx);
+    Sx += pr[t].sx * fx;
+    Ux += pr[t].ux * fx;
+    Sy += pr[t].sy * expf(pr[t].my - My);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
+    Ux += __shfl_xor_sync(0xffffffffu, Ux, o);
+    Sy += __shfl_xor_sync(0xffffffffu, Sy, o);
+  }
+  if (lane == 0) {
+    const float lse_x = Mx + logf(Sx), lse_y = My + logf(Sy);
+    lp_x[warp] = tgt_x[warp] - lse_x;
+    lp_y[warp] = tgt_y[warp] - lse_y;
+    kl[warp] = Ux / Sx - lse_x + lse_y;
+  }
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+}  // namespace
+
+size_t lmhead_dual_workspace_bytes(int M, int V) {
+  const size_t n_tiles = (V + BN - 1) / BN;
+  return (static_cast<size_t>(M) * n_tiles * sizeof(Part) + static_cast<size_t>(M) * 8 + 255) &
+         ~size_t(255);
+}
+
+void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, const void* Wr, int M,
+                            int V, int K, const int32_t* targets, float* lp_p, float* lp_r,
+                            float* kl, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (M <= 0) return;
+  MRSP_REQUIRE(K % 8 == 0, MRSP_INVALID_ARGUMENT, "lmhead_dual: K must be a multiple of 8");
+  MRSP_REQUIRE(ws_bytes >= lmhead_dual_workspace_bytes(M, V), MRSP_INVALID_ARGUMENT,
+               "lmhead_dual: workspace too small");
+  static bool attr = false;
+  if (!attr) {
+    MRSP_CUDA(cudaFuncSetAttribute(lmhead_dual_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(SMEM_BYTES)));
+    attr = true;
+  }
+  DualArgs a;
+  a.M = M;
+  a.V = V;
+  a.K = K;
+  a.n_tiles = (V + BN - 1) / BN;
+  a.targets = targets;
+  a.part = static_cast<Part*>(ws);
+  a.tgt_x = reinterpret_cast<float*>(a.part + static_cast<size_t>(M) * a.n_tiles);
+  a.tgt_y = a.tgt_x + M;
+  CUtensorMap ax = make_tmap_bf16_2d(Xp, M, K, K, BM, BK);
+  CUtensorMap bx = make_tmap_bf16_2d(Wp, V, K, K, BN, BK);
+  CUtensorMap ay = make_tmap_bf16_2d(Xr, M, K, K, BM, BK);
+  CUtensorMap by = make_tmap_bf16_2d(Wr, V, K, K, BN, BK);
+  const int tiles = ((M + BM - 1) / BM) * a.n_tiles;
+  lmhead_dual_tcgen05<<<std::min(tiles, sm_count()), THREADS, SMEM_BYTES, stream>>>(ax, bx, ay, by, a);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  lmhead_dual_combine<<<(M + 7) / 8, 256, 0, stream>>>(a.part, a.n_tiles, a.tgt_x, a.tgt_y, M, lp_p,
+                                                       lp_r, kl);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrsp
+
+extern "C" size_t mrsp_lmhead_dual_workspace_bytes(int M, int V) {
+  return mrsp::lmhead_dual_workspace_bytes(M, V);
+}
+
+extern "C" mrsp_status mrsp_op_lmhead_dual(const void* X_policy, const void* W_policy,
+                                           const void* X_ref, const void* W_ref, int M, int V, int K,
+                                           const int32_t* targets, float* logprob_policy,
+                                           float* logprob_ref, float* kl, void* workspace,
+                                           size_t ws_bytes, void* stream) {
+  return mrsp::guard([&] {
+    mrsp::require_device();
+    mrsp::lmhead_dual_logprob_kl(X_policy, W_policy, X_ref, W_ref, M, V, K, targets, logprob_policy,
+                                 logprob_ref, kl, workspace, ws_bytes,
+                                 static_cast<cudaStream_t>(stream));
+  });
+}

@@ -195,25 +195,29 @@ class Engine:
             _ptr(lse, ctypes.c_float), 0))
         return (lp, lse) if with_lse else lp
 
-    def step(self, vid: str, pixels, group: Group, use_cache: bool = True, out=None):
-        """run_step: G fetches + policy and reference log-probs. `out` = optional
-        pair of device tensors to receive the log-probs without a D2H copy."""
+    def step(self, vid: str, pixels, group: Group, use_cache: bool = True, out=None,
+             with_kl: bool = False):
+        """run_step: G fetches + policy and reference log-probs (+ exact per-token
+        KL from the fused dual LM head). `out` = optional tuple of device tensors
+        (lp_policy, lp_ref[, kl]) to receive the results without a D2H copy."""
         on_dev = hasattr(pixels, "is_cuda") and pixels.is_cuda
         n = group.scored
         if out is None:
             lp_p = np.zeros(n, dtype=np.float32)
             lp_r = np.zeros(n, dtype=np.float32)
+            kl = np.zeros(n, dtype=np.float32) if with_kl else None
             out_dev = 0
         else:
-            lp_p, lp_r = out
+            lp_p, lp_r = out[0], out[1]
+            kl = out[2] if len(out) > 2 else None
             out_dev = 1
         check(_lib.lib().mrsp_engine_step(
             self._h, vid.encode(), _ptr(pixels, ctypes.c_float), int(pixels.shape[0]), int(on_dev),
             int(use_cache), _ptr(np.ascontiguousarray(group.question)), len(group.question),
             _ptr(np.ascontiguousarray(group.resp)), _ptr(np.ascontiguousarray(group.lengths)),
             int(group.resp.shape[0]), group.Lmax, _ptr(lp_p, ctypes.c_float),
-            _ptr(lp_r, ctypes.c_float), out_dev))
-        return lp_p, lp_r
+            _ptr(lp_r, ctypes.c_float), _ptr(kl, ctypes.c_float), out_dev))
+        return (lp_p, lp_r, kl) if with_kl or (out is not None and len(out) > 2) else (lp_p, lp_r)
 
     def stats(self, reset: bool = False) -> dict:
         out = (ctypes.c_uint64 * 6)()

@@ -155,3 +155,30 @@ def test_full_width_shapes_vs_oracle(gpu):
     d = np.abs(lp - want_lp)
     assert d.max() <= 5e-2 and d.mean() <= 5e-3, (d.max(), d.mean())
     assert np.abs(lse - want_lse).max() <= 5e-2
+
+
+def test_step_exact_kl_vs_oracle(gpu, c1_oracle):
+    """Fused dual LM head inside the step: per-token exact KL(policy || ref)
+    over the full vocabulary vs the oracle's materialised log-softmaxes."""
+    c = T.Cfg.from_any(W1.cfg)
+    eng = E.Engine(W1.cfg, sp=2, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    pix, grp = c1_oracle["pix"], c1_oracle["grp"]
+    lp_p, lp_r, kl = eng.step("vK", pix, grp, with_kl=True)
+    eng.close()
+    emb = c1_oracle["emb"]
+    # oracle: full log-softmax of both models at the scored positions
+    outs = []
+    for seed, pre in ((PSEED, "policy."), (RSEED, "ref.")):
+        W = T.llm_weights(c, seed, pre)
+        _, _, h = T.llm_logprobs(c, W, emb, grp.question, grp.resp, grp.lengths, return_hidden=True)
+        tok, pos, pad, Lp, L = T.pack(emb.shape[0], grp.question, grp.resp, grp.lengths)
+        rows = [Lp + g * grp.Lmax + j for g in range(len(grp.lengths)) for j in range(grp.lengths[g])]
+        logits = T.linear(T.rmsnorm(h[rows], W["final_norm"], c.rms_eps), W["lm_head"])
+        m = logits.max(-1, keepdims=True)
+        outs.append(logits - (m + np.log(np.exp(logits - m).sum(-1, keepdims=True))))
+    a, b = outs
+    want_kl = (np.exp(a) * (a - b)).sum(-1)
+    assert np.abs(lp_p - c1_oracle["lp_p"]).max() <= 5e-2
+    assert np.abs(lp_r - c1_oracle["lp_r"]).max() <= 5e-2
+    d = np.abs(kl - want_kl)
+    assert d.max() <= 5e-2 and d.mean() <= 5e-3, (d.max(), d.mean())

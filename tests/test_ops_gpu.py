@@ -84,3 +84,28 @@ def test_patchify_matches_oracle(gpu):
     want = T.patchify(pix.cpu().numpy(), S, P)
     got = out.float().cpu().numpy()
     assert np.array_equal(got[:, :588], want) and (got[:, 588:] == 0).all()
+
+
+@pytest.mark.parametrize("M,V,K", [(77, 32, 256), (300, 152064, 3584), (1000, 5000, 512)])
+def test_lmhead_dual_logprob_kl(gpu, M, V, K):
+    """Fused policy+reference LM head vs torch fp64: both log-probs and the exact
+    KL(p||q) = sum_v p (log p - log q) (grpo.cpp:94-96)."""
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + V)
+    Xp = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    Xr = (Xp.float() + 0.3 * torch.randn(M, K, device="cuda", generator=g)).bfloat16()
+    Wp = (torch.randn(V, K, device="cuda", generator=g) / K ** 0.5 * 2).bfloat16()
+    Wr = (Wp.float() + 0.2 * torch.randn(V, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32, generator=g)
+    lp_p, lp_r, kl = (torch.empty(M, device="cuda") for _ in range(3))
+    wsb = _lib.lib().mrsp_lmhead_dual_workspace_bytes(M, V)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib().mrsp_op_lmhead_dual(vp(Xp), vp(Wp), vp(Xr), vp(Wr), M, V, K, vp(tgt),
+                                              vp(lp_p), vp(lp_r), vp(kl), vp(ws), wsb, None))
+    a = torch.log_softmax(Xp.double() @ Wp.double().T, -1)
+    b = torch.log_softmax(Xr.double() @ Wr.double().T, -1)
+    want_kl = (a.exp() * (a - b)).sum(-1)
+    torch.cuda.synchronize()
+    assert (lp_p.double() - a.gather(1, tgt.long()[:, None])[:, 0]).abs().max().item() < 2e-3
+    assert (lp_r.double() - b.gather(1, tgt.long()[:, None])[:, 0]).abs().max().item() < 2e-3
+    assert (kl.double() - want_kl).abs().max().item() < 2e-3 + 1e-3 * want_kl.abs().max().item()
+    assert (kl >= -1e-4).all()
