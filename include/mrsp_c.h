@@ -149,6 +149,16 @@ mrsp_status mrsp_op_lmhead_dual(const void* X_policy, const void* W_policy, cons
                                 float* logprob_policy, float* logprob_ref, float* kl,
                                 void* workspace, size_t ws_bytes, void* stream);
 
+/* GRPO token terms (evaluate_from_logits, grpo.cpp:68-108) over per-token
+ * device vectors in (rollout, position) order: log pi_theta(y), log pi_old(y),
+ * log pi_ref(y) (sampled_kl) or the exact per-token KL (from
+ * mrsp_op_lmhead_dual), per-rollout advantages and lengths. out4 (device,
+ * fp64) = [objective, mean_kl, clip_fraction, token_count]. */
+mrsp_status mrsp_op_grpo_stats(const float* logprob, const float* old_logprob,
+                               const float* ref_logprob, const float* kl, const float* advantages,
+                               const int32_t* lengths, int G, double clip_eps, double kl_beta,
+                               int sampled_kl, double* out4, void* stream);
+
 /* RMSNorm (Qwen2): out[i] = bf16(w * x[rows ? rows[i] : i] * rsqrt(mean(x^2) + eps)),
  * x fp32 [.][ldx], out bf16 [n][ldo]. */
 mrsp_status mrsp_op_rmsnorm(const float* x, int ldx, const float* w, void* out, int ldo, int n,

@@ -14,6 +14,7 @@
 
 #include "json.hpp"
 #include "lvrl/engine.hpp"
+#include "lvrl/grpo.hpp"
 
 using namespace lvrl;
 using json = nlohmann::ordered_json;
@@ -115,6 +116,48 @@ int main(int argc, char** argv) {
                         {"gather_bytes", group.stats().gather_bytes.load()}});
     }
     j["cache_script"] = script;
+  }
+
+  // GRPO token terms (grpo.cpp:68-108) on a sampled group: per-token inputs
+  // from the public API + the reference's own GroupStats, exact and sampled KL.
+  {
+    policy::PolicyDims dims{32, 8, 12, 16};
+    auto theta = policy::PolicyParams::random(dims, 17, 0.4);
+    auto ref = policy::PolicyParams::random(dims, 18, 0.4);
+    auto enc = policy::EncoderParams::generate(1, 8, 16);
+    auto video = mmseq::gen_video(3, 8, 16);
+    auto sample = mmseq::gen_task(video, mmseq::TaskFamily::ArgmaxChannel);
+    auto seq = mmseq::build_sequence(mrsp::serial_encode(enc, video), sample);
+    auto theta_old = policy::PolicyParams::random(dims, 19, 0.4);  // ratios != 1
+    Rng rng(6);
+    grpo::RolloutGroup group;
+    Vec rewards;
+    for (int i = 0; i < 6; ++i) {
+      auto r = policy::sample_rollout(theta_old, seq, 1.0, 12, rng);
+      rewards.push_back(rng.uniform());
+      group.rollouts.push_back(std::move(r));
+    }
+    group.advantages = grpo::compute_advantages(rewards, 1e-8);
+    json rolls = json::array();
+    for (const auto& r : group.rollouts) {
+      rolls.push_back({{"tokens", r.tokens},
+                       {"old_logprobs", r.old_logprobs},
+                       {"logprobs", policy::sequence_logprobs(theta, seq, r.tokens)},
+                       {"ref_logprobs", policy::sequence_logprobs(ref, seq, r.tokens)},
+                       {"kl", policy::kl_per_position(theta, ref, seq, r.tokens)}});
+    }
+    grpo::GrpoConfig cfg;
+    grpo::GroupStats exact, sampled;
+    grpo::grpo_objective(group, theta, ref, seq, cfg, &exact);
+    cfg.sampled_kl = true;
+    grpo::grpo_objective(group, theta, ref, seq, cfg, &sampled);
+    auto st = [](const grpo::GroupStats& g) {
+      return json{{"objective", g.objective}, {"mean_kl", g.mean_kl},
+                  {"clip_fraction", g.clip_fraction}, {"token_count", g.token_count}};
+    };
+    j["grpo"] = {{"rollouts", rolls}, {"advantages", group.advantages.values},
+                 {"clip_eps", cfg.clip_eps}, {"kl_beta", cfg.kl_beta},
+                 {"stats_exact_kl", st(exact)}, {"stats_sampled_kl", st(sampled)}};
   }
 
   std::ofstream(path) << j.dump(1) << "\n";

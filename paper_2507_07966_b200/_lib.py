@@ -91,6 +91,7 @@ _sig("mrsp_engine_encode", [_V, ctypes.c_char_p, _V, _I, _I, _I, _V])
 _sig("mrsp_engine_prefill_logprobs", [_V, ctypes.c_char_p, _V, _I, _V, _V, _I, _I, _I, _V, _V, _I])
 _sig("mrsp_engine_step", [_V, ctypes.c_char_p, _V, _I, _I, _I, _V, _I, _V, _V, _I, _I, _V, _V, _V, _I])
 _sig("mrsp_lmhead_dual_workspace_bytes", [_I, _I], ctypes.c_size_t)
+_sig("mrsp_op_grpo_stats", [_V, _V, _V, _V, _V, _V, _I, ctypes.c_double, ctypes.c_double, _I, _V, _V])
 _sig("mrsp_op_lmhead_dual", [_V, _V, _V, _V, _I, _I, _I, _V, _V, _V, _V, _V, ctypes.c_size_t, _V])
 _sig("mrsp_engine_stats", [_V, _V, _I])
 _sig("mrsp_engine_cache", [_V, _I, _I, _V])

@@ -109,3 +109,24 @@ def test_lmhead_dual_logprob_kl(gpu, M, V, K):
     assert (lp_r.double() - b.gather(1, tgt.long()[:, None])[:, 0]).abs().max().item() < 2e-3
     assert (kl.double() - want_kl).abs().max().item() < 2e-3 + 1e-3 * want_kl.abs().max().item()
     assert (kl >= -1e-4).all()
+
+
+def test_grpo_stats_vs_reference(gpu):
+    """Device GRPO token terms vs the reference's own GroupStats (golden)."""
+    import json
+    import pathlib
+    gold = json.loads((pathlib.Path(__file__).parent / "golden" / "ref_toy.json").read_text())["grpo"]
+    r = gold["rollouts"]
+    cat = lambda k: torch.tensor([v for x in r for v in x[k]], dtype=torch.float32, device="cuda")
+    lp, old, ref, kl = cat("logprobs"), cat("old_logprobs"), cat("ref_logprobs"), cat("kl")
+    adv = torch.tensor(gold["advantages"], dtype=torch.float32, device="cuda")
+    lens = torch.tensor([len(x["tokens"]) for x in r], dtype=torch.int32, device="cuda")
+    for key, sampled in (("stats_exact_kl", 0), ("stats_sampled_kl", 1)):
+        out = torch.zeros(4, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().mrsp_op_grpo_stats(vp(lp), vp(old), vp(ref), vp(kl), vp(adv), vp(lens),
+                                                 len(r), gold["clip_eps"], gold["kl_beta"], sampled,
+                                                 vp(out), None))
+        o = out.cpu().tolist()
+        want = gold[key]
+        assert o[3] == want["token_count"] and abs(o[2] - want["clip_fraction"]) < 1e-12
+        assert abs(o[0] - want["objective"]) < 1e-5 and abs(o[1] - want["mean_kl"]) < 1e-5

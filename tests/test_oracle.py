@@ -89,3 +89,19 @@ def test_glibc_tanh_model():
                     "-lm"], check=True)
     r = subprocess.run([str(exe), "2000000"], check=True, capture_output=True, text=True)
     assert r.stdout.strip().endswith("mismatches 0"), r.stdout
+
+
+def test_grpo_stats_oracle_vs_reference():
+    """oracle/grpo.py reproduces the reference's GroupStats (grpo_objective)."""
+    from oracle import grpo
+    g = GOLD["grpo"]
+    r = g["rollouts"]
+    for key, sampled in (("stats_exact_kl", False), ("stats_sampled_kl", True)):
+        got = grpo.group_stats([x["logprobs"] for x in r], [x["old_logprobs"] for x in r],
+                               [x["ref_logprobs"] for x in r], [x["kl"] for x in r],
+                               g["advantages"], g["clip_eps"], g["kl_beta"], sampled)
+        want = g[key]
+        assert got["token_count"] == want["token_count"]
+        assert got["clip_fraction"] == want["clip_fraction"]
+        assert abs(got["objective"] - want["objective"]) < 1e-12
+        assert abs(got["mean_kl"] - want["mean_kl"]) < 1e-12
