@@ -1,5 +1,8 @@
-"""Attention throughput probe (CUDA events) — dev tool."""
-import sys, pathlib, json, math
+"""Attention throughput probe (CUDA events) — dev tool.
+
+  python tools/attn_perf.py [poly ...]   # sweep MRSP_ATTN_POLY values
+"""
+import sys, pathlib, json, math, os
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import torch
 from paper_2507_07966_b200 import ops
@@ -20,7 +23,12 @@ def bench(L, nq, nkv, Lp=None, Lmax=0, iters=5):
     return dict(L=L, nq=nq, nkv=nkv, Lp=Lp_, Lmax=Lmax, ms=round(ms, 3), tflops=round(flops / ms / 1e9, 1))
 
 if __name__ == "__main__":
-    print(json.dumps(bench(16384, 28, 4)), flush=True)
-    print(json.dumps(bench(32768, 28, 4)), flush=True)
-    print(json.dumps(bench(16421 + 8 * 1024, 28, 4, 16421, 1024)), flush=True)
-    print(json.dumps(bench(131109 + 8 * 1011, 28, 4, 131109, 1011, iters=2)), flush=True)
+    polys = sys.argv[1:] or [os.environ.get("MRSP_ATTN_POLY", "")]
+    for p in polys:
+        if p:
+            os.environ["MRSP_ATTN_POLY"] = p
+        for args in [(16384, 28, 4), (32768, 28, 4), (16421 + 8 * 1024, 28, 4, 16421, 1024),
+                     (131109 + 8 * 1011, 28, 4, 131109, 1011)]:
+            r = bench(*args, iters=2 if args[0] > 100000 else 5)
+            r["poly"] = p
+            print(json.dumps(r), flush=True)
