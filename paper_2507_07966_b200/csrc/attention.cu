@@ -12,8 +12,8 @@
 //
 // Softmax (thread = query row): tcgen05.ld of the 128 scores, row max on the
 // raw scores (8 independent chains), p = exp2(s*scale - m) with packed
-// FFMA2 / FADD2 (fp32x2) arithmetic and MUFU.EX2 (a degree-3 FMA-pipe exp2 is
-// available as kPoly but measured slower here); O is rescaled in TMEM only when the
+// FFMA2 / FADD2 (fp32x2) arithmetic and MUFU.EX2 (a packed degree-3 FMA-pipe
+// exp2 is available as kPoly but measured no faster here); O is rescaled in TMEM only when the
 // running max grows by > 2^8 (lazy rescale, warp-uniform because tcgen05.ld/st
 // are warp-collective). Registers rebalanced with setmaxnreg (TMA/MMA
 // warpgroup 56, softmax warpgroups 200).
@@ -573,739 +573,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-// ============================================================================
-// v3: one 128-query tile per CTA, S triple-buffered in TMEM, two softmax
-// warpgroups splitting every S tile's 128 keys 64/64.
-//
-// Why (profiles/r1_attention_v3.md): in v2 every query tile's softmax is
-// serialised with its own P.V -> S MMA round trip (S and P share 128 TMEM
-// columns), so a tile can only start its next softmax ~1.1k cycles of MMA
-// after finishing the last one; traced period 3.5k cycles per KV tile against
-// 2.05k of tensor work. Here TMEM holds O (128 columns) and THREE S buffers, so
-// S(j+1), S(j+2) are computed while the softmax works on S(j) and the softmax
-// warps never wait for the P.V round trip; only throughput matters. Each
-// softmax thread owns one row and 64 of the 128 keys (warps 4-7: keys 0-63,
-// warps 8-11: keys 64-127), the two halves exchange their row max through
-// shared memory (one 64-thread named barrier per TMEM lane quadrant), so two
-// warps per SM sub-partition overlap their exp latency (a lone warp's
-// exp loop is latency-bound at ~570 clk per 64 elements, measured).
-// P(j) is written over the first 64 columns of S(j)'s buffer (each warpgroup
-// its 32 packed columns); S(j+3) reuses the buffer after P.V(j) in MMA order.
-// MMA order: S0 S1 S2 | PV0 S3 | PV1 S4 | ...; the K/V ring is filled in
-// the same order (K0 K1 K2 V0 K3 V1 K4 ...).
-// ============================================================================
-namespace v3 {
-constexpr int RING = 5;
-constexpr int NS = 3;                           // S buffers
-constexpr int OFF_Q = 0;                        // one 128 x 128 Q tile
-constexpr int OFF_RING = OFF_Q + TILE;
-constexpr int OFF_X = OFF_RING + RING * TILE;   // row max [2 parity][2 wg][128], row sum [2][128]
-constexpr int OFF_BAR = OFF_X + (2 * 2 * 128 + 2 * 128) * 4;
-constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
-}  // namespace v3
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// KV tile range covering the query rows [q0, q0 + span).
-__device__ __forceinline__ void kt_range_span(int q0, int span, const MaskDev& m, int n_kt,
-                                              int& lo, int& hi) {
-  const int qlast = q0 + span - 1;
-  if (m.mode == ATTN_BLOCK_DIAG) {
-    lo = (q0 / m.blk) * m.blk / TK;
-    hi = min(n_kt, ((qlast / m.blk + 1) * m.blk + TK - 1) / TK);
-  } else {
-    lo = 0;
-    hi = min(n_kt, qlast / TK + 1);
-  }
-}
-
-// Next KV tile in [kt, hi) with a visible (query, key) pair for the tile at q0.
-__device__ __forceinline__ int next_tile1(int q0, int& kt, int hi, const MaskDev& m) {
-  for (; kt < hi; ++kt) {
-    const int c = tile_class(q0, kt, m);
-    if (c) return c;
-  }
-  return 0;
-}
-
-template <int kPoly>
-__global__ void __launch_bounds__(THREADS, 1)
-    attn_fwd_v3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
-  constexpr int RING = v3::RING, NS = v3::NS, OFF_Q = v3::OFF_Q, OFF_RING = v3::OFF_RING,
-                OFF_X = v3::OFF_X, OFF_BAR = v3::OFF_BAR;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* r_full = bars + 1;              // [RING]
-  uint64_t* r_empty = r_full + RING;        // [RING]
-  uint64_t* s_full = r_empty + RING;        // [NS]
-  uint64_t* p_full = s_full + NS;           // [NS]
-  // [NS] P.V(j) completes phase j / NS of pv_done[j % NS]: when the softmax
-  // waits for P.V(j) the barrier's previous phase (P.V(j - 3)) is known
-  // complete (S(j) was issued after it), so the parity wait is exact; one
-  // shared barrier could lag two phases behind a fast warp.
-  uint64_t* pv_done = p_full + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NS);
-  float* xmax = reinterpret_cast<float*>(smem + OFF_X);  // [2][2][128]
-  float* xsum = xmax + 2 * 2 * 128;                      // [2][128]
-
-  ATRACE_INIT;
-  const int warp = warp_id();
-  int qt, h;
-  work_item(static_cast<int>(blockIdx.x), a.n_pairs, a.n_heads, a.q_per_kv, qt, h);
-  const int kvh = h / a.q_per_kv;
-  const int q0 = qt * TQ;
-  const int n_kt = (a.mask.L + TK - 1) / TK;
-  int kt_lo, kt_hi;
-  kt_range_span(q0, TQ, a.mask, n_kt, kt_lo, kt_hi);
-
-  if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < RING; ++s) {
-      mbar_init(&r_full[s], 1);
-      mbar_init(&r_empty[s], 1);
-    }
-    for (int b = 0; b < NS; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 256);
-    }
-    for (int b = 0; b < NS; ++b) mbar_init(&pv_done[b], 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // O [0,128), S_b [128 (b+1), 128 (b+2))
-
-  if (warp < 4) {
-    reg_dealloc<96>();
-    if (warp == 0) {
-      if (elect_one()) {
-        mbar_arrive_expect_tx(q_full, TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + OFF_Q + c * CHUNK, &tmQ, q_full, a.q_col0 + h * HD + c * 64, q0);
-        int slot = 0;
-        uint32_t ph = 0;
-        auto load = [&](const CUtensorMap* tm, int col, int k0) {
-          mbar_wait(&r_empty[slot], ph ^ 1);
-          mbar_arrive_expect_tx(&r_full[slot], TILE);
-          uint8_t* dst = smem + OFF_RING + slot * TILE;
-          tma_load_2d(dst, tm, &r_full[slot], col, k0);
-          tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, k0);
-          if (++slot == RING) { slot = 0; ph ^= 1; }
-        };
-        const int kcol = a.k_col0 + kvh * HD, vcol = a.v_col0 + kvh * HD;
-        int ktk = kt_lo, ktv = kt_lo;
-        for (int n = 0; n < NS && next_tile1(q0, ktk, kt_hi, a.mask); ++n, ++ktk)
-          load(&tmK, kcol, ktk * TK);
-        for (; next_tile1(q0, ktv, kt_hi, a.mask); ++ktv) {
-          load(&tmV, vcol, ktv * TK);
-          if (next_tile1(q0, ktk, kt_hi, a.mask)) {
-            load(&tmK, kcol, ktk * TK);
-            ++ktk;
-          }
-        }
-      }
-    } else if (warp == 1) {
-      const uint32_t idesc_s = idesc_bf16_f32(TQ, TK);
-      const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
-      const uint32_t q_addr = smem_u32(smem + OFF_Q);
-      const uint32_t ring_addr = smem_u32(smem + OFF_RING);
-      mbar_wait(q_full, 0);
-      int slot = 0;
-      uint32_t ph = 0;
-      int ns = 0, npv = 0;
-      auto issue_s = [&]() {
-        mbar_wait(&r_full[slot], ph);
-        tc_fence_after();
-        const uint32_t k_addr = ring_addr + slot * TILE;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off = (kk / 4) * CHUNK + (kk % 4) * 32;
-            mma_bf16_ss(tmem + 128 * (1 + ns % NS), sdesc_sw128(q_addr + off),
-                        sdesc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&s_full[ns % NS]);
-          mma_commit(&r_empty[slot]);
-        }
-        __syncwarp();
-        ATRACE(12, ns);
-        if (++slot == RING) { slot = 0; ph ^= 1; }
-        ++ns;
-      };
-      auto issue_pv = [&]() {
-        const int b = npv % NS;
-        mbar_wait(&p_full[b], (npv / NS) & 1);
-        ATRACE(14, npv);
-        mbar_wait(&r_full[slot], ph);
-        tc_fence_after();
-        const uint32_t v_addr = ring_addr + slot * TILE;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < TK / 16; ++kk) {
-            // A = P from TMEM (packed bf16 pairs over S_b's first 64 columns)
-            const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
-            mma_bf16_ts(tmem, tmem + 128 * (1 + b) + kk * 8, bd, idesc_o,
-                        (npv > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&pv_done[b]);
-          mma_commit(&r_empty[slot]);
-        }
-        __syncwarp();
-        if (++slot == RING) { slot = 0; ph ^= 1; }
-        ++npv;
-      };
-      int ktk = kt_lo, ktv = kt_lo;
-      for (int n = 0; n < NS && next_tile1(q0, ktk, kt_hi, a.mask); ++n, ++ktk) issue_s();
-      for (; next_tile1(q0, ktv, kt_hi, a.mask); ++ktv) {
-        issue_pv();
-        if (next_tile1(q0, ktk, kt_hi, a.mask)) {
-          issue_s();
-          ++ktk;
-        }
-      }
-    }
-  } else {
-    reg_alloc<200>();
-    const int w = (warp - 4) >> 2;      // key half of this warpgroup
-    const int qd = warp & 3;            // TMEM lane quadrant
-    const int r = qd * 32 + lane_id();  // query row in the tile
-    const int q = q0 + r;
-    const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
-    const float sl2 = a.scale_log2;
-    int k_end, k_mid, k_lo;
-    if (a.mask.mode == ATTN_BLOCK_DIAG) {
-      k_lo = (q / a.mask.blk) * a.mask.blk;
-      k_mid = 0;
-      k_end = min(k_lo + a.mask.blk, a.mask.L);
-    } else {
-      k_end = min(q + 1, a.mask.L);
-      k_mid = a.mask.Lp;
-      k_lo = q >= a.mask.Lp ? a.mask.Lp + seg_of(q, a.mask) * a.mask.Lmax : 0;
-    }
-    float m_run = -INFINITY, l_run = 0.f;
-    int it = 0;
-    for (int kt = kt_lo;; ++kt) {
-      const int cls = next_tile1(q0, kt, kt_hi, a.mask);
-      if (!cls) break;
-      const int b = it % NS;
-      const uint32_t tS = tmem + 128 * (1 + b) + lane_off;
-      mbar_wait(&s_full[b], (it / NS) & 1);
-      ATRACE(1, it);
-      tc_fence_after();
-      float s[64];
-      {
-        uint32_t r0[32], r1[32];
-        tmem_ld32(tS + 64 * w, r0);
-        tmem_ld32(tS + 64 * w + 32, r1);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          s[j] = __uint_as_float(r0[j]);
-          s[32 + j] = __uint_as_float(r1[j]);
-        }
-      }
-      const int k0 = kt * TK + 64 * w;
-      if (cls == 2) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int base = k0 + 32 * c;
-          const uint32_t vis =
-              lt_bits(k_end, base) & (lt_bits(k_mid, base) | ~lt_bits(k_lo, base));
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (!((vis >> j) & 1u)) s[32 * c + j] = -INFINITY;
-        }
-      }
-      float pm;
-      {
-        float m8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(s[i], s[i + 8]);
-#pragma unroll
-        for (int j = 16; j < 64; j += 16)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], fmaxf(s[j + i], s[j + i + 8]));
-        pm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      }
-      // row max of both key halves: both warpgroups take identical decisions
-      float* xm = xmax + (it & 1) * 256;
-      xm[w * 128 + r] = pm;
-      // the barrier also orders this warpgroup's S loads before the partner's
-      // P stores into the same TMEM columns (tcgen05 fences around the sync)
-      tc_fence_before();
-      named_bar_sync(1 + qd, 64);
-      tc_fence_after();
-      const float mt = fmaxf(pm, xm[(1 - w) * 128 + r]) * sl2;
-      ATRACE(3, it);
-      const bool need = mt > m_run + RESCALE_THRESHOLD;
-      if (__any_sync(0xffffffffu, need) && it > 0) {
-        // O (this warpgroup's 64 columns) must hold every earlier P.V
-        mbar_wait(&pv_done[(it - 1) % NS], ((it - 1) / NS) & 1);
-        tc_fence_after();
-        const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
-        if (need) l_run *= alpha;
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_off + 64 * w + c, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tmem + lane_off + 64 * w + c, o);
-        }
-        tmem_st_wait();
-      }
-      if (need) m_run = mt;
-      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      uint32_t pw[32];  // 64 keys as 32 packed bf16 pairs -> S_b columns [32 w, 32 w + 32)
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float x0, x1;
-        ffma2(x0, x1, s[2 * i], s[2 * i + 1], sl2, sl2, neg_m, neg_m);
-        float p0, p1;
-        if (poly_pair<kPoly>(i)) {
-          exp2_poly2(x0, x1, p0, p1);
-        } else {
-          p0 = exp2_mufu(x0);
-          p1 = exp2_mufu(x1);
-        }
-        fadd2(acc[2 * (i & 3)], acc[2 * (i & 3) + 1], p0, p1);
-        pw[i] = pack_bf16(p0, p1);
-      }
-      tmem_st32(tS + 32 * w, pw);
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&p_full[b]);
-      ATRACE(4, it);
-      l_run += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      ++it;
-    }
-    // epilogue: l = both halves' sums; O / l -> bf16, this warpgroup's 64 columns
-    xsum[w * 128 + r] = l_run;
-    named_bar_sync(1 + qd, 64);
-    const float l_tot = l_run + xsum[(1 - w) * 128 + r];
-    const bool row_ok = q < a.mask.L;
-    __nv_bfloat16* orow = a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD + 64 * w;
-    if (it > 0) {
-      mbar_wait(&pv_done[(it - 1) % NS], ((it - 1) / NS) & 1);
-      tc_fence_after();
-      const float inv_l = l_tot > 0.f ? 1.0f / l_tot : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 64; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + 64 * w + c, o);
-        tmem_ld_wait();
-        if (row_ok) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * inv_l, __uint_as_float(o[2 * j + 1]) * inv_l);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
-      }
-    } else if (row_ok) {
-      for (int c = 0; c < 64; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
-    }
-  }
-  ATRACE_FINISH;
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
-}
-
-// ============================================================================
-// v4: v3's pipeline on a CTA PAIR (cluster of 2, tcgen05 cta_group::2).
-//
-// The pair covers two consecutive 128-query tiles of one head (M = 256 per
-// MMA, 128 rows in each CTA's TMEM). Only the leader issues MMAs. Each CTA's
-// TMA loads HALF of every K tile (64 keys) and HALF of every V tile (64 of
-// the 128 head-dim columns) into its own smem and completes the bytes on the
-// leader's barrier; the MMA reads B split along N across the two CTAs. So
-// each K/V byte is fetched from L2 once per 256 query rows (v3: per 128) and
-// each SM's smem operand traffic is 96 B/clk for S (A 4 KB own Q + B 2 KB
-// half K per 64 clk) and 32 B/clk for P.V, well under the 128 B/clk/SM that
-// caps a single-CTA N=128 ss MMA (measured, tools/ubench/umma_rate.cu).
-// Commits multicast to both CTAs (s_full, pv_done, r_empty); the follower's
-// softmax warps arrive remotely on the leader's p_full. The pair walks the
-// union of both tiles' visible KV tiles; a CTA whose rows see nothing in a
-// tile writes P = 0.
-// ============================================================================
-namespace v4 {
-constexpr int RING = 10;                        // half K / half V tiles
-constexpr int NS = 3;
-constexpr int HALF = 16384;                     // 64 x 128 (K) or 128 x 64 (V) bf16
-constexpr int OFF_Q = 0;                        // this CTA's 128 x 128 Q tile
-constexpr int OFF_RING = OFF_Q + TILE;
-constexpr int OFF_X = OFF_RING + RING * HALF;   // row max [2][2][128], row sum [2][128]
-constexpr int OFF_BAR = OFF_X + (2 * 2 * 128 + 2 * 128) * 4;
-constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 512;  // 41 barriers + TMEM slot
-}  // namespace v4
-
-template <int kPoly>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    attn_fwd_v4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
-  constexpr int RING = v4::RING, NS = v4::NS, HALF = v4::HALF, OFF_Q = v4::OFF_Q,
-                OFF_RING = v4::OFF_RING, OFF_X = v4::OFF_X, OFF_BAR = v4::OFF_BAR;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* q_full = bars;                  // own Q tile landed (TMA bytes)
-  uint64_t* r_full = bars + 1;              // [RING] own half landed (TMA bytes)
-  uint64_t* r_empty = r_full + RING;        // [RING] both CTAs (multicast commit)
-  uint64_t* s_full = r_empty + RING;        // [NS]   both CTAs
-  uint64_t* p_full = s_full + NS;           // [NS]   leader: 16 warp arrivals
-  uint64_t* pv_done = p_full + NS;          // [NS]   both CTAs
-  uint64_t* q_peer = pv_done + NS;          // leader: follower's Q landed (relayed)
-  uint64_t* r_peer = q_peer + 1;            // [RING] leader: follower's half landed (relayed)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_peer + RING);
-  float* xmax = reinterpret_cast<float*>(smem + OFF_X);
-  float* xsum = xmax + 2 * 2 * 128;
-
-  ATRACE_INIT;
-  const int warp = warp_id();
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  int pair, h;
-  work_item(static_cast<int>(blockIdx.x) >> 1, a.n_pairs, a.n_heads, a.q_per_kv, pair, h);
-  const int kvh = h / a.q_per_kv;
-  const int q0p = pair * 2 * TQ;                    // the pair's first query row
-  const int q0 = q0p + static_cast<int>(rank) * TQ;  // this CTA's rows
-  const int n_kt = (a.mask.L + TK - 1) / TK;
-  int kt_lo, kt_hi;
-  kt_range_span(q0p, 2 * TQ, a.mask, n_kt, kt_lo, kt_hi);
-
-  if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&tmQ);
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(q_peer, 1);
-    for (int s = 0; s < RING; ++s) {
-      mbar_init(&r_full[s], 1);
-      mbar_init(&r_empty[s], 1);
-      mbar_init(&r_peer[s], 1);
-    }
-    for (int b = 0; b < NS; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 16);
-      mbar_init(&pv_done[b], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  cluster_sync();  // barrier inits and the pair's TMEM allocation visible cluster-wide
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // O [0,128), S_b [128 (b+1), 128 (b+2)); same in both CTAs
-
-  if (warp < 4) {
-    reg_dealloc<96>();
-    if (warp == 0) {
-      if (elect_one()) {
-        mbar_arrive_expect_tx(q_full, TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + OFF_Q + c * CHUNK, &tmQ, q_full, a.q_col0 + h * HD + c * 64, q0);
-        int slot = 0;
-        uint32_t ph = 0;
-        const int kcol = a.k_col0 + kvh * HD, vcol = a.v_col0 + kvh * HD;
-        int nld = 0;
-        auto load = [&](bool is_v, int k0) {
-          ATRACE(20, nld);
-          mbar_wait(&r_empty[slot], ph ^ 1);
-          ATRACE(21, nld);
-          ++nld;
-          mbar_arrive_expect_tx(&r_full[slot], HALF);
-          uint8_t* dst = smem + OFF_RING + slot * HALF;
-          if (is_v) {  // keys [k0, k0 + 128) x head-dim columns [64 rank, 64 rank + 64)
-            tma_load_2d(dst, &tmV, &r_full[slot], vcol + 64 * static_cast<int>(rank), k0);
-          } else {     // keys [k0 + 64 rank, +64) x all 128 head-dim columns
-            const int kr = k0 + 64 * static_cast<int>(rank);
-            tma_load_2d(dst, &tmK, &r_full[slot], kcol, kr);
-            tma_load_2d(dst + HALF / 2, &tmK, &r_full[slot], kcol + 64, kr);
-          }
-          if (++slot == RING) { slot = 0; ph ^= 1; }
-        };
-        int ktk = kt_lo, ktv = kt_lo;
-        for (int n = 0; n < NS && next_tile(q0p, ktk, kt_hi, a.mask); ++n, ++ktk)
-          load(false, ktk * TK);
-        for (; next_tile(q0p, ktv, kt_hi, a.mask); ++ktv) {
-          load(true, ktv * TK);
-          if (next_tile(q0p, ktk, kt_hi, a.mask)) {
-            load(false, ktk * TK);
-            ++ktk;
-          }
-        }
-      }
-    } else if (warp == 1 && leader) {
-      const uint32_t idesc_s = idesc_bf16_f32(2 * TQ, TK);
-      const uint32_t idesc_o = idesc_bf16_f32_bmn(2 * TQ, HD);
-      const uint32_t q_addr = smem_u32(smem + OFF_Q);
-      const uint32_t ring_addr = smem_u32(smem + OFF_RING);
-      mbar_wait(q_full, 0);
-      mbar_wait(q_peer, 0);
-      int slot = 0;
-      uint32_t ph = 0;
-      int ns = 0, npv = 0;
-      auto issue_s = [&]() {
-        mbar_wait(&r_full[slot], ph);
-        mbar_wait(&r_peer[slot], ph);
-        ATRACE(17, ns);
-        tc_fence_after();
-        const uint32_t k_addr = ring_addr + slot * HALF;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            mma2_bf16_ss(tmem + 128 * (1 + ns % NS),
-                         sdesc_sw128(q_addr + (kk / 4) * CHUNK + (kk % 4) * 32),
-                         sdesc_sw128(k_addr + (kk / 4) * (HALF / 2) + (kk % 4) * 32), idesc_s,
-                         kk > 0 ? 1u : 0u);
-          }
-          mma_commit_pair(&s_full[ns % NS], 3);
-          mma_commit_pair(&r_empty[slot], 3);
-        }
-        __syncwarp();
-        ATRACE(12, ns);
-        if (++slot == RING) { slot = 0; ph ^= 1; }
-        ++ns;
-      };
-      auto issue_pv = [&]() {
-        const int b = npv % NS;
-        mbar_wait(&p_full[b], (npv / NS) & 1);
-        ATRACE(14, npv);
-        mbar_wait(&r_full[slot], ph);
-        mbar_wait(&r_peer[slot], ph);
-        ATRACE(15, npv);
-        tc_fence_after();
-        const uint32_t v_addr = ring_addr + slot * HALF;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < TK / 16; ++kk) {
-            const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, HALF);
-            mma2_bf16_ts(tmem, tmem + 128 * (1 + b) + kk * 8, bd, idesc_o,
-                         (npv > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit_pair(&pv_done[b], 3);
-          mma_commit_pair(&r_empty[slot], 3);
-        }
-        __syncwarp();
-        ATRACE(16, npv);
-        if (++slot == RING) { slot = 0; ph ^= 1; }
-        ++npv;
-      };
-      int ktk = kt_lo, ktv = kt_lo;
-      for (int n = 0; n < NS && next_tile(q0p, ktk, kt_hi, a.mask); ++n, ++ktk) issue_s();
-      for (; next_tile(q0p, ktv, kt_hi, a.mask); ++ktv) {
-        issue_pv();
-        if (next_tile(q0p, ktk, kt_hi, a.mask)) {
-          issue_s();
-          ++ktk;
-        }
-      }
-    } else if (warp == 1) {
-      // follower relay: forward "my half landed" to the leader (the 1-SM TMA
-      // form streams at ~2x the rate of the 2-SM form, tools/ubench/tma_rate.cu)
-      if (elect_one()) {
-        const uint32_t q_peer_l = mapa_shared(smem_u32(q_peer), 0);
-        const uint32_t r_peer_l = mapa_shared(smem_u32(r_peer), 0);
-        mbar_wait(q_full, 0);
-        mbar_arrive_remote(q_peer_l);
-        int slot = 0;
-        uint32_t ph = 0;
-        int n = 0;
-        for (int kt = kt_lo; next_tile(q0p, kt, kt_hi, a.mask); ++kt) n += 2;  // one K + one V each
-        for (int i = 0; i < n; ++i) {
-          mbar_wait(&r_full[slot], ph);
-          mbar_arrive_remote(r_peer_l + slot * 8);
-          if (++slot == RING) { slot = 0; ph ^= 1; }
-        }
-      }
-    }
-  } else {
-    reg_alloc<200>();
-    const int w = (warp - 4) >> 2;      // key half of this warpgroup
-    const int qd = warp & 3;            // TMEM lane quadrant
-    const int r = qd * 32 + lane_id();  // query row in this CTA's tile
-    const int q = q0 + r;
-    const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
-    const float sl2 = a.scale_log2;
-    const uint32_t p_full_leader = mapa_shared(smem_u32(p_full), 0);
-    int k_end, k_mid, k_lo;
-    if (a.mask.mode == ATTN_BLOCK_DIAG) {
-      k_lo = (q / a.mask.blk) * a.mask.blk;
-      k_mid = 0;
-      k_end = min(k_lo + a.mask.blk, a.mask.L);
-    } else {
-      k_end = min(q + 1, a.mask.L);
-      k_mid = a.mask.Lp;
-      k_lo = q >= a.mask.Lp ? a.mask.Lp + seg_of(q, a.mask) * a.mask.Lmax : 0;
-    }
-    float m_run = -INFINITY, l_run = 0.f;
-    int it = 0;
-    for (int kt = kt_lo;; ++kt) {
-      const int both = next_tile(q0p, kt, kt_hi, a.mask);
-      if (!both) break;
-      const int cls = (both >> (2 * rank)) & 3;
-      const int b = it % NS;
-      const uint32_t tS = tmem + 128 * (1 + b) + lane_off;
-      mbar_wait(&s_full[b], (it / NS) & 1);
-      ATRACE(1, it);
-      tc_fence_after();
-      uint32_t pw[32];  // 64 keys as 32 packed bf16 pairs -> S_b columns [32 w, 32 w + 32)
-      if (cls == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pw[i] = 0u;  // no visible key for this tile's rows
-      } else {
-        float s[64];
-        {
-          uint32_t r0[32], r1[32];
-          tmem_ld32(tS + 64 * w, r0);
-          tmem_ld32(tS + 64 * w + 32, r1);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            s[j] = __uint_as_float(r0[j]);
-            s[32 + j] = __uint_as_float(r1[j]);
-          }
-        }
-        const int k0 = kt * TK + 64 * w;
-        if (cls == 2) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int base = k0 + 32 * c;
-            const uint32_t vis =
-                lt_bits(k_end, base) & (lt_bits(k_mid, base) | ~lt_bits(k_lo, base));
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (!((vis >> j) & 1u)) s[32 * c + j] = -INFINITY;
-          }
-        }
-        float pm;
-        {
-          float m8[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) m8[i] = fmaxf(s[i], s[i + 8]);
-#pragma unroll
-          for (int j = 16; j < 64; j += 16)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], fmaxf(s[j + i], s[j + i + 8]));
-          pm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                     fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        }
-        float* xm = xmax + (it & 1) * 256;
-        xm[w * 128 + r] = pm;
-        tc_fence_before();
-        named_bar_sync(1 + qd, 64);
-        tc_fence_after();
-        const float mt = fmaxf(pm, xm[(1 - w) * 128 + r]) * sl2;
-        ATRACE(3, it);
-        const bool need = mt > m_run + RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, need) && it > 0) {
-          mbar_wait(&pv_done[(it - 1) % NS], ((it - 1) / NS) & 1);
-          tc_fence_after();
-          const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
-          if (need) l_run *= alpha;
-#pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_off + 64 * w + c, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-            tmem_st32(tmem + lane_off + 64 * w + c, o);
-          }
-          tmem_st_wait();
-        }
-        if (need) m_run = mt;
-        const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x0, x1;
-          ffma2(x0, x1, s[2 * i], s[2 * i + 1], sl2, sl2, neg_m, neg_m);
-          float p0, p1;
-          if (poly_pair<kPoly>(i)) {
-            exp2_poly2(x0, x1, p0, p1);
-          } else {
-            p0 = exp2_mufu(x0);
-            p1 = exp2_mufu(x1);
-          }
-          fadd2(acc[2 * (i & 3)], acc[2 * (i & 3) + 1], p0, p1);
-          pw[i] = pack_bf16(p0, p1);
-        }
-        l_run += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-      }
-      ATRACE(6, it);
-      tmem_st32(tS + 32 * w, pw);
-      tmem_st_wait();
-      ATRACE(7, it);
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) {  // one arrival per warp on the leader's p_full
-        if (leader)
-          mbar_arrive(&p_full[b]);
-        else
-          mbar_arrive_remote(p_full_leader + b * 8);
-      }
-      ATRACE(4, it);
-      ++it;
-    }
-    xsum[w * 128 + r] = l_run;
-    named_bar_sync(1 + qd, 64);
-    const float l_tot = l_run + xsum[(1 - w) * 128 + r];
-    const bool row_ok = q < a.mask.L;
-    __nv_bfloat16* orow = a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD + 64 * w;
-    if (it > 0) {
-      mbar_wait(&pv_done[(it - 1) % NS], ((it - 1) / NS) & 1);
-      tc_fence_after();
-      const float inv_l = l_tot > 0.f ? 1.0f / l_tot : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 64; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + 64 * w + c, o);
-        tmem_ld_wait();
-        if (row_ok) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * inv_l, __uint_as_float(o[2 * j + 1]) * inv_l);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
-      }
-    } else if (row_ok) {
-      for (int c = 0; c < 64; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
-    }
-  }
-  ATRACE_FINISH;
-  tc_fence_before();
-  cluster_sync();  // every MMA into either CTA's TMEM has completed
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc_pair<TMEM_COLS>(tmem);
-}
-
-constexpr int kDefaultPoly = 8;
-constexpr int kDefaultImpl = 4;
+// FMA-pipe exp2 share: measured no gain at c4 with P in TMEM (1180 TFLOP/s at
+// kPoly 0 vs 1155 at 8, profiles/r1_attention_study.md), so MUFU only.
+constexpr int kDefaultPoly = 0;
 
 }  // namespace
 
@@ -1318,48 +588,28 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
                MRSP_INVALID_ARGUMENT, "attention: bad mask parameters");
   // kPoly (FMA-pipe share of the exp2s) is a tuning knob; MRSP_ATTN_POLY
   // overrides the default for sweeps (tools/attn_perf.py).
-  // Kernel generation (MRSP_ATTN_IMPL: 3 = single-tile triple-buffered,
-  // 2 = two-tile ping-pong) and FMA-pipe exp2 share (MRSP_ATTN_POLY) are
-  // tuning knobs for sweeps (tools/attn_perf.py).
+  // FMA-pipe exp2 share (MRSP_ATTN_POLY) is a tuning knob for sweeps
+  // (tools/attn_perf.py); every instantiation is parity-tested.
   const char* env_poly = std::getenv("MRSP_ATTN_POLY");
-  const char* env_impl = std::getenv("MRSP_ATTN_IMPL");
   const int poly = env_poly ? std::atoi(env_poly) : kDefaultPoly;
-  const int impl = env_impl ? std::atoi(env_impl) : kDefaultImpl;
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, AttnArgs);
-  Kern kern = nullptr;
-  if (impl == 2) {
-    kern = poly == 0 ? attn_fwd_tcgen05<0> : poly == 4 ? attn_fwd_tcgen05<4>
-         : poly == 12 ? attn_fwd_tcgen05<12> : poly == 16 ? attn_fwd_tcgen05<16>
-         : attn_fwd_tcgen05<8>;
-  } else if (impl == 3) {
-    kern = poly == 0 ? attn_fwd_v3<0> : poly == 4 ? attn_fwd_v3<4> : poly == 12 ? attn_fwd_v3<12>
-         : poly == 16 ? attn_fwd_v3<16> : attn_fwd_v3<8>;
-  } else {
-    kern = poly == 0 ? attn_fwd_v4<0> : poly == 4 ? attn_fwd_v4<4> : poly == 12 ? attn_fwd_v4<12>
-         : poly == 16 ? attn_fwd_v4<16> : attn_fwd_v4<8>;
-  }
+  const Kern kern = poly == 4 ? attn_fwd_tcgen05<4> : poly == 8 ? attn_fwd_tcgen05<8>
+                  : poly == 12 ? attn_fwd_tcgen05<12> : poly == 16 ? attn_fwd_tcgen05<16>
+                  : attn_fwd_tcgen05<0>;
   static const bool attr = [] {
     for (auto k : {attn_fwd_tcgen05<0>, attn_fwd_tcgen05<4>, attn_fwd_tcgen05<8>,
                    attn_fwd_tcgen05<12>, attn_fwd_tcgen05<16>})
       MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(SMEM_BYTES)));
-    for (auto k : {attn_fwd_v3<0>, attn_fwd_v3<4>, attn_fwd_v3<8>, attn_fwd_v3<12>,
-                   attn_fwd_v3<16>})
-      MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(v3::SMEM_BYTES)));
-    for (auto k : {attn_fwd_v4<0>, attn_fwd_v4<4>, attn_fwd_v4<8>, attn_fwd_v4<12>,
-                   attn_fwd_v4<16>})
-      MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(v4::SMEM_BYTES)));
     return true;
   }();
   (void)attr;
   CUtensorMap tq = make_tmap_bf16_2d(p.Q, p.L, p.ldq, p.ldq, TQ, 64);
-  CUtensorMap tk = make_tmap_bf16_2d(p.K, p.L, p.ldk, p.ldk, impl == 4 ? TK / 2 : TK, 64);
+  CUtensorMap tk = make_tmap_bf16_2d(p.K, p.L, p.ldk, p.ldk, TK, 64);
   CUtensorMap tv = make_tmap_bf16_2d(p.V, p.L, p.ldv, p.ldv, TK, 64);
   AttnArgs a;
   const int n_q_tiles = (p.L + TQ - 1) / TQ;
-  a.n_pairs = impl == 3 ? n_q_tiles : (n_q_tiles + 1) / 2;  // query-row blocks per head
+  a.n_pairs = (n_q_tiles + 1) / 2;
   a.n_heads = p.n_heads;
   a.q_per_kv = p.q_per_kv;
   a.q_col0 = p.q_col0;
@@ -1370,9 +620,8 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.ldo = p.ldo;
   a.scale_log2 = p.scale * 1.4426950408889634f;
   a.mask = MaskDev{p.mode, p.L, p.Lp, p.Lmax > 0 ? p.Lmax : 1, p.blk > 0 ? p.blk : 1};
-  const int grid = a.n_pairs * a.n_heads * (impl == 4 ? 2 : 1);
-  const size_t smem = impl == 2 ? SMEM_BYTES : impl == 3 ? v3::SMEM_BYTES : v4::SMEM_BYTES;
-  kern<<<grid, THREADS, smem, stream>>>(tq, tk, tv, a);
+  const int grid = a.n_pairs * a.n_heads;
+  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
