@@ -84,39 +84,58 @@ __constant__ float c_inv_freq[64];
 
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int ld, int col0, int n_heads,
                             const int* __restrict__ pos, int n) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (row, i)
-  if (idx >= n * 64) return;
-  const int row = idx >> 6, i = idx & 63;
-  const float ang = __fmul_rn(static_cast<float>(pos[row]), c_inv_freq[i]);
-  float sn, cs;
-  sincosf(ang, &sn, &cs);
-  __nv_bfloat16* base = qkv + static_cast<size_t>(row) * ld + col0;
+  // thread = (row, frequency pair): bf16x2 accesses, one sincos pair reused
+  // over every head of the row
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * 32) return;
+  const int row = idx >> 5, i = (idx & 31) * 2;
+  const float p = static_cast<float>(pos[row]);
+  float sn0, cs0, sn1, cs1;
+  sincosf(__fmul_rn(p, c_inv_freq[i]), &sn0, &cs0);
+  sincosf(__fmul_rn(p, c_inv_freq[i + 1]), &sn1, &cs1);
+  __nv_bfloat16* base = qkv + static_cast<size_t>(row) * ld + col0 + i;
   for (int h = 0; h < n_heads; ++h) {
-    __nv_bfloat16* hp = base + h * 128;
-    const float x1 = __bfloat162float(hp[i]), x2 = __bfloat162float(hp[i + 64]);
-    hp[i] = __float2bfloat16_rn(x1 * cs - x2 * sn);
-    hp[i + 64] = __float2bfloat16_rn(x2 * cs + x1 * sn);
+    __nv_bfloat162* lo = reinterpret_cast<__nv_bfloat162*>(base + h * 128);
+    __nv_bfloat162* hi = reinterpret_cast<__nv_bfloat162*>(base + h * 128 + 64);
+    const float2 a = __bfloat1622float2(*lo), b = __bfloat1622float2(*hi);
+    *lo = __floats2bfloat162_rn(a.x * cs0 - b.x * sn0, a.y * cs1 - b.y * sn1);
+    *hi = __floats2bfloat162_rn(b.x * cs0 + a.x * sn0, b.y * cs1 + a.y * sn1);
   }
 }
 
 // ---- patchify: pixels [F][3][H][W] fp32 -> patches bf16 [F*T][kpad] ----------
 // column c*P*P + ky*P + kx (the conv weight layout [dim][3][P][P]); zero pad.
+// One CTA per (frame, patch row): the 3 x P x W input rows are staged in
+// shared memory with coalesced float4 loads, then the W/P tokens' kpad-wide
+// output rows (contiguous in HBM) are written with coalesced bf16x2 stores.
 __global__ void patchify_kernel(const float* __restrict__ pix, __nv_bfloat16* __restrict__ out,
                                 int F, int H, int W, int P, int kpad) {
-  const int gw = W / P, T = (H / P) * gw, kreal = 3 * P * P;
-  const size_t total = static_cast<size_t>(F) * T * kpad;
-  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int k = static_cast<int>(idx % kpad);
-    const size_t tok = idx / kpad;
-    float v = 0.f;
-    if (k < kreal) {
-      const int f = static_cast<int>(tok / T), t = static_cast<int>(tok % T);
-      const int py = t / gw, px = t % gw;
-      const int c = k / (P * P), ky = (k / P) % P, kx = k % P;
-      v = pix[((static_cast<size_t>(f) * 3 + c) * H + py * P + ky) * W + px * P + kx];
+  extern __shared__ float tile[];  // [3][P][W] staged rows, then [kpad] column -> tile offset
+  const int gh = H / P, gw = W / P, PP = P * P, kreal = 3 * PP;
+  const int f = blockIdx.x / gh, py = blockIdx.x % gh;
+  int* koff = reinterpret_cast<int*>(tile + 3 * P * W);
+  for (int k = threadIdx.x; k < kpad; k += blockDim.x)
+    koff[k] = k < kreal ? ((k / PP) * P + (k / P) % P) * W + k % P : -1;
+  for (int c = 0; c < 3; ++c) {
+    const float* src = pix + ((static_cast<size_t>(f) * 3 + c) * H + py * P) * W;
+    float* dst = tile + c * P * W;
+    if ((W & 3) == 0) {
+      for (int j = threadIdx.x; j < P * W / 4; j += blockDim.x)
+        reinterpret_cast<float4*>(dst)[j] = reinterpret_cast<const float4*>(src)[j];
+    } else {
+      for (int j = threadIdx.x; j < P * W; j += blockDim.x) dst[j] = src[j];
     }
-    out[idx] = __float2bfloat16_rn(v);
+  }
+  __syncthreads();
+  __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(
+      out + (static_cast<size_t>(f) * gh * gw + static_cast<size_t>(py) * gw) * kpad);
+  const int half = kpad / 2;
+  for (int px = 0; px < gw; ++px) {
+    const float* tp = tile + px * P;
+    for (int k2 = threadIdx.x; k2 < half; k2 += blockDim.x) {
+      const int o0 = koff[2 * k2], o1 = koff[2 * k2 + 1];
+      o[px * half + k2] = __floats2bfloat162_rn(o0 >= 0 ? tp[o0] : 0.f, o1 >= 0 ? tp[o1] : 0.f);
+    }
   }
 }
 
@@ -272,7 +291,8 @@ void set_rope_inv_freq(const float* inv_freq64, cudaStream_t s) {
 void rope(__nv_bfloat16* qkv, int ld, int col0, int n_heads, const int* pos, int n,
           cudaStream_t s) {
   if (n <= 0 || n_heads <= 0) return;
-  const int work = n * 64;
+  MRSP_REQUIRE(ld % 2 == 0 && col0 % 2 == 0, MRSP_INVALID_ARGUMENT, "rope: odd leading dim");
+  const int work = n * 32;
   rope_kernel<<<(work + 255) / 256, 256, 0, s>>>(qkv, ld, col0, n_heads, pos, n);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
@@ -282,7 +302,16 @@ void patchify(const float* pix, __nv_bfloat16* out, int F, int H, int W, int P, 
               cudaStream_t s) {
   const size_t total = static_cast<size_t>(F) * (H / P) * (W / P) * kpad;
   if (!total) return;
-  patchify_kernel<<<grid_for(total, 256), 256, 0, s>>>(pix, out, F, H, W, P, kpad);
+  MRSP_REQUIRE(kpad % 2 == 0 && kpad >= 3 * P * P, MRSP_INVALID_ARGUMENT, "patchify: bad kpad");
+  const size_t smem = (static_cast<size_t>(3) * P * W + kpad) * sizeof(float);
+  MRSP_REQUIRE(smem <= 200 * 1024, MRSP_INVALID_ARGUMENT, "patchify: image rows too wide");
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    MRSP_CUDA(cudaFuncSetAttribute(patchify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+    attr = true;
+  }
+  patchify_kernel<<<F * (H / P), 256, smem, s>>>(pix, out, F, H, W, P, kpad);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

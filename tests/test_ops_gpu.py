@@ -75,15 +75,17 @@ def test_rope_matches_oracle(gpu):
     assert (got == want).mean() > 0.97
 
 
-def test_patchify_matches_oracle(gpu):
-    F, S, P = 3, 224, 14
+@pytest.mark.parametrize("F,S,P,kpad", [(3, 224, 14, 592), (5, 64, 8, 192), (2, 30, 6, 112)])
+def test_patchify_matches_oracle(gpu, F, S, P, kpad):
+    # SigLIP (224^2, patch 14, K padded 588 -> 592), c1 (64^2, patch 8), and a
+    # width that is not a multiple of 4 (scalar staging path)
     pix = torch.rand(F, 3 * S * S, device="cuda") * 2 - 1
-    kpad = 592
     out = torch.empty(F * (S // P) ** 2, kpad, device="cuda", dtype=torch.bfloat16)
     _lib.check(_lib.lib().mrsp_op_patchify(vp(pix), vp(out), F, S, S, P, kpad, None))
     want = T.patchify(pix.cpu().numpy(), S, P)
     got = out.float().cpu().numpy()
-    assert np.array_equal(got[:, :588], want) and (got[:, 588:] == 0).all()
+    kreal = 3 * P * P
+    assert np.array_equal(got[:, :kreal], want) and (got[:, kreal:] == 0).all()
 
 
 @pytest.mark.parametrize("M,V,K", [(77, 32, 256), (300, 152064, 3584), (1000, 5000, 512)])
