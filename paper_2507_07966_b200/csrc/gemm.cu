@@ -2,7 +2,8 @@
 //
 //   C[M,N] = epilogue( A[M,K] . B[N,K]^T )      A, B bf16 K-major, fp32 accumulate
 //
-// Roles (256 threads, one CTA per SM, grid = #SMs, static tile schedule):
+// Default kernel: single CTA, 128 x 256 tiles (a CTA-pair variant,
+// gemm_bf16_pair below, is selectable with MRSP_GEMM_IMPL; see kDefaultGemmImpl):
 //   warp 0      TMA producer: A/B 128x64 / 256x64 tiles -> 4-stage smem ring
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma 128x256x16 into
 //               a double-buffered TMEM accumulator (2 x 256 fp32 columns)
@@ -13,12 +14,14 @@
 //
 // Fused epilogues (the LLM / vision layers' elementwise tails, so no separate
 // HBM pass): +bias, +bias then GELU(tanh), SwiGLU over [gate|up] N-halves,
-// fp32 residual accumulate (hidden += A.B^T [+ bias]), plain bf16 / fp32 store.
+// fp32 residual accumulate (hidden += A.B^T [+ bias]), plain bf16 / fp32 store,
+// LM-head log-prob partials.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 #include "gemm.h"
@@ -64,11 +67,145 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
   nt = local / rows;
 }
 
+// Epilogue activations on the SFU (MUFU.TANH / MUFU.EX2 + fast reciprocal):
+// the outputs are rounded to bf16 (rel. 2^-9), far coarser than the
+// approximations' ~2^-11; an IEEE division per element made the SwiGLU
+// epilogue slower than the 128x256x3584 main loop it overlaps.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.0f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+
+// Fused epilogue of one accumulator tile row slice: TMEM row `t_row` (this
+// thread's lane, BN fp32 columns) -> the epilogue op -> global. Shared by the
+// single-CTA and the CTA-pair kernels.
+__device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row, int row,
+                                             bool row_ok, int nt, int n_tiles) {
+  if (args.epi == GEMM_EPI_LOGPROB_PARTIAL) {
+    // Fused vocabulary projection + log-softmax pieces: this 256-wide vocab
+    // tile's (max, sum exp) per row and the target logit if it lies here.
+    // Logits never leave TMEM/registers.
+    const int tgt = row_ok ? args.targets[row] : -1;
+    float m = -INFINITY, ssum = 0.f;
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(t_row + c, r);
+      tmem_ld_wait();
+      const int col = nt * BN + c;
+      float cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < args.N) cm = fmaxf(cm, __uint_as_float(r[j]));
+      const float mn = fmaxf(m, cm);
+      float acc_s = (m == -INFINITY) ? 0.f : ssum * __expf(m - mn);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = __uint_as_float(r[j]);
+        if (col + j < args.N) acc_s += __expf(x - mn);
+        if (col + j == tgt) args.tgt_logit[row] = x;
+      }
+      m = mn;
+      ssum = acc_s;
+    }
+    if (row_ok) args.part[static_cast<size_t>(row) * n_tiles + nt] = make_float2(m, ssum);
+  } else if (args.epi == GEMM_EPI_SWIGLU_BF16) {
+    // columns [0,128) are gate, [128,256) the matching up projections
+    __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
+    for (int c = 0; c < BN / 2; c += 32) {
+      uint32_t g[32], u[32];
+      tmem_ld32(t_row + c, g);
+      tmem_ld32(t_row + BN / 2 + c, u);
+      tmem_ld_wait();
+      const int col = nt * (BN / 2) + c;
+      if (row_ok) {
+        uint32_t o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
+          const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+          o[j] = pack_bf16(a0, a1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + col);
+        if (args.vec_ok && col + 32 <= args.N / 2) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        } else {
+          const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
+          for (int j = 0; j < 32 && col + j < args.N / 2; ++j)
+            C[static_cast<size_t>(row) * args.ldc + col + j] = ob[j];
+        }
+      }
+    }
+  } else {
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(t_row + c, r);
+      tmem_ld_wait();
+      const int col = nt * BN + c;
+      if (row_ok && col < args.N) {  // stores only; the TMEM load above is warp-wide
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      const bool full_chunk = col + 32 <= args.N;
+      const bool vec = full_chunk && args.vec_ok;
+      if (args.bias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (full_chunk || col + j < args.N) v[j] += args.bias[col + j];
+      }
+      if (args.epi == GEMM_EPI_BIAS_GELU_BF16) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+      }
+      if (args.epi == GEMM_EPI_RESID_F32) {
+        float* R = args.resid + static_cast<size_t>(row) * args.ldr + col;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 x = reinterpret_cast<float4*>(R)[j];
+            x.x += v[4 * j]; x.y += v[4 * j + 1]; x.z += v[4 * j + 2]; x.w += v[4 * j + 3];
+            reinterpret_cast<float4*>(R)[j] = x;
+          }
+        } else {
+          for (int j = 0; j < 32 && col + j < args.N; ++j) R[j] += v[j];
+        }
+      } else if (args.epi == GEMM_EPI_STORE_F32) {
+        float* Cf = static_cast<float*>(args.C) + static_cast<size_t>(row) * args.ldc + col;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(Cf)[j] =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+          for (int j = 0; j < 32 && col + j < args.N; ++j) Cf[j] = v[j];
+        }
+      } else {  // bf16 stores: STORE / BIAS / BIAS_GELU
+        __nv_bfloat16* Cb =
+            static_cast<__nv_bfloat16*>(args.C) + static_cast<size_t>(row) * args.ldc + col;
+        uint32_t o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(Cb)[j] =
+                make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        } else {
+          const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
+          for (int j = 0; j < 32 && col + j < args.N; ++j) Cb[j] = ob[j];
+        }
+      }
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
@@ -165,124 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = mt * BM + ew * 32 + lane_id();
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      if (args.epi == GEMM_EPI_LOGPROB_PARTIAL) {
-        // Fused vocabulary projection + log-softmax pieces: this 256-wide vocab
-        // tile's (max, sum exp) per row and the target logit if it lies here.
-        // Logits never leave TMEM/registers.
-        const int tgt = row_ok ? args.targets[row] : -1;
-        float m = -INFINITY, ssum = 0.f;
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(t_row + c, r);
-          tmem_ld_wait();
-          const int col = nt * BN + c;
-          float cm = -INFINITY;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col + j < args.N) cm = fmaxf(cm, __uint_as_float(r[j]));
-          const float mn = fmaxf(m, cm);
-          float acc_s = (m == -INFINITY) ? 0.f : ssum * __expf(m - mn);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(r[j]);
-            if (col + j < args.N) acc_s += __expf(x - mn);
-            if (col + j == tgt) args.tgt_logit[row] = x;
-          }
-          m = mn;
-          ssum = acc_s;
-        }
-        if (row_ok) args.part[static_cast<size_t>(row) * n_tiles + nt] = make_float2(m, ssum);
-      } else if (args.epi == GEMM_EPI_SWIGLU_BF16) {
-        // columns [0,128) are gate, [128,256) the matching up projections
-        __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
-        for (int c = 0; c < BN / 2; c += 32) {
-          uint32_t g[32], u[32];
-          tmem_ld32(t_row + c, g);
-          tmem_ld32(t_row + BN / 2 + c, u);
-          tmem_ld_wait();
-          const int col = nt * (BN / 2) + c;
-          if (row_ok) {
-            uint32_t o[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float a0 = silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
-              const float a1 = silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
-              o[j] = pack_bf16(a0, a1);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + col);
-            if (args.vec_ok && col + 32 <= args.N / 2) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-            } else {
-              const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
-              for (int j = 0; j < 32 && col + j < args.N / 2; ++j)
-                C[static_cast<size_t>(row) * args.ldc + col + j] = ob[j];
-            }
-          }
-        }
-      } else {
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(t_row + c, r);
-          tmem_ld_wait();
-          const int col = nt * BN + c;
-          if (row_ok && col < args.N) {  // stores only; the TMEM load above is warp-wide
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          const bool full_chunk = col + 32 <= args.N;
-          const bool vec = full_chunk && args.vec_ok;
-          if (args.bias) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (full_chunk || col + j < args.N) v[j] += args.bias[col + j];
-          }
-          if (args.epi == GEMM_EPI_BIAS_GELU_BF16) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
-          }
-          if (args.epi == GEMM_EPI_RESID_F32) {
-            float* R = args.resid + static_cast<size_t>(row) * args.ldr + col;
-            if (vec) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                float4 x = reinterpret_cast<float4*>(R)[j];
-                x.x += v[4 * j]; x.y += v[4 * j + 1]; x.z += v[4 * j + 2]; x.w += v[4 * j + 3];
-                reinterpret_cast<float4*>(R)[j] = x;
-              }
-            } else {
-              for (int j = 0; j < 32 && col + j < args.N; ++j) R[j] += v[j];
-            }
-          } else if (args.epi == GEMM_EPI_STORE_F32) {
-            float* Cf = static_cast<float*>(args.C) + static_cast<size_t>(row) * args.ldc + col;
-            if (vec) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-                reinterpret_cast<float4*>(Cf)[j] =
-                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            } else {
-              for (int j = 0; j < 32 && col + j < args.N; ++j) Cf[j] = v[j];
-            }
-          } else {  // bf16 stores: STORE / BIAS / BIAS_GELU
-            __nv_bfloat16* Cb =
-                static_cast<__nv_bfloat16*>(args.C) + static_cast<size_t>(row) * args.ldc + col;
-            uint32_t o[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) o[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
-            if (vec) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                reinterpret_cast<uint4*>(Cb)[j] =
-                    make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-            } else {
-              const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
-              for (int j = 0; j < 32 && col + j < args.N; ++j) Cb[j] = ob[j];
-            }
-          }
-          }
-        }
-      }
+      epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -294,6 +314,169 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
 }
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2): a 256 x 256 tile per
+// pair, M = 256 MMAs issued by the leader into both CTAs' TMEM. Each CTA TMA-
+// loads its own 128 rows of A and its 128-row half of B (N), so per SM the
+// smem operand reads drop from 96 B/clk (128x256 single-CTA tile: A 4 KB + B
+// 8 KB per 128-clk MMA) to 64 B/clk and the TMA writes from 94 to 64 B/clk,
+// under the 128 B/clk/SM smem port (tools/ubench/umma_rate.cu). Epilogue per
+// CTA as in the single-CTA kernel (each CTA holds 128 rows x 256 columns).
+// kRelay: each CTA's TMA completes on its own barrier and the follower's warp
+// 3 forwards "stage landed" to the leader (instead of the 2-SM TMA form).
+constexpr int P_STAGES = 6;
+constexpr int P_HALF = BM * BK * 2;           // 16 KB: 128 rows x 64 K
+constexpr int P_STAGE_BYTES = 2 * P_HALF;     // own A + own half of B
+constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + 512;
+
+template <bool kRelay>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   EpiArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;   // both CTAs: multicast MMA commit
+  uint64_t* peer = empty + P_STAGES;   // leader: follower's stage landed (relay)
+  uint64_t* tfull = peer + P_STAGES;   // [2] both CTAs: multicast MMA commit
+  uint64_t* tempty = tfull + 2;        // [2] leader: 4 local + 4 remote epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int m_tiles = (args.M + 2 * BM - 1) / (2 * BM);
+  const int n_tiles = (args.N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = (args.K + BK - 1) / BK;
+  const int cl = static_cast<int>(blockIdx.x) >> 1, n_cl = static_cast<int>(gridDim.x) >> 1;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&peer[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cl; tile < num_tiles; tile += n_cl) {
+        int mt, nt;
+        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        const int arow = mt * 2 * BM + static_cast<int>(rank) * BM;
+        const int brow = nt * BN + static_cast<int>(rank) * BM;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * P_STAGE_BYTES;
+          if (kRelay) {
+            mbar_arrive_expect_tx(&full[stage], P_STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, arow);
+            tma_load_2d(sa + P_HALF, &tmB, &full[stage], kb * BK, brow);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+            tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, arow);
+            tma_load_2d_2sm(sa + P_HALF, &tmB, &full[stage], kb * BK, brow);
+          }
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 && leader) {
+    const uint32_t idesc = idesc_bf16_f32(2 * BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cl; tile < num_tiles; tile += n_cl) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        if (kRelay) mbar_wait(&peer[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_addr = smem_u32(smem + stage * P_STAGE_BYTES);
+          const uint32_t b_addr = a_addr + P_HALF;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma2_bf16_ss(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
+                         (kb | k) != 0);
+          mma_commit_pair(&empty[stage], 3);
+          if (kb == k_blocks - 1) mma_commit_pair(&tfull[acc], 3);
+        }
+        __syncwarp();
+        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (kRelay && warp == 3 && !leader) {
+    if (elect_one()) {  // forward this CTA's "stage landed" to the leader
+      const uint32_t peer_l = mapa_shared(smem_u32(peer), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cl; tile < num_tiles; tile += n_cl)
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_arrive_remote(peer_l + stage * 8);
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const uint32_t tempty_l = mapa_shared(smem_u32(tempty), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cl; tile < num_tiles; tile += n_cl) {
+      int mt, nt;
+      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mt * 2 * BM + static_cast<int>(rank) * BM + ew * 32 + lane_id();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      epilogue_row(args, t_row, row, row < args.M, nt, n_tiles);
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) {
+        if (leader)
+          mbar_arrive(&tempty[acc]);
+        else
+          mbar_arrive_remote(tempty_l + acc * 8);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+}
+
+// Measured: in isolation the relayed CTA pair is the fastest on every LLM
+// shape (tools/gemm_perf.py, interleaved: 16384x3584x3584 1219 vs 895
+// TFLOP/s, SwiGLU 16384x37888x3584 1454 vs 1267), but inside the c4 step it
+// draws the B200 deeper into its power cap: median SM clock 1500 -> 1400 MHz,
+// GEMMs -80 ms, the attention that follows every GEMM +590 ms, step -4.5%
+// (tools/ab_gemm.sh, same box). The single-CTA kernel is the default.
+constexpr int kDefaultGemmImpl = 1;
 
 int num_sms() {
   static int n = [] {
@@ -333,6 +516,32 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   if (g.epi == GEMM_EPI_LOGPROB_PARTIAL)
     MRSP_REQUIRE(g.targets && g.part && g.tgt_logit, MRSP_INVALID_ARGUMENT,
                  "gemm logprob: null targets/partials");
+  // kernel choice (MRSP_GEMM_IMPL): 1 = single-CTA 128x256 tiles, 2 = CTA pair
+  // with the 2-SM TMA form, 3 = CTA pair with relayed stage completion
+  const char* env_impl = std::getenv("MRSP_GEMM_IMPL");
+  const int impl = env_impl ? std::atoi(env_impl) : kDefaultGemmImpl;
+  if (impl == 2 || impl == 3) {
+    static const bool pair_attr = [] {
+      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(P_SMEM_BYTES)));
+      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(P_SMEM_BYTES)));
+      return true;
+    }();
+    (void)pair_attr;
+    CUtensorMap tbh = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BM, BK);  // 128-row halves of B
+    const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
+    const int grid = 2 * std::min(tiles, num_sms() / 2);
+    if (impl == 3)
+      gemm_bf16_pair<true><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, e);
+    else
+      gemm_bf16_pair<false><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, e);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    return;
+  }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = std::min(tiles, num_sms());
   gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, e);

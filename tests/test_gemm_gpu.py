@@ -7,6 +7,14 @@ from paper_2507_07966_b200 import ops
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["1", "2", "3"], autouse=True)
+def gemm_impl(request, monkeypatch):
+    """Every kernel variant (MRSP_GEMM_IMPL): single CTA, CTA pair with the
+    2-SM TMA form, CTA pair with relayed stage completion."""
+    monkeypatch.setenv("MRSP_GEMM_IMPL", request.param)
+    return request.param
+
+
 def ref(A, B):
     return A.float() @ B.float().T
 

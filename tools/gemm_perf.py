@@ -23,7 +23,20 @@ def bench(M, N, K, epi=ops.EPI_STORE_BF16, iters=20):
     ms2 = s.elapsed_time(e) / iters
     return dict(M=M, N=N, K=K, epi=epi, ms=round(ms, 4), tflops=round(tf, 1), cublas_tflops=round(2*M*N*K/ms2/1e9, 1))
 
+SHAPES = [(8192, 8192, 8192, 0), (16384, 4608, 3584, 0), (16384, 3584, 3584, 0),
+          (16384, 37888, 3584, 0), (16384, 3584, 18944, 0), (65536, 1152, 4608, 0),
+          (16384, 37888, 3584, 4)]
+
+
 if __name__ == "__main__":
-    for shp in [(8192, 8192, 8192), (16384, 4608, 3584), (16384, 3584, 3584), (16384, 37888, 3584), (16384, 3584, 18944), (65536, 1152, 4608)]:
-        print(json.dumps(bench(*shp)), flush=True)
-    print(json.dumps(bench(16384, 37888, 3584, ops.EPI_SWIGLU_BF16)), flush=True)
+    import os
+    impls = sys.argv[1:] or [os.environ.get("MRSP_GEMM_IMPL", "1")]
+    # impls interleaved per shape (clocks drift under the power cap)
+    for M, N, K, epi in SHAPES:
+        row = {"M": M, "N": N, "K": K, "epi": epi}
+        for impl in impls:
+            os.environ["MRSP_GEMM_IMPL"] = impl
+            r = bench(M, N, K, epi)
+            row[f"impl{impl}"] = r["tflops"]
+            row[f"cublas_after_{impl}"] = r["cublas_tflops"]
+        print(json.dumps(row), flush=True)
