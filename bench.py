@@ -354,7 +354,10 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "attention_dram_bytes.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            # the capture is one launch of a given workload at SP = 1
+            if tj.get("workload") == w.name and tj.get("world", 1) == world:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "attn_fwd_tcgen05 (LLM layer attention)",
