@@ -112,7 +112,10 @@ typedef enum {
   GEMM_EPI_SWIGLU_BF16 = 4,    /* per 256-col tile [gate128|up128]:
                                   C[:, tile*128 + j] = silu(g_j) * u_j      */
   GEMM_EPI_STORE_F32 = 5,      /* C(fp32) = A.B^T (+ bias)                  */
-  GEMM_EPI_LOGPROB_PARTIAL = 6 /* internal: LM-head tile (max, sumexp, target) */
+  GEMM_EPI_LOGPROB_PARTIAL = 6, /* internal: LM-head tile (max, sumexp, target) */
+  GEMM_EPI_QKV_SCATTER = 7      /* internal: +bias, bf16, RoPE on q/k heads, each 128-col
+                                   head block stored to its owner rank(s) (fused Ulysses
+                                   sequence -> head all-to-all)                           */
 } mrsp_gemm_epilogue;
 
 /* tcgen05 BF16 GEMM, fp32 accumulate: A[M][lda], B[N][ldb] (both K-major),

@@ -115,7 +115,18 @@ struct AttnArgs {
   int ldo;
   float scale_log2;
   MaskDev mask;
+  int n_dst, dst_ld, dst_col0;  // fused O scatter (AttnParams)
+  long dst_bounds[9];
+  __nv_bfloat16* dst_base[8];
 };
+
+// Destination row of query row q, head h: O itself, or the owner shard's buffer.
+__device__ __forceinline__ __nv_bfloat16* out_row(const AttnArgs& a, int q, int h) {
+  if (a.n_dst == 0) return a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD;
+  int p = 0;
+  while (p + 1 < a.n_dst && q >= a.dst_bounds[p + 1]) ++p;
+  return a.dst_base[p] + static_cast<size_t>(q - a.dst_bounds[p]) * a.dst_ld + a.dst_col0 + h * HD;
+}
 
 // Work order: KV-head-major, then query-row blocks heaviest (longest KV sweep)
 // first, then the q_per_kv query heads sharing that KV head. Every CTA of a
@@ -541,7 +552,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // epilogue: O / l -> bf16 global
     const bool row_ok = q < a.mask.L;
-    __nv_bfloat16* orow = a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD;
+    __nv_bfloat16* orow = row_ok ? out_row(a, q, h) : nullptr;
     if (it > 0) {
       mbar_wait(&pv_done[t], (it - 1) & 1);
       tc_fence_after();
@@ -620,6 +631,12 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.ldo = p.ldo;
   a.scale_log2 = p.scale * 1.4426950408889634f;
   a.mask = MaskDev{p.mode, p.L, p.Lp, p.Lmax > 0 ? p.Lmax : 1, p.blk > 0 ? p.blk : 1};
+  MRSP_REQUIRE(p.n_dst >= 0 && p.n_dst <= 8, MRSP_INVALID_ARGUMENT, "attention: <= 8 shards");
+  a.n_dst = p.n_dst;
+  a.dst_ld = p.dst_ld;
+  a.dst_col0 = p.dst_col0;
+  for (int i = 0; i < 9; ++i) a.dst_bounds[i] = p.dst_bounds[i];
+  for (int i = 0; i < 8; ++i) a.dst_base[i] = static_cast<__nv_bfloat16*>(p.dst_base[i]);
   const int grid = a.n_pairs * a.n_heads;
   kern<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
   count_launch();

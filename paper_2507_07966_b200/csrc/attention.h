@@ -19,6 +19,14 @@ struct AttnParams {
   int L, n_heads, q_per_kv;
   float scale;
   int mode, Lp, Lmax, blk;
+  // Optional fused Ulysses head -> sequence all-to-all: when n_dst > 0, row q
+  // of head h is stored to dst_base[p] + (q - dst_bounds[p]) * dst_ld +
+  // dst_col0 + 128 h for the shard p with dst_bounds[p] <= q < dst_bounds[p+1]
+  // (peer GPUs' buffers over NVLink, or virtual ranks') instead of O.
+  int n_dst = 0;
+  long dst_bounds[9] = {};
+  void* dst_base[8] = {};
+  int dst_ld = 0, dst_col0 = 0;
 };
 
 void attention_fwd(const AttnParams& p, cudaStream_t stream);

@@ -156,8 +156,47 @@ Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n
   for (int i = 0; i < 64; ++i)
     inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(cfg.rope_theta), (2.0 * i) / 128.0));
   set_rope_inv_freq(inv, stream_);
+  build_routes(inv);
   init_weights(vision_seed, policy_seed, ref_seed, with_ref);
   MRSP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// Route of every 128-column head block of a sequence-shard QKV row to the SP
+// rank(s) owning that head (a kv head has two owners when SP > n_kv), as
+// (rank, destination column) — the static part of the fused all-to-all.
+void Engine::build_routes(const float* inv_freq) {
+  const int nq = cfg_.n_q_heads, nkv = cfg_.n_kv_heads, nblk = nq + 2 * nkv;
+  MRSP_REQUIRE(k_ <= 8, MRSP_INVALID_ARGUMENT, "engine: SP degree <= 8");
+  std::vector<int2> route(2 * nblk, make_int2(-1, 0));
+  std::vector<int> ld(8, 0);
+  auto add = [&](int hb, int rank, int col) {
+    int2* r = &route[2 * hb];
+    MRSP_REQUIRE(r[1].x < 0, MRSP_INVALID_ARGUMENT, "ulysses: a head block with > 2 owners");
+    if (r[0].x < 0) r[0] = make_int2(rank, col);
+    else r[1] = make_int2(rank, col);
+  };
+  if (k_ == 1) {
+    for (int hb = 0; hb < nblk; ++hb) add(hb, 0, hb * 128);
+    ld[0] = nblk * 128;
+  } else {
+    for (int p = 0; p < k_; ++p) {
+      const HeadSplit hs = head_split(nq, nkv, k_, p);
+      ld[p] = (hs.nq() + 2 * hs.nkv()) * 128;
+      if (hs.nq() == 0) continue;  // no query head: never reads K/V (SP > n_q / q_per_kv)
+      for (const auto& blk : ulysses_blocks(nq, nkv, hs))
+        for (int c = 0; c < blk[2]; c += 128) add((blk[0] + c) / 128, p, blk[1] + c);
+    }
+  }
+  const size_t off_route = 256, off_ld = off_route + route.size() * sizeof(int2);
+  const size_t off_base = (off_ld + 8 * sizeof(int) + 15) & ~size_t(15);
+  uint8_t* base = static_cast<uint8_t*>(route_buf_.ensure(off_base + 8 * sizeof(void*)));
+  d_inv_freq_ = reinterpret_cast<float*>(base);
+  d_route_ = reinterpret_cast<int2*>(base + off_route);
+  d_peer_ld_ = reinterpret_cast<int*>(base + off_ld);
+  d_peer_base_ = reinterpret_cast<void**>(base + off_base);
+  MRSP_CUDA(cudaMemcpy(d_inv_freq_, inv_freq, 64 * sizeof(float), cudaMemcpyHostToDevice));
+  MRSP_CUDA(cudaMemcpy(d_route_, route.data(), route.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  MRSP_CUDA(cudaMemcpy(d_peer_ld_, ld.data(), 8 * sizeof(int), cudaMemcpyHostToDevice));
 }
 
 Engine::~Engine() {
@@ -766,6 +805,12 @@ void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n
     R.xs.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
     R.xs2.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
   }
+  if (fused_a2a()) {  // this group's destinations of the fused all-to-all
+    for (int p = 0; p < k_; ++p)
+      h_peer_base_[p] = k_ == 1 ? ranks_[0].qkv.p : ranks_[p].qh.p;
+    MRSP_CUDA(cudaMemcpyAsync(d_peer_base_, h_peer_base_.data(), 8 * sizeof(void*),
+                              cudaMemcpyHostToDevice, s));
+  }
 }
 
 // One model's pass over the packed group: pack, the decoder stack with Ulysses
@@ -792,6 +837,26 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
         Prof pm(*this, P_MISC);
         rmsnorm(R.h.as<float>(), d, Lw.attn_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
       }
+      if (fused_a2a()) {
+        // QKV projection + bias + RoPE + the Ulysses sequence -> head exchange
+        // in one kernel: every head block lands in its owner rank's buffer
+        Prof pg(*this, P_GEMM);
+        GemmArgs ga{R.xn.p, Lw.wqkv, nullptr, n, Cqkv, d, d, d, 0, GEMM_EPI_QKV_SCATTER,
+                    Lw.bqkv, nullptr, 0};
+        ga.pos = R.pos.as<int>();
+        ga.inv_freq = d_inv_freq_;
+        ga.n_rope_blocks = nq + nkv;
+        ga.row0 = k_ == 1 ? 0 : R.b;
+        ga.route = d_route_;
+        ga.peer_base = d_peer_base_;
+        ga.peer_ld = d_peer_ld_;
+        gemm_bf16(ga, s);
+        if (k_ > 1)
+          for (int p = 0; p < k_; ++p)
+            if (p != R.g)
+              a2a_bytes.fetch_add(static_cast<uint64_t>(n) * (ranks_[p].hs.nq() + 2 * ranks_[p].hs.nkv()) * 256);
+        continue;
+      }
       {
         Prof pg(*this, P_GEMM);
         gemm_bf16({R.xn.p, Lw.wqkv, R.qkv.p, n, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv,
@@ -803,7 +868,7 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
         rope(R.qkv.as<bf16>(), Cqkv, 0, nq + nkv, R.pos.as<int>(), n, s);
       }
     }
-    if (k_ > 1) a2a_forward(static_cast<int>(g.Ltot));
+    if (k_ > 1 && !fused_a2a()) a2a_forward(static_cast<int>(g.Ltot));
     for (auto& R : ranks_) {
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -815,14 +880,28 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
                       s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
-        attention_fwd({R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr,
-                       (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(g.Ltot),
-                       nqr, R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp),
-                       g.Lmax, 0},
-                      s);
+        AttnParams ap{R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr,
+                      (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(g.Ltot),
+                      nqr, R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp),
+                      g.Lmax, 0};
+        if (fused_a2a()) {
+          // the head -> sequence exchange in the attention epilogue: each O
+          // row goes straight to the rank owning that token
+          ap.n_dst = k_;
+          for (int p = 0; p < k_; ++p) {
+            ap.dst_bounds[p] = token_b_[p];
+            ap.dst_base[p] = ranks_[p].ol.p;
+            if (p != R.g)
+              a2a_bytes.fetch_add(static_cast<uint64_t>(token_e_[p] - token_b_[p]) * nqr * 256);
+          }
+          ap.dst_bounds[k_] = token_e_[k_ - 1];
+          ap.dst_ld = Cq;
+          ap.dst_col0 = R.hs.q_lo * 128;
+        }
+        attention_fwd(ap, s);
       }
     }
-    if (k_ > 1) a2a_backward(static_cast<int>(g.Ltot));
+    if (k_ > 1 && !fused_a2a()) a2a_backward(static_cast<int>(g.Ltot));
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;

@@ -168,6 +168,16 @@ class Engine {
   bool has_ref_ = false;
   int vhd_pad_ = 128;
   std::vector<long> token_b_, token_e_;  // current stage-2 plan
+  // fused Ulysses routing (GEMM_EPI_QKV_SCATTER / attention O scatter): device
+  // [inv_freq 64 f32 | route int2[2 * n_blocks] | peer_ld int[8] | peer_base ptr[8]]
+  DevBuf route_buf_;
+  float* d_inv_freq_ = nullptr;
+  int2* d_route_ = nullptr;
+  int* d_peer_ld_ = nullptr;
+  void** d_peer_base_ = nullptr;
+  std::array<void*, 8> h_peer_base_{};
+  void build_routes(const float* inv_freq);
+  bool fused_a2a() const { return !nccl_; }
   std::mutex cache_mu_;
   std::map<std::string, std::shared_ptr<CacheEntry>> cache_;
   uint64_t cache_seq_ = 0;

@@ -52,6 +52,14 @@ struct EpiArgs {
   const int* targets;  // LOGPROB: target id per row
   float2* part;        // LOGPROB: [M][n_tiles] (tile max, sum exp(x - max))
   float* tgt_logit;    // LOGPROB: logit of the target per row
+  // QKV_SCATTER (see GemmArgs)
+  const int* pos;
+  const float* inv_freq;
+  int n_rope_blocks;
+  long row0;
+  const int2* route;
+  void* const* peer_base;
+  const int* peer_ld;
 };
 
 // Grouped raster: consecutive tiles sweep a GROUP_M-tall band of m-tiles with
@@ -87,7 +95,66 @@ __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __e
 // single-CTA and the CTA-pair kernels.
 __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row, int row,
                                              bool row_ok, int nt, int n_tiles) {
-  if (args.epi == GEMM_EPI_LOGPROB_PARTIAL) {
+  if (args.epi == GEMM_EPI_QKV_SCATTER) {
+    // Fused Ulysses sequence -> head all-to-all: this tile's two 128-column
+    // head blocks get +bias, bf16 rounding and (q, k heads) rotate-half RoPE
+    // exactly as the BIAS_BF16 epilogue followed by the rope kernel would
+    // compute them, then go straight to the owner rank's head-shard buffer
+    // (a peer GPU's memory over NVLink, or a virtual rank's buffer).
+    const float p = row_ok ? static_cast<float>(args.pos[row]) : 0.f;
+    const long grow = args.row0 + row;
+#pragma unroll 1
+    for (int hl = 0; hl < BN / 128; ++hl) {
+      const int hb = nt * (BN / 128) + hl;
+      if (hb * 128 >= args.N) break;  // warp-uniform
+      const bool rope = hb < args.n_rope_blocks;
+      const int2 d0 = args.route[2 * hb], d1 = args.route[2 * hb + 1];
+#pragma unroll 1
+      for (int j = 0; j < 64; j += 32) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(t_row + hl * 128 + j, ra);
+        tmem_ld32(t_row + hl * 128 + 64 + j, rb);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t oa[16], ob[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float x1[2], x2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = hb * 128 + j + i + e;
+              x1[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ra[i + e]) + args.bias[c]));
+              x2[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rb[i + e]) + args.bias[c + 64]));
+              if (rope) {
+                float sn, cs;
+                sincosf(__fmul_rn(p, args.inv_freq[j + i + e]), &sn, &cs);
+                const float y1 = __fsub_rn(__fmul_rn(x1[e], cs), __fmul_rn(x2[e], sn));
+                const float y2 = __fadd_rn(__fmul_rn(x2[e], cs), __fmul_rn(x1[e], sn));
+                x1[e] = y1;
+                x2[e] = y2;
+              }
+            }
+            oa[i / 2] = pack_bf16(x1[0], x1[1]);
+            ob[i / 2] = pack_bf16(x2[0], x2[1]);
+          }
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int2 dd = t ? d1 : d0;
+            if (dd.x < 0) continue;
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.peer_base[dd.x]) +
+                                 grow * args.peer_ld[dd.x] + dd.y + j;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              reinterpret_cast<uint4*>(dst)[q4] =
+                  make_uint4(oa[4 * q4], oa[4 * q4 + 1], oa[4 * q4 + 2], oa[4 * q4 + 3]);
+              reinterpret_cast<uint4*>(dst + 64)[q4] =
+                  make_uint4(ob[4 * q4], ob[4 * q4 + 1], ob[4 * q4 + 2], ob[4 * q4 + 3]);
+            }
+          }
+        }
+      }
+    }
+  } else if (args.epi == GEMM_EPI_LOGPROB_PARTIAL) {
     // Fused vocabulary projection + log-softmax pieces: this 256-wide vocab
     // tile's (max, sum exp) per row and the target logit if it lies here.
     // Logits never leave TMEM/registers.
@@ -512,7 +579,12 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   const int elem_per_16b = (f32_out || g.epi == GEMM_EPI_RESID_F32) ? 4 : 8;
   const int vec_ok = (out_addr % 16 == 0) && (ld_out % elem_per_16b == 0);
   EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     g.C,        g.ldc,
-            g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit};
+            g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
+            g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld};
+  if (g.epi == GEMM_EPI_QKV_SCATTER)
+    MRSP_REQUIRE(g.N % 128 == 0 && g.bias && g.pos && g.inv_freq && g.route && g.peer_base &&
+                     g.peer_ld,
+                 MRSP_INVALID_ARGUMENT, "gemm qkv scatter: incomplete routing");
   if (g.epi == GEMM_EPI_LOGPROB_PARTIAL)
     MRSP_REQUIRE(g.targets && g.part && g.tgt_logit, MRSP_INVALID_ARGUMENT,
                  "gemm logprob: null targets/partials");

@@ -20,6 +20,17 @@ struct GemmArgs {
   const int* targets = nullptr;  // GEMM_EPI_LOGPROB_PARTIAL
   float2* part = nullptr;
   float* tgt_logit = nullptr;
+  // GEMM_EPI_QKV_SCATTER (fused RoPE + Ulysses all-to-all): local row r goes to
+  // global row row0 + r; head block hb (128 columns) to route[2 hb + j] =
+  // {peer, dst_col} (peer < 0: none), i.e. peer_base[peer] + row * peer_ld[peer]
+  // + dst_col; blocks < n_rope_blocks (q and k heads) are rotated at pos[r].
+  const int* pos = nullptr;
+  const float* inv_freq = nullptr;  // [64]
+  int n_rope_blocks = 0;
+  long row0 = 0;
+  const int2* route = nullptr;
+  void* const* peer_base = nullptr;
+  const int* peer_ld = nullptr;
 };
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);

@@ -98,8 +98,12 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int ld, int col0, i
     __nv_bfloat162* lo = reinterpret_cast<__nv_bfloat162*>(base + h * 128);
     __nv_bfloat162* hi = reinterpret_cast<__nv_bfloat162*>(base + h * 128 + 64);
     const float2 a = __bfloat1622float2(*lo), b = __bfloat1622float2(*hi);
-    *lo = __floats2bfloat162_rn(a.x * cs0 - b.x * sn0, a.y * cs1 - b.y * sn1);
-    *hi = __floats2bfloat162_rn(b.x * cs0 + a.x * sn0, b.y * cs1 + a.y * sn1);
+    // explicit round-to-nearest ops (no FMA contraction): the fused QKV-scatter
+    // GEMM epilogue computes the identical bits
+    *lo = __floats2bfloat162_rn(__fsub_rn(__fmul_rn(a.x, cs0), __fmul_rn(b.x, sn0)),
+                                __fsub_rn(__fmul_rn(a.y, cs1), __fmul_rn(b.y, sn1)));
+    *hi = __floats2bfloat162_rn(__fadd_rn(__fmul_rn(b.x, cs0), __fmul_rn(a.x, sn0)),
+                                __fadd_rn(__fmul_rn(b.y, cs1), __fmul_rn(a.y, sn1)));
   }
 }
 
