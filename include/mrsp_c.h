@@ -255,6 +255,22 @@ typedef struct mrsp_engine mrsp_engine;
  * to sp/n_kv ranks that split its query-head group with plan_shards. */
 mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
 
+/* Peer-memory transport (one process per GPU, no NCCL): create the engine with
+ * n_procs > 1 and nccl_id = NULL, then on every rank
+ *   mrsp_engine_p2p_export(e, max_frames, max_tokens, max_scored, blob)   -> blob
+ *   (all-gather the n_procs blobs in rank order on the host)
+ *   mrsp_engine_p2p_import(e, blobs)
+ * Each rank exports fixed landing buffers (its head shard of the packed
+ * sequence, its sequence shard of attention output, the gathered video, the
+ * group outputs) through CUDA IPC; the fused QKV / attention epilogues and the
+ * gathers store straight into peers' buffers over NVLink, ordered by a device
+ * barrier. Capacities bound the video (frames), the packed sequence (tokens)
+ * and the scored tokens of every later call. */
+size_t mrsp_p2p_blob_bytes(void);
+mrsp_status mrsp_engine_p2p_export(mrsp_engine* e, int max_frames, long max_tokens,
+                                   long max_scored, void* blob_out);
+mrsp_status mrsp_engine_p2p_import(mrsp_engine* e, const void* blobs);
+
 /* Fills the 128-byte NCCL unique id (call on rank 0, broadcast to all). */
 mrsp_status mrsp_nccl_unique_id(void* out128);
 

@@ -98,6 +98,9 @@ _sig("mrsp_engine_cache", [_V, _I, _I, _V])
 _sig("mrsp_engine_get_embeddings", [_V, ctypes.c_char_p, _V])
 _sig("mrsp_engine_profile", [_V, _I, _I, _V, _V])
 _sig("mrsp_engine_stream", [_V], ctypes.c_void_p)
+_sig("mrsp_p2p_blob_bytes", [], ctypes.c_size_t)
+_sig("mrsp_engine_p2p_export", [_V, _I, ctypes.c_long, ctypes.c_long, _V])
+_sig("mrsp_engine_p2p_import", [_V, _V])
 
 
 def lib() -> ctypes.CDLL:

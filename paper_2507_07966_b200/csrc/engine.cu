@@ -143,8 +143,10 @@ Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n
   MRSP_CUDA(cudaGetDevice(&device_));
   MRSP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   if (n_procs > 1) {
-    MRSP_REQUIRE(nccl_id != nullptr, MRSP_INVALID_ARGUMENT, "engine: NCCL id required");
-    nccl_ = std::make_unique<Nccl>(n_procs, proc_rank, nccl_id, device_);
+    if (nccl_id)
+      nccl_ = std::make_unique<Nccl>(n_procs, proc_rank, nccl_id, device_);
+    else  // peer memory: mrsp_engine_p2p_export / _import before the first call
+      mesh_ = std::make_unique<PeerMesh>(n_procs, proc_rank);
   }
   const int local = n_procs > 1 ? 1 : k_;
   ranks_.resize(local);
@@ -538,7 +540,25 @@ std::shared_ptr<CacheEntry> Engine::get_or_encode(const std::string& id, const f
     auto emb = std::make_shared<DevBuf>();
     const size_t row_bytes = static_cast<size_t>(T) * d * 2;  // one frame's embeddings
     bf16* full = static_cast<bf16*>(emb->ensure(static_cast<size_t>(F) * row_bytes));
-    if (!nccl_) {
+    if (mesh_) {
+      // one process per GPU over peer memory: encode this rank's frames, then
+      // copy-engine P2P writes of the slice into every rank's landing buffer
+      MRSP_REQUIRE(mesh_->ready() && F <= mesh_->caps().frames, MRSP_INVALID_ARGUMENT,
+                   "p2p: mesh not set up or video longer than its frame capacity");
+      RankCtx& R = ranks_[0];
+      const auto [fb, fe] = fplan[R.g];
+      uint8_t* sendb = static_cast<uint8_t*>(R.send.ensure(std::max<long>(fe - fb, 1) * row_bytes));
+      encode_rank(R, pixels, on_device, F, fb, fe, reinterpret_cast<bf16*>(sendb));
+      Prof pc(*this, P_COMM);
+      mesh_->barrier(stream_);  // every rank has copied the previous video out
+      if (fe > fb)
+        for (int p = 0; p < k_; ++p)
+          MRSP_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(mesh_->emb(p)) + fb * row_bytes, sendb,
+                                    (fe - fb) * row_bytes, cudaMemcpyDeviceToDevice, stream_));
+      mesh_->barrier(stream_);
+      MRSP_CUDA(cudaMemcpyAsync(full, mesh_->emb(R.g), F * row_bytes, cudaMemcpyDeviceToDevice,
+                                stream_));
+    } else if (!nccl_) {
       // virtual ranks share this device: each rank's projector writes its
       // slice of the gathered buffer directly (the in-process all-gather)
       for (auto& R : ranks_) {
@@ -794,11 +814,17 @@ void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n
     R.h.ensure(nn * d * 4);
     R.xn.ensure(nn * d * 2);
     R.qkv.ensure(nn * Cqkv * 2);
-    R.ol.ensure(nn * Cq * 2);
+    if (mesh_) {
+      MRSP_REQUIRE(mesh_->ready() && g.Ltot <= mesh_->caps().tokens && n <= mesh_->caps().shard &&
+                       g.total_scored <= mesh_->caps().scored,
+                   MRSP_INVALID_ARGUMENT, "p2p: group exceeds the exported capacities");
+    } else {
+      R.ol.ensure(nn * Cq * 2);
+    }
     R.act.ensure(nn * c.mlp * 2);
     R.pos.ensure(nn * 4);
     R.pad.ensure(nn);
-    if (k_ > 1) {
+    if (k_ > 1 && !mesh_) {
       R.qh.ensure(static_cast<size_t>(g.Ltot) * (R.hs.nq() + 2 * R.hs.nkv()) * 128 * 2);
       R.oh.ensure(static_cast<size_t>(g.Ltot) * std::max(R.hs.nq(), 1) * 128 * 2);
     }
@@ -806,8 +832,7 @@ void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n
     R.xs2.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
   }
   if (fused_a2a()) {  // this group's destinations of the fused all-to-all
-    for (int p = 0; p < k_; ++p)
-      h_peer_base_[p] = k_ == 1 ? ranks_[0].qkv.p : ranks_[p].qh.p;
+    for (int p = 0; p < k_; ++p) h_peer_base_[p] = k_ == 1 ? ranks_[0].qkv.p : qh_dst(p);
     MRSP_CUDA(cudaMemcpyAsync(d_peer_base_, h_peer_base_.data(), 8 * sizeof(void*),
                               cudaMemcpyHostToDevice, s));
   }
@@ -853,8 +878,10 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
         gemm_bf16(ga, s);
         if (k_ > 1)
           for (int p = 0; p < k_; ++p)
-            if (p != R.g)
-              a2a_bytes.fetch_add(static_cast<uint64_t>(n) * (ranks_[p].hs.nq() + 2 * ranks_[p].hs.nkv()) * 256);
+            if (p != R.g) {
+              const HeadSplit hp = head_split(nq, nkv, k_, p);
+              if (hp.nq()) a2a_bytes.fetch_add(static_cast<uint64_t>(n) * (hp.nq() + 2 * hp.nkv()) * 256);
+            }
         continue;
       }
       {
@@ -869,6 +896,7 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
       }
     }
     if (k_ > 1 && !fused_a2a()) a2a_forward(static_cast<int>(g.Ltot));
+    if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
     for (auto& R : ranks_) {
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -880,7 +908,8 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
                       s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
-        AttnParams ap{R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr,
+        void* qh = fused_a2a() ? qh_dst(R.g) : R.qh.p;
+        AttnParams ap{qh, Cr, 0, qh, Cr, nqr * 128, qh, Cr,
                       (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128, 0, static_cast<int>(g.Ltot),
                       nqr, R.hs.q_per_kv, scale, ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp),
                       g.Lmax, 0};
@@ -890,7 +919,7 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
           ap.n_dst = k_;
           for (int p = 0; p < k_; ++p) {
             ap.dst_bounds[p] = token_b_[p];
-            ap.dst_base[p] = ranks_[p].ol.p;
+            ap.dst_base[p] = ol_dst(p);
             if (p != R.g)
               a2a_bytes.fetch_add(static_cast<uint64_t>(token_e_[p] - token_b_[p]) * nqr * 256);
           }
@@ -902,13 +931,14 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
       }
     }
     if (k_ > 1 && !fused_a2a()) a2a_backward(static_cast<int>(g.Ltot));
+    if (mesh_) mesh_->barrier(s);  // every rank's O rows have landed
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
       {
         Prof pg(*this, P_GEMM);
-        gemm_bf16({R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr,
-                   R.h.as<float>(), d},
+        gemm_bf16({mesh_ ? ol_dst(R.g) : R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0,
+                   GEMM_EPI_RESID_F32, nullptr, R.h.as<float>(), d},
                   s);
       }
       {
@@ -948,6 +978,29 @@ __global__ void scatter3_kernel(const float* __restrict__ src, const int* __rest
 void Engine::finish_group(int nvec, float* const* outs, bool out_on_device) {
   const GroupState& g = grp_;
   cudaStream_t s = stream_;
+  if (mesh_) {
+    // each rank writes its scored positions into every rank's landing buffer
+    const long stride = mesh_->caps().scored + 16;
+    const RankCtx& R = ranks_[0];
+    Prof pc(*this, P_COMM);
+    mesh_->barrier(s);  // every rank has read the previous group's outputs
+    if (R.n_scored)
+      for (int p = 0; p < k_; ++p) {
+        scatter3_kernel<<<(R.n_scored + 255) / 256, 256, 0, s>>>(
+            R.lp.as<float>(), R.scored_idx.as<int32_t>() + 2 * R.n_scored, R.n_scored, nvec,
+            mesh_->lp(p), stride);
+        count_launch();
+        MRSP_CUDA(cudaGetLastError());
+      }
+    mesh_->barrier(s);
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    for (int v = 0; v < nvec; ++v)
+      if (outs[v] && g.total_scored)
+        MRSP_CUDA(cudaMemcpyAsync(outs[v], mesh_->lp(R.g) + v * stride, g.total_scored * 4, kind, s));
+    MRSP_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    return;
+  }
   for (auto& R : ranks_) {
     if (R.n_scored == 0) continue;
     scatter3_kernel<<<(R.n_scored + 255) / 256, 256, 0, s>>>(
@@ -1015,6 +1068,28 @@ void Engine::group_logprobs(const CacheEntry& emb, const int32_t* question, int 
   finish_group(3, outs, out_on_device);
 }
 
+size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void* blob) {
+  MRSP_REQUIRE(mesh_ != nullptr, MRSP_LOGIC_ERROR, "p2p: engine was created with NCCL or 1 process");
+  MRSP_REQUIRE(max_frames >= 1 && max_tokens >= 1 && max_scored >= 0, MRSP_INVALID_ARGUMENT,
+               "p2p: capacities must be positive");
+  const RankCtx& R = ranks_[0];
+  PeerCaps caps;
+  caps.tokens = max_tokens;
+  caps.shard = (max_tokens + k_ - 1) / k_;
+  caps.frames = max_frames;
+  caps.scored = max_scored;
+  caps.c_head_shard = std::max(1, R.hs.nq() + 2 * R.hs.nkv()) * 128;
+  caps.cq = cfg_.n_q_heads * 128;
+  caps.tok_row = tokens_per_frame() * cfg_.dim;
+  if (blob) mesh_->export_blob(caps, blob);
+  return PeerMesh::kBlobBytes;
+}
+
+void Engine::p2p_import(const void* blobs) {
+  MRSP_REQUIRE(mesh_ != nullptr, MRSP_LOGIC_ERROR, "p2p: engine was created with NCCL or 1 process");
+  mesh_->import_blobs(blobs);
+}
+
 size_t Engine::cache_size() {
   std::lock_guard<std::mutex> lock(cache_mu_);
   return cache_.size();
@@ -1056,6 +1131,8 @@ extern "C" mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, in
       for (int j = 0; j < 3; ++j) out14[5 + 3 * i + j] = b[i][j];
   });
 }
+
+extern "C" size_t mrsp_p2p_blob_bytes(void) { return mrsp::PeerMesh::kBlobBytes; }
 
 extern "C" mrsp_status mrsp_nccl_unique_id(void* out128) {
   return guard([&] { Nccl::unique_id(out128); });
@@ -1193,3 +1270,20 @@ extern "C" mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, 
 }
 
 extern "C" void* mrsp_engine_stream(mrsp_engine* e) { return e ? e->impl->stream() : nullptr; }
+
+extern "C" mrsp_status mrsp_engine_p2p_export(mrsp_engine* e, int max_frames, long max_tokens,
+                                              long max_scored, void* blob_out) {
+  return mrsp::guard([&] {
+    MRSP_REQUIRE(e && e->impl, MRSP_INVALID_ARGUMENT, "null engine");
+    std::lock_guard<std::mutex> lock(e->mu);
+    e->impl->p2p_export(max_frames, max_tokens, max_scored, blob_out);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_p2p_import(mrsp_engine* e, const void* blobs) {
+  return mrsp::guard([&] {
+    MRSP_REQUIRE(e && e->impl, MRSP_INVALID_ARGUMENT, "null engine");
+    std::lock_guard<std::mutex> lock(e->mu);
+    e->impl->p2p_import(blobs);
+  });
+}

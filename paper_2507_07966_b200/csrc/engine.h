@@ -15,6 +15,7 @@
 
 #include "comm.h"
 #include "mrsp_c.h"
+#include "peer.h"
 
 namespace mrsp {
 
@@ -178,6 +179,18 @@ class Engine {
   std::array<void*, 8> h_peer_base_{};
   void build_routes(const float* inv_freq);
   bool fused_a2a() const { return !nccl_; }
+  // one process per GPU over CUDA-IPC peer memory (no NCCL id given)
+  std::unique_ptr<PeerMesh> mesh_;
+  // head-shard / sequence-shard output buffers of SP rank p (a virtual rank's
+  // own buffer, or a peer's mapped landing buffer)
+  void* qh_dst(int p) { return mesh_ ? mesh_->qh(p) : ranks_[p].qh.p; }
+  void* ol_dst(int p) { return mesh_ ? mesh_->ol(p) : ranks_[p].ol.p; }
+
+ public:
+  size_t p2p_export(int max_frames, long max_tokens, long max_scored, void* blob);
+  void p2p_import(const void* blobs);
+
+ private:
   std::mutex cache_mu_;
   std::map<std::string, std::shared_ptr<CacheEntry>> cache_;
   uint64_t cache_seq_ = 0;

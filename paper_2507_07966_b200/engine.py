@@ -160,6 +160,20 @@ class Engine:
                                             policy_seed, ref_seed, int(with_ref), idb,
                                             ctypes.byref(self._h)))
 
+    # ---- peer-memory transport (one process per GPU, no NCCL) -------------
+    def p2p_export(self, max_frames: int, max_tokens: int, max_scored: int) -> bytes:
+        """Allocates this rank's IPC landing buffers; returns its blob for the
+        host all-gather (engine created with n_procs > 1 and no nccl_id)."""
+        n = _lib.lib().mrsp_p2p_blob_bytes()
+        buf = ctypes.create_string_buffer(n)
+        check(_lib.lib().mrsp_engine_p2p_export(self._h, max_frames, max_tokens, max_scored, buf))
+        return buf.raw
+
+    def p2p_import(self, blobs) -> None:
+        """Maps every rank's landing buffers; blobs in rank order."""
+        data = b"".join(blobs)
+        check(_lib.lib().mrsp_engine_p2p_import(self._h, ctypes.create_string_buffer(data, len(data))))
+
     def close(self):
         if self._h:
             check(_lib.lib().mrsp_engine_destroy(self._h))
