@@ -260,16 +260,36 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # MRSP_BENCH_SAME_DEVICE=1 (tests): every rank on device 0 and a gloo host
+    # group, so the multi-process flow runs on a one-GPU box
+    same_dev = os.environ.get("MRSP_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
+    # Engine data path for N > 1: peer memory over NVLink (CUDA IPC, fused
+    # QKV / attention scatters, device barrier) by default; MRSP_COMM=nccl
+    # selects the NCCL all-gather / all-to-all path instead. The torch process
+    # group is host plumbing only (blob exchange, barrier, max-over-ranks).
+    comm = os.environ.get("MRSP_COMM", "p2p")
     nccl_id = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        obj = [E.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if comm == "nccl":
+            obj = [E.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
     from paper_2507_07966_b200 import _lib
     eng = E.Engine(w.cfg, sp=world, rank=rank, n_procs=world, vision_seed=2, policy_seed=3,
                    ref_seed=4, with_ref=True, nccl_id=nccl_id)
+    if world > 1 and nccl_id is None:
+        L = w.frames * w.cfg.tokens_per_frame + len(group.question) + group.resp.shape[0] * group.Lmax
+        blob = eng.p2p_export(w.frames, L, group.scored)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        eng.p2p_import(blobs)
     eng.cache_capacity(2)
     S = w.cfg.image_size
     pix_host = torch.from_numpy(E.gen_video(1, w.frames, 3 * S * S)).pin_memory()
@@ -286,7 +306,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if same_dev else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -371,7 +391,9 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": workload_config(w, group, fl, world),
+        "config": {**workload_config(w, group, fl, world),
+                   "comm": (("nccl" if nccl_id else "p2p: CUDA-IPC peer memory, fused QKV/attention "
+                             "scatters") if world > 1 else "none (SP=1)")},
         "roofline": roofline,
         "step_roofline": {"flops_per_step": fl["step"], "achieved_tflops": step_tflops,
                           "frac_of_sustained": step_tflops / world / peak},
