@@ -255,6 +255,25 @@ typedef struct mrsp_engine mrsp_engine;
  * to sp/n_kv ranks that split its query-head group with plan_shards. */
 mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
 
+/* Weights as safetensors with Hugging Face tensor names (SigLIP
+ * vision_model.*, projector mm_projector.{0,2}.*, Qwen2 model.* / lm_head.weight;
+ * the GRPO reference model is saved with the prefix "ref."), unpadded HF shapes.
+ * load: part 0 = vision tower + projector, 1 = policy LLM, 2 = reference LLM,
+ * reading the names under `prefix` ("" or e.g. "ref."); BF16 and F32 tensors are
+ * converted to the engine's storage type; a missing tensor or a shape that does
+ * not match the engine geometry is MRSP_INVALID_ARGUMENT. */
+mrsp_status mrsp_engine_save_weights(mrsp_engine* e, const char* path);
+mrsp_status mrsp_engine_load_weights(mrsp_engine* e, const char* path, int part,
+                                     const char* prefix);
+
+/* Embedding-cache persistence: write a cached (encoded) video's gathered
+ * embeddings to `path`; load them under `video_id` so later fetches hit without
+ * encoding (the file records frames, tokens/frame, dim and an encoder-geometry
+ * fingerprint; a mismatch is MRSP_INVALID_ARGUMENT). */
+mrsp_status mrsp_engine_cache_save(mrsp_engine* e, const char* video_id, const char* path);
+mrsp_status mrsp_engine_cache_load(mrsp_engine* e, const char* video_id, const char* path,
+                                   int* frames_out);
+
 /* Peer-memory transport (one process per GPU, no NCCL): create the engine with
  * n_procs > 1 and nccl_id = NULL, then on every rank
  *   mrsp_engine_p2p_export(e, max_frames, max_tokens, max_scored, blob)   -> blob

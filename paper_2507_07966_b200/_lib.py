@@ -99,6 +99,10 @@ _sig("mrsp_engine_get_embeddings", [_V, ctypes.c_char_p, _V])
 _sig("mrsp_engine_profile", [_V, _I, _I, _V, _V])
 _sig("mrsp_engine_stream", [_V], ctypes.c_void_p)
 _sig("mrsp_p2p_blob_bytes", [], ctypes.c_size_t)
+_sig("mrsp_engine_save_weights", [_V, ctypes.c_char_p])
+_sig("mrsp_engine_load_weights", [_V, ctypes.c_char_p, _I, ctypes.c_char_p])
+_sig("mrsp_engine_cache_save", [_V, ctypes.c_char_p, ctypes.c_char_p])
+_sig("mrsp_engine_cache_load", [_V, ctypes.c_char_p, ctypes.c_char_p, _V])
 _sig("mrsp_engine_p2p_export", [_V, _I, ctypes.c_long, ctypes.c_long, _V])
 _sig("mrsp_engine_p2p_import", [_V, _V])
 

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 
@@ -1098,6 +1099,86 @@ void Engine::cache_clear() {
   std::lock_guard<std::mutex> lock(cache_mu_);
   cache_.clear();
 }
+// ---------------------------------------------------------------------------
+// Embedding-cache persistence (the reference never persists
+// its cache, engine.hpp:105-128). File: "MRSPEMB1", u32 version 1, frames,
+// tokens/frame, dim, dtype (1 = bf16), u64 fingerprint of the vision + projector
+// geometry, then [frames * tokens][dim] bf16 row-major.
+namespace {
+constexpr char kEmbMagic[8] = {'M', 'R', 'S', 'P', 'E', 'M', 'B', '1'};
+struct EmbHeader {
+  char magic[8];
+  uint32_t version, frames, tokens, dim, dtype, pad;
+  uint64_t fingerprint;
+};
+static_assert(sizeof(EmbHeader) == 40, "packed header");
+uint64_t encoder_fingerprint(const mrsp_model_config& c) {
+  const int v[] = {c.image_size, c.patch, c.v_dim, c.v_heads, c.v_head_dim, c.v_mlp, c.v_layers,
+                   c.dim};
+  std::string s;
+  for (int x : v) s += std::to_string(x) + ",";
+  return fnv1a(s);
+}
+}  // namespace
+
+void Engine::cache_save(const CacheEntry& e, const std::string& path) {
+  const int T = tokens_per_frame();
+  const size_t n = static_cast<size_t>(e.n_frames) * T * cfg_.dim;
+  std::vector<uint16_t> host(n);
+  MRSP_CUDA(cudaMemcpy(host.data(), e.emb->p, n * 2, cudaMemcpyDeviceToHost));
+  EmbHeader h{};
+  std::memcpy(h.magic, kEmbMagic, 8);
+  h.version = 1;
+  h.frames = static_cast<uint32_t>(e.n_frames);
+  h.tokens = static_cast<uint32_t>(T);
+  h.dim = static_cast<uint32_t>(cfg_.dim);
+  h.dtype = 1;
+  h.fingerprint = encoder_fingerprint(cfg_);
+  FILE* f = std::fopen(path.c_str(), "wb");
+  MRSP_REQUIRE(f != nullptr, MRSP_RUNTIME_ERROR, "cache_save: cannot open " + path);
+  const bool ok = std::fwrite(&h, sizeof(h), 1, f) == 1 && std::fwrite(host.data(), 2, n, f) == n;
+  const bool closed = std::fclose(f) == 0;
+  MRSP_REQUIRE(ok && closed, MRSP_RUNTIME_ERROR, "cache_save: write failed: " + path);
+}
+
+std::shared_ptr<CacheEntry> Engine::cache_load(const std::string& id, const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  MRSP_REQUIRE(f != nullptr, MRSP_RUNTIME_ERROR, "cache_load: cannot open " + path);
+  EmbHeader h{};
+  const bool got = std::fread(&h, sizeof(h), 1, f) == 1;
+  if (!got || std::memcmp(h.magic, kEmbMagic, 8) != 0 || h.version != 1 || h.dtype != 1) {
+    std::fclose(f);
+    fail(MRSP_INVALID_ARGUMENT, "cache_load: not an MRSP embedding file: " + path);
+  }
+  if (static_cast<int>(h.tokens) != tokens_per_frame() || static_cast<int>(h.dim) != cfg_.dim ||
+      h.fingerprint != encoder_fingerprint(cfg_) || h.frames < 1) {
+    std::fclose(f);
+    fail(MRSP_INVALID_ARGUMENT, "cache_load: embeddings were made by a different encoder geometry");
+  }
+  const size_t n = static_cast<size_t>(h.frames) * h.tokens * h.dim;
+  std::vector<uint16_t> host(n);
+  const bool read_ok = std::fread(host.data(), 2, n, f) == n;
+  std::fclose(f);
+  MRSP_REQUIRE(read_ok, MRSP_RUNTIME_ERROR, "cache_load: truncated file " + path);
+  auto emb = std::make_shared<DevBuf>();
+  MRSP_CUDA(cudaMemcpy(emb->ensure(n * 2), host.data(), n * 2, cudaMemcpyHostToDevice));
+  auto entry = std::make_shared<CacheEntry>();
+  entry->emb = emb;
+  entry->n_frames = static_cast<int>(h.frames);
+  entry->ready = true;
+  std::lock_guard<std::mutex> lock(cache_mu_);
+  entry->seq = ++cache_seq_;
+  cache_[id] = entry;  // later fetches of `id` hit without encoding
+  if (cache_capacity > 0)
+    while (static_cast<int>(cache_.size()) > cache_capacity) {
+      auto oldest = std::min_element(cache_.begin(), cache_.end(), [](auto& a, auto& b) {
+        return a.second->seq < b.second->seq;
+      });
+      cache_.erase(oldest);
+    }
+  return entry;
+}
+
 void Engine::copy_embeddings(const CacheEntry& e, void* host_out) {
   MRSP_CUDA(cudaMemcpy(host_out, e.emb->p,
                        static_cast<size_t>(e.n_frames) * tokens_per_frame() * cfg_.dim * 2,
@@ -1246,6 +1327,47 @@ extern "C" mrsp_status mrsp_engine_cache(mrsp_engine* e, int op, int arg, uint64
       e->impl->cache_capacity = arg;
     }
     if (size_out) *size_out = e->impl->cache_size();
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_save_weights(mrsp_engine* e, const char* path) {
+  return guard([&] {
+    MRSP_REQUIRE(e && path, MRSP_INVALID_ARGUMENT, "save_weights: null argument");
+    e->impl->save_weights(path);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_load_weights(mrsp_engine* e, const char* path, int part,
+                                               const char* prefix) {
+  return guard([&] {
+    MRSP_REQUIRE(e && path, MRSP_INVALID_ARGUMENT, "load_weights: null argument");
+    e->impl->load_weights(path, part, prefix ? prefix : "");
+    if (part == 0) {  // embeddings of the old tower are stale
+      std::lock_guard<std::mutex> lock(e->mu);
+      e->last.clear();
+    }
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_cache_save(mrsp_engine* e, const char* video_id,
+                                              const char* path) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && path, MRSP_INVALID_ARGUMENT, "cache_save: null argument");
+    auto entry = lookup(e, video_id);
+    e->impl->cache_save(*entry, path);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_cache_load(mrsp_engine* e, const char* video_id,
+                                              const char* path, int* frames_out) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && path, MRSP_INVALID_ARGUMENT, "cache_load: null argument");
+    auto entry = e->impl->cache_load(video_id, path);
+    {
+      std::lock_guard<std::mutex> lock(e->mu);
+      e->last[video_id] = entry;
+    }
+    if (frames_out) *frames_out = entry->n_frames;
   });
 }
 

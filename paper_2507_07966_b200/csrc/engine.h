@@ -132,6 +132,13 @@ class Engine {
       pad_reads{0}, a2a_bytes{0};
   size_t cache_size();
   void cache_clear();
+  // weights to / from safetensors with HF names (csrc/weights_io.cpp); part 0 =
+  // vision tower + projector, 1 = policy LLM, 2 = reference LLM
+  void save_weights(const std::string& path);
+  void load_weights(const std::string& path, int part, const std::string& prefix);
+  // cache persistence: a gathered video's embeddings to / from a file
+  void cache_save(const CacheEntry& e, const std::string& path);
+  std::shared_ptr<CacheEntry> cache_load(const std::string& id, const std::string& path);
   int cache_capacity = 0;  // 0 = unbounded
 
   // profiling: CUDA-event time per kernel class

@@ -160,6 +160,29 @@ class Engine:
                                             policy_seed, ref_seed, int(with_ref), idb,
                                             ctypes.byref(self._h)))
 
+    # ---- weights (safetensors, HF names) -------------------------------------
+    VISION, POLICY, REFERENCE = 0, 1, 2
+
+    def save_weights(self, path: str) -> None:
+        check(_lib.lib().mrsp_engine_save_weights(self._h, str(path).encode()))
+
+    def load_weights(self, path: str, part: int, prefix: str = "") -> None:
+        """part: Engine.VISION (tower + projector), POLICY or REFERENCE LLM, read
+        from the tensors named `prefix` + the HF name."""
+        check(_lib.lib().mrsp_engine_load_weights(self._h, str(path).encode(), part,
+                                                  prefix.encode()))
+
+    # ---- embedding-cache persistence ---------------------------------------
+    def cache_save(self, vid: str, path: str) -> None:
+        check(_lib.lib().mrsp_engine_cache_save(self._h, vid.encode(), str(path).encode()))
+
+    def cache_load(self, vid: str, path: str) -> int:
+        """Loads saved embeddings under `vid`; returns the frame count."""
+        f = ctypes.c_int(0)
+        check(_lib.lib().mrsp_engine_cache_load(self._h, vid.encode(), str(path).encode(),
+                                                ctypes.byref(f)))
+        return f.value
+
     # ---- peer-memory transport (one process per GPU, no NCCL) -------------
     def p2p_export(self, max_frames: int, max_tokens: int, max_scored: int) -> bytes:
         """Allocates this rank's IPC landing buffers; returns its blob for the

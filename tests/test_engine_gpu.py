@@ -182,3 +182,69 @@ def test_step_exact_kl_vs_oracle(gpu, c1_oracle):
     assert np.abs(lp_r - c1_oracle["lp_r"]).max() <= 5e-2
     d = np.abs(kl - want_kl)
     assert d.max() <= 5e-2 and d.mean() <= 5e-3, (d.max(), d.mean())
+
+
+def test_cache_save_load_roundtrip(gpu, c1_oracle, tmp_path):
+    """Embedding-cache persistence: a saved video loads into a
+    fresh engine as a cache entry — the step then hits G times, never encodes, and
+    returns bit-identical log-probs; wrong files are rejected."""
+    pix, grp = c1_oracle["pix"], c1_oracle["grp"]
+    a = E.Engine(W1.cfg, sp=1, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    a.encode("v", pix)
+    want = a.step("v", pix, grp)
+    emb = a.embeddings("v", W1.frames)
+    path = tmp_path / "v.mrspemb"
+    a.cache_save("v", path)
+    a.close()
+    b = E.Engine(W1.cfg, sp=2, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    assert b.cache_load("v2", path) == W1.frames
+    assert np.array_equal(b.embeddings("v2", W1.frames), emb)
+    got = b.step("v2", pix, grp)
+    st = b.stats()
+    assert st["encoder_invocations"] == 0 and st["cache_hits"] == W1.G and st["cache_misses"] == 0
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    bad = tmp_path / "bad"
+    bad.write_bytes(b"not an embedding file" * 4)
+    with pytest.raises(_lib.InvalidArgument):
+        b.cache_load("x", bad)
+    with pytest.raises(_lib.MrspError):
+        b.cache_load("x", tmp_path / "missing")
+    b.close()
+
+
+def test_weights_safetensors_roundtrip(gpu, c1_oracle, tmp_path):
+    """Weights I/O: an engine's weights saved as safetensors
+    with HF names / unpadded HF shapes load into an engine built from other seeds
+    and reproduce its outputs bit-exactly (head padding, q/k/v split and gate/up
+    interleave invert exactly)."""
+    import json
+    import struct
+    pix, grp = c1_oracle["pix"], c1_oracle["grp"]
+    a = E.Engine(W1.cfg, sp=1, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    a.encode("v", pix)
+    want = a.step("v", pix, grp)
+    path = tmp_path / "w.safetensors"
+    a.save_weights(path)
+    a.close()
+    raw = path.read_bytes()
+    n = struct.unpack("<Q", raw[:8])[0]
+    hdr = json.loads(raw[8:8 + n])
+    c = W1.cfg
+    assert hdr["model.layers.0.self_attn.q_proj.weight"]["shape"] == [c.n_q_heads * 128, c.dim]
+    assert hdr["model.layers.1.mlp.gate_proj.weight"]["shape"] == [c.mlp, c.dim]
+    assert hdr["vision_model.encoder.layers.0.self_attn.out_proj.weight"]["shape"] == [c.v_dim, c.v_dim]
+    assert hdr["vision_model.embeddings.patch_embedding.weight"]["shape"] == [c.v_dim, 3, c.patch, c.patch]
+    assert hdr["mm_projector.2.weight"]["shape"] == [c.dim, c.dim] and "ref.lm_head.weight" in hdr
+    b = E.Engine(W1.cfg, sp=2, vision_seed=11, policy_seed=12, ref_seed=13)
+    b.load_weights(path, E.Engine.VISION)
+    b.load_weights(path, E.Engine.POLICY)
+    b.load_weights(path, E.Engine.REFERENCE, "ref.")
+    b.encode("v", pix)
+    got = b.step("v", pix, grp)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    b.load_weights(path, E.Engine.REFERENCE, "")  # the policy checkpoint as the reference
+    got2 = b.step("v", pix, grp)
+    assert np.array_equal(got2[0], got2[1])
+    with pytest.raises(_lib.InvalidArgument):
+        b.load_weights(path, E.Engine.REFERENCE, "nope.")
+    b.close()
