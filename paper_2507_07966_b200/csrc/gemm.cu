@@ -565,12 +565,12 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     MRSP_REQUIRE(g.N % BN == 0, MRSP_INVALID_ARGUMENT, "gemm swiglu: N must be a multiple of 256");
   if (g.epi == GEMM_EPI_RESID_F32)
     MRSP_REQUIRE(g.resid != nullptr, MRSP_INVALID_ARGUMENT, "gemm resid: null residual");
-  static bool attr_set = false;
-  if (!attr_set) {
+  static const bool attr_set = [] {  // thread-safe one-time setup (C-ABI callers may race)
     MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM_BYTES)));
-    attr_set = true;
-  }
+    return true;
+  }();
+  (void)attr_set;
   CUtensorMap ta = make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, BM, BK);
   CUtensorMap tb = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BN, BK);
   const bool f32_out = g.epi == GEMM_EPI_STORE_F32;

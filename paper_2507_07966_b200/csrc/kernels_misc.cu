@@ -309,12 +309,12 @@ void patchify(const float* pix, __nv_bfloat16* out, int F, int H, int W, int P, 
   MRSP_REQUIRE(kpad % 2 == 0 && kpad >= 3 * P * P, MRSP_INVALID_ARGUMENT, "patchify: bad kpad");
   const size_t smem = (static_cast<size_t>(3) * P * W + kpad) * sizeof(float);
   MRSP_REQUIRE(smem <= 200 * 1024, MRSP_INVALID_ARGUMENT, "patchify: image rows too wide");
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
+  static const bool attr = [] {  // thread-safe one-time setup
     MRSP_CUDA(cudaFuncSetAttribute(patchify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   patchify_kernel<<<F * (H / P), 256, smem, s>>>(pix, out, F, H, W, P, kpad);
   count_launch();
   MRSP_CUDA(cudaGetLastError());

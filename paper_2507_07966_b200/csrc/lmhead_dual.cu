@@ -253,12 +253,12 @@ void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, cons
   MRSP_REQUIRE(K % 8 == 0, MRSP_INVALID_ARGUMENT, "lmhead_dual: K must be a multiple of 8");
   MRSP_REQUIRE(ws_bytes >= lmhead_dual_workspace_bytes(M, V), MRSP_INVALID_ARGUMENT,
                "lmhead_dual: workspace too small");
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {  // thread-safe one-time setup
     MRSP_CUDA(cudaFuncSetAttribute(lmhead_dual_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM_BYTES)));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   DualArgs a;
   a.M = M;
   a.V = V;

@@ -248,3 +248,46 @@ def test_weights_safetensors_roundtrip(gpu, c1_oracle, tmp_path):
     with pytest.raises(_lib.InvalidArgument):
         b.load_weights(path, E.Engine.REFERENCE, "nope.")
     b.close()
+
+
+EDGE_CASES = {
+    # (frames, question, lengths, Lmax): the reference's edge cases on the engine path —
+    # one frame, rows of length 0 (pad_batch allows empty rows, test_engine.cpp:133-144),
+    # a single one-token row, no question tokens, odd ragged lengths
+    "one_frame": (1, [10, 11, 12], [3, 7], 7),
+    "empty_rows": (8, [10, 11, 12], [0, 12, 0, 5], 12),
+    "single_token": (8, [10, 11, 12], [1], 1),
+    "no_question": (8, [], [4, 2], 4),
+    "ragged_odd": (3, [13, 17, 19, 23, 29], [1, 9, 4, 11, 6], 11),
+}
+
+
+@pytest.mark.parametrize("case", sorted(EDGE_CASES))
+def test_edge_groups_vs_oracle(gpu, case):
+    frames, q, lengths, Lmax = EDGE_CASES[case]
+    c = T.Cfg.from_any(W1.cfg)
+    rng = np.random.default_rng(len(case))
+    pix = E.gen_video(5, frames, 3 * c.image_size ** 2)
+    resp = np.zeros((len(lengths), Lmax), dtype=np.int32)  # PAD = 0 past each length
+    for g, n in enumerate(lengths):
+        resp[g, :n] = rng.integers(10, W1.cfg.vocab, size=n)
+    grp = E.Group(np.array(q, dtype=np.int32), resp, np.array(lengths, dtype=np.int32))
+    emb = T.vision_forward(c, T.vision_weights(c, VSEED), pix)
+    want, _ = T.llm_logprobs(c, T.llm_weights(c, PSEED, "policy."), emb, grp.question, grp.resp,
+                             grp.lengths)
+    outs = []
+    for sp in (1, 2):
+        eng = E.Engine(W1.cfg, sp=sp, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+        eng.encode("v", pix)
+        outs.append(eng.prefill_logprobs("v", grp, 0))
+        st = eng.stats()
+        assert st["pad_reads"] == 0 and st["encoder_invocations"] == frames
+        eng.close()
+    assert outs[0].shape == (sum(lengths),)
+    assert np.array_equal(outs[0], outs[1]), "SP=2 differs from SP=1"
+    if len(want):
+        # max |d| <= 5e-2 per token; the mean bound (5e-3) is a population
+        # statistic, applied from 16 scored tokens up
+        d = np.abs(outs[0] - want)
+        assert d.max() <= 5e-2, (case, d.max())
+        assert len(d) < 16 or d.mean() <= 5e-3, (case, d.mean())
