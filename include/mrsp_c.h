@@ -255,6 +255,20 @@ typedef struct mrsp_engine mrsp_engine;
  * to sp/n_kv ranks that split its query-head group with plan_shards. */
 mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
 
+/* Rollout generation (policy.cpp:121-157 sample_rollout):
+ * G rows sampled from the policy after the prompt [cached video | question]:
+ * one prompt prefill keeps every layer's K/V, then each decode step runs the G
+ * rows through the LLM (decode attention over the prompt K/V and the row's own
+ * keys) and samples token t of every unfinished row with probability
+ * softmax(logits / temperature), u = splitmix64-hash(seed, row, t) in [0, 1);
+ * a row stops after EOS (1). Outputs: tokens [G][max_len] (PAD = 0 after the
+ * end), lengths [G] (EOS included), old_logprobs [G][max_len] =
+ * log_softmax(logits)[token] at temperature 1. Single-GPU engines (SP = 1). */
+mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id, const int32_t* question,
+                                 int n_q, int G, int max_len, float temperature, uint64_t seed,
+                                 int32_t* tokens_out, int32_t* lengths_out,
+                                 float* old_logprobs_out);
+
 /* Weights as safetensors with Hugging Face tensor names (SigLIP
  * vision_model.*, projector mm_projector.{0,2}.*, Qwen2 model.* / lm_head.weight;
  * the GRPO reference model is saved with the prefix "ref."), unpadded HF shapes.

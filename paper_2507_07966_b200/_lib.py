@@ -100,6 +100,7 @@ _sig("mrsp_engine_profile", [_V, _I, _I, _V, _V])
 _sig("mrsp_engine_stream", [_V], ctypes.c_void_p)
 _sig("mrsp_p2p_blob_bytes", [], ctypes.c_size_t)
 _sig("mrsp_engine_save_weights", [_V, ctypes.c_char_p])
+_sig("mrsp_engine_generate", [_V, ctypes.c_char_p, _V, _I, _I, _I, _F, _U64, _V, _V, _V])
 _sig("mrsp_engine_load_weights", [_V, ctypes.c_char_p, _I, ctypes.c_char_p])
 _sig("mrsp_engine_cache_save", [_V, ctypes.c_char_p, ctypes.c_char_p])
 _sig("mrsp_engine_cache_load", [_V, ctypes.c_char_p, ctypes.c_char_p, _V])

@@ -855,7 +855,9 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
                   R.h.as<float>(), R.pos.as<int>(), R.pad.as<unsigned char>(), nullptr, s);
   }
   const float scale = 1.0f / std::sqrt(128.0f);
+  int layer = -1;
   for (const auto& Lw : W.layers) {
+    ++layer;
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
@@ -898,6 +900,13 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
     }
     if (k_ > 1 && !fused_a2a()) a2a_forward(static_cast<int>(g.Ltot));
     if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
+    if (capture_kv_) {  // generation: keep this layer's prompt K | V (SP = 1)
+      const size_t w = static_cast<size_t>(2 * nkv) * 128;
+      MRSP_CUDA(cudaMemcpy2DAsync(kv_prefix_.as<bf16>() + static_cast<size_t>(layer) * g.Lp * w,
+                                  w * 2, ranks_[0].qkv.as<bf16>() + nq * 128,
+                                  static_cast<size_t>(Cqkv) * 2, w * 2, g.Lp,
+                                  cudaMemcpyDeviceToDevice, s));
+    }
     for (auto& R : ranks_) {
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -1067,6 +1076,120 @@ void Engine::group_logprobs(const CacheEntry& emb, const int32_t* question, int 
   }
   float* outs[3] = {lp_policy, lp_ref, kl};
   finish_group(3, outs, out_on_device);
+}
+
+void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, int G,
+                      int max_len, float temperature, uint64_t seed, int32_t* tokens_out,
+                      int32_t* lengths_out, float* old_lp_out) {
+  const auto& c = cfg_;
+  MRSP_REQUIRE(k_ == 1 && !nccl_ && !mesh_, MRSP_INVALID_ARGUMENT,
+               "generate: single-GPU engines (SP = 1) only");
+  MRSP_REQUIRE(temperature > 0.f, MRSP_INVALID_ARGUMENT,
+               "sample_rollout: temperature must be > 0");
+  MRSP_REQUIRE(max_len >= 1, MRSP_INVALID_ARGUMENT, "sample_rollout: max_len must be >= 1");
+  const int nq = c.n_q_heads, nkv = c.n_kv_heads, qpk = nq / nkv, d = c.dim;
+  MRSP_REQUIRE(G >= 1 && G * qpk <= 64, MRSP_INVALID_ARGUMENT,
+               "generate: 1 <= G and G x q_per_kv <= 64");
+  std::lock_guard<std::mutex> run(run_mu_);
+  cudaStream_t s = stream_;
+  // 1. prompt prefill (the policy over [video | question]) keeping every layer's K/V
+  const int32_t dummy_resp = 0, zero_len = 0;
+  prepare_group(emb, question, n_q, &dummy_resp, &zero_len, 1, 1);
+  const long Lp = grp_.Lp;
+  const size_t kvw = static_cast<size_t>(2 * nkv) * 128;  // one position's K | V
+  kv_prefix_.ensure(static_cast<size_t>(c.layers) * std::max<long>(Lp, 1) * kvw * 2);
+  capture_kv_ = true;
+  try {
+    run_pass(emb, 0, 0);
+  } catch (...) {
+    capture_kv_ = false;
+    throw;
+  }
+  capture_kv_ = false;
+  // 2. decode state
+  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128;
+  RankCtx& R = ranks_[0];
+  DevBuf& st = R.recv;  // generation scratch (R.send/R.recv are unused at SP = 1)
+  const size_t n_tok = static_cast<size_t>(G) * max_len;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_rows = carve(static_cast<size_t>(c.layers) * max_len * G * kvw * 2);
+  const size_t o_h = carve(static_cast<size_t>(G) * d * 4), o_xn = carve(static_cast<size_t>(G) * d * 2);
+  const size_t o_qkv = carve(static_cast<size_t>(G) * Cqkv * 2), o_o = carve(static_cast<size_t>(G) * Cq * 2);
+  const size_t o_act = carve(static_cast<size_t>(G) * c.mlp * 2);
+  const size_t o_logit = carve(static_cast<size_t>(G) * c.vocab * 4);
+  const size_t o_part = carve(decode_partial_bytes(static_cast<int>(Lp), max_len, G, nkv));
+  const size_t o_tok = carve(n_tok * 4), o_lp = carve(n_tok * 4), o_len = carve(G * 4);
+  const size_t o_done = carve(G * 4), o_pos = carve(G * 4);
+  uint8_t* b = static_cast<uint8_t*>(st.ensure(off));
+  bf16* kv_rows = reinterpret_cast<bf16*>(b + o_rows);
+  float* h = reinterpret_cast<float*>(b + o_h);
+  bf16* xn = reinterpret_cast<bf16*>(b + o_xn);
+  bf16* qkv = reinterpret_cast<bf16*>(b + o_qkv);
+  bf16* od = reinterpret_cast<bf16*>(b + o_o);
+  bf16* act = reinterpret_cast<bf16*>(b + o_act);
+  float* logits = reinterpret_cast<float*>(b + o_logit);
+  float* part = reinterpret_cast<float*>(b + o_part);
+  int* tokens = reinterpret_cast<int*>(b + o_tok);
+  float* old_lp = reinterpret_cast<float*>(b + o_lp);
+  int* lengths = reinterpret_cast<int*>(b + o_len);
+  int* done = reinterpret_cast<int*>(b + o_done);
+  int* pos = reinterpret_cast<int*>(b + o_pos);
+  MRSP_CUDA(cudaMemsetAsync(tokens, 0, n_tok * 4, s));  // PAD
+  MRSP_CUDA(cudaMemsetAsync(old_lp, 0, n_tok * 4, s));
+  MRSP_CUDA(cudaMemsetAsync(lengths, 0, G * 4, s));
+  MRSP_CUDA(cudaMemsetAsync(done, 0, G * 4, s));
+  const LlmW& W = llm_[0];
+  const float scale = 1.0f / std::sqrt(128.0f);
+  std::vector<int> done_h(G);
+  // 3. decode steps: tokens -> embeddings -> 28 layers (G-row GEMMs, decode
+  // attention over prompt K/V + own-row K/V) -> LM head logits -> sample
+  for (int t = 0; t < max_len; ++t) {
+    decode_embed(W.embed, d, tokens, max_len, t, G, static_cast<int>(Lp + t), h, pos, s);
+    for (int l = 0; l < c.layers; ++l) {
+      const LlmLayerW& Lw = W.layers[l];
+      rmsnorm(h, d, Lw.attn_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      gemm_bf16({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr, 0},
+                s);
+      rope(qkv, Cqkv, 0, nq + nkv, pos, G, s);
+      bf16* rows_l = kv_rows + static_cast<size_t>(l) * max_len * G * kvw;
+      MRSP_CUDA(cudaMemcpy2DAsync(rows_l + static_cast<size_t>(t) * G * kvw, kvw * 2,
+                                  qkv + nq * 128, static_cast<size_t>(Cqkv) * 2, kvw * 2, G,
+                                  cudaMemcpyDeviceToDevice, s));
+      decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
+                       rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t, qpk,
+                       nkv, scale, part, od, Cq, s);
+      gemm_bf16({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d}, s);
+      rmsnorm(h, d, Lw.mlp_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      gemm_bf16({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
+                 nullptr, 0},
+                s);
+      gemm_bf16({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
+                 nullptr, h, d},
+                s);
+    }
+    rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+    gemm_bf16({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
+               nullptr, 0},
+              s);
+    sample_tokens(logits, G, c.vocab, temperature, seed, t, done, tokens, old_lp, lengths, max_len,
+                  s);
+    if ((t & 15) == 15 || t == max_len - 1) {  // stop once every row has sampled EOS
+      MRSP_CUDA(cudaMemcpyAsync(done_h.data(), done, G * 4, cudaMemcpyDeviceToHost, s));
+      MRSP_CUDA(cudaStreamSynchronize(s));
+      bool all = true;
+      for (int v : done_h) all = all && v;
+      if (all) break;
+    }
+  }
+  MRSP_CUDA(cudaMemcpyAsync(tokens_out, tokens, n_tok * 4, cudaMemcpyDeviceToHost, s));
+  MRSP_CUDA(cudaMemcpyAsync(old_lp_out, old_lp, n_tok * 4, cudaMemcpyDeviceToHost, s));
+  MRSP_CUDA(cudaMemcpyAsync(lengths_out, lengths, G * 4, cudaMemcpyDeviceToHost, s));
+  MRSP_CUDA(cudaStreamSynchronize(s));
 }
 
 size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void* blob) {
@@ -1327,6 +1450,20 @@ extern "C" mrsp_status mrsp_engine_cache(mrsp_engine* e, int op, int arg, uint64
       e->impl->cache_capacity = arg;
     }
     if (size_out) *size_out = e->impl->cache_size();
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id,
+                                            const int32_t* question, int n_q, int G, int max_len,
+                                            float temperature, uint64_t seed, int32_t* tokens_out,
+                                            int32_t* lengths_out, float* old_logprobs_out) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && (question || n_q == 0) && tokens_out && lengths_out &&
+                     old_logprobs_out,
+                 MRSP_INVALID_ARGUMENT, "generate: null argument");
+    auto entry = lookup(e, video_id);
+    e->impl->generate(*entry, question, n_q, G, max_len, temperature, seed, tokens_out,
+                      lengths_out, old_logprobs_out);
   });
 }
 

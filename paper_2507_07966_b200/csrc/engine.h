@@ -132,6 +132,13 @@ class Engine {
       pad_reads{0}, a2a_bytes{0};
   size_t cache_size();
   void cache_clear();
+  // Rollout generation (policy.cpp:121-157): G rows sampled
+  // autoregressively from the policy after the prompt [video | question],
+  // reusing the cached video embeddings and the prompt's K/V (one prefix
+  // prefill, then decode steps). SP = 1, one process.
+  void generate(const CacheEntry& emb, const int32_t* question, int n_q, int G, int max_len,
+                float temperature, uint64_t seed, int32_t* tokens_out, int32_t* lengths_out,
+                float* old_lp_out);
   // weights to / from safetensors with HF names (csrc/weights_io.cpp); part 0 =
   // vision tower + projector, 1 = policy LLM, 2 = reference LLM
   void save_weights(const std::string& path);
@@ -156,6 +163,10 @@ class Engine {
   void prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
                      const int32_t* resp, const int32_t* lengths, int G, int Lmax);
   void run_pass(const CacheEntry& emb, int model, int xs_slot);
+  // prefix K/V capture for generation (run_pass copies rows [0, Lp) of every
+  // layer's post-RoPE K and V when set): [layers][Lp][2 n_kv 128] bf16
+  DevBuf kv_prefix_;
+  bool capture_kv_ = false;
   void finish_group(int nvec, float* const* outs, bool out_on_device);
 
   struct GroupState {

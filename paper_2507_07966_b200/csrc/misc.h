@@ -27,4 +27,16 @@ void init_uniform_bf16(__nv_bfloat16* w, size_t n, uint64_t key, float scale, cu
 void init_uniform_f32(float* w, size_t n, uint64_t key, float scale, float offset, cudaStream_t s);
 void convert_bf16_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_t s);
 
+// rollout generation (csrc/decode.cu)
+size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv);
+void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
+                      const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
+                      int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,
+                      cudaStream_t s);
+void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len, int t, int G,
+                  int pos, float* hidden, int* pos_out, cudaStream_t s);
+void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed, int t,
+                   int* done, int* tokens, float* old_lp, int* lengths, int max_len,
+                   cudaStream_t s);
+
 }  // namespace mrsp

@@ -160,6 +160,20 @@ class Engine:
                                             policy_seed, ref_seed, int(with_ref), idb,
                                             ctypes.byref(self._h)))
 
+    # ---- rollout generation ------------------------------------------------
+    def generate(self, vid: str, question, G: int, max_len: int, temperature: float = 1.0,
+                 seed: int = 0):
+        """Samples G rollouts after [cached video | question]; returns
+        (tokens [G, max_len] int32, lengths [G], old_logprobs [G, max_len])."""
+        q = np.ascontiguousarray(np.asarray(question, dtype=np.int32))
+        tok = np.zeros((G, max_len), dtype=np.int32)
+        lens = np.zeros(G, dtype=np.int32)
+        olp = np.zeros((G, max_len), dtype=np.float32)
+        check(_lib.lib().mrsp_engine_generate(self._h, vid.encode(), _ptr(q), len(q), G, max_len,
+                                              float(temperature), int(seed), _ptr(tok), _ptr(lens),
+                                              _ptr(olp, ctypes.c_float)))
+        return tok, lens, olp
+
     # ---- weights (safetensors, HF names) -------------------------------------
     VISION, POLICY, REFERENCE = 0, 1, 2
 

@@ -1,0 +1,83 @@
+"""GPU: rollout generation (sample_rollout, policy.cpp:121-157)
+reusing the cached video embeddings and the prompt's K/V.
+
+The sampled tokens are checked by teacher forcing: the log-probabilities
+recorded while sampling (old_logprobs, temperature 1) must equal, within the
+BF16/FP32 tolerance, (a) the engine's own prefill log-probs of the same tokens
+(a different kernel path: full-sequence attention instead of decode attention
+over the cached K/V) and (b) the numpy fp64 oracle's. Plus the reference's
+sampling contract: EOS ends a row (and is its last token), PAD after it,
+lengths, seed determinism, argument errors."""
+import numpy as np
+import pytest
+
+from oracle import transformer as T
+from paper_2507_07966_b200 import _lib, engine as E
+
+pytestmark = pytest.mark.gpu
+
+W1 = E.workloads()["c1"]
+VSEED, PSEED, RSEED = 2, 3, 4
+EOS, PAD = 1, 0
+
+
+def _rows(tok, lens):
+    G, max_len = tok.shape
+    resp = np.zeros((G, max_len), dtype=np.int32)
+    for g in range(G):
+        resp[g, :lens[g]] = tok[g, :lens[g]]
+    return resp
+
+
+@pytest.fixture(scope="module")
+def gen():
+    c = T.Cfg.from_any(W1.cfg)
+    pix = E.gen_video(1, W1.frames, 3 * c.image_size ** 2)
+    q = np.array([10, 11, 12], dtype=np.int32)
+    eng = E.Engine(W1.cfg, sp=1, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    eng.encode("v", pix)
+    G, max_len = 16, 24
+    tok, lens, olp = eng.generate("v", q, G, max_len, temperature=1.0, seed=7)
+    yield dict(eng=eng, pix=pix, q=q, tok=tok, lens=lens, olp=olp, c=c)
+    eng.close()
+
+
+def test_generation_contract(gpu, gen):
+    tok, lens, olp = gen["tok"], gen["lens"], gen["olp"]
+    G, max_len = tok.shape
+    assert ((lens >= 1) & (lens <= max_len)).all()
+    for g in range(G):
+        n = lens[g]
+        body = tok[g, :n]
+        assert ((body >= 0) & (body < W1.cfg.vocab)).all()
+        assert (body[:-1] != EOS).all(), "EOS must end the row"
+        assert n == max_len or body[-1] == EOS
+        assert (tok[g, n:] == PAD).all() and (olp[g, :n] <= 0).all()
+    assert (lens < max_len).any() or (tok == EOS).sum() == 0  # V = 32: some rows end early
+
+
+def test_old_logprobs_match_prefill_and_oracle(gpu, gen):
+    eng, q, tok, lens, olp, c = gen["eng"], gen["q"], gen["tok"], gen["lens"], gen["olp"], gen["c"]
+    resp = _rows(tok, lens)
+    grp = E.Group(q, resp, lens.astype(np.int32))
+    want_engine = eng.prefill_logprobs("v", grp, 0)
+    got = np.concatenate([olp[g, :lens[g]] for g in range(len(lens))])
+    d = np.abs(got - want_engine)
+    assert d.max() <= 5e-2 and d.mean() <= 5e-3, ("vs engine prefill", d.max(), d.mean())
+    emb = T.vision_forward(c, T.vision_weights(c, VSEED), gen["pix"])
+    want_oracle, _ = T.llm_logprobs(c, T.llm_weights(c, PSEED, "policy."), emb, q, resp, lens)
+    d = np.abs(got - want_oracle)
+    assert d.max() <= 5e-2 and d.mean() <= 5e-3, ("vs oracle", d.max(), d.mean())
+
+
+def test_seed_determinism_and_errors(gpu, gen):
+    eng, q = gen["eng"], gen["q"]
+    a = eng.generate("v", q, 4, 10, temperature=0.7, seed=123)
+    b = eng.generate("v", q, 4, 10, temperature=0.7, seed=123)
+    c = eng.generate("v", q, 4, 10, temperature=0.7, seed=124)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert not np.array_equal(a[0], c[0])
+    with pytest.raises(_lib.InvalidArgument):
+        eng.generate("v", q, 4, 10, temperature=0.0)  # sample_rollout: temperature must be > 0
+    with pytest.raises(_lib.InvalidArgument):
+        eng.generate("v", q, 4, 0)  # max_len must be >= 1
