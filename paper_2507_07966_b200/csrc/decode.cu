@@ -26,7 +26,7 @@ namespace {
 
 constexpr int DEC_QN = 64;      // max queries per kv head (q_per_kv x G)
 constexpr int DEC_KT = 64;      // keys per smem tile
-constexpr int DEC_CHUNK = 1024; // keys per CTA
+constexpr int DEC_CHUNK = 512;  // keys per CTA
 constexpr int HD = 128;
 
 struct DecArgs {
@@ -41,13 +41,20 @@ struct DecArgs {
   float* part;  // [n_chunks][n_kv][DEC_QN][HD + 2]
 };
 
+// Register-blocked CUDA-core flash-decoding tile loop. 256 threads; per 64-key
+// tile: S[64 q][64 k] with a 4 q x 4 k block per thread (float4 smem loads
+// along the head dim: 16 FMAs per 2 LDS.128), online softmax per query row
+// (a row's 64 scores live in 16 lanes of one warp), then O[64 q][128 d] +=
+// P.V with a 4 q x 8 d block per thread (32 FMAs per 3 LDS.128).
 __global__ void __launch_bounds__(256)
     dec_attn_kernel(DecArgs a) {
-  extern __shared__ float sm[];
-  float* Qs = sm;                          // [DEC_QN][HD]
-  float* Ks = Qs + DEC_QN * HD;            // [DEC_KT][HD + 1]
-  float* Vs = Ks + DEC_KT * (HD + 1);      // [DEC_KT][HD]
-  float* Ps = Vs + DEC_KT * HD;            // [DEC_QN][DEC_KT + 1]
+  extern __shared__ __align__(16) float sm[];
+  constexpr int QS = HD + 4;                  // padded row strides (floats)
+  float* Qs = sm;                             // [DEC_QN][QS]
+  float* Ks = Qs + DEC_QN * QS;               // [DEC_KT][QS]
+  float* Vs = Ks + DEC_KT * QS;               // [DEC_KT][HD]
+  float* Pt = Vs + DEC_KT * HD;               // [DEC_KT][DEC_QN]  (P transposed)
+  float* row_alpha = Pt + DEC_KT * DEC_QN;    // [DEC_QN]
   const int chunk = blockIdx.x, kvh = blockIdx.y, tid = threadIdx.x;
   const int qn = a.q_per_kv * a.G;
   const bool rows_src = chunk >= a.n_prefix_chunks;
@@ -55,8 +62,7 @@ __global__ void __launch_bounds__(256)
   const long k_total = rows_src ? static_cast<long>(a.t + 1) * a.G : a.Lp;
   const long k_end = std::min<long>(k_begin + DEC_CHUNK, k_total);
   const __nv_bfloat16* src = rows_src ? a.kv_rows : a.kv_prefix;
-  // queries: index qi = hl * G + g (hl: head within the kv group)
-  for (int i = tid; i < DEC_QN * HD; i += blockDim.x) {
+  for (int i = tid; i < DEC_QN * HD; i += blockDim.x) {  // qi = hl * G + g
     const int qi = i / HD, d = i % HD;
     float v = 0.f;
     if (qi < qn) {
@@ -64,88 +70,132 @@ __global__ void __launch_bounds__(256)
       v = __bfloat162float(a.q[static_cast<size_t>(g) * a.ldq + a.q_col0 +
                                (kvh * a.q_per_kv + hl) * HD + d]);
     }
-    Qs[i] = v;
+    Qs[qi * QS + d] = v * a.scale_log2;  // scores come out in the log2 domain
   }
-  // thread -> (query, 16 keys) for S, (query, 32 head dims) for O
-  const int q = tid >> 2, sub = tid & 3;
-  const int g_of_q = q % max(a.G, 1);
-  float m = -INFINITY, l = 0.f, o[32];
+  // S mapping: query block qb (4 rows) x keys kb + 16 c (c < 4): the 16 lanes
+  // of a row group read 16 consecutive K rows (row stride 132 floats -> a
+  // different 4-bank group per lane, no conflicts; 4 kb + c was 8-way)
+  const int qb = tid >> 4, kb = tid & 15;
+  // O mapping: query block ob (4 rows), head-dim block db (8 dims)
+  const int ob = tid >> 4, db = tid & 15;
+  float m_row[4], l_row[4];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) o[j] = 0.f;
+  for (int r = 0; r < 4; ++r) {
+    m_row[r] = -INFINITY;
+    l_row[r] = 0.f;
+  }
+  float o[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[r][j] = 0.f;
   for (long k0 = k_begin; k0 < k_end; k0 += DEC_KT) {
     __syncthreads();
-    for (int i = tid; i < DEC_KT * (HD / 8); i += blockDim.x) {  // 16-byte loads
+    for (int i = tid; i < DEC_KT * (HD / 8); i += blockDim.x) {  // 16-byte global loads
       const int kk = i / (HD / 8), c8 = (i % (HD / 8)) * 8;
       const long k = k0 + kk;
-      float kv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, vv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
       if (k < k_end) {
         const __nv_bfloat16* row = src + static_cast<size_t>(k) * a.ld_kv;
-        const uint4 ku = *reinterpret_cast<const uint4*>(row + kvh * HD + c8);
-        const uint4 vu = *reinterpret_cast<const uint4*>(row + a.v_off + kvh * HD + c8);
-        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ku);
-        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vu);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 kf = __bfloat1622float2(k2[e]), vf = __bfloat1622float2(v2[e]);
-          kv[2 * e] = kf.x;
-          kv[2 * e + 1] = kf.y;
-          vv[2 * e] = vf.x;
-          vv[2 * e + 1] = vf.y;
-        }
+        ku = *reinterpret_cast<const uint4*>(row + kvh * HD + c8);
+        vu = *reinterpret_cast<const uint4*>(row + a.v_off + kvh * HD + c8);
       }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        Ks[kk * (HD + 1) + c8 + e] = kv[e];
-        Vs[kk * HD + c8 + e] = vv[e];
-      }
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ku);
+      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vu);
+      float4* kd = reinterpret_cast<float4*>(Ks + kk * QS + c8);
+      float4* vd = reinterpret_cast<float4*>(Vs + kk * HD + c8);
+      const float2 k01 = __bfloat1622float2(k2[0]), k23 = __bfloat1622float2(k2[1]);
+      const float2 k45 = __bfloat1622float2(k2[2]), k67 = __bfloat1622float2(k2[3]);
+      const float2 v01 = __bfloat1622float2(v2[0]), v23 = __bfloat1622float2(v2[1]);
+      const float2 v45 = __bfloat1622float2(v2[2]), v67 = __bfloat1622float2(v2[3]);
+      kd[0] = make_float4(k01.x, k01.y, k23.x, k23.y);
+      kd[1] = make_float4(k45.x, k45.y, k67.x, k67.y);
+      vd[0] = make_float4(v01.x, v01.y, v23.x, v23.y);
+      vd[1] = make_float4(v45.x, v45.y, v67.x, v67.y);
     }
     __syncthreads();
-    // scores for 16 keys of this thread's query (log2 domain)
-    float s[16];
-    float mx = -INFINITY;
+    float sc[4][4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int kk = sub * 16 + j;
-      const long k = k0 + kk;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int d = 0; d < HD; ++d) acc = fmaf(Qs[q * HD + d], Ks[kk * (HD + 1) + d], acc);
-      bool vis = q < qn && k < k_end;
-      if (rows_src) vis = vis && static_cast<int>(k % a.G) == g_of_q;  // own row only
-      s[j] = vis ? acc * a.scale_log2 : -INFINITY;
-      mx = fmaxf(mx, s[j]);
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sc[r][c] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < HD; d += 4) {
+      float4 qv[4], kv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) qv[r] = *reinterpret_cast<const float4*>(Qs + (qb * 4 + r) * QS + d);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) kv[c] = *reinterpret_cast<const float4*>(Ks + (kb + 16 * c) * QS + d);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          sc[r][c] = fmaf(qv[r].x, kv[c].x, fmaf(qv[r].y, kv[c].y,
+                     fmaf(qv[r].z, kv[c].z, fmaf(qv[r].w, kv[c].w, sc[r][c]))));
     }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float m_new = fmaxf(m, mx);
-    const float alpha = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
-    float ls = 0.f;
+    // mask, online softmax per row (the row's 64 scores: 16 lanes x 4)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float p = m_new == -INFINITY ? 0.f : exp2f(s[j] - m_new);
-      Ps[q * (DEC_KT + 1) + sub * 16 + j] = p;
-      ls += p;
+    for (int r = 0; r < 4; ++r) {
+      const int qi = qb * 4 + r;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const long k = k0 + kb + 16 * c;
+        bool vis = qi < qn && k < k_end;
+        if (rows_src) vis = vis && static_cast<int>(k % a.G) == qi % a.G;  // own row only
+        if (!vis) sc[r][c] = -INFINITY;
+        mx = fmaxf(mx, sc[r][c]);
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float m_new = fmaxf(m_row[r], mx);
+      const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_row[r] - m_new);
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float p = m_new == -INFINITY ? 0.f : exp2f(sc[r][c] - m_new);
+        Pt[(kb + 16 * c) * DEC_QN + qi] = p;
+        ls += p;
+      }
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+      l_row[r] = l_row[r] * alpha + ls;
+      m_row[r] = m_new;
+      if (kb == 0) row_alpha[qi] = alpha;
     }
-    ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-    ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-    l = l * alpha + ls;
-    m = m_new;
-    __syncwarp();
+    __syncthreads();
+    float al[4];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) o[j] *= alpha;
+    for (int r = 0; r < 4; ++r) al[r] = row_alpha[ob * 4 + r];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[r][j] *= al[r];
+#pragma unroll 4
     for (int kk = 0; kk < DEC_KT; ++kk) {
-      const float p = Ps[q * (DEC_KT + 1) + kk];
+      const float4 pv = *reinterpret_cast<const float4*>(Pt + kk * DEC_QN + ob * 4);
+      const float4 v0 = *reinterpret_cast<const float4*>(Vs + kk * HD + db * 8);
+      const float4 v1 = *reinterpret_cast<const float4*>(Vs + kk * HD + db * 8 + 4);
+      const float pr[4] = {pv.x, pv.y, pv.z, pv.w};
+      const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-      for (int j = 0; j < 32; ++j) o[j] = fmaf(p, Vs[kk * HD + sub * 32 + j], o[j]);
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[r][j] = fmaf(pr[r], vv[j], o[r][j]);
     }
   }
-  if (q < qn) {
-    float* out = a.part + ((static_cast<size_t>(chunk) * a.n_kv + kvh) * DEC_QN + q) * (HD + 2);
+  // partial (m, l, O): the S-mapping threads hold (m, l) of rows qb*4+r, the
+  // O-mapping threads hold O of rows ob*4+r (same block index: qb == ob)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) out[sub * 32 + j] = o[j];
-    if (sub == 0) {
-      out[HD] = m;
-      out[HD + 1] = l;
+  for (int r = 0; r < 4; ++r) {
+    const int qi = ob * 4 + r;
+    if (qi >= qn) continue;
+    float* out = a.part + ((static_cast<size_t>(chunk) * a.n_kv + kvh) * DEC_QN + qi) * (HD + 2);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[db * 8 + j] = o[r][j];
+    if (db == 0) {
+      out[HD] = m_row[r];
+      out[HD + 1] = l_row[r];
     }
   }
 }
@@ -334,7 +384,7 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   a.scale_log2 = scale * 1.4426950408889634f;
   a.part = part;
   const size_t smem =
-      (DEC_QN * HD + DEC_KT * (HD + 1) + DEC_KT * HD + DEC_QN * (DEC_KT + 1)) * sizeof(float);
+      (DEC_QN * (HD + 4) + DEC_KT * (HD + 4) + DEC_KT * HD + DEC_KT * DEC_QN + DEC_QN) * sizeof(float);
   static const bool attr = [smem] {
     MRSP_CUDA(cudaFuncSetAttribute(dec_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
