@@ -17,9 +17,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.h"
 #include "misc.h"
+#include "sm100.cuh"
+#include "tma.h"
 
 namespace mrsp {
 namespace {
@@ -200,6 +204,237 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core decode attention (long prompts): one CTA per (chunk, kv head),
+// the <= 64 queries of the kv group as one 128-row Q tile (zero rows pad it)
+// written to smem in the SW128 K-major layout, 128-key K/V tiles by TMA
+// through a 4-slot ring, S = Q.K^T and O += P.V on tcgen05 with S, P (bf16
+// over S) and O in TMEM — the prefill kernel's tile pipeline for one Q tile.
+// Same unnormalised (m, l, O) partial as the CUDA-core kernel.
+namespace tc {
+using namespace sm100;
+constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK, RING = 4;
+constexpr int OFF_Q = 0, OFF_RING = TILE, OFF_BAR = OFF_RING + RING * TILE;
+constexpr size_t SMEM = 1024 + OFF_BAR + 256;
+
+struct Args {
+  const __nv_bfloat16* q;
+  int ldq, q_col0, G, t, Lp, q_per_kv, n_kv, n_prefix_chunks, chunk_keys;
+  int v_off;
+  float scale_log2;
+  float* part;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    dec_attn_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmR,
+                       Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* q_ready = bars;
+  uint64_t* r_full = bars + 1;        // [RING]
+  uint64_t* r_empty = r_full + RING;  // [RING]
+  uint64_t* s_full = r_empty + RING;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* pv_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  const int warp = warp_id(), chunk = blockIdx.x, kvh = blockIdx.y;
+  const int qn = a.q_per_kv * a.G;
+  const bool rows_src = chunk >= a.n_prefix_chunks;
+  const long k_begin = static_cast<long>(rows_src ? chunk - a.n_prefix_chunks : chunk) * a.chunk_keys;
+  const long k_total = rows_src ? static_cast<long>(a.t + 1) * a.G : a.Lp;
+  const long k_end = std::min<long>(k_begin + a.chunk_keys, k_total);
+  const int n_tiles = static_cast<int>((k_end - k_begin + TK - 1) / TK);
+  const CUtensorMap* tm = rows_src ? &tmR : &tmP;
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(tm);
+    mbar_init(q_ready, 128);
+    for (int i = 0; i < RING; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S [0,128) (P over its first 64), O [128,256)
+  if (warp == 0) {
+    if (elect_one()) {  // K_j, V_j alternate through the ring
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < n_tiles; ++j)
+        for (int kv = 0; kv < 2; ++kv) {
+          mbar_wait(&r_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&r_full[slot], TILE);
+          uint8_t* dst = smem + OFF_RING + slot * TILE;
+          const int col = (kv ? a.v_off : 0) + kvh * 128;
+          const int row = static_cast<int>(k_begin) + j * TK;
+          tma_load_2d(dst, tm, &r_full[slot], col, row);
+          tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, row);
+          if (++slot == RING) { slot = 0; ph ^= 1; }
+        }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc_s = idesc_bf16_f32(TQ, TK), idesc_o = idesc_bf16_f32_bmn(TQ, 128);
+    const uint32_t q_addr = smem_u32(smem + OFF_Q), ring = smem_u32(smem + OFF_RING);
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(&r_full[slot], ph);  // K_j
+      tc_fence_after();
+      const uint32_t k_addr = ring + slot * TILE;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk / 4) * CHUNK + (kk % 4) * 32;
+          mma_bf16_ss(tmem, sdesc_sw128(q_addr + off), sdesc_sw128(k_addr + off), idesc_s,
+                      kk > 0 ? 1u : 0u);
+        }
+        mma_commit(s_full);
+        mma_commit(&r_empty[slot]);
+      }
+      __syncwarp();
+      if (++slot == RING) { slot = 0; ph ^= 1; }
+      mbar_wait(p_full, j & 1);
+      mbar_wait(&r_full[slot], ph);  // V_j
+      tc_fence_after();
+      const uint32_t v_addr = ring + slot * TILE;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_bf16_ts(tmem + 128, tmem + kk * 8, sdesc_sw128_mn(v_addr + kk * 2048, CHUNK), idesc_o,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(pv_done);
+        mma_commit(&r_empty[slot]);
+      }
+      __syncwarp();
+      if (++slot == RING) { slot = 0; ph ^= 1; }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane_id();  // query row = TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    {  // Q row r -> smem, SW128 K-major: 16-byte unit u of a 128-byte row at u ^ (r & 7)
+      uint4 v[16];
+      if (r < qn) {
+        const int hl = r / a.G, g = r % a.G;
+        const uint4* src = reinterpret_cast<const uint4*>(
+            a.q + static_cast<size_t>(g) * a.ldq + a.q_col0 + (kvh * a.q_per_kv + hl) * 128);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = src[u];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int half = u / 8, uu = u % 8;
+        *reinterpret_cast<uint4*>(smem + OFF_Q + half * CHUNK + r * 128 + ((uu ^ (r & 7)) * 16)) = v[u];
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(q_ready);
+    }
+    const int g_of_r = r % a.G;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      float s[TK];
+      {
+        uint32_t x0[32], x1[32], x2[32], x3[32];
+        tmem_ld32(tmem + lane_off + 0, x0);
+        tmem_ld32(tmem + lane_off + 32, x1);
+        tmem_ld32(tmem + lane_off + 64, x2);
+        tmem_ld32(tmem + lane_off + 96, x3);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(x0[i]);
+          s[32 + i] = __uint_as_float(x1[i]);
+          s[64 + i] = __uint_as_float(x2[i]);
+          s[96 + i] = __uint_as_float(x3[i]);
+        }
+      }
+      const long k0 = k_begin + static_cast<long>(j) * TK;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < TK; ++i) {
+        const long k = k0 + i;
+        bool vis = r < qn && k < k_end;
+        if (rows_src) vis = vis && static_cast<int>(k % a.G) == g_of_r;
+        s[i] = vis ? s[i] * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      const float m_new = fmaxf(m_run, mx);
+      if (j > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O (after P.V(j-1))
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        const float alpha = m_new > m_run && m_run != -INFINITY ? exp2f(m_run - m_new) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + 128 + c, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_off + 128 + c, o);
+        }
+        tmem_st_wait();
+        l_run *= alpha;
+      }
+      m_run = m_new;
+      const float nm = m_run == -INFINITY ? 0.f : -m_run;
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = exp2f(s[c * 64 + 2 * i] + nm), p1 = exp2f(s[c * 64 + 2 * i + 1] + nm);
+          acc += p0 + p1;
+          w[i] = pack_bf16(p0, p1);
+        }
+        tmem_st32(tmem + lane_off + c * 32, w);
+      }
+      tmem_st_wait();
+      l_run += acc;
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // epilogue: the unnormalised partial of this chunk
+    if (n_tiles > 0) {
+      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    float* out = a.part + ((static_cast<size_t>(chunk) * a.n_kv + kvh) * DEC_QN + r) * (HD + 2);
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_off + 128 + c, o);
+      tmem_ld_wait();
+      if (r < qn)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) out[c + i] = n_tiles > 0 ? __uint_as_float(o[i]) : 0.f;
+    }
+    if (r < qn) {
+      out[HD] = n_tiles > 0 ? m_run : -INFINITY;
+      out[HD + 1] = l_run;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<256>(tmem);
+}
+}  // namespace tc
+
 // O[g][h*128 + d] = sum_c O_c 2^(m_c - m) / sum_c l_c 2^(m_c - m)
 __global__ void dec_merge_kernel(const float* __restrict__ part, int n_chunks, int n_kv,
                                  int q_per_kv, int G, __nv_bfloat16* __restrict__ out, int ldo) {
@@ -360,10 +595,27 @@ size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv) {
   return static_cast<size_t>(chunks) * n_kv * DEC_QN * (HD + 2) * sizeof(float);
 }
 
+// Kernel choice: the tcgen05 kernel wins once the prompt K/V stream dominates
+// (c4, 131K tokens: 10.9 vs 18.3 ms per decode step); for short prompts the
+// register-blocked CUDA-core kernel's lower fixed cost wins (c2, 16K tokens).
+// MRSP_DECODE_CC=1 / 0 forces one.
+bool decode_use_tensor_cores(int Lp) {
+  const char* e = std::getenv("MRSP_DECODE_CC");
+  if (e) return std::atoi(e) == 0;
+  return Lp >= 32768;
+}
+
+void decode_tensor_maps(const void* kv_prefix, int Lp, const void* kv_rows, long rows, int ld_kv,
+                        void* maps_out) {
+  CUtensorMap* m = static_cast<CUtensorMap*>(maps_out);
+  m[0] = make_tmap_bf16_2d(kv_prefix, std::max(Lp, 1), ld_kv, ld_kv, 128, 64);
+  m[1] = make_tmap_bf16_2d(kv_rows, std::max<long>(rows, 1), ld_kv, ld_kv, 128, 64);
+}
+
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                       const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
                       int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,
-                      cudaStream_t s) {
+                      cudaStream_t s, const void* maps) {
   MRSP_REQUIRE(q_per_kv * G <= DEC_QN, MRSP_INVALID_ARGUMENT,
                "generate: q_per_kv x G must be <= 64");
   DecArgs a;
@@ -383,6 +635,45 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   a.n_row_chunks = ((t + 1) * G + DEC_CHUNK - 1) / DEC_CHUNK;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.part = part;
+  if (decode_use_tensor_cores(Lp)) {
+    tc::Args ta;
+    ta.q = a.q;
+    ta.ldq = ldq;
+    ta.q_col0 = q_col0;
+    ta.G = G;
+    ta.t = t;
+    ta.Lp = Lp;
+    ta.q_per_kv = q_per_kv;
+    ta.n_kv = n_kv;
+    ta.n_prefix_chunks = a.n_prefix_chunks;
+    ta.chunk_keys = DEC_CHUNK;
+    ta.v_off = v_off;
+    ta.scale_log2 = a.scale_log2;
+    ta.part = part;
+    static const bool tc_attr = [] {
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tc::SMEM)));
+      return true;
+    }();
+    (void)tc_attr;
+    // prompt K|V [Lp][ld_kv] and the row cache as TMA tensors (rows past the
+    // current step are masked; the caller's row cache is zero-initialised)
+    CUtensorMap tm[2];
+    if (maps)
+      std::memcpy(tm, maps, sizeof(tm));
+    else
+      decode_tensor_maps(kv_prefix, Lp, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
+    const int chunks = a.n_prefix_chunks + a.n_row_chunks;
+    tc::dec_attn_tc_kernel<<<dim3(chunks, n_kv), 256, tc::SMEM, s>>>(tm[0], tm[1], ta);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    dec_merge_kernel<<<dim3(q_per_kv * G, n_kv), HD, 0, s>>>(part, chunks, n_kv, q_per_kv, G,
+                                                             static_cast<__nv_bfloat16*>(out), ldo);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    return;
+  }
   const size_t smem =
       (DEC_QN * (HD + 4) + DEC_KT * (HD + 4) + DEC_KT * HD + DEC_KT * DEC_QN + DEC_QN) * sizeof(float);
   static const bool attr = [smem] {

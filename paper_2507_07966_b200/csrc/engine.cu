@@ -13,6 +13,7 @@
 //   run_step               engine.cpp:203-225 -> mrsp_engine_step
 #include "engine.h"
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -1139,6 +1140,14 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   int* lengths = reinterpret_cast<int*>(b + o_len);
   int* done = reinterpret_cast<int*>(b + o_done);
   int* pos = reinterpret_cast<int*>(b + o_pos);
+  MRSP_CUDA(cudaMemsetAsync(kv_rows, 0, static_cast<size_t>(c.layers) * max_len * G * kvw * 2, s));
+  // TMA descriptors of every layer's prompt K/V and row cache, built once
+  const bool tc_decode = decode_use_tensor_cores(static_cast<int>(Lp));
+  std::vector<CUtensorMap> maps(tc_decode ? 2 * c.layers : 0);
+  for (int l = 0; tc_decode && l < c.layers; ++l)
+    decode_tensor_maps(kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw, static_cast<int>(Lp),
+                       kv_rows + static_cast<size_t>(l) * max_len * G * kvw,
+                       static_cast<long>(max_len) * G, static_cast<int>(kvw), &maps[2 * l]);
   MRSP_CUDA(cudaMemsetAsync(tokens, 0, n_tok * 4, s));  // PAD
   MRSP_CUDA(cudaMemsetAsync(old_lp, 0, n_tok * 4, s));
   MRSP_CUDA(cudaMemsetAsync(lengths, 0, G * 4, s));
@@ -1162,7 +1171,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
                                   cudaMemcpyDeviceToDevice, s));
       decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
                        rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t, qpk,
-                       nkv, scale, part, od, Cq, s);
+                       nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
       gemm_bf16({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d}, s);
       rmsnorm(h, d, Lw.mlp_norm, xn, d, G, d, c.rms_eps, nullptr, s);
       gemm_bf16({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,

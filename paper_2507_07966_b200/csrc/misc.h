@@ -29,10 +29,15 @@ void convert_bf16_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_
 
 // rollout generation (csrc/decode.cu)
 size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv);
+// maps: optional TMA descriptors {prompt K|V [Lp][ld_kv], row cache [rows][ld_kv]}
+// built once per generation (decode_tensor_maps) so a step encodes none
+bool decode_use_tensor_cores(int Lp);
+void decode_tensor_maps(const void* kv_prefix, int Lp, const void* kv_rows, long rows, int ld_kv,
+                        void* maps_out /* 2 x CUtensorMap */);
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                       const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
                       int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,
-                      cudaStream_t s);
+                      cudaStream_t s, const void* maps = nullptr);
 void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len, int t, int G,
                   int pos, float* hidden, int* pos_out, cudaStream_t s);
 void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed, int t,

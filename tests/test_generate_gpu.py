@@ -81,3 +81,17 @@ def test_seed_determinism_and_errors(gpu, gen):
         eng.generate("v", q, 4, 10, temperature=0.0)  # sample_rollout: temperature must be > 0
     with pytest.raises(_lib.InvalidArgument):
         eng.generate("v", q, 4, 0)  # max_len must be >= 1
+
+
+@pytest.mark.parametrize("cc", ["0", "1"])
+def test_decode_kernels_agree(gpu, gen, cc, monkeypatch):
+    """Both decode-attention kernels (tcgen05 / CUDA cores) give old log-probs that
+    match the engine's prefill of the sampled tokens."""
+    monkeypatch.setenv("MRSP_DECODE_CC", cc)
+    eng, q = gen["eng"], gen["q"]
+    tok, lens, olp = eng.generate("v", q, 8, 16, temperature=0.8, seed=99)
+    grp = E.Group(q, _rows(tok, lens), lens.astype(np.int32))
+    want = eng.prefill_logprobs("v", grp, 0)
+    got = np.concatenate([olp[g, :lens[g]] for g in range(len(lens))])
+    d = np.abs(got - want)
+    assert d.max() <= 5e-2 and d.mean() <= 5e-3, (cc, d.max(), d.mean())
