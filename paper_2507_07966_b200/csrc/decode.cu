@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(256)
 // Same unnormalised (m, l, O) partial as the CUDA-core kernel.
 namespace tc {
 using namespace sm100;
-constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK, RING = 4;
+constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK, RING = 2;
+constexpr int KEYS = 2048;  // keys per CTA: 16 tiles amortise the CTA setup; 96 KB smem -> 2 CTAs/SM
 constexpr int OFF_Q = 0, OFF_RING = TILE, OFF_BAR = OFF_RING + RING * TILE;
 constexpr size_t SMEM = 1024 + OFF_BAR + 256;
 
@@ -225,7 +226,7 @@ struct Args {
   float* part;
 };
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     dec_attn_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmR,
                        Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -343,34 +344,26 @@ __global__ void __launch_bounds__(256, 1)
     }
     const int g_of_r = r % a.G;
     float m_run = -INFINITY, l_run = 0.f;
+    // two passes over S in TMEM (32 columns at a time, <= 128 registers per
+    // thread so two CTAs share an SM): row max, then exp / P / row sum
+    auto visible = [&](long k) {
+      bool vis = r < qn && k < k_end;
+      if (rows_src) vis = vis && static_cast<int>(k % a.G) == g_of_r;
+      return vis;
+    };
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
-      float s[TK];
-      {
-        uint32_t x0[32], x1[32], x2[32], x3[32];
-        tmem_ld32(tmem + lane_off + 0, x0);
-        tmem_ld32(tmem + lane_off + 32, x1);
-        tmem_ld32(tmem + lane_off + 64, x2);
-        tmem_ld32(tmem + lane_off + 96, x3);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = __uint_as_float(x0[i]);
-          s[32 + i] = __uint_as_float(x1[i]);
-          s[64 + i] = __uint_as_float(x2[i]);
-          s[96 + i] = __uint_as_float(x3[i]);
-        }
-      }
       const long k0 = k_begin + static_cast<long>(j) * TK;
       float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < TK; c += 32) {
+        uint32_t x[32];
+        tmem_ld32(tmem + lane_off + c, x);
+        tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < TK; ++i) {
-        const long k = k0 + i;
-        bool vis = r < qn && k < k_end;
-        if (rows_src) vis = vis && static_cast<int>(k % a.G) == g_of_r;
-        s[i] = vis ? s[i] * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < 32; ++i)
+          if (visible(k0 + c + i)) mx = fmaxf(mx, __uint_as_float(x[i]) * a.scale_log2);
       }
       const float m_new = fmaxf(m_run, mx);
       if (j > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O (after P.V(j-1))
@@ -392,16 +385,26 @@ __global__ void __launch_bounds__(256, 1)
       m_run = m_new;
       const float nm = m_run == -INFINITY ? 0.f : -m_run;
       float acc = 0.f;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {  // 64-key halves: P(half h) -> columns [32 h, 32 h + 32),
+        uint32_t w[32];               // over S columns whose keys are already consumed
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t w[32];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = h * 64 + cc * 32;
+          uint32_t x[32];
+          tmem_ld32(tmem + lane_off + c, x);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = exp2f(s[c * 64 + 2 * i] + nm), p1 = exp2f(s[c * 64 + 2 * i + 1] + nm);
-          acc += p0 + p1;
-          w[i] = pack_bf16(p0, p1);
+          for (int i = 0; i < 32; i += 2) {
+            const float p0 =
+                visible(k0 + c + i) ? exp2f(__uint_as_float(x[i]) * a.scale_log2 + nm) : 0.f;
+            const float p1 =
+                visible(k0 + c + i + 1) ? exp2f(__uint_as_float(x[i + 1]) * a.scale_log2 + nm) : 0.f;
+            acc += p0 + p1;
+            w[cc * 16 + i / 2] = pack_bf16(p0, p1);
+          }
         }
-        tmem_st32(tmem + lane_off + c * 32, w);
+        tmem_st32(tmem + lane_off + 32 * h, w);
       }
       tmem_st_wait();
       l_run += acc;
@@ -645,8 +648,8 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     ta.Lp = Lp;
     ta.q_per_kv = q_per_kv;
     ta.n_kv = n_kv;
-    ta.n_prefix_chunks = a.n_prefix_chunks;
-    ta.chunk_keys = DEC_CHUNK;
+    ta.n_prefix_chunks = (Lp + tc::KEYS - 1) / tc::KEYS;
+    ta.chunk_keys = tc::KEYS;
     ta.v_off = v_off;
     ta.scale_log2 = a.scale_log2;
     ta.part = part;
@@ -664,7 +667,7 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
       std::memcpy(tm, maps, sizeof(tm));
     else
       decode_tensor_maps(kv_prefix, Lp, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
-    const int chunks = a.n_prefix_chunks + a.n_row_chunks;
+    const int chunks = ta.n_prefix_chunks + ((t + 1) * G + tc::KEYS - 1) / tc::KEYS;
     tc::dec_attn_tc_kernel<<<dim3(chunks, n_kv), 256, tc::SMEM, s>>>(tm[0], tm[1], ta);
     count_launch();
     MRSP_CUDA(cudaGetLastError());

@@ -1158,35 +1158,66 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   // 3. decode steps: tokens -> embeddings -> 28 layers (G-row GEMMs, decode
   // attention over prompt K/V + own-row K/V) -> LM head logits -> sample
   for (int t = 0; t < max_len; ++t) {
-    decode_embed(W.embed, d, tokens, max_len, t, G, static_cast<int>(Lp + t), h, pos, s);
+    {
+      Prof pm(*this, P_MISC);
+      decode_embed(W.embed, d, tokens, max_len, t, G, static_cast<int>(Lp + t), h, pos, s);
+    }
     for (int l = 0; l < c.layers; ++l) {
       const LlmLayerW& Lw = W.layers[l];
-      rmsnorm(h, d, Lw.attn_norm, xn, d, G, d, c.rms_eps, nullptr, s);
-      gemm_bf16({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr, 0},
-                s);
-      rope(qkv, Cqkv, 0, nq + nkv, pos, G, s);
+      {
+        Prof pm(*this, P_MISC);
+        rmsnorm(h, d, Lw.attn_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      }
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr,
+                   0},
+                  s);
+      }
       bf16* rows_l = kv_rows + static_cast<size_t>(l) * max_len * G * kvw;
-      MRSP_CUDA(cudaMemcpy2DAsync(rows_l + static_cast<size_t>(t) * G * kvw, kvw * 2,
-                                  qkv + nq * 128, static_cast<size_t>(Cqkv) * 2, kvw * 2, G,
-                                  cudaMemcpyDeviceToDevice, s));
-      decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
-                       rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t, qpk,
-                       nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
-      gemm_bf16({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d}, s);
-      rmsnorm(h, d, Lw.mlp_norm, xn, d, G, d, c.rms_eps, nullptr, s);
-      gemm_bf16({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
+      {
+        Prof pm(*this, P_MISC);
+        rope(qkv, Cqkv, 0, nq + nkv, pos, G, s);
+        MRSP_CUDA(cudaMemcpy2DAsync(rows_l + static_cast<size_t>(t) * G * kvw, kvw * 2,
+                                    qkv + nq * 128, static_cast<size_t>(Cqkv) * 2, kvw * 2, G,
+                                    cudaMemcpyDeviceToDevice, s));
+      }
+      {
+        Prof pa(*this, P_ATTN);
+        decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
+                         rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t,
+                         qpk, nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
+      }
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d}, s);
+      }
+      {
+        Prof pm(*this, P_MISC);
+        rmsnorm(h, d, Lw.mlp_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      }
+      {
+        Prof pg(*this, P_GEMM);
+        gemm_bf16({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
+                   nullptr, 0},
+                  s);
+        gemm_bf16({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
+                   nullptr, h, d},
+                  s);
+      }
+    }
+    {
+      Prof pl(*this, P_LMHEAD);
+      rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      gemm_bf16({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
                  nullptr, 0},
                 s);
-      gemm_bf16({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
-                 nullptr, h, d},
-                s);
     }
-    rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
-    gemm_bf16({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
-               nullptr, 0},
-              s);
-    sample_tokens(logits, G, c.vocab, temperature, seed, t, done, tokens, old_lp, lengths, max_len,
-                  s);
+    {
+      Prof psm(*this, P_MISC);
+      sample_tokens(logits, G, c.vocab, temperature, seed, t, done, tokens, old_lp, lengths,
+                    max_len, s);
+    }
     if ((t & 15) == 15 || t == max_len - 1) {  // stop once every row has sampled EOS
       MRSP_CUDA(cudaMemcpyAsync(done_h.data(), done, G * 4, cudaMemcpyDeviceToHost, s));
       MRSP_CUDA(cudaStreamSynchronize(s));
@@ -1199,6 +1230,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   MRSP_CUDA(cudaMemcpyAsync(old_lp_out, old_lp, n_tok * 4, cudaMemcpyDeviceToHost, s));
   MRSP_CUDA(cudaMemcpyAsync(lengths_out, lengths, G * 4, cudaMemcpyDeviceToHost, s));
   MRSP_CUDA(cudaStreamSynchronize(s));
+  prof_collect();
 }
 
 size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void* blob) {

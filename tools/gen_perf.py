@@ -17,12 +17,16 @@ pix = torch.from_numpy(E.gen_video(1, w.frames, 3 * S * S)).cuda()
 eng.encode("v", pix)
 q = np.arange(10, 10 + w.n_question, dtype=np.int32)
 eng.generate("v", q, G, 4, seed=1)  # warm
-t = {}
+t, prof = {}, {}
 for n in (8, 40):
+    eng.profile(True)
     torch.cuda.synchronize(); t0 = time.perf_counter()
     tok, lens, _ = eng.generate("v", q, G, n, seed=2)
     torch.cuda.synchronize(); t[n] = time.perf_counter() - t0
+    prof[n] = eng.profile(False)
     assert (lens == n).all(), lens
+# device time per decode step by class (prefill cancels in the difference)
+per_step = {k: round((prof[40][k][0] - prof[8][k][0]) / 32, 3) for k in prof[40]}
 step = (t[40] - t[8]) / 32
 L, d, nq, nkv, mlp, V = c.layers, c.dim, c.n_q_heads, c.n_kv_heads, c.mlp, c.vocab
 weights = 2 * (L * (d * (nq + 2 * nkv) * 128 + nq * 128 * d + 3 * d * mlp) + V * d)
@@ -33,4 +37,5 @@ ideal = (weights + kv) / (peaks["hbm_gbs"] * 1e9)
 print(json.dumps({"workload": name, "G": G, "prompt_tokens": Lp, "prefill_plus_8_steps_s": round(t[8], 3),
                   "decode_step_ms": round(step * 1e3, 3), "tokens_per_s": round(G / step, 1),
                   "hbm_bytes_per_step": weights + kv, "hbm_roofline_step_ms": round(ideal * 1e3, 3),
-                  "roofline_frac": round(ideal / step, 3)}), flush=True)
+                  "roofline_frac": round(ideal / step, 3), "device_ms_per_step_by_class": per_step}),
+      flush=True)
