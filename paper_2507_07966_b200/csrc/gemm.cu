@@ -38,12 +38,17 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;  // two 128x256 fp32 accumulators
 constexpr int THREADS = 256;
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+// Staged epilogue: per epilogue warp two 32-row x 128-byte boxes (SW128) that
+// TMA stores (or reduce-adds) to global while the next box is being filled.
+constexpr int OUT_BOX = 32 * 128;
+constexpr int OUT_BYTES = 4 * 2 * OUT_BOX;
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + OUT_BYTES + 256;
 
 struct EpiArgs {
   int M, N, K;
   int epi;
   int vec_ok;  // output/residual rows are 16-byte aligned -> vector stores
+  int staged;  // epilogue goes through smem + TMA store / reduce-add (tmC)
   void* C;
   int ldc;
   const float* bias;
@@ -274,13 +279,118 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
   }
 }
 
+// Uniform (warp-broadcast) bias loads for `n` columns starting at `col`;
+// columns at or past N read as 0 (their outputs are clipped by the TMA store).
+// No bias reads as -0, the additive identity (x + -0 == x, signed zeros kept).
+template <int n>
+__device__ __forceinline__ void load_bias(const float* bias, int col, int N, float (&b)[n]) {
+  if (bias == nullptr) {
+#pragma unroll
+    for (int j = 0; j < n; ++j) b[j] = -0.f;
+  } else if (col + n <= N) {
+#pragma unroll
+    for (int j = 0; j < n; j += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(bias + col + j));
+      b[j] = x.x; b[j + 1] = x.y; b[j + 2] = x.z; b[j + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < n; ++j) b[j] = col + j < N ? bias[col + j] : 0.f;
+  }
+}
+
+// Staged epilogue of one warp's 32 accumulator rows: per 128-byte output chunk
+// (64 bf16 or 32 fp32 columns) TMEM -> registers -> fused op -> this warp's
+// SW128 smem box (row = lane; 16-byte unit u of row r at u ^ (r & 7), so the
+// row-per-lane st.shared are conflict-free) -> one TMA store (fp32 residual:
+// TMA reduce-add in L2, i.e. resid += v rounded once, as the load/add/store
+// path). Two boxes per warp: filling one overlaps the other's bulk copy.
+// Rows past M / columns past N are clipped by the TMA unit.
+__device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUtensorMap* tmC,
+                                                uint32_t t_row, int ew, int mt, int nt,
+                                                uint8_t* boxes, uint32_t& buf) {
+  const int lane = lane_id();
+  const int y = mt * BM + ew * 32;
+  const bool f32 = args.epi == GEMM_EPI_RESID_F32 || args.epi == GEMM_EPI_STORE_F32;
+  const bool swiglu = args.epi == GEMM_EPI_SWIGLU_BF16;
+  const int out_cols = swiglu ? BN / 2 : BN;
+  const int col0 = nt * out_cols;
+  const int out_n = swiglu ? args.N / 2 : args.N;
+#pragma unroll 1
+  for (int c = 0; c < out_cols; c += f32 ? 32 : 64) {
+    if (col0 + c >= out_n) break;  // warp-uniform: the whole box is past N
+    uint32_t w[32];  // this lane's 128 output bytes
+    if (f32) {
+      uint32_t r[32];
+      tmem_ld32(t_row + c, r);
+      float b[32];
+      load_bias<32>(args.bias, col0 + c, args.N, b);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(__uint_as_float(r[j]) + b[j]);
+    } else if (swiglu) {
+#pragma unroll
+      for (int h = 0; h < 64; h += 32) {
+        uint32_t g[32], u[32];
+        tmem_ld32(t_row + c + h, g);
+        tmem_ld32(t_row + BN / 2 + c + h, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          w[h / 2 + j] = pack_bf16(silu(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]),
+                                   silu(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]));
+      }
+    } else {
+      const bool gelu = args.epi == GEMM_EPI_BIAS_GELU_BF16;
+#pragma unroll
+      for (int h = 0; h < 64; h += 32) {
+        uint32_t r[32];
+        tmem_ld32(t_row + c + h, r);
+        float b[32];
+        load_bias<32>(args.bias, col0 + c + h, args.N, b);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float v0 = __uint_as_float(r[2 * j]) + b[2 * j];
+          float v1 = __uint_as_float(r[2 * j + 1]) + b[2 * j + 1];
+          if (gelu) {
+            v0 = gelu_tanh(v0);
+            v1 = gelu_tanh(v1);
+          }
+          w[h / 2 + j] = pack_bf16(v0, v1);
+        }
+      }
+    }
+    uint8_t* box = boxes + buf * OUT_BOX;
+    if (lane == 0) bulk_wait_read<1>();  // the copy that last read this box is done
+    __syncwarp();
+    const uint32_t row = smem_u32(box) + lane * 128;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      st_shared_v4(row + ((u ^ (lane & 7)) << 4), w[4 * u], w[4 * u + 1], w[4 * u + 2],
+                   w[4 * u + 3]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (args.epi == GEMM_EPI_RESID_F32)
+        tma_reduce_add_2d(tmC, smem_u32(box), col0 + c, y);
+      else
+        tma_store_2d(tmC, smem_u32(box), col0 + c, y);
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB, EpiArgs args) {
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* out_boxes = smem + STAGES * STAGE_BYTES;  // [4 warps][2][OUT_BOX]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_boxes + OUT_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -295,6 +405,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (args.staged) tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -359,6 +470,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;  // TMEM lanes [32 ew, 32 ew + 32)
+    uint8_t* boxes = out_boxes + ew * 2 * OUT_BOX;
+    uint32_t buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -369,11 +482,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int row = mt * BM + ew * 32 + lane_id();
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
+      if (args.staged)
+        epilogue_staged(args, &tmC, t_row, ew, mt, nt, boxes, buf);
+      else
+        epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (args.staged && lane_id() == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -578,7 +695,7 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   const int ld_out = g.epi == GEMM_EPI_RESID_F32 ? g.ldr : g.ldc;
   const int elem_per_16b = (f32_out || g.epi == GEMM_EPI_RESID_F32) ? 4 : 8;
   const int vec_ok = (out_addr % 16 == 0) && (ld_out % elem_per_16b == 0);
-  EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     g.C,        g.ldc,
+  EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     0,          g.C,        g.ldc,
             g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
             g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld};
   if (g.epi == GEMM_EPI_QKV_SCATTER)
@@ -614,9 +731,41 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     MRSP_CUDA(cudaGetLastError());
     return;
   }
+  // TMA-store epilogue for the plain / bias / GELU / SwiGLU / fp32 / residual
+  // outputs when the output rows meet the tensor-map alignment rules
+  // (MRSP_GEMM_EPI_DIRECT=1 keeps the per-row global-store epilogue).
+  static const bool direct_env = [] {
+    const char* v = std::getenv("MRSP_GEMM_EPI_DIRECT");
+    return v != nullptr && std::atoi(v) != 0;
+  }();
+  CUtensorMap tc = ta;
+  if (vec_ok && !direct_env) {
+    switch (g.epi) {
+      case GEMM_EPI_STORE_BF16:
+      case GEMM_EPI_BIAS_BF16:
+      case GEMM_EPI_BIAS_GELU_BF16:
+        tc = make_tmap_bf16_2d(g.C, g.M, g.N, g.ldc, 32, 64);
+        e.staged = 1;
+        break;
+      case GEMM_EPI_SWIGLU_BF16:
+        tc = make_tmap_bf16_2d(g.C, g.M, g.N / 2, g.ldc, 32, 64);
+        e.staged = 1;
+        break;
+      case GEMM_EPI_STORE_F32:
+        tc = make_tmap_f32_2d(g.C, g.M, g.N, g.ldc, 32, 32);
+        e.staged = 1;
+        break;
+      case GEMM_EPI_RESID_F32:
+        tc = make_tmap_f32_2d(g.resid, g.M, g.N, g.ldr, 32, 32);
+        e.staged = 1;
+        break;
+      default:
+        break;
+    }
+  }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = std::min(tiles, num_sms());
-  gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, e);
+  gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, tc, e);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

@@ -49,4 +49,26 @@ inline CUtensorMap make_tmap_bf16_2d(const void* base, uint64_t rows, uint64_t c
   return m;
 }
 
+// 2-D fp32 tensor [rows][cols], row pitch `ld` elements (epilogue stores /
+// reduce-adds of fp32 outputs and the residual stream).
+inline CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                                    uint32_t box_rows, uint32_t box_cols,
+                                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  MRSP_REQUIRE((ld * 4) % 16 == 0, MRSP_INVALID_ARGUMENT,
+               "TMA: row pitch must be a multiple of 16 bytes");
+  MRSP_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, MRSP_INVALID_ARGUMENT,
+               "TMA: base must be 16-byte aligned");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t elem[2] = {1, 1};
+  CUresult r = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+                                 dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MRSP_REQUIRE(r == CUDA_SUCCESS, MRSP_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
 }  // namespace mrsp
