@@ -99,6 +99,39 @@ mrsp_status mrsp_toy_prefill(int sp_degree, const double* theta, int V, int d, i
                              const uint64_t* lengths, uint64_t n_rows, uint64_t max_len,
                              const uint64_t* ranges, double* out, uint64_t* pad_reads);
 
+/* Backward of the toy policy: grpo_gradient
+ * (grpo.cpp:122-206 over GradAccumulator, policy.cpp:195-260) and
+ * sft_loss_and_grad (grpo.cpp:208-223) on the device. Replaces those two
+ * reference functions (grpo.hpp:52-62) for a sequence given as its frame
+ * embeddings + text tokens (MultimodalSequence, mmseq.hpp).
+ *   theta, ref    host, param_count(V, d, h) doubles each (policy.hpp:39-56)
+ *   frame_emb     host, n_frames x d;  text_tokens host, n_text
+ *   tokens        host, the rollouts' tokens concatenated (sum(lengths));
+ *                 old_logprobs likewise; advantages host, n_rollouts
+ *   ranges        host, 2 * sp_degree: ShardPlan over the longest rollout's
+ *                 positions (as mrsp_toy_prefill); rank w runs the positions
+ *                 t in [b_w, e_w) of every rollout
+ *   grad          host out, param_count doubles
+ *   stats         host out, 4: objective, mean_kl, clip_fraction, token_count
+ * The position terms run sharded; the parameter sums run in the reference's
+ * serial (rollout, t) order, so every sp_degree returns the same bits.
+ * Errors: empty group / rollout / targets, token or text token out of range,
+ * empty sequence -> MRSP_INVALID_ARGUMENT. */
+mrsp_status mrsp_toy_grpo_gradient(int sp_degree, const double* theta, const double* ref, int V,
+                                   int d, int h, const double* frame_emb, uint64_t n_frames,
+                                   const int32_t* text_tokens, uint64_t n_text,
+                                   const int32_t* tokens, const uint64_t* lengths,
+                                   uint64_t n_rollouts, const double* old_logprobs,
+                                   const double* advantages, double clip_eps, double kl_beta,
+                                   int sampled_kl, const uint64_t* ranges, double* grad,
+                                   double* stats);
+/* loss: host out, 1 (mean teacher-forced cross-entropy); ranges over n_targets */
+mrsp_status mrsp_toy_sft_loss_and_grad(int sp_degree, const double* theta, int V, int d, int h,
+                                       const double* frame_emb, uint64_t n_frames,
+                                       const int32_t* text_tokens, uint64_t n_text,
+                                       const int32_t* targets, uint64_t n_targets,
+                                       const uint64_t* ranges, double* loss, double* grad);
+
 /* ------------------------------------------------------------------------
  * Device operators of the transformer-shaped path (dev pointers, async on
  * `stream`). They are the building blocks the engine below chains; exported

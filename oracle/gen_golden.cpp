@@ -7,7 +7,9 @@
 // rows (engine.cpp:31-50), synthetic frames (mmseq.cpp:58-72), encoder and
 // policy init (policy.cpp:12-34, :56-61), encode_frame (policy.cpp:36-47),
 // serial_prefill/step_logits (engine.cpp:59-71, policy.cpp:85-119),
-// log_softmax (common.hpp:95-104) and cache/bench counters (engine.cpp:155-283).
+// log_softmax (common.hpp:95-104), cache/bench counters (engine.cpp:155-283),
+// GRPO stats (grpo.cpp:68-108) and the analytic GRPO / SFT gradients
+// (grpo.cpp:122-223, policy.cpp:195-260).
 #include <cstdio>
 #include <fstream>
 #include <iostream>
@@ -158,6 +160,27 @@ int main(int argc, char** argv) {
     j["grpo"] = {{"rollouts", rolls}, {"advantages", group.advantages.values},
                  {"clip_eps", cfg.clip_eps}, {"kl_beta", cfg.kl_beta},
                  {"stats_exact_kl", st(exact)}, {"stats_sampled_kl", st(sampled)}};
+
+    // Backward (grpo.cpp:122-223, policy.cpp:195-260): the reference's exact
+    // analytic gradients on the same group and sequence — exact KL, sampled
+    // (k3) KL, no KL — and SFT loss + gradient on the sample's SFT target.
+    grpo::GroupStats g_exact, g_sampled, g_nokl;
+    cfg.sampled_kl = false;
+    Vec grad_exact = grpo::grpo_gradient(group, theta, ref, seq, cfg, &g_exact);
+    cfg.sampled_kl = true;
+    Vec grad_sampled = grpo::grpo_gradient(group, theta, ref, seq, cfg, &g_sampled);
+    cfg.sampled_kl = false;
+    cfg.kl_beta = 0.0;
+    Vec grad_nokl = grpo::grpo_gradient(group, theta, ref, seq, cfg, &g_nokl);
+    auto target = grpo::sft_target(sample);
+    auto [sft_loss, sft_grad] = grpo::sft_loss_and_grad(theta, seq, target);
+    j["backward"] = {{"theta", theta.theta}, {"ref", ref.theta},
+                     {"frame_embeddings", seq.frame_embeddings}, {"text_tokens", seq.text_tokens},
+                     {"clip_eps", 0.2}, {"kl_beta", 0.04},
+                     {"grad_exact_kl", grad_exact}, {"stats_exact_kl", st(g_exact)},
+                     {"grad_sampled_kl", grad_sampled}, {"stats_sampled_kl", st(g_sampled)},
+                     {"grad_no_kl", grad_nokl}, {"stats_no_kl", st(g_nokl)},
+                     {"sft_target", target}, {"sft_loss", sft_loss}, {"sft_grad", sft_grad}};
   }
 
   std::ofstream(path) << j.dump(1) << "\n";

@@ -230,3 +230,204 @@ int oracle_context_vector(const double* theta, int V, int d, const double* frame
   for (int k = 0; k < d; ++k) ctx[k] *= inv;
   return 0;
 }
+
+/* ---- backward: GradAccumulator (policy.cpp:195-260) ---- */
+typedef struct {
+  const double* theta;
+  int V, d, h;
+  const double* ctx; /* context_vector(seq, theta) */
+  double* grad;      /* param_count */
+  double* d_ctx;     /* d */
+} grad_acc;
+
+/* add_position (policy.cpp:202-247): logits = U s + b, s = tanh(A ctx + B e_prev + c) */
+static void acc_add_position(grad_acc* a, int prev, const double* g_logits) {
+  const int V = a->V, d = a->d, h = a->h;
+  const double* A = a->theta + (long)V * d;
+  const double* B = A + (long)h * d;
+  const double* c = B + (long)h * d;
+  const double* U = c + h;
+  const double* e_prev = a->theta + (long)prev * d;
+  double* gE = a->grad;
+  double* gA = gE + (long)V * d;
+  double* gB = gA + (long)h * d;
+  double* gc = gB + (long)h * d;
+  double* gU = gc + h;
+  double* gb = gU + (long)V * h;
+  double* s = (double*)malloc(sizeof(double) * (size_t)h);
+  double* ds = (double*)calloc((size_t)h, sizeof(double));
+  for (int r = 0; r < h; ++r) { /* hidden_state (policy.cpp:85-101) */
+    double z = c[r];
+    for (int k = 0; k < d; ++k) z += A[(long)r * d + k] * a->ctx[k] + B[(long)r * d + k] * e_prev[k];
+    s[r] = tanh(z);
+  }
+  for (int v = 0; v < V; ++v) {
+    double g = g_logits[v];
+    if (g == 0.0) continue;
+    gb[v] += g;
+    for (int r = 0; r < h; ++r) {
+      gU[(long)v * h + r] += g * s[r];
+      ds[r] += g * U[(long)v * h + r];
+    }
+  }
+  for (int r = 0; r < h; ++r) {
+    double dz = ds[r] * (1.0 - s[r] * s[r]);
+    if (dz == 0.0) continue;
+    gc[r] += dz;
+    for (int k = 0; k < d; ++k) {
+      gA[(long)r * d + k] += dz * a->ctx[k];
+      gB[(long)r * d + k] += dz * e_prev[k];
+      gE[(long)prev * d + k] += dz * B[(long)r * d + k];
+      a->d_ctx[k] += dz * A[(long)r * d + k];
+    }
+  }
+  free(s);
+  free(ds);
+}
+
+/* take (policy.cpp:249-260): text rows receive d_context / total_len each */
+static void acc_take(grad_acc* a, const int32_t* text, long n_text, long total_len) {
+  double inv = 1.0 / (double)total_len;
+  for (long i = 0; i < n_text; ++i)
+    for (int k = 0; k < a->d; ++k) a->grad[(long)text[i] * a->d + k] += inv * a->d_ctx[k];
+}
+
+static long theta_count(int V, int d, int h) {
+  return (long)V * d + 2L * h * d + h + (long)V * h + V;
+}
+
+/* grpo_gradient (grpo.cpp:122-206). Rollouts packed: tokens / old_lp are the
+ * concatenation of the G rollouts (lengths[i] >= 1 each). stats = {objective,
+ * mean_kl, clip_fraction, token_count}. Returns 0, or -1 on bad input. */
+int oracle_grpo_gradient(const double* theta, const double* ref, int V, int d, int h,
+                         const double* frame_emb, long n_frames, const int32_t* text, long n_text,
+                         const int32_t* tokens, const long* lengths, long G, const double* old_lp,
+                         const double* adv, double clip_eps, double kl_beta, int sampled_kl,
+                         double* grad, double* stats) {
+  if (G < 1) return -1;
+  long n_tokens = 0;
+  for (long i = 0; i < G; ++i) {
+    if (lengths[i] < 1) return -1;
+    n_tokens += lengths[i];
+  }
+  double* ctx_ref = (double*)malloc(sizeof(double) * (size_t)d);
+  double* ctx_theta = (double*)malloc(sizeof(double) * (size_t)d);
+  if (oracle_context_vector(ref, V, d, frame_emb, n_frames, text, n_text, ctx_ref) ||
+      oracle_context_vector(theta, V, d, frame_emb, n_frames, text, n_text, ctx_theta)) {
+    free(ctx_ref);
+    free(ctx_theta);
+    return -1;
+  }
+  memset(grad, 0, sizeof(double) * (size_t)theta_count(V, d, h));
+  double* d_ctx = (double*)calloc((size_t)d, sizeof(double));
+  grad_acc acc = {theta, V, d, h, ctx_theta, grad, d_ctx};
+  double* lg = (double*)malloc(sizeof(double) * (size_t)V);
+  double* lp = (double*)malloc(sizeof(double) * (size_t)V);
+  double* lp_ref = (double*)malloc(sizeof(double) * (size_t)V);
+  double* pi = (double*)malloc(sizeof(double) * (size_t)V);
+  double* g = (double*)malloc(sizeof(double) * (size_t)V);
+  double kl_sum = 0.0, policy_term = 0.0;
+  long n_clipped = 0, o = 0;
+  const double Gd = (double)G;
+  const double kl_w = -kl_beta / (double)n_tokens;
+  int bad = 0;
+  for (long i = 0; i < G && !bad; ++i) {
+    const double a = adv[i];
+    const double tok_w = 1.0 / (Gd * (double)lengths[i]);
+    double seq_term = 0.0;
+    int prev = 1; /* Vocab::kEos */
+    for (long t = 0; t < lengths[i]; ++t, ++o) {
+      int y = tokens[o];
+      if (y < 0 || y >= V) { bad = 1; break; }
+      oracle_step_logits(theta, V, d, h, ctx_theta, prev, lg);
+      oracle_log_softmax(lg, V, lp);
+      oracle_step_logits(ref, V, d, h, ctx_ref, prev, lg);
+      oracle_log_softmax(lg, V, lp_ref);
+      for (int v = 0; v < V; ++v) pi[v] = exp(lp[v]);
+      double ratio = exp(lp[y] - old_lp[o]);
+      double lo = 1.0 - clip_eps, hi = 1.0 + clip_eps;
+      double clipped = ratio < lo ? lo : (hi < ratio ? hi : ratio); /* std::clamp */
+      double u1 = ratio * a, u2 = clipped * a;
+      seq_term += u2 < u1 ? u2 : u1; /* std::min */
+      int plateau = (a > 0 && ratio > 1.0 + clip_eps) || (a < 0 && ratio < 1.0 - clip_eps);
+      if (plateau) ++n_clipped;
+      for (int v = 0; v < V; ++v) g[v] = 0.0;
+      if (a != 0.0 && !plateau) {
+        double coeff = tok_w * a * ratio;
+        for (int v = 0; v < V; ++v) g[v] -= coeff * pi[v];
+        g[y] += coeff;
+      }
+      if (kl_beta != 0.0) {
+        if (sampled_kl) {
+          double lr = lp_ref[y] - lp[y];
+          kl_sum += exp(lr) - 1.0 - lr;
+          double coeff = kl_w * (1.0 - exp(lr));
+          for (int v = 0; v < V; ++v) g[v] -= coeff * pi[v];
+          g[y] += coeff;
+        } else {
+          double kl = 0.0;
+          for (int v = 0; v < V; ++v) kl += pi[v] * (lp[v] - lp_ref[v]);
+          kl_sum += kl;
+          for (int v = 0; v < V; ++v) g[v] += kl_w * pi[v] * (lp[v] - lp_ref[v] - kl);
+        }
+      } else if (sampled_kl) {
+        double lr = lp_ref[y] - lp[y];
+        kl_sum += exp(lr) - 1.0 - lr;
+      } else {
+        double kl = 0.0;
+        for (int v = 0; v < V; ++v) kl += pi[v] * (lp[v] - lp_ref[v]);
+        kl_sum += kl;
+      }
+      acc_add_position(&acc, prev, g);
+      prev = y;
+    }
+    policy_term += seq_term / (double)lengths[i] / Gd;
+  }
+  if (!bad) {
+    acc_take(&acc, text, n_text, n_frames + n_text);
+    stats[3] = (double)n_tokens;
+    stats[1] = kl_sum / (double)n_tokens;
+    stats[2] = (double)n_clipped / (double)n_tokens;
+    stats[0] = policy_term - kl_beta * stats[1];
+  }
+  free(ctx_ref); free(ctx_theta); free(d_ctx); free(lg); free(lp); free(lp_ref); free(pi); free(g);
+  return bad ? -1 : 0;
+}
+
+/* sft_loss_and_grad (grpo.cpp:208-223) */
+int oracle_sft_loss_and_grad(const double* theta, int V, int d, int h, const double* frame_emb,
+                             long n_frames, const int32_t* text, long n_text,
+                             const int32_t* targets, long n_targets, double* loss, double* grad) {
+  if (n_targets < 1) return -1;
+  double* ctx = (double*)malloc(sizeof(double) * (size_t)d);
+  if (oracle_context_vector(theta, V, d, frame_emb, n_frames, text, n_text, ctx)) {
+    free(ctx);
+    return -1;
+  }
+  memset(grad, 0, sizeof(double) * (size_t)theta_count(V, d, h));
+  double* d_ctx = (double*)calloc((size_t)d, sizeof(double));
+  grad_acc acc = {theta, V, d, h, ctx, grad, d_ctx};
+  double* lg = (double*)malloc(sizeof(double) * (size_t)V);
+  double* lp = (double*)malloc(sizeof(double) * (size_t)V);
+  double* g = (double*)malloc(sizeof(double) * (size_t)V);
+  const double inv_t = 1.0 / (double)n_targets;
+  double l = 0.0;
+  int prev = 1, bad = 0;
+  for (long t = 0; t < n_targets; ++t) {
+    int y = targets[t];
+    if (y < 0 || y >= V) { bad = 1; break; }
+    oracle_step_logits(theta, V, d, h, ctx, prev, lg);
+    oracle_log_softmax(lg, V, lp);
+    l += -lp[y];
+    for (int v = 0; v < V; ++v) g[v] = inv_t * exp(lp[v]);
+    g[y] -= inv_t;
+    acc_add_position(&acc, prev, g);
+    prev = y;
+  }
+  if (!bad) {
+    acc_take(&acc, text, n_text, n_frames + n_text);
+    *loss = l * inv_t;
+  }
+  free(ctx); free(d_ctx); free(lg); free(lp); free(g);
+  return bad ? -1 : 0;
+}

@@ -45,6 +45,14 @@ def lib():
         l.oracle_log_softmax.argtypes = [_d, ctypes.c_int, _d]
         l.oracle_context_vector.argtypes = [_d, ctypes.c_int, ctypes.c_int, _d, ctypes.c_long, _i32,
                                             ctypes.c_long, _d]
+        _l64 = ctypes.POINTER(ctypes.c_long)
+        l.oracle_grpo_gradient.argtypes = [_d, _d, ctypes.c_int, ctypes.c_int, ctypes.c_int, _d,
+                                           ctypes.c_long, _i32, ctypes.c_long, _i32, _l64,
+                                           ctypes.c_long, _d, _d, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_int, _d, _d]
+        l.oracle_sft_loss_and_grad.argtypes = [_d, ctypes.c_int, ctypes.c_int, ctypes.c_int, _d,
+                                               ctypes.c_long, _i32, ctypes.c_long, _i32,
+                                               ctypes.c_long, _d, _d]
         _l = l
     return _l
 
@@ -140,3 +148,43 @@ def context_vector(theta, V, d, frame_emb, text):
                                    _p(text, ctypes.c_int32), text.shape[0], _p(out)):
         raise ValueError("context_vector: bad input")
     return out
+
+
+def grpo_gradient(theta, ref, V, d, h, frame_emb, text, tokens, old_logprobs, advantages,
+                  clip_eps=0.2, kl_beta=0.04, sampled_kl=False):
+    """grpo_gradient (grpo.cpp:122-206) -> (grad, stats dict). `tokens` and
+    `old_logprobs` are per-rollout lists."""
+    frame_emb = np.ascontiguousarray(frame_emb, dtype=np.float64).reshape(-1, d)
+    text = np.ascontiguousarray(text, dtype=np.int32)
+    lens = np.array([len(t) for t in tokens], dtype=np.int64)
+    tok = np.ascontiguousarray(np.concatenate([np.asarray(t, dtype=np.int32) for t in tokens]))
+    old = np.ascontiguousarray(np.concatenate([np.asarray(o, dtype=np.float64)
+                                               for o in old_logprobs]))
+    adv = np.ascontiguousarray(advantages, dtype=np.float64)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    ref = np.ascontiguousarray(ref, dtype=np.float64)
+    grad = np.zeros(theta.shape[0])
+    st = np.zeros(4)
+    if lib().oracle_grpo_gradient(_p(theta), _p(ref), V, d, h, _p(frame_emb), frame_emb.shape[0],
+                                  _p(text, ctypes.c_int32), text.shape[0],
+                                  _p(tok, ctypes.c_int32), _p(lens, ctypes.c_long), lens.shape[0],
+                                  _p(old), _p(adv), clip_eps, kl_beta, int(sampled_kl), _p(grad),
+                                  _p(st)):
+        raise ValueError("grpo_gradient: bad input")
+    return grad, {"objective": st[0], "mean_kl": st[1], "clip_fraction": st[2],
+                  "token_count": int(st[3])}
+
+
+def sft_loss_and_grad(theta, V, d, h, frame_emb, text, targets):
+    """sft_loss_and_grad (grpo.cpp:208-223) -> (loss, grad)."""
+    frame_emb = np.ascontiguousarray(frame_emb, dtype=np.float64).reshape(-1, d)
+    text = np.ascontiguousarray(text, dtype=np.int32)
+    tg = np.ascontiguousarray(targets, dtype=np.int32)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    grad = np.zeros(theta.shape[0])
+    loss = np.zeros(1)
+    if lib().oracle_sft_loss_and_grad(_p(theta), V, d, h, _p(frame_emb), frame_emb.shape[0],
+                                      _p(text, ctypes.c_int32), text.shape[0],
+                                      _p(tg, ctypes.c_int32), tg.shape[0], _p(loss), _p(grad)):
+        raise ValueError("sft_loss_and_grad: bad input")
+    return float(loss[0]), grad

@@ -65,6 +65,14 @@ _sig("mrsp_toy_encode", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, c_f64
                          c_u64p, c_f64p, c_u64p])
 _sig("mrsp_toy_prefill", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_f64p,
                           c_i32p, c_u64p, ctypes.c_uint64, ctypes.c_uint64, c_u64p, c_f64p, c_u64p])
+_sig("mrsp_toy_grpo_gradient", [ctypes.c_int, c_f64p, c_f64p, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int, c_f64p, ctypes.c_uint64, c_i32p, ctypes.c_uint64,
+                                c_i32p, c_u64p, ctypes.c_uint64, c_f64p, c_f64p, ctypes.c_double,
+                                ctypes.c_double, ctypes.c_int, c_u64p, c_f64p, c_f64p])
+_sig("mrsp_toy_sft_loss_and_grad", [ctypes.c_int, c_f64p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, c_f64p, ctypes.c_uint64, c_i32p,
+                                    ctypes.c_uint64, c_i32p, ctypes.c_uint64, c_u64p, c_f64p,
+                                    c_f64p])
 _sig("mrsp_op_gemm_bf16", [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                            ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,

@@ -307,10 +307,9 @@ __device__ __forceinline__ void load_bias(const float* bias, int col, int N, flo
 // path). Two boxes per warp: filling one overlaps the other's bulk copy.
 // Rows past M / columns past N are clipped by the TMA unit.
 __device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUtensorMap* tmC,
-                                                uint32_t t_row, int ew, int mt, int nt,
-                                                uint8_t* boxes, uint32_t& buf) {
+                                                uint32_t t_row, int y, int nt, uint8_t* boxes,
+                                                uint32_t& buf) {
   const int lane = lane_id();
-  const int y = mt * BM + ew * 32;
   const bool f32 = args.epi == GEMM_EPI_RESID_F32 || args.epi == GEMM_EPI_STORE_F32;
   const bool swiglu = args.epi == GEMM_EPI_SWIGLU_BF16;
   const int out_cols = swiglu ? BN / 2 : BN;
@@ -483,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (args.staged)
-        epilogue_staged(args, &tmC, t_row, ew, mt, nt, boxes, buf);
+        epilogue_staged(args, &tmC, t_row, mt * BM + ew * 32, nt, boxes, buf);
       else
         epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
       tc_fence_before();
@@ -512,16 +511,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int P_STAGES = 6;
 constexpr int P_HALF = BM * BK * 2;           // 16 KB: 128 rows x 64 K
 constexpr int P_STAGE_BYTES = 2 * P_HALF;     // own A + own half of B
-constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + 512;
+constexpr size_t P_SMEM_BYTES = 1024 + P_STAGES * P_STAGE_BYTES + OUT_BYTES + 512;
 
 template <bool kRelay>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   EpiArgs args) {
+                   const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint8_t* out_boxes = smem + P_STAGES * P_STAGE_BYTES;  // [4 warps][2][OUT_BOX]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_boxes + OUT_BYTES);
   uint64_t* empty = full + P_STAGES;   // both CTAs: multicast MMA commit
   uint64_t* peer = empty + P_STAGES;   // leader: follower's stage landed (relay)
   uint64_t* tfull = peer + P_STAGES;   // [2] both CTAs: multicast MMA commit
@@ -540,6 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (args.staged) tma_prefetch_desc(&tmC);
     for (int s = 0; s < P_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -626,6 +627,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const uint32_t tempty_l = mapa_shared(smem_u32(tempty), 0);
+    uint8_t* boxes = out_boxes + ew * 2 * OUT_BOX;
+    uint32_t buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cl; tile < num_tiles; tile += n_cl) {
@@ -633,9 +636,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tile_coords(tile, m_tiles, n_tiles, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mt * 2 * BM + static_cast<int>(rank) * BM + ew * 32 + lane_id();
+      const int y = mt * 2 * BM + static_cast<int>(rank) * BM + ew * 32;
+      const int row = y + lane_id();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      epilogue_row(args, t_row, row, row < args.M, nt, n_tiles);
+      if (args.staged)
+        epilogue_staged(args, &tmC, t_row, y, nt, boxes, buf);
+      else
+        epilogue_row(args, t_row, row, row < args.M, nt, n_tiles);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
@@ -646,6 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (args.staged && lane_id() == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -705,32 +713,6 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   if (g.epi == GEMM_EPI_LOGPROB_PARTIAL)
     MRSP_REQUIRE(g.targets && g.part && g.tgt_logit, MRSP_INVALID_ARGUMENT,
                  "gemm logprob: null targets/partials");
-  // kernel choice (MRSP_GEMM_IMPL): 1 = single-CTA 128x256 tiles, 2 = CTA pair
-  // with the 2-SM TMA form, 3 = CTA pair with relayed stage completion
-  const char* env_impl = std::getenv("MRSP_GEMM_IMPL");
-  const int impl = env_impl ? std::atoi(env_impl) : kDefaultGemmImpl;
-  if (impl == 2 || impl == 3) {
-    static const bool pair_attr = [] {
-      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(P_SMEM_BYTES)));
-      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(P_SMEM_BYTES)));
-      return true;
-    }();
-    (void)pair_attr;
-    CUtensorMap tbh = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BM, BK);  // 128-row halves of B
-    const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
-    const int grid = 2 * std::min(tiles, num_sms() / 2);
-    if (impl == 3)
-      gemm_bf16_pair<true><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, e);
-    else
-      gemm_bf16_pair<false><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, e);
-    count_launch();
-    MRSP_CUDA(cudaGetLastError());
-    return;
-  }
   // TMA-store epilogue for the plain / bias / GELU / SwiGLU / fp32 / residual
   // outputs when the output rows meet the tensor-map alignment rules
   // (MRSP_GEMM_EPI_DIRECT=1 keeps the per-row global-store epilogue).
@@ -762,6 +744,32 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
       default:
         break;
     }
+  }
+  // kernel choice (MRSP_GEMM_IMPL): 1 = single-CTA 128x256 tiles, 2 = CTA pair
+  // with the 2-SM TMA form, 3 = CTA pair with relayed stage completion
+  const char* env_impl = std::getenv("MRSP_GEMM_IMPL");
+  const int impl = env_impl ? std::atoi(env_impl) : kDefaultGemmImpl;
+  if (impl == 2 || impl == 3) {
+    static const bool pair_attr = [] {
+      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(P_SMEM_BYTES)));
+      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_pair<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(P_SMEM_BYTES)));
+      return true;
+    }();
+    (void)pair_attr;
+    CUtensorMap tbh = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BM, BK);  // 128-row halves of B
+    const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
+    const int grid = 2 * std::min(tiles, num_sms() / 2);
+    if (impl == 3)
+      gemm_bf16_pair<true><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, tc, e);
+    else
+      gemm_bf16_pair<false><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, tc, e);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    return;
   }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int grid = std::min(tiles, num_sms());

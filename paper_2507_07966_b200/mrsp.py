@@ -267,3 +267,106 @@ class EmbeddingCache:
     def clear(self) -> None:
         with self._mu:
             self._map.clear()
+
+
+# ---- backward: grpo.hpp:14-62 ----
+
+@dataclass
+class MultimodalSequence:
+    """mmseq.hpp: the frame embeddings (n_frames x d) + the question's text tokens."""
+    frame_embeddings: np.ndarray
+    text_tokens: Sequence[int]
+
+
+@dataclass
+class Rollout:
+    """policy.hpp: sampled tokens + the log-probs recorded while sampling."""
+    tokens: Sequence[int]
+    old_logprobs: Sequence[float]
+
+
+@dataclass
+class RolloutGroup:
+    """grpo.hpp:34-38 (advantages = Advantages::values)."""
+    rollouts: List[Rollout]
+    advantages: Sequence[float]
+    sample_id: str = ""
+
+
+@dataclass
+class GrpoConfig:
+    """grpo.hpp:14-23 (the fields the objective and gradient read)."""
+    clip_eps: float = 0.2
+    kl_beta: float = 0.04
+    sampled_kl: bool = False
+
+
+@dataclass
+class GroupStats:
+    """grpo.hpp:40-45."""
+    objective: float = 0.0
+    mean_kl: float = 0.0
+    clip_fraction: float = 0.0
+    token_count: int = 0
+
+
+def _seq_arrays(params: PolicyParams, seq: MultimodalSequence):
+    fe = np.ascontiguousarray(seq.frame_embeddings, dtype=np.float64).reshape(-1, params.d)
+    text = np.ascontiguousarray(np.asarray(seq.text_tokens, dtype=np.int32))
+    return fe, text
+
+
+def grpo_gradient(group: RolloutGroup, theta: PolicyParams, ref: PolicyParams,
+                  seq: MultimodalSequence, cfg: GrpoConfig, sp_degree: int = 1):
+    """grpo.cpp:122-206 on the device -> (grad, GroupStats). The positions run
+    sharded over `sp_degree` ranks (plan_shards over the longest rollout)."""
+    if not group.rollouts:
+        raise InvalidArgument(1, "grpo: empty rollout group")
+    for r in group.rollouts:
+        if len(r.tokens) == 0:
+            raise InvalidArgument(1, "grpo: empty rollout")
+        if len(r.old_logprobs) != len(r.tokens):
+            raise InvalidArgument(1, "grpo: old_logprobs missing")
+    if (theta.V, theta.d, theta.h) != (ref.V, ref.d, ref.h):
+        raise InvalidArgument(1, "kl_per_position: vocab mismatch")
+    fe, text = _seq_arrays(theta, seq)
+    lens = np.array([len(r.tokens) for r in group.rollouts], dtype=np.uint64)
+    tok = np.ascontiguousarray(np.concatenate([np.asarray(r.tokens, dtype=np.int32)
+                                               for r in group.rollouts]))
+    old = np.ascontiguousarray(np.concatenate([np.asarray(r.old_logprobs, dtype=np.float64)
+                                               for r in group.rollouts]))
+    adv = np.ascontiguousarray(np.asarray(group.advantages, dtype=np.float64))
+    if adv.shape[0] != len(group.rollouts):
+        raise InvalidArgument(1, "grpo: one advantage per rollout required")
+    th = np.ascontiguousarray(theta.theta, dtype=np.float64)
+    rf = np.ascontiguousarray(ref.theta, dtype=np.float64)
+    ranges = _flat(plan_shards(int(lens.max()), sp_degree))
+    grad = np.empty(th.shape[0])
+    st = np.zeros(4)
+    c = _lib.ctypes
+    check(_lib.lib().mrsp_toy_grpo_gradient(
+        sp_degree, ptr(th, c.c_double), ptr(rf, c.c_double), theta.V, theta.d, theta.h,
+        ptr(fe, c.c_double), fe.shape[0], ptr(text, c.c_int32), text.shape[0],
+        ptr(tok, c.c_int32), ptr(lens, c.c_uint64), lens.shape[0], ptr(old, c.c_double),
+        ptr(adv, c.c_double), cfg.clip_eps, cfg.kl_beta, int(cfg.sampled_kl),
+        ptr(ranges, c.c_uint64), ptr(grad, c.c_double), ptr(st, c.c_double)))
+    return grad, GroupStats(float(st[0]), float(st[1]), float(st[2]), int(st[3]))
+
+
+def sft_loss_and_grad(theta: PolicyParams, seq: MultimodalSequence,
+                      target_tokens: Sequence[int], sp_degree: int = 1):
+    """grpo.cpp:208-223 on the device -> (loss, grad)."""
+    if len(target_tokens) == 0:
+        raise InvalidArgument(1, "sft_loss_and_grad: empty targets")
+    fe, text = _seq_arrays(theta, seq)
+    tg = np.ascontiguousarray(np.asarray(target_tokens, dtype=np.int32))
+    th = np.ascontiguousarray(theta.theta, dtype=np.float64)
+    ranges = _flat(plan_shards(tg.shape[0], sp_degree))
+    grad = np.empty(th.shape[0])
+    loss = np.zeros(1)
+    c = _lib.ctypes
+    check(_lib.lib().mrsp_toy_sft_loss_and_grad(
+        sp_degree, ptr(th, c.c_double), theta.V, theta.d, theta.h, ptr(fe, c.c_double),
+        fe.shape[0], ptr(text, c.c_int32), text.shape[0], ptr(tg, c.c_int32), tg.shape[0],
+        ptr(ranges, c.c_uint64), ptr(loss, c.c_double), ptr(grad, c.c_double)))
+    return float(loss[0]), grad
