@@ -159,6 +159,19 @@ mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, int M, int 
                               int ldb, int ldc, int epilogue, const float* bias, float* resid,
                               int ldr, void* stream);
 
+/* Same GEMM with a split-K workspace (device, fp32): when M <= 128 and the
+ * N tiles cannot fill the SMs (the decode steps' G-row projections), K is
+ * split across CTAs, fp32 partials land in the workspace and a second kernel
+ * sums them in split order and applies the epilogue (deterministic).
+ * mrsp_gemm_splitk_workspace_bytes(M) bytes let every such GEMM split fully;
+ * a smaller workspace (or none) just splits less. Plain epilogues only
+ * (STORE/BIAS/GELU/RESID/SWIGLU/STORE_F32). */
+mrsp_status mrsp_op_gemm_bf16_splitk(const void* A, const void* B, void* C, int M, int N, int K,
+                                     int lda, int ldb, int ldc, int epilogue, const float* bias,
+                                     float* resid, int ldr, void* workspace, size_t ws_bytes,
+                                     void* stream);
+size_t mrsp_gemm_splitk_workspace_bytes(int M);
+
 /* Fused vocabulary projection + log-softmax + gather (north-star item 5):
  *   logprob[i] = log_softmax(X[i] . W^T)[targets[i]],  lse[i] = logsumexp(X[i] . W^T)
  * X [M][ldx] bf16 (final-normed hidden at scored positions), W [V][K] bf16.

@@ -57,6 +57,17 @@ void require_device();
 // Count of kernels this library has launched (evidence for bench.py's gpu_launches).
 void count_launch(uint64_t n = 1);
 
+// SMs of the current device (grid sizing); 148 on B200.
+inline int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
 }  // namespace mrsp
 
 #define MRSP_CUDA(x) ::mrsp::check_cuda((x), #x, __FILE__, __LINE__)

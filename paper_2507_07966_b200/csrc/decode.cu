@@ -36,7 +36,7 @@ constexpr int HD = 128;
 struct DecArgs {
   const __nv_bfloat16* q;  // [G][ldq] bf16, head h at column q_col0 + 128 h
   int ldq, q_col0;
-  const __nv_bfloat16* kv_prefix;  // [Lp][ld_kv]: K of kv head j at 128 j, V at v_off + 128 j
+  const __nv_bfloat16* kv_prefix;  // head-major [n_kv][K | V][Lp][128] (contiguous per head)
   const __nv_bfloat16* kv_rows;    // [(t+1) * G][ld_kv] time-major: row (s*G + g)
   int ld_kv, v_off;
   int Lp, G, t, q_per_kv, n_kv;
@@ -100,9 +100,15 @@ __global__ void __launch_bounds__(256)
       const long k = k0 + kk;
       uint4 ku = make_uint4(0, 0, 0, 0), vu = make_uint4(0, 0, 0, 0);
       if (k < k_end) {
-        const __nv_bfloat16* row = src + static_cast<size_t>(k) * a.ld_kv;
-        ku = *reinterpret_cast<const uint4*>(row + kvh * HD + c8);
-        vu = *reinterpret_cast<const uint4*>(row + a.v_off + kvh * HD + c8);
+        if (rows_src) {
+          const __nv_bfloat16* row = src + static_cast<size_t>(k) * a.ld_kv;
+          ku = *reinterpret_cast<const uint4*>(row + kvh * HD + c8);
+          vu = *reinterpret_cast<const uint4*>(row + a.v_off + kvh * HD + c8);
+        } else {
+          const __nv_bfloat16* kr = src + (static_cast<size_t>(2 * kvh) * a.Lp + k) * HD;
+          ku = *reinterpret_cast<const uint4*>(kr + c8);
+          vu = *reinterpret_cast<const uint4*>(kr + static_cast<size_t>(a.Lp) * HD + c8);
+        }
       }
       const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ku);
       const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vu);
@@ -213,10 +219,18 @@ __global__ void __launch_bounds__(256)
 // Same unnormalised (m, l, O) partial as the CUDA-core kernel.
 namespace tc {
 using namespace sm100;
-constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK, RING = 2;
-constexpr int KEYS = 2048;  // keys per CTA: 16 tiles amortise the CTA setup; 96 KB smem -> 2 CTAs/SM
-constexpr int OFF_Q = 0, OFF_RING = TILE, OFF_BAR = OFF_RING + RING * TILE;
-constexpr size_t SMEM = 1024 + OFF_BAR + 256;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK;
+constexpr int KEYS = 2048;  // kRing 2: keys per CTA (16 tiles), 96 KB smem -> 2 CTAs/SM
+constexpr int OFF_Q = 0, OFF_RING = TILE;
+// kRing = K/V ring slots: 2 (two CTAs per SM) or 6 (one CTA per SM, three
+// tiles of K/V in flight so the HBM latency is off the per-tile chain)
+template <int kRing>
+constexpr size_t smem_bytes() { return 1024 + OFF_RING + kRing * TILE + 256; }
 
 struct Args {
   const __nv_bfloat16* q;
@@ -226,9 +240,12 @@ struct Args {
   float* part;
 };
 
-__global__ void __launch_bounds__(256, 2)
+template <int kRing>
+__global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
     dec_attn_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmR,
                        Args a) {
+  constexpr int RING = kRing;
+  constexpr int OFF_BAR = OFF_RING + RING * TILE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -274,8 +291,10 @@ __global__ void __launch_bounds__(256, 2)
           mbar_wait(&r_empty[slot], ph ^ 1);
           mbar_arrive_expect_tx(&r_full[slot], TILE);
           uint8_t* dst = smem + OFF_RING + slot * TILE;
-          const int col = (kv ? a.v_off : 0) + kvh * 128;
-          const int row = static_cast<int>(k_begin) + j * TK;
+          // row cache [rows][K heads | V heads]; prompt prefix head-major
+          // [n_kv][K | V][Lp][128], so each box is 16 KB of contiguous HBM
+          const int col = rows_src ? (kv ? a.v_off : 0) + kvh * 128 : 0;
+          const int row = (rows_src ? 0 : (2 * kvh + kv) * a.Lp) + static_cast<int>(k_begin) + j * TK;
           tma_load_2d(dst, tm, &r_full[slot], col, row);
           tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, row);
           if (++slot == RING) { slot = 0; ph ^= 1; }
@@ -345,25 +364,36 @@ __global__ void __launch_bounds__(256, 2)
     const int g_of_r = r % a.G;
     float m_run = -INFINITY, l_run = 0.f;
     // two passes over S in TMEM (32 columns at a time, <= 128 registers per
-    // thread so two CTAs share an SM): row max, then exp / P / row sum
-    auto visible = [&](long k) {
-      bool vis = r < qn && k < k_end;
-      if (rows_src) vis = vis && static_cast<int>(k % a.G) == g_of_r;
-      return vis;
-    };
+    // thread so two CTAs share an SM): row max, then exp / P / row sum.
+    // Visibility is one 32-bit mask per 32 keys, built once per tile: keys
+    // below the chunk end, and (row cache) only this query's own rollout row.
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const long k0 = k_begin + static_cast<long>(j) * TK;
+      const int nv = r < qn ? static_cast<int>(std::min<long>(TK, k_end - k0)) : 0;
+      const int o = rows_src ? static_cast<int>(((g_of_r - k0 % a.G) % a.G + a.G) % a.G) : 0;
+      uint32_t vis[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int n = nv - 32 * q;
+        uint32_t m = n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : (1u << n) - 1u);
+        if (rows_src) {  // key k0 + 32 q + i is row (k0 + 32 q + i) % G
+          uint32_t rm = 0;
+          for (int i = (o - 32 * q % a.G + a.G) % a.G; i < 32; i += a.G) rm |= 1u << i;
+          m &= rm;
+        }
+        vis[q] = m;
+      }
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < TK; c += 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
         uint32_t x[32];
-        tmem_ld32(tmem + lane_off + c, x);
+        tmem_ld32(tmem + lane_off + 32 * q, x);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (visible(k0 + c + i)) mx = fmaxf(mx, __uint_as_float(x[i]) * a.scale_log2);
+          mx = fmaxf(mx, (vis[q] >> i) & 1u ? __uint_as_float(x[i]) * a.scale_log2 : -INFINITY);
       }
       const float m_new = fmaxf(m_run, mx);
       if (j > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O (after P.V(j-1))
@@ -394,12 +424,14 @@ __global__ void __launch_bounds__(256, 2)
           uint32_t x[32];
           tmem_ld32(tmem + lane_off + c, x);
           tmem_ld_wait();
+          const uint32_t vm = vis[c / 32];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float p0 =
-                visible(k0 + c + i) ? exp2f(__uint_as_float(x[i]) * a.scale_log2 + nm) : 0.f;
-            const float p1 =
-                visible(k0 + c + i + 1) ? exp2f(__uint_as_float(x[i + 1]) * a.scale_log2 + nm) : 0.f;
+          for (int i = 0; i < 32; i += 2) {  // ex2(-inf) = 0 for masked keys
+            const float p0 = ex2_approx((vm >> i) & 1u ? fmaf(__uint_as_float(x[i]), a.scale_log2, nm)
+                                                       : -INFINITY);
+            const float p1 = ex2_approx((vm >> (i + 1)) & 1u
+                                            ? fmaf(__uint_as_float(x[i + 1]), a.scale_log2, nm)
+                                            : -INFINITY);
             acc += p0 + p1;
             w[cc * 16 + i / 2] = pack_bf16(p0, p1);
           }
@@ -598,20 +630,20 @@ size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv) {
   return static_cast<size_t>(chunks) * n_kv * DEC_QN * (HD + 2) * sizeof(float);
 }
 
-// Kernel choice: the tcgen05 kernel wins once the prompt K/V stream dominates
-// (c4, 131K tokens: 10.9 vs 18.3 ms per decode step); for short prompts the
-// register-blocked CUDA-core kernel's lower fixed cost wins (c2, 16K tokens).
-// MRSP_DECODE_CC=1 / 0 forces one.
+// Kernel choice: the tcgen05 kernel (attention 2.0-2.4 ms per c4 decode step,
+// 0.18 ms at c2) beats the register-blocked CUDA-core one (10+ / 0.61 ms) at
+// every prompt length measured; MRSP_DECODE_CC=1 selects the CUDA-core kernel.
 bool decode_use_tensor_cores(int Lp) {
+  (void)Lp;
   const char* e = std::getenv("MRSP_DECODE_CC");
-  if (e) return std::atoi(e) == 0;
-  return Lp >= 32768;
+  return !(e && std::atoi(e) != 0);
 }
 
-void decode_tensor_maps(const void* kv_prefix, int Lp, const void* kv_rows, long rows, int ld_kv,
-                        void* maps_out) {
+void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_rows, long rows,
+                        int ld_kv, void* maps_out) {
   CUtensorMap* m = static_cast<CUtensorMap*>(maps_out);
-  m[0] = make_tmap_bf16_2d(kv_prefix, std::max(Lp, 1), ld_kv, ld_kv, 128, 64);
+  m[0] = make_tmap_bf16_2d(kv_prefix, static_cast<uint64_t>(2 * n_kv) * std::max(Lp, 1), 128, 128,
+                           128, 64);
   m[1] = make_tmap_bf16_2d(kv_rows, std::max<long>(rows, 1), ld_kv, ld_kv, 128, 64);
 }
 
@@ -654,21 +686,37 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     ta.scale_log2 = a.scale_log2;
     ta.part = part;
     static const bool tc_attr = [] {
-      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel,
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tc::SMEM)));
+                                     static_cast<int>(tc::smem_bytes<2>())));
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<6>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tc::smem_bytes<6>())));
       return true;
     }();
     (void)tc_attr;
+    const char* env_ring = std::getenv("MRSP_DECODE_RING");
+    // long prompts: one CTA per SM with 3 tiles of K/V in flight (c4: 1.6-1.8
+    // vs 2.2-2.8 ms per step); short ones: two CTAs per SM (c2: 0.12 vs 0.17)
+    const int ring = env_ring ? std::atoi(env_ring) : (Lp >= 32768 ? 6 : 2);
+    {  // chunks sized so n_kv x chunks ~ one wave (2 or 1 resident CTAs per SM)
+      const int per_kv = std::max(1, (ring == 2 ? 2 : 1) * num_sms() / n_kv);
+      ta.chunk_keys = std::max(512, (Lp + per_kv - 1) / per_kv);
+      ta.chunk_keys = (ta.chunk_keys + tc::TK - 1) / tc::TK * tc::TK;
+      ta.n_prefix_chunks = (Lp + ta.chunk_keys - 1) / ta.chunk_keys;
+    }
     // prompt K|V [Lp][ld_kv] and the row cache as TMA tensors (rows past the
     // current step are masked; the caller's row cache is zero-initialised)
     CUtensorMap tm[2];
     if (maps)
       std::memcpy(tm, maps, sizeof(tm));
     else
-      decode_tensor_maps(kv_prefix, Lp, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
-    const int chunks = ta.n_prefix_chunks + ((t + 1) * G + tc::KEYS - 1) / tc::KEYS;
-    tc::dec_attn_tc_kernel<<<dim3(chunks, n_kv), 256, tc::SMEM, s>>>(tm[0], tm[1], ta);
+      decode_tensor_maps(kv_prefix, Lp, n_kv, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
+    const int chunks = ta.n_prefix_chunks + ((t + 1) * G + ta.chunk_keys - 1) / ta.chunk_keys;
+    if (ring == 2)
+      tc::dec_attn_tc_kernel<2><<<dim3(chunks, n_kv), 256, tc::smem_bytes<2>(), s>>>(tm[0], tm[1], ta);
+    else
+      tc::dec_attn_tc_kernel<6><<<dim3(chunks, n_kv), 256, tc::smem_bytes<6>(), s>>>(tm[0], tm[1], ta);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
     dec_merge_kernel<<<dim3(q_per_kv * G, n_kv), HD, 0, s>>>(part, chunks, n_kv, q_per_kv, G,

@@ -901,12 +901,17 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
     }
     if (k_ > 1 && !fused_a2a()) a2a_forward(static_cast<int>(g.Ltot));
     if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
-    if (capture_kv_) {  // generation: keep this layer's prompt K | V (SP = 1)
+    if (capture_kv_) {  // generation: keep this layer's prompt K and V (SP = 1),
+      // head-major [kv head][K | V][Lp][128] so decode streams contiguous HBM
       const size_t w = static_cast<size_t>(2 * nkv) * 128;
-      MRSP_CUDA(cudaMemcpy2DAsync(kv_prefix_.as<bf16>() + static_cast<size_t>(layer) * g.Lp * w,
-                                  w * 2, ranks_[0].qkv.as<bf16>() + nq * 128,
-                                  static_cast<size_t>(Cqkv) * 2, w * 2, g.Lp,
-                                  cudaMemcpyDeviceToDevice, s));
+      bf16* dst = kv_prefix_.as<bf16>() + static_cast<size_t>(layer) * g.Lp * w;
+      for (int j = 0; j < 2 * nkv; ++j) {  // j = 2 h + (0: K, 1: V)
+        const int src_head = nq + (j & 1) * nkv + (j >> 1);
+        MRSP_CUDA(cudaMemcpy2DAsync(dst + static_cast<size_t>(j) * g.Lp * 128, 256,
+                                    ranks_[0].qkv.as<bf16>() + static_cast<size_t>(src_head) * 128,
+                                    static_cast<size_t>(Cqkv) * 2, 256, g.Lp,
+                                    cudaMemcpyDeviceToDevice, s));
+      }
     }
     for (auto& R : ranks_) {
       const int nqr = R.hs.nq();
@@ -1126,6 +1131,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   const size_t o_part = carve(decode_partial_bytes(static_cast<int>(Lp), max_len, G, nkv));
   const size_t o_tok = carve(n_tok * 4), o_lp = carve(n_tok * 4), o_len = carve(G * 4);
   const size_t o_done = carve(G * 4), o_pos = carve(G * 4);
+  const size_t splitk_bytes = gemm_splitk_ws_bytes(G), o_splitk = carve(splitk_bytes);
   uint8_t* b = static_cast<uint8_t*>(st.ensure(off));
   bf16* kv_rows = reinterpret_cast<bf16*>(b + o_rows);
   float* h = reinterpret_cast<float*>(b + o_h);
@@ -1140,13 +1146,22 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   int* lengths = reinterpret_cast<int*>(b + o_len);
   int* done = reinterpret_cast<int*>(b + o_done);
   int* pos = reinterpret_cast<int*>(b + o_pos);
+  // G-row GEMMs split K over the SMs (MRSP_DECODE_SPLITK=0: one CTA per n tile)
+  const char* env_sk = std::getenv("MRSP_DECODE_SPLITK");
+  float* splitk = (env_sk && std::atoi(env_sk) == 0) ? nullptr
+                                                     : reinterpret_cast<float*>(b + o_splitk);
+  auto dec_gemm = [&](GemmArgs g) {
+    g.splitk_ws = splitk;
+    g.splitk_ws_bytes = splitk_bytes;
+    gemm_bf16(g, s);
+  };
   MRSP_CUDA(cudaMemsetAsync(kv_rows, 0, static_cast<size_t>(c.layers) * max_len * G * kvw * 2, s));
   // TMA descriptors of every layer's prompt K/V and row cache, built once
   const bool tc_decode = decode_use_tensor_cores(static_cast<int>(Lp));
   std::vector<CUtensorMap> maps(tc_decode ? 2 * c.layers : 0);
   for (int l = 0; tc_decode && l < c.layers; ++l)
     decode_tensor_maps(kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw, static_cast<int>(Lp),
-                       kv_rows + static_cast<size_t>(l) * max_len * G * kvw,
+                       nkv, kv_rows + static_cast<size_t>(l) * max_len * G * kvw,
                        static_cast<long>(max_len) * G, static_cast<int>(kvw), &maps[2 * l]);
   MRSP_CUDA(cudaMemsetAsync(tokens, 0, n_tok * 4, s));  // PAD
   MRSP_CUDA(cudaMemsetAsync(old_lp, 0, n_tok * 4, s));
@@ -1170,9 +1185,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
       }
       {
         Prof pg(*this, P_GEMM);
-        gemm_bf16({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr,
-                   0},
-                  s);
+        dec_gemm({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr, 0});
       }
       bf16* rows_l = kv_rows + static_cast<size_t>(l) * max_len * G * kvw;
       {
@@ -1190,7 +1203,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
       }
       {
         Prof pg(*this, P_GEMM);
-        gemm_bf16({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d}, s);
+        dec_gemm({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d});
       }
       {
         Prof pm(*this, P_MISC);
@@ -1198,20 +1211,17 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
       }
       {
         Prof pg(*this, P_GEMM);
-        gemm_bf16({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
-                   nullptr, 0},
-                  s);
-        gemm_bf16({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
-                   nullptr, h, d},
-                  s);
+        dec_gemm({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
+                  nullptr, 0});
+        dec_gemm({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
+                  nullptr, h, d});
       }
     }
     {
       Prof pl(*this, P_LMHEAD);
       rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
-      gemm_bf16({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
-                 nullptr, 0},
-                s);
+      dec_gemm({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
+                nullptr, 0});
     }
     {
       Prof psm(*this, P_MISC);

@@ -49,6 +49,8 @@ struct EpiArgs {
   int epi;
   int vec_ok;  // output/residual rows are 16-byte aligned -> vector stores
   int staged;  // epilogue goes through smem + TMA store / reduce-add (tmC)
+  int k_splits;  // > 1: fp32 partials of K range ks to ws[ks][M][N]
+  float* ws;
   void* C;
   int ldc;
   const float* bias;
@@ -398,8 +400,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = warp_id();
   const int m_tiles = (args.M + BM - 1) / BM;
   const int n_tiles = (args.N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  const int ks_n = args.k_splits;
+  const int num_tiles = m_tiles * n_tiles * ks_n;
   const int k_blocks = (args.K + BK - 1) / BK;
+  // work item -> (m tile, n tile, K split [kb0, kb1))
+  auto decode_tile = [&](int tile, int& mt, int& nt, int& kb0, int& kb1) {
+    const int ks = tile % ks_n;
+    tile_coords(tile / ks_n, m_tiles, n_tiles, mt, nt);
+    kb0 = ks * k_blocks / ks_n;
+    kb1 = (ks + 1) * k_blocks / ks_n;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
@@ -426,9 +436,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, mt, nt);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int mt, nt, kb0, kb1;
+        decode_tile(tile, mt, nt, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -445,10 +455,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int mt, nt, kb0, kb1;
+      decode_tile(tile, mt, nt, kb0, kb1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -457,10 +469,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             mma_bf16_ss(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
-                        (kb | k) != 0);
+                        (kb != kb0 || k != 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
-          if (kb == k_blocks - 1) mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -474,14 +486,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      int mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      int mt, nt, kb0, kb1;
+      decode_tile(tile, mt, nt, kb0, kb1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mt * BM + ew * 32 + lane_id();
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      if (args.staged)
+      if (ks_n > 1) {  // fp32 partial of this K split (rows < M only)
+        float* P = args.ws + (static_cast<size_t>(tile % ks_n) * args.M + row) * args.N;
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c, r);
+          tmem_ld_wait();
+          const int col = nt * BN + c;
+          if (row_ok && col < args.N) {
+            if (col + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                reinterpret_cast<float4*>(P + col)[j] =
+                    make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col + j < args.N) P[col + j] = __uint_as_float(r[j]);
+            }
+          }
+        }
+      } else if (args.staged)
         epilogue_staged(args, &tmC, t_row, mt * BM + ew * 32, nt, boxes, buf);
       else
         epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
@@ -496,6 +529,45 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// Split-K second pass: one thread per (row, output column); the splits are
+// summed in order, then the epilogue is applied exactly as epilogue_row does
+// (bias, GELU, SwiGLU over [gate128 | up128] tiles, residual, stores).
+__global__ void splitk_reduce_kernel(EpiArgs args) {
+  const bool swiglu = args.epi == GEMM_EPI_SWIGLU_BF16;
+  const int n_out = swiglu ? args.N / 2 : args.N;
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(args.M) * n_out) return;
+  const int row = static_cast<int>(i / n_out), col = static_cast<int>(i % n_out);
+  const size_t plane = static_cast<size_t>(args.M) * args.N;
+  auto sum = [&](int c) {
+    const float* p = args.ws + static_cast<size_t>(row) * args.N + c;
+    float v = p[0];
+    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
+    return v;
+  };
+  if (swiglu) {
+    const int c0 = (col / 128) * 256 + col % 128;
+    const float g = sum(c0), u = sum(c0 + 128);
+    static_cast<__nv_bfloat16*>(args.C)[static_cast<size_t>(row) * args.ldc + col] =
+        __float2bfloat16_rn(silu(g) * u);
+    return;
+  }
+  float v = sum(col);
+  if (args.bias) v += args.bias[col];
+  switch (args.epi) {
+    case GEMM_EPI_RESID_F32:
+      args.resid[static_cast<size_t>(row) * args.ldr + col] += v;
+      break;
+    case GEMM_EPI_STORE_F32:
+      static_cast<float*>(args.C)[static_cast<size_t>(row) * args.ldc + col] = v;
+      break;
+    default:
+      if (args.epi == GEMM_EPI_BIAS_GELU_BF16) v = gelu_tanh(v);
+      static_cast<__nv_bfloat16*>(args.C)[static_cast<size_t>(row) * args.ldc + col] =
+          __float2bfloat16_rn(v);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -670,16 +742,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // (tools/ab_gemm.sh, same box). The single-CTA kernel is the default.
 constexpr int kDefaultGemmImpl = 1;
 
-int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v > 0 ? v : 148;
-  }();
-  return n;
-}
-
 }  // namespace
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
@@ -703,7 +765,8 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   const int ld_out = g.epi == GEMM_EPI_RESID_F32 ? g.ldr : g.ldc;
   const int elem_per_16b = (f32_out || g.epi == GEMM_EPI_RESID_F32) ? 4 : 8;
   const int vec_ok = (out_addr % 16 == 0) && (ld_out % elem_per_16b == 0);
-  EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     0,          g.C,        g.ldc,
+  EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     0,          1, nullptr, g.C,
+            g.ldc,
             g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
             g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld};
   if (g.epi == GEMM_EPI_QKV_SCATTER)
@@ -771,11 +834,36 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     MRSP_CUDA(cudaGetLastError());
     return;
   }
-  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  // split-K: one m tile, too few n tiles for the SMs, a workspace, a plain epilogue
+  const int k_blocks = (g.K + BK - 1) / BK;
+  const bool plain = g.epi == GEMM_EPI_STORE_BF16 || g.epi == GEMM_EPI_BIAS_BF16 ||
+                     g.epi == GEMM_EPI_BIAS_GELU_BF16 || g.epi == GEMM_EPI_RESID_F32 ||
+                     g.epi == GEMM_EPI_SWIGLU_BF16 || g.epi == GEMM_EPI_STORE_F32;
+  if (g.splitk_ws && plain && g.M <= BM && 2 * tiles <= num_sms()) {
+    const int splits = std::min({num_sms() / tiles, k_blocks / 4, 16});
+    if (splits >= 2 && static_cast<size_t>(splits) * g.M * g.N * 4 <= g.splitk_ws_bytes) {
+      e.k_splits = splits;
+      e.ws = g.splitk_ws;
+      e.staged = 0;
+      tiles *= splits;
+    }
+  }
   const int grid = std::min(tiles, num_sms());
   gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, tc, e);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
+  if (e.k_splits > 1) {
+    const long n = static_cast<long>(g.M) * (g.epi == GEMM_EPI_SWIGLU_BF16 ? g.N / 2 : g.N);
+    splitk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(e);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+  }
+}
+
+size_t gemm_splitk_ws_bytes(int M) {
+  // splits x n tiles <= SMs, so splits x M x N <= SMs x M x BN
+  return static_cast<size_t>(num_sms()) * M * BN * sizeof(float);
 }
 
 size_t lmhead_workspace_bytes(int M, int V) {
@@ -811,6 +899,26 @@ extern "C" mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, 
     mrsp::GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, epilogue, bias, resid, ldr};
     mrsp::gemm_bf16(g, static_cast<cudaStream_t>(stream));
   });
+}
+
+extern "C" mrsp_status mrsp_op_gemm_bf16_splitk(const void* A, const void* B, void* C, int M,
+                                                int N, int K, int lda, int ldb, int ldc,
+                                                int epilogue, const float* bias, float* resid,
+                                                int ldr, void* workspace, size_t ws_bytes,
+                                                void* stream) {
+  return mrsp::guard([&] {
+    mrsp::require_device();
+    MRSP_REQUIRE(epilogue >= GEMM_EPI_STORE_BF16 && epilogue <= GEMM_EPI_STORE_F32,
+                 MRSP_INVALID_ARGUMENT, "gemm splitk: plain epilogues only");
+    mrsp::GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, epilogue, bias, resid, ldr};
+    g.splitk_ws = static_cast<float*>(workspace);
+    g.splitk_ws_bytes = workspace ? ws_bytes : 0;
+    mrsp::gemm_bf16(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" size_t mrsp_gemm_splitk_workspace_bytes(int M) {
+  return mrsp::gemm_splitk_ws_bytes(M);
 }
 
 extern "C" mrsp_status mrsp_op_lmhead_logprob(const void* X, int ldx, const void* W, int M, int V,

@@ -31,7 +31,16 @@ struct GemmArgs {
   const int2* route = nullptr;
   void* const* peer_base = nullptr;
   const int* peer_ld = nullptr;
+  // Split-K for one-m-tile GEMMs (M <= 128: the decode steps' G rows): with a
+  // workspace, K is split so that (n tiles x splits) fills the SMs; fp32
+  // partials go to splitk_ws and a second kernel sums them in split order
+  // (deterministic) and applies the epilogue. Null: no split.
+  float* splitk_ws = nullptr;
+  size_t splitk_ws_bytes = 0;
 };
+
+// Workspace that lets every one-m-tile GEMM of M rows split fully.
+size_t gemm_splitk_ws_bytes(int M);
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
 

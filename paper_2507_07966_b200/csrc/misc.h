@@ -29,11 +29,13 @@ void convert_bf16_f32(const __nv_bfloat16* in, float* out, size_t n, cudaStream_
 
 // rollout generation (csrc/decode.cu)
 size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv);
-// maps: optional TMA descriptors {prompt K|V [Lp][ld_kv], row cache [rows][ld_kv]}
-// built once per generation (decode_tensor_maps) so a step encodes none
+// The prompt K/V is head-major, [n_kv][K | V][Lp][128]; the row cache of
+// generated tokens is [rows][ld_kv] (K heads | V heads at v_off).
+// maps: optional TMA descriptors {prompt K/V, row cache} built once per
+// generation (decode_tensor_maps) so a step encodes none
 bool decode_use_tensor_cores(int Lp);
-void decode_tensor_maps(const void* kv_prefix, int Lp, const void* kv_rows, long rows, int ld_kv,
-                        void* maps_out /* 2 x CUtensorMap */);
+void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_rows, long rows,
+                        int ld_kv, void* maps_out /* 2 x CUtensorMap */);
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                       const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
                       int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,

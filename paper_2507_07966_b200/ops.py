@@ -26,8 +26,10 @@ def _p(t):
 
 
 def gemm(A: torch.Tensor, B: torch.Tensor, epi: int = EPI_STORE_BF16, bias=None, resid=None,
-         out=None) -> torch.Tensor:
-    """C = epi(A @ B.T) on the tcgen05 GEMM. A [M,K] bf16, B [N,K] bf16."""
+         out=None, splitk_ws=None) -> torch.Tensor:
+    """C = epi(A @ B.T) on the tcgen05 GEMM. A [M,K] bf16, B [N,K] bf16.
+    splitk_ws: optional device workspace (uint8) enabling split-K for M <= 128
+    (mrsp_op_gemm_bf16_splitk; size from splitk_workspace_bytes(M))."""
     M, K = A.shape
     N = B.shape[0]
     assert A.dtype == torch.bfloat16 and B.dtype == torch.bfloat16 and B.shape[1] == K
@@ -40,10 +42,20 @@ def gemm(A: torch.Tensor, B: torch.Tensor, epi: int = EPI_STORE_BF16, bias=None,
             out = torch.empty(M, N // 2, dtype=torch.bfloat16, device=A.device)
         else:
             out = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+    if splitk_ws is not None:
+        check(_lib.lib().mrsp_op_gemm_bf16_splitk(
+            _p(A), _p(B), _p(out), M, N, K, A.stride(0), B.stride(0), out.stride(0), epi,
+            _p(bias), _p(resid), resid.stride(0) if resid is not None else 0, _p(splitk_ws),
+            splitk_ws.numel() * splitk_ws.element_size(), _stream()))
+        return out
     check(_lib.lib().mrsp_op_gemm_bf16(
         _p(A), _p(B), _p(out), M, N, K, A.stride(0), B.stride(0), out.stride(0), epi, _p(bias),
         _p(resid), resid.stride(0) if resid is not None else 0, _stream()))
     return out
+
+
+def splitk_workspace_bytes(M: int) -> int:
+    return int(_lib.lib().mrsp_gemm_splitk_workspace_bytes(M))
 
 
 ATTN_CAUSAL_PREFIX, ATTN_BLOCK_DIAG = 0, 1

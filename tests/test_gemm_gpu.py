@@ -68,3 +68,39 @@ def test_gemm_strided_operands(gpu):
     A = X[:, 256:768]
     B = torch.randn(384, 512, device="cuda").bfloat16()
     assert rel_err(ops.gemm(A, B, ops.EPI_STORE_F32), ref(A, B)) < 1e-5
+
+
+# Decode-shaped GEMMs (M = G rows): split-K over the SMs with a workspace,
+# every plain epilogue, against the fp32 reference and the unsplit kernel.
+SPLITK = [(8, 4608, 3584), (8, 3584, 3584), (8, 3584, 18944), (1, 1152, 4304), (77, 640, 2048),
+          (128, 512, 8192), (8, 37888, 3584)]
+
+
+@pytest.mark.parametrize("M,N,K", SPLITK)
+def test_gemm_splitk_epilogues(gpu, gemm_impl, M, N, K):
+    if gemm_impl != "1":
+        pytest.skip("split-K is a mode of the single-CTA kernel")
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    ws = torch.empty(ops.splitk_workspace_bytes(M), dtype=torch.uint8, device="cuda")
+    r = ref(A, B)
+    C = ops.gemm(A, B, ops.EPI_STORE_F32, splitk_ws=ws)
+    assert rel_err(C, r) < 5e-5  # fp32 sums over K up to 18944 in another order
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_BF16, bias=bias, splitk_ws=ws), r + bias) < 5e-3
+    gelu = torch.nn.functional.gelu(r + bias, approximate="tanh")
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_GELU_BF16, bias=bias, splitk_ws=ws), gelu) < 5e-3
+    resid = torch.randn(M, N, device="cuda", generator=g)
+    want = resid + r + bias
+    ops.gemm(A, B, ops.EPI_RESID_F32, resid=resid, bias=bias, splitk_ws=ws)
+    assert rel_err(resid, want) < 5e-5
+    if N % 256 == 0:
+        out = ops.gemm(A, B, ops.EPI_SWIGLU_BF16, splitk_ws=ws)
+        rr = r.view(M, N // 256, 2, 128)
+        sw = (torch.nn.functional.silu(rr[:, :, 0]) * rr[:, :, 1]).reshape(M, N // 2)
+        assert rel_err(out, sw) < 5e-3
+    # deterministic: same bits twice; close to the unsplit kernel
+    C2 = ops.gemm(A, B, ops.EPI_STORE_F32, splitk_ws=ws)
+    assert torch.equal(C, C2)
+    assert rel_err(C, ops.gemm(A, B, ops.EPI_STORE_F32)) < 5e-5
