@@ -4,7 +4,7 @@
 //
 // Decode attention (one generation step, G rows): per kv head, the q_per_kv x G
 // queries (<= 64) attend to the shared prefix K/V (computed once by the prefix
-// prefill, [Lp][kv][128] per layer) and to the keys of their own row generated
+// prefill, head-major [kv][K|V][Lp][128] per layer) and to the keys of their own row generated
 // so far (time-major row cache [t][G][kv][128], row mask). The key range is
 // split into chunks of DEC_CHUNK keys, one CTA per (chunk, kv head): each K/V
 // tile read from HBM serves all of the kv group's queries (GQA reuse), and the
@@ -211,12 +211,12 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core decode attention (long prompts): one CTA per (chunk, kv head),
+// Tensor-core decode attention (the default): one CTA per (chunk, kv head),
 // the <= 64 queries of the kv group as one 128-row Q tile (zero rows pad it)
 // written to smem in the SW128 K-major layout, 128-key K/V tiles by TMA
-// through a 4-slot ring, S = Q.K^T and O += P.V on tcgen05 with S, P (bf16
-// over S) and O in TMEM — the prefill kernel's tile pipeline for one Q tile.
-// Same unnormalised (m, l, O) partial as the CUDA-core kernel.
+// through a kRing-slot ring, S = Q.K^T and O += P.V on tcgen05 with S, P
+// (bf16 over S) and O in TMEM — the prefill kernel's tile pipeline for one Q
+// tile. Same unnormalised (m, l, O) partial as the CUDA-core kernel.
 namespace tc {
 using namespace sm100;
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -225,7 +225,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 constexpr int TQ = 128, TK = 128, CHUNK = 128 * 64 * 2, TILE = 2 * CHUNK;
-constexpr int KEYS = 2048;  // kRing 2: keys per CTA (16 tiles), 96 KB smem -> 2 CTAs/SM
 constexpr int OFF_Q = 0, OFF_RING = TILE;
 // kRing = K/V ring slots: 2 (two CTAs per SM) or 6 (one CTA per SM, three
 // tiles of K/V in flight so the HBM latency is off the per-tile chain)
