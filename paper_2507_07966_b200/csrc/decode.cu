@@ -679,8 +679,6 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     ta.Lp = Lp;
     ta.q_per_kv = q_per_kv;
     ta.n_kv = n_kv;
-    ta.n_prefix_chunks = (Lp + tc::KEYS - 1) / tc::KEYS;
-    ta.chunk_keys = tc::KEYS;
     ta.v_off = v_off;
     ta.scale_log2 = a.scale_log2;
     ta.part = part;
