@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gen", action="store_true", help="skip the rollout-generation side line")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -411,10 +412,48 @@ def main():
             except Exception as e:
                 line["cpu_baseline"] = {"error": str(e)}
         line["reference_toy_engine"] = reference_toy_engine() if world == 1 else None
+        if world == 1 and not args.no_gen:
+            try:
+                line["rollout_generation"] = generation_side_line(eng, w, group, peaks, pix)
+            except Exception as e:
+                line["rollout_generation"] = {"error": str(e)}
         print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def generation_side_line(eng, w, group, peaks, pix):
+    """SURVEY §8f rank 2, not the metric: G rollouts of the same workload's
+    prompt (cached video + question) sampled by the engine (Engine::generate).
+    Device time per decode step from two runs 64 steps apart (the prompt
+    prefill cancels), against the HBM bound of a step (policy weights + the
+    prompt K/V read once)."""
+    import numpy as np
+    c = w.cfg
+    G = int(group.resp.shape[0])
+    q = np.asarray(group.question, dtype=np.int32)
+    vid = "rollout-gen"
+    eng.encode(vid, pix)
+    eng.generate(vid, q, G, 4, seed=1)  # warm
+    dev = {}
+    n1, n2 = 8, 72
+    for n in (n1, n2):
+        eng.profile(True)
+        eng.generate(vid, q, G, n, temperature=1.0, seed=2)
+        prof = eng.profile(False)
+        dev[n] = sum(v[0] for v in prof.values())
+    step_ms = (dev[n2] - dev[n1]) / (n2 - n1)
+    L, d, nq, nkv, mlp, V = c.layers, c.dim, c.n_q_heads, c.n_kv_heads, c.mlp, c.vocab
+    weights = 2 * (L * (d * (nq + 2 * nkv) * 128 + nq * 128 * d + 3 * d * mlp) + V * d)
+    Lp = w.frames * c.tokens_per_frame + len(q)
+    kv = 2 * L * Lp * 2 * nkv * 128
+    bound_ms = (weights + kv) / (peaks.get("hbm_gbs", 7000.0) * 1e9) * 1e3
+    return {"rows": G, "prompt_tokens": Lp, "decode_step_ms_device": round(step_ms, 3),
+            "tokens_per_s_device": round(G / (step_ms / 1e3), 1),
+            "hbm_bytes_per_step": weights + kv, "hbm_bound_step_ms": round(bound_ms, 3),
+            "hbm_frac": round(bound_ms / step_ms, 3),
+            "note": "device busy time per decode step (engine profile classes), 64-step difference"}
 
 
 def workload_config(w, group, fl, n):
