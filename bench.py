@@ -453,7 +453,7 @@ def generation_side_line(eng, w, group, peaks, pix):
             "tokens_per_s_device": round(G / (step_ms / 1e3), 1),
             "hbm_bytes_per_step": weights + kv, "hbm_bound_step_ms": round(bound_ms, 3),
             "hbm_frac": round(bound_ms / step_ms, 3),
-            "note": "device busy time per decode step (engine profile classes), 64-step difference"}
+            "note": "device time per decode step (engine profile classes: steps t >= 1 are one CUDA-graph replay each), 64-step difference"}
 
 
 def workload_config(w, group, fl, n):

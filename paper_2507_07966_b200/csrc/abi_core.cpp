@@ -12,6 +12,10 @@ static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static thread_local bool g_pdl = false;
+bool pdl_enabled() { return g_pdl; }
+void set_pdl(bool on) { g_pdl = on; }
+
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 void require_device() {

@@ -57,6 +57,10 @@ void require_device();
 // Count of kernels this library has launched (evidence for bench.py's gpu_launches).
 void count_launch(uint64_t n = 1);
 
+// Programmatic dependent launch for the calling thread's launches (pdl.cuh).
+bool pdl_enabled();
+void set_pdl(bool on);
+
 // SMs of the current device (grid sizing); 148 on B200.
 inline int num_sms() {
   static int n = [] {

@@ -22,6 +22,7 @@
 
 #include "common.h"
 #include "misc.h"
+#include "pdl.cuh"
 #include "sm100.cuh"
 #include "tma.h"
 
@@ -39,7 +40,8 @@ struct DecArgs {
   const __nv_bfloat16* kv_prefix;  // head-major [n_kv][K | V][Lp][128] (contiguous per head)
   const __nv_bfloat16* kv_rows;    // [(t+1) * G][ld_kv] time-major: row (s*G + g)
   int ld_kv, v_off;
-  int Lp, G, t, q_per_kv, n_kv;
+  int Lp, G, q_per_kv, n_kv;
+  const int* tdev;  // step index t (device)
   int n_prefix_chunks, n_row_chunks;
   float scale_log2;
   float* part;  // [n_chunks][n_kv][DEC_QN][HD + 2]
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(256)
   const int qn = a.q_per_kv * a.G;
   const bool rows_src = chunk >= a.n_prefix_chunks;
   const long k_begin = static_cast<long>(rows_src ? chunk - a.n_prefix_chunks : chunk) * DEC_CHUNK;
-  const long k_total = rows_src ? static_cast<long>(a.t + 1) * a.G : a.Lp;
+  const long k_total = rows_src ? static_cast<long>(*a.tdev + 1) * a.G : a.Lp;
   const long k_end = std::min<long>(k_begin + DEC_CHUNK, k_total);
   const __nv_bfloat16* src = rows_src ? a.kv_rows : a.kv_prefix;
   for (int i = tid; i < DEC_QN * HD; i += blockDim.x) {  // qi = hl * G + g
@@ -233,7 +235,8 @@ constexpr size_t smem_bytes() { return 1024 + OFF_RING + kRing * TILE + 256; }
 
 struct Args {
   const __nv_bfloat16* q;
-  int ldq, q_col0, G, t, Lp, q_per_kv, n_kv, n_prefix_chunks, chunk_keys;
+  const int* tdev;  // step index t (device)
+  int ldq, q_col0, G, Lp, q_per_kv, n_kv, n_prefix_chunks, chunk_keys;
   int v_off;
   float scale_log2;
   float* part;
@@ -260,9 +263,10 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
   const int qn = a.q_per_kv * a.G;
   const bool rows_src = chunk >= a.n_prefix_chunks;
   const long k_begin = static_cast<long>(rows_src ? chunk - a.n_prefix_chunks : chunk) * a.chunk_keys;
-  const long k_total = rows_src ? static_cast<long>(a.t + 1) * a.G : a.Lp;
+  const long k_total = rows_src ? static_cast<long>(*a.tdev + 1) * a.G : a.Lp;
   const long k_end = std::min<long>(k_begin + a.chunk_keys, k_total);
-  const int n_tiles = static_cast<int>((k_end - k_begin + TK - 1) / TK);
+  // chunks past the live row keys (graph replays size the grid for max_len) are empty
+  const int n_tiles = k_end > k_begin ? static_cast<int>((k_end - k_begin + TK - 1) / TK) : 0;
   const CUtensorMap* tm = rows_src ? &tmR : &tmP;
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(tm);
@@ -281,6 +285,8 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;  // S [0,128) (P over its first 64), O [128,256)
+  pdl_wait();
+  pdl_trigger();
   if (warp == 0) {
     if (elect_one()) {  // K_j, V_j alternate through the ring
       int slot = 0;
@@ -472,6 +478,8 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
 // O[g][h*128 + d] = sum_c O_c 2^(m_c - m) / sum_c l_c 2^(m_c - m)
 __global__ void dec_merge_kernel(const float* __restrict__ part, int n_chunks, int n_kv,
                                  int q_per_kv, int G, __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int qi = blockIdx.x, kvh = blockIdx.y, d = threadIdx.x;  // blockDim = 128
   const int hl = qi / G, g = qi % G;
   float m = -INFINITY;
@@ -501,10 +509,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // at temperature 1 (policy.cpp:130-134). Rows already finished (EOS) only
 // record PAD. One thread-block scan over the vocabulary, fp64 accumulation.
 __global__ void __launch_bounds__(1024)
-    sample_kernel(const float* __restrict__ logits, int V, float inv_temp, uint64_t seed, int t,
+    sample_kernel(const float* __restrict__ logits, int V, float inv_temp, uint64_t seed,
+                  const int* __restrict__ tdev,
                   int* __restrict__ done, int* __restrict__ tokens, float* __restrict__ old_lp,
                   int* __restrict__ lengths, int max_len, int eos, int pad) {
-  const int g = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  pdl_wait();
+  pdl_trigger();
+  const int g = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, t = *tdev;
   __shared__ double red[32];
   __shared__ float redf[32];
   __shared__ int pick;
@@ -604,9 +615,12 @@ __global__ void __launch_bounds__(1024)
 // hidden[g] = embed[prev token of row g] (EOS at t = 0, policy.cpp:127), and
 // the position id Lp + t of every row (rows restart at Lp, as in the pack).
 __global__ void decode_embed_kernel(const __nv_bfloat16* __restrict__ embed, int d,
-                                    const int* __restrict__ tokens, int max_len, int t, int pos,
+                                    const int* __restrict__ tokens, int max_len,
+                                    const int* __restrict__ tdev, int pos_base,
                                     float* __restrict__ hidden, int* __restrict__ pos_out) {
-  const int g = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  const int g = blockIdx.x, t = *tdev, pos = pos_base + t;
   const int tok = t == 0 ? 1 /* Vocab::kEos */ : tokens[static_cast<size_t>(g) * max_len + t - 1];
   if (threadIdx.x == 0) pos_out[g] = pos;
   const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(embed + static_cast<size_t>(tok) * d);
@@ -614,11 +628,45 @@ __global__ void decode_embed_kernel(const __nv_bfloat16* __restrict__ embed, int
   for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
 }
 
+// rows[t * G + g] = qkv[g][col0, col0 + kvw): this step's post-RoPE K and V
+// of every rollout row into the row cache, at the device-side step index.
+__global__ void decode_append_kv_kernel(const __nv_bfloat16* __restrict__ qkv, int ldq, int col0,
+                                        __nv_bfloat16* __restrict__ rows, int kvw,
+                                        const int* __restrict__ tdev) {
+  pdl_wait();
+  pdl_trigger();
+  const int g = blockIdx.x, G = gridDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(qkv + static_cast<size_t>(g) * ldq + col0);
+  uint4* dst = reinterpret_cast<uint4*>(rows + (static_cast<size_t>(*tdev) * G + g) * kvw);
+  for (int i = threadIdx.x; i < kvw / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void decode_step_advance_kernel(int* tdev) {
+  pdl_wait();
+  if (threadIdx.x == 0) *tdev += 1;
+}
+
 }  // namespace
 
-void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len, int t, int G,
-                  int pos, float* hidden, int* pos_out, cudaStream_t s) {
-  decode_embed_kernel<<<G, 256, 0, s>>>(embed, d, tokens, max_len, t, pos, hidden, pos_out);
+void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len,
+                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s) {
+  launch_pdl(decode_embed_kernel, dim3(G), dim3(256), 0, s, embed, d, tokens, max_len, tdev, pos_base,
+             hidden, pos_out);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void decode_append_kv(const __nv_bfloat16* qkv, int ldq, int col0, __nv_bfloat16* rows, int kvw,
+                      int G, const int* tdev, cudaStream_t s) {
+  MRSP_REQUIRE(kvw % 8 == 0 && ldq % 8 == 0 && col0 % 8 == 0, MRSP_INVALID_ARGUMENT,
+               "decode_append_kv: 16-byte aligned rows");
+  launch_pdl(decode_append_kv_kernel, dim3(G), dim3(128), 0, s, qkv, ldq, col0, rows, kvw, tdev);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void decode_step_advance(int* tdev, cudaStream_t s) {
+  launch_pdl(decode_step_advance_kernel, dim3(1), dim3(32), 0, s, tdev);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
@@ -647,9 +695,10 @@ void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_
 }
 
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
-                      const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
-                      int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,
-                      cudaStream_t s, const void* maps) {
+                      const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t_grid,
+                      const int* tdev, int q_per_kv, int n_kv, float scale, float* part, void* out,
+                      int ldo, cudaStream_t s, const void* maps) {
+  const int t = t_grid;
   MRSP_REQUIRE(q_per_kv * G <= DEC_QN, MRSP_INVALID_ARGUMENT,
                "generate: q_per_kv x G must be <= 64");
   DecArgs a;
@@ -662,7 +711,7 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   a.v_off = v_off;
   a.Lp = Lp;
   a.G = G;
-  a.t = t;
+  a.tdev = tdev;
   a.q_per_kv = q_per_kv;
   a.n_kv = n_kv;
   a.n_prefix_chunks = (Lp + DEC_CHUNK - 1) / DEC_CHUNK;
@@ -675,7 +724,7 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     ta.ldq = ldq;
     ta.q_col0 = q_col0;
     ta.G = G;
-    ta.t = t;
+    ta.tdev = tdev;
     ta.Lp = Lp;
     ta.q_per_kv = q_per_kv;
     ta.n_kv = n_kv;
@@ -711,13 +760,15 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
       decode_tensor_maps(kv_prefix, Lp, n_kv, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
     const int chunks = ta.n_prefix_chunks + ((t + 1) * G + ta.chunk_keys - 1) / ta.chunk_keys;
     if (ring == 2)
-      tc::dec_attn_tc_kernel<2><<<dim3(chunks, n_kv), 256, tc::smem_bytes<2>(), s>>>(tm[0], tm[1], ta);
+      launch_pdl(tc::dec_attn_tc_kernel<2>, dim3(chunks, n_kv), dim3(256), tc::smem_bytes<2>(), s,
+                 tm[0], tm[1], ta);
     else
-      tc::dec_attn_tc_kernel<6><<<dim3(chunks, n_kv), 256, tc::smem_bytes<6>(), s>>>(tm[0], tm[1], ta);
+      launch_pdl(tc::dec_attn_tc_kernel<6>, dim3(chunks, n_kv), dim3(256), tc::smem_bytes<6>(), s,
+                 tm[0], tm[1], ta);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
-    dec_merge_kernel<<<dim3(q_per_kv * G, n_kv), HD, 0, s>>>(part, chunks, n_kv, q_per_kv, G,
-                                                             static_cast<__nv_bfloat16*>(out), ldo);
+    launch_pdl(dec_merge_kernel, dim3(q_per_kv * G, n_kv), dim3(HD), 0, s, part, chunks, n_kv,
+               q_per_kv, G, static_cast<__nv_bfloat16*>(out), ldo);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
     return;
@@ -740,11 +791,11 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   MRSP_CUDA(cudaGetLastError());
 }
 
-void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed, int t,
-                   int* done, int* tokens, float* old_lp, int* lengths, int max_len,
-                   cudaStream_t s) {
-  sample_kernel<<<G, 1024, 0, s>>>(logits, V, 1.0f / temperature, seed, t, done, tokens, old_lp,
-                                   lengths, max_len, /*Vocab::kEos*/ 1, /*Vocab::kPad*/ 0);
+void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed,
+                   const int* tdev, int* done, int* tokens, float* old_lp, int* lengths,
+                   int max_len, cudaStream_t s) {
+  launch_pdl(sample_kernel, dim3(G), dim3(1024), 0, s, logits, V, 1.0f / temperature, seed, tdev,
+             done, tokens, old_lp, lengths, max_len, /*Vocab::kEos*/ 1, /*Vocab::kPad*/ 0);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

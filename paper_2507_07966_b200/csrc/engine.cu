@@ -27,6 +27,7 @@
 #include "common.h"
 #include "gemm.h"
 #include "misc.h"
+#include "pdl.cuh"
 
 namespace mrsp {
 
@@ -438,7 +439,8 @@ struct Prof {
   }
 };
 
-enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5 };
+enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5,
+       P_DECODE_GRAPH = 6 };
 
 // ---------------------------------------------------------------------------
 // Stage 1 for one SP rank: frames [fb, fe) -> projector output rows.
@@ -1130,7 +1132,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   const size_t o_logit = carve(static_cast<size_t>(G) * c.vocab * 4);
   const size_t o_part = carve(decode_partial_bytes(static_cast<int>(Lp), max_len, G, nkv));
   const size_t o_tok = carve(n_tok * 4), o_lp = carve(n_tok * 4), o_len = carve(G * 4);
-  const size_t o_done = carve(G * 4), o_pos = carve(G * 4);
+  const size_t o_done = carve(G * 4), o_pos = carve(G * 4), o_t = carve(4);
   const size_t splitk_bytes = gemm_splitk_ws_bytes(G), o_splitk = carve(splitk_bytes);
   uint8_t* b = static_cast<uint8_t*>(st.ensure(off));
   bf16* kv_rows = reinterpret_cast<bf16*>(b + o_rows);
@@ -1146,6 +1148,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   int* lengths = reinterpret_cast<int*>(b + o_len);
   int* done = reinterpret_cast<int*>(b + o_done);
   int* pos = reinterpret_cast<int*>(b + o_pos);
+  int* tdev = reinterpret_cast<int*>(b + o_t);  // the step index t, advanced on the device
   // G-row GEMMs split K over the SMs (MRSP_DECODE_SPLITK=0: one CTA per n tile)
   const char* env_sk = std::getenv("MRSP_DECODE_SPLITK");
   float* splitk = (env_sk && std::atoi(env_sk) == 0) ? nullptr
@@ -1167,15 +1170,17 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   MRSP_CUDA(cudaMemsetAsync(old_lp, 0, n_tok * 4, s));
   MRSP_CUDA(cudaMemsetAsync(lengths, 0, G * 4, s));
   MRSP_CUDA(cudaMemsetAsync(done, 0, G * 4, s));
+  MRSP_CUDA(cudaMemsetAsync(tdev, 0, 4, s));
   const LlmW& W = llm_[0];
   const float scale = 1.0f / std::sqrt(128.0f);
   std::vector<int> done_h(G);
-  // 3. decode steps: tokens -> embeddings -> 28 layers (G-row GEMMs, decode
-  // attention over prompt K/V + own-row K/V) -> LM head logits -> sample
-  for (int t = 0; t < max_len; ++t) {
+  // 3. one decode step: tokens -> embeddings -> 28 layers (G-row GEMMs, decode
+  // attention over prompt K/V + own-row K/V) -> LM head logits -> sample -> t + 1.
+  // Every kernel reads t from `tdev`; t_grid only sizes the attention grid.
+  auto step = [&](int t_grid) {
     {
       Prof pm(*this, P_MISC);
-      decode_embed(W.embed, d, tokens, max_len, t, G, static_cast<int>(Lp + t), h, pos, s);
+      decode_embed(W.embed, d, tokens, max_len, tdev, G, static_cast<int>(Lp), h, pos, s);
     }
     for (int l = 0; l < c.layers; ++l) {
       const LlmLayerW& Lw = W.layers[l];
@@ -1191,15 +1196,13 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
       {
         Prof pm(*this, P_MISC);
         rope(qkv, Cqkv, 0, nq + nkv, pos, G, s);
-        MRSP_CUDA(cudaMemcpy2DAsync(rows_l + static_cast<size_t>(t) * G * kvw, kvw * 2,
-                                    qkv + nq * 128, static_cast<size_t>(Cqkv) * 2, kvw * 2, G,
-                                    cudaMemcpyDeviceToDevice, s));
+        decode_append_kv(qkv, Cqkv, nq * 128, rows_l, static_cast<int>(kvw), G, tdev, s);
       }
       {
         Prof pa(*this, P_ATTN);
         decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
-                         rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t,
-                         qpk, nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
+                         rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t_grid,
+                         tdev, qpk, nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
       }
       {
         Prof pg(*this, P_GEMM);
@@ -1225,8 +1228,60 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
     }
     {
       Prof psm(*this, P_MISC);
-      sample_tokens(logits, G, c.vocab, temperature, seed, t, done, tokens, old_lp, lengths,
+      sample_tokens(logits, G, c.vocab, temperature, seed, tdev, done, tokens, old_lp, lengths,
                     max_len, s);
+      decode_step_advance(tdev, s);
+    }
+  };
+  // Steps t >= 1 replay one CUDA graph of a step, captured with the attention
+  // grid sized for t = max_len - 1: the ~13 launches per layer become one graph
+  // launch per step. Step 0 runs eagerly (one-time kernel attribute setup).
+  // MRSP_DECODE_GRAPH=0 launches every step eagerly; the CUDA-core decode
+  // attention (MRSP_DECODE_CC=1) is eager only.
+  const char* env_graph = std::getenv("MRSP_DECODE_GRAPH");
+  const bool use_graph = tc_decode && max_len > 2 && !(env_graph && std::atoi(env_graph) == 0);
+  // MRSP_DECODE_PDL=1: programmatic dependent launches inside the graph (each
+  // kernel's launch and prologue overlap its predecessor's tail). Measured
+  // neutral at c4 and 15-25% slower at c2 (profiles/r1_generation_perf.jsonl),
+  // so off by default.
+  const char* env_pdl = std::getenv("MRSP_DECODE_PDL");
+  const bool use_pdl = env_pdl && std::atoi(env_pdl) != 0;
+  struct GraphGuard {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    ~GraphGuard() {
+      if (x) cudaGraphExecDestroy(x);
+      if (g) cudaGraphDestroy(g);
+    }
+  } graph;
+  uint64_t graph_launches = 0;
+  for (int t = 0; t < max_len; ++t) {
+    if (!use_graph || t == 0) {
+      step(t);
+    } else {
+      if (!graph.x) {
+        const bool prof_was = prof_;
+        prof_ = false;  // no timing events inside the capture
+        const uint64_t n0 = mrsp_launch_count();
+        MRSP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+          PdlScope pdl(use_pdl);
+          step(max_len - 1);
+        } catch (...) {
+          cudaGraph_t dead = nullptr;
+          cudaStreamEndCapture(s, &dead);
+          if (dead) cudaGraphDestroy(dead);
+          prof_ = prof_was;
+          throw;
+        }
+        MRSP_CUDA(cudaStreamEndCapture(s, &graph.g));
+        prof_ = prof_was;
+        graph_launches = mrsp_launch_count() - n0;
+        MRSP_CUDA(cudaGraphInstantiate(&graph.x, graph.g, 0));
+      }
+      Prof pd(*this, P_DECODE_GRAPH);
+      MRSP_CUDA(cudaGraphLaunch(graph.x, s));
+      count_launch(graph_launches);
     }
     if ((t & 15) == 15 || t == max_len - 1) {  // stop once every row has sampled EOS
       MRSP_CUDA(cudaMemcpyAsync(done_h.data(), done, G * 4, cudaMemcpyDeviceToHost, s));

@@ -26,6 +26,7 @@
 #include "common.h"
 #include "gemm.h"
 #include "misc.h"
+#include "pdl.cuh"
 #include "sm100.cuh"
 #include "tma.h"
 
@@ -430,6 +431,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // decode graphs: the predecessor's outputs are visible from here
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -535,6 +538,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // summed in order, then the epilogue is applied exactly as epilogue_row does
 // (bias, GELU, SwiGLU over [gate128 | up128] tiles, residual, stores).
 __global__ void splitk_reduce_kernel(EpiArgs args) {
+  pdl_wait();
+  pdl_trigger();
   const bool swiglu = args.epi == GEMM_EPI_SWIGLU_BF16;
   const int n_out = swiglu ? args.N / 2 : args.N;
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -850,12 +855,13 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     }
   }
   const int grid = std::min(tiles, num_sms());
-  gemm_bf16_tcgen05<<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, tc, e);
+  launch_pdl(gemm_bf16_tcgen05, dim3(grid), dim3(THREADS), SMEM_BYTES, stream, ta, tb, tc, e);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
   if (e.k_splits > 1) {
     const long n = static_cast<long>(g.M) * (g.epi == GEMM_EPI_SWIGLU_BF16 ? g.N / 2 : g.N);
-    splitk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(e);
+    launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0,
+               stream, e);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }

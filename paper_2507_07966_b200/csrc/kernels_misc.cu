@@ -9,6 +9,7 @@
 
 #include "common.h"
 #include "misc.h"
+#include "pdl.cuh"
 
 namespace mrsp {
 namespace {
@@ -25,6 +26,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ w,
                                __nv_bfloat16* __restrict__ out, int ldo, int n, int d, float eps,
                                const int* __restrict__ rows) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -86,6 +89,8 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, int ld, int col0, i
                             const int* __restrict__ pos, int n) {
   // thread = (row, frequency pair): bf16x2 accesses, one sincos pair reused
   // over every head of the row
+  pdl_wait();
+  pdl_trigger();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * 32) return;
   const int row = idx >> 5, i = (idx & 31) * 2;
@@ -273,7 +278,8 @@ void rmsnorm(const float* x, int ldx, const float* w, __nv_bfloat16* out, int ld
              float eps, const int* rows, cudaStream_t s) {
   MRSP_REQUIRE(d % 4 == 0 && ldx % 4 == 0, MRSP_INVALID_ARGUMENT, "rmsnorm: d % 4");
   if (n <= 0) return;
-  rmsnorm_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, ldx, w, out, ldo, n, d, eps, rows);
+  launch_pdl(rmsnorm_kernel, dim3((n + 7) / 8), dim3(256), 0, s, x, ldx, w, out, ldo, n, d, eps,
+             rows);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
@@ -297,7 +303,8 @@ void rope(__nv_bfloat16* qkv, int ld, int col0, int n_heads, const int* pos, int
   if (n <= 0 || n_heads <= 0) return;
   MRSP_REQUIRE(ld % 2 == 0 && col0 % 2 == 0, MRSP_INVALID_ARGUMENT, "rope: odd leading dim");
   const int work = n * 32;
-  rope_kernel<<<(work + 255) / 256, 256, 0, s>>>(qkv, ld, col0, n_heads, pos, n);
+  launch_pdl(rope_kernel, dim3((work + 255) / 256), dim3(256), 0, s, qkv, ld, col0, n_heads, pos,
+             n);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

@@ -36,14 +36,22 @@ size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv);
 bool decode_use_tensor_cores(int Lp);
 void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_rows, long rows,
                         int ld_kv, void* maps_out /* 2 x CUtensorMap */);
+// Decode steps read the step index t from device memory (`tdev`), so one
+// captured CUDA graph of a step replays for every t; host-side `t_grid` only
+// sizes the attention grid (the current t eagerly, max_len - 1 in a graph:
+// chunks past the live row keys write empty partials).
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
-                      const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t,
-                      int q_per_kv, int n_kv, float scale, float* part, void* out, int ldo,
-                      cudaStream_t s, const void* maps = nullptr);
-void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len, int t, int G,
-                  int pos, float* hidden, int* pos_out, cudaStream_t s);
-void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed, int t,
-                   int* done, int* tokens, float* old_lp, int* lengths, int max_len,
-                   cudaStream_t s);
+                      const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t_grid,
+                      const int* tdev, int q_per_kv, int n_kv, float scale, float* part, void* out,
+                      int ldo, cudaStream_t s, const void* maps = nullptr);
+void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len,
+                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s);
+// rows[t * G + g][0, kvw) = qkv[g][col0, col0 + kvw) (this step's K | V per row)
+void decode_append_kv(const __nv_bfloat16* qkv, int ldq, int col0, __nv_bfloat16* rows, int kvw,
+                      int G, const int* tdev, cudaStream_t s);
+void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed,
+                   const int* tdev, int* done, int* tokens, float* old_lp, int* lengths,
+                   int max_len, cudaStream_t s);
+void decode_step_advance(int* tdev, cudaStream_t s);
 
 }  // namespace mrsp

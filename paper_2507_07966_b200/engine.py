@@ -295,7 +295,8 @@ class Engine:
                                                     raw.ctypes.data_as(ctypes.c_void_p)))
         return (raw.astype(np.uint32) << 16).view(np.float32)
 
-    PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc"]
+    PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc",
+                       "decode_graph"]
 
     def profile(self, enable: Optional[bool] = None) -> dict:
         en = -1 if enable is None else int(enable)

@@ -95,3 +95,17 @@ def test_decode_kernels_agree(gpu, gen, cc, monkeypatch):
     got = np.concatenate([olp[g, :lens[g]] for g in range(len(lens))])
     d = np.abs(got - want)
     assert d.max() <= 5e-2 and d.mean() <= 5e-3, (cc, d.max(), d.mean())
+
+
+def test_graph_replay_matches_eager(gpu, gen, monkeypatch):
+    """Steps t >= 1 replay one captured CUDA graph whose attention grid is sized
+    for t = max_len - 1 (chunks past the live row keys are empty): tokens,
+    lengths and old log-probs are bit-identical to launching every step eagerly.
+    G x max_len = 640 row keys, so early steps run with an empty row chunk."""
+    eng, q = gen["eng"], gen["q"]
+    monkeypatch.setenv("MRSP_DECODE_GRAPH", "0")
+    eager = eng.generate("v", q, 16, 40, temperature=0.9, seed=5)
+    monkeypatch.setenv("MRSP_DECODE_GRAPH", "1")
+    graph = eng.generate("v", q, 16, 40, temperature=0.9, seed=5)
+    for x, y in zip(eager, graph):
+        assert np.array_equal(x, y)
