@@ -242,11 +242,23 @@ struct Args {
   float* part;
 };
 
-template <int kRing>
-__global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
+// kStreams = 2 (one CTA per SM): the chunk's KV tiles alternate between two
+// streams with their own S and O in TMEM (S0 S1 O0 O1 = 512 columns) and their
+// own softmax warpgroup; the MMA issuer interleaves
+//     S(0) S(1) | P.V(0) S(2) | P.V(1) S(3) | ...
+// so one warpgroup's softmax overlaps the other stream's MMAs (the prefill
+// kernel's ping-pong, over keys instead of query tiles). Each stream writes
+// its own (m, l, O) partial (chunk slots 2c and 2c + 1; dec_merge_kernel
+// combines them). kStreams = 1 (two CTAs per SM, short prompts): one stream.
+template <int kStreams>
+constexpr int threads() { return 128 + 128 * kStreams; }
+
+template <int kRing, int kStreams>
+__global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     dec_attn_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmR,
                        Args a) {
   constexpr int RING = kRing;
+  constexpr uint32_t TMEM_COLS = 256 * kStreams;
   constexpr int OFF_BAR = OFF_RING + RING * TILE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -255,10 +267,10 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
   uint64_t* q_ready = bars;
   uint64_t* r_full = bars + 1;        // [RING]
   uint64_t* r_empty = r_full + RING;  // [RING]
-  uint64_t* s_full = r_empty + RING;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* pv_done = p_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  uint64_t* s_full = r_empty + RING;  // [kStreams]
+  uint64_t* p_full = s_full + kStreams;
+  uint64_t* pv_done = p_full + kStreams;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + kStreams);
   const int warp = warp_id(), chunk = blockIdx.x, kvh = blockIdx.y;
   const int qn = a.q_per_kv * a.G;
   const bool rows_src = chunk >= a.n_prefix_chunks;
@@ -275,20 +287,23 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
       mbar_init(&r_full[i], 1);
       mbar_init(&r_empty[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
+    for (int w = 0; w < kStreams; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&pv_done[w], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S [0,128) (P over its first 64), O [128,256)
+  // S_w at column 128 w (P over its first 64), O_w at 128 kStreams + 128 w
+  const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();
   if (warp == 0) {
-    if (elect_one()) {  // K_j, V_j alternate through the ring
+    if (elect_one()) {  // K_j, V_j alternate through the ring (ring item 2j, 2j + 1)
       int slot = 0;
       uint32_t ph = 0;
       for (int j = 0; j < n_tiles; ++j)
@@ -310,43 +325,52 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
     const uint32_t q_addr = smem_u32(smem + OFF_Q), ring = smem_u32(smem + OFF_RING);
     mbar_wait(q_ready, 0);
     tc_fence_after();
-    int slot = 0;
-    uint32_t ph = 0;
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(&r_full[slot], ph);  // K_j
+    // ring item i sits in slot i % RING, completion phase (i / RING) & 1
+    auto issue_s = [&](int j) {  // S_{j % kStreams} = Q K_j^T
+      const int item = 2 * j, slot = item % RING;
+      mbar_wait(&r_full[slot], (item / RING) & 1);
       tc_fence_after();
       const uint32_t k_addr = ring + slot * TILE;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk / 4) * CHUNK + (kk % 4) * 32;
-          mma_bf16_ss(tmem, sdesc_sw128(q_addr + off), sdesc_sw128(k_addr + off), idesc_s,
-                      kk > 0 ? 1u : 0u);
+          mma_bf16_ss(tmem + (j % kStreams) * 128, sdesc_sw128(q_addr + off), sdesc_sw128(k_addr + off),
+                      idesc_s, kk > 0 ? 1u : 0u);
         }
-        mma_commit(s_full);
+        mma_commit(&s_full[j % kStreams]);
         mma_commit(&r_empty[slot]);
       }
       __syncwarp();
-      if (++slot == RING) { slot = 0; ph ^= 1; }
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&r_full[slot], ph);  // V_j
+    };
+    auto issue_pv = [&](int j) {  // O_{j % kStreams} += P_j V_j
+      const int w = j % kStreams, item = 2 * j + 1, slot = item % RING;
+      mbar_wait(&p_full[w], (j / kStreams) & 1);
+      mbar_wait(&r_full[slot], (item / RING) & 1);
       tc_fence_after();
       const uint32_t v_addr = ring + slot * TILE;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_bf16_ts(tmem + 128, tmem + kk * 8, sdesc_sw128_mn(v_addr + kk * 2048, CHUNK), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(pv_done);
+          mma_bf16_ts(tmem + 128 * kStreams + 128 * w, tmem + w * 128 + kk * 8,
+                      sdesc_sw128_mn(v_addr + kk * 2048, CHUNK), idesc_o,
+                      (j >= kStreams || kk > 0) ? 1u : 0u);
+        mma_commit(&pv_done[w]);
         mma_commit(&r_empty[slot]);
       }
       __syncwarp();
-      if (++slot == RING) { slot = 0; ph ^= 1; }
+    };
+    for (int j = 0; j < kStreams && j < n_tiles; ++j) issue_s(j);
+    for (int j = 0; j < n_tiles; ++j) {
+      issue_pv(j);  // P_j is read before S_{j + kStreams} overwrites it (in-order MMAs)
+      if (j + kStreams < n_tiles) issue_s(j + kStreams);
     }
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane_id();  // query row = TMEM lane
-    const uint32_t lane_off = static_cast<uint32_t>((warp - 4) * 32) << 16;
-    {  // Q row r -> smem, SW128 K-major: 16-byte unit u of a 128-byte row at u ^ (r & 7)
+    const int w = (warp - 4) >> 2;                    // stream of this warpgroup
+    const int r = ((warp - 4) & 3) * 32 + lane_id();  // query row = TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 128 * w, tO = tmem + lane_off + 128 * kStreams + 128 * w;
+    if (w == 0) {  // Q row r -> smem, SW128 K-major: 16-byte unit u of a 128-byte row at u ^ (r & 7)
       uint4 v[16];
       if (r < qn) {
         const int hl = r / a.G, g = r % a.G;
@@ -368,12 +392,13 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
     }
     const int g_of_r = r % a.G;
     float m_run = -INFINITY, l_run = 0.f;
+    int it = 0;  // tiles of this stream
     // two passes over S in TMEM (32 columns at a time, <= 128 registers per
     // thread so two CTAs share an SM): row max, then exp / P / row sum.
     // Visibility is one 32-bit mask per 32 keys, built once per tile: keys
     // below the chunk end, and (row cache) only this query's own rollout row.
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(s_full, j & 1);
+    for (int j = w; j < n_tiles; j += kStreams, ++it) {
+      mbar_wait(&s_full[w], it & 1);
       tc_fence_after();
       const long k0 = k_begin + static_cast<long>(j) * TK;
       const int nv = r < qn ? static_cast<int>(std::min<long>(TK, k_end - k0)) : 0;
@@ -394,25 +419,25 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint32_t x[32];
-        tmem_ld32(tmem + lane_off + 32 * q, x);
+        tmem_ld32(tS + 32 * q, x);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           mx = fmaxf(mx, (vis[q] >> i) & 1u ? __uint_as_float(x[i]) * a.scale_log2 : -INFINITY);
       }
       const float m_new = fmaxf(m_run, mx);
-      if (j > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O (after P.V(j-1))
-        mbar_wait(pv_done, (j - 1) & 1);
+      if (it > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O_w (after its last P.V)
+        mbar_wait(&pv_done[w], (it - 1) & 1);
         tc_fence_after();
         const float alpha = m_new > m_run && m_run != -INFINITY ? exp2f(m_run - m_new) : 1.f;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t o[32];
-          tmem_ld32(tmem + lane_off + 128 + c, o);
+          tmem_ld32(tO + c, o);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(tmem + lane_off + 128 + c, o);
+          tmem_st32(tO + c, o);
         }
         tmem_st_wait();
         l_run *= alpha;
@@ -422,12 +447,12 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
       float acc = 0.f;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {  // 64-key halves: P(half h) -> columns [32 h, 32 h + 32),
-        uint32_t w[32];               // over S columns whose keys are already consumed
+        uint32_t wv[32];              // over S columns whose keys are already consumed
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = h * 64 + cc * 32;
           uint32_t x[32];
-          tmem_ld32(tmem + lane_off + c, x);
+          tmem_ld32(tS + c, x);
           tmem_ld_wait();
           const uint32_t vm = vis[c / 32];
 #pragma unroll
@@ -438,40 +463,41 @@ __global__ void __launch_bounds__(256, kRing == 2 ? 2 : 1)
                                             ? fmaf(__uint_as_float(x[i + 1]), a.scale_log2, nm)
                                             : -INFINITY);
             acc += p0 + p1;
-            w[cc * 16 + i / 2] = pack_bf16(p0, p1);
+            wv[cc * 16 + i / 2] = pack_bf16(p0, p1);
           }
         }
-        tmem_st32(tmem + lane_off + 32 * h, w);
+        tmem_st32(tS + 32 * h, wv);
       }
       tmem_st_wait();
       l_run += acc;
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[w]);
     }
-    // epilogue: the unnormalised partial of this chunk
-    if (n_tiles > 0) {
-      mbar_wait(pv_done, (n_tiles - 1) & 1);
+    // epilogue: the unnormalised partial of this stream of the chunk
+    if (it > 0) {
+      mbar_wait(&pv_done[w], (it - 1) & 1);
       tc_fence_after();
     }
-    float* out = a.part + ((static_cast<size_t>(chunk) * a.n_kv + kvh) * DEC_QN + r) * (HD + 2);
+    float* out = a.part +
+                 ((static_cast<size_t>(chunk * kStreams + w) * a.n_kv + kvh) * DEC_QN + r) * (HD + 2);
 #pragma unroll 1
     for (int c = 0; c < 128; c += 32) {
       uint32_t o[32];
-      tmem_ld32(tmem + lane_off + 128 + c, o);
+      tmem_ld32(tO + c, o);
       tmem_ld_wait();
       if (r < qn)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) out[c + i] = n_tiles > 0 ? __uint_as_float(o[i]) : 0.f;
+        for (int i = 0; i < 32; ++i) out[c + i] = it > 0 ? __uint_as_float(o[i]) : 0.f;
     }
     if (r < qn) {
-      out[HD] = n_tiles > 0 ? m_run : -INFINITY;
+      out[HD] = it > 0 ? m_run : -INFINITY;
       out[HD + 1] = l_run;
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<256>(tmem);
+  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
 }
 }  // namespace tc
 
@@ -674,7 +700,8 @@ void decode_step_advance(int* tdev, cudaStream_t s) {
 size_t decode_partial_bytes(int max_prefix, int max_len, int G, int n_kv) {
   const int chunks = (max_prefix + DEC_CHUNK - 1) / DEC_CHUNK +
                      (max_len * G + DEC_CHUNK - 1) / DEC_CHUNK;
-  return static_cast<size_t>(chunks) * n_kv * DEC_QN * (HD + 2) * sizeof(float);
+  // x 2: the tcgen05 kernel writes one partial per KV stream (two per chunk)
+  return 2 * static_cast<size_t>(chunks) * n_kv * DEC_QN * (HD + 2) * sizeof(float);
 }
 
 // Kernel choice: the tcgen05 kernel (attention 2.0-2.4 ms per c4 decode step,
@@ -732,10 +759,13 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     ta.scale_log2 = a.scale_log2;
     ta.part = part;
     static const bool tc_attr = [] {
-      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<2>,
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<2, 1>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(tc::smem_bytes<2>())));
-      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<6>,
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<6, 1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tc::smem_bytes<6>())));
+      MRSP_CUDA(cudaFuncSetAttribute(tc::dec_attn_tc_kernel<6, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(tc::smem_bytes<6>())));
       return true;
@@ -759,16 +789,22 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     else
       decode_tensor_maps(kv_prefix, Lp, n_kv, kv_rows, static_cast<long>(t + 1) * G, ld_kv, tm);
     const int chunks = ta.n_prefix_chunks + ((t + 1) * G + ta.chunk_keys - 1) / ta.chunk_keys;
+    // one CTA per SM: two KV streams per CTA (MRSP_DECODE_STREAMS=1: one)
+    const char* env_streams = std::getenv("MRSP_DECODE_STREAMS");
+    const int streams = ring == 2 ? 1 : (env_streams ? std::max(1, std::min(2, std::atoi(env_streams))) : 2);
     if (ring == 2)
-      launch_pdl(tc::dec_attn_tc_kernel<2>, dim3(chunks, n_kv), dim3(256), tc::smem_bytes<2>(), s,
-                 tm[0], tm[1], ta);
+      launch_pdl(tc::dec_attn_tc_kernel<2, 1>, dim3(chunks, n_kv), dim3(tc::threads<1>()),
+                 tc::smem_bytes<2>(), s, tm[0], tm[1], ta);
+    else if (streams == 1)
+      launch_pdl(tc::dec_attn_tc_kernel<6, 1>, dim3(chunks, n_kv), dim3(tc::threads<1>()),
+                 tc::smem_bytes<6>(), s, tm[0], tm[1], ta);
     else
-      launch_pdl(tc::dec_attn_tc_kernel<6>, dim3(chunks, n_kv), dim3(256), tc::smem_bytes<6>(), s,
-                 tm[0], tm[1], ta);
+      launch_pdl(tc::dec_attn_tc_kernel<6, 2>, dim3(chunks, n_kv), dim3(tc::threads<2>()),
+                 tc::smem_bytes<6>(), s, tm[0], tm[1], ta);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
-    launch_pdl(dec_merge_kernel, dim3(q_per_kv * G, n_kv), dim3(HD), 0, s, part, chunks, n_kv,
-               q_per_kv, G, static_cast<__nv_bfloat16*>(out), ldo);
+    launch_pdl(dec_merge_kernel, dim3(q_per_kv * G, n_kv), dim3(HD), 0, s, part, chunks * streams,
+               n_kv, q_per_kv, G, static_cast<__nv_bfloat16*>(out), ldo);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
     return;

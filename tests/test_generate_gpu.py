@@ -83,11 +83,18 @@ def test_seed_determinism_and_errors(gpu, gen):
         eng.generate("v", q, 4, 0)  # max_len must be >= 1
 
 
-@pytest.mark.parametrize("cc", ["0", "1"])
-def test_decode_kernels_agree(gpu, gen, cc, monkeypatch):
-    """Both decode-attention kernels (tcgen05 / CUDA cores) give old log-probs that
-    match the engine's prefill of the sampled tokens."""
-    monkeypatch.setenv("MRSP_DECODE_CC", cc)
+@pytest.mark.parametrize("env", [{"MRSP_DECODE_CC": "0"}, {"MRSP_DECODE_CC": "1"},
+                                 {"MRSP_DECODE_RING": "6"},
+                                 {"MRSP_DECODE_RING": "6", "MRSP_DECODE_STREAMS": "1"}],
+                         ids=["tc-ring2", "cuda-cores", "tc-ring6-2streams", "tc-ring6-1stream"])
+def test_decode_kernels_agree(gpu, gen, env, monkeypatch):
+    """Every decode-attention variant (tcgen05 with two CTAs per SM; tcgen05 with
+    one CTA per SM and two or one KV streams; CUDA cores) gives old log-probs that
+    match the engine's prefill of the sampled tokens. At c1 (515 prompt keys,
+    512-key chunks) the second chunk's second stream has no tile (empty partial)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cc = env.get("MRSP_DECODE_CC", "0")
     eng, q = gen["eng"], gen["q"]
     tok, lens, olp = eng.generate("v", q, 8, 16, temperature=0.8, seed=99)
     grp = E.Group(q, _rows(tok, lens), lens.astype(np.int32))
@@ -97,12 +104,15 @@ def test_decode_kernels_agree(gpu, gen, cc, monkeypatch):
     assert d.max() <= 5e-2 and d.mean() <= 5e-3, (cc, d.max(), d.mean())
 
 
-def test_graph_replay_matches_eager(gpu, gen, monkeypatch):
+@pytest.mark.parametrize("ring", ["", "6"], ids=["default", "ring6-2streams"])
+def test_graph_replay_matches_eager(gpu, gen, ring, monkeypatch):
     """Steps t >= 1 replay one captured CUDA graph whose attention grid is sized
     for t = max_len - 1 (chunks past the live row keys are empty): tokens,
     lengths and old log-probs are bit-identical to launching every step eagerly.
     G x max_len = 640 row keys, so early steps run with an empty row chunk."""
     eng, q = gen["eng"], gen["q"]
+    if ring:
+        monkeypatch.setenv("MRSP_DECODE_RING", ring)
     monkeypatch.setenv("MRSP_DECODE_GRAPH", "0")
     eager = eng.generate("v", q, 16, 40, temperature=0.9, seed=5)
     monkeypatch.setenv("MRSP_DECODE_GRAPH", "1")

@@ -58,10 +58,14 @@ def main(names):
         Lp = w.frames * c.tokens_per_frame + w.n_question
         bound_ms = (weights + 2 * L * Lp * 2 * nkv * 128) / (peaks["hbm_gbs"] * 1e9) * 1e3
         for rnd in range(2):
-            for mode in (("0", "0"), ("1", "0"), ("1", "1")):
+            modes = (("0", "0"), ("1", "0"), ("1", "1"))
+            if os.environ.get("GEN_AB_GRAPH_ONLY"):
+                modes = (("1", "0"),)
+            for mode in modes:
                 r = per_step(eng, q, G, mode, profile=False)
                 r.update(per_step(eng, q, G, mode, profile=True))
                 r.update({"workload": name, "G": G, "prompt_tokens": Lp, "graph": mode[0] == "1", "pdl": mode[1] == "1",
+                          "streams": os.environ.get("MRSP_DECODE_STREAMS", "default"),
                           "round": rnd, "hbm_bound_step_ms": round(bound_ms, 3),
                           "hbm_frac_wall": round(bound_ms / r["wall_step_ms"], 3)})
                 print(json.dumps(r), flush=True)
