@@ -23,6 +23,7 @@
 #include "common.h"
 #include "misc.h"
 #include "pdl.cuh"
+#include "rownorm.cuh"
 #include "sm100.cuh"
 #include "tma.h"
 
@@ -643,7 +644,9 @@ __global__ void __launch_bounds__(1024)
 __global__ void decode_embed_kernel(const __nv_bfloat16* __restrict__ embed, int d,
                                     const int* __restrict__ tokens, int max_len,
                                     const int* __restrict__ tdev, int pos_base,
-                                    float* __restrict__ hidden, int* __restrict__ pos_out) {
+                                    float* __restrict__ hidden, int* __restrict__ pos_out,
+                                    const float* __restrict__ norm_w,
+                                    __nv_bfloat16* __restrict__ norm_out, float eps) {
   pdl_wait();
   pdl_trigger();
   const int g = blockIdx.x, t = *tdev, pos = pos_base + t;
@@ -652,6 +655,11 @@ __global__ void decode_embed_kernel(const __nv_bfloat16* __restrict__ embed, int
   const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(embed + static_cast<size_t>(tok) * d);
   float2* dst = reinterpret_cast<float2*>(hidden + static_cast<size_t>(g) * d);
   for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+  if (norm_w) {  // fused first RMSNorm of the step (rmsnorm_kernel's bits)
+    __syncthreads();
+    block_rmsnorm_row(hidden + static_cast<size_t>(g) * d, norm_w, norm_out + static_cast<size_t>(g) * d,
+                      d, eps);
+  }
 }
 
 // rows[t * G + g] = qkv[g][col0, col0 + kvw): this step's post-RoPE K and V
@@ -675,9 +683,11 @@ __global__ void decode_step_advance_kernel(int* tdev) {
 }  // namespace
 
 void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len,
-                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s) {
+                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s,
+                  const float* norm_w, __nv_bfloat16* norm_out, float eps) {
+  MRSP_REQUIRE(d % 4 == 0, MRSP_INVALID_ARGUMENT, "decode_embed: d % 4");
   launch_pdl(decode_embed_kernel, dim3(G), dim3(256), 0, s, embed, d, tokens, max_len, tdev, pos_base,
-             hidden, pos_out);
+             hidden, pos_out, norm_w, norm_out, eps);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
@@ -723,8 +733,8 @@ void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_
 
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                       const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t_grid,
-                      const int* tdev, int q_per_kv, int n_kv, float scale, float* part, void* out,
-                      int ldo, cudaStream_t s, const void* maps) {
+                      int max_rows, const int* tdev, int q_per_kv, int n_kv, float scale,
+                      float* part, void* out, int ldo, cudaStream_t s, const void* maps) {
   const int t = t_grid;
   MRSP_REQUIRE(q_per_kv * G <= DEC_QN, MRSP_INVALID_ARGUMENT,
                "generate: q_per_kv x G must be <= 64");
@@ -775,10 +785,15 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
     // long prompts: one CTA per SM with 3 tiles of K/V in flight (c4: 1.6-1.8
     // vs 2.2-2.8 ms per step); short ones: two CTAs per SM (c2: 0.12 vs 0.17)
     const int ring = env_ring ? std::atoi(env_ring) : (Lp >= 32768 ? 6 : 2);
-    {  // chunks sized so n_kv x chunks ~ one wave (2 or 1 resident CTAs per SM)
+    {  // chunks sized so that n_kv x (prompt chunks + row-cache chunks) fits in
+       // one wave (2 or 1 resident CTAs per SM): a second wave of a few full
+       // chunks would double the kernel's time
       const int per_kv = std::max(1, (ring == 2 ? 2 : 1) * num_sms() / n_kv);
-      ta.chunk_keys = std::max(512, (Lp + per_kv - 1) / per_kv);
-      ta.chunk_keys = (ta.chunk_keys + tc::TK - 1) / tc::TK * tc::TK;
+      const long row_keys = static_cast<long>(max_rows);  // independent of t: eager = graph bits
+      int ck = std::max(512, (Lp + per_kv - 1) / per_kv);
+      ck = (ck + tc::TK - 1) / tc::TK * tc::TK;
+      while ((Lp + ck - 1) / ck + (row_keys + ck - 1) / ck > per_kv) ck += tc::TK;
+      ta.chunk_keys = ck;
       ta.n_prefix_chunks = (Lp + ta.chunk_keys - 1) / ta.chunk_keys;
     }
     // prompt K|V [Lp][ld_kv] and the row cache as TMA tensors (rows past the

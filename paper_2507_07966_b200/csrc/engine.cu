@@ -1177,23 +1177,48 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   // 3. one decode step: tokens -> embeddings -> 28 layers (G-row GEMMs, decode
   // attention over prompt K/V + own-row K/V) -> LM head logits -> sample -> t + 1.
   // Every kernel reads t from `tdev`; t_grid only sizes the attention grid.
+  // Decode fusions (MRSP_DECODE_FUSE=0: off): the first RMSNorm rides on the
+  // token embedding, RoPE + the K|V row-cache append on the QKV split-K
+  // reduction, and each following RMSNorm on the residual split-K reduction
+  // before it (O projection -> MLP norm, down projection -> next layer's
+  // attention norm or the final norm). Same bits as the separate kernels.
+  const char* env_fuse = std::getenv("MRSP_DECODE_FUSE");
+  const bool fuse = !(env_fuse && std::atoi(env_fuse) == 0);
   auto step = [&](int t_grid) {
+    bool xn_ready = false;  // xn already holds the norm the next GEMM needs
     {
       Prof pm(*this, P_MISC);
-      decode_embed(W.embed, d, tokens, max_len, tdev, G, static_cast<int>(Lp), h, pos, s);
+      decode_embed(W.embed, d, tokens, max_len, tdev, G, static_cast<int>(Lp), h, pos, s,
+                   fuse ? W.layers[0].attn_norm : nullptr, xn, c.rms_eps);
+      xn_ready = fuse;
     }
     for (int l = 0; l < c.layers; ++l) {
       const LlmLayerW& Lw = W.layers[l];
-      {
+      const float* next_norm = l + 1 < c.layers ? W.layers[l + 1].attn_norm : W.final_norm;
+      if (!xn_ready) {
         Prof pm(*this, P_MISC);
         rmsnorm(h, d, Lw.attn_norm, xn, d, G, d, c.rms_eps, nullptr, s);
       }
+      bf16* rows_l = kv_rows + static_cast<size_t>(l) * max_len * G * kvw;
+      bool roped = false;
       {
         Prof pg(*this, P_GEMM);
-        dec_gemm({xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr, 0});
+        GemmArgs ga{xn, Lw.wqkv, qkv, G, Cqkv, d, d, d, Cqkv, GEMM_EPI_BIAS_BF16, Lw.bqkv, nullptr, 0};
+        if (fuse) {
+          ga.post = GEMM_POST_ROPE_APPEND;
+          ga.pos = pos;
+          ga.inv_freq = d_inv_freq_;
+          ga.n_rope_blocks = nq + nkv;
+          ga.kv_rows = rows_l;
+          ga.kvw = static_cast<int>(kvw);
+          ga.kv_col0 = nq * 128;
+          ga.tdev = tdev;
+        }
+        ga.splitk_ws = splitk;
+        ga.splitk_ws_bytes = splitk_bytes;
+        roped = gemm_bf16(ga, s);
       }
-      bf16* rows_l = kv_rows + static_cast<size_t>(l) * max_len * G * kvw;
-      {
+      if (!roped) {
         Prof pm(*this, P_MISC);
         rope(qkv, Cqkv, 0, nq + nkv, pos, G, s);
         decode_append_kv(qkv, Cqkv, nq * 128, rows_l, static_cast<int>(kvw), G, tdev, s);
@@ -1202,13 +1227,26 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
         Prof pa(*this, P_ATTN);
         decode_attention(qkv, Cqkv, 0, kv_prefix_.as<bf16>() + static_cast<size_t>(l) * Lp * kvw,
                          rows_l, static_cast<int>(kvw), nkv * 128, static_cast<int>(Lp), G, t_grid,
-                         tdev, qpk, nkv, scale, part, od, Cq, s, tc_decode ? &maps[2 * l] : nullptr);
+                         max_len * G, tdev, qpk, nkv, scale, part, od, Cq, s,
+                         tc_decode ? &maps[2 * l] : nullptr);
       }
-      {
+      // residual GEMM (h += A W^T), optionally followed by the fused norm -> xn
+      auto resid_gemm = [&](const bf16* A, const bf16* Wt, int K, const float* norm_w) {
         Prof pg(*this, P_GEMM);
-        dec_gemm({od, Lw.wo, nullptr, G, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, h, d});
-      }
-      {
+        GemmArgs ga{A, Wt, nullptr, G, d, K, K, K, 0, GEMM_EPI_RESID_F32, nullptr, h, d};
+        if (fuse) {
+          ga.post = GEMM_POST_RMSNORM;
+          ga.norm_w = norm_w;
+          ga.norm_out = xn;
+          ga.ld_norm = d;
+          ga.norm_eps = c.rms_eps;
+        }
+        ga.splitk_ws = splitk;
+        ga.splitk_ws_bytes = splitk_bytes;
+        return gemm_bf16(ga, s);
+      };
+      xn_ready = resid_gemm(od, Lw.wo, Cq, Lw.mlp_norm);
+      if (!xn_ready) {
         Prof pm(*this, P_MISC);
         rmsnorm(h, d, Lw.mlp_norm, xn, d, G, d, c.rms_eps, nullptr, s);
       }
@@ -1216,13 +1254,12 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
         Prof pg(*this, P_GEMM);
         dec_gemm({xn, Lw.wgu, act, G, 2 * c.mlp, d, d, d, c.mlp, GEMM_EPI_SWIGLU_BF16, nullptr,
                   nullptr, 0});
-        dec_gemm({act, Lw.wdown, nullptr, G, d, c.mlp, c.mlp, c.mlp, 0, GEMM_EPI_RESID_F32,
-                  nullptr, h, d});
       }
+      xn_ready = resid_gemm(act, Lw.wdown, c.mlp, next_norm);
     }
     {
       Prof pl(*this, P_LMHEAD);
-      rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
+      if (!xn_ready) rmsnorm(h, d, W.final_norm, xn, d, G, d, c.rms_eps, nullptr, s);
       dec_gemm({xn, W.lm_head, logits, G, c.vocab, d, d, d, c.vocab, GEMM_EPI_STORE_F32, nullptr,
                 nullptr, 0});
     }

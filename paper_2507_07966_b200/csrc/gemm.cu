@@ -27,6 +27,7 @@
 #include "gemm.h"
 #include "misc.h"
 #include "pdl.cuh"
+#include "rownorm.cuh"
 #include "sm100.cuh"
 #include "tma.h"
 
@@ -68,6 +69,15 @@ struct EpiArgs {
   const int2* route;
   void* const* peer_base;
   const int* peer_ld;
+  // decode fusions of the split-K reduction (GemmArgs::post)
+  int post;
+  __nv_bfloat16* kv_rows;
+  int kvw, kv_col0;
+  const int* tdev;
+  const float* norm_w;
+  __nv_bfloat16* norm_out;
+  int ld_norm;
+  float norm_eps;
 };
 
 // Grouped raster: consecutive tiles sweep a GROUP_M-tall band of m-tiles with
@@ -537,6 +547,72 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Split-K second pass: one thread per (row, output column); the splits are
 // summed in order, then the epilogue is applied exactly as epilogue_row does
 // (bias, GELU, SwiGLU over [gate128 | up128] tiles, residual, stores).
+// Split-K reduction + bias + bf16 rounding (GEMM_EPI_BIAS_BF16), then RoPE on
+// the q / k head blocks and the K | V copy into the generation row cache: one
+// thread per (row, head block, frequency pair). The arithmetic is the plain
+// reduction's followed by rope_kernel's (csrc/kernels_misc.cu), element for
+// element, so the fused and unfused decode steps give identical bits.
+__global__ void splitk_reduce_rope_append_kernel(EpiArgs args) {
+  pdl_wait();
+  pdl_trigger();
+  const int nb = args.N / 128;
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(args.M) * nb * 64) return;
+  const int row = static_cast<int>(i / (nb * 64)), rem = static_cast<int>(i % (nb * 64));
+  const int hb = rem / 64, f = rem % 64;
+  const int c0 = hb * 128 + f, c1 = c0 + 64;
+  const size_t plane = static_cast<size_t>(args.M) * args.N;
+  auto sum = [&](int c) {
+    const float* p = args.ws + static_cast<size_t>(row) * args.N + c;
+    float v = p[0];
+    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
+    return v;
+  };
+  float v0 = sum(c0), v1 = sum(c1);
+  if (args.bias) {
+    v0 += args.bias[c0];
+    v1 += args.bias[c1];
+  }
+  __nv_bfloat16 b0 = __float2bfloat16_rn(v0), b1 = __float2bfloat16_rn(v1);
+  if (hb < args.n_rope_blocks) {
+    float sn, cs;
+    sincosf(__fmul_rn(static_cast<float>(args.pos[row]), args.inv_freq[f]), &sn, &cs);
+    const float a = __bfloat162float(b0), b = __bfloat162float(b1);
+    b0 = __float2bfloat16_rn(__fsub_rn(__fmul_rn(a, cs), __fmul_rn(b, sn)));
+    b1 = __float2bfloat16_rn(__fadd_rn(__fmul_rn(b, cs), __fmul_rn(a, sn)));
+  }
+  __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(args.C) + static_cast<size_t>(row) * args.ldc;
+  crow[c0] = b0;
+  crow[c1] = b1;
+  if (c0 >= args.kv_col0 && c1 < args.kv_col0 + args.kvw) {
+    __nv_bfloat16* kr =
+        args.kv_rows + (static_cast<size_t>(*args.tdev) * args.M + row) * args.kvw - args.kv_col0;
+    kr[c0] = b0;
+    kr[c1] = b1;
+  }
+}
+
+// Split-K reduction into the fp32 residual (GEMM_EPI_RESID_F32), then the
+// RMSNorm of the updated row (block_rmsnorm_row: rmsnorm_kernel's bits). One
+// CTA per row.
+__global__ void splitk_reduce_resid_norm_kernel(EpiArgs args) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x;
+  const size_t plane = static_cast<size_t>(args.M) * args.N;
+  float* hr = args.resid + static_cast<size_t>(row) * args.ldr;
+  for (int col = threadIdx.x; col < args.N; col += blockDim.x) {
+    const float* p = args.ws + static_cast<size_t>(row) * args.N + col;
+    float v = p[0];
+    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
+    if (args.bias) v += args.bias[col];
+    hr[col] += v;
+  }
+  __syncthreads();
+  block_rmsnorm_row(hr, args.norm_w, args.norm_out + static_cast<size_t>(row) * args.ld_norm, args.N,
+                    args.norm_eps);
+}
+
 __global__ void splitk_reduce_kernel(EpiArgs args) {
   pdl_wait();
   pdl_trigger();
@@ -749,7 +825,7 @@ constexpr int kDefaultGemmImpl = 1;
 
 }  // namespace
 
-void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
+bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   MRSP_REQUIRE(g.M > 0 && g.N > 0 && g.K > 0, MRSP_INVALID_ARGUMENT, "gemm: empty problem");
   MRSP_REQUIRE(g.K % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0, MRSP_INVALID_ARGUMENT,
                "gemm: K and leading dims must be multiples of 8 (16-byte TMA pitch)");
@@ -773,7 +849,17 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   EpiArgs e{g.M,     g.N,       g.K,     g.epi,     vec_ok,     0,          1, nullptr, g.C,
             g.ldc,
             g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
-            g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld};
+            g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld,
+            GEMM_POST_NONE, static_cast<__nv_bfloat16*>(g.kv_rows), g.kvw, g.kv_col0, g.tdev,
+            g.norm_w, static_cast<__nv_bfloat16*>(g.norm_out), g.ld_norm, g.norm_eps};
+  if (g.post == GEMM_POST_ROPE_APPEND)
+    MRSP_REQUIRE(g.epi == GEMM_EPI_BIAS_BF16 && g.N % 128 == 0 && g.pos && g.inv_freq &&
+                     g.kv_rows && g.tdev && g.kvw % 128 == 0 && g.kv_col0 % 128 == 0,
+                 MRSP_INVALID_ARGUMENT, "gemm rope/append: incomplete arguments");
+  if (g.post == GEMM_POST_RMSNORM)
+    MRSP_REQUIRE(g.epi == GEMM_EPI_RESID_F32 && g.norm_w && g.norm_out && g.N % 4 == 0 &&
+                     g.ldr % 4 == 0,
+                 MRSP_INVALID_ARGUMENT, "gemm resid/norm: incomplete arguments");
   if (g.epi == GEMM_EPI_QKV_SCATTER)
     MRSP_REQUIRE(g.N % 128 == 0 && g.bias && g.pos && g.inv_freq && g.route && g.peer_base &&
                      g.peer_ld,
@@ -837,7 +923,7 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
       gemm_bf16_pair<false><<<grid, THREADS, P_SMEM_BYTES, stream>>>(ta, tbh, tc, e);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
-    return;
+    return false;
   }
   int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   // split-K: one m tile, too few n tiles for the SMs, a workspace, a plain epilogue
@@ -858,13 +944,21 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   launch_pdl(gemm_bf16_tcgen05, dim3(grid), dim3(THREADS), SMEM_BYTES, stream, ta, tb, tc, e);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
-  if (e.k_splits > 1) {
+  if (e.k_splits <= 1) return false;
+  if (g.post == GEMM_POST_ROPE_APPEND) {
+    const long n = static_cast<long>(g.M) * (g.N / 128) * 64;
+    launch_pdl(splitk_reduce_rope_append_kernel, dim3(static_cast<unsigned>((n + 255) / 256)),
+               dim3(256), 0, stream, e);
+  } else if (g.post == GEMM_POST_RMSNORM) {
+    launch_pdl(splitk_reduce_resid_norm_kernel, dim3(g.M), dim3(256), 0, stream, e);
+  } else {
     const long n = static_cast<long>(g.M) * (g.epi == GEMM_EPI_SWIGLU_BF16 ? g.N / 2 : g.N);
     launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0,
                stream, e);
-    count_launch();
-    MRSP_CUDA(cudaGetLastError());
   }
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  return g.post != GEMM_POST_NONE;
 }
 
 size_t gemm_splitk_ws_bytes(int M) {

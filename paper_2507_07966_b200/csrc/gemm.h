@@ -37,12 +37,31 @@ struct GemmArgs {
   // (deterministic) and applies the epilogue. Null: no split.
   float* splitk_ws = nullptr;
   size_t splitk_ws_bytes = 0;
+  // Decode fusions done by the split-K reduction (gemm_bf16 returns true when
+  // it applied them; false when K was not split and the caller must run them
+  // as separate kernels):
+  //  GEMM_POST_ROPE_APPEND (GEMM_EPI_BIAS_BF16): after bias + bf16 rounding,
+  //    RoPE the first n_rope_blocks 128-column head blocks at pos (inv_freq),
+  //    and copy columns [kv_col0, kv_col0 + kvw) of row r to
+  //    kv_rows + ((*tdev) * M + r) * kvw (the generation row cache);
+  //  GEMM_POST_RMSNORM (GEMM_EPI_RESID_F32): after the residual add,
+  //    norm_out[r] = bf16(rmsnorm(resid[r]) * norm_w), one CTA per row.
+  int post = 0;
+  void* kv_rows = nullptr;
+  int kvw = 0, kv_col0 = 0;
+  const int* tdev = nullptr;
+  const float* norm_w = nullptr;
+  void* norm_out = nullptr;
+  int ld_norm = 0;
+  float norm_eps = 0.f;
 };
+
+enum { GEMM_POST_NONE = 0, GEMM_POST_ROPE_APPEND = 1, GEMM_POST_RMSNORM = 2 };
 
 // Workspace that lets every one-m-tile GEMM of M rows split fully.
 size_t gemm_splitk_ws_bytes(int M);
 
-void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
+bool gemm_bf16(const GemmArgs& g, cudaStream_t stream);
 
 // Fused LM head: per row, log softmax(X W^T)[target] and the log-partition,
 // never materialising the [M x V] logits.

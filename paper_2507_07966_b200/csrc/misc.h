@@ -39,13 +39,17 @@ void decode_tensor_maps(const void* kv_prefix, int Lp, int n_kv, const void* kv_
 // Decode steps read the step index t from device memory (`tdev`), so one
 // captured CUDA graph of a step replays for every t; host-side `t_grid` only
 // sizes the attention grid (the current t eagerly, max_len - 1 in a graph:
-// chunks past the live row keys write empty partials).
+// chunks past the live row keys write empty partials). max_rows (max_len x G)
+// sizes the chunks, so eager and graph steps split the keys identically.
 void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                       const void* kv_rows, int ld_kv, int v_off, int Lp, int G, int t_grid,
-                      const int* tdev, int q_per_kv, int n_kv, float scale, float* part, void* out,
-                      int ldo, cudaStream_t s, const void* maps = nullptr);
+                      int max_rows, const int* tdev, int q_per_kv, int n_kv, float scale,
+                      float* part, void* out, int ldo, cudaStream_t s, const void* maps = nullptr);
+// norm_w non-null: also out = RMSNorm(hidden) (the first layer's attention norm)
 void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_len,
-                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s);
+                  const int* tdev, int G, int pos_base, float* hidden, int* pos_out, cudaStream_t s,
+                  const float* norm_w = nullptr, __nv_bfloat16* norm_out = nullptr,
+                  float eps = 0.f);
 // rows[t * G + g][0, kvw) = qkv[g][col0, col0 + kvw) (this step's K | V per row)
 void decode_append_kv(const __nv_bfloat16* qkv, int ldq, int col0, __nv_bfloat16* rows, int kvw,
                       int G, const int* tdev, cudaStream_t s);

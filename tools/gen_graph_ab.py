@@ -66,6 +66,7 @@ def main(names):
                 r.update(per_step(eng, q, G, mode, profile=True))
                 r.update({"workload": name, "G": G, "prompt_tokens": Lp, "graph": mode[0] == "1", "pdl": mode[1] == "1",
                           "streams": os.environ.get("MRSP_DECODE_STREAMS", "default"),
+                          "fuse": os.environ.get("MRSP_DECODE_FUSE", "default"),
                           "round": rnd, "hbm_bound_step_ms": round(bound_ms, 3),
                           "hbm_frac_wall": round(bound_ms / r["wall_step_ms"], 3)})
                 print(json.dumps(r), flush=True)
