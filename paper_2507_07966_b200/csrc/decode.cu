@@ -502,23 +502,66 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
 }
 }  // namespace tc
 
-// O[g][h*128 + d] = sum_c O_c 2^(m_c - m) / sum_c l_c 2^(m_c - m)
-__global__ void dec_merge_kernel(const float* __restrict__ part, int n_chunks, int n_kv,
-                                 int q_per_kv, int G, __nv_bfloat16* __restrict__ out, int ldo) {
+// O[g][h*128 + d] = sum_c O_c 2^(m_c - m) / sum_c l_c 2^(m_c - m). The chunk
+// maxima and weights are formed by all threads at once (smem); four groups of
+// 128 threads (one per column) sum every fourth chunk with the loads unrolled,
+// and the four group sums are added in group order (deterministic). Empty
+// chunks (m_c = -inf) carry weight 0 and zero partials.
+constexpr int kMergeMaxChunks = 1024, kMergeGroups = 4;
+__global__ void __launch_bounds__(HD * kMergeGroups)
+    dec_merge_kernel(const float* __restrict__ part, int n_chunks, int n_kv, int q_per_kv, int G,
+                     __nv_bfloat16* __restrict__ out, int ldo) {
   pdl_wait();
   pdl_trigger();
-  const int qi = blockIdx.x, kvh = blockIdx.y, d = threadIdx.x;  // blockDim = 128
+  __shared__ float s_w[kMergeMaxChunks], s_l[kMergeMaxChunks], s_red[HD * kMergeGroups / 32];
+  __shared__ float s_o[kMergeGroups][HD], s_lg[kMergeGroups];
+  const int qi = blockIdx.x, kvh = blockIdx.y, tid = threadIdx.x;
+  const int d = tid % HD, grp = tid / HD;
   const int hl = qi / G, g = qi % G;
+  auto row = [&](int c) {
+    return part + ((static_cast<size_t>(c) * n_kv + kvh) * DEC_QN + qi) * (HD + 2);
+  };
   float m = -INFINITY;
-  for (int c = 0; c < n_chunks; ++c)
-    m = fmaxf(m, part[((static_cast<size_t>(c) * n_kv + kvh) * DEC_QN + qi) * (HD + 2) + HD]);
+  for (int c = tid; c < n_chunks; c += blockDim.x) {
+    const float mc = row(c)[HD];
+    s_w[c] = mc;
+    s_l[c] = row(c)[HD + 1];
+    m = fmaxf(m, mc);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) s_red[tid >> 5] = m;
+  __syncthreads();
+  m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < HD * kMergeGroups / 32; ++i) m = fmaxf(m, s_red[i]);
+  for (int c = tid; c < n_chunks; c += blockDim.x) s_w[c] = s_w[c] == -INFINITY ? 0.f : exp2f(s_w[c] - m);
+  __syncthreads();
+  float lg = 0.f, og = 0.f;
+  int c = grp;
+  for (; c + 3 * kMergeGroups < n_chunks; c += 4 * kMergeGroups) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = row(c + u * kMergeGroups)[d];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      lg += s_l[c + u * kMergeGroups] * s_w[c + u * kMergeGroups];
+      og += v[u] * s_w[c + u * kMergeGroups];
+    }
+  }
+  for (; c < n_chunks; c += kMergeGroups) {
+    lg += s_l[c] * s_w[c];
+    og += row(c)[d] * s_w[c];
+  }
+  s_o[grp][d] = og;
+  if (d == 0) s_lg[grp] = lg;
+  __syncthreads();
+  if (grp != 0) return;
   float l = 0.f, o = 0.f;
-  for (int c = 0; c < n_chunks; ++c) {
-    const float* p = part + ((static_cast<size_t>(c) * n_kv + kvh) * DEC_QN + qi) * (HD + 2);
-    if (p[HD] == -INFINITY) continue;
-    const float w = exp2f(p[HD] - m);
-    l += p[HD + 1] * w;
-    o += p[d] * w;
+#pragma unroll
+  for (int k = 0; k < kMergeGroups; ++k) {
+    l += s_lg[k];
+    o += s_o[k][d];
   }
   out[static_cast<size_t>(g) * ldo + (kvh * q_per_kv + hl) * HD + d] =
       __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
@@ -818,7 +861,10 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
                  tc::smem_bytes<6>(), s, tm[0], tm[1], ta);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
-    launch_pdl(dec_merge_kernel, dim3(q_per_kv * G, n_kv), dim3(HD), 0, s, part, chunks * streams,
+    MRSP_REQUIRE(chunks * streams <= kMergeMaxChunks, MRSP_INVALID_ARGUMENT,
+                 "decode attention: too many key chunks");
+    launch_pdl(dec_merge_kernel, dim3(q_per_kv * G, n_kv), dim3(HD * kMergeGroups), 0, s, part,
+               chunks * streams,
                n_kv, q_per_kv, G, static_cast<__nv_bfloat16*>(out), ldo);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
@@ -836,7 +882,8 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   dec_attn_kernel<<<dim3(chunks, n_kv), 256, smem, s>>>(a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
-  dec_merge_kernel<<<dim3(q_per_kv * G, n_kv), HD, 0, s>>>(part, chunks, n_kv, q_per_kv, G,
+  MRSP_REQUIRE(chunks <= kMergeMaxChunks, MRSP_INVALID_ARGUMENT, "decode attention: too many key chunks");
+  dec_merge_kernel<<<dim3(q_per_kv * G, n_kv), HD * kMergeGroups, 0, s>>>(part, chunks, n_kv, q_per_kv, G,
                                                            static_cast<__nv_bfloat16*>(out), ldo);
   count_launch();
   MRSP_CUDA(cudaGetLastError());

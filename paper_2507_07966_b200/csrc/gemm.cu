@@ -547,6 +547,21 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Split-K second pass: one thread per (row, output column); the splits are
 // summed in order, then the epilogue is applied exactly as epilogue_row does
 // (bias, GELU, SwiGLU over [gate128 | up128] tiles, residual, stores).
+// Sum of the k_splits fp32 partials of (row, c) in split order, with every
+// partial's load issued before the first add (the reductions are latency-bound).
+constexpr int kMaxSplits = 16;
+__device__ __forceinline__ float split_sum(const EpiArgs& args, int row, int c, size_t plane) {
+  const float* p = args.ws + static_cast<size_t>(row) * args.N + c;
+  float pv[kMaxSplits];
+#pragma unroll
+  for (int s = 0; s < kMaxSplits; ++s) pv[s] = s < args.k_splits ? p[s * plane] : 0.f;
+  float v = pv[0];
+#pragma unroll
+  for (int s = 1; s < kMaxSplits; ++s)
+    if (s < args.k_splits) v += pv[s];
+  return v;
+}
+
 // Split-K reduction + bias + bf16 rounding (GEMM_EPI_BIAS_BF16), then RoPE on
 // the q / k head blocks and the K | V copy into the generation row cache: one
 // thread per (row, head block, frequency pair). The arithmetic is the plain
@@ -562,12 +577,7 @@ __global__ void splitk_reduce_rope_append_kernel(EpiArgs args) {
   const int hb = rem / 64, f = rem % 64;
   const int c0 = hb * 128 + f, c1 = c0 + 64;
   const size_t plane = static_cast<size_t>(args.M) * args.N;
-  auto sum = [&](int c) {
-    const float* p = args.ws + static_cast<size_t>(row) * args.N + c;
-    float v = p[0];
-    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
-    return v;
-  };
+  auto sum = [&](int c) { return split_sum(args, row, c, plane); };
   float v0 = sum(c0), v1 = sum(c1);
   if (args.bias) {
     v0 += args.bias[c0];
@@ -593,24 +603,56 @@ __global__ void splitk_reduce_rope_append_kernel(EpiArgs args) {
 }
 
 // Split-K reduction into the fp32 residual (GEMM_EPI_RESID_F32), then the
-// RMSNorm of the updated row (block_rmsnorm_row: rmsnorm_kernel's bits). One
-// CTA per row.
-__global__ void splitk_reduce_resid_norm_kernel(EpiArgs args) {
+// RMSNorm of the updated row. One cluster of 4 CTAs per row, one column per
+// thread (every split partial of the row in flight at once); the sum of
+// squares is reduced per CTA in a fixed order and combined over the cluster
+// through distributed shared memory in rank order, so every CTA derives the
+// same scale and the result is deterministic.
+__device__ __forceinline__ float ld_shared_cluster_f32(const float* p, uint32_t rank) {
+  const uint32_t a = mapa_shared(smem_u32(p), rank);
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+constexpr int kNormParts = 4;
+__global__ void __cluster_dims__(kNormParts, 1, 1) __launch_bounds__(1024)
+    splitk_reduce_resid_norm_kernel(EpiArgs args) {
   pdl_wait();
   pdl_trigger();
-  const int row = blockIdx.x;
+  __shared__ float s_warp[32];
+  __shared__ float s_ss;
+  const int part = blockIdx.x, row = blockIdx.y, tid = threadIdx.x;
+  const int cols = args.N / kNormParts, col = part * cols + tid;
+  const bool act = tid < cols;
   const size_t plane = static_cast<size_t>(args.M) * args.N;
-  float* hr = args.resid + static_cast<size_t>(row) * args.ldr;
-  for (int col = threadIdx.x; col < args.N; col += blockDim.x) {
-    const float* p = args.ws + static_cast<size_t>(row) * args.N + col;
-    float v = p[0];
-    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
+  float h = 0.f;
+  if (act) {
+    float v = split_sum(args, row, col, plane);
     if (args.bias) v += args.bias[col];
-    hr[col] += v;
+    float* hp = args.resid + static_cast<size_t>(row) * args.ldr + col;
+    h = *hp + v;
+    *hp = h;
   }
+  float ss = h * h;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((tid & 31) == 0) s_warp[tid >> 5] = ss;
   __syncthreads();
-  block_rmsnorm_row(hr, args.norm_w, args.norm_out + static_cast<size_t>(row) * args.ld_norm, args.N,
-                    args.norm_eps);
+  if (tid < 32) {
+    float w = tid < static_cast<int>(blockDim.x >> 5) ? s_warp[tid] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (tid == 0) s_ss = w;
+  }
+  cluster_sync();
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormParts; ++k) tot += ld_shared_cluster_f32(&s_ss, k);
+  const float r = rsqrtf(tot / static_cast<float>(args.N) + args.norm_eps);
+  if (act)
+    args.norm_out[static_cast<size_t>(row) * args.ld_norm + col] =
+        __float2bfloat16_rn(args.norm_w[col] * (h * r));
+  cluster_sync();  // peers may still read s_ss
 }
 
 __global__ void splitk_reduce_kernel(EpiArgs args) {
@@ -622,12 +664,7 @@ __global__ void splitk_reduce_kernel(EpiArgs args) {
   if (i >= static_cast<long>(args.M) * n_out) return;
   const int row = static_cast<int>(i / n_out), col = static_cast<int>(i % n_out);
   const size_t plane = static_cast<size_t>(args.M) * args.N;
-  auto sum = [&](int c) {
-    const float* p = args.ws + static_cast<size_t>(row) * args.N + c;
-    float v = p[0];
-    for (int s = 1; s < args.k_splits; ++s) v += p[s * plane];
-    return v;
-  };
+  auto sum = [&](int c) { return split_sum(args, row, c, plane); };
   if (swiglu) {
     const int c0 = (col / 128) * 256 + col % 128;
     const float g = sum(c0), u = sum(c0 + 128);
@@ -950,7 +987,10 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     launch_pdl(splitk_reduce_rope_append_kernel, dim3(static_cast<unsigned>((n + 255) / 256)),
                dim3(256), 0, stream, e);
   } else if (g.post == GEMM_POST_RMSNORM) {
-    launch_pdl(splitk_reduce_resid_norm_kernel, dim3(g.M), dim3(256), 0, stream, e);
+    MRSP_REQUIRE(g.N % kNormParts == 0 && g.N / kNormParts <= 1024, MRSP_INVALID_ARGUMENT,
+                 "gemm resid/norm: row too long");
+    launch_pdl(splitk_reduce_resid_norm_kernel, dim3(kNormParts, g.M),
+               dim3(((g.N / kNormParts + 31) / 32) * 32), 0, stream, e);
   } else {
     const long n = static_cast<long>(g.M) * (g.epi == GEMM_EPI_SWIGLU_BF16 ? g.N / 2 : g.N);
     launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0,
