@@ -394,15 +394,37 @@ __device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUten
   }
 }
 
+// kStages / kARows: the ring depth and the rows of A loaded per stage. The
+// default (4, 128) serves every prefill GEMM. The skinny variant (6, 16) is for
+// M <= 16 (the decode steps' G rows): each stage holds a 16-row A box (2 KB)
+// in front of its 32 KB B tile, so 6 stages of weights are in flight instead of
+// 4; the M = 128 MMA still reads 128 A rows, rows 16..127 being whatever bytes
+// follow in the stage (the B tile) — they only produce accumulator rows >= 16,
+// which no epilogue stores. No staged-epilogue boxes (row epilogue only).
+template <int kStages, int kARows>
+struct GemmCfg {
+  static constexpr int kABytes = kARows * BK * 2;
+  static constexpr int kStageBytes = kABytes + B_BYTES;
+  static constexpr int kOutBytes = kARows == BM ? OUT_BYTES : 0;
+  static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kOutBytes + 256;
+  static_assert(kABytes % 1024 == 0, "A box = whole SW128 atoms");
+  static_assert(kARows == BM || kStageBytes >= A_BYTES, "MMA reads 128 A rows inside the stage");
+};
+
+template <int kStages, int kARows>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
+  using Cfg = GemmCfg<kStages, kARows>;
+  constexpr int STAGES = kStages;
+  constexpr int STAGE_BYTES = Cfg::kStageBytes;
+  constexpr int A_STAGE = Cfg::kABytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* out_boxes = smem + STAGES * STAGE_BYTES;  // [4 warps][2][OUT_BOX]
-  uint64_t* full = reinterpret_cast<uint64_t*>(out_boxes + OUT_BYTES);
+  uint8_t* out_boxes = smem + STAGES * STAGE_BYTES;  // [4 warps][2][OUT_BOX] (default only)
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_boxes + Cfg::kOutBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -456,7 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint8_t* sa = smem + stage * STAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+          tma_load_2d(sa + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -478,7 +500,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
+          const uint32_t b_addr = a_addr + A_STAGE;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             mma_bf16_ss(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-      } else if (args.staged)
+      } else if (kARows == BM && args.staged)
         epilogue_staged(args, &tmC, t_row, mt * BM + ew * 32, nt, boxes, buf);
       else
         epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
@@ -535,7 +557,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (args.staged && lane_id() == 0) bulk_wait_all();
+    if (kARows == BM && args.staged && lane_id() == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -859,6 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // GEMMs -80 ms, the attention that follows every GEMM +590 ms, step -4.5%
 // (tools/ab_gemm.sh, same box). The single-CTA kernel is the default.
 constexpr int kDefaultGemmImpl = 1;
+constexpr int kSkinnyStages = 6, kSkinnyRows = 16;
 
 }  // namespace
 
@@ -871,12 +894,22 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   if (g.epi == GEMM_EPI_RESID_F32)
     MRSP_REQUIRE(g.resid != nullptr, MRSP_INVALID_ARGUMENT, "gemm resid: null residual");
   static const bool attr_set = [] {  // thread-safe one-time setup (C-ABI callers may race)
-    MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(SMEM_BYTES)));
+    MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<STAGES, BM>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(GemmCfg<STAGES, BM>::kSmem)));
+    MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<kSkinnyStages, kSkinnyRows>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(GemmCfg<kSkinnyStages, kSkinnyRows>::kSmem)));
     return true;
   }();
   (void)attr_set;
-  CUtensorMap ta = make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, BM, BK);
+  // skinny ring for M <= 16 (MRSP_GEMM_SKINNY=0: off), plain epilogues only
+  const char* env_skinny = std::getenv("MRSP_GEMM_SKINNY");
+  const bool skinny_epi = g.epi == GEMM_EPI_STORE_BF16 || g.epi == GEMM_EPI_BIAS_BF16 ||
+                          g.epi == GEMM_EPI_BIAS_GELU_BF16 || g.epi == GEMM_EPI_RESID_F32 ||
+                          g.epi == GEMM_EPI_SWIGLU_BF16 || g.epi == GEMM_EPI_STORE_F32;
+  const bool skinny = g.M <= kSkinnyRows && skinny_epi && !(env_skinny && std::atoi(env_skinny) == 0);
+  CUtensorMap ta = make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, skinny ? kSkinnyRows : BM, BK);
   CUtensorMap tb = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BN, BK);
   const bool f32_out = g.epi == GEMM_EPI_STORE_F32;
   const uintptr_t out_addr = reinterpret_cast<uintptr_t>(g.epi == GEMM_EPI_RESID_F32 ? g.resid : g.C);
@@ -978,7 +1011,14 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
     }
   }
   const int grid = std::min(tiles, num_sms());
-  launch_pdl(gemm_bf16_tcgen05, dim3(grid), dim3(THREADS), SMEM_BYTES, stream, ta, tb, tc, e);
+  if (skinny) {
+    e.staged = 0;
+    launch_pdl(gemm_bf16_tcgen05<kSkinnyStages, kSkinnyRows>, dim3(grid), dim3(THREADS),
+               GemmCfg<kSkinnyStages, kSkinnyRows>::kSmem, stream, ta, tb, tc, e);
+  } else {
+    launch_pdl(gemm_bf16_tcgen05<STAGES, BM>, dim3(grid), dim3(THREADS), GemmCfg<STAGES, BM>::kSmem,
+               stream, ta, tb, tc, e);
+  }
   count_launch();
   MRSP_CUDA(cudaGetLastError());
   if (e.k_splits <= 1) return false;

@@ -104,3 +104,26 @@ def test_gemm_splitk_epilogues(gpu, gemm_impl, M, N, K):
     C2 = ops.gemm(A, B, ops.EPI_STORE_F32, splitk_ws=ws)
     assert torch.equal(C, C2)
     assert rel_err(C, ops.gemm(A, B, ops.EPI_STORE_F32)) < 5e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 4608, 3584), (16, 37888, 3584), (3, 152064, 256)])
+def test_gemm_skinny_matches_default(gpu, gemm_impl, M, N, K, monkeypatch):
+    """M <= 16: the skinny ring (16-row A boxes, 6 stages) gives the same bits as
+    the default 128-row tile for the rows that exist, split or not."""
+    if gemm_impl != "1":
+        pytest.skip("the skinny ring is a mode of the single-CTA kernel")
+    g = torch.Generator(device="cuda").manual_seed(M * N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    ws = torch.empty(ops.splitk_workspace_bytes(M), dtype=torch.uint8, device="cuda")
+    out = {}
+    for sk in ("0", "1"):
+        monkeypatch.setenv("MRSP_GEMM_SKINNY", sk)
+        out[sk] = [ops.gemm(A, B, ops.EPI_STORE_F32), ops.gemm(A, B, ops.EPI_STORE_F32, splitk_ws=ws),
+                   ops.gemm(A, B, ops.EPI_BIAS_BF16, bias=bias),
+                   ops.gemm(A, B, ops.EPI_SWIGLU_BF16) if N % 256 == 0 else None]
+    for x, y in zip(out["0"], out["1"]):
+        if x is not None:
+            assert torch.equal(x, y)
+    assert rel_err(out["1"][0], ref(A, B)) < 1e-5
