@@ -418,13 +418,16 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t x[32];
-        tmem_ld32(tS + 32 * q, x);
+      for (int qq = 0; qq < 4; qq += 2) {  // two TMEM loads in flight per wait
+        uint32_t x[2][32];
+        tmem_ld32(tS + 32 * qq, x[0]);
+        tmem_ld32(tS + 32 * qq + 32, x[1]);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          mx = fmaxf(mx, (vis[q] >> i) & 1u ? __uint_as_float(x[i]) * a.scale_log2 : -INFINITY);
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            mx = fmaxf(mx, (vis[qq + u] >> i) & 1u ? __uint_as_float(x[u][i]) * a.scale_log2 : -INFINITY);
       }
       const float m_new = fmaxf(m_run, mx);
       if (it > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O_w (after its last P.V)
@@ -449,12 +452,14 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {  // 64-key halves: P(half h) -> columns [32 h, 32 h + 32),
         uint32_t wv[32];              // over S columns whose keys are already consumed
+        uint32_t xh[2][32];
+        tmem_ld32(tS + h * 64, xh[0]);
+        tmem_ld32(tS + h * 64 + 32, xh[1]);
+        tmem_ld_wait();
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = h * 64 + cc * 32;
-          uint32_t x[32];
-          tmem_ld32(tS + c, x);
-          tmem_ld_wait();
+          const uint32_t* x = xh[cc];
           const uint32_t vm = vis[c / 32];
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {  // ex2(-inf) = 0 for masked keys
