@@ -579,80 +579,129 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// One CTA per row: p = softmax(logits / T); token = first v with cdf(v) > u,
-// u = (splitmix64(seed, row, t) >> 11) * 2^-53; old_lp = log_softmax(logits)[token]
+// Sampling, p = softmax(logits / T); token = first v with cdf(v) > u,
+// u = (splitmix64(seed, row, t) >> 11) * 2^-53 * Z; old_lp = log_softmax(logits)[token]
 // at temperature 1 (policy.cpp:130-134). Rows already finished (EOS) only
-// record PAD. One thread-block scan over the vocabulary, fp64 accumulation.
+// record PAD. fp64 accumulation. Two kernels so the vocabulary sweep spreads
+// over the SMs: sample_slices_kernel (grid kSampleSlices x G) reduces each
+// vocabulary slice to (max, sum exp((x - max) / T), sum exp(x - max)), and
+// sample_pick_kernel (one CTA per row) combines the slices in slice order,
+// finds the slice holding u, and walks only that slice.
+constexpr int kSampleSlices = 16;
+
+template <typename T>
+__device__ __forceinline__ T block_reduce(T v, T* red, bool is_max) {
+  const int tid = threadIdx.x, nw = blockDim.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    const T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? (v > w ? v : w) : v + w;
+  }
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  if (tid < 32) {
+    v = tid < nw ? red[tid] : (is_max ? static_cast<T>(-INFINITY) : static_cast<T>(0));
+    for (int o = 16; o; o >>= 1) {
+      const T w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? (v > w ? v : w) : v + w;
+    }
+    if (tid == 0) red[0] = v;
+  }
+  __syncthreads();
+  const T r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256)
+    sample_slices_kernel(const float* __restrict__ logits, int V, float inv_temp,
+                         const int* __restrict__ done, double* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
+  const int sl = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+  if (done[g]) return;
+  __shared__ float redf[32];
+  __shared__ double red[32];
+  const int v0 = static_cast<int>(static_cast<long>(V) * sl / kSampleSlices);
+  const int v1 = static_cast<int>(static_cast<long>(V) * (sl + 1) / kSampleSlices);
+  const float* x = logits + static_cast<size_t>(g) * V;
+  float mx = -INFINITY;
+  for (int v = v0 + tid; v < v1; v += blockDim.x) mx = fmaxf(mx, x[v]);
+  mx = block_reduce<float>(mx, redf, true);
+  double zs = 0.0, z1 = 0.0;
+  for (int v = v0 + tid; v < v1; v += blockDim.x) {
+    const double d = static_cast<double>(x[v]) - mx;
+    zs += exp(d * inv_temp);
+    z1 += exp(d);
+  }
+  zs = block_reduce<double>(zs, red, false);
+  z1 = block_reduce<double>(z1, red, false);
+  if (tid == 0) {
+    double* p = part + (static_cast<size_t>(g) * kSampleSlices + sl) * 3;
+    p[0] = mx;
+    p[1] = zs;
+    p[2] = z1;
+  }
+}
+
 __global__ void __launch_bounds__(1024)
-    sample_kernel(const float* __restrict__ logits, int V, float inv_temp, uint64_t seed,
-                  const int* __restrict__ tdev,
-                  int* __restrict__ done, int* __restrict__ tokens, float* __restrict__ old_lp,
-                  int* __restrict__ lengths, int max_len, int eos, int pad) {
+    sample_pick_kernel(const float* __restrict__ logits, int V, float inv_temp, uint64_t seed,
+                       const int* __restrict__ tdev, const double* __restrict__ part,
+                       int* __restrict__ done, int* __restrict__ tokens, float* __restrict__ old_lp,
+                       int* __restrict__ lengths, int max_len, int eos, int pad) {
   pdl_wait();
   pdl_trigger();
   const int g = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, t = *tdev;
   __shared__ double red[32];
-  __shared__ float redf[32];
-  __shared__ int pick;
+  __shared__ double s_cum[kSampleSlices];
+  __shared__ int pick, s_slice;
+  __shared__ double s_base, s_m, s_z1;
   if (done[g]) {
     if (tid == 0) tokens[static_cast<size_t>(g) * max_len + t] = pad;
     return;
   }
   const float* x = logits + static_cast<size_t>(g) * V;
-  auto block_max = [&](float v) {
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((tid & 31) == 0) redf[tid >> 5] = v;
-    __syncthreads();
-    if (tid < 32) {
-      v = tid < (nt >> 5) ? redf[tid] : -INFINITY;
-      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (tid == 0) redf[0] = v;
+  const double* p = part + static_cast<size_t>(g) * kSampleSlices * 3;
+  if (tid == 0) {  // combine the slices in slice order
+    double m = -INFINITY;
+    for (int s = 0; s < kSampleSlices; ++s) m = fmax(m, p[3 * s]);
+    double zs = 0.0, z1 = 0.0;
+    for (int s = 0; s < kSampleSlices; ++s) {
+      zs += p[3 * s + 1] * exp((p[3 * s] - m) * inv_temp);
+      z1 += p[3 * s + 2] * exp(p[3 * s] - m);
+      s_cum[s] = zs;
     }
-    __syncthreads();
-    const float r = redf[0];
-    __syncthreads();
-    return r;
-  };
-  auto block_sum = [&](double v) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) red[tid >> 5] = v;
-    __syncthreads();
-    if (tid < 32) {
-      v = tid < (nt >> 5) ? red[tid] : 0.0;
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (tid == 0) red[0] = v;
-    }
-    __syncthreads();
-    const double r = red[0];
-    __syncthreads();
-    return r;
-  };
-  float mx = -INFINITY;
-  for (int v = tid; v < V; v += nt) mx = fmaxf(mx, x[v]);
-  mx = block_max(mx);
-  double zs = 0.0, z1 = 0.0;  // sum exp((x - mx) / T), sum exp(x - mx)
-  for (int v = tid; v < V; v += nt) {
-    zs += exp((static_cast<double>(x[v]) - mx) * inv_temp);
-    z1 += exp(static_cast<double>(x[v]) - mx);
+    const double u = static_cast<double>(mix64(seed ^ mix64((static_cast<uint64_t>(g) << 32) |
+                                                           static_cast<uint32_t>(t))) >> 11) *
+                     0x1.0p-53 * zs;
+    int sl = kSampleSlices - 1;
+    for (int s = 0; s < kSampleSlices; ++s)
+      if (u < s_cum[s]) {
+        sl = s;
+        break;
+      }
+    s_slice = sl;
+    s_base = u - (sl ? s_cum[sl - 1] : 0.0);  // u relative to the slice start
+    s_m = m;
+    s_z1 = z1;
   }
-  zs = block_sum(zs);
-  z1 = block_sum(z1);
-  const double u = static_cast<double>(mix64(seed ^ mix64((static_cast<uint64_t>(g) << 32) |
-                                                         static_cast<uint32_t>(t))) >> 11) *
-                   0x1.0p-53 * zs;
-  // inverse CDF: each thread owns a contiguous slice; exclusive scan of the
-  // slice sums finds the slice containing u, then that thread walks it
-  const int per = (V + nt - 1) / nt, v0 = tid * per, v1 = min(V, v0 + per);
+  __syncthreads();
+  const int sl = s_slice;
+  const double m = s_m, u = s_base;
+  const int v0s = static_cast<int>(static_cast<long>(V) * sl / kSampleSlices);
+  const int v1s = static_cast<int>(static_cast<long>(V) * (sl + 1) / kSampleSlices);
+  // inverse CDF inside the slice: each thread owns a contiguous piece; an
+  // exclusive scan of the piece sums finds the piece containing u, then that
+  // thread walks it
+  const int per = (v1s - v0s + nt - 1) / nt, v0 = v0s + tid * per, v1 = min(v1s, v0 + per);
   double mine = 0.0;
-  for (int v = v0; v < v1; ++v) mine += exp((static_cast<double>(x[v]) - mx) * inv_temp);
-  // block-wide inclusive scan via warp scans
+  for (int v = v0; v < v1; ++v) mine += exp((static_cast<double>(x[v]) - m) * inv_temp);
   double inc = mine;
   for (int o = 1; o < 32; o <<= 1) {
     const double n = __shfl_up_sync(0xffffffffu, inc, o);
     if ((tid & 31) >= o) inc += n;
   }
   if ((tid & 31) == 31) red[tid >> 5] = inc;
-  if (tid == 0) pick = V - 1;
+  if (tid == 0) pick = v1s - 1;
   __syncthreads();
   if (tid < 32) {
     double w = tid < (nt >> 5) ? red[tid] : 0.0;
@@ -664,11 +713,11 @@ __global__ void __launch_bounds__(1024)
   }
   __syncthreads();
   const double before = inc - mine + ((tid >> 5) ? red[(tid >> 5) - 1] : 0.0);
-  if (u >= before && u < before + mine) {
+  if (v0 < v1 && u >= before && u < before + mine) {
     double c = before;
     int chosen = v1 - 1;
     for (int v = v0; v < v1; ++v) {
-      c += exp((static_cast<double>(x[v]) - mx) * inv_temp);
+      c += exp((static_cast<double>(x[v]) - m) * inv_temp);
       if (u < c) {
         chosen = v;
         break;
@@ -681,7 +730,7 @@ __global__ void __launch_bounds__(1024)
     const int tok = pick;
     tokens[static_cast<size_t>(g) * max_len + t] = tok;
     old_lp[static_cast<size_t>(g) * max_len + t] =
-        static_cast<float>(static_cast<double>(x[tok]) - mx - log(z1));
+        static_cast<float>(static_cast<double>(x[tok]) - m - log(s_z1));
     lengths[g] = t + 1;
     if (tok == eos) done[g] = 1;
   }
@@ -894,11 +943,19 @@ void decode_attention(const void* q, int ldq, int q_col0, const void* kv_prefix,
   MRSP_CUDA(cudaGetLastError());
 }
 
+size_t sample_workspace_bytes(int G) { return static_cast<size_t>(G) * kSampleSlices * 3 * sizeof(double); }
+
 void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed,
                    const int* tdev, int* done, int* tokens, float* old_lp, int* lengths,
-                   int max_len, cudaStream_t s) {
-  launch_pdl(sample_kernel, dim3(G), dim3(1024), 0, s, logits, V, 1.0f / temperature, seed, tdev,
-             done, tokens, old_lp, lengths, max_len, /*Vocab::kEos*/ 1, /*Vocab::kPad*/ 0);
+                   int max_len, void* ws, cudaStream_t s) {
+  MRSP_REQUIRE(V >= kSampleSlices, MRSP_INVALID_ARGUMENT, "sample: vocabulary smaller than the slices");
+  double* part = static_cast<double*>(ws);
+  launch_pdl(sample_slices_kernel, dim3(kSampleSlices, G), dim3(256), 0, s, logits, V,
+             1.0f / temperature, done, part);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  launch_pdl(sample_pick_kernel, dim3(G), dim3(1024), 0, s, logits, V, 1.0f / temperature, seed, tdev,
+             part, done, tokens, old_lp, lengths, max_len, /*Vocab::kEos*/ 1, /*Vocab::kPad*/ 0);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

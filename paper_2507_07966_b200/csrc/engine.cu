@@ -1134,6 +1134,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   const size_t o_tok = carve(n_tok * 4), o_lp = carve(n_tok * 4), o_len = carve(G * 4);
   const size_t o_done = carve(G * 4), o_pos = carve(G * 4), o_t = carve(4);
   const size_t splitk_bytes = gemm_splitk_ws_bytes(G), o_splitk = carve(splitk_bytes);
+  const size_t o_sample = carve(sample_workspace_bytes(G));
   uint8_t* b = static_cast<uint8_t*>(st.ensure(off));
   bf16* kv_rows = reinterpret_cast<bf16*>(b + o_rows);
   float* h = reinterpret_cast<float*>(b + o_h);
@@ -1266,7 +1267,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
     {
       Prof psm(*this, P_MISC);
       sample_tokens(logits, G, c.vocab, temperature, seed, tdev, done, tokens, old_lp, lengths,
-                    max_len, s);
+                    max_len, b + o_sample, s);
       decode_step_advance(tdev, s);
     }
   };

@@ -53,9 +53,10 @@ void decode_embed(const __nv_bfloat16* embed, int d, const int* tokens, int max_
 // rows[t * G + g][0, kvw) = qkv[g][col0, col0 + kvw) (this step's K | V per row)
 void decode_append_kv(const __nv_bfloat16* qkv, int ldq, int col0, __nv_bfloat16* rows, int kvw,
                       int G, const int* tdev, cudaStream_t s);
+size_t sample_workspace_bytes(int G);
 void sample_tokens(const float* logits, int G, int V, float temperature, uint64_t seed,
                    const int* tdev, int* done, int* tokens, float* old_lp, int* lengths,
-                   int max_len, cudaStream_t s);
+                   int max_len, void* ws /* sample_workspace_bytes(G) */, cudaStream_t s);
 void decode_step_advance(int* tdev, cudaStream_t s);
 
 }  // namespace mrsp
