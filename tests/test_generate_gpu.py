@@ -150,3 +150,22 @@ def test_decode_fusions(gpu, monkeypatch):
             assert d.max() <= 5e-2 and d.mean() <= 5e-3, (fuse, d.max(), d.mean())
     finally:
         eng.close()
+
+
+def test_generation_edges(gpu, gen):
+    """One rollout row (G = 1) and the largest group a decode-attention Q tile
+    holds (G x q_per_kv <= 64) sample under the same contract; one row more is
+    an invalid argument (generate's own limit, not the reference's)."""
+    eng, q, c = gen["eng"], gen["q"], gen["c"]
+    qpk = c.n_q_heads // c.n_kv_heads
+    g_max = 64 // qpk
+    for G in (1, g_max):
+        tok, lens, olp = eng.generate("v", q, G, 9, temperature=1.0, seed=3)
+        assert tok.shape == (G, 9) and ((lens >= 1) & (lens <= 9)).all()
+        grp = E.Group(q, _rows(tok, lens), lens.astype(np.int32))
+        want = eng.prefill_logprobs("v", grp, 0)
+        got = np.concatenate([olp[g, :lens[g]] for g in range(G)])
+        d = np.abs(got - want)
+        assert d.max() <= 5e-2 and d.mean() <= 5e-3, (G, d.max(), d.mean())
+    with pytest.raises(_lib.InvalidArgument):
+        eng.generate("v", q, g_max + 1, 4)
