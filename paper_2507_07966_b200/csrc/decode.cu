@@ -254,6 +254,49 @@ struct Args {
 template <int kStreams>
 constexpr int threads() { return 128 + 128 * kStreams; }
 
+constexpr float kDecRescale = 8.0f;  // log2 domain (lazy O rescale)
+
+// Packed fp32x2 FMA / add (FFMA2 / FADD2): half the issue slots of the scalar forms.
+__device__ __forceinline__ void dec_ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                          float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void dec_fadd2(float& d0, float& d1, float a0, float a1) {
+  asm("{\n\t.reg .b64 ra, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rd, {%0, %1};\n\t"
+      "add.rn.f32x2 rd, rd, ra;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1));
+}
+
+// Optional clock() timeline of CTA (0, 0) (tools/ubench/dec_trace.cu builds this
+// file with MRSP_DEC_TRACE): lane 0 of each warp stamps (event, tile, clock).
+#ifdef MRSP_DEC_TRACE
+constexpr int kDecTraceCap = 4096;
+__device__ uint64_t g_dec_trace[12][kDecTraceCap];
+__device__ int g_dec_trace_n[12];
+#define DTRACE(ev, j)                                                                          \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && dtn < kDecTraceCap) \
+      g_dec_trace[threadIdx.x >> 5][dtn++] = (static_cast<uint64_t>(ev) << 56) |              \
+                                             (static_cast<uint64_t>((j) & 0xffffff) << 32) |   \
+                                             static_cast<uint32_t>(clock());                   \
+  } while (0)
+#define DTRACE_INIT int dtn = 0
+#define DTRACE_FINISH \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0) g_dec_trace_n[threadIdx.x >> 5] = dtn
+#else
+#define DTRACE(ev, j) \
+  do {                \
+  } while (0)
+#define DTRACE_INIT
+#define DTRACE_FINISH
+#endif
+
 template <int kRing, int kStreams>
 __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     dec_attn_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmR,
@@ -303,6 +346,8 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_trigger();
+  DTRACE_INIT;
+  DTRACE(0, 0);
   if (warp == 0) {
     if (elect_one()) {  // K_j, V_j alternate through the ring (ring item 2j, 2j + 1)
       int slot = 0;
@@ -310,6 +355,7 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
       for (int j = 0; j < n_tiles; ++j)
         for (int kv = 0; kv < 2; ++kv) {
           mbar_wait(&r_empty[slot], ph ^ 1);
+          DTRACE(1, 2 * j + kv);
           mbar_arrive_expect_tx(&r_full[slot], TILE);
           uint8_t* dst = smem + OFF_RING + slot * TILE;
           // row cache [rows][K heads | V heads]; prompt prefix head-major
@@ -329,7 +375,9 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     // ring item i sits in slot i % RING, completion phase (i / RING) & 1
     auto issue_s = [&](int j) {  // S_{j % kStreams} = Q K_j^T
       const int item = 2 * j, slot = item % RING;
+      DTRACE(2, j);
       mbar_wait(&r_full[slot], (item / RING) & 1);
+      DTRACE(3, j);
       tc_fence_after();
       const uint32_t k_addr = ring + slot * TILE;
       if (elect_one()) {
@@ -346,8 +394,11 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     };
     auto issue_pv = [&](int j) {  // O_{j % kStreams} += P_j V_j
       const int w = j % kStreams, item = 2 * j + 1, slot = item % RING;
+      DTRACE(4, j);
       mbar_wait(&p_full[w], (j / kStreams) & 1);
+      DTRACE(5, j);
       mbar_wait(&r_full[slot], (item / RING) & 1);
+      DTRACE(6, j);
       tc_fence_after();
       const uint32_t v_addr = ring + slot * TILE;
       if (elect_one()) {
@@ -400,40 +451,60 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     // below the chunk end, and (row cache) only this query's own rollout row.
     for (int j = w; j < n_tiles; j += kStreams, ++it) {
       mbar_wait(&s_full[w], it & 1);
+      DTRACE(7, j);
       tc_fence_after();
       const long k0 = k_begin + static_cast<long>(j) * TK;
-      const int nv = r < qn ? static_cast<int>(std::min<long>(TK, k_end - k0)) : 0;
-      const int o = rows_src ? static_cast<int>(((g_of_r - k0 % a.G) % a.G + a.G) % a.G) : 0;
-      uint32_t vis[4];
+      // full prompt tile: every row sees all 128 keys (rows >= qn are padding
+      // whose results are never stored), so no element mask — warp-uniform
+      const bool full = !rows_src && k0 + TK <= k_end;
+      uint32_t vis[4] = {~0u, ~0u, ~0u, ~0u};
+      if (!full) {
+        const int nv = r < qn ? static_cast<int>(std::min<long>(TK, k_end - k0)) : 0;
+        const int o = rows_src ? static_cast<int>(((g_of_r - k0 % a.G) % a.G + a.G) % a.G) : 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int n = nv - 32 * q;
-        uint32_t m = n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : (1u << n) - 1u);
-        if (rows_src) {  // key k0 + 32 q + i is row (k0 + 32 q + i) % G
-          uint32_t rm = 0;
-          for (int i = (o - 32 * q % a.G + a.G) % a.G; i < 32; i += a.G) rm |= 1u << i;
-          m &= rm;
+        for (int q = 0; q < 4; ++q) {
+          const int n = nv - 32 * q;
+          uint32_t m = n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : (1u << n) - 1u);
+          if (rows_src) {  // key k0 + 32 q + i is row (k0 + 32 q + i) % G
+            uint32_t rm = 0;
+            for (int i = (o - 32 * q % a.G + a.G) % a.G; i < 32; i += a.G) rm |= 1u << i;
+            m &= rm;
+          }
+          vis[q] = m;
         }
-        vis[q] = m;
       }
       float mx = -INFINITY;
+      if (full) {  // max of the raw scores (scale > 0), two independent FMNMX3 chains
+        float m2[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-      for (int qq = 0; qq < 4; qq += 2) {  // two TMEM loads in flight per wait
-        uint32_t x[2][32];
-        tmem_ld32(tS + 32 * qq, x[0]);
-        tmem_ld32(tS + 32 * qq + 32, x[1]);
-        tmem_ld_wait();
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x[32];
+          tmem_ld32(tS + 32 * q, x);
+          tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+          for (int i = 0; i < 32; i += 2)
+            m2[(i >> 1) & 1] = fmaxf(m2[(i >> 1) & 1], fmaxf(__uint_as_float(x[i]), __uint_as_float(x[i + 1])));
+        }
+        mx = fmaxf(m2[0], m2[1]) * a.scale_log2;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x[32];
+          tmem_ld32(tS + 32 * q, x);
+          tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            mx = fmaxf(mx, (vis[qq + u] >> i) & 1u ? __uint_as_float(x[u][i]) * a.scale_log2 : -INFINITY);
+            mx = fmaxf(mx, (vis[q] >> i) & 1u ? __uint_as_float(x[i]) * a.scale_log2 : -INFINITY);
+        }
       }
+      // lazy rescale (as the prefill kernel): O and l are rescaled only when a
+      // row's max grows by more than 2^8; P = 2^(s - m_run) <= 2^8 otherwise
       const float m_new = fmaxf(m_run, mx);
-      if (it > 0 && __any_sync(0xffffffffu, m_new > m_run)) {  // rescale O_w (after its last P.V)
+      const bool need = m_new > m_run + kDecRescale;
+      if (it > 0 && __any_sync(0xffffffffu, need)) {  // rescale O_w (after its last P.V)
         mbar_wait(&pv_done[w], (it - 1) & 1);
         tc_fence_after();
-        const float alpha = m_new > m_run && m_run != -INFINITY ? exp2f(m_run - m_new) : 1.f;
+        const float alpha = need && m_run != -INFINITY ? exp2f(m_run - m_new) : 1.f;
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t o[32];
@@ -446,38 +517,61 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
         tmem_st_wait();
         l_run *= alpha;
       }
-      m_run = m_new;
+      if (need) m_run = m_new;
       const float nm = m_run == -INFINITY ? 0.f : -m_run;
+      const float sl = a.scale_log2;
       float acc = 0.f;
+      if (full) {  // packed fp32x2 FMA / add, 8 partial sums
+        float ac[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {  // 64-key halves: P(half h) -> columns [32 h, 32 h + 32),
-        uint32_t wv[32];              // over S columns whose keys are already consumed
-        uint32_t xh[2][32];
-        tmem_ld32(tS + h * 64, xh[0]);
-        tmem_ld32(tS + h * 64 + 32, xh[1]);
-        tmem_ld_wait();
+        for (int h = 0; h < 2; ++h) {
+          uint32_t wv[32];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = h * 64 + cc * 32;
-          const uint32_t* x = xh[cc];
-          const uint32_t vm = vis[c / 32];
+          for (int cc = 0; cc < 2; ++cc) {
+            uint32_t x[32];
+            tmem_ld32(tS + h * 64 + cc * 32, x);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {  // ex2(-inf) = 0 for masked keys
-            const float p0 = ex2_approx((vm >> i) & 1u ? fmaf(__uint_as_float(x[i]), a.scale_log2, nm)
-                                                       : -INFINITY);
-            const float p1 = ex2_approx((vm >> (i + 1)) & 1u
-                                            ? fmaf(__uint_as_float(x[i + 1]), a.scale_log2, nm)
-                                            : -INFINITY);
-            acc += p0 + p1;
-            wv[cc * 16 + i / 2] = pack_bf16(p0, p1);
+            for (int i = 0; i < 32; i += 2) {
+              float y0, y1;
+              dec_ffma2(y0, y1, __uint_as_float(x[i]), __uint_as_float(x[i + 1]), sl, sl, nm, nm);
+              const float p0 = ex2_approx(y0), p1 = ex2_approx(y1);
+              const int q = ((i >> 1) & 3) * 2;
+              dec_fadd2(ac[q], ac[q + 1], p0, p1);
+              wv[cc * 16 + i / 2] = pack_bf16(p0, p1);
+            }
           }
+          tmem_st32(tS + 32 * h, wv);
         }
-        tmem_st32(tS + 32 * h, wv);
+        acc = ((ac[0] + ac[1]) + (ac[2] + ac[3])) + ((ac[4] + ac[5]) + (ac[6] + ac[7]));
+      } else {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {  // 64-key halves: P(half h) -> columns [32 h, 32 h + 32),
+          uint32_t wv[32];              // over S columns whose keys are already consumed
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = h * 64 + cc * 32;
+            uint32_t x[32];
+            tmem_ld32(tS + c, x);
+            tmem_ld_wait();
+            const uint32_t vm = vis[c / 32];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {  // ex2(-inf) = 0 for masked keys
+              const float p0 = ex2_approx((vm >> i) & 1u ? fmaf(__uint_as_float(x[i]), sl, nm) : -INFINITY);
+              const float p1 =
+                  ex2_approx((vm >> (i + 1)) & 1u ? fmaf(__uint_as_float(x[i + 1]), sl, nm) : -INFINITY);
+              acc += p0 + p1;
+              wv[cc * 16 + i / 2] = pack_bf16(p0, p1);
+            }
+          }
+          tmem_st32(tS + 32 * h, wv);
+        }
       }
       tmem_st_wait();
       l_run += acc;
       tc_fence_before();
       mbar_arrive(&p_full[w]);
+      DTRACE(8, j);
     }
     // epilogue: the unnormalised partial of this stream of the chunk
     if (it > 0) {
@@ -500,6 +594,8 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
       out[HD + 1] = l_run;
     }
   }
+  DTRACE(9, 0);
+  DTRACE_FINISH;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
