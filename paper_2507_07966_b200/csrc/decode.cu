@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
   tc_fence_after();
   // S_w at column 128 w (P over its first 64), O_w at 128 kStreams + 128 w
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();
+  // PDL (decode graphs): the prompt K/V (written by the prefill, long before)
+  // streams in before pdl_wait(); Q, the row cache and the partials wait.
   pdl_trigger();
   DTRACE_INIT;
   DTRACE(0, 0);
@@ -352,8 +353,13 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     if (elect_one()) {  // K_j, V_j alternate through the ring (ring item 2j, 2j + 1)
       int slot = 0;
       uint32_t ph = 0;
+      bool waited = false;
       for (int j = 0; j < n_tiles; ++j)
         for (int kv = 0; kv < 2; ++kv) {
+          if (!waited && (rows_src || 2 * j + kv >= RING)) {  // first slot reuse / row cache
+            pdl_wait();
+            waited = true;
+          }
           mbar_wait(&r_empty[slot], ph ^ 1);
           DTRACE(1, 2 * j + kv);
           mbar_arrive_expect_tx(&r_full[slot], TILE);
@@ -422,6 +428,7 @@ __global__ void __launch_bounds__(threads<kStreams>(), kRing == 2 ? 2 : 1)
     const int r = ((warp - 4) & 3) * 32 + lane_id();  // query row = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_off + 128 * w, tO = tmem + lane_off + 128 * kStreams + 128 * w;
+    pdl_wait();  // Q and (epilogue) the partials depend on / are read by earlier kernels
     if (w == 0) {  // Q row r -> smem, SW128 K-major: 16-byte unit u of a 128-byte row at u ^ (r & 7)
       uint4 v[16];
       if (r < qn) {

@@ -463,22 +463,40 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // decode graphs: the predecessor's outputs are visible from here
+  // Programmatic dependent launch (decode graphs): the successor may become
+  // resident now; the weights (B) of the first stages do not depend on the
+  // predecessor kernel, so the producer streams them in before pdl_wait() and
+  // only the activation (A) loads and the epilogue's global accesses wait.
+  // Without PDL both instructions are no-ops.
   pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      int pre = 0;  // first-tile k blocks whose B load was issued before the wait
+      if (static_cast<int>(blockIdx.x) < num_tiles) {
+        int mt, nt, kb0, kb1;
+        decode_tile(blockIdx.x, mt, nt, kb0, kb1);
+        for (; pre < STAGES && kb0 + pre < kb1; ++pre) {
+          mbar_arrive_expect_tx(&full[pre], STAGE_BYTES);  // stages start empty
+          tma_load_2d(smem + pre * STAGE_BYTES + A_STAGE, &tmB, &full[pre], (kb0 + pre) * BK, nt * BN);
+        }
+      }
+      pdl_wait();
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int mt, nt, kb0, kb1;
         decode_tile(tile, mt, nt, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(sa + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+          if (pre > 0 && tile == static_cast<int>(blockIdx.x) && kb - kb0 < pre) {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);  // B already in flight
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);
+            tma_load_2d(sa + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -515,6 +533,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // the epilogue reads the residual and writes outputs
     const int ew = warp - 4;  // TMEM lanes [32 ew, 32 ew + 32)
     uint8_t* boxes = out_boxes + ew * 2 * OUT_BOX;
     uint32_t buf = 0;
