@@ -9,9 +9,12 @@
 // split into chunks of DEC_CHUNK keys, one CTA per (chunk, kv head): each K/V
 // tile read from HBM serves all of the kv group's queries (GQA reuse), and the
 // CTA emits an unnormalised partial (m, l, O) merged by dec_merge_kernel —
-// flash-decoding. Work per key is q·k and p·v for <= 64 queries (a few
-// thousand FMAs per 256 B of K and V): CUDA-core FP32 is enough to keep the
-// kernel near the HBM rate of the prefix KV stream.
+// flash-decoding. Two implementations: the tcgen05 kernel (default; S, P, O in
+// TMEM, TMA K/V ring, two KV streams per CTA for long prompts, an unmasked
+// packed-FP32 softmax for full prompt tiles) and a register-blocked CUDA-core
+// kernel (MRSP_DECODE_CC=1). Every kernel reads the step index from device
+// memory, so a whole decode step is captured once as a CUDA graph
+// (Engine::generate) and replayed for every t.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
