@@ -9,8 +9,10 @@ Qwen2.5-7B-shaped LLM, G = 8) split over N GPUs as SP = N (strong scaling).
 
   python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload c4]
 
-Prints ONE JSON line on rank 0. Multi-GPU: launched by torch.distributed.run,
-one process per GPU; the engine's collectives run over NCCL.
+Prints ONE JSON line on rank 0. Multi-GPU: one process per GPU under
+torch.distributed.run (`--gpus N` without WORLD_SIZE re-executes itself that
+way); the engine's exchanges go over CUDA-IPC peer memory (MRSP_COMM=nccl:
+NCCL), the torch process group is host plumbing only.
 """
 from __future__ import annotations
 
@@ -167,6 +169,7 @@ def cpu_port_timing(w, group, budget_s: float = 20.0):
         pass
     return {
         "value": fl["tokens"] / step_s, "unit": "tokens/s", "cores": cores, "kind": "port",
+        **cpu_host(),
         "sample": ("oracle/transformer.py (fp64 numpy over bf16 tensors): 1 SigLIP-shaped frame "
                    "(27 layers + projector), 1 Qwen2.5-7B-shaped decoder layer (linear) on 512 "
                    "tokens, attention 28 heads x 256 q x 4096 k, LM head 32 tokens; extrapolated "
@@ -205,6 +208,31 @@ def reference_toy_engine():
         return {"error": str(e)}
 
 
+def self_launch(n: int) -> int:
+    """Re-executes this command as N ranks (torch.distributed.run, 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    return subprocess.call(cmd + sys.argv[1:])
+
+
+def cpu_host():
+    """Host CPU model (lscpu 'Model name') and logical core count."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.strip().startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 # -------------------------------------------------------------- the bench
 def main():
     ap = argparse.ArgumentParser()
@@ -219,9 +247,15 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # `bench.py --gpus N` without a launcher: one process per GPU under
+        # torch.distributed.run (rank 0 prints the line)
+        sys.exit(self_launch(args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "b200" and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     from paper_2507_07966_b200 import engine as E
     from oracle import transformer as T  # FLOP accounting (the algorithmic numerator)
@@ -340,7 +374,16 @@ def main():
         barrier()
     prof = eng.profile(False)
     launches = int(_lib.lib().mrsp_launch_count()) - launches0
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    rank_ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(rank_ms)
+    # per-rank device time by kernel class (imbalance across SP ranks)
+    mine = {"rank": rank, "ms_per_step": round(rank_ms, 3),
+            **{k: round(v[0] / args.steps, 2) for k, v in prof.items()}}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+        launches = int(max_over_ranks(float(launches)))
     stats = eng.stats(reset=True)
     value = fl["tokens"] / (ms / 1e3)
 
@@ -392,14 +435,15 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {**workload_config(w, group, fl, world),
-                   "comm": (("nccl" if nccl_id else "p2p: CUDA-IPC peer memory, fused QKV/attention "
-                             "scatters") if world > 1 else "none (SP=1)")},
+        "config": workload_config(w, group, fl, world),
+        "comm": (("nccl" if nccl_id else "p2p: CUDA-IPC peer memory, fused QKV/attention "
+                  "scatters") if world > 1 else "none (SP=1)"),
         "roofline": roofline,
         "step_roofline": {"flops_per_step": fl["step"], "achieved_tflops": step_tflops,
                           "frac_of_sustained": step_tflops / world / peak},
         "kernel_ms": {k: round(v[0] / args.steps, 2) for k, v in prof.items()},
         "kernel_launches": {k: v[1] for k, v in prof.items()},
+        "kernel_ms_per_rank": per_rank if world > 1 else None,
         "e2e": e2e, "gpu_launches": launches, "counters_per_step":
             {k: v // args.steps for k, v in stats.items()},
     }

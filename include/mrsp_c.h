@@ -393,8 +393,11 @@ mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, const float* 
 mrsp_status mrsp_engine_stats(mrsp_engine* e, uint64_t* out6, int reset);
 mrsp_status mrsp_engine_cache(mrsp_engine* e, int op /*0 size,1 clear,2 set capacity*/, int arg,
                               uint64_t* size_out);
-/* Copies the cached [F*T][dim] bf16 embeddings of video_id to host. */
-mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* video_id, void* host_out);
+/* Copies the cached [F*T][dim] bf16 embeddings of video_id to host_out, which
+ * holds capacity_bytes (MRSP_INVALID_ARGUMENT when too small; nothing is
+ * written). frames_out (may be NULL) receives F; host_out == NULL only queries F. */
+mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* video_id, void* host_out,
+                                       size_t capacity_bytes, int* frames_out);
 /* Per-kernel-class CUDA-event timing: cls 0 LLM attention, 1 LLM GEMMs,
  * 2 vision tower, 3 LM head, 4 collectives, 5 norms/rope/pack. */
 mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, double* ms, int64_t* launches);

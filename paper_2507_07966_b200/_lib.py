@@ -108,7 +108,7 @@ _sig("mrsp_op_grpo_stats", [_V, _V, _V, _V, _V, _V, _I, ctypes.c_double, ctypes.
 _sig("mrsp_op_lmhead_dual", [_V, _V, _V, _V, _I, _I, _I, _V, _V, _V, _V, _V, ctypes.c_size_t, _V])
 _sig("mrsp_engine_stats", [_V, _V, _I])
 _sig("mrsp_engine_cache", [_V, _I, _I, _V])
-_sig("mrsp_engine_get_embeddings", [_V, ctypes.c_char_p, _V])
+_sig("mrsp_engine_get_embeddings", [_V, ctypes.c_char_p, _V, ctypes.c_size_t, _V])
 _sig("mrsp_engine_profile", [_V, _I, _I, _V, _V])
 _sig("mrsp_engine_stream", [_V], ctypes.c_void_p)
 _sig("mrsp_p2p_blob_bytes", [], ctypes.c_size_t)

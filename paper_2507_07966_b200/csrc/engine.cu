@@ -1446,10 +1446,12 @@ std::shared_ptr<CacheEntry> Engine::cache_load(const std::string& id, const std:
   return entry;
 }
 
+size_t Engine::embedding_bytes(const CacheEntry& e) const {
+  return static_cast<size_t>(e.n_frames) * tokens_per_frame() * cfg_.dim * 2;
+}
+
 void Engine::copy_embeddings(const CacheEntry& e, void* host_out) {
-  MRSP_CUDA(cudaMemcpy(host_out, e.emb->p,
-                       static_cast<size_t>(e.n_frames) * tokens_per_frame() * cfg_.dim * 2,
-                       cudaMemcpyDeviceToHost));
+  MRSP_CUDA(cudaMemcpy(host_out, e.emb->p, embedding_bytes(e), cudaMemcpyDeviceToHost));
 }
 
 }  // namespace mrsp
@@ -1538,8 +1540,9 @@ extern "C" mrsp_status mrsp_engine_prefill_logprobs(mrsp_engine* e, const char* 
                                                     int G, int Lmax, int model, float* logprob,
                                                     float* lse, int out_on_device) {
   return guard([&] {
-    MRSP_REQUIRE(e && video_id && resp && lengths && logprob, MRSP_INVALID_ARGUMENT,
-                 "prefill: null argument");
+    MRSP_REQUIRE(e && video_id && resp && lengths && logprob && (question || n_q == 0),
+                 MRSP_INVALID_ARGUMENT, "prefill: null argument");
+    MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "pad_batch: empty batch");
     auto entry = lookup(e, video_id);
     e->impl->prefill_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, model, logprob, lse,
                               out_on_device != 0);
@@ -1553,7 +1556,9 @@ extern "C" mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, co
                                         float* logprob_policy, float* logprob_ref, float* kl,
                                         int out_on_device) {
   return guard([&] {
-    MRSP_REQUIRE(e && video_id && pixels, MRSP_INVALID_ARGUMENT, "step: null argument");
+    MRSP_REQUIRE(e && video_id && pixels && resp && lengths && (question || n_q == 0),
+                 MRSP_INVALID_ARGUMENT, "step: null argument");
+    MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "pad_batch: empty batch");  // engine.cpp:32
     std::shared_ptr<CacheEntry> entry;
     for (int g = 0; g < G; ++g) {  // one embedding fetch per rollout (grpo.cpp:376-379)
       bool h = false;
@@ -1653,9 +1658,17 @@ extern "C" mrsp_status mrsp_engine_cache_load(mrsp_engine* e, const char* video_
 }
 
 extern "C" mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* video_id,
-                                                  void* host_out) {
+                                                  void* host_out, size_t capacity_bytes,
+                                                  int* frames_out) {
   return guard([&] {
+    MRSP_REQUIRE(e && video_id, MRSP_INVALID_ARGUMENT, "get_embeddings: null argument");
     auto entry = lookup(e, video_id);
+    const size_t need = e->impl->embedding_bytes(*entry);
+    if (frames_out) *frames_out = entry->n_frames;
+    if (!host_out) return;  // size query
+    MRSP_REQUIRE(capacity_bytes >= need, MRSP_INVALID_ARGUMENT,
+                 "get_embeddings: host buffer holds " + std::to_string(capacity_bytes) +
+                     " bytes, the entry needs " + std::to_string(need));
     e->impl->copy_embeddings(*entry, host_out);
   });
 }

@@ -151,6 +151,7 @@ class Engine {
   // profiling: CUDA-event time per kernel class
   void set_profiling(bool on);
   void profile_read(int cls, double* ms, long* launches);
+  size_t embedding_bytes(const CacheEntry& e) const;
   void copy_embeddings(const CacheEntry& e, void* host_out);
 
  private:

@@ -82,7 +82,10 @@ __global__ void toy_prefill_kernel(const double* __restrict__ theta, const doubl
 }
 
 // Per-process pool of rank streams (ranks = streams on the current device).
-std::vector<cudaStream_t>& rank_streams(int k) {
+// Returns a copy of the first k handles taken under the lock: the pool only
+// grows, and a concurrent caller growing it must not move a vector another
+// thread is still indexing.
+std::vector<cudaStream_t> rank_streams(int k) {
   static std::mutex mu;
   static std::vector<cudaStream_t> pool;
   std::lock_guard<std::mutex> lock(mu);
@@ -91,7 +94,7 @@ std::vector<cudaStream_t>& rank_streams(int k) {
     MRSP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     pool.push_back(s);
   }
-  return pool;
+  return std::vector<cudaStream_t>(pool.begin(), pool.begin() + k);
 }
 
 template <typename T>
@@ -467,7 +470,7 @@ void toy_backward(int sp_degree, const double* theta, const double* ref, int V, 
       tok_w[i] = 1.0 / (static_cast<double>(n_rows) * static_cast<double>(lengths[i]));
   const uint64_t n_theta = static_cast<uint64_t>(V) * d + 2ull * h * d + h +
                            static_cast<uint64_t>(V) * h + V;
-  auto& streams = rank_streams(sp_degree);
+  const auto streams = rank_streams(sp_degree);
   cudaStream_t s0 = streams[0];
   DevBuf<double> dth(n_theta), dref(cfg.sft ? 0 : n_theta), dfr(n_frames * d), dctx(2 * d),
       dold(cfg.sft ? 0 : P), dadv(cfg.sft ? 0 : n_rows), dtw(tok_w.size()), dg(P * V), ds(P * h),
@@ -553,7 +556,7 @@ extern "C" mrsp_status mrsp_toy_encode(int sp_degree, const double* enc_w, int d
       for (int w = 0; w < sp_degree; ++w) rank_items[w] = 0;
       return;
     }
-    auto& streams = rank_streams(sp_degree);
+    const auto streams = rank_streams(sp_degree);
     DevBuf<double> dw(static_cast<size_t>(d) * p), dx(n_frames * p), dout(n_frames * d);
     MRSP_CUDA(cudaMemcpyAsync(dw.p, enc_w, sizeof(double) * d * p, cudaMemcpyHostToDevice, streams[0]));
     MRSP_CUDA(cudaMemcpyAsync(dx.p, frames, sizeof(double) * n_frames * p, cudaMemcpyHostToDevice,
@@ -620,7 +623,7 @@ extern "C" mrsp_status mrsp_toy_prefill(int sp_degree, const double* theta, int 
     }
     const uint64_t n_theta = static_cast<uint64_t>(V) * d + 2ull * h * d + h +
                              static_cast<uint64_t>(V) * h + V;
-    auto& streams = rank_streams(sp_degree);
+    const auto streams = rank_streams(sp_degree);
     DevBuf<double> dtheta(n_theta), dctx(n_rows * d), dout(total * V);
     DevBuf<Pos> dpos(total);
     MRSP_CUDA(cudaMemcpyAsync(dtheta.p, theta, sizeof(double) * n_theta, cudaMemcpyHostToDevice,

@@ -146,6 +146,42 @@ def _ptr(a, t=ctypes.c_int32):
     return a.ctypes.data_as(ctypes.POINTER(t))
 
 
+def _i32(a) -> np.ndarray:
+    """Host int32 buffer the C side reads (a caller's int64 array would
+    otherwise be reinterpreted)."""
+    return np.ascontiguousarray(np.asarray(a), dtype=np.int32)
+
+
+def _group_arrays(group: "Group"):
+    q, resp, lens = _i32(group.question).reshape(-1), _i32(group.resp), _i32(group.lengths)
+    if resp.ndim != 2 or lens.shape != (resp.shape[0],):
+        raise ValueError(f"group: resp must be [G, Lmax] and lengths [G], got {resp.shape} / "
+                         f"{lens.shape}")
+    return q, resp, lens
+
+
+def _pixels(pixels, cfg: "ModelConfig"):
+    """(pointer, F, on_device) for a [F, 3*S*S] fp32 host array or CUDA tensor."""
+    want = 3 * cfg.image_size ** 2
+    if hasattr(pixels, "is_cuda"):
+        import torch
+        if not pixels.is_cuda or pixels.dtype != torch.float32 or not pixels.is_contiguous() \
+                or pixels.dim() != 2 or pixels.shape[1] != want:
+            raise ValueError(f"pixels: need a contiguous float32 CUDA tensor [F, {want}]")
+        return _ptr(pixels, ctypes.c_float), int(pixels.shape[0]), 1, pixels
+    arr = np.ascontiguousarray(pixels, dtype=np.float32)
+    if arr.ndim != 2 or arr.shape[1] != want:
+        raise ValueError(f"pixels: need [F, {want}] float32, got {arr.shape}")
+    return _ptr(arr, ctypes.c_float), int(arr.shape[0]), 0, arr
+
+
+def _out_tensor(t, n: int, name: str):
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() >= n):
+        raise ValueError(f"{name}: need a contiguous float32 CUDA tensor with >= {n} elements")
+    return t
+
+
 class Engine:
     """One process's share of an SP group (sp virtual ranks when n_procs == 1)."""
 
@@ -228,22 +264,20 @@ class Engine:
 
     def encode(self, vid: str, pixels, use_cache: bool = True) -> bool:
         """Stage 1; pixels [F, 3*S*S] fp32 numpy (host) or torch CUDA tensor."""
-        on_dev = hasattr(pixels, "is_cuda") and pixels.is_cuda
-        F = int(pixels.shape[0])
+        pp, F, on_dev, _keep = _pixels(pixels, self.cfg)
         hit = ctypes.c_int(0)
-        check(_lib.lib().mrsp_engine_encode(self._h, vid.encode(), _ptr(pixels, ctypes.c_float), F,
-                                            int(on_dev), int(use_cache), ctypes.byref(hit)))
+        check(_lib.lib().mrsp_engine_encode(self._h, vid.encode(), pp, F, on_dev, int(use_cache),
+                                            ctypes.byref(hit)))
         return bool(hit.value)
 
     def prefill_logprobs(self, vid: str, group: Group, model: int = 0, with_lse: bool = False):
-        n = group.scored
+        q, resp, lens = _group_arrays(group)
+        n = int(lens.sum())
         lp = np.zeros(n, dtype=np.float32)
         lse = np.zeros(n, dtype=np.float32) if with_lse else None
         check(_lib.lib().mrsp_engine_prefill_logprobs(
-            self._h, vid.encode(), _ptr(np.ascontiguousarray(group.question)), len(group.question),
-            _ptr(np.ascontiguousarray(group.resp)), _ptr(np.ascontiguousarray(group.lengths)),
-            int(group.resp.shape[0]), group.Lmax, model, _ptr(lp, ctypes.c_float),
-            _ptr(lse, ctypes.c_float), 0))
+            self._h, vid.encode(), _ptr(q), len(q), _ptr(resp), _ptr(lens), int(resp.shape[0]),
+            int(resp.shape[1]), model, _ptr(lp, ctypes.c_float), _ptr(lse, ctypes.c_float), 0))
         return (lp, lse) if with_lse else lp
 
     def step(self, vid: str, pixels, group: Group, use_cache: bool = True, out=None,
@@ -251,22 +285,22 @@ class Engine:
         """run_step: G fetches + policy and reference log-probs (+ exact per-token
         KL from the fused dual LM head). `out` = optional tuple of device tensors
         (lp_policy, lp_ref[, kl]) to receive the results without a D2H copy."""
-        on_dev = hasattr(pixels, "is_cuda") and pixels.is_cuda
-        n = group.scored
+        pp, F, on_dev, _keep = _pixels(pixels, self.cfg)
+        q, resp, lens = _group_arrays(group)
+        n = int(lens.sum())
         if out is None:
             lp_p = np.zeros(n, dtype=np.float32)
             lp_r = np.zeros(n, dtype=np.float32)
             kl = np.zeros(n, dtype=np.float32) if with_kl else None
             out_dev = 0
         else:
-            lp_p, lp_r = out[0], out[1]
-            kl = out[2] if len(out) > 2 else None
+            lp_p = _out_tensor(out[0], n, "out[0]")
+            lp_r = _out_tensor(out[1], n, "out[1]")
+            kl = _out_tensor(out[2], n, "out[2]") if len(out) > 2 else None
             out_dev = 1
         check(_lib.lib().mrsp_engine_step(
-            self._h, vid.encode(), _ptr(pixels, ctypes.c_float), int(pixels.shape[0]), int(on_dev),
-            int(use_cache), _ptr(np.ascontiguousarray(group.question)), len(group.question),
-            _ptr(np.ascontiguousarray(group.resp)), _ptr(np.ascontiguousarray(group.lengths)),
-            int(group.resp.shape[0]), group.Lmax, _ptr(lp_p, ctypes.c_float),
+            self._h, vid.encode(), pp, F, on_dev, int(use_cache), _ptr(q), len(q), _ptr(resp),
+            _ptr(lens), int(resp.shape[0]), int(resp.shape[1]), _ptr(lp_p, ctypes.c_float),
             _ptr(lp_r, ctypes.c_float), _ptr(kl, ctypes.c_float), out_dev))
         return (lp_p, lp_r, kl) if with_kl or (out is not None and len(out) > 2) else (lp_p, lp_r)
 
@@ -287,12 +321,23 @@ class Engine:
     def cache_capacity(self, n: int):
         check(_lib.lib().mrsp_engine_cache(self._h, 2, n, None))
 
-    def embeddings(self, vid: str, frames: int) -> np.ndarray:
-        """Cached [F*T, dim] embeddings as float32 (from bf16)."""
+    def embedding_frames(self, vid: str) -> int:
+        f = ctypes.c_int(0)
+        check(_lib.lib().mrsp_engine_get_embeddings(self._h, vid.encode(), None, 0,
+                                                    ctypes.byref(f)))
+        return f.value
+
+    def embeddings(self, vid: str, frames: Optional[int] = None) -> np.ndarray:
+        """Cached [F*T, dim] embeddings as float32 (from bf16). The buffer is
+        sized from the entry (frames, when given, must match it)."""
         T = self.cfg.tokens_per_frame
-        raw = np.empty((frames * T, self.cfg.dim), dtype=np.uint16)
+        F = self.embedding_frames(vid)
+        if frames is not None and frames != F:
+            raise ValueError(f"embeddings: {vid} holds {F} frames, not {frames}")
+        raw = np.empty((F * T, self.cfg.dim), dtype=np.uint16)
         check(_lib.lib().mrsp_engine_get_embeddings(self._h, vid.encode(),
-                                                    raw.ctypes.data_as(ctypes.c_void_p)))
+                                                    raw.ctypes.data_as(ctypes.c_void_p),
+                                                    raw.nbytes, None))
         return (raw.astype(np.uint32) << 16).view(np.float32)
 
     PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc",

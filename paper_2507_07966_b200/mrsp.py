@@ -234,6 +234,7 @@ class EmbeddingCache:
             self.cv = threading.Condition()
             self.ready = False
             self.value = None
+            self.error = None  # set when the fill raised
 
     def __init__(self):
         self._mu = threading.Lock()
@@ -250,7 +251,19 @@ class EmbeddingCache:
             else:
                 group.stats().add("cache_hits", 1)
         if filler:
-            value = all_gather(group.parallel_encode(frames, plan), group.degree(), group.stats())
+            try:
+                value = all_gather(group.parallel_encode(frames, plan), group.degree(),
+                                   group.stats())
+            except BaseException as exc:
+                # publish the failure: drop the key (a later call retries) and
+                # wake the waiters, which re-raise instead of blocking forever
+                with self._mu:
+                    if self._map.get(video_id) is entry:
+                        del self._map[video_id]
+                with entry.cv:
+                    entry.error, entry.ready = exc, True
+                    entry.cv.notify_all()
+                raise
             value.setflags(write=False)
             with entry.cv:
                 entry.value, entry.ready = value, True
@@ -258,6 +271,9 @@ class EmbeddingCache:
             return value, False
         with entry.cv:
             entry.cv.wait_for(lambda: entry.ready)
+            if entry.error is not None:
+                raise RuntimeError(f"EmbeddingCache: encoding {video_id} failed in another "
+                                   f"caller") from entry.error
             return entry.value, True
 
     def size(self) -> int:

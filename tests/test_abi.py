@@ -69,3 +69,34 @@ def test_compute_fails_loudly_without_gpu():
     enc = mrsp.EncoderParams(4, 8, np.ones((4, 8)))
     with pytest.raises(_lib.MrspError, match="no CPU fallback"):
         mrsp.serial_encode(enc, np.ones((2, 8)))
+
+
+def test_gen_video_matches_reference_golden():
+    """mrsp_gen_video (the engine's frame source) is float32 of the reference's
+    fp64 gen_video(7, 2, 4) (mmseq.cpp:58-72), element for element."""
+    import json
+    from paper_2507_07966_b200 import engine as E
+    gold = json.loads((ROOT / "tests" / "golden" / "ref_toy.json").read_text())["gen_video_7_2_4"]
+    got = E.gen_video(7, 2, 4)
+    assert got.dtype == np.float32
+    assert np.array_equal(got, np.asarray(gold["frames"], dtype=np.float64).astype(np.float32))
+    assert E.video_id(7, 2) == gold["id"]
+
+
+def test_engine_front_end_validates_host_buffers():
+    """The Python front-end coerces token arrays to int32 (a default-int64
+    array must not be reinterpreted) and rejects mis-shaped pixels before any
+    pointer reaches the C side."""
+    from paper_2507_07966_b200 import engine as E
+    w = E.workloads()["c1"]
+    g = E.Group(np.array([10, 11], dtype=np.int64), np.array([[12, 13, 0], [14, 15, 16]]),
+                np.array([2, 3]))
+    q, resp, lens = E._group_arrays(g)
+    assert q.dtype == resp.dtype == lens.dtype == np.int32
+    assert lens.tolist() == [2, 3] and resp[1].tolist() == [14, 15, 16]
+    with pytest.raises(ValueError):
+        E._group_arrays(E.Group(q, resp, np.array([2, 3, 4])))
+    with pytest.raises(ValueError):
+        E._pixels(np.zeros((2, 10), np.float32), w.cfg)
+    ptr, F, on_dev, keep = E._pixels(np.zeros((3, 3 * 64 * 64), np.float64), w.cfg)
+    assert F == 3 and on_dev == 0 and keep.dtype == np.float32
