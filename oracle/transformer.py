@@ -3,7 +3,15 @@
 Imported only by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 --impl reference legs; never by the product package.
 
-Parity status: PINNED to the reference's CONVENTIONS, UNPINNED in arithmetic.
+Parity status: PINNED. Conventions to the reference (below); arithmetic to
+the published implementations of both model families — with storage rounding
+off (`exact()`), vision_forward matches HF transformers' SiglipVisionModel
+(+ an mlp2x_gelu projector) to 2e-15 and llm_logprobs matches
+Qwen2ForCausalLM to 4e-15 in float64 (2e-7 against stock HF, whose RMSNorm
+statistic and RoPE cos/sin are float32), at c1 and at production widths
+(tests/test_oracle_hf_pin.py). The RoPE inverse frequencies follow HF's
+float32 formula (rope_inv_freq).
+
 The reference (lvrl, /root/reference/proj) has no transformer: its "vision
 tower" is tanh(Wx) (policy.cpp:36-47) and its "LLM" a pooled-context MLP
 (policy.cpp:85-119). This restatement keeps every contract the reference fixes
@@ -182,17 +190,47 @@ def _f64(x):
     return np.asarray(x, dtype=np.float64)
 
 
+# Storage rounding. The device stores bf16 activations and an fp32 residual
+# stream; the oracle rounds at exactly those tensor boundaries. Inside
+# `exact()` both are the identity: the same algorithm in plain float64, which
+# is what tests/test_oracle_hf_pin.py compares with the published
+# implementations (HF transformers SigLIP / Qwen2) to pin the conventions.
+_EXACT = [False]
+
+
+def _b(x):
+    """bf16 storage (fp32 then round-to-nearest-even bf16)."""
+    return _f64(x) if _EXACT[0] else bf16_round(np.asarray(x).astype(np.float32))
+
+
+def _s(x):
+    """fp32 storage."""
+    return _f64(x) if _EXACT[0] else np.asarray(x).astype(np.float32)
+
+
+class exact:
+    """Context manager: the oracle's algorithm without storage rounding."""
+
+    def __enter__(self):
+        self._old = _EXACT[0]
+        _EXACT[0] = True
+        return self
+
+    def __exit__(self, *a):
+        _EXACT[0] = self._old
+
+
 def layernorm(x, w, b, eps):
     x = _f64(x)
     mu = x.mean(-1, keepdims=True)
     var = ((x - mu) ** 2).mean(-1, keepdims=True)
-    return bf16_round(((x - mu) / np.sqrt(var + eps) * w + b).astype(np.float32))
+    return _b((x - mu) / np.sqrt(var + eps) * w + b)
 
 
 def rmsnorm(x, w, eps):
     x = _f64(x)
     r = 1.0 / np.sqrt((x * x).mean(-1, keepdims=True) + eps)
-    return bf16_round((w * (x * r)).astype(np.float32))
+    return _b(w * (x * r))
 
 
 def gelu_tanh(x):
@@ -213,7 +251,7 @@ def patchify(pixels: np.ndarray, S: int, P: int) -> np.ndarray:
     F = pixels.shape[0]
     g = S // P
     x = pixels.reshape(F, 3, g, P, g, P).transpose(0, 2, 4, 1, 3, 5)
-    return bf16_round(x.reshape(F * g * g, 3 * P * P).astype(np.float32))
+    return _b(x.reshape(F * g * g, 3 * P * P))
 
 
 def attention(q, k, v, mask, scale):
@@ -245,26 +283,25 @@ def vision_forward(c: Cfg, W, pixels: np.ndarray) -> np.ndarray:
     F = pixels.shape[0]
     T, vd, hd = c.T, c.v_dim, c.v_head_dim
     x = patchify(pixels, c.image_size, c.patch)
-    h = np.tile(_f64(W["pos"]), (F, 1)) + linear(x, W["patch_w"], W["patch_b"])
-    h = h.astype(np.float32)
+    h = _s(np.tile(_f64(W["pos"]), (F, 1)) + linear(x, W["patch_w"], W["patch_b"]))
     blk = np.kron(np.eye(F, dtype=bool), np.ones((T, T), dtype=bool))
     for l in range(c.v_layers):
         p = f"vision.{l}."
         xn = layernorm(h, W[p + "ln1_w"], W[p + "ln1_b"], c.ln_eps)
-        qkv = bf16_round(linear(xn, W[p + "wqkv"], W[p + "bqkv"]).astype(np.float32))
+        qkv = _b(linear(xn, W[p + "wqkv"], W[p + "bqkv"]))
         n = qkv.shape[0]
         q = _f64(qkv[:, :vd]).reshape(n, c.v_heads, hd).transpose(1, 0, 2)
         k = _f64(qkv[:, vd:2 * vd]).reshape(n, c.v_heads, hd).transpose(1, 0, 2)
         v = _f64(qkv[:, 2 * vd:]).reshape(n, c.v_heads, hd).transpose(1, 0, 2)
         o = attention(q, k, v, blk, 1.0 / math.sqrt(hd)).transpose(1, 0, 2).reshape(n, vd)
-        o = bf16_round(o.astype(np.float32))
-        h = (h + linear(o, W[p + "wo"], W[p + "bo"])).astype(np.float32)
+        o = _b(o)
+        h = _s(h + linear(o, W[p + "wo"], W[p + "bo"]))
         xn = layernorm(h, W[p + "ln2_w"], W[p + "ln2_b"], c.ln_eps)
-        mid = bf16_round(gelu_tanh(linear(xn, W[p + "w1"], W[p + "b1"])).astype(np.float32))
-        h = (h + linear(mid, W[p + "w2"], W[p + "b2"])).astype(np.float32)
+        mid = _b(gelu_tanh(linear(xn, W[p + "w1"], W[p + "b1"])))
+        h = _s(h + linear(mid, W[p + "w2"], W[p + "b2"]))
     xn = layernorm(h, W["post_w"], W["post_b"], c.ln_eps)
-    p1 = bf16_round(gelu_tanh(linear(xn, W["p1_w"], W["p1_b"])).astype(np.float32))
-    return bf16_round(linear(p1, W["p2_w"], W["p2_b"]).astype(np.float32))
+    p1 = _b(gelu_tanh(linear(xn, W["p1_w"], W["p1_b"])))
+    return _b(linear(p1, W["p2_w"], W["p2_b"]))
 
 
 # -------------------------------------------------------------------- stage 2
@@ -292,17 +329,30 @@ def pack(n_frame_tok: int, question, resp, lengths):
     return tok, pos, pad, Lp, L
 
 
+def rope_inv_freq(theta: float) -> np.ndarray:
+    """inv_freq[i] = 1 / theta^(2i/128) in float32, as HF transformers builds it
+    (`1.0 / (base ** (torch.arange(0, dim, 2).float() / dim))`, Qwen2
+    RotaryEmbedding): the exponent and the power are float32, the power
+    correctly rounded (torch's CPU powf can differ by 1 ulp in one entry of 64
+    for theta = 1e6; tests/test_oracle_hf_pin.py bounds that)."""
+    e = np.arange(0, 128, 2).astype(np.float32) / np.float32(128.0)
+    a = np.power(np.float64(np.float32(theta)), e.astype(np.float64)).astype(np.float32)
+    return (np.float32(1.0) / a).astype(np.float32)
+
+
 def rope_tables(c: Cfg, pos: np.ndarray):
-    inv = (1.0 / np.power(np.float64(c.rope_theta), np.arange(64) * 2.0 / 128.0)).astype(np.float32)
+    """cos/sin of the fp32 angle pos * inv_freq (fp32 product, as HF and the
+    device compute it), each rounded to fp32."""
+    inv = rope_inv_freq(c.rope_theta)
     ang = pos.astype(np.float32)[:, None] * inv[None, :]  # fp32 product (as the device)
     return np.cos(_f64(ang)).astype(np.float32), np.sin(_f64(ang)).astype(np.float32)
 
 
 def apply_rope(x: np.ndarray, cos, sin) -> np.ndarray:
-    """x [L, H, 128] bf16-valued fp32 -> bf16 (rotate-half)."""
-    x1, x2 = x[..., :64], x[..., 64:]
-    c, s = cos[:, None, :], sin[:, None, :]
-    return bf16_round(np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], -1).astype(np.float32))
+    """x [L, H, 128] bf16-valued -> bf16 (rotate-half)."""
+    x1, x2 = _f64(x[..., :64]), _f64(x[..., 64:])
+    c, s = _f64(cos[:, None, :]), _f64(sin[:, None, :])
+    return _b(np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], -1))
 
 
 def llm_logprobs(c: Cfg, W, frame_emb, question, resp, lengths, return_hidden=False):
@@ -311,26 +361,26 @@ def llm_logprobs(c: Cfg, W, frame_emb, question, resp, lengths, return_hidden=Fa
     tok, pos, pad, Lp, L = pack(n_frame_tok, question, resp, lengths)
     G, Lmax = resp.shape
     d, hd, nq, nkv = c.dim, c.head_dim, c.n_q_heads, c.n_kv_heads
-    h = np.empty((L, d), dtype=np.float32)
+    h = np.empty((L, d), dtype=np.float64 if _EXACT[0] else np.float32)
     h[:n_frame_tok] = frame_emb
     h[n_frame_tok:] = W["embed"][tok[n_frame_tok:]]
     cos, sin = rope_tables(c, pos)
     mask = mrsp_mask(L, Lp, Lmax)
     for l in range(c.layers):
         xn = rmsnorm(h, W[f"{l}.attn_norm"], c.rms_eps)
-        qkv = bf16_round(linear(xn, W[f"{l}.wqkv"], W[f"{l}.bqkv"]).astype(np.float32))
+        qkv = _b(linear(xn, W[f"{l}.wqkv"], W[f"{l}.bqkv"]))
         q = apply_rope(qkv[:, : nq * hd].reshape(L, nq, hd), cos, sin)
         k = apply_rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(L, nkv, hd), cos, sin)
         v = qkv[:, (nq + nkv) * hd:].reshape(L, nkv, hd)
         o = attention(_f64(q).transpose(1, 0, 2), _f64(k).transpose(1, 0, 2),
                       _f64(v).transpose(1, 0, 2), mask, 1.0 / math.sqrt(hd))
-        o = bf16_round(o.transpose(1, 0, 2).reshape(L, nq * hd).astype(np.float32))
-        h = (h + linear(o, W[f"{l}.wo"])).astype(np.float32)
+        o = _b(o.transpose(1, 0, 2).reshape(L, nq * hd))
+        h = _s(h + linear(o, W[f"{l}.wo"]))
         xn = rmsnorm(h, W[f"{l}.mlp_norm"], c.rms_eps)
-        g_ = linear(xn, W[f"{l}.w_gate"]).astype(np.float32)
-        u_ = linear(xn, W[f"{l}.w_up"]).astype(np.float32)
-        act = bf16_round((silu(_f64(g_)) * u_).astype(np.float32))
-        h = (h + linear(act, W[f"{l}.w_down"])).astype(np.float32)
+        g_ = _s(linear(xn, W[f"{l}.w_gate"]))
+        u_ = _s(linear(xn, W[f"{l}.w_up"]))
+        act = _b(silu(_f64(g_)) * u_)
+        h = _s(h + linear(act, W[f"{l}.w_down"]))
     rows, tgts = [], []
     for g in range(G):
         for j in range(int(lengths[g])):

@@ -33,8 +33,7 @@ mrsp_status mrsp_op_rope(void* qkv, int ld, int col0, int n_heads, const int32_t
   return guard([&] {
     require_device();
     float inv[64];
-    for (int i = 0; i < 64; ++i)
-      inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(theta), (2.0 * i) / 128.0));
+    rope_inv_freq(theta, inv);
     set_rope_inv_freq(inv, S(stream));
     rope(static_cast<__nv_bfloat16*>(qkv), ld, col0, n_heads, pos, n, S(stream));
   });

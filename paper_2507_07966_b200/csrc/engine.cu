@@ -158,8 +158,7 @@ Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n
     ranks_[i].hs = head_split(cfg.n_q_heads, cfg.n_kv_heads, k_, ranks_[i].g);
   }
   float inv[64];
-  for (int i = 0; i < 64; ++i)
-    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(cfg.rope_theta), (2.0 * i) / 128.0));
+  rope_inv_freq(cfg.rope_theta, inv);  // HF float32 convention (kernels_misc.cu)
   set_rope_inv_freq(inv, stream_);
   build_routes(inv);
   init_weights(vision_seed, policy_seed, ref_seed, with_ref);

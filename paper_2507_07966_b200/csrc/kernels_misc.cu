@@ -2,6 +2,7 @@
 // norms, RoPE, patchify, the MR-SP sequence pack, the log-prob combine and the
 // counter-based weight initialiser. All use 128-bit vector accesses on the
 // contiguous (feature) dimension and grids sized as multiples of the SM count.
+#include <cmath>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -291,6 +292,19 @@ void layernorm(const float* x, int ldx, const float* w, const float* b, __nv_bfl
   layernorm_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, ldx, w, b, out, ldo, n, d, eps);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
+}
+
+// RoPE inverse frequencies as HF transformers builds them (Qwen2
+// RotaryEmbedding: 1.0 / base ** (arange(0, dim, 2).float() / dim)): float32
+// exponent, float32 power (correctly rounded here), float32 reciprocal.
+// Restated by oracle/transformer.py:rope_inv_freq and pinned against HF in
+// tests/test_oracle_hf_pin.py.
+void rope_inv_freq(float theta, float* inv64) {
+  for (int i = 0; i < 64; ++i) {
+    const float e = static_cast<float>(2 * i) / 128.0f;
+    const float a = static_cast<float>(std::pow(static_cast<double>(theta), static_cast<double>(e)));
+    inv64[i] = 1.0f / a;
+  }
 }
 
 void set_rope_inv_freq(const float* inv_freq64, cudaStream_t s) {

@@ -12,6 +12,7 @@ void rmsnorm(const float* x, int ldx, const float* w, __nv_bfloat16* out, int ld
              float eps, const int* rows, cudaStream_t s);
 void layernorm(const float* x, int ldx, const float* w, const float* b, __nv_bfloat16* out,
                int ldo, int n, int d, float eps, cudaStream_t s);
+void rope_inv_freq(float theta, float* inv64);  // HF float32 convention
 void set_rope_inv_freq(const float* inv_freq64, cudaStream_t s);
 void rope(__nv_bfloat16* qkv, int ld, int col0, int n_heads, const int* pos, int n, cudaStream_t s);
 void patchify(const float* pix, __nv_bfloat16* out, int F, int H, int W, int P, int kpad,
