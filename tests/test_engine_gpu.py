@@ -148,8 +148,13 @@ def test_full_width_shapes_vs_oracle(gpu):
     lp, lse = eng.prefill_logprobs(vid, grp, 0, with_lse=True)
     eng.close()
     want_emb = T.vision_forward(c, T.vision_weights(c, VSEED), pix)
+    # SURVEY §8c bound. Measured (tools/vision_numerics.py): engine vs oracle
+    # rel-L2 5.4e-3, the oracle's own bf16 storage vs exact float64 4.3e-3 and
+    # the engine vs exact float64 4.3e-3 — the engine is as close to the truth
+    # as the bf16 oracle is.
     rel = np.linalg.norm(emb - want_emb, axis=1) / np.linalg.norm(want_emb, axis=1)
-    assert rel.max() <= 2e-2 and rel.mean() <= 1e-2, (rel.max(), rel.mean())
+    cos = (emb * want_emb).sum(1) / (np.linalg.norm(emb, axis=1) * np.linalg.norm(want_emb, axis=1))
+    assert rel.max() <= 1e-2 and cos.min() >= 0.9995, (rel.max(), cos.min())
     want_lp, want_lse = T.llm_logprobs(c, T.llm_weights(c, PSEED, "policy."), emb, grp.question,
                                        grp.resp, grp.lengths)
     d = np.abs(lp - want_lp)
