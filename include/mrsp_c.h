@@ -301,6 +301,15 @@ typedef struct mrsp_engine mrsp_engine;
  * to sp/n_kv ranks that split its query-head group with plan_shards. */
 mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
 
+/* Query-row split used instead by the peer-memory / virtual-rank transports
+ * when sp > n_kv (MRSP_ULYSSES_SPLIT=heads restores the head split above):
+ * the m = sp / n_kv ranks sharing kv head g = rank / m each hold all n_q/n_kv
+ * of its query heads and compute the 256-row query blocks b of n_blocks =
+ * ceil(L / 256) with mrsp_attn_row_part(b, n_blocks, m) == rank % m — blocks
+ * dealt heaviest-first (causal cost grows with b) in a snake, so the m shares
+ * of attention work differ by at most one block. Returns -1 on bad input. */
+int mrsp_attn_row_part(int block, int n_blocks, int m);
+
 /* Rollout generation (policy.cpp:121-157 sample_rollout):
  * G rows sampled from the policy after the prompt [cached video | question]:
  * one prompt prefill keeps every layer's K/V, then each decode step runs the G

@@ -48,6 +48,7 @@ namespace {
 using namespace sm100;
 
 constexpr int TQ = 128, TK = 128, HD = 128;
+static_assert(2 * TQ == ATTN_ROW_BLOCK, "a CTA's query block is the row-split unit");
 constexpr int CHUNK = 128 * 64 * 2;  // one 128-row x 64-col bf16 SW128 block (16 KB)
 constexpr int TILE = 2 * CHUNK;      // a 128 x 128 bf16 operand (32 KB)
 constexpr int RING = 5;              // K/V ring slots
@@ -110,6 +111,7 @@ __device__ __forceinline__ int next_tile(int q0, int& kt, int hi, const MaskDev&
 
 struct AttnArgs {
   int n_pairs, n_heads, q_per_kv;
+  int n_local, row_parts, row_part;  // query blocks of this row part (all when 1 part)
   int q_col0, k_col0, v_col0, o_col0;
   __nv_bfloat16* O;
   int ldo;
@@ -133,14 +135,16 @@ __device__ __forceinline__ __nv_bfloat16* out_row(const AttnArgs& a, int q, int 
 // wave then streams the same KV head's K/V (71 MB at c4 for K+V, fits the
 // 126 MB L2) instead of all four heads' 285 MB — measured 44 GB of DRAM reads
 // per c4 launch with head-minor order.
-__device__ __forceinline__ void work_item(int idx, int n_blocks, int n_heads, int q_per_kv,
-                                          int& block, int& h) {
-  const int per_kv = n_blocks * q_per_kv;
+// With a query-row split the rank's share of blocks (attn_row_block) is walked
+// in the same heaviest-first order.
+__device__ __forceinline__ void work_item(int idx, const AttnArgs& a, int& block, int& h) {
+  const int per_kv = a.n_local * a.q_per_kv;
   const int kvh = idx / per_kv;
   const int rem = idx - kvh * per_kv;
-  block = n_blocks - 1 - rem / q_per_kv;
-  h = kvh * q_per_kv + rem % q_per_kv;
-  (void)n_heads;
+  const int li = rem / a.q_per_kv;
+  block = a.row_parts > 1 ? attn_row_block(li, a.row_part, a.n_pairs, a.row_parts)
+                          : a.n_pairs - 1 - li;
+  h = kvh * a.q_per_kv + rem % a.q_per_kv;
 }
 
 // Optional per-phase timeline of one CTA (tools/ubench/attn_trace.cu builds
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   ATRACE_INIT;
   const int warp = warp_id();
   int pair, h;
-  work_item(static_cast<int>(blockIdx.x), a.n_pairs, a.n_heads, a.q_per_kv, pair, h);
+  work_item(static_cast<int>(blockIdx.x), a, pair, h);
   const int kvh = h / a.q_per_kv;
   const int q0 = pair * 2 * TQ;
   const int n_kt = (a.mask.L + TK - 1) / TK;
@@ -637,7 +641,16 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.dst_col0 = p.dst_col0;
   for (int i = 0; i < 9; ++i) a.dst_bounds[i] = p.dst_bounds[i];
   for (int i = 0; i < 8; ++i) a.dst_base[i] = static_cast<__nv_bfloat16*>(p.dst_base[i]);
-  const int grid = a.n_pairs * a.n_heads;
+  MRSP_REQUIRE(p.row_parts >= 1 && p.row_part >= 0 && p.row_part < p.row_parts,
+               MRSP_INVALID_ARGUMENT, "attention: bad query-row split");
+  a.row_parts = p.row_parts;
+  a.row_part = p.row_part;
+  a.n_local = 0;
+  while (a.row_parts == 1 ? a.n_local < a.n_pairs
+                          : attn_row_block(a.n_local, a.row_part, a.n_pairs, a.row_parts) >= 0)
+    ++a.n_local;
+  if (a.n_local == 0) return;
+  const int grid = a.n_local * a.n_heads;
   kern<<<grid, THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());

@@ -27,6 +27,9 @@ struct AttnParams {
   long dst_bounds[9] = {};
   void* dst_base[8] = {};
   int dst_ld = 0, dst_col0 = 0;
+  // Query-row split (common.h attn_row_part): only the 256-row query blocks
+  // of part row_part of row_parts are computed (all heads).
+  int row_parts = 1, row_part = 0;
 };
 
 void attention_fwd(const AttnParams& p, cudaStream_t stream);

@@ -72,6 +72,24 @@ inline int num_sms() {
   return n;
 }
 
+// Query-row split of one kv head's attention over the m SP ranks sharing it
+// (HeadSplit::rparts). The work unit is the attention kernel's query block of
+// ATTN_ROW_BLOCK rows (two 128-row tiles, one CTA per head). Blocks are dealt
+// heaviest first — block b of n sees ~b KV tiles under the causal mask, so
+// i = n - 1 - b orders them by descending cost — in a snake 0..m-1, m-1..0, ...
+// so the m shares differ by at most one block's cost.
+constexpr int ATTN_ROW_BLOCK = 256;
+
+__host__ __device__ inline int attn_row_part(int b, int n_blocks, int m) {
+  const int i = n_blocks - 1 - b, r = i / m, p = i - r * m;
+  return (r & 1) ? m - 1 - p : p;
+}
+
+// Block of the li-th share of part p (< 0: p owns fewer than li + 1 blocks).
+__host__ __device__ inline int attn_row_block(int li, int part, int n_blocks, int m) {
+  return n_blocks - 1 - (li * m + ((li & 1) ? m - 1 - part : part));
+}
+
 }  // namespace mrsp
 
 #define MRSP_CUDA(x) ::mrsp::check_cuda((x), #x, __FILE__, __LINE__)

@@ -90,9 +90,12 @@ struct Carver {
 }  // namespace
 
 // Ulysses head split for SP rank r of k: contiguous head blocks
-// when k <= n_kv; otherwise k / n_kv ranks share one kv head (replicated) and
-// split its query-head group with plan_shards (28/4 at SP=8 -> 4+3 heads).
-HeadSplit head_split(int nq, int nkv, int k, int r) {
+// when k <= n_kv; otherwise m = k / n_kv ranks share one kv head (replicated)
+// and either split its query-head group with plan_shards (28/4 at SP=8 -> 4+3
+// heads: 12.5% attention imbalance; the NCCL transport) or, with row_split,
+// each take all of its query heads over 1/m of the query-row blocks, dealt by
+// a causal-cost snake (attn_row_part) so the shares are equal to one block.
+HeadSplit head_split(int nq, int nkv, int k, int r, bool row_split) {
   HeadSplit h{};
   if (k <= nkv) {
     MRSP_REQUIRE(nkv % k == 0 && nq % k == 0, MRSP_INVALID_ARGUMENT,
@@ -106,6 +109,16 @@ HeadSplit head_split(int nq, int nkv, int k, int r) {
     MRSP_REQUIRE(k % nkv == 0, MRSP_INVALID_ARGUMENT,
                  "ulysses: SP degree must be a multiple of the kv head count");
     const int m = k / nkv, g = r / m, j = r % m, qpk = nq / nkv;
+    if (row_split) {
+      h.q_lo = g * qpk;
+      h.q_hi = (g + 1) * qpk;
+      h.kv_lo = g;
+      h.kv_hi = g + 1;
+      h.q_per_kv = qpk;
+      h.rparts = m;
+      h.rpart = j;
+      return h;
+    }
     const auto p = plan(qpk, m)[j];
     h.q_lo = g * qpk + static_cast<int>(p.first);
     h.q_hi = g * qpk + static_cast<int>(p.second);
@@ -151,11 +164,15 @@ Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n
     else  // peer memory: mrsp_engine_p2p_export / _import before the first call
       mesh_ = std::make_unique<PeerMesh>(n_procs, proc_rank);
   }
+  {
+    const char* split = std::getenv("MRSP_ULYSSES_SPLIT");
+    row_split_ = !nccl_ && k_ > cfg.n_kv_heads && !(split && std::string(split) == "heads");
+  }
   const int local = n_procs > 1 ? 1 : k_;
   ranks_.resize(local);
   for (int i = 0; i < local; ++i) {
     ranks_[i].g = n_procs > 1 ? proc_rank : i;
-    ranks_[i].hs = head_split(cfg.n_q_heads, cfg.n_kv_heads, k_, ranks_[i].g);
+    ranks_[i].hs = split_of(ranks_[i].g);
   }
   float inv[64];
   rope_inv_freq(cfg.rope_theta, inv);  // HF float32 convention (kernels_misc.cu)
@@ -182,9 +199,25 @@ void Engine::build_routes(const float* inv_freq) {
   if (k_ == 1) {
     for (int hb = 0; hb < nblk; ++hb) add(hb, 0, hb * 128);
     ld[0] = nblk * 128;
+  } else if (row_split_) {
+    // every rank of kv group g holds [its group's qpk Q heads | K_g | V_g];
+    // a Q head block goes to ONE of the group's m ranks, chosen per row block
+    // in the QKV epilogue (route (-2, m)); K and V go to all m (route (-3, m))
+    const int m = k_ / nkv, qpk = nq / nkv;
+    for (int p = 0; p < k_; ++p) ld[p] = (qpk + 2) * 128;
+    for (int g = 0; g < nkv; ++g) {
+      for (int j = 0; j < qpk; ++j) {
+        route[2 * (g * qpk + j)] = make_int2(g * m, j * 128);
+        route[2 * (g * qpk + j) + 1] = make_int2(-2, m);
+      }
+      route[2 * (nq + g)] = make_int2(g * m, qpk * 128);
+      route[2 * (nq + g) + 1] = make_int2(-3, m);
+      route[2 * (nq + nkv + g)] = make_int2(g * m, (qpk + 1) * 128);
+      route[2 * (nq + nkv + g) + 1] = make_int2(-3, m);
+    }
   } else {
     for (int p = 0; p < k_; ++p) {
-      const HeadSplit hs = head_split(nq, nkv, k_, p);
+      const HeadSplit hs = split_of(p);
       ld[p] = (hs.nq() + 2 * hs.nkv()) * 128;
       if (hs.nq() == 0) continue;  // no query head: never reads K/V (SP > n_q / q_per_kv)
       for (const auto& blk : ulysses_blocks(nq, nkv, hs))
@@ -200,6 +233,7 @@ void Engine::build_routes(const float* inv_freq) {
   d_peer_base_ = reinterpret_cast<void**>(base + off_base);
   MRSP_CUDA(cudaMemcpy(d_inv_freq_, inv_freq, 64 * sizeof(float), cudaMemcpyHostToDevice));
   MRSP_CUDA(cudaMemcpy(d_route_, route.data(), route.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  route_h_ = route;
   MRSP_CUDA(cudaMemcpy(d_peer_ld_, ld.data(), 8 * sizeof(int), cudaMemcpyHostToDevice));
 }
 
@@ -653,7 +687,7 @@ void Engine::a2a_forward(int L) {
   std::vector<size_t> soff(k_ + 1, 0);
   std::vector<HeadSplit> hs(k_);
   for (int p = 0; p < k_; ++p) {
-    hs[p] = head_split(nq, nkv, k_, p);
+    hs[p] = split_of(p);
     soff[p + 1] = soff[p] + static_cast<size_t>(n_me) * (hs[p].nq() + 2 * hs[p].nkv()) * 128;
   }
   bf16* sendb = static_cast<bf16*>(me.send.ensure(std::max<size_t>(soff[k_], 1) * 2));
@@ -709,7 +743,7 @@ void Engine::a2a_backward(int L) {
   std::vector<HeadSplit> hs(k_);
   std::vector<size_t> roff(k_ + 1, 0);
   for (int p = 0; p < k_; ++p) {
-    hs[p] = head_split(nq, cfg_.n_kv_heads, k_, p);
+    hs[p] = split_of(p);
     roff[p + 1] = roff[p] + static_cast<size_t>(n_me) * hs[p].nq() * 128;
   }
   bf16* recvb = static_cast<bf16*>(me.recv.ensure(std::max<size_t>(roff[k_], 1) * 2));
@@ -805,6 +839,31 @@ void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n
       }
     }
     R.n_scored = static_cast<int>(idx.size());
+    R.sc_lo = slot.empty() ? 0 : slot[0];  // scored tokens are slot-ordered by position
+    {  // this rank's LM-head slice and its [targets | slots]
+      if (spread_lm()) {
+        const auto sp = plan(g.total_scored, k_)[R.g];
+        R.lm_lo = static_cast<long>(sp.first);
+        R.lm_n = static_cast<int>(sp.second - sp.first);
+      } else {
+        R.lm_lo = R.sc_lo;
+        R.lm_n = R.n_scored;
+      }
+      std::vector<int32_t> lm(2 * static_cast<size_t>(R.lm_n));
+      for (int i = 0, r = 0; i < R.lm_n; ++i) {
+        const long sl = R.lm_lo + i;
+        while (row_off[r + 1] <= sl) ++r;
+        lm[i] = resp[static_cast<size_t>(r) * Lmax + (sl - row_off[r])];
+        lm[R.lm_n + i] = static_cast<int32_t>(sl);
+      }
+      int32_t* dl = static_cast<int32_t*>(R.lm_idx.ensure((lm.size() + 1) * 4));
+      if (!lm.empty()) {
+        MRSP_CUDA(cudaMemcpyAsync(dl, lm.data(), lm.size() * 4, cudaMemcpyHostToDevice, s));
+        MRSP_CUDA(cudaStreamSynchronize(s));
+      }
+      if (spread_lm() && !mesh_)
+        R.lmx.ensure(static_cast<size_t>(2) * std::max(R.lm_n, 1) * d * 2);
+    }
     int32_t* di = static_cast<int32_t*>(R.scored_idx.ensure((idx.size() + 1) * 4 * 3));
     if (!idx.empty()) {
       MRSP_CUDA(cudaMemcpyAsync(di, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
@@ -834,10 +893,51 @@ void Engine::prepare_group(const CacheEntry& emb, const int32_t* question, int n
     R.xs.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
     R.xs2.ensure(static_cast<size_t>(std::max(R.n_scored, 1)) * d * 2);
   }
+  if (k_ > 1 && fused_a2a()) plan_a2a_bytes();
   if (fused_a2a()) {  // this group's destinations of the fused all-to-all
     for (int p = 0; p < k_; ++p) h_peer_base_[p] = k_ == 1 ? ranks_[0].qkv.p : qh_dst(p);
     MRSP_CUDA(cudaMemcpyAsync(d_peer_base_, h_peer_base_.data(), 8 * sizeof(void*),
                               cudaMemcpyHostToDevice, s));
+  }
+}
+
+// Bytes each local rank's fused exchanges send to OTHER ranks per layer,
+// following the device routing exactly: the QKV epilogue's head-block routes
+// (sequence -> heads) and the attention epilogue's O rows (heads -> sequence).
+void Engine::plan_a2a_bytes() {
+  const GroupState& g = grp_;
+  const int nq = cfg_.n_q_heads, nkv = cfg_.n_kv_heads, nblk = nq + 2 * nkv;
+  const int n_blocks = static_cast<int>((g.Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
+  a2a_fwd_bytes_.assign(ranks_.size(), 0);
+  a2a_bwd_bytes_.assign(ranks_.size(), 0);
+  auto owner = [&](long row) {  // sequence shard holding a token
+    int p = 0;
+    while (p + 1 < k_ && row >= token_b_[p + 1]) ++p;
+    return p;
+  };
+  for (size_t i = 0; i < ranks_.size(); ++i) {
+    const RankCtx& R = ranks_[i];
+    for (int b = 0; b < n_blocks; ++b) {
+      const long r0 = static_cast<long>(b) * ATTN_ROW_BLOCK, r1 = std::min(r0 + ATTN_ROW_BLOCK, g.Ltot);
+      // forward: R's rows of this block, every head block to its owner(s)
+      const long n = std::max(0L, std::min(r1, R.e) - std::max(r0, R.b));
+      if (n > 0)
+        for (int hb = 0; hb < nblk; ++hb) {
+          const int2 d0 = route_h_[2 * hb], d1 = route_h_[2 * hb + 1];
+          const int n_to = d1.x == -3 ? d1.y : d1.x == -2 ? 1 : 2;
+          for (int t = 0; t < n_to; ++t) {
+            const int dst = d1.x == -2 ? d0.x + attn_row_part(b, n_blocks, d1.y)
+                          : d1.x == -3 ? d0.x + t : (t ? d1.x : d0.x);
+            if (dst >= 0 && dst != R.g) a2a_fwd_bytes_[i] += static_cast<uint64_t>(n) * 256;
+          }
+        }
+      // backward: O rows of the blocks R computes, to each token's shard
+      if (R.hs.nq() == 0 ||
+          (R.hs.rparts > 1 && attn_row_part(b, n_blocks, R.hs.rparts) != R.hs.rpart))
+        continue;
+      for (long r = r0; r < r1; ++r)
+        if (owner(r) != R.g) a2a_bwd_bytes_[i] += static_cast<uint64_t>(R.hs.nq()) * 256;
+    }
   }
 }
 
@@ -880,13 +980,9 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
         ga.route = d_route_;
         ga.peer_base = d_peer_base_;
         ga.peer_ld = d_peer_ld_;
+        ga.row_blocks = static_cast<int>((g.Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
         gemm_bf16(ga, s);
-        if (k_ > 1)
-          for (int p = 0; p < k_; ++p)
-            if (p != R.g) {
-              const HeadSplit hp = head_split(nq, nkv, k_, p);
-              if (hp.nq()) a2a_bytes.fetch_add(static_cast<uint64_t>(n) * (hp.nq() + 2 * hp.nkv()) * 256);
-            }
+        if (k_ > 1) a2a_bytes.fetch_add(a2a_fwd_bytes_[&R - ranks_.data()]);
         continue;
       }
       {
@@ -937,9 +1033,10 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
           for (int p = 0; p < k_; ++p) {
             ap.dst_bounds[p] = token_b_[p];
             ap.dst_base[p] = ol_dst(p);
-            if (p != R.g)
-              a2a_bytes.fetch_add(static_cast<uint64_t>(token_e_[p] - token_b_[p]) * nqr * 256);
           }
+          a2a_bytes.fetch_add(a2a_bwd_bytes_[&R - ranks_.data()]);
+          ap.row_parts = R.hs.rparts;
+          ap.row_part = R.hs.rpart;
           ap.dst_bounds[k_] = token_e_[k_ - 1];
           ap.dst_ld = Cq;
           ap.dst_col0 = R.hs.q_lo * 128;
@@ -1001,11 +1098,10 @@ void Engine::finish_group(int nvec, float* const* outs, bool out_on_device) {
     const RankCtx& R = ranks_[0];
     Prof pc(*this, P_COMM);
     mesh_->barrier(s);  // every rank has read the previous group's outputs
-    if (R.n_scored)
+    if (R.lm_n)
       for (int p = 0; p < k_; ++p) {
-        scatter3_kernel<<<(R.n_scored + 255) / 256, 256, 0, s>>>(
-            R.lp.as<float>(), R.scored_idx.as<int32_t>() + 2 * R.n_scored, R.n_scored, nvec,
-            mesh_->lp(p), stride);
+        scatter3_kernel<<<(R.lm_n + 255) / 256, 256, 0, s>>>(
+            R.lp.as<float>(), R.lm_idx.as<int32_t>() + R.lm_n, R.lm_n, nvec, mesh_->lp(p), stride);
         count_launch();
         MRSP_CUDA(cudaGetLastError());
       }
@@ -1019,10 +1115,9 @@ void Engine::finish_group(int nvec, float* const* outs, bool out_on_device) {
     return;
   }
   for (auto& R : ranks_) {
-    if (R.n_scored == 0) continue;
-    scatter3_kernel<<<(R.n_scored + 255) / 256, 256, 0, s>>>(
-        R.lp.as<float>(), R.scored_idx.as<int32_t>() + 2 * R.n_scored, R.n_scored, nvec, g.full,
-        g.stride);
+    if (R.lm_n == 0) continue;
+    scatter3_kernel<<<(R.lm_n + 255) / 256, 256, 0, s>>>(
+        R.lp.as<float>(), R.lm_idx.as<int32_t>() + R.lm_n, R.lm_n, nvec, g.full, g.stride);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
@@ -1038,6 +1133,44 @@ void Engine::finish_group(int nvec, float* const* outs, bool out_on_device) {
   prof_collect();
 }
 
+const void* Engine::lm_rows(RankCtx& R, int m) {
+  if (!spread_lm()) return (m ? R.xs2 : R.xs).p;
+  const size_t cap = mesh_ ? static_cast<size_t>(mesh_->caps().lm_rows) : static_cast<size_t>(R.lm_n);
+  const void* base = mesh_ ? mesh_->xs(R.g) : R.lmx.p;
+  return static_cast<const bf16*>(base) + static_cast<size_t>(m) * cap * cfg_.dim;
+}
+
+// Spread LM head: every owner copies its scored tokens' final-norm rows into
+// the landing rows of the rank(s) whose LM-head slice holds them (copy-engine
+// P2P over NVLink between processes; a device copy between virtual ranks).
+void Engine::lm_exchange(int n_models) {
+  if (!spread_lm()) return;
+  const GroupState& g = grp_;
+  const int d = cfg_.dim;
+  const auto lm_plan = plan(g.total_scored, k_);
+  Prof pc(*this, P_COMM);
+  if (mesh_) mesh_->barrier(stream_);  // every rank has consumed its previous slice
+  for (auto& R : ranks_) {
+    for (int p = 0; p < k_; ++p) {
+      const long lo = std::max<long>(R.sc_lo, static_cast<long>(lm_plan[p].first));
+      const long hi = std::min<long>(R.sc_lo + R.n_scored, static_cast<long>(lm_plan[p].second));
+      if (hi <= lo) continue;
+      const size_t cap = mesh_ ? static_cast<size_t>(mesh_->caps().lm_rows)
+                               : static_cast<size_t>(ranks_[p].lm_n);
+      bf16* dst = static_cast<bf16*>(mesh_ ? mesh_->xs(p) : ranks_[p].lmx.p);
+      for (int m = 0; m < n_models; ++m) {
+        const bf16* src = (m ? R.xs2 : R.xs).as<bf16>();
+        MRSP_CUDA(cudaMemcpyAsync(dst + (m * cap + (lo - static_cast<long>(lm_plan[p].first))) * d,
+                                  src + static_cast<size_t>(lo - R.sc_lo) * d,
+                                  static_cast<size_t>(hi - lo) * d * 2, cudaMemcpyDeviceToDevice,
+                                  stream_));
+      }
+      if (p != R.g) a2a_bytes.fetch_add(static_cast<uint64_t>(hi - lo) * d * 2 * n_models);
+    }
+  }
+  if (mesh_) mesh_->barrier(stream_);  // every slice has landed
+}
+
 void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, int n_q,
                               const int32_t* resp, const int32_t* lengths, int G, int Lmax,
                               int model, float* lp_out, float* lse_out, bool out_on_device) {
@@ -1045,16 +1178,17 @@ void Engine::prefill_logprobs(const CacheEntry& emb, const int32_t* question, in
   std::lock_guard<std::mutex> run(run_mu_);
   prepare_group(emb, question, n_q, resp, lengths, G, Lmax);
   run_pass(emb, model, 0);
+  lm_exchange(1);
   const auto& c = cfg_;
   for (auto& R : ranks_) {
-    const int ns = R.n_scored;
+    const int ns = R.lm_n;
     if (ns == 0) continue;
     float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 4 * 3));
     const size_t wsb = lmhead_workspace_bytes(ns, c.vocab);
     void* ws = R.ws.ensure(wsb);
     Prof pl(*this, P_LMHEAD);
-    lmhead_logprob(R.xs.p, c.dim, llm_[model].lm_head, ns, c.vocab, c.dim,
-                   R.scored_idx.as<int32_t>() + ns, lp, lp + ns, ws, wsb, stream_);
+    lmhead_logprob(lm_rows(R, 0), c.dim, llm_[model].lm_head, ns, c.vocab, c.dim,
+                   R.lm_idx.as<int32_t>(), lp, lp + ns, ws, wsb, stream_);
   }
   float* outs[2] = {lp_out, lse_out};
   finish_group(2, outs, out_on_device);
@@ -1069,17 +1203,18 @@ void Engine::group_logprobs(const CacheEntry& emb, const int32_t* question, int 
   prepare_group(emb, question, n_q, resp, lengths, G, Lmax);
   run_pass(emb, 0, 0);
   run_pass(emb, 1, 1);
+  lm_exchange(2);
   const auto& c = cfg_;
   for (auto& R : ranks_) {
-    const int ns = R.n_scored;
+    const int ns = R.lm_n;
     if (ns == 0) continue;
     float* lp = static_cast<float*>(R.lp.ensure(static_cast<size_t>(ns) * 4 * 3));
     const size_t wsb = lmhead_dual_workspace_bytes(ns, c.vocab);
     void* ws = R.ws.ensure(wsb);
     Prof pl(*this, P_LMHEAD);
-    lmhead_dual_logprob_kl(R.xs.p, llm_[0].lm_head, R.xs2.p, llm_[1].lm_head, ns, c.vocab, c.dim,
-                           R.scored_idx.as<int32_t>() + ns, lp, lp + ns, lp + 2 * ns, ws, wsb,
-                           stream_);
+    lmhead_dual_logprob_kl(lm_rows(R, 0), llm_[0].lm_head, lm_rows(R, 1), llm_[1].lm_head, ns,
+                           c.vocab, c.dim, R.lm_idx.as<int32_t>(), lp, lp + ns, lp + 2 * ns, ws,
+                           wsb, stream_);
   }
   float* outs[3] = {lp_policy, lp_ref, kl};
   finish_group(3, outs, out_on_device);
@@ -1348,6 +1483,8 @@ size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void
   caps.c_head_shard = std::max(1, R.hs.nq() + 2 * R.hs.nkv()) * 128;
   caps.cq = cfg_.n_q_heads * 128;
   caps.tok_row = tokens_per_frame() * cfg_.dim;
+  caps.lm_rows = (max_scored + k_ - 1) / k_;
+  caps.dim = cfg_.dim;
   if (blob) mesh_->export_blob(caps, blob);
   return PeerMesh::kBlobBytes;
 }
@@ -1481,6 +1618,11 @@ extern "C" mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, in
   });
 }
 
+extern "C" int mrsp_attn_row_part(int block, int n_blocks, int m) {
+  if (m < 1 || n_blocks < 1 || block < 0 || block >= n_blocks) return -1;
+  return mrsp::attn_row_part(block, n_blocks, m);
+}
+
 extern "C" size_t mrsp_p2p_blob_bytes(void) { return mrsp::PeerMesh::kBlobBytes; }
 
 extern "C" mrsp_status mrsp_nccl_unique_id(void* out128) {
@@ -1512,6 +1654,19 @@ static std::shared_ptr<CacheEntry> lookup(mrsp_engine* e, const char* id) {
   return it->second;
 }
 
+// The entries the last encodes / steps produced, by video id (<= 4 kept): what
+// prefill and get_embeddings resolve a video id to, also for cache-off fills.
+static void remember(mrsp_engine* e, const char* video_id, const std::shared_ptr<CacheEntry>& entry) {
+  std::lock_guard<std::mutex> lock(e->mu);
+  e->last[video_id] = entry;
+  while (e->last.size() > 4) {
+    auto oldest = std::min_element(e->last.begin(), e->last.end(),
+                                   [](auto& a, auto& b) { return a.second->seq < b.second->seq; });
+    if (oldest->first == video_id) break;
+    e->last.erase(oldest);
+  }
+}
+
 extern "C" mrsp_status mrsp_engine_encode(mrsp_engine* e, const char* video_id,
                                           const float* pixels, int F, int pixels_on_device,
                                           int use_cache, int* hit) {
@@ -1519,16 +1674,7 @@ extern "C" mrsp_status mrsp_engine_encode(mrsp_engine* e, const char* video_id,
     MRSP_REQUIRE(e && video_id && pixels, MRSP_INVALID_ARGUMENT, "encode: null argument");
     bool h = false;
     auto entry = e->impl->get_or_encode(video_id, pixels, F, pixels_on_device != 0, use_cache != 0, &h);
-    {
-      std::lock_guard<std::mutex> lock(e->mu);
-      e->last[video_id] = entry;
-      while (e->last.size() > 4) {
-        auto oldest = std::min_element(e->last.begin(), e->last.end(),
-                                       [](auto& a, auto& b) { return a.second->seq < b.second->seq; });
-        if (oldest->first == video_id) break;
-        e->last.erase(oldest);
-      }
-    }
+    remember(e, video_id, entry);
     if (hit) *hit = h ? 1 : 0;
   });
 }
@@ -1563,6 +1709,7 @@ extern "C" mrsp_status mrsp_engine_step(mrsp_engine* e, const char* video_id, co
       bool h = false;
       entry = e->impl->get_or_encode(video_id, pixels, F, pixels_on_device != 0, use_cache != 0, &h);
     }
+    remember(e, video_id, entry);
     e->impl->group_logprobs(*entry, question, n_q, resp, lengths, G, Lmax, logprob_policy,
                             logprob_ref, kl, out_on_device != 0);
   });

@@ -73,9 +73,15 @@ struct LlmW {
 
 struct HeadSplit {
   int q_lo, q_hi, kv_lo, kv_hi, q_per_kv;
+  // Query-row split (SP > n_kv, peer-memory transport): the rparts ranks
+  // sharing a kv head each take ALL its query heads over part rpart of the
+  // 256-row query blocks (attn_row_part), instead of splitting the heads 4+3.
+  int rparts = 1, rpart = 0;
   int nq() const { return q_hi - q_lo; }
   int nkv() const { return kv_hi - kv_lo; }
 };
+
+HeadSplit head_split(int nq, int nkv, int k, int r, bool row_split = false);
 
 // One SP rank living in this process (k of them in loopback mode, 1 with NCCL).
 struct RankCtx {
@@ -87,6 +93,13 @@ struct RankCtx {
   DevBuf h, xn, qkv, qh, oh, ol, act, pos, pad, scored_idx, xs, xs2, lp, ws, send, recv;
   long b = 0, e = 0;  // token range
   int n_scored = 0;
+  // spread LM head: this rank computes the scored tokens [lm_lo, lm_lo + lm_n)
+  // of the group (plan_shards over the scored tokens), its own scored tokens
+  // being [sc_lo, sc_lo + n_scored); lm_idx = [targets | slots] of its slice,
+  // lmx = [2][lm_n][d] landing rows (virtual ranks)
+  long sc_lo = 0, lm_lo = 0;
+  int lm_n = 0;
+  DevBuf lm_idx, lmx;
 };
 
 struct CacheEntry {
@@ -198,6 +211,23 @@ class Engine {
   std::array<void*, 8> h_peer_base_{};
   void build_routes(const float* inv_freq);
   bool fused_a2a() const { return !nccl_; }
+  // query-row split of a shared kv head's query heads (HeadSplit::rparts):
+  // the fused transports at SP > n_kv, unless MRSP_ULYSSES_SPLIT=heads
+  bool row_split_ = false;
+  HeadSplit split_of(int p) const {
+    return head_split(cfg_.n_q_heads, cfg_.n_kv_heads, k_, p, row_split_);
+  }
+  // bytes this group's fused all-to-alls move off each local rank per layer
+  std::vector<uint64_t> a2a_fwd_bytes_, a2a_bwd_bytes_;
+  std::vector<int2> route_h_;  // host copy of d_route_
+  // LM head over plan_shards of the scored tokens instead of on the shards
+  // that own them (the response rows are the sequence tail, i.e. the last
+  // shard): the final-norm rows move to their computing rank first
+  bool spread_lm() const { return k_ > 1 && fused_a2a(); }
+  // rows X of local rank R's LM-head slice for model slot m (0: xs, 1: xs2)
+  const void* lm_rows(RankCtx& R, int m);
+  void lm_exchange(int n_models);
+  void plan_a2a_bytes();
   // one process per GPU over CUDA-IPC peer memory (no NCCL id given)
   std::unique_ptr<PeerMesh> mesh_;
   // head-shard / sequence-shard output buffers of SP rank p (a virtual rank's
@@ -232,7 +262,6 @@ class Engine {
   DevBuf io_;  // step I/O staging
 };
 
-HeadSplit head_split(int nq, int nkv, int k, int r);
 std::array<std::array<int, 3>, 3> ulysses_blocks(int nq, int nkv, const HeadSplit& hs);
 
 }  // namespace mrsp

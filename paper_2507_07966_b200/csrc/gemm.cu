@@ -69,6 +69,7 @@ struct EpiArgs {
   const int2* route;
   void* const* peer_base;
   const int* peer_ld;
+  int row_blocks;
   // decode fusions of the split-K reduction (GemmArgs::post)
   int post;
   __nv_bfloat16* kv_rows;
@@ -98,6 +99,9 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
 // approximations' ~2^-11; an IEEE division per element made the SwiGLU
 // epilogue slower than the 128x256x3584 main loop it overlaps.
 __device__ __forceinline__ float tanh_fast(float x) {
+#ifdef MRSP_NUMERICS_PROBE_ACCURATE_TANH  // numerics probe builds only (tools/vision_numerics.py)
+  return tanhf(x);
+#endif
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
@@ -155,9 +159,18 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
             oa[i / 2] = pack_bf16(x1[0], x1[1]);
             ob[i / 2] = pack_bf16(x2[0], x2[1]);
           }
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int2 dd = t ? d1 : d0;
+          // destinations: d0 and d1 (x < 0: none); d1 = (-2, m): ONE of the m
+          // ranks from d0.x, by the row's query block (query-row split); d1 =
+          // (-3, m): all m ranks from d0.x (the shared K / V head)
+          const int n_to = d1.x == -3 ? d1.y : d1.x == -2 ? 1 : 2;
+#pragma unroll 1
+          for (int t = 0; t < n_to; ++t) {
+            int2 dd = t ? d1 : d0;
+            if (d1.x == -2)
+              dd = make_int2(d0.x + attn_row_part(static_cast<int>(grow / ATTN_ROW_BLOCK),
+                                                  args.row_blocks, d1.y), d0.y);
+            else if (d1.x == -3)
+              dd = make_int2(d0.x + t, d0.y);
             if (dd.x < 0) continue;
             __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.peer_base[dd.x]) +
                                  grow * args.peer_ld[dd.x] + dd.y + j;
@@ -939,7 +952,7 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
             g.ldc,
             g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
             g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld,
-            GEMM_POST_NONE, static_cast<__nv_bfloat16*>(g.kv_rows), g.kvw, g.kv_col0, g.tdev,
+            g.row_blocks, GEMM_POST_NONE, static_cast<__nv_bfloat16*>(g.kv_rows), g.kvw, g.kv_col0, g.tdev,
             g.norm_w, static_cast<__nv_bfloat16*>(g.norm_out), g.ld_norm, g.norm_eps};
   if (g.post == GEMM_POST_ROPE_APPEND)
     MRSP_REQUIRE(g.epi == GEMM_EPI_BIAS_BF16 && g.N % 128 == 0 && g.pos && g.inv_freq &&

@@ -31,6 +31,8 @@ struct GemmArgs {
   const int2* route = nullptr;
   void* const* peer_base = nullptr;
   const int* peer_ld = nullptr;
+  // route (-2, m): query-row split over ceil(total rows / ATTN_ROW_BLOCK) blocks
+  int row_blocks = 0;
   // Split-K for one-m-tile GEMMs (M <= 128: the decode steps' G rows): with a
   // workspace, K is split so that (n tiles x splits) fills the SMs; fp32
   // partials go to splitk_ws and a second kernel sums them in split order

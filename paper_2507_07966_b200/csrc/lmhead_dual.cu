@@ -6,9 +6,12 @@
 // :94-96; per-position KL in policy.cpp:176-193). Logits never leave TMEM.
 //
 // Tile = 128 tokens x 256 vocab entries, BOTH models: two tcgen05 accumulators
-// (2 x 256 TMEM columns), A_p/B_p/A_r/B_r staged by TMA (2-stage ring of
-// 96 KB). Epilogue per row (thread = token): online over the tile's 256
-// columns, with x = policy logit, y = reference logit,
+// (2 x 256 TMEM columns). The TMA ring holds one model's k-block per stage
+// (A 16 KB + B 32 KB) and alternates policy / reference, so 4 stages keep three
+// 48 KB loads in flight behind the MMA (a 2-stage ring of 96 KB policy+reference
+// stages kept one: 0.47 of the sustained peak). Epilogue: two warpgroups, each
+// the tile's 128 rows (thread = token) over one 128-column half, online over
+// its columns, with x = policy logit, y = reference logit,
 //   m_x, s_x = sum e^(x - m_x), u = sum e^(x - m_x) (x - y), m_y, s_y = sum e^(y - m_y)
 // plus the two target logits; a combine kernel merges the vocab tiles:
 //   lse_x = M_x + log S_x,  KL = U / S_x - lse_x + lse_y,  lp = logit[y] - lse.
@@ -28,10 +31,11 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 2;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // policy + reference operands
-constexpr int THREADS = 256;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // one model's k-block
+constexpr int THREADS = 384;                    // TMA, MMA, alloc, idle, 8 epilogue warps
+constexpr int HALVES = 2;                       // epilogue column halves (one per warpgroup)
 constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
 
 struct Part {  // per (token, vocab tile)
@@ -39,7 +43,7 @@ struct Part {  // per (token, vocab tile)
 };
 
 struct DualArgs {
-  int M, V, K, n_tiles;
+  int M, V, K, n_tiles;  // vocab tiles; partials per row = HALVES * n_tiles
   const int* targets;
   Part* part;
   float* tgt_x;
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(tempty, 32 * 8);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -89,14 +93,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mt = tile % m_tiles, nt = tile / m_tiles;  // vocab-major: W tiles stream once
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* s = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(s, &tmAx, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(s + A_BYTES, &tmBx, &full[stage], kb * BK, nt * BN);
-          tma_load_2d(s + A_BYTES + B_BYTES, &tmAy, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(s + 2 * A_BYTES + B_BYTES, &tmBy, &full[stage], kb * BK, nt * BN);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int y = 0; y < 2; ++y) {  // policy k-block, then reference k-block
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* s = smem + stage * STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(s, y ? &tmAy : &tmAx, &full[stage], kb * BK, mt * BM);
+            tma_load_2d(s + A_BYTES, y ? &tmBy : &tmBx, &full[stage], kb * BK, nt * BN);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -109,27 +113,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(tempty, tphase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < k_blocks; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t s = smem_u32(smem + stage * STAGE_BYTES);
+        for (int y = 0; y < 2; ++y) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t s = smem_u32(smem + stage * STAGE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            mma_bf16_ss(tmem, sdesc_sw128(s + k * 32), sdesc_sw128(s + A_BYTES + k * 32), idesc,
-                        (kb | k) != 0);
-            mma_bf16_ss(tmem + BN, sdesc_sw128(s + A_BYTES + B_BYTES + k * 32),
-                        sdesc_sw128(s + 2 * A_BYTES + B_BYTES + k * 32), idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss(tmem + y * BN, sdesc_sw128(s + k * 32), sdesc_sw128(s + A_BYTES + k * 32),
+                          idesc, (kb | k) != 0);
+            mma_commit(&empty[stage]);
+            if (kb == k_blocks - 1 && y == 1) mma_commit(tfull);
           }
-          mma_commit(&empty[stage]);
-          if (kb == k_blocks - 1) mma_commit(tfull);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       tphase ^= 1;
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;  // TMEM lane quarter, column half
     uint32_t tphase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int mt = tile % m_tiles, nt = tile / m_tiles;
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int tgt = row_ok ? a.targets[row] : -1;
       const uint32_t tr = tmem + (static_cast<uint32_t>(ew * 32) << 16);
       float mx = -INFINITY, sx = 0.f, ux = 0.f, my = -INFINITY, sy = 0.f;
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * (BN / HALVES); c < (half + 1) * (BN / HALVES); c += 32) {
         uint32_t rx[32], ry[32];
         tmem_ld32(tr + c, rx);
         tmem_ld32(tr + BN + c, ry);
@@ -177,7 +180,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         ux = au;
         sy = ay;
       }
-      if (row_ok) a.part[static_cast<size_t>(row) * a.n_tiles + nt] = Part{mx, sx, ux, my, sy};
+      if (row_ok)
+        a.part[(static_cast<size_t>(row) * a.n_tiles + nt) * HALVES + half] = Part{mx, sx, ux, my, sy};
       tc_fence_before();
       mbar_arrive(tempty);
       tphase ^= 1;
@@ -242,7 +246,7 @@ int sm_count() {
 
 size_t lmhead_dual_workspace_bytes(int M, int V) {
   const size_t n_tiles = (V + BN - 1) / BN;
-  return (static_cast<size_t>(M) * n_tiles * sizeof(Part) + static_cast<size_t>(M) * 8 + 255) &
+  return (static_cast<size_t>(M) * n_tiles * HALVES * sizeof(Part) + static_cast<size_t>(M) * 8 + 255) &
          ~size_t(255);
 }
 
@@ -266,7 +270,7 @@ void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, cons
   a.n_tiles = (V + BN - 1) / BN;
   a.targets = targets;
   a.part = static_cast<Part*>(ws);
-  a.tgt_x = reinterpret_cast<float*>(a.part + static_cast<size_t>(M) * a.n_tiles);
+  a.tgt_x = reinterpret_cast<float*>(a.part + static_cast<size_t>(M) * a.n_tiles * HALVES);
   a.tgt_y = a.tgt_x + M;
   CUtensorMap ax = make_tmap_bf16_2d(Xp, M, K, K, BM, BK);
   CUtensorMap bx = make_tmap_bf16_2d(Wp, V, K, K, BN, BK);
@@ -276,7 +280,7 @@ void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, cons
   lmhead_dual_tcgen05<<<std::min(tiles, sm_count()), THREADS, SMEM_BYTES, stream>>>(ax, bx, ay, by, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
-  lmhead_dual_combine<<<(M + 7) / 8, 256, 0, stream>>>(a.part, a.n_tiles, a.tgt_x, a.tgt_y, M, lp_p,
+  lmhead_dual_combine<<<(M + 7) / 8, 256, 0, stream>>>(a.part, a.n_tiles * HALVES, a.tgt_x, a.tgt_y, M, lp_p,
                                                        lp_r, kl);
   count_launch();
   MRSP_CUDA(cudaGetLastError());

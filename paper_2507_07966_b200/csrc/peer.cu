@@ -62,13 +62,14 @@ void PeerMesh::export_blob(const PeerCaps& caps, void* blob) {
   bytes_[2] = static_cast<size_t>(caps.frames) * caps.tok_row * 2;
   bytes_[3] = static_cast<size_t>(4) * (caps.scored + 16) * 4;
   bytes_[4] = 64 * sizeof(uint32_t);
+  bytes_[5] = static_cast<size_t>(2) * caps.lm_rows * caps.dim * 2;
   uint8_t* out = static_cast<uint8_t*>(blob);
   const int32_t hdr[2] = {me_, n_};
   std::memcpy(out, hdr, 8);
   for (int b = 0; b < kBuffers; ++b) {
     const size_t nb = std::max<size_t>((bytes_[b] + 255) & ~size_t(255), 256);
     MRSP_CUDA(cudaMalloc(&own_[b], nb));
-    MRSP_CUDA(cudaMemset(own_[b], 0, b >= 3 ? nb : 256));
+    MRSP_CUDA(cudaMemset(own_[b], 0, (b == 3 || b == 4) ? nb : 256));
     cudaIpcMemHandle_t h;
     MRSP_CUDA(cudaIpcGetMemHandle(&h, own_[b]));
     std::memcpy(out + 8 + b * 72, &h, 64);

@@ -10,6 +10,8 @@
 //   emb  [F_cap*T][d]    the gathered video embeddings (Stage 1 all-gather)
 //   lp   [4][S_cap+16]   the group-ordered per-token outputs (log-prob gather)
 //   flags [64] u32       barrier flags, slot p written by rank p
+//   xs   [2][lm_rows][d] this rank's slice of the scored tokens' final-norm rows
+//                        (both models) for the spread LM head
 // A device-side barrier (st.release.sys / ld.acquire.sys on the flags)
 // orders the remote stores of one phase before the reads of the next.
 #pragma once
@@ -30,11 +32,13 @@ struct PeerCaps {
   int c_head_shard = 0; // this rank's head-shard row width (elements)
   int cq = 0;           // n_q_heads * 128
   int tok_row = 0;      // tokens per frame * dim (elements per frame)
+  long lm_rows = 0;     // max scored tokens per rank's LM-head slice
+  int dim = 0;          // model dim
 };
 
 class PeerMesh {
  public:
-  static constexpr int kBuffers = 5;  // qh, ol, emb, lp, flags
+  static constexpr int kBuffers = 6;  // qh, ol, emb, lp, flags, xs
   static constexpr size_t kBlobBytes = 8 + kBuffers * (64 + 8);
 
   PeerMesh(int nranks, int rank);
@@ -52,6 +56,7 @@ class PeerMesh {
   void* ol(int p) const { return ptr_[p][1]; }
   void* emb(int p) const { return ptr_[p][2]; }
   float* lp(int p) const { return static_cast<float*>(ptr_[p][3]); }
+  void* xs(int p) const { return ptr_[p][5]; }
   const PeerCaps& caps() const { return caps_; }
   int nranks() const { return n_; }
   int rank() const { return me_; }

@@ -1,8 +1,12 @@
 """GPU: the production head geometry at SP = 8 (28 query / 4 kv heads, hd 128:
-every kv head replicated to a rank pair whose 7 query heads split 4 + 3,
-SURVEY H1) on a narrow model, end to end — 8 virtual ranks in one process and
-8 processes sharing one B200 through CUDA-IPC peer memory (the transport the
-N = 8 bench uses) are both bit-identical to SP = 1, and close to the oracle."""
+every kv head replicated to a rank pair) on a narrow model, end to
+end. The pair splits the kv head's work by query rows — each rank all 7 query
+heads over half of the 256-row query blocks, dealt by causal cost
+(mrsp_attn_row_part; the default of the fused transports) — or, with
+MRSP_ULYSSES_SPLIT=heads, by query heads 4 + 3 (the NCCL transport's plan).
+8 virtual ranks in one process (both splits) and 8 processes sharing one B200
+through CUDA-IPC peer memory (the transport the N = 8 bench uses) are
+bit-identical to SP = 1, and close to the oracle."""
 import numpy as np
 import pytest
 
@@ -39,7 +43,9 @@ def test_plan_is_the_production_split():
     assert [p["kv"] for p in plans] == [(g, g + 1) for g in range(4) for _ in range(2)]
 
 
-def test_sp8_virtual_ranks_bit_exact_and_oracle(gpu):
+@pytest.mark.parametrize("split", ["rows", "heads"])
+def test_sp8_virtual_ranks_bit_exact_and_oracle(gpu, split, monkeypatch):
+    monkeypatch.setenv("MRSP_ULYSSES_SPLIT", split)
     pix, grp = _inputs()
     base = _run_local(1, pix, grp)
     got = _run_local(8, pix, grp)
