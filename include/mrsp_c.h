@@ -318,7 +318,12 @@ int mrsp_attn_row_part(int block, int n_blocks, int m);
  * softmax(logits / temperature), u = splitmix64-hash(seed, row, t) in [0, 1);
  * a row stops after EOS (1). Outputs: tokens [G][max_len] (PAD = 0 after the
  * end), lengths [G] (EOS included), old_logprobs [G][max_len] =
- * log_softmax(logits)[token] at temperature 1. Single-GPU engines (SP = 1). */
+ * log_softmax(logits)[token] at temperature 1. SP > 1 (virtual ranks or one
+ * process per GPU over peer memory; not the NCCL transport): the prompt
+ * prefill is sequence-parallel, every rank gathers the prompt K/V of all kv
+ * heads from the ranks' head shards and runs the decode — the outputs are
+ * bit-identical on every rank and to SP = 1 (grpo.cpp:376-386 generates the G
+ * rollouts inside the SP engine loop). */
 mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id, const int32_t* question,
                                  int n_q, int G, int max_len, float temperature, uint64_t seed,
                                  int32_t* tokens_out, int32_t* lengths_out,

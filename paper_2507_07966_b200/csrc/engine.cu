@@ -998,16 +998,31 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
     }
     if (k_ > 1 && !fused_a2a()) a2a_forward(static_cast<int>(g.Ltot));
     if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
-    if (capture_kv_) {  // generation: keep this layer's prompt K and V (SP = 1),
-      // head-major [kv head][K | V][Lp][128] so decode streams contiguous HBM
+    if (capture_kv_) {  // generation: keep this layer's prompt K and V of every
+      // kv head, head-major [kv head][K | V][Lp][128] so decode streams
+      // contiguous HBM. SP = 1: from the QKV rows; SP > 1: from the head shard
+      // of a rank owning that kv head (a peer's landing buffer over NVLink) —
+      // read before this layer's closing barrier, so before any rank's next
+      // QKV scatter overwrites it.
       const size_t w = static_cast<size_t>(2 * nkv) * 128;
       bf16* dst = kv_prefix_.as<bf16>() + static_cast<size_t>(layer) * g.Lp * w;
       for (int j = 0; j < 2 * nkv; ++j) {  // j = 2 h + (0: K, 1: V)
-        const int src_head = nq + (j & 1) * nkv + (j >> 1);
-        MRSP_CUDA(cudaMemcpy2DAsync(dst + static_cast<size_t>(j) * g.Lp * 128, 256,
-                                    ranks_[0].qkv.as<bf16>() + static_cast<size_t>(src_head) * 128,
-                                    static_cast<size_t>(Cqkv) * 2, 256, g.Lp,
-                                    cudaMemcpyDeviceToDevice, s));
+        const int hkv = j >> 1, is_v = j & 1;
+        const bf16* src;
+        size_t ld;
+        if (k_ == 1) {
+          src = ranks_[0].qkv.as<bf16>() + static_cast<size_t>(nq + is_v * nkv + hkv) * 128;
+          ld = Cqkv;
+        } else {
+          int p = 0;  // first rank holding kv head hkv (ranks without query heads get no K/V)
+          while (!(split_of(p).kv_lo <= hkv && hkv < split_of(p).kv_hi && split_of(p).nq() > 0)) ++p;
+          const HeadSplit hp = split_of(p);
+          ld = static_cast<size_t>(hp.nq() + 2 * hp.nkv()) * 128;
+          src = static_cast<const bf16*>(qh_dst(p)) +
+                static_cast<size_t>(hp.nq() + is_v * hp.nkv() + (hkv - hp.kv_lo)) * 128;
+        }
+        MRSP_CUDA(cudaMemcpy2DAsync(dst + static_cast<size_t>(j) * g.Lp * 128, 256, src, ld * 2,
+                                    256, g.Lp, cudaMemcpyDeviceToDevice, s));
       }
     }
     for (auto& R : ranks_) {
@@ -1224,8 +1239,11 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
                       int max_len, float temperature, uint64_t seed, int32_t* tokens_out,
                       int32_t* lengths_out, float* old_lp_out) {
   const auto& c = cfg_;
-  MRSP_REQUIRE(k_ == 1 && !nccl_ && !mesh_, MRSP_INVALID_ARGUMENT,
-               "generate: single-GPU engines (SP = 1) only");
+  // SP > 1: the prompt prefill is sequence-parallel and every rank gathers the
+  // prompt K/V of all kv heads from the head shards; the G-row decode then runs
+  // on every rank (replicated: bit-identical tokens and log-probs everywhere).
+  MRSP_REQUIRE(!nccl_, MRSP_INVALID_ARGUMENT,
+               "generate: SP > 1 needs the peer-memory transport (no NCCL id)");
   MRSP_REQUIRE(temperature > 0.f, MRSP_INVALID_ARGUMENT,
                "sample_rollout: temperature must be > 0");
   MRSP_REQUIRE(max_len >= 1, MRSP_INVALID_ARGUMENT, "sample_rollout: max_len must be >= 1");
@@ -1251,7 +1269,7 @@ void Engine::generate(const CacheEntry& emb, const int32_t* question, int n_q, i
   // 2. decode state
   const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128;
   RankCtx& R = ranks_[0];
-  DevBuf& st = R.recv;  // generation scratch (R.send/R.recv are unused at SP = 1)
+  DevBuf& st = R.recv;  // generation scratch (R.send/R.recv serve only the NCCL exchange)
   const size_t n_tok = static_cast<size_t>(G) * max_len;
   size_t off = 0;
   auto carve = [&](size_t bytes) {

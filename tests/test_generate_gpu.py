@@ -169,3 +169,22 @@ def test_generation_edges(gpu, gen):
         assert d.max() <= 5e-2 and d.mean() <= 5e-3, (G, d.max(), d.mean())
     with pytest.raises(_lib.InvalidArgument):
         eng.generate("v", q, g_max + 1, 4)
+
+
+@pytest.mark.parametrize("sp", [2, 4, 8])
+def test_generation_sp_bit_exact(gpu, gen, sp):
+    """Generation inside an SP engine (grpo.cpp:376-386): the prompt prefill
+    runs sequence-parallel over `sp` virtual ranks (at SP 8 > n_kv the kv
+    heads are shared by query-row split ranks), the prompt K/V of every kv head
+    is gathered from the ranks' head shards, and the sampled tokens, lengths
+    and old log-probs are bit-identical to SP = 1."""
+    eng1, q = gen["eng"], gen["q"]
+    want = eng1.generate("v", q, 8, 20, temperature=1.0, seed=21)
+    eng = E.Engine(W1.cfg, sp=sp, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED)
+    try:
+        eng.encode("v", gen["pix"])
+        got = eng.generate("v", q, 8, 20, temperature=1.0, seed=21)
+    finally:
+        eng.close()
+    for x, y in zip(want, got):
+        assert np.array_equal(x, y), sp

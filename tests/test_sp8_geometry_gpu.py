@@ -76,6 +76,7 @@ def _worker(rank, world, port, q):
         eng.p2p_import(blobs)
         eng.encode("v", pix)
         out = eng.step("v", pix, grp, with_kl=True)
+        out = tuple(out) + tuple(eng.generate("v", grp.question, 4, 12, temperature=1.0, seed=5))
         dist.barrier()
         eng.close()
         dist.destroy_process_group()
@@ -85,9 +86,15 @@ def _worker(rank, world, port, q):
 
 
 def test_sp8_processes_p2p_bit_exact(gpu):
+    """... and rollout generation in the 8-process engine (prompt K/V gathered
+    from the peers' head shards over CUDA-IPC) is bit-identical to SP = 1."""
     import multiprocessing as mp
     pix, grp = _inputs()
-    base = _run_local(1, pix, grp)
+    eng = E.Engine(CFG, sp=1, vision_seed=2, policy_seed=3, ref_seed=4)
+    eng.encode("v", pix)
+    base = tuple(eng.step("v", pix, grp, with_kl=True)) + tuple(
+        eng.generate("v", grp.question, 4, 12, temperature=1.0, seed=5))
+    eng.close()
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
     port = P._free_port()

@@ -1,6 +1,8 @@
 """Attention throughput probe (CUDA events) — dev tool.
 
-  python tools/attn_perf.py [poly ...]   # sweep MRSP_ATTN_POLY values
+  python tools/attn_perf.py [poly[:split] ...]   # sweep MRSP_ATTN_POLY / MRSP_ATTN_SPLIT
+  (variants interleaved per shape, repeated `MRSP_PERF_REPS` times: clocks drift
+  under the power cap)
 """
 import sys, pathlib, json, math, os
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
@@ -23,12 +25,16 @@ def bench(L, nq, nkv, Lp=None, Lmax=0, iters=5):
     return dict(L=L, nq=nq, nkv=nkv, Lp=Lp_, Lmax=Lmax, ms=round(ms, 3), tflops=round(flops / ms / 1e9, 1))
 
 if __name__ == "__main__":
-    polys = sys.argv[1:] or [os.environ.get("MRSP_ATTN_POLY", "")]
-    for p in polys:
-        if p:
-            os.environ["MRSP_ATTN_POLY"] = p
-        for args in [(16384, 28, 4), (32768, 28, 4), (16421 + 8 * 1024, 28, 4, 16421, 1024),
-                     (131109 + 8 * 1011, 28, 4, 131109, 1011)]:
-            r = bench(*args, iters=2 if args[0] > 100000 else 5)
-            r["poly"] = p
-            print(json.dumps(r), flush=True)
+    variants = sys.argv[1:] or [os.environ.get("MRSP_ATTN_POLY", "0")]
+    reps = int(os.environ.get("MRSP_PERF_REPS", "1"))
+    shapes = [(16384, 28, 4), (32768, 28, 4), (16421 + 8 * 1024, 28, 4, 16421, 1024),
+              (131109 + 8 * 1011, 28, 4, 131109, 1011)]
+    for args in shapes:
+        for rep in range(reps):
+            for v in variants:
+                poly, _, split = v.partition(":")
+                os.environ["MRSP_ATTN_POLY"] = poly or "0"
+                os.environ["MRSP_ATTN_SPLIT"] = split or "1"
+                r = bench(*args, iters=2 if args[0] > 100000 else 5)
+                r["poly"], r["split"], r["rep"] = poly or "0", split or "1", rep
+                print(json.dumps(r), flush=True)
