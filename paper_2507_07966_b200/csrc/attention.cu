@@ -113,6 +113,10 @@ struct AttnArgs {
   int n_pairs, n_heads, q_per_kv;
   int n_local, row_parts, row_part;  // query blocks of this row part (all when 1 part)
   int q_col0, k_col0, v_col0, o_col0;
+  // head stride in columns: HD (2-D maps, col0s in columns) or, when < HD,
+  // the real head dim (3-D maps [rows][heads][hs], col0s in heads; the boxes'
+  // columns past hs are zero-filled by TMA, so the tiles are hd-128 tiles)
+  int hs;
   __nv_bfloat16* O;
   int ldo;
   float scale_log2;
@@ -124,10 +128,10 @@ struct AttnArgs {
 
 // Destination row of query row q, head h: O itself, or the owner shard's buffer.
 __device__ __forceinline__ __nv_bfloat16* out_row(const AttnArgs& a, int q, int h) {
-  if (a.n_dst == 0) return a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * HD;
+  if (a.n_dst == 0) return a.O + static_cast<size_t>(q) * a.ldo + a.o_col0 + h * a.hs;
   int p = 0;
   while (p + 1 < a.n_dst && q >= a.dst_bounds[p + 1]) ++p;
-  return a.dst_base[p] + static_cast<size_t>(q - a.dst_bounds[p]) * a.dst_ld + a.dst_col0 + h * HD;
+  return a.dst_base[p] + static_cast<size_t>(q - a.dst_bounds[p]) * a.dst_ld + a.dst_col0 + h * a.hs;
 }
 
 // Work order: KV-head-major, then query-row blocks heaviest (longest KV sweep)
@@ -326,9 +330,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         // Q0, Q1 (rows past L are zero-filled by TMA)
         mbar_arrive_expect_tx(q_full, 2 * TILE);
         for (int t = 0; t < 2; ++t)
-          for (int c = 0; c < 2; ++c)
-            tma_load_2d(smem + OFF_Q + t * TILE + c * CHUNK, &tmQ, q_full,
-                        a.q_col0 + h * HD + c * 64, q0 + t * TQ);
+          for (int c = 0; c < 2; ++c) {
+            if (a.hs == HD)
+              tma_load_2d(smem + OFF_Q + t * TILE + c * CHUNK, &tmQ, q_full,
+                          a.q_col0 + h * HD + c * 64, q0 + t * TQ);
+            else
+              tma_load_3d(smem + OFF_Q + t * TILE + c * CHUNK, &tmQ, q_full, c * 64,
+                          a.q_col0 + h, q0 + t * TQ);
+          }
         int slot = 0;
         uint32_t ph = 0;
         for (int kt = kt_lo; next_tile(q0, kt, kt_hi, a.mask); ++kt) {
@@ -338,9 +347,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive_expect_tx(&r_full[slot], TILE);
             uint8_t* dst = smem + OFF_RING + slot * TILE;
             const CUtensorMap* tm = kv ? &tmV : &tmK;
-            const int col = (kv ? a.v_col0 : a.k_col0) + kvh * HD;
-            tma_load_2d(dst, tm, &r_full[slot], col, k0);
-            tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, k0);
+            if (a.hs == HD) {
+              const int col = (kv ? a.v_col0 : a.k_col0) + kvh * HD;
+              tma_load_2d(dst, tm, &r_full[slot], col, k0);
+              tma_load_2d(dst + CHUNK, tm, &r_full[slot], col + 64, k0);
+            } else {
+              const int head = (kv ? a.v_col0 : a.k_col0) + kvh;
+              tma_load_3d(dst, tm, &r_full[slot], 0, head, k0);
+              tma_load_3d(dst + CHUNK, tm, &r_full[slot], 64, head, k0);
+            }
             if (++slot == RING) { slot = 0; ph ^= 1; }
           }
         }
@@ -562,7 +577,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
 #pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
+      for (int c = 0; c < a.hs; c += 32) {  // the head's hs columns (O past hs is 0)
         uint32_t o[32];
         tmem_ld32(tO + c, o);
         tmem_ld_wait();
@@ -572,13 +587,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 16; ++j)
             pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * inv_l, __uint_as_float(o[2 * j + 1]) * inv_l);
           uint4* dst = reinterpret_cast<uint4*>(orow + c);
+          const int nv = min(4, (a.hs - c) / 8);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            if (j < nv) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         }
       }
     } else if (row_ok) {  // no visible key (only possible for rows past L)
-      for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < a.hs; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
     }
   }
   ATRACE_FINISH;
@@ -619,17 +635,30 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
     return true;
   }();
   (void)attr;
-  CUtensorMap tq = make_tmap_bf16_2d(p.Q, p.L, p.ldq, p.ldq, TQ, 64);
-  CUtensorMap tk = make_tmap_bf16_2d(p.K, p.L, p.ldk, p.ldk, TK, 64);
-  CUtensorMap tv = make_tmap_bf16_2d(p.V, p.L, p.ldv, p.ldv, TK, 64);
+  MRSP_REQUIRE(p.hstride == HD || (p.hstride > 0 && p.hstride < HD && p.hstride % 8 == 0 &&
+                                   p.ldq % p.hstride == 0 && p.ldk % p.hstride == 0 &&
+                                   p.ldv % p.hstride == 0 && p.q_col0 % p.hstride == 0 &&
+                                   p.k_col0 % p.hstride == 0 && p.v_col0 % p.hstride == 0 &&
+                                   p.n_dst == 0),
+               MRSP_INVALID_ARGUMENT, "attention: head stride must be 128 or a multiple of 8 "
+                                      "dividing the row pitches and column offsets");
+  const bool h3 = p.hstride != HD;
+  auto tmap = [&](const void* base, int ld, int box_rows) {
+    return h3 ? make_tmap_bf16_3d_heads(base, p.L, ld / p.hstride, p.hstride, ld, box_rows, 64)
+              : make_tmap_bf16_2d(base, p.L, ld, ld, box_rows, 64);
+  };
+  CUtensorMap tq = tmap(p.Q, p.ldq, TQ);
+  CUtensorMap tk = tmap(p.K, p.ldk, TK);
+  CUtensorMap tv = tmap(p.V, p.ldv, TK);
   AttnArgs a;
   const int n_q_tiles = (p.L + TQ - 1) / TQ;
   a.n_pairs = (n_q_tiles + 1) / 2;
   a.n_heads = p.n_heads;
   a.q_per_kv = p.q_per_kv;
-  a.q_col0 = p.q_col0;
-  a.k_col0 = p.k_col0;
-  a.v_col0 = p.v_col0;
+  a.hs = p.hstride;
+  a.q_col0 = h3 ? p.q_col0 / p.hstride : p.q_col0;
+  a.k_col0 = h3 ? p.k_col0 / p.hstride : p.k_col0;
+  a.v_col0 = h3 ? p.v_col0 / p.hstride : p.v_col0;
   a.o_col0 = p.o_col0;
   a.O = static_cast<__nv_bfloat16*>(p.O);
   a.ldo = p.ldo;

@@ -30,6 +30,10 @@ struct AttnParams {
   // Query-row split (common.h attn_row_part): only the 256-row query blocks
   // of part row_part of row_parts are computed (all heads).
   int row_parts = 1, row_part = 0;
+  // Column stride of one head in Q, K, V and O (128, or a real head dim < 128
+  // such as SigLIP's 72: the tiles are zero-filled to 128 on chip and only hs
+  // output columns are written).
+  int hstride = 128;
 };
 
 void attention_fwd(const AttnParams& p, cudaStream_t stream);

@@ -129,6 +129,12 @@ HeadSplit head_split(int nq, int nkv, int k, int r, bool row_split) {
   return h;
 }
 
+int vision_head_stride(const mrsp_model_config& c) {
+  const char* pad = std::getenv("MRSP_VISION_PAD");
+  if (pad && std::atoi(pad) != 0) return 128;
+  return c.v_head_dim % 8 == 0 ? c.v_head_dim : 128;
+}
+
 // Column blocks of a sequence-shard QKV row [Q heads | K heads | V heads] that
 // the destination rank of `hs` owns, as (src col, dst col, width) for Q, K, V;
 // the destination stores them as [its Q | its K | its V].
@@ -174,6 +180,7 @@ Engine::Engine(const mrsp_model_config& cfg, int sp_degree, int proc_rank, int n
     ranks_[i].g = n_procs > 1 ? proc_rank : i;
     ranks_[i].hs = split_of(ranks_[i].g);
   }
+  vstride_ = vision_head_stride(cfg);
   float inv[64];
   rope_inv_freq(cfg.rope_theta, inv);  // HF float32 convention (kernels_misc.cu)
   set_rope_inv_freq(inv, stream_);
@@ -255,7 +262,8 @@ Engine::~Engine() {
 void Engine::init_weights(uint64_t vseed, uint64_t pseed, uint64_t rseed, int with_ref) {
   const auto& c = cfg_;
   const int T = tokens_per_frame(), kreal = 3 * c.patch * c.patch, kpad = (kreal + 7) / 8 * 8;
-  const int vd = c.v_dim, vh = c.v_heads, vhd = c.v_head_dim, vq = vh * 128;
+  const int vd = c.v_dim, vh = c.v_heads, vhd = c.v_head_dim, vs = vstride_;
+  const int vq = vh * vs;
   const int d = c.dim, qkv_rows = (c.n_q_heads + 2 * c.n_kv_heads) * 128;
   has_ref_ = with_ref != 0;
   // size the single weight allocation
@@ -314,14 +322,14 @@ void Engine::init_weights(uint64_t vseed, uint64_t pseed, uint64_t rseed, int wi
     const std::string p = "vision." + std::to_string(l) + ".";
     L.ln1_w = cv.take<float>(vd); f32(L.ln1_w, vd, vseed, p + "ln1_w", kNorm, 1.f);
     L.ln1_b = cv.take<float>(vd); f32(L.ln1_b, vd, vseed, p + "ln1_b", kBias, 0.f);
-    // QKV / O with heads padded 72 -> 128 (zero rows / columns)
+    // QKV / O with head stride vs (vs > vhd: zero rows / columns)
     L.wqkv = cv.take<bf16>(static_cast<size_t>(3) * vq * vd);
     {
       bf16* t = static_cast<bf16*>(tmp.ensure(static_cast<size_t>(3) * vd * vd * 2));
       bf(t, static_cast<size_t>(3) * vd * vd, vseed, p + "wqkv", wscale(vd));
       for (int part = 0; part < 3; ++part)
         for (int h = 0; h < vh; ++h)
-          MRSP_CUDA(cudaMemcpyAsync(L.wqkv + (static_cast<size_t>(part) * vq + h * 128) * vd,
+          MRSP_CUDA(cudaMemcpyAsync(L.wqkv + (static_cast<size_t>(part) * vq + h * vs) * vd,
                                     t + (static_cast<size_t>(part) * vd + h * vhd) * vd,
                                     static_cast<size_t>(vhd) * vd * 2, cudaMemcpyDeviceToDevice, s));
     }
@@ -331,7 +339,7 @@ void Engine::init_weights(uint64_t vseed, uint64_t pseed, uint64_t rseed, int wi
       f32(t, 3 * vd, vseed, p + "bqkv", kBias, 0.f);
       for (int part = 0; part < 3; ++part)
         for (int h = 0; h < vh; ++h)
-          MRSP_CUDA(cudaMemcpyAsync(L.bqkv + part * vq + h * 128, t + part * vd + h * vhd, vhd * 4,
+          MRSP_CUDA(cudaMemcpyAsync(L.bqkv + part * vq + h * vs, t + part * vd + h * vhd, vhd * 4,
                                     cudaMemcpyDeviceToDevice, s));
     }
     L.wo = cv.take<bf16>(static_cast<size_t>(vd) * vq);
@@ -339,7 +347,7 @@ void Engine::init_weights(uint64_t vseed, uint64_t pseed, uint64_t rseed, int wi
       bf16* t = static_cast<bf16*>(tmp.ensure(static_cast<size_t>(vd) * vd * 2));
       bf(t, static_cast<size_t>(vd) * vd, vseed, p + "wo", wscale(vd));
       for (int h = 0; h < vh; ++h)
-        MRSP_CUDA(cudaMemcpy2DAsync(L.wo + h * 128, static_cast<size_t>(vq) * 2, t + h * vhd,
+        MRSP_CUDA(cudaMemcpy2DAsync(L.wo + h * vs, static_cast<size_t>(vq) * 2, t + h * vhd,
                                     static_cast<size_t>(vd) * 2, vhd * 2, vd,
                                     cudaMemcpyDeviceToDevice, s));
     }
@@ -485,7 +493,7 @@ void Engine::encode_rank(RankCtx& R, const float* pixels, bool on_device, int F,
   if (nf <= 0) return;
   const int T = tokens_per_frame(), S = c.image_size, P = c.patch;
   const int kreal = 3 * P * P, kpad = (kreal + 7) / 8 * 8;
-  const int vd = c.v_dim, vq = c.v_heads * 128, ntok = nf * T;
+  const int vd = c.v_dim, vs = vstride_, vq = c.v_heads * vs, ntok = nf * T;
   cudaStream_t s = stream_;
   const size_t frame_px = static_cast<size_t>(3) * S * S;
   Prof pv(*this, P_VISION);
@@ -511,9 +519,10 @@ void Engine::encode_rank(RankCtx& R, const float* pixels, bool on_device, int F,
     gemm_bf16({xn, L.wqkv, qkv, ntok, 3 * vq, vd, vd, vd, 3 * vq, GEMM_EPI_BIAS_BF16, L.bqkv,
                nullptr, 0},
               s);
-    attention_fwd({qkv, 3 * vq, 0, qkv, 3 * vq, vq, qkv, 3 * vq, 2 * vq, o, vq, 0, ntok,
-                   c.v_heads, 1, vscale, ATTN_BLOCK_DIAG, 0, 0, T},
-                  s);
+    AttnParams ap{qkv, 3 * vq, 0, qkv, 3 * vq, vq, qkv, 3 * vq, 2 * vq, o, vq, 0, ntok,
+                  c.v_heads, 1, vscale, ATTN_BLOCK_DIAG, 0, 0, T};
+    ap.hstride = vs;
+    attention_fwd(ap, s);
     gemm_bf16({o, L.wo, nullptr, ntok, vd, vq, vq, vq, 0, GEMM_EPI_RESID_F32, L.bo, vh, vd}, s);
     layernorm(vh, vd, L.ln2_w, L.ln2_b, xn, vd, ntok, vd, c.ln_eps, s);
     gemm_bf16({xn, L.w1, mid, ntok, c.v_mlp, vd, vd, vd, c.v_mlp, GEMM_EPI_BIAS_GELU_BF16, L.b1,

@@ -83,6 +83,13 @@ struct HeadSplit {
 
 HeadSplit head_split(int nq, int nkv, int k, int r, bool row_split = false);
 
+// Column stride of one vision head in the engine's QKV / attention-output
+// storage: the real head dim (SigLIP 72: unpadded GEMMs; the attention's 3-D
+// TMA boxes zero-fill 72 -> 128 on chip) when its rows are 16-byte multiples,
+// else 128 (zero-padded in HBM). MRSP_VISION_PAD=1 forces 128 (read when an
+// engine is created).
+int vision_head_stride(const mrsp_model_config& c);
+
 // One SP rank living in this process (k of them in loopback mode, 1 with NCCL).
 struct RankCtx {
   int g = 0;  // global SP rank
@@ -214,6 +221,7 @@ class Engine {
   // query-row split of a shared kv head's query heads (HeadSplit::rparts):
   // the fused transports at SP > n_kv, unless MRSP_ULYSSES_SPLIT=heads
   bool row_split_ = false;
+  int vstride_ = 128;  // vision_head_stride(cfg_), fixed at construction
   HeadSplit split_of(int p) const {
     return head_split(cfg_.n_q_heads, cfg_.n_kv_heads, k_, p, row_split_);
   }

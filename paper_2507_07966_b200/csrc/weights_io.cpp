@@ -12,8 +12,8 @@
 //                   mlp.{gate,up,down}_proj}.*, model.norm.weight, lm_head.weight
 // (the reference model of the GRPO pair is saved with the prefix "ref.").
 // Logical tensors are the unpadded HF shapes; the engine's storage transforms
-// (q/k/v concatenation, gate/up interleaved in 128-row blocks, vision heads
-// zero-padded 72 -> 128, patch K padded to a multiple of 8) are described per
+// (q/k/v concatenation, gate/up interleaved in 128-row blocks, vision heads at
+// the engine's head stride, patch K padded to a multiple of 8) are described per
 // tensor as 2-D strided segments, so save and load are exact inverses.
 #include <cuda_runtime.h>
 
@@ -205,10 +205,11 @@ float bf16_to_f32(uint16_t h) {
 // projector, 1 = policy LLM, 2 = reference LLM.
 static std::vector<TensorDesc> describe(const mrsp_model_config& c, const VisionW& vis,
                                         const LlmW& llm, int part, const std::string& pre,
-                                        int tokens_per_frame) {
+                                        int tokens_per_frame, int vs_) {
   std::vector<TensorDesc> t;
   const size_t P = c.patch, kreal = 3 * P * P, kpad = (kreal + 7) / 8 * 8;
-  const size_t vd = c.v_dim, vh = c.v_heads, vhd = c.v_head_dim, vq = vh * 128;
+  const size_t vd = c.v_dim, vh = c.v_heads, vhd = c.v_head_dim, vs = vs_;
+  const size_t vq = vh * vs;
   const size_t d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads, mlp = c.mlp, V = c.vocab;
   auto plain = [&](const std::string& name, DType dt, std::vector<long> shape, void* dev) {
     TensorDesc x{pre + name, dt, shape, {}};
@@ -232,24 +233,24 @@ static std::vector<TensorDesc> describe(const mrsp_model_config& c, const Vision
       plain(p + "layer_norm1.bias", F32, {static_cast<long>(vd)}, L.ln1_b);
       const char* qkv[3] = {"q_proj", "k_proj", "v_proj"};
       for (int part3 = 0; part3 < 3; ++part3) {
-        // rows h*vhd .. +vhd  ->  engine rows part*vq + h*128 (heads padded to 128)
+        // rows h*vhd .. +vhd  ->  engine rows part*vq + h*vs (head stride vs >= vhd)
         TensorDesc w{pre + p + "self_attn." + qkv[part3] + ".weight", BF16,
                      {static_cast<long>(vd), static_cast<long>(vd)}, {}};
         TensorDesc b{pre + p + "self_attn." + qkv[part3] + ".bias", F32, {static_cast<long>(vd)}, {}};
         for (size_t h = 0; h < vh; ++h) {
-          w.segs.push_back(Seg{L.wqkv + (part3 * vq + h * 128) * vd, vhd * vd * 2, h * vhd * vd * 2,
+          w.segs.push_back(Seg{L.wqkv + (part3 * vq + h * vs) * vd, vhd * vd * 2, h * vhd * vd * 2,
                                vhd * vd * 2, vhd * vd * 2, 1});
-          b.segs.push_back(Seg{L.bqkv + part3 * vq + h * 128, vhd * 4, h * vhd * 4, vhd * 4,
+          b.segs.push_back(Seg{L.bqkv + part3 * vq + h * vs, vhd * 4, h * vhd * 4, vhd * 4,
                                vhd * 4, 1});
         }
         t.push_back(std::move(w));
         t.push_back(std::move(b));
       }
-      {  // out_proj [vd][vd]: column block h*vhd .. -> engine columns h*128 ..
+      {  // out_proj [vd][vd]: column block h*vhd .. -> engine columns h*vs ..
         TensorDesc w{pre + p + "self_attn.out_proj.weight", BF16,
                      {static_cast<long>(vd), static_cast<long>(vd)}, {}};
         for (size_t h = 0; h < vh; ++h)
-          w.segs.push_back(Seg{L.wo + h * 128, vq * 2, h * vhd * 2, vd * 2, vhd * 2, vd});
+          w.segs.push_back(Seg{L.wo + h * vs, vq * 2, h * vhd * 2, vd * 2, vhd * 2, vd});
         t.push_back(std::move(w));
       }
       plain(p + "self_attn.out_proj.bias", F32, {static_cast<long>(vd)}, L.bo);
@@ -303,7 +304,7 @@ void Engine::save_weights(const std::string& path) {
   std::vector<TensorDesc> all;
   for (int part = 0; part < (has_ref_ ? 3 : 2); ++part) {
     auto v = describe(cfg_, vis_, llm_[part == 2 ? 1 : 0], part, part == 2 ? "ref." : "",
-                      tokens_per_frame());
+                      tokens_per_frame(), vstride_);
     all.insert(all.end(), v.begin(), v.end());
   }
   std::string hdr = "{\"__metadata__\":{\"format\":\"pt\",\"producer\":\"mrsp-b200\"}";
@@ -362,7 +363,8 @@ void Engine::load_weights(const std::string& path, int part, const std::string& 
     throw;
   }
   const long data0 = static_cast<long>(8 + hlen);
-  const auto want = describe(cfg_, vis_, llm_[part == 2 ? 1 : 0], part, prefix, tokens_per_frame());
+  const auto want =
+      describe(cfg_, vis_, llm_[part == 2 ? 1 : 0], part, prefix, tokens_per_frame(), vstride_);
   std::vector<uint8_t> raw, host;
   for (const auto& x : want) {
     auto it = table.find(x.name);

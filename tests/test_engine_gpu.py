@@ -50,6 +50,17 @@ def test_c1_embeddings_vs_oracle(gpu, c1_oracle):
     assert cos.min() >= 0.9995, cos.min()
 
 
+def test_c1_embeddings_padded_heads_vs_oracle(gpu, c1_oracle, monkeypatch):
+    """MRSP_VISION_PAD=1: vision heads zero-padded to 128 columns in HBM (the
+    default keeps the real head dim and zero-fills on chip via 3-D TMA)."""
+    monkeypatch.setenv("MRSP_VISION_PAD", "1")
+    emb, *_ = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
+    want = c1_oracle["emb"]
+    rel = np.linalg.norm(emb - want, axis=1) / np.linalg.norm(want, axis=1)
+    cos = (emb * want).sum(1) / (np.linalg.norm(emb, axis=1) * np.linalg.norm(want, axis=1))
+    assert rel.max() <= 1e-2 and cos.min() >= 0.9995, (rel.max(), cos.min())
+
+
 def test_c1_logprobs_vs_oracle(gpu, c1_oracle):
     _, lp_p, lse_p, lp_r, st = run_engine(1, c1_oracle["pix"], c1_oracle["grp"])
     for got, want in ((lp_p, c1_oracle["lp_p"]), (lp_r, c1_oracle["lp_r"])):
