@@ -146,9 +146,13 @@ typedef enum {
                                   C[:, tile*128 + j] = silu(g_j) * u_j      */
   GEMM_EPI_STORE_F32 = 5,      /* C(fp32) = A.B^T (+ bias)                  */
   GEMM_EPI_LOGPROB_PARTIAL = 6, /* internal: LM-head tile (max, sumexp, target) */
-  GEMM_EPI_QKV_SCATTER = 7      /* internal: +bias, bf16, RoPE on q/k heads, each 128-col
+  GEMM_EPI_QKV_SCATTER = 7,     /* internal: +bias, bf16, RoPE on q/k heads, each 128-col
                                    head block stored to its owner rank(s) (fused Ulysses
                                    sequence -> head all-to-all)                           */
+  GEMM_EPI_SWIGLU_BWD = 8       /* internal (backward): per 256-col tile [gate128|up128]
+                                   with dA = the gradient of the SwiGLU output: C = [dA u
+                                   silu'(g) | dA silu(g)] (bf16, same interleave as the
+                                   weight rows) and the forward output silu(g) u again   */
 } mrsp_gemm_epilogue;
 
 /* tcgen05 BF16 GEMM, fp32 accumulate: A[M][lda], B[N][ldb] (both K-major),
@@ -158,6 +162,17 @@ typedef enum {
 mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int lda,
                               int ldb, int ldc, int epilogue, const float* bias, float* resid,
                               int ldr, void* stream);
+
+/* Same GEMM with MN-major operands, for the backward pass (grpo.cpp:122-223
+ * turned into a transformer backward): a_mn = 1 means A is stored [K][lda]
+ * (element (m, k) at A[k*lda + m]); b_mn = 1 means B is stored [K][ldb].
+ * dgrad dX = dY . W reads the weight W[N_out][K_in] with b_mn = 1; wgrad
+ * dW = dY^T . X reads both token-major activations with a_mn = b_mn = 1 (K =
+ * tokens, any count). Epilogues STORE_BF16 / BIAS_BF16 / STORE_F32 /
+ * RESID_F32. */
+mrsp_status mrsp_op_gemm_bf16_mn(const void* A, const void* B, void* C, int M, int N, int K,
+                                 int lda, int ldb, int ldc, int a_mn, int b_mn, int epilogue,
+                                 const float* bias, float* resid, int ldr, void* stream);
 
 /* Same GEMM with a split-K workspace (device, fp32): when M <= 128 and the
  * N tiles cannot fill the SMs (the decode steps' G-row projections), K is
@@ -250,6 +265,46 @@ mrsp_status mrsp_op_attention(const void* Q, int ldq, int q_col0, const void* K,
                               int o_col0, int L, int n_heads, int q_per_kv, float scale, int mode,
                               int Lp, int Lmax, int blk, void* stream);
 
+/* Backward-pass operators (grpo.cpp:122-223 carried through
+ * the transformer-shaped model). Same argument conventions as above.
+ *
+ * Attention forward that also writes the per-(head, row) log-sum-exp the
+ * backward needs: lse[h*lse_ld + q] = log2 sum_k 2^(s_qk * scale * log2 e). */
+mrsp_status mrsp_op_attention_lse(const void* Q, int ldq, int q_col0, const void* K, int ldk,
+                                  int k_col0, const void* V, int ldv, int v_col0, void* O,
+                                  int ldo, int o_col0, int L, int n_heads, int q_per_kv,
+                                  float scale, int Lp, int Lmax, float* lse, int lse_ld,
+                                  void* stream);
+/* Attention backward (MR-SP causal-prefix mask, head dim 128): qkv [L][ld_qkv]
+ * post-RoPE (q heads at q_col0 + 128h, kv heads at k_col0 / v_col0 + 128g),
+ * O / dO [L][..] (head h at 128h), lse from mrsp_op_attention_lse, D a
+ * [n_heads][ld_stat] fp32 workspace; dq / dk / dv land in dqkv at the qkv
+ * column layout. Deterministic (no atomics). */
+mrsp_status mrsp_op_attention_bwd(const void* qkv, int ld_qkv, int q_col0, int k_col0, int v_col0,
+                                  const void* O, int ld_o, const void* dO, int ld_do,
+                                  const float* lse, float* D, int ld_stat, void* dqkv,
+                                  int ld_dqkv, int L, int n_heads, int q_per_kv, float scale,
+                                  int Lp, int Lmax, void* stream);
+/* RMSNorm backward: dx_acc[row] += dL/dx (x fp32, dy fp32), dw_out[d] = dL/dw
+ * (may be NULL); rows (may be NULL) maps row i of dy to the x / dx_acc row. */
+mrsp_status mrsp_op_rmsnorm_bwd(const float* x, int ldx, const float* w, const float* dy, int ldy,
+                                float* dx_acc, int ld_dx, int n, int d, float eps,
+                                const int32_t* rows, float* dw_out, void* stream);
+/* SwiGLU backward fused into the gate/up GEMM (GEMM_EPI_SWIGLU_BWD): X [M][K],
+ * W_gu [N][K] ([gate128 | up128] row blocks), dA [M][N/2] -> dGU [M][N] and the
+ * forward output act [M][N/2] (bf16). */
+mrsp_status mrsp_op_gemm_swiglu_bwd(const void* X, const void* W_gu, const void* dA, void* dGU,
+                                    void* act, int M, int N, int K, void* stream);
+/* dJ/dlogits of the GRPO objective from both models' final hidden rows, one
+ * vocabulary tile at a time (never the [M x V] fp32 logits):
+ * G[t][v] = pi (kw (lp - lq - kl_t) - coef_t) + coef_t [v == y_t], bf16 [M][ldg].
+ * lse_*: per-row log-partitions (natural log). */
+mrsp_status mrsp_op_lmhead_dual_dlogits(const void* X_policy, const void* W_policy,
+                                        const void* X_ref, const void* W_ref, int M, int V, int K,
+                                        const int32_t* targets, const float* coef, float kw,
+                                        const float* kl, const float* lse_policy,
+                                        const float* lse_ref, void* G, int ldg, void* stream);
+
 /* ------------------------------------------------------------------------
  * The MR-SP engine (transformer-shaped model; BASELINE.json configs c1..c5).
  *
@@ -328,6 +383,25 @@ mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id, const int
                                  int n_q, int G, int max_len, float temperature, uint64_t seed,
                                  int32_t* tokens_out, int32_t* lengths_out,
                                  float* old_logprobs_out);
+
+/* GRPO gradient of the policy LLM through the MR-SP prefill (
+ * grpo_gradient, grpo.cpp:122-206, with the exact or k3 KL): the video must
+ * be encoded (mrsp_engine_encode / _step). Runs the reference and policy
+ * passes, the fused dual LM head, then the backward of the LM head and every
+ * decoder layer (recomputed from its kept input) into fp32 gradients held by
+ * the engine (mrsp_engine_save_grads). old_logprobs: sum(lengths) host floats
+ * (row-major), advantages: G host floats; stats4 (host) = {objective, mean_kl,
+ * clip_fraction, token_count}; logprob_policy (host, may be NULL). SP = 1
+ * engines; the vision tower and projector are frozen. */
+mrsp_status mrsp_engine_grpo_backward(mrsp_engine* e, const char* video_id,
+                                      const int32_t* question, int n_q, const int32_t* resp,
+                                      const int32_t* lengths, int G, int Lmax,
+                                      const float* old_logprobs, const float* advantages,
+                                      double clip_eps, double kl_beta, int sampled_kl,
+                                      double* stats4, float* logprob_policy);
+/* The last mrsp_engine_grpo_backward's gradients as F32 safetensors under the
+ * policy's tensor names (model.layers.N.*, model.embed_tokens.weight, ...). */
+mrsp_status mrsp_engine_save_grads(mrsp_engine* e, const char* path);
 
 /* Weights as safetensors with Hugging Face tensor names (SigLIP
  * vision_model.*, projector mm_projector.{0,2}.*, Qwen2 model.* / lm_head.weight;

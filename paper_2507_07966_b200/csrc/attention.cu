@@ -41,13 +41,14 @@
 #include "common.h"
 #include "sm100.cuh"
 #include "tma.h"
+#include "attn_common.cuh"
 
 namespace mrsp {
 namespace {
 
 using namespace sm100;
+using namespace attn_detail;
 
-constexpr int TQ = 128, TK = 128, HD = 128;
 static_assert(2 * TQ == ATTN_ROW_BLOCK, "a CTA's query block is the row-split unit");
 constexpr int CHUNK = 128 * 64 * 2;  // one 128-row x 64-col bf16 SW128 block (16 KB)
 constexpr int TILE = 2 * CHUNK;      // a 128 x 128 bf16 operand (32 KB)
@@ -59,33 +60,6 @@ constexpr size_t SMEM_BYTES = 1024 + OFF_BAR + 256;
 constexpr int THREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;  // S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
-
-struct MaskDev {
-  int mode, L, Lp, Lmax, blk;
-};
-
-__device__ __forceinline__ int seg_of(int x, const MaskDev& m) { return (x - m.Lp) / m.Lmax; }
-
-// 0 = skip, 1 = fully visible, 2 = needs the element mask.
-__device__ __forceinline__ int tile_class(int q0, int kt, const MaskDev& m) {
-  const int k0 = kt * TK, klast = k0 + TK - 1, qlast = q0 + TQ - 1;
-  if (k0 >= m.L || q0 >= m.L) return 0;
-  if (m.mode == ATTN_BLOCK_DIAG) {
-    const int kb0 = k0 / m.blk, kb1 = min(klast, m.L - 1) / m.blk;
-    const int qb0 = q0 / m.blk, qb1 = qlast / m.blk;
-    if (kb1 < qb0 || kb0 > qb1) return 0;
-    return (kb0 == kb1 && qb0 == qb1 && kb0 == qb0 && klast < m.L) ? 1 : 2;
-  }
-  if (k0 > qlast) return 0;
-  if (klast >= m.L) return 2;
-  if (klast < m.Lp) return klast <= q0 ? 1 : 2;
-  if (k0 < m.Lp) return 2;  // straddles the prefix / rows boundary
-  if (qlast < m.Lp) return 0;
-  const int sk0 = seg_of(k0, m), sk1 = seg_of(klast, m);
-  const int qs0 = seg_of(max(q0, m.Lp), m), qs1 = seg_of(qlast, m);
-  if (sk1 < qs0 || sk0 > qs1) return 0;
-  return (sk0 == sk1 && qs0 == qs1 && sk0 == qs0 && q0 >= m.Lp && klast <= q0) ? 1 : 2;
-}
 
 // KV tile range covering both query tiles [q0, q0 + 256).
 __device__ __forceinline__ void kt_range(int q0, const MaskDev& m, int n_kt, int& lo, int& hi) {
@@ -124,6 +98,8 @@ struct AttnArgs {
   int n_dst, dst_ld, dst_col0;  // fused O scatter (AttnParams)
   long dst_bounds[9];
   __nv_bfloat16* dst_base[8];
+  float* lse;  // optional [heads][lse_ld] (scaled log2 domain)
+  int lse_ld;
 };
 
 // Destination row of query row q, head h: O itself, or the owner shard's buffer.
@@ -194,30 +170,6 @@ __device__ int g_attn_trace_cta;
 #define ATRACE_FINISH
 #endif
 
-// Packed fp32x2 FMA / add / sub (FFMA2 / FADD2 on sm_100a): half the issue slots.
-__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1,
-                                      float c0, float c1) {
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1) {
-  asm("{\n\t.reg .b64 ra, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rd, {%0, %1};\n\t"
-      "add.rn.f32x2 rd, rd, ra;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "+f"(d0), "+f"(d1)
-      : "f"(a0), "f"(a1));
-}
-__device__ __forceinline__ void fsub2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-
 // (2^x0, 2^x1) on the FMA pipe, packed: x = j + f with j = round(x) taken from
 // the low mantissa bits of x + 1.5*2^23, f in [-0.5, 0.5], degree-3 minimax
 // polynomial for 2^f (max rel. error 7.7e-5, far below bf16's 3.9e-3), then j
@@ -248,27 +200,6 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float& p0, float&
 template <int kPoly>
 __device__ __forceinline__ constexpr bool poly_pair(int i) {
   return kPoly > 0 && ((i + 1) * kPoly) / 32 != (i * kPoly) / 32;
-}
-
-// bit j set iff base + j < bound (j in [0, 32)).
-__device__ __forceinline__ uint32_t lt_bits(int bound, int base) {
-  const int n = bound - base;
-  return n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : (1u << n) - 1u);
-}
-
-__device__ __forceinline__ float exp2_mufu(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-template <uint32_t kRegs>
-__device__ __forceinline__ void reg_alloc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
-}
-template <uint32_t kRegs>
-__device__ __forceinline__ void reg_dealloc() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (0 = all MUFU).
@@ -572,6 +503,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // epilogue: O / l -> bf16 global
     const bool row_ok = q < a.mask.L;
     __nv_bfloat16* orow = row_ok ? out_row(a, q, h) : nullptr;
+    if (a.lse != nullptr && row_ok)
+      a.lse[static_cast<size_t>(h) * a.lse_ld + q] = l_run > 0.f ? m_run + log2f(l_run) : INFINITY;
     if (it > 0) {
       mbar_wait(&pv_done[t], (it - 1) & 1);
       tc_fence_after();
@@ -670,6 +603,10 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   a.dst_col0 = p.dst_col0;
   for (int i = 0; i < 9; ++i) a.dst_bounds[i] = p.dst_bounds[i];
   for (int i = 0; i < 8; ++i) a.dst_base[i] = static_cast<__nv_bfloat16*>(p.dst_base[i]);
+  a.lse = p.lse;
+  a.lse_ld = p.lse_ld;
+  MRSP_REQUIRE(p.lse == nullptr || p.lse_ld >= p.L, MRSP_INVALID_ARGUMENT,
+               "attention: lse row pitch shorter than L");
   MRSP_REQUIRE(p.row_parts >= 1 && p.row_part >= 0 && p.row_part < p.row_parts,
                MRSP_INVALID_ARGUMENT, "attention: bad query-row split");
   a.row_parts = p.row_parts;

@@ -34,6 +34,11 @@ struct AttnParams {
   // such as SigLIP's 72: the tiles are zero-filled to 128 on chip and only hs
   // output columns are written).
   int hstride = 128;
+  // Optional log-sum-exp per (head, query row) for the backward pass, in the
+  // kernel's scaled log2 domain: lse[h * lse_ld + q] = log2 sum_k 2^(s_qk *
+  // scale * log2 e) (+inf for a row with no visible key).
+  float* lse = nullptr;
+  int lse_ld = 0;
 };
 
 void attention_fwd(const AttnParams& p, cudaStream_t stream);

@@ -1,0 +1,876 @@
+// backward.cu — the backward pass of the transformer-shaped MR-SP prefill
+// ("backward through the SP prefill (GRPO/SFT gradients)";
+// the reference differentiates its toy policy analytically, grpo.cpp:122-223
+// through the GradAccumulator of policy.cpp:195-260 — here the same GRPO
+// objective is differentiated through the Qwen-shaped decoder stack).
+//
+// Attention backward (head dim 128, the MR-SP causal-prefix mask), as two
+// tcgen05 kernels so that every output is written once and the result is
+// deterministic (no atomics; SP = k stays bit-identical to SP = 1):
+//
+//   attn_bwd_dq    one CTA per (128-query tile, query head), sweeping the KV
+//                  tiles it sees:  S = Q K^T, dP = dO V^T (TMEM), then per
+//                  element P = 2^(S scale log2e - lse), dS = P (dP - D) packed
+//                  bf16 back into TMEM, and dQ += dS K (A operand from TMEM,
+//                  K read MN-major from the same smem tile). dQ = scale dQ.
+//   attn_bwd_dkdv  one CTA per (128-key tile, kv head), sweeping the q_per_kv
+//                  query heads x the query tiles that see it:  S^T = K Q^T,
+//                  dP^T = V dO^T, P^T and dS^T packed into TMEM, then
+//                  dV += P^T dO and dK += dS^T Q (dO, Q read MN-major).
+//                  TMEM = S^T | dP^T | dV | dK (512 columns).
+//
+// lse is the forward kernel's per-row log-sum-exp (scaled log2 domain,
+// AttnParams::lse), D = rowsum(dO o O) (attn_bwd_prep). Roles as in the
+// forward kernel: warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warps 4-11 two warpgroups that each take one 64-column half of the tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "attn_common.cuh"
+#include "backward.h"
+#include "common.h"
+#include "gemm.h"
+#include "sm100.cuh"
+#include "tma.h"
+
+namespace mrsp {
+namespace {
+
+using namespace sm100;
+using namespace attn_detail;
+
+constexpr int CHUNK = 128 * 64 * 2;  // 128 rows x 64 bf16 columns, SW128 (16 KB)
+constexpr int TILE = 2 * CHUNK;      // 128 x 128 bf16 (32 KB)
+constexpr int THREADS = 384;
+
+struct BwdArgs {
+  int L, Lp, Lmax, n_heads, q_per_kv;
+  int q_col0, k_col0, v_col0;  // columns of head 0 in qkv (and in dqkv)
+  float scale, scale_log2;
+  const float* lse;  // [n_heads][ld_stat]
+  const float* D;
+  int ld_stat;
+  __nv_bfloat16* dqkv;
+  int ld_dqkv;
+};
+
+__device__ __forceinline__ MaskDev mask_of(const BwdArgs& a) {
+  return MaskDev{ATTN_CAUSAL_PREFIX, a.L, a.Lp, a.Lmax, 1};
+}
+
+// K-major SW128 operand: 16-element K step kk of a 128 x 128 tile (two 64-col chunks)
+__device__ __forceinline__ uint32_t kmajor_off(int kk) { return (kk / 4) * CHUNK + (kk % 4) * 32; }
+
+// ----------------------------------------------------------------------------
+// dQ: one CTA per (query tile, query head). Work order: kv-head-major, then the
+// query tiles heaviest (longest key sweep) first, then the heads of the group.
+constexpr int DQ_RING = 4;  // K / V single-tile slots
+constexpr int DQ_OFF_Q = 0, DQ_OFF_DO = TILE, DQ_OFF_RING = 2 * TILE;
+constexpr int DQ_OFF_BAR = DQ_OFF_RING + DQ_RING * TILE;
+constexpr size_t DQ_SMEM = 1024 + DQ_OFF_BAR + 256;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dq(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DQ_OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* r_full = bars + 1;              // [DQ_RING]
+  uint64_t* r_empty = bars + 1 + DQ_RING;   // [DQ_RING]
+  uint64_t* s_full = bars + 1 + 2 * DQ_RING;
+  uint64_t* ds_full = s_full + 1;
+  uint64_t* dq_done = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+
+  const int warp = warp_id();
+  const MaskDev m = mask_of(a);
+  const int n_qt = (a.L + TQ - 1) / TQ, n_kt = (a.L + TK - 1) / TK;
+  const int per_kv = n_qt * a.q_per_kv;
+  const int kvh = blockIdx.x / per_kv;
+  const int rem = blockIdx.x - kvh * per_kv;
+  const int qt = n_qt - 1 - rem / a.q_per_kv;
+  const int h = kvh * a.q_per_kv + rem % a.q_per_kv;
+  const int q0 = qt * TQ;
+  const int kt_hi = min(n_kt, (q0 + TQ - 1) / TK + 1);
+  auto next = [&](int& kt) {  // next visible KV tile at or after kt (class, 0 = done)
+    for (; kt < kt_hi; ++kt) {
+      const int c = tile_class(q0, kt, m);
+      if (c) return c;
+    }
+    return 0;
+  };
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < DQ_RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 256);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S [0,128) dP [128,256) dQ [256,384)
+
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(q_full, 2 * TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + DQ_OFF_Q + c * CHUNK, &tmQKV, q_full, a.q_col0 + h * HD + c * 64, q0);
+          tma_load_2d(smem + DQ_OFF_DO + c * CHUNK, &tmDO, q_full, h * HD + c * 64, q0);
+        }
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int kt = 0; next(kt); ++kt) {
+          for (int kv = 0; kv < 2; ++kv) {  // K_j then V_j
+            mbar_wait(&r_empty[slot], ph ^ 1);
+            mbar_arrive_expect_tx(&r_full[slot], TILE);
+            const int col = (kv ? a.v_col0 : a.k_col0) + kvh * HD;
+            uint8_t* dst = smem + DQ_OFF_RING + slot * TILE;
+            tma_load_2d(dst, &tmQKV, &r_full[slot], col, kt * TK);
+            tma_load_2d(dst + CHUNK, &tmQKV, &r_full[slot], col + 64, kt * TK);
+            if (++slot == DQ_RING) { slot = 0; ph ^= 1; }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TQ, TK);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
+      const uint32_t q_addr = smem_u32(smem + DQ_OFF_Q), do_addr = smem_u32(smem + DQ_OFF_DO);
+      const uint32_t ring = smem_u32(smem + DQ_OFF_RING);
+      mbar_wait(q_full, 0);
+      int slot = 0, it = 0;
+      uint32_t ph = 0;
+      for (int kt = 0; next(kt); ++kt, ++it) {
+        const int ks = slot;
+        mbar_wait(&r_full[ks], ph);
+        if (++slot == DQ_RING) { slot = 0; ph ^= 1; }
+        const int vs = slot;
+        mbar_wait(&r_full[vs], ph);
+        if (++slot == DQ_RING) { slot = 0; ph ^= 1; }
+        const uint32_t k_addr = ring + ks * TILE, v_addr = ring + vs * TILE;
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem, sdesc_sw128(q_addr + kmajor_off(kk)),
+                        sdesc_sw128(k_addr + kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem + 128, sdesc_sw128(do_addr + kmajor_off(kk)),
+                        sdesc_sw128(v_addr + kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(s_full);
+          mma_commit(&r_empty[vs]);
+        }
+        __syncwarp();
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          // dQ += dS . K: dS packed bf16 in S columns [0,32) (keys 0-63) and
+          // [64,96) (keys 64-127); K_j read MN-major (hd contiguous)
+#pragma unroll
+          for (int kk = 0; kk < TK / 16; ++kk)
+            mma_bf16_ts(tmem + 256, tmem + (kk / 4) * 64 + (kk % 4) * 8,
+                        sdesc_sw128_mn(k_addr + kk * 2048, CHUNK), idesc_o,
+                        (it > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&r_empty[ks]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(dq_done);
+      __syncwarp();
+    }
+  } else {
+    reg_alloc<200>();
+    const int hf = (warp - 4) >> 2;     // key half of the tile this warpgroup handles
+    const int ew = (warp - 4) & 3;      // TMEM lane quarter
+    const int r = ew * 32 + lane_id();  // query row in the tile
+    const int q = q0 + r;
+    const bool row_ok = q < a.L;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const float lse = row_ok ? a.lse[static_cast<size_t>(h) * a.ld_stat + q] : INFINITY;
+    const float Dq = row_ok ? a.D[static_cast<size_t>(h) * a.ld_stat + q] : 0.f;
+    const float sl2 = a.scale_log2;
+    const int k_end = min(q + 1, a.L), k_mid = a.Lp;
+    const int k_lo = q >= a.Lp ? a.Lp + seg_of(q, m) * a.Lmax : 0;
+    int it = 0;
+    for (int kt = 0;; ++kt, ++it) {
+      const int cls = next(kt);
+      if (!cls) break;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t s0[32], s1[32], d0[32], d1[32];
+      tmem_ld32(tmem + lane_off + hf * 64, s0);
+      tmem_ld32(tmem + lane_off + hf * 64 + 32, s1);
+      tmem_ld32(tmem + lane_off + 128 + hf * 64, d0);
+      tmem_ld32(tmem + lane_off + 128 + hf * 64 + 32, d1);
+      tmem_ld_wait();
+      const int kb = kt * TK + hf * 64;
+      uint32_t vis0 = 0xffffffffu, vis1 = 0xffffffffu;
+      if (cls == 2) {
+        vis0 = lt_bits(k_end, kb) & (lt_bits(k_mid, kb) | ~lt_bits(k_lo, kb));
+        vis1 = lt_bits(k_end, kb + 32) & (lt_bits(k_mid, kb + 32) | ~lt_bits(k_lo, kb + 32));
+      }
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float p[4], g[4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * i + e;
+          p[e] = ((vis0 >> j) & 1u) ? exp2_mufu(__uint_as_float(s0[j]) * sl2 - lse) : 0.f;
+          p[2 + e] = ((vis1 >> j) & 1u) ? exp2_mufu(__uint_as_float(s1[j]) * sl2 - lse) : 0.f;
+          g[e] = p[e] * (__uint_as_float(d0[j]) - Dq);
+          g[2 + e] = p[2 + e] * (__uint_as_float(d1[j]) - Dq);
+        }
+        w[i] = pack_bf16(g[0], g[1]);
+        w[16 + i] = pack_bf16(g[2], g[3]);
+      }
+      tmem_st32(tmem + lane_off + hf * 64, w);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    // epilogue: dQ (scaled) -> bf16, this warpgroup's 64 head columns
+    __nv_bfloat16* out = a.dqkv + static_cast<size_t>(q) * a.ld_dqkv + a.q_col0 + h * HD + hf * 64;
+    if (it > 0) {
+      mbar_wait(dq_done, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + 256 + hf * 64 + c, o);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * a.scale, __uint_as_float(o[2 * j + 1]) * a.scale);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+    } else if (row_ok) {
+      for (int c = 0; c < 64; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ----------------------------------------------------------------------------
+// dK, dV: one CTA per (key tile, kv head), key tiles in ascending order (the
+// prefix keys, seen by every later query, are the heaviest).
+constexpr int KV_RING = 2;                       // (Q_i, dO_i, lse_i, D_i) stages
+constexpr int KV_STAT = 2 * 128 * 4;             // lse + D of one query tile
+constexpr int KV_STAGE = 2 * TILE + KV_STAT;     // 64 KB + 1 KB
+constexpr int KV_OFF_K = 0, KV_OFF_V = TILE, KV_OFF_RING = 2 * TILE;
+constexpr int KV_OFF_BAR = KV_OFF_RING + KV_RING * KV_STAGE;
+constexpr size_t KV_SMEM = 1024 + KV_OFF_BAR + 256;
+static_assert(KV_STAGE % 1024 == 0, "stages stay 1024-byte aligned (SW128 atoms)");
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dkdv(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                  const __grid_constant__ CUtensorMap tmLSE, const __grid_constant__ CUtensorMap tmD,
+                  BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KV_OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* r_full = bars + 1;             // [KV_RING]
+  uint64_t* r_empty = bars + 1 + KV_RING;  // [KV_RING]
+  uint64_t* s_full = bars + 1 + 2 * KV_RING;
+  uint64_t* ds_full = s_full + 1;
+  uint64_t* acc_done = s_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 3);
+
+  const int warp = warp_id();
+  const MaskDev m = mask_of(a);
+  const int n_qt = (a.L + TQ - 1) / TQ, n_kt = (a.L + TK - 1) / TK;
+  const int kvh = blockIdx.x / n_kt;
+  const int kt = blockIdx.x - kvh * n_kt;
+  const int k0 = kt * TK;
+  // query tiles that can see this key tile: from the diagonal up to the end of
+  // the sequence (prefix keys) or of the last key's rollout row
+  const int klast = min(k0 + TK - 1, a.L - 1);
+  const int q_end = klast < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(klast, m) + 1) * a.Lmax);
+  const int qt_lo = k0 / TQ, qt_hi = min(n_qt, (q_end + TQ - 1) / TQ);
+  const int n_items = (qt_hi - qt_lo) * a.q_per_kv;  // (head, query tile), head-minor
+  auto next = [&](int& i, int& hh, int& qt) {  // next visible item at or after i
+    for (; i < n_items; ++i) {
+      qt = qt_lo + i / a.q_per_kv;
+      hh = i % a.q_per_kv;
+      const int c = tile_class(qt * TQ, kt, m);
+      if (c) return c;
+    }
+    return 0;
+  };
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmLSE);
+    tma_prefetch_desc(&tmD);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < KV_RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 256);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
+
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + KV_OFF_K + c * CHUNK, &tmQKV, kv_full, a.k_col0 + kvh * HD + c * 64, k0);
+          tma_load_2d(smem + KV_OFF_V + c * CHUNK, &tmQKV, kv_full, a.v_col0 + kvh * HD + c * 64, k0);
+        }
+        int slot = 0;
+        uint32_t ph = 0;
+        int hh, qt;
+        for (int i = 0; next(i, hh, qt); ++i) {
+          const int h = kvh * a.q_per_kv + hh;
+          mbar_wait(&r_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&r_full[slot], KV_STAGE);
+          uint8_t* st = smem + KV_OFF_RING + slot * KV_STAGE;
+          for (int c = 0; c < 2; ++c) {
+            tma_load_2d(st + c * CHUNK, &tmQKV, &r_full[slot], a.q_col0 + h * HD + c * 64, qt * TQ);
+            tma_load_2d(st + TILE + c * CHUNK, &tmDO, &r_full[slot], h * HD + c * 64, qt * TQ);
+          }
+          tma_load_2d(st + 2 * TILE, &tmLSE, &r_full[slot], qt * TQ, h);
+          tma_load_2d(st + 2 * TILE + 512, &tmD, &r_full[slot], qt * TQ, h);
+          if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TK, TQ);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TK, HD);
+      const uint32_t k_addr = smem_u32(smem + KV_OFF_K), v_addr = smem_u32(smem + KV_OFF_V);
+      const uint32_t ring = smem_u32(smem + KV_OFF_RING);
+      mbar_wait(kv_full, 0);
+      int slot = 0, it = 0;
+      uint32_t ph = 0;
+      int hh, qt;
+      for (int i = 0; next(i, hh, qt); ++i, ++it) {
+        mbar_wait(&r_full[slot], ph);
+        tc_fence_after();
+        const uint32_t q_addr = ring + slot * KV_STAGE, do_addr = q_addr + TILE;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem, sdesc_sw128(k_addr + kmajor_off(kk)),
+                        sdesc_sw128(q_addr + kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem + 128, sdesc_sw128(v_addr + kmajor_off(kk)),
+                        sdesc_sw128(do_addr + kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(s_full);
+        }
+        __syncwarp();
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          // dV += P^T . dO, dK += dS^T . Q (A from TMEM, packed pairs in
+          // columns [0,32) + [64,96) of S^T / dP^T; B read MN-major)
+#pragma unroll
+          for (int kk = 0; kk < TQ / 16; ++kk) {
+            const uint32_t acol = (kk / 4) * 64 + (kk % 4) * 8;
+            mma_bf16_ts(tmem + 256, tmem + acol, sdesc_sw128_mn(do_addr + kk * 2048, CHUNK),
+                        idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_ts(tmem + 384, tmem + 128 + acol, sdesc_sw128_mn(q_addr + kk * 2048, CHUNK),
+                        idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&r_empty[slot]);
+        }
+        __syncwarp();
+        if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+      }
+      if (elect_one()) mma_commit(acc_done);
+      __syncwarp();
+    }
+  } else {
+    reg_alloc<200>();
+    const int hf = (warp - 4) >> 2;     // query half of the tile
+    const int ew = (warp - 4) & 3;
+    const int r = ew * 32 + lane_id();  // key row in the tile
+    const int k = k0 + r;
+    const bool row_ok = k < a.L;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const float sl2 = a.scale_log2;
+    // queries that see key k: [k, q_vis_end)
+    const int q_vis_end = !row_ok ? 0 : k < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(k, m) + 1) * a.Lmax);
+    int slot = 0, it = 0;
+    uint32_t ph = 0;
+    int hh, qt;
+    for (int i = 0; next(i, hh, qt); ++i, ++it) {
+      mbar_wait(&r_full[slot], ph);  // this stage's lse / D have landed
+      const float* st_lse = reinterpret_cast<const float*>(smem + KV_OFF_RING + slot * KV_STAGE + 2 * TILE);
+      const float* st_d = st_lse + 128;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t s0[32], s1[32], d0[32], d1[32];
+      tmem_ld32(tmem + lane_off + hf * 64, s0);
+      tmem_ld32(tmem + lane_off + hf * 64 + 32, s1);
+      tmem_ld32(tmem + lane_off + 128 + hf * 64, d0);
+      tmem_ld32(tmem + lane_off + 128 + hf * 64 + 32, d1);
+      tmem_ld_wait();
+      const int qb = qt * TQ + hf * 64;
+      // visible query columns: k <= q < q_vis_end
+      const uint32_t vis0 = lt_bits(q_vis_end, qb) & ~lt_bits(k, qb);
+      const uint32_t vis1 = lt_bits(q_vis_end, qb + 32) & ~lt_bits(k, qb + 32);
+      uint32_t wp[32], wd[32];
+#pragma unroll
+      for (int i2 = 0; i2 < 16; ++i2) {
+        float p[4], g[4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * i2 + e;
+          const int c0 = hf * 64 + j, c1 = c0 + 32;
+          p[e] = ((vis0 >> j) & 1u) ? exp2_mufu(__uint_as_float(s0[j]) * sl2 - st_lse[c0]) : 0.f;
+          p[2 + e] = ((vis1 >> j) & 1u) ? exp2_mufu(__uint_as_float(s1[j]) * sl2 - st_lse[c1]) : 0.f;
+          g[e] = p[e] * (__uint_as_float(d0[j]) - st_d[c0]);
+          g[2 + e] = p[2 + e] * (__uint_as_float(d1[j]) - st_d[c1]);
+        }
+        wp[i2] = pack_bf16(p[0], p[1]);
+        wp[16 + i2] = pack_bf16(p[2], p[3]);
+        wd[i2] = pack_bf16(g[0], g[1]);
+        wd[16 + i2] = pack_bf16(g[2], g[3]);
+      }
+      tmem_st32(tmem + lane_off + hf * 64, wp);
+      tmem_st32(tmem + lane_off + 128 + hf * 64, wd);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+      if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+    }
+    // epilogue: warpgroup 0 writes dV, warpgroup 1 dK (scaled)
+    const int col0 = (hf ? a.k_col0 : a.v_col0) + kvh * HD;
+    const float mul = hf ? a.scale : 1.0f;
+    __nv_bfloat16* out = a.dqkv + static_cast<size_t>(k) * a.ld_dqkv + col0;
+    if (it > 0) {
+      mbar_wait(acc_done, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+    } else if (row_ok) {
+      for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// D[h][q] = sum_c dO[q][128 h + c] * O[q][128 h + c] (fp32), one warp per (q, h).
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dO, int ldo,
+                                     const __nv_bfloat16* __restrict__ O, int ld_o, int L,
+                                     int n_heads, float* __restrict__ D, int ld_stat) {
+  const long w = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= static_cast<long>(L) * n_heads) return;
+  const int q = static_cast<int>(w / n_heads), h = static_cast<int>(w % n_heads);
+  const uint2 g = *reinterpret_cast<const uint2*>(dO + static_cast<size_t>(q) * ldo + h * 128 + lane * 4);
+  const uint2 o = *reinterpret_cast<const uint2*>(O + static_cast<size_t>(q) * ld_o + h * 128 + lane * 4);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float2 a = __bfloat1622float2(g2[i]), b = __bfloat1622float2(o2[i]);
+    s = fmaf(a.x, b.x, s);
+    s = fmaf(a.y, b.y, s);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) D[static_cast<size_t>(h) * ld_stat + q] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise / reduction kernels of the backward pass (HBM-bound).
+constexpr int NORM_ROWS = 64;  // rows per CTA (one dw partial per chunk)
+constexpr int NORM_MAXC = 16;  // columns per thread: d <= 16 * 256
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red may still be read by a previous call
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];  // fixed order
+  return t;
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(
+    const float* __restrict__ x, int ldx, const float* __restrict__ w, const float* __restrict__ dy,
+    int ldy, float* __restrict__ dx, int ld_dx, int n, int d, float eps, const int* __restrict__ rows,
+    float* __restrict__ dw_part) {
+  __shared__ float red[8];
+  float dwp[NORM_MAXC];
+#pragma unroll
+  for (int t = 0; t < NORM_MAXC; ++t) dwp[t] = 0.f;
+  const int r0 = blockIdx.x * NORM_ROWS, r1 = min(n, r0 + NORM_ROWS);
+  for (int i = r0; i < r1; ++i) {
+    const long row = rows ? rows[i] : i;
+    const float* xr = x + row * ldx;
+    const float* gr = dy + static_cast<long>(i) * ldy;
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int t = 0; t < NORM_MAXC; ++t) {
+      const int j = threadIdx.x + 256 * t;
+      if (j < d) {
+        const float xv = xr[j];
+        ss = fmaf(xv, xv, ss);
+        dot = fmaf(w[j] * gr[j], xv, dot);
+      }
+    }
+    ss = block_sum(ss, red);
+    dot = block_sum(dot, red);
+    const float r = rsqrtf(ss / static_cast<float>(d) + eps);
+    const float c = r * r * r * dot / static_cast<float>(d);
+    float* dr = dx + row * ld_dx;
+#pragma unroll
+    for (int t = 0; t < NORM_MAXC; ++t) {
+      const int j = threadIdx.x + 256 * t;
+      if (j < d) {
+        const float xv = xr[j], g = gr[j];
+        dr[j] += r * w[j] * g - xv * c;
+        dwp[t] = fmaf(g * xv, r, dwp[t]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NORM_MAXC; ++t) {
+    const int j = threadIdx.x + 256 * t;
+    if (j < d) dw_part[static_cast<size_t>(blockIdx.x) * d + j] = dwp[t];
+  }
+}
+
+// out[c] = sum over chunks of part[chunk][c], chunks in order (deterministic)
+__global__ void chunk_sum_kernel(const float* __restrict__ part, int n_chunks, int n_cols,
+                                 float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  float s = 0.f;
+  for (int k = 0; k < n_chunks; ++k) s += part[static_cast<size_t>(k) * n_cols + c];
+  out[c] = s;
+}
+
+constexpr int COLSUM_ROWS = 128;
+__global__ void colsum_part_kernel(const __nv_bfloat16* __restrict__ X, int ld, int n_rows,
+                                   int n_cols, float* __restrict__ part) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  const int r0 = blockIdx.y * COLSUM_ROWS, r1 = min(n_rows, r0 + COLSUM_ROWS);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += __bfloat162float(X[static_cast<size_t>(r) * ld + c]);
+  part[static_cast<size_t>(blockIdx.y) * n_cols + c] = s;
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, int ld_in,
+                                     __nv_bfloat16* __restrict__ out, int ld_out, int n_rows,
+                                     int n_cols) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int pairs = n_cols / 2;
+  if (i >= static_cast<long>(n_rows) * pairs) return;
+  const long r = i / pairs;
+  const int c = static_cast<int>(i % pairs) * 2;
+  const float2 v = *reinterpret_cast<const float2*>(in + r * ld_in + c);
+  *reinterpret_cast<__nv_bfloat162*>(out + r * ld_out + c) = __floats2bfloat162_rn(v.x, v.y);
+}
+
+__global__ void negate_i32_kernel(const int* __restrict__ in, int* __restrict__ out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = -in[i];
+}
+
+__global__ void embed_grad_kernel(const float* __restrict__ dh, int d, const int* __restrict__ seg_tok,
+                                  const int* __restrict__ seg_off, const int* __restrict__ positions,
+                                  float* __restrict__ dE) {
+  const int sg = blockIdx.x;
+  const int b = seg_off[sg], e = seg_off[sg + 1];
+  float* out = dE + static_cast<size_t>(seg_tok[sg]) * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int i = b; i < e; ++i) s += dh[static_cast<size_t>(positions[i]) * d + c];
+    out[c] = s;
+  }
+}
+
+__global__ void grpo_coeff_kernel(const float* __restrict__ lp, const float* __restrict__ old_lp,
+                                  const float* __restrict__ lp_ref, const float* __restrict__ adv,
+                                  const int* __restrict__ lengths, int G, int n_tokens,
+                                  double clip_eps, double beta, int sampled, float* __restrict__ coef) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  long off = 0;
+  for (int i = 0; i < g; ++i) off += lengths[i];
+  const double A = adv[g];
+  const double tok_w = 1.0 / (static_cast<double>(G) * lengths[g]);
+  const double kl_w = -beta / static_cast<double>(n_tokens);
+  for (int t = 0; t < lengths[g]; ++t) {
+    const double l = lp[off + t];
+    const double ratio = exp(l - static_cast<double>(old_lp[off + t]));
+    const bool plateau = (A > 0 && ratio > 1.0 + clip_eps) || (A < 0 && ratio < 1.0 - clip_eps);
+    double c = (A != 0.0 && !plateau) ? tok_w * A * ratio : 0.0;
+    if (sampled && beta != 0.0) c += kl_w * (1.0 - exp(static_cast<double>(lp_ref[off + t]) - l));
+    coef[off + t] = static_cast<float>(c);
+  }
+}
+
+}  // namespace
+
+void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
+  MRSP_REQUIRE(p.L > 0 && p.n_heads > 0 && p.q_per_kv > 0 && p.n_heads % p.q_per_kv == 0,
+               MRSP_INVALID_ARGUMENT, "attention_bwd: empty problem");
+  MRSP_REQUIRE(p.ld_qkv % 8 == 0 && p.ld_do % 8 == 0 && p.ld_o % 8 == 0 && p.ld_dqkv % 8 == 0 &&
+                   p.ld_stat % 4 == 0 && p.ld_stat >= p.L,
+               MRSP_INVALID_ARGUMENT, "attention_bwd: leading dims");
+  MRSP_REQUIRE(p.Lmax > 0 || p.Lp >= p.L, MRSP_INVALID_ARGUMENT, "attention_bwd: bad mask");
+  static const bool attr = [] {
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(DQ_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(KV_SMEM)));
+    return true;
+  }();
+  (void)attr;
+  // D = rowsum(dO o O) into the workspace p.D
+  {
+    const long warps = static_cast<long>(p.L) * p.n_heads;
+    attn_bwd_prep_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(p.dO), p.ld_do, static_cast<const __nv_bfloat16*>(p.O),
+        p.ld_o, p.L, p.n_heads, p.D, p.ld_stat);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+  }
+  BwdArgs a;
+  a.L = p.L;
+  a.Lp = p.Lp;
+  a.Lmax = p.Lmax > 0 ? p.Lmax : 1;
+  a.n_heads = p.n_heads;
+  a.q_per_kv = p.q_per_kv;
+  a.q_col0 = p.q_col0;
+  a.k_col0 = p.k_col0;
+  a.v_col0 = p.v_col0;
+  a.scale = p.scale;
+  a.scale_log2 = p.scale * 1.4426950408889634f;
+  a.lse = p.lse;
+  a.D = p.D;
+  a.ld_stat = p.ld_stat;
+  a.dqkv = static_cast<__nv_bfloat16*>(p.dqkv);
+  a.ld_dqkv = p.ld_dqkv;
+  CUtensorMap tqkv = make_tmap_bf16_2d(p.qkv, p.L, p.ld_qkv, p.ld_qkv, 128, 64);
+  CUtensorMap tdo = make_tmap_bf16_2d(p.dO, p.L, p.ld_do, p.ld_do, 128, 64);
+  CUtensorMap tlse = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap td = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const int n_qt = (p.L + TQ - 1) / TQ, n_kt = (p.L + TK - 1) / TK;
+  attn_bwd_dq<<<n_qt * p.n_heads, THREADS, DQ_SMEM, stream>>>(tqkv, tdo, a);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  attn_bwd_dkdv<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrsp
+
+namespace mrsp {
+
+size_t rmsnorm_bwd_workspace_bytes(int n, int d) {
+  return static_cast<size_t>((n + NORM_ROWS - 1) / NORM_ROWS) * d * 4 + 256;
+}
+
+void rmsnorm_bwd(const float* x, int ldx, const float* w, const float* dy, int ldy, float* dx_acc,
+                 int ld_dx, int n, int d, float eps, const int* rows, float* dw_out, void* ws,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  MRSP_REQUIRE(d <= NORM_MAXC * 256, MRSP_INVALID_ARGUMENT, "rmsnorm_bwd: d too large");
+  const int chunks = (n + NORM_ROWS - 1) / NORM_ROWS;
+  float* part = static_cast<float*>(ws);
+  rmsnorm_bwd_kernel<<<chunks, 256, 0, s>>>(x, ldx, w, dy, ldy, dx_acc, ld_dx, n, d, eps, rows, part);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  if (dw_out) {
+    chunk_sum_kernel<<<(d + 255) / 256, 256, 0, s>>>(part, chunks, d, dw_out);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+  }
+}
+
+size_t colsum_workspace_bytes(int n_rows, int n_cols) {
+  return static_cast<size_t>((n_rows + COLSUM_ROWS - 1) / COLSUM_ROWS) * n_cols * 4 + 256;
+}
+
+void colsum_bf16(const __nv_bfloat16* X, int ld, int n_rows, int n_cols, float* out, void* ws,
+                 cudaStream_t s) {
+  if (n_rows <= 0) {
+    MRSP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(n_cols) * 4, s));
+    return;
+  }
+  const int chunks = (n_rows + COLSUM_ROWS - 1) / COLSUM_ROWS;
+  float* part = static_cast<float*>(ws);
+  colsum_part_kernel<<<dim3((n_cols + 255) / 256, chunks), 256, 0, s>>>(X, ld, n_rows, n_cols, part);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  chunk_sum_kernel<<<(n_cols + 255) / 256, 256, 0, s>>>(part, chunks, n_cols, out);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void cast_f32_bf16(const float* in, int ld_in, __nv_bfloat16* out, int ld_out, int n_rows,
+                   int n_cols, cudaStream_t s) {
+  MRSP_REQUIRE(n_cols % 2 == 0 && ld_in % 2 == 0 && ld_out % 2 == 0, MRSP_INVALID_ARGUMENT,
+               "cast_f32_bf16: even widths");
+  const long n = static_cast<long>(n_rows) * (n_cols / 2);
+  if (n == 0) return;
+  cast_f32_bf16_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(in, ld_in, out, ld_out,
+                                                                             n_rows, n_cols);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void negate_i32(const int* in, int* out, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  negate_i32_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, out, n);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void embed_grad(const float* dh, int d, const int* seg_tok, const int* seg_off,
+                const int* positions, int n_seg, float* dE, cudaStream_t s) {
+  if (n_seg <= 0) return;
+  embed_grad_kernel<<<n_seg, 256, 0, s>>>(dh, d, seg_tok, seg_off, positions, dE);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void grpo_token_coeffs(const float* lp, const float* old_lp, const float* lp_ref,
+                       const float* adv, const int* lengths, int G, int n_tokens, double clip_eps,
+                       double kl_beta, int sampled_kl, float* coef, cudaStream_t s) {
+  if (G <= 0 || n_tokens <= 0) return;
+  grpo_coeff_kernel<<<(G + 127) / 128, 128, 0, s>>>(lp, old_lp, lp_ref, adv, lengths, G, n_tokens,
+                                                    clip_eps, kl_beta, sampled_kl, coef);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrsp
+
+using namespace mrsp;
+
+extern "C" mrsp_status mrsp_op_attention_lse(const void* Q, int ldq, int q_col0, const void* K,
+                                             int ldk, int k_col0, const void* V, int ldv,
+                                             int v_col0, void* O, int ldo, int o_col0, int L,
+                                             int n_heads, int q_per_kv, float scale, int Lp,
+                                             int Lmax, float* lse, int lse_ld, void* stream) {
+  return guard([&] {
+    require_device();
+    AttnParams p{Q, ldq, q_col0, K, ldk, k_col0, V, ldv, v_col0, O, ldo, o_col0,
+                 L, n_heads, q_per_kv, scale, ATTN_CAUSAL_PREFIX, Lp, Lmax, 0};
+    p.lse = lse;
+    p.lse_ld = lse_ld;
+    attention_fwd(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" mrsp_status mrsp_op_attention_bwd(const void* qkv, int ld_qkv, int q_col0, int k_col0,
+                                             int v_col0, const void* O, int ld_o, const void* dO,
+                                             int ld_do, const float* lse, float* D, int ld_stat,
+                                             void* dqkv, int ld_dqkv, int L, int n_heads,
+                                             int q_per_kv, float scale, int Lp, int Lmax,
+                                             void* stream) {
+  return guard([&] {
+    require_device();
+    AttnBwdParams p{qkv, ld_qkv, q_col0, k_col0, v_col0, O, ld_o, dO, ld_do, lse, D, ld_stat,
+                    dqkv, ld_dqkv, L, n_heads, q_per_kv, scale, Lp, Lmax};
+    attention_bwd(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" mrsp_status mrsp_op_rmsnorm_bwd(const float* x, int ldx, const float* w,
+                                           const float* dy, int ldy, float* dx_acc, int ld_dx,
+                                           int n, int d, float eps, const int32_t* rows,
+                                           float* dw_out, void* stream) {
+  return guard([&] {
+    require_device();
+    void* ws = nullptr;
+    const size_t b = rmsnorm_bwd_workspace_bytes(n, d);
+    MRSP_CUDA(cudaMallocAsync(&ws, b, static_cast<cudaStream_t>(stream)));
+    rmsnorm_bwd(x, ldx, w, dy, ldy, dx_acc, ld_dx, n, d, eps, rows, dw_out, ws,
+                static_cast<cudaStream_t>(stream));
+    MRSP_CUDA(cudaFreeAsync(ws, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+extern "C" mrsp_status mrsp_op_gemm_swiglu_bwd(const void* X, const void* W_gu, const void* dA,
+                                               void* dGU, void* act, int M, int N, int K,
+                                               void* stream) {
+  return guard([&] {
+    require_device();
+    GemmArgs g{X, W_gu, dGU, M, N, K, K, K, N, GEMM_EPI_SWIGLU_BWD, nullptr, nullptr, 0};
+    g.aux = dA;
+    g.ld_aux = N / 2;
+    g.aux_out = act;
+    g.ld_aux_out = N / 2;
+    gemm_bf16(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" mrsp_status mrsp_op_lmhead_dual_dlogits(const void* X_policy, const void* W_policy,
+                                                   const void* X_ref, const void* W_ref, int M,
+                                                   int V, int K, const int32_t* targets,
+                                                   const float* coef, float kw, const float* kl,
+                                                   const float* lse_policy, const float* lse_ref,
+                                                   void* G, int ldg, void* stream) {
+  return guard([&] {
+    require_device();
+    lmhead_dual_dlogits(X_policy, W_policy, X_ref, W_ref, M, V, K, targets, coef, kw, kl,
+                        lse_policy, lse_ref, G, ldg, static_cast<cudaStream_t>(stream));
+  });
+}

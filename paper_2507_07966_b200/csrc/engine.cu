@@ -470,18 +470,6 @@ void Engine::profile_read(int cls, double* ms, long* launches) {
 }
 
 // RAII timing scope for one kernel class.
-struct Prof {
-  Engine& e;
-  int cls;
-  cudaEvent_t a = nullptr;
-  Prof(Engine& en, int c) : e(en), cls(c) { e.prof_begin(cls, &a); }
-  ~Prof() {
-    if (a) e.prof_end(cls, a);
-  }
-};
-
-enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5,
-       P_DECODE_GRAPH = 6 };
 
 // ---------------------------------------------------------------------------
 // Stage 1 for one SP rank: frames [fb, fe) -> projector output rows.
@@ -969,6 +957,11 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
   int layer = -1;
   for (const auto& Lw : W.layers) {
     ++layer;
+    if (stash_) {  // backward: keep this layer's input (SP = 1)
+      const size_t nd = static_cast<size_t>(ranks_[0].e - ranks_[0].b) * d;
+      MRSP_CUDA(cudaMemcpyAsync(stash_ + layer * nd, ranks_[0].h.p, nd * 4,
+                                cudaMemcpyDeviceToDevice, s));
+    }
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
@@ -1786,6 +1779,31 @@ extern "C" mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id
     auto entry = lookup(e, video_id);
     e->impl->generate(*entry, question, n_q, G, max_len, temperature, seed, tokens_out,
                       lengths_out, old_logprobs_out);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_grpo_backward(mrsp_engine* e, const char* video_id,
+                                                 const int32_t* question, int n_q,
+                                                 const int32_t* resp, const int32_t* lengths, int G,
+                                                 int Lmax, const float* old_logprobs,
+                                                 const float* advantages, double clip_eps,
+                                                 double kl_beta, int sampled_kl, double* stats4,
+                                                 float* logprob_policy) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && resp && lengths && old_logprobs && advantages && stats4 &&
+                     (question || n_q == 0),
+                 MRSP_INVALID_ARGUMENT, "grpo_backward: null argument");
+    MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "grpo: empty rollout group");  // grpo.cpp:60
+    auto entry = lookup(e, video_id);
+    e->impl->grpo_backward(*entry, question, n_q, resp, lengths, G, Lmax, old_logprobs, advantages,
+                           clip_eps, kl_beta, sampled_kl, stats4, logprob_policy);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_save_grads(mrsp_engine* e, const char* path) {
+  return guard([&] {
+    MRSP_REQUIRE(e && path, MRSP_INVALID_ARGUMENT, "save_grads: null argument");
+    e->impl->save_grads(path);
   });
 }
 

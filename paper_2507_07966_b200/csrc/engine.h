@@ -168,6 +168,23 @@ class Engine {
   std::shared_ptr<CacheEntry> cache_load(const std::string& id, const std::string& path);
   int cache_capacity = 0;  // 0 = unbounded
 
+  // GRPO gradient of the policy LLM (grpo_gradient,
+  // grpo.cpp:122-206, through the transformer-shaped decoder): both prefill
+  // passes (the policy's with its layer inputs kept), the fused dual LM head,
+  // then the backward of the LM head, the final norm, every decoder layer
+  // (recomputed from its kept input) and the text embeddings. The vision tower
+  // and projector are frozen (the reference differentiates only the policy).
+  // Host in: old_lp [sum(lengths)], adv [G]; host out: stats4 = {objective,
+  // mean_kl, clip_fraction, tokens}, optional lp [sum(lengths)]. Gradients
+  // stay on the device (grads_) until save_grads.
+  void grpo_backward(const CacheEntry& emb, const int32_t* question, int n_q,
+                     const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                     const float* old_lp, const float* adv, double clip_eps, double kl_beta,
+                     int sampled_kl, double* stats4, float* lp_out);
+  // the last grpo_backward's gradients as an F32 safetensors file (policy
+  // tensor names, csrc/weights_io.cpp)
+  void save_grads(const std::string& path);
+
   // profiling: CUDA-event time per kernel class
   void set_profiling(bool on);
   void profile_read(int cls, double* ms, long* launches);
@@ -184,6 +201,12 @@ class Engine {
   void prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
                      const int32_t* resp, const int32_t* lengths, int G, int Lmax);
   void run_pass(const CacheEntry& emb, int model, int xs_slot);
+  // backward: per-layer input hidden states kept by run_pass ([layers][n][d]
+  // fp32, SP = 1) and the fp32 gradients in the engine's weight layout
+  float* stash_ = nullptr;
+  DevBuf stash_buf_, grad_buf_, bwd_ws_;
+  LlmW grads_{};  // fp32 storage typed as the weight struct (see save_grads)
+  bool have_grads_ = false;
   // prefix K/V capture for generation (run_pass copies rows [0, Lp) of every
   // layer's post-RoPE K and V when set): [layers][Lp][2 n_kv 128] bf16
   DevBuf kv_prefix_;
@@ -271,5 +294,19 @@ class Engine {
 };
 
 std::array<std::array<int, 3>, 3> ulysses_blocks(int nq, int nkv, const HeadSplit& hs);
+
+// CUDA-event time of one kernel class while profiling is on (scoped).
+struct Prof {
+  Engine& e;
+  int cls;
+  cudaEvent_t a = nullptr;
+  Prof(Engine& en, int c) : e(en), cls(c) { e.prof_begin(cls, &a); }
+  ~Prof() {
+    if (a) e.prof_end(cls, a);
+  }
+};
+
+enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5,
+       P_DECODE_GRAPH = 6, P_BACKWARD = 7 };
 
 }  // namespace mrsp

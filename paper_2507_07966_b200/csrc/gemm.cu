@@ -79,6 +79,11 @@ struct EpiArgs {
   __nv_bfloat16* norm_out;
   int ld_norm;
   float norm_eps;
+  // GEMM_EPI_SWIGLU_BWD (GemmArgs::aux / aux_out)
+  const __nv_bfloat16* aux;
+  int ld_aux;
+  __nv_bfloat16* aux_out;
+  int ld_aux_out;
 };
 
 // Grouped raster: consecutive tiles sweep a GROUP_M-tall band of m-tiles with
@@ -212,6 +217,55 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
       ssum = acc_s;
     }
     if (row_ok) args.part[static_cast<size_t>(row) * n_tiles + nt] = make_float2(m, ssum);
+  } else if (args.epi == GEMM_EPI_SWIGLU_BWD) {
+    // SwiGLU backward: with s = sigmoid(g), silu(g) = g s, silu'(g) = s (1 + g (1 - s)),
+    //   dg = dA u silu'(g), du = dA silu(g)   -> C[:, nt*256 + j] | C[:, nt*256 + 128 + j]
+    // and the forward output silu(g) u (bit-identical to GEMM_EPI_SWIGLU_BF16) -> aux_out
+    __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
+    for (int c = 0; c < BN / 2; c += 32) {
+      uint32_t g[32], u[32];
+      tmem_ld32(t_row + c, g);
+      tmem_ld32(t_row + BN / 2 + c, u);
+      tmem_ld_wait();
+      const int col = nt * (BN / 2) + c;
+      if (row_ok) {
+        const uint4* da4 = reinterpret_cast<const uint4*>(args.aux + static_cast<size_t>(row) * args.ld_aux + col);
+        uint32_t dar[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 v = da4[j];
+          dar[4 * j] = v.x; dar[4 * j + 1] = v.y; dar[4 * j + 2] = v.z; dar[4 * j + 3] = v.w;
+        }
+        uint32_t og[16], ou[16], oa[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 da = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dar[j]));
+          float rg[2], ru[2], ra[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float gv = __uint_as_float(g[2 * j + e]), uv = __uint_as_float(u[2 * j + e]);
+            const float dv = e ? da.y : da.x;
+            const float sg = __fdividef(1.0f, 1.0f + __expf(-gv));
+            const float sl = silu(gv);
+            rg[e] = dv * uv * (sg * (1.0f + gv * (1.0f - sg)));
+            ru[e] = dv * sl;
+            ra[e] = sl * uv;
+          }
+          og[j] = pack_bf16(rg[0], rg[1]);
+          ou[j] = pack_bf16(ru[0], ru[1]);
+          oa[j] = pack_bf16(ra[0], ra[1]);
+        }
+        uint4* dg = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * BN + c);
+        uint4* du = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * BN + BN / 2 + c);
+        uint4* ac = reinterpret_cast<uint4*>(args.aux_out + static_cast<size_t>(row) * args.ld_aux_out + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dg[j] = make_uint4(og[4 * j], og[4 * j + 1], og[4 * j + 2], og[4 * j + 3]);
+          du[j] = make_uint4(ou[4 * j], ou[4 * j + 1], ou[4 * j + 2], ou[4 * j + 3]);
+          ac[j] = make_uint4(oa[4 * j], oa[4 * j + 1], oa[4 * j + 2], oa[4 * j + 3]);
+        }
+      }
+    }
   } else if (args.epi == GEMM_EPI_SWIGLU_BF16) {
     // columns [0,128) are gate, [128,256) the matching up projections
     __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
@@ -424,11 +478,21 @@ struct GemmCfg {
   static_assert(kARows == BM || kStageBytes >= A_BYTES, "MMA reads 128 A rows inside the stage");
 };
 
-template <int kStages, int kARows>
+// kMajor: bit 0 = A stored MN-major (A^T rows: element (m, k) at A[k * lda + m]),
+// bit 1 = B stored MN-major (element (n, k) at B[k * ldb + n]) — the backward
+// pass's dgrad (B = a weight read as its transpose) and wgrad (both operands
+// token-major) GEMMs. An MN-major operand tile is loaded as 64 x 64 boxes
+// (64 K rows x 128 bytes of M/N) and read through MN-major SW128 descriptors
+// (LBO = one 64-wide box, 8 KB); the instruction descriptor's transpose bits
+// tell the tensor core. kMajor 0 is the forward kernel, unchanged.
+constexpr int MN_BOX = 64 * 64 * 2;
+template <int kStages, int kARows, int kMajor = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
+  constexpr bool kAMN = (kMajor & 1) != 0, kBMN = (kMajor & 2) != 0;
+  static_assert(kMajor == 0 || kARows == BM, "MN-major operands: full tiles only");
   using Cfg = GemmCfg<kStages, kARows>;
   constexpr int STAGES = kStages;
   constexpr int STAGE_BYTES = Cfg::kStageBytes;
@@ -483,6 +547,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   // Without PDL both instructions are no-ops.
   pdl_trigger();
 
+  auto load_a = [&](uint8_t* dst, uint64_t* bar, int kb, int mt) {
+    if constexpr (kAMN) {
+#pragma unroll
+      for (int c = 0; c < BM / 64; ++c) tma_load_2d(dst + c * MN_BOX, &tmA, bar, mt * BM + c * 64, kb * BK);
+    } else {
+      tma_load_2d(dst, &tmA, bar, kb * BK, mt * BM);
+    }
+  };
+  auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int nt) {
+    if constexpr (kBMN) {
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tma_load_2d(dst + c * MN_BOX, &tmB, bar, nt * BN + c * 64, kb * BK);
+    } else {
+      tma_load_2d(dst, &tmB, bar, kb * BK, nt * BN);
+    }
+  };
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
@@ -493,7 +573,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         decode_tile(blockIdx.x, mt, nt, kb0, kb1);
         for (; pre < STAGES && kb0 + pre < kb1; ++pre) {
           mbar_arrive_expect_tx(&full[pre], STAGE_BYTES);  // stages start empty
-          tma_load_2d(smem + pre * STAGE_BYTES + A_STAGE, &tmB, &full[pre], (kb0 + pre) * BK, nt * BN);
+          load_b(smem + pre * STAGE_BYTES + A_STAGE, &full[pre], kb0 + pre, nt);
         }
       }
       pdl_wait();
@@ -503,19 +583,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           uint8_t* sa = smem + stage * STAGE_BYTES;
           if (pre > 0 && tile == static_cast<int>(blockIdx.x) && kb - kb0 < pre) {
-            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);  // B already in flight
+            load_a(sa, &full[stage], kb, mt);  // B already in flight
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mt * BM);
-            tma_load_2d(sa + A_STAGE, &tmB, &full[stage], kb * BK, nt * BN);
+            load_a(sa, &full[stage], kb, mt);
+            load_b(sa + A_STAGE, &full[stage], kb, nt);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_bf16_f32(BM, BN);
+    const uint32_t idesc =
+        idesc_bf16_f32(BM, BN) | (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -534,8 +615,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t b_addr = a_addr + A_STAGE;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            mma_bf16_ss(d_tmem, sdesc_sw128(a_addr + k * 32), sdesc_sw128(b_addr + k * 32), idesc,
-                        (kb != kb0 || k != 0) ? 1u : 0u);
+            // K-major: the 16-element K step is 32 bytes along the row; MN-major:
+            // 16 K rows of 128 bytes
+            const uint64_t ad = kAMN ? sdesc_sw128_mn(a_addr + k * 2048, MN_BOX)
+                                     : sdesc_sw128(a_addr + k * 32);
+            const uint64_t bd = kBMN ? sdesc_sw128_mn(b_addr + k * 2048, MN_BOX)
+                                     : sdesc_sw128(b_addr + k * 32);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
           if (kb == kb1 - 1) mma_commit(&tfull[acc]);
@@ -917,12 +1003,72 @@ constexpr int kSkinnyStages = 6, kSkinnyRows = 16;
 
 }  // namespace
 
+// Backward-pass GEMMs with MN-major operands (GemmArgs::a_mn / b_mn): the
+// default single-CTA kernel, plain epilogues (bf16 / fp32 stores, fp32
+// residual accumulate), staged TMA-store epilogue when aligned.
+bool gemm_bf16_mn(const GemmArgs& g, cudaStream_t stream) {
+  MRSP_REQUIRE(g.epi == GEMM_EPI_STORE_BF16 || g.epi == GEMM_EPI_STORE_F32 ||
+                   g.epi == GEMM_EPI_RESID_F32 || g.epi == GEMM_EPI_BIAS_BF16,
+               MRSP_INVALID_ARGUMENT, "gemm (MN-major operands): plain epilogues only");
+  using K1 = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, EpiArgs);
+  const int major = (g.a_mn ? 1 : 0) | (g.b_mn ? 2 : 0);
+  const K1 kern = major == 1 ? gemm_bf16_tcgen05<STAGES, BM, 1>
+                : major == 2 ? gemm_bf16_tcgen05<STAGES, BM, 2>
+                             : gemm_bf16_tcgen05<STAGES, BM, 3>;
+  static const bool attr_set = [] {
+    for (K1 k : {gemm_bf16_tcgen05<STAGES, BM, 1>, gemm_bf16_tcgen05<STAGES, BM, 2>,
+                 gemm_bf16_tcgen05<STAGES, BM, 3>})
+      MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(GemmCfg<STAGES, BM>::kSmem)));
+    return true;
+  }();
+  (void)attr_set;
+  CUtensorMap ta = g.a_mn ? make_tmap_bf16_2d(g.A, g.K, g.M, g.lda, BK, 64)
+                          : make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, BM, BK);
+  CUtensorMap tb = g.b_mn ? make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, BK, 64)
+                          : make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, BN, BK);
+  const bool f32_out = g.epi == GEMM_EPI_STORE_F32 || g.epi == GEMM_EPI_RESID_F32;
+  const uintptr_t out_addr = reinterpret_cast<uintptr_t>(g.epi == GEMM_EPI_RESID_F32 ? g.resid : g.C);
+  const int ld_out = g.epi == GEMM_EPI_RESID_F32 ? g.ldr : g.ldc;
+  const int vec_ok = (out_addr % 16 == 0) && (ld_out % (f32_out ? 4 : 8) == 0);
+  EpiArgs e{};
+  e.M = g.M;
+  e.N = g.N;
+  e.K = g.K;
+  e.epi = g.epi;
+  e.vec_ok = vec_ok;
+  e.k_splits = 1;
+  e.C = g.C;
+  e.ldc = g.ldc;
+  e.bias = g.bias;
+  e.resid = g.resid;
+  e.ldr = g.ldr;
+  CUtensorMap tc = ta;
+  if (vec_ok) {
+    tc = g.epi == GEMM_EPI_RESID_F32 ? make_tmap_f32_2d(g.resid, g.M, g.N, g.ldr, 32, 32)
+       : g.epi == GEMM_EPI_STORE_F32 ? make_tmap_f32_2d(g.C, g.M, g.N, g.ldc, 32, 32)
+                                     : make_tmap_bf16_2d(g.C, g.M, g.N, g.ldc, 32, 64);
+    e.staged = 1;
+  }
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  kern<<<std::min(tiles, num_sms()), THREADS, GemmCfg<STAGES, BM>::kSmem, stream>>>(ta, tb, tc, e);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+  return false;
+}
+
 bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
   MRSP_REQUIRE(g.M > 0 && g.N > 0 && g.K > 0, MRSP_INVALID_ARGUMENT, "gemm: empty problem");
-  MRSP_REQUIRE(g.K % 8 == 0 && g.lda % 8 == 0 && g.ldb % 8 == 0, MRSP_INVALID_ARGUMENT,
+  MRSP_REQUIRE((g.K % 8 == 0 || (g.a_mn && g.b_mn)) && g.lda % 8 == 0 && g.ldb % 8 == 0,
+               MRSP_INVALID_ARGUMENT,
                "gemm: K and leading dims must be multiples of 8 (16-byte TMA pitch)");
+  if (g.a_mn || g.b_mn) return gemm_bf16_mn(g, stream);
   if (g.epi == GEMM_EPI_SWIGLU_BF16)
     MRSP_REQUIRE(g.N % BN == 0, MRSP_INVALID_ARGUMENT, "gemm swiglu: N must be a multiple of 256");
+  if (g.epi == GEMM_EPI_SWIGLU_BWD)
+    MRSP_REQUIRE(g.N % BN == 0 && g.aux && g.aux_out && g.ld_aux % 8 == 0 &&
+                     g.ld_aux_out % 8 == 0 && g.ldc % 8 == 0,
+                 MRSP_INVALID_ARGUMENT, "gemm swiglu backward: bad arguments");
   if (g.epi == GEMM_EPI_RESID_F32)
     MRSP_REQUIRE(g.resid != nullptr, MRSP_INVALID_ARGUMENT, "gemm resid: null residual");
   static const bool attr_set = [] {  // thread-safe one-time setup (C-ABI callers may race)
@@ -953,7 +1099,9 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
             g.bias,  g.resid,   g.ldr,   g.targets, g.part,     g.tgt_logit,
             g.pos,   g.inv_freq, g.n_rope_blocks, g.row0, g.route, g.peer_base, g.peer_ld,
             g.row_blocks, GEMM_POST_NONE, static_cast<__nv_bfloat16*>(g.kv_rows), g.kvw, g.kv_col0, g.tdev,
-            g.norm_w, static_cast<__nv_bfloat16*>(g.norm_out), g.ld_norm, g.norm_eps};
+            g.norm_w, static_cast<__nv_bfloat16*>(g.norm_out), g.ld_norm, g.norm_eps,
+            static_cast<const __nv_bfloat16*>(g.aux), g.ld_aux,
+            static_cast<__nv_bfloat16*>(g.aux_out), g.ld_aux_out};
   if (g.post == GEMM_POST_ROPE_APPEND)
     MRSP_REQUIRE(g.epi == GEMM_EPI_BIAS_BF16 && g.N % 128 == 0 && g.pos && g.inv_freq &&
                      g.kv_rows && g.tdev && g.kvw % 128 == 0 && g.kv_col0 % 128 == 0,
@@ -1109,6 +1257,19 @@ extern "C" mrsp_status mrsp_op_gemm_bf16(const void* A, const void* B, void* C, 
   return mrsp::guard([&] {
     mrsp::require_device();
     mrsp::GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, epilogue, bias, resid, ldr};
+    mrsp::gemm_bf16(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" mrsp_status mrsp_op_gemm_bf16_mn(const void* A, const void* B, void* C, int M, int N,
+                                            int K, int lda, int ldb, int ldc, int a_mn, int b_mn,
+                                            int epilogue, const float* bias, float* resid, int ldr,
+                                            void* stream) {
+  return mrsp::guard([&] {
+    mrsp::require_device();
+    mrsp::GemmArgs g{A, B, C, M, N, K, lda, ldb, ldc, epilogue, bias, resid, ldr};
+    g.a_mn = a_mn;
+    g.b_mn = b_mn;
     mrsp::gemm_bf16(g, static_cast<cudaStream_t>(stream));
   });
 }

@@ -8,8 +8,8 @@
 namespace mrsp {
 
 struct GemmArgs {
-  const void* A;  // [M][lda] bf16, K-major
-  const void* B;  // [N][ldb] bf16, K-major (nn.Linear weight layout)
+  const void* A;  // [M][lda] bf16, K-major (a_mn: [K][lda], M contiguous)
+  const void* B;  // [N][ldb] bf16, K-major, the nn.Linear weight layout (b_mn: [K][ldb])
   void* C;        // output (bf16 or fp32 per epilogue)
   int M, N, K;
   int lda, ldb, ldc;
@@ -56,6 +56,16 @@ struct GemmArgs {
   void* norm_out = nullptr;
   int ld_norm = 0;
   float norm_eps = 0.f;
+  // MN-major operands (the backward GEMMs): dgrad dX = dY . W reads the weight
+  // [N_out][K_in] as an MN-major B; wgrad dW = dY^T . X reads both token-major
+  // activations as MN-major A and B. Plain epilogues, no split-K / skinny / pair.
+  int a_mn = 0, b_mn = 0;
+  // GEMM_EPI_SWIGLU_BWD: aux = dA [M][ld_aux] bf16 (gradient of the SwiGLU
+  // output), aux_out = the recomputed SwiGLU output [M][ld_aux_out] bf16.
+  const void* aux = nullptr;
+  int ld_aux = 0;
+  void* aux_out = nullptr;
+  int ld_aux_out = 0;
 };
 
 enum { GEMM_POST_NONE = 0, GEMM_POST_ROPE_APPEND = 1, GEMM_POST_RMSNORM = 2 };

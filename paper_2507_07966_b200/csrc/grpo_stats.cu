@@ -11,6 +11,7 @@
 // fixed-order reduction — deterministic.
 #include <cuda_runtime.h>
 
+#include "backward.h"
 #include "common.h"
 
 namespace mrsp {
@@ -63,6 +64,19 @@ __global__ void grpo_stats_kernel(const float* __restrict__ lp, const float* __r
 }
 
 }  // namespace
+
+void grpo_stats(const float* lp, const float* old_lp, const float* lp_ref, const float* kl,
+                const float* adv, const int* lengths, int G, double clip_eps, double kl_beta,
+                int sampled_kl, double* out4, cudaStream_t s) {
+  MRSP_REQUIRE(G >= 1 && G <= 1024, MRSP_INVALID_ARGUMENT, "grpo_stats: 1 <= G <= 1024");
+  MRSP_REQUIRE(sampled_kl ? lp_ref != nullptr : kl != nullptr, MRSP_INVALID_ARGUMENT,
+               "grpo_stats: missing KL input");
+  grpo_stats_kernel<<<1, 128, 0, s>>>(lp, old_lp, lp_ref, kl, adv, lengths, G, clip_eps, kl_beta,
+                                      sampled_kl, out4);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
 }  // namespace mrsp
 
 extern "C" mrsp_status mrsp_op_grpo_stats(const float* logprob, const float* old_logprob,
@@ -72,13 +86,7 @@ extern "C" mrsp_status mrsp_op_grpo_stats(const float* logprob, const float* old
                                           double* out4, void* stream) {
   return mrsp::guard([&] {
     mrsp::require_device();
-    MRSP_REQUIRE(G >= 1 && G <= 1024, MRSP_INVALID_ARGUMENT, "grpo_stats: 1 <= G <= 1024");
-    MRSP_REQUIRE(sampled_kl ? ref_logprob != nullptr : kl != nullptr, MRSP_INVALID_ARGUMENT,
-                 "grpo_stats: missing KL input");
-    mrsp::grpo_stats_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        logprob, old_logprob, ref_logprob, kl, advantages, lengths, G, clip_eps, kl_beta,
-        sampled_kl, out4);
-    mrsp::count_launch();
-    MRSP_CUDA(cudaGetLastError());
+    mrsp::grpo_stats(logprob, old_logprob, ref_logprob, kl, advantages, lengths, G, clip_eps,
+                     kl_beta, sampled_kl, out4, static_cast<cudaStream_t>(stream));
   });
 }

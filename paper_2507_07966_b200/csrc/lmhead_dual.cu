@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "backward.h"
 #include "gemm.h"
 #include "sm100.cuh"
 #include "tma.h"
@@ -48,8 +49,19 @@ struct DualArgs {
   Part* part;
   float* tgt_x;
   float* tgt_y;
+  // backward (kBwd): dJ/dlogits from the recomputed tiles (backward.h)
+  const float* lse_x;
+  const float* lse_y;
+  const float* coef;
+  const float* kl;
+  float kw;
+  __nv_bfloat16* G;
+  int ldg;
 };
 
+// kBwd = false: the forward partials; true: the backward's dJ/dlogits tile
+//   G = pi (kw (lp - lq - kl) - A) + A [v == y]   (grpo.cpp:152-180 per token)
+template <bool kBwd>
 __global__ void __launch_bounds__(THREADS, 1)
     lmhead_dual_tcgen05(const __grid_constant__ CUtensorMap tmAx, const __grid_constant__ CUtensorMap tmBx,
                         const __grid_constant__ CUtensorMap tmAy, const __grid_constant__ CUtensorMap tmBy,
@@ -142,6 +154,45 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool row_ok = row < a.M;
       const int tgt = row_ok ? a.targets[row] : -1;
       const uint32_t tr = tmem + (static_cast<uint32_t>(ew * 32) << 16);
+      if constexpr (kBwd) {
+        const float lx = row_ok ? a.lse_x[row] : 0.f, ly = row_ok ? a.lse_y[row] : 0.f;
+        const float A = row_ok ? a.coef[row] : 0.f, klt = row_ok ? a.kl[row] : 0.f;
+        for (int c = half * (BN / HALVES); c < (half + 1) * (BN / HALVES); c += 32) {
+          uint32_t rx[32], ry[32];
+          tmem_ld32(tr + c, rx);
+          tmem_ld32(tr + BN + c, ry);
+          tmem_ld_wait();
+          const int col = nt * BN + c;
+          if (row_ok && col < a.V) {
+            uint32_t o[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float gv[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const float lp = __uint_as_float(rx[2 * j + e]) - lx;
+                const float lq = __uint_as_float(ry[2 * j + e]) - ly;
+                const float pi = __expf(lp);
+                gv[e] = pi * (a.kw * (lp - lq - klt) - A) + (col + 2 * j + e == tgt ? A : 0.f);
+              }
+              o[j] = pack_bf16(gv[0], gv[1]);
+            }
+            __nv_bfloat16* dst = a.G + static_cast<size_t>(row) * a.ldg + col;
+            if (col + 32 <= a.V) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                reinterpret_cast<uint4*>(dst)[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            } else {
+              const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(o);
+              for (int j = 0; col + j < a.V; ++j) dst[j] = ob[j];
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(tempty);
+        tphase ^= 1;
+        continue;
+      }
       float mx = -INFINITY, sx = 0.f, ux = 0.f, my = -INFINITY, sy = 0.f;
       for (int c = half * (BN / HALVES); c < (half + 1) * (BN / HALVES); c += 32) {
         uint32_t rx[32], ry[32];
@@ -196,7 +247,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 __global__ void lmhead_dual_combine(const Part* __restrict__ part, int n_tiles,
                                     const float* __restrict__ tgt_x, const float* __restrict__ tgt_y,
                                     int n, float* __restrict__ lp_x, float* __restrict__ lp_y,
-                                    float* __restrict__ kl) {
+                                    float* __restrict__ kl, float* __restrict__ lse_xo,
+                                    float* __restrict__ lse_yo) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -229,6 +281,8 @@ __global__ void lmhead_dual_combine(const Part* __restrict__ part, int n_tiles,
     lp_x[warp] = tgt_x[warp] - lse_x;
     lp_y[warp] = tgt_y[warp] - lse_y;
     kl[warp] = Ux / Sx - lse_x + lse_y;
+    if (lse_xo) lse_xo[warp] = lse_x;
+    if (lse_yo) lse_yo[warp] = lse_y;
   }
 }
 
@@ -250,20 +304,70 @@ size_t lmhead_dual_workspace_bytes(int M, int V) {
          ~size_t(255);
 }
 
-void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, const void* Wr, int M,
-                            int V, int K, const int32_t* targets, float* lp_p, float* lp_r,
-                            float* kl, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  if (M <= 0) return;
-  MRSP_REQUIRE(K % 8 == 0, MRSP_INVALID_ARGUMENT, "lmhead_dual: K must be a multiple of 8");
-  MRSP_REQUIRE(ws_bytes >= lmhead_dual_workspace_bytes(M, V), MRSP_INVALID_ARGUMENT,
-               "lmhead_dual: workspace too small");
+namespace {
+void set_dual_attrs() {
   static const bool attr = [] {  // thread-safe one-time setup
-    MRSP_CUDA(cudaFuncSetAttribute(lmhead_dual_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MRSP_CUDA(cudaFuncSetAttribute(lmhead_dual_tcgen05<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(SMEM_BYTES)));
+    MRSP_CUDA(cudaFuncSetAttribute(lmhead_dual_tcgen05<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM_BYTES)));
     return true;
   }();
   (void)attr;
-  DualArgs a;
+}
+}  // namespace
+
+void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, const void* Wr, int M,
+                            int V, int K, const int32_t* targets, float* lp_p, float* lp_r,
+                            float* kl, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  lmhead_dual_logprob_kl_lse(Xp, Wp, Xr, Wr, M, V, K, targets, lp_p, lp_r, kl, nullptr, nullptr,
+                             ws, ws_bytes, stream);
+}
+
+
+void lmhead_dual_dlogits(const void* Xp, const void* Wp, const void* Xr, const void* Wr, int M,
+                         int V, int K, const int32_t* targets, const float* coef, float kw,
+                         const float* kl, const float* lse_p, const float* lse_r, void* G, int ldg,
+                         cudaStream_t stream) {
+  if (M <= 0) return;
+  MRSP_REQUIRE(K % 8 == 0 && ldg % 8 == 0 && ldg >= V, MRSP_INVALID_ARGUMENT,
+               "lmhead_dual_dlogits: K and ldg must be multiples of 8, ldg >= V");
+  set_dual_attrs();
+  DualArgs a{};
+  a.M = M;
+  a.V = V;
+  a.K = K;
+  a.n_tiles = (V + BN - 1) / BN;
+  a.targets = targets;
+  a.lse_x = lse_p;
+  a.lse_y = lse_r;
+  a.coef = coef;
+  a.kl = kl;
+  a.kw = kw;
+  a.G = static_cast<__nv_bfloat16*>(G);
+  a.ldg = ldg;
+  CUtensorMap ax = make_tmap_bf16_2d(Xp, M, K, K, BM, BK);
+  CUtensorMap bx = make_tmap_bf16_2d(Wp, V, K, K, BN, BK);
+  CUtensorMap ay = make_tmap_bf16_2d(Xr, M, K, K, BM, BK);
+  CUtensorMap by = make_tmap_bf16_2d(Wr, V, K, K, BN, BK);
+  const int tiles = ((M + BM - 1) / BM) * a.n_tiles;
+  lmhead_dual_tcgen05<true><<<std::min(tiles, sm_count()), THREADS, SMEM_BYTES, stream>>>(ax, bx, ay, by, a);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void lmhead_dual_logprob_kl_lse(const void* Xp, const void* Wp, const void* Xr, const void* Wr,
+                                int M, int V, int K, const int32_t* targets, float* lp_p,
+                                float* lp_r, float* kl, float* lse_p, float* lse_r, void* ws,
+                                size_t ws_bytes, cudaStream_t stream) {
+  if (M <= 0) return;
+  MRSP_REQUIRE(K % 8 == 0, MRSP_INVALID_ARGUMENT, "lmhead_dual: K must be a multiple of 8");
+  MRSP_REQUIRE(ws_bytes >= lmhead_dual_workspace_bytes(M, V), MRSP_INVALID_ARGUMENT,
+               "lmhead_dual: workspace too small");
+  set_dual_attrs();
+  DualArgs a{};
   a.M = M;
   a.V = V;
   a.K = K;
@@ -277,11 +381,11 @@ void lmhead_dual_logprob_kl(const void* Xp, const void* Wp, const void* Xr, cons
   CUtensorMap ay = make_tmap_bf16_2d(Xr, M, K, K, BM, BK);
   CUtensorMap by = make_tmap_bf16_2d(Wr, V, K, K, BN, BK);
   const int tiles = ((M + BM - 1) / BM) * a.n_tiles;
-  lmhead_dual_tcgen05<<<std::min(tiles, sm_count()), THREADS, SMEM_BYTES, stream>>>(ax, bx, ay, by, a);
+  lmhead_dual_tcgen05<false><<<std::min(tiles, sm_count()), THREADS, SMEM_BYTES, stream>>>(ax, bx, ay, by, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
   lmhead_dual_combine<<<(M + 7) / 8, 256, 0, stream>>>(a.part, a.n_tiles * HALVES, a.tgt_x, a.tgt_y, M, lp_p,
-                                                       lp_r, kl);
+                                                       lp_r, kl, lse_p, lse_r);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

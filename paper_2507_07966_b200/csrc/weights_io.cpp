@@ -17,6 +17,7 @@
 // tensor as 2-D strided segments, so save and load are exact inverses.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cctype>
 #include <cstdio>
 #include <cstring>
@@ -299,14 +300,8 @@ static std::vector<TensorDesc> describe(const mrsp_model_config& c, const Vision
   return t;
 }
 
-void Engine::save_weights(const std::string& path) {
-  std::lock_guard<std::mutex> run(run_mu_);
-  std::vector<TensorDesc> all;
-  for (int part = 0; part < (has_ref_ ? 3 : 2); ++part) {
-    auto v = describe(cfg_, vis_, llm_[part == 2 ? 1 : 0], part, part == 2 ? "ref." : "",
-                      tokens_per_frame(), vstride_);
-    all.insert(all.end(), v.begin(), v.end());
-  }
+static void write_safetensors(const std::string& path, const std::vector<TensorDesc>& all,
+                              const char* what) {
   std::string hdr = "{\"__metadata__\":{\"format\":\"pt\",\"producer\":\"mrsp-b200\"}";
   size_t off = 0;
   for (const auto& x : all) {
@@ -320,7 +315,7 @@ void Engine::save_weights(const std::string& path) {
   hdr += "}";
   while (hdr.size() % 8) hdr += ' ';
   FILE* f = std::fopen(path.c_str(), "wb");
-  MRSP_REQUIRE(f != nullptr, MRSP_RUNTIME_ERROR, "save_weights: cannot open " + path);
+  MRSP_REQUIRE(f != nullptr, MRSP_RUNTIME_ERROR, std::string(what) + ": cannot open " + path);
   const uint64_t hlen = hdr.size();
   bool ok = std::fwrite(&hlen, 8, 1, f) == 1 && std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
   std::vector<uint8_t> host;
@@ -333,7 +328,51 @@ void Engine::save_weights(const std::string& path) {
     ok = std::fwrite(host.data(), 1, host.size(), f) == host.size();
   }
   const bool closed = std::fclose(f) == 0;
-  MRSP_REQUIRE(ok && closed, MRSP_RUNTIME_ERROR, "save_weights: write failed: " + path);
+  MRSP_REQUIRE(ok && closed, MRSP_RUNTIME_ERROR, std::string(what) + ": write failed: " + path);
+}
+
+void Engine::save_weights(const std::string& path) {
+  std::lock_guard<std::mutex> run(run_mu_);
+  std::vector<TensorDesc> all;
+  for (int part = 0; part < (has_ref_ ? 3 : 2); ++part) {
+    auto v = describe(cfg_, vis_, llm_[part == 2 ? 1 : 0], part, part == 2 ? "ref." : "",
+                      tokens_per_frame(), vstride_);
+    all.insert(all.end(), v.begin(), v.end());
+  }
+  write_safetensors(path, all, "save_weights");
+}
+
+// The fp32 gradients of the policy LLM (grads_, engine_bwd.cu) under the
+// policy's tensor names: grads_ mirrors the weight layout element for element
+// with 4-byte elements, so the bf16 weight descriptors are re-used with every
+// byte extent doubled.
+void Engine::save_grads(const std::string& path) {
+  std::lock_guard<std::mutex> run(run_mu_);
+  MRSP_REQUIRE(have_grads_, MRSP_INVALID_ARGUMENT, "save_grads: no gradients (run grpo_backward)");
+  std::vector<TensorDesc> all = describe(cfg_, vis_, grads_, 1, "", tokens_per_frame(), vstride_);
+  // the descriptors address sub-blocks (q / k / v rows, gate / up blocks) by
+  // bf16 pointer arithmetic from a tensor's base: rebase those offsets too
+  std::vector<uintptr_t> bases = {reinterpret_cast<uintptr_t>(grads_.embed),
+                                  reinterpret_cast<uintptr_t>(grads_.lm_head)};
+  for (const auto& L : grads_.layers)
+    for (const void* q : {static_cast<const void*>(L.wqkv), static_cast<const void*>(L.wo),
+                          static_cast<const void*>(L.wgu), static_cast<const void*>(L.wdown)})
+      bases.push_back(reinterpret_cast<uintptr_t>(q));
+  std::sort(bases.begin(), bases.end());
+  for (auto& x : all) {
+    if (x.dtype != BF16) continue;
+    x.dtype = F32;
+    for (auto& sg : x.segs) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(sg.dev);
+      const uintptr_t b = *(std::upper_bound(bases.begin(), bases.end(), a) - 1);
+      sg.dev = reinterpret_cast<void*>(b + 2 * (a - b));
+      sg.dev_pitch *= 2;
+      sg.log_off *= 2;
+      sg.log_pitch *= 2;
+      sg.width *= 2;
+    }
+  }
+  write_safetensors(path, all, "save_grads");
 }
 
 void Engine::load_weights(const std::string& path, int part, const std::string& prefix) {
