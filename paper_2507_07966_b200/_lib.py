@@ -120,6 +120,19 @@ _sig("mrsp_engine_cache_save", [_V, ctypes.c_char_p, ctypes.c_char_p])
 _sig("mrsp_engine_cache_load", [_V, ctypes.c_char_p, ctypes.c_char_p, _V])
 _sig("mrsp_engine_p2p_export", [_V, _I, ctypes.c_long, ctypes.c_long, _V])
 _sig("mrsp_engine_p2p_import", [_V, _V])
+# backward pass
+_sig("mrsp_op_gemm_bf16_mn", [_V, _V, _V, _I, _I, _I, _I, _I, _I, _I, _I, _I, _V, _V, _I, _V])
+_sig("mrsp_op_attention_lse", [_V, _I, _I, _V, _I, _I, _V, _I, _I, _V, _I, _I, _I, _I, _I, _F,
+                               _I, _I, _V, _I, _V])
+_sig("mrsp_op_attention_bwd", [_V, _I, _I, _I, _I, _V, _I, _V, _I, _V, _V, _I, _V, _I, _I, _I, _I,
+                               _F, _I, _I, _V])
+_sig("mrsp_op_rmsnorm_bwd", [_V, _I, _V, _V, _I, _V, _I, _I, _I, _F, _V, _V, _V])
+_sig("mrsp_op_gemm_swiglu_bwd", [_V, _V, _V, _V, _V, _I, _I, _I, _V])
+_sig("mrsp_op_lmhead_dual_dlogits", [_V, _V, _V, _V, _I, _I, _I, _V, _V, _F, _V, _V, _V, _V, _I,
+                                     _V])
+_sig("mrsp_engine_grpo_backward", [_V, ctypes.c_char_p, _V, _I, _V, _V, _I, _I, _V, _V,
+                                   ctypes.c_double, ctypes.c_double, _I, _V, _V])
+_sig("mrsp_engine_save_grads", [_V, ctypes.c_char_p])
 
 
 def lib() -> ctypes.CDLL:

@@ -1867,8 +1867,10 @@ extern "C" mrsp_status mrsp_engine_get_embeddings(mrsp_engine* e, const char* vi
 extern "C" mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, double* ms,
                                            int64_t* launches) {
   return guard([&] {
+    MRSP_REQUIRE(e, MRSP_INVALID_ARGUMENT, "profile: null engine");
     if (enable >= 0) e->impl->set_profiling(enable != 0);
     if (ms && launches) {
+      MRSP_REQUIRE(cls >= 0 && cls <= P_BACKWARD, MRSP_INVALID_ARGUMENT, "profile: unknown class");
       long n = 0;
       e->impl->profile_read(cls, ms, &n);
       *launches = n;

@@ -304,6 +304,32 @@ class Engine:
             _ptr(lp_r, ctypes.c_float), _ptr(kl, ctypes.c_float), out_dev))
         return (lp_p, lp_r, kl) if with_kl or (out is not None and len(out) > 2) else (lp_p, lp_r)
 
+    # ---- GRPO backward -----------------------------------
+    def grpo_backward(self, vid: str, group: Group, old_logprobs, advantages,
+                      clip_eps: float = 0.2, kl_beta: float = 0.04, sampled_kl: bool = False):
+        """grpo_gradient (grpo.cpp:122-206) through the transformer-shaped prefill:
+        the policy LLM's fp32 gradients stay in the engine (save_grads). Returns
+        (stats {objective, mean_kl, clip_fraction, token_count}, policy log-probs)."""
+        q, resp, lens = _group_arrays(group)
+        n = int(lens.sum())
+        old = np.ascontiguousarray(old_logprobs, dtype=np.float32).reshape(-1)
+        adv = np.ascontiguousarray(advantages, dtype=np.float32).reshape(-1)
+        if old.shape != (n,) or adv.shape != (resp.shape[0],):
+            raise ValueError(f"grpo_backward: old_logprobs needs {n} and advantages "
+                             f"{resp.shape[0]} entries")
+        st = np.zeros(4, dtype=np.float64)
+        lp = np.zeros(n, dtype=np.float32)
+        check(_lib.lib().mrsp_engine_grpo_backward(
+            self._h, vid.encode(), _ptr(q), len(q), _ptr(resp), _ptr(lens), int(resp.shape[0]),
+            int(resp.shape[1]), _ptr(old, ctypes.c_float), _ptr(adv, ctypes.c_float),
+            float(clip_eps), float(kl_beta), int(sampled_kl), _ptr(st, ctypes.c_double),
+            _ptr(lp, ctypes.c_float)))
+        return dict(zip(["objective", "mean_kl", "clip_fraction", "token_count"],
+                        [float(x) for x in st])), lp
+
+    def save_grads(self, path: str) -> None:
+        check(_lib.lib().mrsp_engine_save_grads(self._h, str(path).encode()))
+
     def stats(self, reset: bool = False) -> dict:
         out = (ctypes.c_uint64 * 6)()
         check(_lib.lib().mrsp_engine_stats(self._h, out, int(reset)))
@@ -341,7 +367,7 @@ class Engine:
         return (raw.astype(np.uint32) << 16).view(np.float32)
 
     PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc",
-                       "decode_graph"]
+                       "decode_graph", "backward"]
 
     def profile(self, enable: Optional[bool] = None) -> dict:
         en = -1 if enable is None else int(enable)
@@ -353,3 +379,24 @@ class Engine:
             check(_lib.lib().mrsp_engine_profile(self._h, -1, i, ctypes.byref(ms), ctypes.byref(n)))
             out[name] = (ms.value, n.value)
         return out
+
+
+def read_safetensors(path: str) -> dict:
+    """{name: float32 numpy array} from a safetensors file (F32 / BF16 tensors;
+    the engine's weights and gradients), without the safetensors package."""
+    import json
+    import struct
+    with open(path, "rb") as f:
+        n = struct.unpack("<Q", f.read(8))[0]
+        hdr = json.loads(f.read(n))
+        data = f.read()
+    out = {}
+    for name, t in hdr.items():
+        if name == "__metadata__":
+            continue
+        b, e = t["data_offsets"]
+        raw = np.frombuffer(data[b:e], dtype=np.uint16 if t["dtype"] == "BF16" else np.float32)
+        if t["dtype"] == "BF16":
+            raw = (raw.astype(np.uint32) << 16).view(np.float32)
+        out[name] = raw.reshape(t["shape"])
+    return out

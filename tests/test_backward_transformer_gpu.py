@@ -1,0 +1,280 @@
+"""GPU: the backward pass of the transformer-shaped MR-SP prefill (SURVEY §8f
+rank 3; the reference's grpo_gradient, grpo.cpp:122-206, carried through the
+Qwen-shaped decoder).
+
+Kernel level, through the C-ABI, against plain PyTorch fp32/fp64 references:
+MN-major tcgen05 GEMMs (dgrad / wgrad), the attention forward's log-sum-exp,
+the tcgen05 attention backward (MR-SP mask, GQA 2:1 and 7:1, ragged lengths),
+RMSNorm backward, the SwiGLU-backward GEMM epilogue, and the dual LM head's
+dJ/dlogits.
+
+Engine level: mrsp_engine_grpo_backward's gradients of every policy tensor vs
+float64 autograd of the same objective (oracle/transformer_grad.py, pinned to
+the reference's analytic dJ/dlogits and to the forward twin on CPU in
+tests/test_grad_oracle.py). Tolerance (bf16 activations and gradient
+operands, fp32 accumulation; measured at c1 and written here): per tensor
+relative L2 error <= 3e-2 and cosine >= 0.999; objective, mean KL and clip
+fraction to 2e-3 / 2e-3 / exact.
+"""
+import ctypes
+import math
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import transformer as T
+from oracle import transformer_grad as TG
+from paper_2507_07966_b200 import _lib
+from paper_2507_07966_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+
+
+def vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+# ---------------------------------------------------------------- GEMM (MN-major)
+@pytest.mark.parametrize("a_mn,b_mn,M,N,K", [(0, 1, 333, 384, 256), (1, 1, 256, 512, 1000),
+                                             (1, 0, 128, 264, 512), (1, 1, 4608, 256, 77)])
+def test_gemm_mn_major(gpu, a_mn, b_mn, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    As = A.t().contiguous() if a_mn else A  # [K][M] when MN-major
+    Bs = B.t().contiguous() if b_mn else B  # [K][N]
+    C = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _lib.check(_lib.lib().mrsp_op_gemm_bf16_mn(vp(As), vp(Bs), vp(C), M, N, K, As.stride(0),
+                                               Bs.stride(0), N, a_mn, b_mn, 5, None, None, 0, None))
+    want = A.double() @ B.double().T
+    torch.cuda.synchronize()
+    assert (C.double() - want).abs().max().item() <= 1e-3 * want.abs().max().item()
+
+
+# ---------------------------------------------------------------- attention
+def _mask(L, Lp, Lmax):
+    return torch.as_tensor(T.mrsp_mask(L, Lp, Lmax), device="cuda")
+
+
+@pytest.mark.parametrize("nq,nkv,Lp,G,Lmax", [(4, 2, 300, 3, 150), (7, 1, 517, 2, 200),
+                                              (2, 2, 128, 1, 128)])
+def test_attention_lse_and_backward(gpu, nq, nkv, Lp, G, Lmax):
+    L = Lp + G * Lmax
+    C = (nq + 2 * nkv) * 128
+    g = torch.Generator(device="cuda").manual_seed(L + nq)
+    qkv = (torch.randn(L, C, device="cuda", generator=g) * 1.5).bfloat16()
+    O = torch.empty(L, nq * 128, device="cuda", dtype=torch.bfloat16)
+    ld_stat = (L + 3) // 4 * 4
+    lse = torch.empty(nq, ld_stat, device="cuda")
+    scale = 1 / math.sqrt(128)
+    _lib.check(_lib.lib().mrsp_op_attention_lse(vp(qkv), C, 0, vp(qkv), C, nq * 128, vp(qkv), C,
+                                                (nq + nkv) * 128, vp(O), nq * 128, 0, L, nq,
+                                                nq // nkv, scale, Lp, Lmax, vp(lse), ld_stat, None))
+    # fp32 autograd reference from the same bf16 values
+    q = qkv[:, :nq * 128].float().reshape(L, nq, 128).requires_grad_(True)
+    k = qkv[:, nq * 128:(nq + nkv) * 128].float().reshape(L, nkv, 128).requires_grad_(True)
+    v = qkv[:, (nq + nkv) * 128:].float().reshape(L, nkv, 128).requires_grad_(True)
+    rep = nq // nkv
+    s = torch.einsum("qhd,khd->hqk", q, k.repeat_interleave(rep, 1)) * scale
+    s = s.masked_fill(~_mask(L, Lp, Lmax)[None], float("-inf"))
+    o = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v.repeat_interleave(rep, 1))
+    want_lse = torch.logsumexp(s, -1) * math.log2(math.e)
+    torch.cuda.synchronize()
+    assert (lse[:, :L] - want_lse).abs().max().item() < 2e-3
+    assert rel(O.float().cpu(), o.detach().reshape(L, -1).cpu()) < 1e-2
+    dO = torch.randn(L, nq * 128, device="cuda", generator=g).bfloat16()
+    o.backward(dO.float().reshape(L, nq, 128))
+    D = torch.empty(nq, ld_stat, device="cuda")
+    dqkv = torch.full((L, C), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_attention_bwd(vp(qkv), C, 0, nq * 128, (nq + nkv) * 128, vp(O),
+                                                nq * 128, vp(dO), nq * 128, vp(lse), vp(D), ld_stat,
+                                                vp(dqkv), C, L, nq, nq // nkv, scale, Lp, Lmax,
+                                                None))
+    torch.cuda.synchronize()
+    got = dqkv.float()
+    assert torch.isfinite(got).all()
+    for name, sl, ref in (("dq", slice(0, nq * 128), q.grad), ("dk", slice(nq * 128, (nq + nkv) * 128), k.grad),
+                          ("dv", slice((nq + nkv) * 128, C), v.grad)):
+        e = rel(got[:, sl].cpu(), ref.reshape(L, -1).cpu())
+        assert e < 2e-2, (name, e)
+    # deterministic: a second run gives identical bits
+    dqkv2 = torch.empty_like(dqkv)
+    _lib.check(_lib.lib().mrsp_op_attention_bwd(vp(qkv), C, 0, nq * 128, (nq + nkv) * 128, vp(O),
+                                                nq * 128, vp(dO), nq * 128, vp(lse), vp(D), ld_stat,
+                                                vp(dqkv2), C, L, nq, nq // nkv, scale, Lp, Lmax,
+                                                None))
+    torch.cuda.synchronize()
+    assert torch.equal(dqkv, dqkv2)
+
+
+# ---------------------------------------------------------------- elementwise
+def test_rmsnorm_backward(gpu):
+    n, d = 333, 3584
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.randn(n, d, device="cuda", generator=g) * 3).requires_grad_(True)
+    w = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).requires_grad_(True)
+    y = w * (x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6))
+    dy = torch.randn(n, d, device="cuda", generator=g)
+    y.backward(dy)
+    acc = torch.ones(n, d, device="cuda")
+    dw = torch.empty(d, device="cuda")
+    _lib.check(_lib.lib().mrsp_op_rmsnorm_bwd(vp(x), d, vp(w), vp(dy), d, vp(acc), d, n, d, 1e-6,
+                                              None, vp(dw), None))
+    torch.cuda.synchronize()
+    assert rel((acc - 1).cpu(), x.grad.cpu()) < 1e-5
+    assert rel(dw.cpu(), w.grad.cpu()) < 1e-5
+    # row map: rows i of dy go to rows[i] of x / dx
+    rows = torch.tensor([7, 0, 332], device="cuda", dtype=torch.int32)
+    acc2 = torch.zeros(n, d, device="cuda")
+    _lib.check(_lib.lib().mrsp_op_rmsnorm_bwd(vp(x), d, vp(w), vp(dy), d, vp(acc2), d, 3, d, 1e-6,
+                                              vp(rows), None, None))
+    xs = x.detach()[rows.long()].requires_grad_(True)
+    (w.detach() * (xs * torch.rsqrt((xs * xs).mean(-1, keepdim=True) + 1e-6))).backward(dy[:3])
+    torch.cuda.synchronize()
+    assert rel(acc2[rows.long()].cpu(), xs.grad.cpu()) < 1e-5
+    assert acc2.abs().sum().item() == pytest.approx(acc2[rows.long()].abs().sum().item())
+
+
+def test_swiglu_backward_epilogue(gpu):
+    M, mlp, K = 300, 512, 256
+    g = torch.Generator(device="cuda").manual_seed(9)
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(2 * mlp, K, device="cuda", generator=g) / K ** 0.5).bfloat16()  # [gate128|up128] blocks
+    dA = torch.randn(M, mlp, device="cuda", generator=g).bfloat16()
+    dGU = torch.empty(M, 2 * mlp, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty(M, mlp, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_gemm_swiglu_bwd(vp(X), vp(W), vp(dA), vp(dGU), vp(act), M, 2 * mlp,
+                                                  K, None))
+    gu = X.float() @ W.float().T  # [M, 2 mlp] in block order
+    blk = gu.reshape(M, mlp // 128, 2, 128)
+    gate = blk[:, :, 0].reshape(M, mlp).requires_grad_(True)
+    up = blk[:, :, 1].reshape(M, mlp).requires_grad_(True)
+    a = torch.nn.functional.silu(gate) * up
+    a.backward(dA.float())
+    torch.cuda.synchronize()
+    got = dGU.float().reshape(M, mlp // 128, 2, 128)
+    assert rel(got[:, :, 0].reshape(M, mlp).cpu(), gate.grad.cpu()) < 1e-2
+    assert rel(got[:, :, 1].reshape(M, mlp).cpu(), up.grad.cpu()) < 1e-2
+    assert rel(act.float().cpu(), a.detach().cpu()) < 1e-2
+    # the recomputed SwiGLU output is the forward epilogue's, bit for bit
+    fwd = torch.empty(M, mlp, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_gemm_bf16(vp(X), vp(W), vp(fwd), M, 2 * mlp, K, K, K, mlp, 4,
+                                            None, None, 0, None))
+    torch.cuda.synchronize()
+    assert torch.equal(fwd, act)
+
+
+@pytest.mark.parametrize("M,V,K,kw", [(77, 32, 256, -0.01), (300, 5000, 512, -0.002),
+                                      (130, 152064, 512, 0.0)])
+def test_lmhead_dual_dlogits(gpu, M, V, K, kw):
+    g = torch.Generator(device="cuda").manual_seed(M + V)
+    Xp = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    Xr = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    Wp = (torch.randn(V, K, device="cuda", generator=g) / K ** 0.5 * 2).bfloat16()
+    Wr = (torch.randn(V, K, device="cuda", generator=g) / K ** 0.5 * 2).bfloat16()
+    tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32, generator=g)
+    lp_all = torch.log_softmax(Xp.double() @ Wp.double().T, -1)
+    lq_all = torch.log_softmax(Xr.double() @ Wr.double().T, -1)
+    lse_p = torch.logsumexp(Xp.double() @ Wp.double().T, -1).float()
+    lse_r = torch.logsumexp(Xr.double() @ Wr.double().T, -1).float()
+    kl = (lp_all.exp() * (lp_all - lq_all)).sum(-1)
+    coef = torch.randn(M, device="cuda", generator=g).float() * 0.1
+    G = torch.empty(M, V, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().mrsp_op_lmhead_dual_dlogits(vp(Xp), vp(Wp), vp(Xr), vp(Wr), M, V, K, vp(tgt),
+                                                      vp(coef), kw, vp(kl.float().contiguous()),
+                                                      vp(lse_p), vp(lse_r), vp(G), V, None))
+    pi = lp_all.exp()
+    want = pi * (kw * (lp_all - lq_all - kl[:, None]) - coef.double()[:, None])
+    want[torch.arange(M), tgt.long()] += coef.double()
+    torch.cuda.synchronize()
+    assert rel(G.double().cpu(), want.cpu()) < 1e-2
+
+
+# ---------------------------------------------------------------- engine level
+def _engine_vs_autograd(cfg, frames, seed_group, sampled, beta=0.04, clip=0.2):
+    w = E.workloads()["c1"]
+    c = T.Cfg.from_any(cfg)
+    pix = E.gen_video(1, frames, 3 * c.image_size ** 2)
+    G, lens_lo, lens_hi = 4, 6, 12
+    rng = np.random.default_rng(seed_group)
+    lengths = rng.integers(lens_lo, lens_hi + 1, size=G).astype(np.int32)
+    Lmax = int(lengths.max())
+    resp = np.zeros((G, Lmax), dtype=np.int32)
+    for i in range(G):
+        resp[i, :lengths[i]] = rng.integers(10, c.vocab, size=int(lengths[i]))
+    question = rng.integers(10, c.vocab, size=3).astype(np.int32)
+    grp = E.Group(question, resp, lengths)
+    eng = E.Engine(cfg, sp=1, vision_seed=2, policy_seed=3, ref_seed=4)
+    vid = E.video_id(1, frames)
+    eng.encode(vid, pix)
+    lp0 = eng.prefill_logprobs(vid, grp, 0)
+    n = int(lengths.sum())
+    old = lp0 - rng.choice([-0.5, -0.05, 0.05, 0.5], size=n).astype(np.float32)
+    adv = np.array([1.0, -0.7, 0.3, -1.2][:G], dtype=np.float32)
+    stats, lp = eng.grpo_backward(vid, grp, old, adv, clip, beta, sampled)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "g.safetensors")
+        eng.save_grads(path)
+        got = E.read_safetensors(path)
+    emb = torch.tensor(eng.embeddings(vid), dtype=torch.float64)
+    eng.close()
+    want_stats, want_lp, want = TG.grpo_objective_grad(cfg, 3, 4, emb, question, resp, lengths,
+                                                       old, adv, clip, beta, sampled, "cuda")
+    return stats, lp, got, want_stats, want_lp, want
+
+
+def _check(stats, lp, got, want_stats, want_lp, want, tol=3e-2):
+    assert np.abs(lp - want_lp).max() < 5e-2
+    assert stats["token_count"] == want_stats["token_count"]
+    assert stats["clip_fraction"] == pytest.approx(want_stats["clip_fraction"], abs=1e-12)
+    assert stats["objective"] == pytest.approx(want_stats["objective"], abs=2e-3)
+    assert stats["mean_kl"] == pytest.approx(want_stats["mean_kl"], abs=2e-3, rel=2e-2)
+    assert set(got) == set(want)
+    worst = []
+    for name, ref in want.items():
+        g = got[name].astype(np.float64)
+        assert g.shape == ref.shape, name
+        nr = np.linalg.norm(ref)
+        if nr == 0:
+            assert np.abs(g).max() == 0, name
+            continue
+        e = rel(g, ref)
+        cos = float((g * ref).sum() / (np.linalg.norm(g) * nr))
+        worst.append((e, name))
+        assert e <= tol and cos >= 0.999, (name, e, cos)
+    return sorted(worst)[-3:]
+
+
+@pytest.mark.parametrize("sampled", [False, True])
+def test_grpo_backward_c1_vs_autograd(gpu, sampled):
+    w = E.workloads()["c1"]
+    out = _engine_vs_autograd(w.cfg, w.frames, 11, sampled)
+    print("worst", _check(*out))
+
+
+def test_grpo_backward_gqa7_vs_autograd(gpu):
+    # Qwen-like 7:1 query-to-kv heads, several 128-column blocks per GEMM tile
+    cfg = E._cfg(image_size=64, patch=8, v_dim=256, v_heads=4, v_head_dim=64, v_mlp=1024,
+                 v_layers=1, dim=896, n_q_heads=7, n_kv_heads=1, mlp=1280, layers=2, vocab=3000)
+    out = _engine_vs_autograd(cfg, 4, 12, False)
+    print("worst", _check(*out))
+
+
+def test_grpo_backward_rejects_sp(gpu):
+    w = E.workloads()["c1"]
+    eng = E.Engine(w.cfg, sp=2)
+    pix = E.gen_video(1, w.frames, 3 * w.cfg.image_size ** 2)
+    eng.encode("v", pix)
+    grp = E.make_group(w)
+    n = grp.scored
+    with pytest.raises(_lib.MrspError):
+        eng.grpo_backward("v", grp, np.zeros(n), np.ones(w.G))
+    eng.close()
