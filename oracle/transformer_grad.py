@@ -85,7 +85,37 @@ def _rope(x, cos, sin):
     return _b(torch.cat([x1 * cc - x2 * ss, x2 * cc + x1 * ss], -1))
 
 
-def final_hidden(c: T.Cfg, P, frame_emb: torch.Tensor, question, resp, lengths, dev):
+class _AttnBf16Bwd(torch.autograd.Function):
+    """MR-SP attention whose backward rounds what the device rounds: dO, the
+    stored O, P and dS to bf16 (the tcgen05 operands), D = rowsum(dO o O) from
+    the bf16 values (csrc/backward.cu). Forward: exact float64 softmax."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, mask, scale):  # q [L, nq, hd], k / v [L, nq, hd] (repeated)
+        s = torch.einsum("qhd,khd->hqk", q, k) * scale
+        s = s.masked_fill(~mask[None], float("-inf"))
+        p = torch.softmax(s, -1)
+        o = torch.einsum("hqk,khd->qhd", p, v)
+        ctx.save_for_backward(q, k, v, p, o)
+        ctx.scale = scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, p, o = ctx.saved_tensors
+        bf = lambda x: TT._b(x)
+        do_b, o_b = bf(do), bf(o)
+        dp = torch.einsum("qhd,khd->hqk", do_b, v)
+        D = (do_b * o_b).sum(-1).t()[:, :, None]  # [h, q, 1]
+        ds = bf(p * (dp - D))
+        dq = torch.einsum("hqk,khd->qhd", ds, k) * ctx.scale
+        dk = torch.einsum("hqk,qhd->khd", ds, q) * ctx.scale
+        dv = torch.einsum("hqk,qhd->khd", bf(p), do_b)
+        return dq, dk, dv, None, None
+
+
+def final_hidden(c: T.Cfg, P, frame_emb: torch.Tensor, question, resp, lengths, dev,
+                 emulate_bf16_attn_bwd: bool = False):
     """Final-normed hidden rows at the scored positions (row-major over (g, j))."""
     n_frame_tok = frame_emb.shape[0]
     tok, pos, pad, Lp, L = T.pack(n_frame_tok, question, resp, lengths)
@@ -112,10 +142,13 @@ def final_hidden(c: T.Cfg, P, frame_emb: torch.Tensor, question, resp, lengths, 
         v = qkv[:, (nq + nkv) * hd:].reshape(L, nkv, hd)
         kk = k.repeat_interleave(rep, 1)  # [L, nq, hd] (head h uses kv head h // rep)
         vv = v.repeat_interleave(rep, 1)
-        s = torch.einsum("qhd,khd->hqk", q, kk) * scale
-        s = s.masked_fill(~mask[None], float("-inf"))
-        pr = torch.softmax(s, -1)
-        o = _b(torch.einsum("hqk,khd->qhd", pr, vv).reshape(L, nq * hd))
+        if emulate_bf16_attn_bwd:
+            o = _b(_AttnBf16Bwd.apply(q, kk, vv, mask, scale).reshape(L, nq * hd))
+        else:
+            s = torch.einsum("qhd,khd->hqk", q, kk) * scale
+            s = s.masked_fill(~mask[None], float("-inf"))
+            pr = torch.softmax(s, -1)
+            o = _b(torch.einsum("hqk,khd->qhd", pr, vv).reshape(L, nq * hd))
         h = _s(h + o @ P[p + "self_attn.o_proj.weight"].T)
         xn = _rms(h, P[p + "post_attention_layernorm.weight"], c.rms_eps)
         g_ = _s(xn @ P[p + "mlp.gate_proj.weight"].T)
@@ -159,12 +192,15 @@ def objective(lp_all, lq_all, tg, old_lp, adv, lengths, clip_eps: float, kl_beta
 
 def grpo_objective_grad(c: T.Cfg, policy_seed: int, ref_seed: int, frame_emb, question, resp,
                         lengths, old_lp, adv, clip_eps: float, kl_beta: float, sampled_kl: bool,
-                        dev="cpu"):
-    """(stats, policy log-probs, {HF name: dJ/dtheta as float64 numpy})."""
+                        dev="cpu", emulate_bf16_attn_bwd: bool = False):
+    """(stats, policy log-probs, {HF name: dJ/dtheta as float64 numpy}).
+    emulate_bf16_attn_bwd: the attention backward rounds dO, O, P and dS to bf16
+    as the device does (the dominant rounding of the q / k gradients); the
+    default is the exact float64 gradient."""
     c = T.Cfg.from_any(c)
     P = llm_params(c, policy_seed, "policy.", dev, grad=True)
     R = llm_params(c, ref_seed, "ref.", dev, grad=False)
-    xs, tg = final_hidden(c, P, frame_emb, question, resp, lengths, dev)
+    xs, tg = final_hidden(c, P, frame_emb, question, resp, lengths, dev, emulate_bf16_attn_bwd)
     with torch.no_grad():
         xr, _ = final_hidden(c, R, frame_emb, question, resp, lengths, dev)
     lp_all = torch.log_softmax(xs @ P["lm_head.weight"].T, -1)

@@ -310,9 +310,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int kt = blockIdx.x - kvh * n_kt;
   const int k0 = kt * TK;
   // query tiles that can see this key tile: from the diagonal up to the end of
-  // the sequence (prefix keys) or of the last key's rollout row
+  // the sequence (the tile holds a prefix key) or of the last key's rollout row
   const int klast = min(k0 + TK - 1, a.L - 1);
-  const int q_end = klast < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(klast, m) + 1) * a.Lmax);
+  const int q_end = k0 < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(klast, m) + 1) * a.Lmax);
   const int qt_lo = k0 / TQ, qt_hi = min(n_qt, (q_end + TQ - 1) / TQ);
   const int n_items = (qt_hi - qt_lo) * a.q_per_kv;  // (head, query tile), head-minor
   auto next = [&](int& i, int& hh, int& qt) {  // next visible item at or after i

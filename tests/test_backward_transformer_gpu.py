@@ -11,10 +11,16 @@ dJ/dlogits.
 Engine level: mrsp_engine_grpo_backward's gradients of every policy tensor vs
 float64 autograd of the same objective (oracle/transformer_grad.py, pinned to
 the reference's analytic dJ/dlogits and to the forward twin on CPU in
-tests/test_grad_oracle.py). Tolerance (bf16 activations and gradient
-operands, fp32 accumulation; measured at c1 and written here): per tensor
-relative L2 error <= 3e-2 and cosine >= 0.999; objective, mean KL and clip
-fraction to 2e-3 / 2e-3 / exact.
+tests/test_grad_oracle.py). Tolerances (bf16 activations and gradient
+operands, fp32 accumulation; measured at c1 / the 7:1 GQA config and written
+here), per tensor: relative L2 error vs the exact float64 gradient <= 3e-2
+(weights) / 5e-2 (biases: column sums over every token of a bf16 gradient;
+worst measured 0.034, the last layer's k bias) and cosine >= 0.999; vs the same
+autograd with the attention backward rounding dO, O, P and dS to bf16 as the
+device does <= 2.5e-2 (that emulation halves the q / k bias and weight errors
+of the last layer, 0.034 -> 0.021 and 0.021 -> 0.014: the bf16 dS operand is
+the dominant rounding; the rest is the bf16 gradient operands of the dgrad /
+wgrad GEMMs); objective, mean KL and clip fraction to 2e-3 / 2e-3 / exact.
 """
 import ctypes
 import math
@@ -101,10 +107,30 @@ def test_attention_lse_and_backward(gpu, nq, nkv, Lp, G, Lmax):
     torch.cuda.synchronize()
     got = dqkv.float()
     assert torch.isfinite(got).all()
-    for name, sl, ref in (("dq", slice(0, nq * 128), q.grad), ("dk", slice(nq * 128, (nq + nkv) * 128), k.grad),
-                          ("dv", slice((nq + nkv) * 128, C), v.grad)):
-        e = rel(got[:, sl].cpu(), ref.reshape(L, -1).cpu())
-        assert e < 2e-2, (name, e)
+    # The kernel's arithmetic restated (fp32 S and dP, exact-lse P, D from the
+    # bf16 O, P and dS rounded to bf16 as the tensor-core operands): tight.
+    with torch.no_grad():
+        qe, ke, ve = q.detach(), k.detach().repeat_interleave(rep, 1), v.detach().repeat_interleave(rep, 1)
+        P = torch.exp(s.detach() - torch.logsumexp(s.detach(), -1, keepdim=True))
+        dOh = dO.float().reshape(L, nq, 128)
+        dP = torch.einsum("qhd,khd->hqk", dOh, ve)
+        Dq = (dOh * O.float().reshape(L, nq, 128)).sum(-1).t()  # [h, q]
+        dS = (P * (dP - Dq[:, :, None])).bfloat16().float()
+        Pb = P.bfloat16().float()
+        em_dq = torch.einsum("hqk,khd->qhd", dS, ke) * scale
+        em_dk = (torch.einsum("hqk,qhd->khd", dS, qe) * scale).reshape(L, nkv, rep, 128).sum(2)
+        em_dv = torch.einsum("hqk,qhd->khd", Pb, dOh).reshape(L, nkv, rep, 128).sum(2)
+    errs = {}
+    for name, sl, ref, em in (("dq", slice(0, nq * 128), q.grad, em_dq),
+                              ("dk", slice(nq * 128, (nq + nkv) * 128), k.grad, em_dk),
+                              ("dv", slice((nq + nkv) * 128, C), v.grad, em_dv)):
+        errs[name] = (rel(got[:, sl].cpu(), em.reshape(L, -1).cpu()),
+                      rel(got[:, sl].cpu(), ref.reshape(L, -1).cpu()),
+                      rel(em.reshape(L, -1).cpu(), ref.reshape(L, -1).cpu()))
+    print("attn bwd errors (vs emulation, vs fp32 autograd, emulation vs autograd)", errs)
+    for name, (e_em, e_ref, e_floor) in errs.items():
+        assert e_em < 5e-3, (name, errs)
+        assert e_ref < max(2e-2, 1.5 * e_floor), (name, errs)
     # deterministic: a second run gives identical bits
     dqkv2 = torch.empty_like(dqkv)
     _lib.check(_lib.lib().mrsp_op_attention_bwd(vp(qkv), C, 0, nq * 128, (nq + nkv) * 128, vp(O),
@@ -228,10 +254,13 @@ def _engine_vs_autograd(cfg, frames, seed_group, sampled, beta=0.04, clip=0.2):
     eng.close()
     want_stats, want_lp, want = TG.grpo_objective_grad(cfg, 3, 4, emb, question, resp, lengths,
                                                        old, adv, clip, beta, sampled, "cuda")
-    return stats, lp, got, want_stats, want_lp, want
+    _, _, want_em = TG.grpo_objective_grad(cfg, 3, 4, emb, question, resp, lengths, old, adv, clip,
+                                           beta, sampled, "cuda", emulate_bf16_attn_bwd=True)
+    return stats, lp, got, want_stats, want_lp, want, want_em
 
 
-def _check(stats, lp, got, want_stats, want_lp, want, tol=3e-2):
+def _check(stats, lp, got, want_stats, want_lp, want, want_em, tol=3e-2, tol_bias=5e-2,
+           tol_em=2.5e-2):
     assert np.abs(lp - want_lp).max() < 5e-2
     assert stats["token_count"] == want_stats["token_count"]
     assert stats["clip_fraction"] == pytest.approx(want_stats["clip_fraction"], abs=1e-12)
@@ -239,6 +268,7 @@ def _check(stats, lp, got, want_stats, want_lp, want, tol=3e-2):
     assert stats["mean_kl"] == pytest.approx(want_stats["mean_kl"], abs=2e-3, rel=2e-2)
     assert set(got) == set(want)
     worst = []
+    allerr = {}
     for name, ref in want.items():
         g = got[name].astype(np.float64)
         assert g.shape == ref.shape, name
@@ -249,7 +279,14 @@ def _check(stats, lp, got, want_stats, want_lp, want, tol=3e-2):
         e = rel(g, ref)
         cos = float((g * ref).sum() / (np.linalg.norm(g) * nr))
         worst.append((e, name))
-        assert e <= tol and cos >= 0.999, (name, e, cos)
+        e_em = rel(g, want_em[name])
+        allerr[name] = (round(e, 5), round(cos, 6), round(e_em, 5))
+    print("grad errors (rel vs exact, cos vs exact, rel vs bf16-attention-backward emulation)",
+          allerr)
+    for e, name in worst:
+        t = tol_bias if name.endswith(".bias") else tol
+        assert e <= t and allerr[name][1] >= 0.999, (name, allerr[name])
+        assert allerr[name][2] <= tol_em, (name, allerr[name])
     return sorted(worst)[-3:]
 
 
