@@ -244,6 +244,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gen", action="store_true", help="skip the rollout-generation side line")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-bwd", action="store_true", help="skip the GRPO-backward side line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -461,10 +462,67 @@ def main():
                 line["rollout_generation"] = generation_side_line(eng, w, group, peaks, pix)
             except Exception as e:
                 line["rollout_generation"] = {"error": str(e)}
-        print(json.dumps(line), flush=True)
     eng.close()
+    if rank == 0:
+        if world == 1 and not args.no_bwd:
+            try:
+                line["grpo_backward"] = backward_side_line(w, peaks)
+            except Exception as e:
+                line["grpo_backward"] = {"error": str(e)}
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def backward_side_line(w, peaks):
+    """SURVEY §8f rank 3, not the metric: one GRPO gradient through the
+    prefill (mrsp_engine_grpo_backward: reference + policy passes keeping the
+    layer inputs, fused dual LM head, then the backward of the LM head and of
+    every decoder layer recomputed from its kept input), on the same workload
+    when its SP = 1 working set fits next to the gradients (c1-c3), else on c3
+    (28 layers, 65K-token prompt). Wall time of the call, device time of the
+    backward kernels, and the attention-backward kernels' algorithmic TFLOP/s
+    (2.5x the forward attention FLOPs: S, dP, dQ, dK, dV)."""
+    import numpy as np
+    from oracle import transformer as T
+    from paper_2507_07966_b200 import engine as E
+    name = w.name if w.name in ("c1", "c2", "c3") else "c3"
+    wb = E.workloads()[name]
+    c = T.Cfg.from_any(wb.cfg)
+    eng = E.Engine(wb.cfg, sp=1)
+    try:
+        pix = E.gen_video(1, wb.frames, 3 * c.image_size ** 2)
+        grp = E.make_group(wb, seed=3)
+        vid = E.video_id(1, wb.frames)
+        eng.encode(vid, pix)
+        lp = eng.prefill_logprobs(vid, grp, 0)
+        rng = np.random.default_rng(0)
+        old = lp - rng.normal(0, 0.1, size=lp.shape).astype(np.float32)
+        adv = rng.normal(0, 1, size=wb.G).astype(np.float32)
+        eng.grpo_backward(vid, grp, old, adv)  # warm-up: allocations
+        eng.profile(True)
+        t0 = time.perf_counter()
+        st, _ = eng.grpo_backward(vid, grp, old, adv)
+        wall = time.perf_counter() - t0
+        prof = eng.profile(False)
+    finally:
+        eng.close()
+    fl = T.step_flops(c, wb.frames, len(grp.question), list(grp.lengths), passes=1)
+    attn = fl["attn_prefix"] + fl["attn_resp"]
+    bwd_ms, attn_ms = prof["backward"][0], prof["attention_backward"][0]
+    # recompute (1 forward pass of the layers) + dgrad + wgrad + attention backward
+    bwd_flops = 3 * fl["linear"] + attn + 2.5 * attn + 2 * fl["lm_head"]
+    return {"workload": name, "tokens": fl["tokens"], "wall_ms": round(wall * 1e3, 1),
+            "tokens_per_s": round(fl["tokens"] / wall, 1),
+            "backward_kernels_ms": round(bwd_ms, 1),
+            "backward_algorithmic_tflops": round(bwd_flops / (bwd_ms / 1e3) / 1e12, 1),
+            "attention_backward_ms": round(attn_ms, 1),
+            "attention_backward_tflops": round(2.5 * attn / (attn_ms / 1e3) / 1e12, 1),
+            "forward_passes_ms": round(prof["llm_attention"][0] + prof["llm_gemm"][0]
+                                       + prof["lm_head"][0] + prof["misc"][0], 1),
+            "objective": st["objective"],
+            "note": "policy-LLM gradients of the GRPO objective (exact KL, beta 0.04, clip 0.2); "
+                    "vision tower frozen; parity in tests/test_backward_transformer_gpu.py"}
 
 
 def generation_side_line(eng, w, group, peaks, pix):

@@ -457,7 +457,7 @@ void Engine::set_profiling(bool on) {
   prof_collect();
   prof_ = on;
   if (on) {
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kProfClasses; ++i) {
       prof_ms_[i] = 0;
       prof_n_[i] = 0;
     }
@@ -1870,7 +1870,7 @@ extern "C" mrsp_status mrsp_engine_profile(mrsp_engine* e, int enable, int cls, 
     MRSP_REQUIRE(e, MRSP_INVALID_ARGUMENT, "profile: null engine");
     if (enable >= 0) e->impl->set_profiling(enable != 0);
     if (ms && launches) {
-      MRSP_REQUIRE(cls >= 0 && cls <= P_BACKWARD, MRSP_INVALID_ARGUMENT, "profile: unknown class");
+      MRSP_REQUIRE(cls >= 0 && cls <= P_BWD_ATTN, MRSP_INVALID_ARGUMENT, "profile: unknown class");
       long n = 0;
       e->impl->profile_read(cls, ms, &n);
       *launches = n;

@@ -283,8 +283,9 @@ class Engine {
   };
   std::vector<Ev> ev_pending_;
   std::vector<cudaEvent_t> ev_pool_;
-  double prof_ms_[8] = {0};
-  long prof_n_[8] = {0};
+  static constexpr int kProfClasses = 9;
+  double prof_ms_[kProfClasses] = {0};
+  long prof_n_[kProfClasses] = {0};
   void prof_begin(int cls, cudaEvent_t* a);
   void prof_end(int cls, cudaEvent_t a);
   void prof_collect();
@@ -307,6 +308,6 @@ struct Prof {
 };
 
 enum { P_ATTN = 0, P_GEMM = 1, P_VISION = 2, P_LMHEAD = 3, P_COMM = 4, P_MISC = 5,
-       P_DECODE_GRAPH = 6, P_BACKWARD = 7 };
+       P_DECODE_GRAPH = 6, P_BACKWARD = 7, P_BWD_ATTN = 8 };
 
 }  // namespace mrsp

@@ -260,6 +260,7 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
     gemm_mn(dhb, d, 0, Lw.wo, Cq, 1, dO, Cq, n, Cq, d, GEMM_EPI_STORE_BF16);
     gemm_mn(dhb, d, 1, R.ol.p, Cq, 1, Lg.wo, Cq, d, Cq, n, GEMM_EPI_STORE_F32);
     {
+      Prof pa(*this, P_BWD_ATTN);
       AttnBwdParams bp{R.qkv.p, Cqkv, 0, nq * 128, (nq + nkv) * 128, R.ol.p, Cq, dO, Cq, lse, Dst,
                        ld_stat, dqkv, Cqkv, n, nq, nq / nkv, scale, static_cast<int>(g.Lp), g.Lmax};
       attention_bwd(bp, s);

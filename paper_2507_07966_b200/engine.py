@@ -367,7 +367,7 @@ class Engine:
         return (raw.astype(np.uint32) << 16).view(np.float32)
 
     PROFILE_CLASSES = ["llm_attention", "llm_gemm", "vision", "lm_head", "collectives", "misc",
-                       "decode_graph", "backward"]
+                       "decode_graph", "backward", "attention_backward"]
 
     def profile(self, enable: Optional[bool] = None) -> dict:
         en = -1 if enable is None else int(enable)
