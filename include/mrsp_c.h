@@ -285,7 +285,7 @@ mrsp_status mrsp_op_attention_bwd(const void* qkv, int ld_qkv, int q_col0, int k
                                   const float* lse, float* D, int ld_stat, void* dqkv,
                                   int ld_dqkv, int L, int n_heads, int q_per_kv, float scale,
                                   int Lp, int Lmax, void* stream);
-/* RMSNorm backward: dx_acc[row] += dL/dx (x fp32, dy fp32), dw_out[d] = dL/dw
+/* RMSNorm backward: dx_acc[row] += dL/dx (x fp32, dy fp32), dw_out[d] += dL/dw
  * (may be NULL); rows (may be NULL) maps row i of dy to the x / dx_acc row. */
 mrsp_status mrsp_op_rmsnorm_bwd(const float* x, int ldx, const float* w, const float* dy, int ldy,
                                 float* dx_acc, int ld_dx, int n, int d, float eps,

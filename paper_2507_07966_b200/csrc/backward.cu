@@ -591,14 +591,15 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(
   }
 }
 
-// out[c] = sum over chunks of part[chunk][c], chunks in order (deterministic)
+// out[c] += sum over chunks of part[chunk][c], chunks in order (deterministic;
+// the gradients of a group are zeroed once and every SP rank adds its share)
 __global__ void chunk_sum_kernel(const float* __restrict__ part, int n_chunks, int n_cols,
                                  float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_cols) return;
   float s = 0.f;
   for (int k = 0; k < n_chunks; ++k) s += part[static_cast<size_t>(k) * n_cols + c];
-  out[c] = s;
+  out[c] += s;
 }
 
 constexpr int COLSUM_ROWS = 128;
@@ -638,7 +639,7 @@ __global__ void embed_grad_kernel(const float* __restrict__ dh, int d, const int
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     float s = 0.f;
     for (int i = b; i < e; ++i) s += dh[static_cast<size_t>(positions[i]) * d + c];
-    out[c] = s;
+    out[c] += s;
   }
 }
 
@@ -749,10 +750,7 @@ size_t colsum_workspace_bytes(int n_rows, int n_cols) {
 
 void colsum_bf16(const __nv_bfloat16* X, int ld, int n_rows, int n_cols, float* out, void* ws,
                  cudaStream_t s) {
-  if (n_rows <= 0) {
-    MRSP_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(n_cols) * 4, s));
-    return;
-  }
+  if (n_rows <= 0) return;
   const int chunks = (n_rows + COLSUM_ROWS - 1) / COLSUM_ROWS;
   float* part = static_cast<float*>(ws);
   colsum_part_kernel<<<dim3((n_cols + 255) / 256, chunks), 256, 0, s>>>(X, ld, n_rows, n_cols, part);

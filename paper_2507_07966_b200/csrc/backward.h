@@ -36,14 +36,14 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream);
 
 // RMSNorm backward, y = w o x r, r = (mean x^2 + eps)^-1/2:
 //   dx = r (w o dy) - x r^3 mean(w o dy o x)   accumulated: dx_acc[row] += dx
-//   dw = sum_rows dy o x r                     (fixed chunk order -> deterministic)
+//   dw += sum_rows dy o x r                    (fixed chunk order -> deterministic)
 // Row i reads x / dx_acc at rows ? rows[i] : i, dy at i. dw_out may be null.
 size_t rmsnorm_bwd_workspace_bytes(int n, int d);
 void rmsnorm_bwd(const float* x, int ldx, const float* w, const float* dy, int ldy, float* dx_acc,
                  int ld_dx, int n, int d, float eps, const int* rows, float* dw_out, void* ws,
                  cudaStream_t s);
 
-// out[c] = sum_r X[r][c] (bf16 in, fp32 out; fixed chunk order).
+// out[c] += sum_r X[r][c] (bf16 in, fp32 out; fixed chunk order).
 size_t colsum_workspace_bytes(int n_rows, int n_cols);
 void colsum_bf16(const __nv_bfloat16* X, int ld, int n_rows, int n_cols, float* out, void* ws,
                  cudaStream_t s);
@@ -52,7 +52,7 @@ void cast_f32_bf16(const float* in, int ld_in, __nv_bfloat16* out, int ld_out, i
                    int n_cols, cudaStream_t s);
 void negate_i32(const int* in, int* out, int n, cudaStream_t s);
 
-// dE[tok] = sum of dh rows at the positions listed for tok (CSR: seg_tok[i] =
+// dE[tok] += sum of dh rows at the positions listed for tok (CSR: seg_tok[i] =
 // token id of segment i, seg_off[i] .. seg_off[i+1] its ascending positions).
 void embed_grad(const float* dh, int d, const int* seg_tok, const int* seg_off,
                 const int* positions, int n_seg, float* dE, cudaStream_t s);

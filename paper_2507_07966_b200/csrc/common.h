@@ -25,6 +25,7 @@ void set_last_error(const std::string& msg);
 
 inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // a failed API call must not resurface at a later launch check
     char buf[512];
     std::snprintf(buf, sizeof(buf), "CUDA error in %s (%s:%d): %s", what, file, line,
                   cudaGetErrorString(e));

@@ -957,10 +957,11 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
   int layer = -1;
   for (const auto& Lw : W.layers) {
     ++layer;
-    if (stash_) {  // backward: keep this layer's input (SP = 1)
-      const size_t nd = static_cast<size_t>(ranks_[0].e - ranks_[0].b) * d;
-      MRSP_CUDA(cudaMemcpyAsync(stash_ + layer * nd, ranks_[0].h.p, nd * 4,
-                                cudaMemcpyDeviceToDevice, s));
+    for (size_t r = 0; r < stash_.size(); ++r) {  // backward: keep this layer's input
+      const size_t nd = static_cast<size_t>(ranks_[r].e - ranks_[r].b) * d;
+      if (nd)
+        MRSP_CUDA(cudaMemcpyAsync(stash_[r] + layer * nd, ranks_[r].h.p, nd * 4,
+                                  cudaMemcpyDeviceToDevice, s));
     }
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);

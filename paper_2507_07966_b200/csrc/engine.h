@@ -201,10 +201,12 @@ class Engine {
   void prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
                      const int32_t* resp, const int32_t* lengths, int G, int Lmax);
   void run_pass(const CacheEntry& emb, int model, int xs_slot);
-  // backward: per-layer input hidden states kept by run_pass ([layers][n][d]
-  // fp32, SP = 1) and the fp32 gradients in the engine's weight layout
-  float* stash_ = nullptr;
-  DevBuf stash_buf_, grad_buf_, bwd_ws_;
+  // backward: per-layer input hidden states kept by run_pass (per local rank,
+  // [layers][n][d] fp32; empty = off), the per-rank backward workspaces and
+  // the fp32 gradients in the engine's weight layout
+  std::vector<float*> stash_;
+  std::vector<DevBuf> stash_bufs_, bwd_ws_;
+  DevBuf grad_buf_, bwd_group_ws_;
   LlmW grads_{};  // fp32 storage typed as the weight struct (see save_grads)
   bool have_grads_ = false;
   // prefix K/V capture for generation (run_pass copies rows [0, Lp) of every

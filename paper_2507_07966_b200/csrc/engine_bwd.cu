@@ -58,31 +58,35 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
                            const int32_t* resp, const int32_t* lengths, int G, int Lmax,
                            const float* old_lp, const float* adv, double clip_eps, double kl_beta,
                            int sampled_kl, double* stats4, float* lp_out) {
-  MRSP_REQUIRE(k_ == 1 && !mesh_ && !nccl_, MRSP_INVALID_ARGUMENT,
-               "grpo_backward: sequence parallel backward is not built; use an SP = 1 engine");
+  const auto& c = cfg_;
+  const int d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads, mlp = c.mlp, V = c.vocab;
+  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128, NL = c.layers;
+  MRSP_REQUIRE(!mesh_ && !nccl_, MRSP_INVALID_ARGUMENT,
+               "grpo_backward: built for one-process engines (SP ranks as virtual ranks); the "
+               "multi-process backward is not built");
+  MRSP_REQUIRE(k_ <= nkv, MRSP_INVALID_ARGUMENT,
+               "grpo_backward: the SP degree must divide the kv heads (head-sharded attention "
+               "backward; query-row splits are forward-only)");
   MRSP_REQUIRE(has_ref_ || kl_beta == 0.0, MRSP_INVALID_ARGUMENT,
                "grpo_backward: the KL term needs a separate reference model");
   MRSP_REQUIRE(old_lp && adv && stats4, MRSP_INVALID_ARGUMENT, "grpo_backward: null argument");
   MRSP_REQUIRE(clip_eps >= 0.0, MRSP_INVALID_ARGUMENT, "grpo_backward: clip_eps < 0");
-  std::lock_guard<std::mutex> run(run_mu_);
-  const auto& c = cfg_;
-  const int d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads, mlp = c.mlp, V = c.vocab;
-  const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128, NL = c.layers;
   MRSP_REQUIRE(d % 8 == 0 && mlp % 128 == 0 && V % 8 == 0, MRSP_INVALID_ARGUMENT,
                "grpo_backward: unsupported model geometry");
+  std::lock_guard<std::mutex> run(run_mu_);
   cudaStream_t s = stream_;
   prepare_group(emb, question, n_q, resp, lengths, G, Lmax);
   const GroupState& g = grp_;
-  RankCtx& R = ranks_[0];
-  const int n = static_cast<int>(R.e - R.b);
-  const int S = R.n_scored;
-  MRSP_REQUIRE(S == g.total_scored && S >= 1, MRSP_INVALID_ARGUMENT,
-               "grpo_backward: the group has no scored token");
+  const long Ltot = g.Ltot;
+  const int S = static_cast<int>(g.total_scored);
+  MRSP_REQUIRE(S >= 1, MRSP_INVALID_ARGUMENT, "grpo_backward: the group has no scored token");
+  const int K = k_;
 
-  // ---- gradient storage: fp32 in the engine's weight layout ----------------
-  if (!grad_buf_.p) {
-    size_t tot = 0;
-    auto add = [&](size_t elems) { tot += (elems * 4 + 255) & ~size_t(255); };
+  // ---- gradient storage: fp32 in the engine's weight layout, zeroed per call
+  // (every SP rank adds its tokens' share, in rank order: deterministic) -----
+  size_t grad_bytes = 0;
+  {
+    auto add = [&](size_t elems) { grad_bytes += (elems * 4 + 255) & ~size_t(255); };
     add(static_cast<size_t>(V) * d);
     for (int l = 0; l < NL; ++l) {
       add(d); add(static_cast<size_t>(Cqkv) * d); add(Cqkv); add(static_cast<size_t>(d) * Cq);
@@ -90,7 +94,9 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
     }
     add(d);
     add(static_cast<size_t>(V) * d);
-    grad_buf_.ensure(tot);
+  }
+  if (!grad_buf_.p) {
+    grad_buf_.ensure(grad_bytes);
     Carve cv{static_cast<uint8_t*>(grad_buf_.p)};
     grads_.embed = reinterpret_cast<bf16*>(cv.take<float>(static_cast<size_t>(V) * d));
     grads_.layers.resize(NL);
@@ -108,200 +114,369 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
     grads_.lm_head = reinterpret_cast<bf16*>(cv.take<float>(static_cast<size_t>(V) * d));
   }
   have_grads_ = false;
+  MRSP_CUDA(cudaMemsetAsync(grad_buf_.p, 0, grad_bytes, s));
 
-  // ---- workspaces ------------------------------------------------------------
-  const size_t nd = static_cast<size_t>(n) * d;
-  const int ld_stat = (n + 3) / 4 * 4;
-  const int ldg = V;
-  const size_t ws_norm = rmsnorm_bwd_workspace_bytes(std::max(n, S), d);
-  const size_t ws_col = colsum_workspace_bytes(n, Cqkv);
-  const size_t dual_ws = lmhead_dual_workspace_bytes(S, V);
+  // ---- group-wide vectors (group order) -------------------------------------
+  float *lp_f, *lpr_f, *kl_f, *coef_f, *old_f, *adv_f;
+  double* d_stats;
   {
-    size_t tot = 0;
-    auto add = [&](size_t bytes) { tot += (bytes + 255) & ~size_t(255); };
-    add(nd * 4 * 3);                                   // hm, dh, dx
-    add(nd * 2 * 2);                                   // dhb, xn1
-    add(static_cast<size_t>(n) * mlp * 2);             // dact
-    add(static_cast<size_t>(n) * 2 * mlp * 2);         // dgu
-    add(static_cast<size_t>(n) * Cq * 2);              // dO
-    add(static_cast<size_t>(n) * Cqkv * 2);            // dqkv
-    add(static_cast<size_t>(nq) * ld_stat * 4 * 2);    // lse, D
-    add(static_cast<size_t>(n) * 4);                   // -pos
-    add(static_cast<size_t>(S) * ldg * 2);             // G
-    add(static_cast<size_t>(S) * d * 4);               // dxs
-    add(static_cast<size_t>(S) * 4 * 8);               // lp, lp_ref, kl, lse_p, lse_r, coef, old
-    add(static_cast<size_t>(G) * 4 * 2 + 64);          // adv, lengths, stats
-    add(std::max(ws_norm, ws_col));
-    add(dual_ws);
-    bwd_ws_.ensure(tot);
+    auto layout = [&](Carve& cv) {
+      lp_f = cv.take<float>(S);
+      lpr_f = cv.take<float>(S);
+      kl_f = cv.take<float>(S);
+      coef_f = cv.take<float>(S);
+      old_f = cv.take<float>(S);
+      adv_f = cv.take<float>(G);
+      d_stats = cv.take<double>(4);
+    };
+    Carve sizing{nullptr};
+    layout(sizing);
+    bwd_group_ws_.ensure(sizing.off);
+    Carve cv{static_cast<uint8_t*>(bwd_group_ws_.p)};
+    layout(cv);
   }
-  Carve cv{static_cast<uint8_t*>(bwd_ws_.p)};
-  float* hm = cv.take<float>(nd);
-  float* dh = cv.take<float>(nd);
-  float* dx = cv.take<float>(nd);
-  bf16* dhb = cv.take<bf16>(nd);
-  bf16* xn1 = cv.take<bf16>(nd);
-  bf16* dact = cv.take<bf16>(static_cast<size_t>(n) * mlp);
-  bf16* dgu = cv.take<bf16>(static_cast<size_t>(n) * 2 * mlp);
-  bf16* dO = cv.take<bf16>(static_cast<size_t>(n) * Cq);
-  bf16* dqkv = cv.take<bf16>(static_cast<size_t>(n) * Cqkv);
-  float* lse = cv.take<float>(static_cast<size_t>(nq) * ld_stat);
-  float* Dst = cv.take<float>(static_cast<size_t>(nq) * ld_stat);
-  int* negpos = cv.take<int>(n);
-  bf16* Gl = cv.take<bf16>(static_cast<size_t>(S) * ldg);
-  float* dxs = cv.take<float>(static_cast<size_t>(S) * d);
-  float* lp = cv.take<float>(S);
-  float* lp_ref = cv.take<float>(S);
-  float* kl = cv.take<float>(S);
-  float* lse_p = cv.take<float>(S);
-  float* lse_r = cv.take<float>(S);
-  float* coef = cv.take<float>(S);
-  float* d_old = cv.take<float>(S);
-  float* d_adv = cv.take<float>(G);
-  double* d_stats = cv.take<double>(4);
-  void* ws = cv.take<uint8_t>(std::max(ws_norm, ws_col));
-  void* dws = cv.take<uint8_t>(dual_ws);
-  stash_buf_.ensure(static_cast<size_t>(NL) * nd * 4);
+
+  // ---- per-rank workspaces --------------------------------------------------
+  struct RW {
+    float *hm, *dh, *dx, *dxs_own, *lp, *lpr, *kl, *lsep, *lser, *stat_lse, *stat_D, *dxs;
+    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh;
+    int* negpos;
+    void *ws, *dws;
+    int ld_stat;
+  };
+  std::vector<RW> rw(K);
+  stash_bufs_.resize(K);
+  bwd_ws_.resize(K);
+  for (int r = 0; r < K; ++r) {
+    RankCtx& R = ranks_[r];
+    const int n = static_cast<int>(R.e - R.b);
+    const size_t nd = static_cast<size_t>(n) * d;
+    const int nqr = R.hs.nq(), Cr = (R.hs.nq() + 2 * R.hs.nkv()) * 128;
+    const int lm = std::max(R.lm_n, 1), own = std::max(R.n_scored, 1);
+    const long Lh = K == 1 ? n : Ltot;  // rows of the attention (head-shard) problem
+    const int ld_stat = static_cast<int>((Lh + 3) / 4 * 4);
+    const size_t ws_norm = rmsnorm_bwd_workspace_bytes(std::max(n, own), d);
+    const size_t ws_col = colsum_workspace_bytes(n, Cqkv);
+    const size_t dual_ws = lmhead_dual_workspace_bytes(lm, V);
+    RW& w = rw[r];
+    // one layout function, run once to size the buffer and once to carve it
+    auto layout = [&](Carve& cv) {
+      w.hm = cv.take<float>(nd);
+      w.dh = cv.take<float>(nd);
+      w.dx = cv.take<float>(nd);
+      w.dhb = cv.take<bf16>(nd);
+      w.xn1 = cv.take<bf16>(nd);
+      w.dact = cv.take<bf16>(static_cast<size_t>(n) * mlp);
+      w.dgu = cv.take<bf16>(static_cast<size_t>(n) * 2 * mlp);
+      w.dO = cv.take<bf16>(static_cast<size_t>(n) * Cq);
+      w.dqkv = cv.take<bf16>(static_cast<size_t>(n) * Cqkv);
+      w.stat_lse = cv.take<float>(static_cast<size_t>(std::max(nqr, 1)) * ld_stat);
+      w.stat_D = cv.take<float>(static_cast<size_t>(std::max(nqr, 1)) * ld_stat);
+      w.negpos = cv.take<int>(n);
+      w.Gl = cv.take<bf16>(static_cast<size_t>(lm) * V);
+      w.dxs = cv.take<float>(static_cast<size_t>(lm) * d);
+      w.dxs_own = cv.take<float>(static_cast<size_t>(own) * d);
+      w.lp = cv.take<float>(lm);
+      w.lpr = cv.take<float>(lm);
+      w.kl = cv.take<float>(lm);
+      w.lsep = cv.take<float>(lm);
+      w.lser = cv.take<float>(lm);
+      w.ws = cv.take<uint8_t>(std::max(ws_norm, ws_col));
+      w.dws = cv.take<uint8_t>(dual_ws);
+      w.doh = K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128) : nullptr;
+      w.dqkvh = K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * Cr) : nullptr;
+    };
+    Carve sizing{nullptr};
+    layout(sizing);
+    bwd_ws_[r].ensure(sizing.off);
+    Carve cv{static_cast<uint8_t*>(bwd_ws_[r].p)};
+    layout(cv);
+    w.ld_stat = ld_stat;
+    stash_bufs_[r].ensure(std::max<size_t>(static_cast<size_t>(NL) * nd * 4, 256));
+  }
 
   // ---- forward: reference pass, then the policy pass keeping layer inputs --
-  run_pass(emb, 1, 1);  // R.xs2 = reference final-norm rows
-  stash_ = stash_buf_.as<float>();
+  run_pass(emb, 1, 1);  // xs2 = reference final-norm rows
+  stash_.resize(K);
+  for (int r = 0; r < K; ++r) stash_[r] = stash_bufs_[r].as<float>();
   try {
-    run_pass(emb, 0, 0);  // R.xs = policy final-norm rows; R.h = h_L
+    run_pass(emb, 0, 0);  // xs = policy final-norm rows; h = h_L of every shard
   } catch (...) {
-    stash_ = nullptr;
+    stash_.clear();
     throw;
   }
-  stash_ = nullptr;
+  stash_.clear();
+  lm_exchange(2);  // both models' rows to the LM-head slices (spread LM head)
   const LlmW& W = llm_[0];
   const LlmW& Wr = llm_[1];
   {
     Prof pl(*this, P_LMHEAD);
-    lmhead_dual_logprob_kl_lse(R.xs.p, W.lm_head, R.xs2.p, Wr.lm_head, S, V, d,
-                               R.lm_idx.as<int32_t>(), lp, lp_ref, kl, lse_p, lse_r, dws, dual_ws, s);
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      if (R.lm_n == 0) continue;
+      RW& w = rw[r];
+      const size_t dual_ws = lmhead_dual_workspace_bytes(R.lm_n, V);
+      lmhead_dual_logprob_kl_lse(lm_rows(R, 0), W.lm_head, lm_rows(R, 1), Wr.lm_head, R.lm_n, V, d,
+                                 R.lm_idx.as<int32_t>(), w.lp, w.lpr, w.kl, w.lsep, w.lser, w.dws,
+                                 dual_ws, s);
+      // slices are contiguous in group order
+      const size_t off = static_cast<size_t>(R.lm_lo) * 4, bytes = static_cast<size_t>(R.lm_n) * 4;
+      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lp_f) + off, w.lp, bytes, cudaMemcpyDeviceToDevice, s));
+      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lpr_f) + off, w.lpr, bytes, cudaMemcpyDeviceToDevice, s));
+      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(kl_f) + off, w.kl, bytes, cudaMemcpyDeviceToDevice, s));
+    }
   }
-  MRSP_CUDA(cudaMemcpyAsync(d_old, old_lp, static_cast<size_t>(S) * 4, cudaMemcpyHostToDevice, s));
-  MRSP_CUDA(cudaMemcpyAsync(d_adv, adv, static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
-  grpo_stats(lp, d_old, lp_ref, kl, d_adv, g.d_len, G, clip_eps, kl_beta, sampled_kl, d_stats, s);
+  MRSP_CUDA(cudaMemcpyAsync(old_f, old_lp, static_cast<size_t>(S) * 4, cudaMemcpyHostToDevice, s));
+  MRSP_CUDA(cudaMemcpyAsync(adv_f, adv, static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
+  grpo_stats(lp_f, old_f, lpr_f, kl_f, adv_f, g.d_len, G, clip_eps, kl_beta, sampled_kl, d_stats, s);
   {
   Prof pb(*this, P_BACKWARD);
-  grpo_token_coeffs(lp, d_old, lp_ref, d_adv, g.d_len, G, S, clip_eps, kl_beta, sampled_kl, coef, s);
+  grpo_token_coeffs(lp_f, old_f, lpr_f, adv_f, g.d_len, G, S, clip_eps, kl_beta, sampled_kl, coef_f, s);
   const float kw = (sampled_kl || kl_beta == 0.0) ? 0.f : static_cast<float>(-kl_beta / S);
-
-  // ---- LM head and final norm -------------------------------------------------
-  lmhead_dual_dlogits(R.xs.p, W.lm_head, R.xs2.p, Wr.lm_head, S, V, d, R.lm_idx.as<int32_t>(),
-                      coef, kw, kl, lse_p, lse_r, Gl, ldg, s);
   auto gemm_mn = [&](const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
-                     int ldc, int M, int N, int K, int epi, float* resid = nullptr, int ldr = 0) {
-    GemmArgs ga{A, B, C, M, N, K, lda, ldb, ldc, epi, nullptr, resid, ldr};
+                     int ldc, int M, int N, int Kd, int epi) {
+    if (M <= 0 || N <= 0 || Kd <= 0) return;
+    GemmArgs ga{A, B, C, M, N, Kd, lda, ldb, ldc, epi, nullptr, nullptr, 0};
+    if (epi == GEMM_EPI_RESID_F32) {  // C is the fp32 accumulator
+      ga.resid = static_cast<float*>(C);
+      ga.ldr = ldc;
+      ga.C = nullptr;
+    }
     ga.a_mn = a_mn;
     ga.b_mn = b_mn;
     gemm_bf16(ga, s);
   };
-  // dX_s = G . W_lm  (W_lm [V][d] read as the MN-major B of an [S x d x V] GEMM)
-  gemm_mn(Gl, ldg, 0, W.lm_head, d, 1, dxs, d, S, d, V, GEMM_EPI_STORE_F32);
-  // dW_lm = G^T . X_s
-  gemm_mn(Gl, ldg, 1, R.xs.p, d, 1, grads_.lm_head, d, V, d, S, GEMM_EPI_STORE_F32);
-  MRSP_CUDA(cudaMemsetAsync(dh, 0, nd * 4, s));
-  rmsnorm_bwd(R.h.as<float>(), d, W.final_norm, dxs, d, dh, d, S, d, c.rms_eps,
-              R.scored_idx.as<int32_t>(), grads_.final_norm, ws, s);
+  const int ACC = GEMM_EPI_RESID_F32;
+
+  // ---- LM head (each rank's slice) and final norm (each rank's tokens) ------
+  for (int r = 0; r < K; ++r) {
+    RankCtx& R = ranks_[r];
+    if (R.lm_n == 0) continue;
+    RW& w = rw[r];
+    lmhead_dual_dlogits(lm_rows(R, 0), W.lm_head, lm_rows(R, 1), Wr.lm_head, R.lm_n, V, d,
+                        R.lm_idx.as<int32_t>(), coef_f + R.lm_lo, kw, kl_f + R.lm_lo, w.lsep,
+                        w.lser, w.Gl, V, s);
+    gemm_mn(w.Gl, V, 0, W.lm_head, d, 1, w.dxs, d, R.lm_n, d, V, GEMM_EPI_STORE_F32);
+    gemm_mn(w.Gl, V, 1, lm_rows(R, 0), d, 1, grads_.lm_head, d, V, d, R.lm_n, ACC);
+  }
+  for (int r = 0; r < K; ++r) {  // the slices' dX rows back to the ranks owning the tokens
+    RankCtx& R = ranks_[r];
+    for (int p = 0; p < K; ++p) {
+      const RankCtx& P = ranks_[p];
+      const long lo = std::max<long>(R.sc_lo, P.lm_lo);
+      const long hi = std::min<long>(R.sc_lo + R.n_scored, P.lm_lo + P.lm_n);
+      if (hi <= lo) continue;
+      MRSP_CUDA(cudaMemcpyAsync(rw[r].dxs_own + (lo - R.sc_lo) * d, rw[p].dxs + (lo - P.lm_lo) * d,
+                                static_cast<size_t>(hi - lo) * d * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  for (int r = 0; r < K; ++r) {
+    RankCtx& R = ranks_[r];
+    RW& w = rw[r];
+    const int n = static_cast<int>(R.e - R.b);
+    MRSP_CUDA(cudaMemsetAsync(w.dh, 0, static_cast<size_t>(n) * d * 4, s));
+    rmsnorm_bwd(R.h.as<float>(), d, W.final_norm, w.dxs_own, d, w.dh, d, R.n_scored, d, c.rms_eps,
+                R.scored_idx.as<int32_t>(), grads_.final_norm, w.ws, s);
+    negate_i32(R.pos.as<int>(), w.negpos, n, s);
+  }
 
   // ---- decoder layers, last to first ----------------------------------------
-  negate_i32(R.pos.as<int>(), negpos, n, s);
   const float scale = 1.0f / std::sqrt(128.0f);
   for (int l = NL - 1; l >= 0; --l) {
     const LlmLayerW& Lw = W.layers[l];
     LlmLayerW& Lg = grads_.layers[l];
-    const float* h_in = stash_buf_.as<float>() + static_cast<size_t>(l) * nd;
-    // recompute the layer's forward (the same kernels as run_pass at SP = 1)
-    rmsnorm(h_in, d, Lw.attn_norm, xn1, d, n, d, c.rms_eps, nullptr, s);
-    {
-      GemmArgs ga{xn1, Lw.wqkv, nullptr, n, Cqkv, d, d, d, 0, GEMM_EPI_QKV_SCATTER, Lw.bqkv,
+    // (1) recompute the layer's attention input: RMSNorm, QKV + RoPE routed to
+    // the head shards (the forward's fused epilogue), attention with its lse
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      const int n = static_cast<int>(R.e - R.b);
+      if (n <= 0) continue;
+      const float* h_in = stash_bufs_[r].as<float>() + static_cast<size_t>(l) * n * d;
+      rmsnorm(h_in, d, Lw.attn_norm, rw[r].xn1, d, n, d, c.rms_eps, nullptr, s);
+      GemmArgs ga{rw[r].xn1, Lw.wqkv, nullptr, n, Cqkv, d, d, d, 0, GEMM_EPI_QKV_SCATTER, Lw.bqkv,
                   nullptr, 0};
       ga.pos = R.pos.as<int>();
       ga.inv_freq = d_inv_freq_;
       ga.n_rope_blocks = nq + nkv;
-      ga.row0 = 0;
+      ga.row0 = K == 1 ? 0 : R.b;
       ga.route = d_route_;
       ga.peer_base = d_peer_base_;
       ga.peer_ld = d_peer_ld_;
-      ga.row_blocks = static_cast<int>((g.Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
+      ga.row_blocks = static_cast<int>((Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
       gemm_bf16(ga, s);
     }
-    {
-      AttnParams ap{R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
-                    R.ol.p, Cq, 0, n, nq, nq / nkv, scale, ATTN_CAUSAL_PREFIX,
-                    static_cast<int>(g.Lp), g.Lmax, 0};
-      ap.lse = lse;
-      ap.lse_ld = ld_stat;
-      attention_fwd(ap, s);
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      const int nqr = R.hs.nq();
+      if (nqr == 0) continue;
+      if (K == 1) {
+        AttnParams ap{R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
+                      R.ol.p, Cq, 0, static_cast<int>(Ltot), nq, nq / nkv, scale,
+                      ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0};
+        ap.lse = rw[r].stat_lse;
+        ap.lse_ld = rw[r].ld_stat;
+        attention_fwd(ap, s);
+      } else {
+        const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
+        AttnParams ap{R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr, (nqr + R.hs.nkv()) * 128,
+                      R.oh.p, nqr * 128, 0, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
+                      ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0};
+        ap.lse = rw[r].stat_lse;
+        ap.lse_ld = rw[r].ld_stat;
+        attention_fwd(ap, s);
+      }
     }
-    MRSP_CUDA(cudaMemcpyAsync(hm, h_in, nd * 4, cudaMemcpyDeviceToDevice, s));
-    gemm_bf16({R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, hm, d}, s);
-    rmsnorm(hm, d, Lw.mlp_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
-    // MLP backward
-    cast_f32_bf16(dh, d, dhb, d, n, d, s);
-    gemm_mn(dhb, d, 0, Lw.wdown, mlp, 1, dact, mlp, n, mlp, d, GEMM_EPI_STORE_BF16);
-    {
-      GemmArgs ga{R.xn.p, Lw.wgu, dgu, n, 2 * mlp, d, d, d, 2 * mlp, GEMM_EPI_SWIGLU_BWD, nullptr,
-                  nullptr, 0};
-      ga.aux = dact;
-      ga.ld_aux = mlp;
-      ga.aux_out = R.act.p;
-      ga.ld_aux_out = mlp;
-      gemm_bf16(ga, s);
+    if (K > 1)  // heads -> sequence: every head shard's O rows to the token owners
+      for (int p = 0; p < K; ++p) {
+        const HeadSplit& hp = ranks_[p].hs;
+        if (hp.nq() == 0) continue;
+        for (int r = 0; r < K; ++r) {
+          const RankCtx& R = ranks_[r];
+          if (R.e <= R.b) continue;
+          MRSP_CUDA(cudaMemcpy2DAsync(R.ol.as<bf16>() + hp.q_lo * 128, static_cast<size_t>(Cq) * 2,
+                                      ranks_[p].oh.as<bf16>() + static_cast<size_t>(R.b) * hp.nq() * 128,
+                                      static_cast<size_t>(hp.nq()) * 128 * 2,
+                                      static_cast<size_t>(hp.nq()) * 128 * 2, R.e - R.b,
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    // (2) per sequence shard: O projection, MLP recompute, MLP backward, the
+    // post-attention RMSNorm backward, dO
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      RW& w = rw[r];
+      const int n = static_cast<int>(R.e - R.b);
+      if (n <= 0) continue;
+      const size_t nd = static_cast<size_t>(n) * d;
+      const float* h_in = stash_bufs_[r].as<float>() + static_cast<size_t>(l) * nd;
+      MRSP_CUDA(cudaMemcpyAsync(w.hm, h_in, nd * 4, cudaMemcpyDeviceToDevice, s));
+      gemm_bf16({R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, w.hm, d}, s);
+      rmsnorm(w.hm, d, Lw.mlp_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
+      cast_f32_bf16(w.dh, d, w.dhb, d, n, d, s);
+      gemm_mn(w.dhb, d, 0, Lw.wdown, mlp, 1, w.dact, mlp, n, mlp, d, GEMM_EPI_STORE_BF16);
+      {
+        GemmArgs ga{R.xn.p, Lw.wgu, w.dgu, n, 2 * mlp, d, d, d, 2 * mlp, GEMM_EPI_SWIGLU_BWD,
+                    nullptr, nullptr, 0};
+        ga.aux = w.dact;
+        ga.ld_aux = mlp;
+        ga.aux_out = R.act.p;
+        ga.ld_aux_out = mlp;
+        gemm_bf16(ga, s);
+      }
+      gemm_mn(w.dhb, d, 1, R.act.p, mlp, 1, Lg.wdown, mlp, d, mlp, n, ACC);
+      gemm_mn(w.dgu, 2 * mlp, 1, R.xn.p, d, 1, Lg.wgu, d, 2 * mlp, d, n, ACC);
+      gemm_mn(w.dgu, 2 * mlp, 0, Lw.wgu, d, 1, w.dx, d, n, d, 2 * mlp, GEMM_EPI_STORE_F32);
+      rmsnorm_bwd(w.hm, d, Lw.mlp_norm, w.dx, d, w.dh, d, n, d, c.rms_eps, nullptr, Lg.mlp_norm,
+                  w.ws, s);
+      cast_f32_bf16(w.dh, d, w.dhb, d, n, d, s);
+      gemm_mn(w.dhb, d, 0, Lw.wo, Cq, 1, w.dO, Cq, n, Cq, d, GEMM_EPI_STORE_BF16);
+      gemm_mn(w.dhb, d, 1, R.ol.p, Cq, 1, Lg.wo, Cq, d, Cq, n, ACC);
     }
-    gemm_mn(dhb, d, 1, R.act.p, mlp, 1, Lg.wdown, mlp, d, mlp, n, GEMM_EPI_STORE_F32);
-    gemm_mn(dgu, 2 * mlp, 1, R.xn.p, d, 1, Lg.wgu, d, 2 * mlp, d, n, GEMM_EPI_STORE_F32);
-    gemm_mn(dgu, 2 * mlp, 0, Lw.wgu, d, 1, dx, d, n, d, 2 * mlp, GEMM_EPI_STORE_F32);
-    rmsnorm_bwd(hm, d, Lw.mlp_norm, dx, d, dh, d, n, d, c.rms_eps, nullptr, Lg.mlp_norm, ws, s);
-    // attention backward
-    cast_f32_bf16(dh, d, dhb, d, n, d, s);
-    gemm_mn(dhb, d, 0, Lw.wo, Cq, 1, dO, Cq, n, Cq, d, GEMM_EPI_STORE_BF16);
-    gemm_mn(dhb, d, 1, R.ol.p, Cq, 1, Lg.wo, Cq, d, Cq, n, GEMM_EPI_STORE_F32);
-    {
+    if (K > 1)  // sequence -> heads: every shard's dO columns to the head owners
+      for (int r = 0; r < K; ++r) {
+        const RankCtx& R = ranks_[r];
+        if (R.e <= R.b) continue;
+        for (int p = 0; p < K; ++p) {
+          const HeadSplit& hp = ranks_[p].hs;
+          if (hp.nq() == 0) continue;
+          MRSP_CUDA(cudaMemcpy2DAsync(rw[p].doh + static_cast<size_t>(R.b) * hp.nq() * 128,
+                                      static_cast<size_t>(hp.nq()) * 128 * 2, rw[r].dO + hp.q_lo * 128,
+                                      static_cast<size_t>(Cq) * 2, static_cast<size_t>(hp.nq()) * 128 * 2,
+                                      R.e - R.b, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    // (3) attention backward on the head shards
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      const int nqr = R.hs.nq();
+      if (nqr == 0) continue;
       Prof pa(*this, P_BWD_ATTN);
-      AttnBwdParams bp{R.qkv.p, Cqkv, 0, nq * 128, (nq + nkv) * 128, R.ol.p, Cq, dO, Cq, lse, Dst,
-                       ld_stat, dqkv, Cqkv, n, nq, nq / nkv, scale, static_cast<int>(g.Lp), g.Lmax};
-      attention_bwd(bp, s);
+      if (K == 1) {
+        AttnBwdParams bp{R.qkv.p, Cqkv, 0, nq * 128, (nq + nkv) * 128, R.ol.p, Cq, rw[r].dO, Cq,
+                         rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat, rw[r].dqkv, Cqkv,
+                         static_cast<int>(Ltot), nq, nq / nkv, scale, static_cast<int>(g.Lp), g.Lmax};
+        attention_bwd(bp, s);
+      } else {
+        const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
+        AttnBwdParams bp{R.qh.p, Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128,
+                         rw[r].doh, nqr * 128, rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat,
+                         rw[r].dqkvh, Cr, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
+                         static_cast<int>(g.Lp), g.Lmax};
+        attention_bwd(bp, s);
+      }
     }
-    rope(dqkv, Cqkv, 0, nq + nkv, negpos, n, s);  // transpose rotation of the q / k heads
-    colsum_bf16(dqkv, Cqkv, n, Cqkv, Lg.bqkv, ws, s);
-    gemm_mn(dqkv, Cqkv, 1, xn1, d, 1, Lg.wqkv, d, Cqkv, d, n, GEMM_EPI_STORE_F32);
-    gemm_mn(dqkv, Cqkv, 0, Lw.wqkv, d, 1, dx, d, n, d, Cqkv, GEMM_EPI_STORE_F32);
-    rmsnorm_bwd(h_in, d, Lw.attn_norm, dx, d, dh, d, n, d, c.rms_eps, nullptr, Lg.attn_norm, ws, s);
+    if (K > 1)  // heads -> sequence: dq | dk | dv rows to the token owners
+      for (int p = 0; p < K; ++p) {
+        const HeadSplit& hp = ranks_[p].hs;
+        if (hp.nq() == 0) continue;
+        const int Cr = (hp.nq() + 2 * hp.nkv()) * 128;
+        const int src_col[3] = {0, hp.nq() * 128, (hp.nq() + hp.nkv()) * 128};
+        const int dst_col[3] = {hp.q_lo * 128, (nq + hp.kv_lo) * 128, (nq + nkv + hp.kv_lo) * 128};
+        const int width[3] = {hp.nq() * 128, hp.nkv() * 128, hp.nkv() * 128};
+        for (int r = 0; r < K; ++r) {
+          const RankCtx& R = ranks_[r];
+          if (R.e <= R.b) continue;
+          for (int b = 0; b < 3; ++b)
+            MRSP_CUDA(cudaMemcpy2DAsync(rw[r].dqkv + dst_col[b], static_cast<size_t>(Cqkv) * 2,
+                                        rw[p].dqkvh + static_cast<size_t>(R.b) * Cr + src_col[b],
+                                        static_cast<size_t>(Cr) * 2, static_cast<size_t>(width[b]) * 2,
+                                        R.e - R.b, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    // (4) per sequence shard: RoPE backward, QKV bias / weight gradients, dX,
+    // the input RMSNorm backward
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      RW& w = rw[r];
+      const int n = static_cast<int>(R.e - R.b);
+      if (n <= 0) continue;
+      const float* h_in = stash_bufs_[r].as<float>() + static_cast<size_t>(l) * n * d;
+      rope(w.dqkv, Cqkv, 0, nq + nkv, w.negpos, n, s);  // transpose rotation of the q / k heads
+      colsum_bf16(w.dqkv, Cqkv, n, Cqkv, Lg.bqkv, w.ws, s);
+      gemm_mn(w.dqkv, Cqkv, 1, w.xn1, d, 1, Lg.wqkv, d, Cqkv, d, n, ACC);
+      gemm_mn(w.dqkv, Cqkv, 0, Lw.wqkv, d, 1, w.dx, d, n, d, Cqkv, GEMM_EPI_STORE_F32);
+      rmsnorm_bwd(h_in, d, Lw.attn_norm, w.dx, d, w.dh, d, n, d, c.rms_eps, nullptr, Lg.attn_norm,
+                  w.ws, s);
+    }
   }
   }  // Prof P_BACKWARD
 
-  // ---- text embeddings: dE[tok] = sum of dh at the token's positions ---------
+  // ---- text embeddings: dE[tok] += dh at the token's positions, per shard ---
+  std::vector<int> blob_all;
   {
-    std::map<int, std::vector<int>> at;  // token -> ascending positions (text, non-pad)
-    for (int i = 0; i < n_q; ++i) at[question[i]].push_back(static_cast<int>(g.n_frame_tok) + i);
-    for (int r = 0; r < G; ++r)
-      for (int j = 0; j < lengths[r]; ++j) {
-        const int tok = j == 0 ? 1 /* Vocab::kEos */ : resp[static_cast<size_t>(r) * Lmax + j - 1];
-        at[tok].push_back(static_cast<int>(g.Lp + static_cast<long>(r) * Lmax + j));
-      }
-    std::vector<int> seg_tok, seg_off{0}, positions;
-    for (auto& kv : at) {
-      seg_tok.push_back(kv.first);
-      positions.insert(positions.end(), kv.second.begin(), kv.second.end());
-      seg_off.push_back(static_cast<int>(positions.size()));
-    }
-    const int n_seg = static_cast<int>(seg_tok.size());
-    std::vector<int> blob;
-    blob.insert(blob.end(), seg_tok.begin(), seg_tok.end());
-    blob.insert(blob.end(), seg_off.begin(), seg_off.end());
-    blob.insert(blob.end(), positions.begin(), positions.end());
-    int* dblob = static_cast<int*>(R.send.ensure(blob.size() * 4 + 16));
-    MRSP_CUDA(cudaMemcpyAsync(dblob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice, s));
     float* dE = reinterpret_cast<float*>(grads_.embed);
-    MRSP_CUDA(cudaMemsetAsync(dE, 0, static_cast<size_t>(V) * d * 4, s));
-    embed_grad(dh, d, dblob, dblob + n_seg, dblob + 2 * n_seg + 1, n_seg, dE, s);
-    MRSP_CUDA(cudaMemcpyAsync(stats4, d_stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (lp_out) MRSP_CUDA(cudaMemcpyAsync(lp_out, lp, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
-    MRSP_CUDA(cudaStreamSynchronize(s));  // host blob goes out of scope
+    std::vector<std::pair<int, long>> tp;  // (token, global position) of the text positions
+    for (int i = 0; i < n_q; ++i) tp.emplace_back(question[i], g.n_frame_tok + i);
+    for (int r = 0; r < G; ++r)
+      for (int j = 0; j < lengths[r]; ++j)
+        tp.emplace_back(j == 0 ? 1 /* Vocab::kEos */ : resp[static_cast<size_t>(r) * Lmax + j - 1],
+                        g.Lp + static_cast<long>(r) * Lmax + j);
+    for (int r = 0; r < K; ++r) {
+      RankCtx& R = ranks_[r];
+      std::map<int, std::vector<int>> at;  // token -> ascending local rows
+      for (const auto& t : tp)
+        if (t.second >= R.b && t.second < R.e) at[t.first].push_back(static_cast<int>(t.second - R.b));
+      if (at.empty()) continue;
+      std::vector<int> seg_tok, seg_off{0}, positions;
+      for (auto& kv : at) {
+        seg_tok.push_back(kv.first);
+        positions.insert(positions.end(), kv.second.begin(), kv.second.end());
+        seg_off.push_back(static_cast<int>(positions.size()));
+      }
+      const int n_seg = static_cast<int>(seg_tok.size());
+      std::vector<int> blob;
+      blob.insert(blob.end(), seg_tok.begin(), seg_tok.end());
+      blob.insert(blob.end(), seg_off.begin(), seg_off.end());
+      blob.insert(blob.end(), positions.begin(), positions.end());
+      int* dblob = static_cast<int*>(R.send.ensure(blob.size() * 4 + 16));
+      MRSP_CUDA(cudaMemcpyAsync(dblob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice, s));
+      embed_grad(rw[r].dh, d, dblob, dblob + n_seg, dblob + 2 * n_seg + 1, n_seg, dE, s);
+      MRSP_CUDA(cudaStreamSynchronize(s));  // the host blob goes out of scope
+    }
   }
+  MRSP_CUDA(cudaMemcpyAsync(stats4, d_stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (lp_out) MRSP_CUDA(cudaMemcpyAsync(lp_out, lp_f, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
+  MRSP_CUDA(cudaStreamSynchronize(s));
   prof_collect();
   have_grads_ = true;
 }

@@ -151,7 +151,7 @@ def test_rmsnorm_backward(gpu):
     dy = torch.randn(n, d, device="cuda", generator=g)
     y.backward(dy)
     acc = torch.ones(n, d, device="cuda")
-    dw = torch.empty(d, device="cuda")
+    dw = torch.zeros(d, device="cuda")
     _lib.check(_lib.lib().mrsp_op_rmsnorm_bwd(vp(x), d, vp(w), vp(dy), d, vp(acc), d, n, d, 1e-6,
                                               None, vp(dw), None))
     torch.cuda.synchronize()
@@ -305,13 +305,65 @@ def test_grpo_backward_gqa7_vs_autograd(gpu):
     print("worst", _check(*out))
 
 
-def test_grpo_backward_rejects_sp(gpu):
+def test_grpo_backward_rejects_unsupported(gpu):
+    """SP above the kv-head count (query-row split) and bad inputs are
+    invalid arguments, not crashes."""
     w = E.workloads()["c1"]
-    eng = E.Engine(w.cfg, sp=2)
     pix = E.gen_video(1, w.frames, 3 * w.cfg.image_size ** 2)
-    eng.encode("v", pix)
     grp = E.make_group(w)
     n = grp.scored
-    with pytest.raises(_lib.MrspError):
+    eng = E.Engine(w.cfg, sp=4)
+    eng.encode("v", pix)
+    with pytest.raises(_lib.InvalidArgument):
         eng.grpo_backward("v", grp, np.zeros(n), np.ones(w.G))
     eng.close()
+    eng = E.Engine(w.cfg, sp=1)
+    eng.encode("v", pix)
+    with pytest.raises(ValueError):
+        eng.grpo_backward("v", grp, np.zeros(n - 1), np.ones(w.G))
+    with pytest.raises(_lib.InvalidArgument):
+        eng.grpo_backward("v", grp, np.zeros(n), np.ones(w.G), clip_eps=-1.0)
+    with pytest.raises(_lib.InvalidArgument):
+        eng.save_grads("/tmp/none.safetensors")  # no gradients yet
+    eng.close()
+
+
+def _grads(cfg, frames, sp, grp, old, adv, sampled=False):
+    c = T.Cfg.from_any(cfg)
+    pix = E.gen_video(1, frames, 3 * c.image_size ** 2)
+    eng = E.Engine(cfg, sp=sp, vision_seed=2, policy_seed=3, ref_seed=4)
+    vid = E.video_id(1, frames)
+    eng.encode(vid, pix)
+    stats, lp = eng.grpo_backward(vid, grp, old, adv, 0.2, 0.04, sampled)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "g.safetensors")
+        eng.save_grads(path)
+        got = E.read_safetensors(path)
+    eng.close()
+    return stats, lp, got
+
+
+@pytest.mark.parametrize("wname,sps", [("c1", (2,)), ("c2", (2, 4))])
+def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
+    """Sequence-parallel backward (virtual ranks: head-sharded attention
+    backward, dO / dq dk dv exchanged between sequence and head shards, weight
+    gradients summed over the ranks' token shards) vs SP = 1: every per-token
+    quantity is computed by the same kernels on the same rows, so log-probs and
+    the group statistics are bit-identical; the weight gradients differ only by
+    the order of the per-shard token sums."""
+    w = E.workloads()[wname]
+    grp = E.make_group(w, seed=5)
+    n = grp.scored
+    rng = np.random.default_rng(1)
+    base_stats, base_lp, base = _grads(w.cfg, w.frames, 1, grp, np.zeros(n, np.float32),
+                                       np.ones(w.G, np.float32))
+    old = base_lp - rng.choice([-0.5, -0.05, 0.05, 0.5], size=n).astype(np.float32)
+    adv = rng.normal(size=w.G).astype(np.float32)
+    base_stats, base_lp, base = _grads(w.cfg, w.frames, 1, grp, old, adv)
+    for sp in sps:
+        stats, lp, got = _grads(w.cfg, w.frames, sp, grp, old, adv)
+        assert np.array_equal(lp, base_lp), sp
+        assert stats == base_stats, sp
+        worst = max(rel(got[k], base[k]) for k in base if np.linalg.norm(base[k]) > 0)
+        print(wname, "sp", sp, "worst grad rel diff vs sp1", worst)
+        assert worst < 1e-4, (sp, worst)
