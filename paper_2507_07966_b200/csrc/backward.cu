@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "attn_common.cuh"
 #include "backward.h"
@@ -505,6 +506,457 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ----------------------------------------------------------------------------
+// v2: the same two kernels with the S / dP work split into 64-wide halves and
+// TWO TMEM buffers, so the tensor core computes the next half's S and dP (and
+// the previous half's accumulator MMAs) while the softmax warps turn this
+// half's S, dP into P, dS — v1 leaves the tensor pipe idle during every
+// softmax (41-44% busy under ncu). TMEM = [S_0 | dP_0] [S_1 | dP_1] (64 + 64
+// columns each) | two 128-column accumulators. The 64-wide S / dP MMAs
+// (M 128, N 64, both operands in smem) run at 2/3 rate (smem bandwidth); the
+// accumulator MMAs take A from TMEM at full rate.
+constexpr int H_CHUNK = 64 * 64 * 2;  // 64 rows x 64 bf16 columns, SW128 (8 KB)
+constexpr int HALF = 2 * H_CHUNK;     // 64 x 128 bf16 (16 KB)
+
+__device__ __forceinline__ uint32_t half_kmajor_off(int kk) { return (kk / 4) * H_CHUNK + (kk % 4) * 32; }
+
+// Does any query of [q0, q0 + nq) see any key of [k0, k0 + nk)? (superset test;
+// the softmax warps apply the exact per-element mask)
+__device__ __forceinline__ bool range_visible(int q0, int nq, int k0, int nk, const MaskDev& m) {
+  const int q1 = min(q0 + nq - 1, m.L - 1), k1 = min(k0 + nk - 1, m.L - 1);
+  if (q0 >= m.L || k0 >= m.L || k0 > q1) return false;
+  if (k0 < m.Lp) return true;  // a prefix key: seen by every later query
+  if (q1 < m.Lp) return false;
+  const int sk0 = seg_of(k0, m), sk1 = seg_of(k1, m);
+  const int qs0 = seg_of(max(q0, m.Lp), m), qs1 = seg_of(q1, m);
+  return sk1 >= qs0 && sk0 <= qs1;
+}
+
+// dK, dV (v2): one CTA per (key tile, kv head); items = (64-query half block,
+// query head of the group).
+constexpr int KV2_RING = 4;
+constexpr int KV2_STAT = 2 * 64 * 4;
+constexpr int KV2_STAGE = (2 * HALF + KV2_STAT + 1023) / 1024 * 1024;
+constexpr int KV2_OFF_K = 0, KV2_OFF_V = TILE, KV2_OFF_RING = 2 * TILE;
+constexpr int KV2_OFF_BAR = KV2_OFF_RING + KV2_RING * KV2_STAGE;
+constexpr size_t KV2_SMEM = 1024 + KV2_OFF_BAR + 256;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dkdv2(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmQ64,
+                   const __grid_constant__ CUtensorMap tmDO64, const __grid_constant__ CUtensorMap tmLSE,
+                   const __grid_constant__ CUtensorMap tmD, BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KV2_OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* r_full = bars + 1;              // [KV2_RING]
+  uint64_t* r_empty = bars + 1 + KV2_RING;  // [KV2_RING]
+  uint64_t* s_full = bars + 1 + 2 * KV2_RING;  // [2] per TMEM buffer
+  uint64_t* ds_full = s_full + 2;              // [2]
+  uint64_t* acc_done = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+
+  const int warp = warp_id();
+  const MaskDev m = mask_of(a);
+  const int n_kt = (a.L + TK - 1) / TK;
+  const int kvh = blockIdx.x / n_kt;
+  const int kt = blockIdx.x - kvh * n_kt;
+  const int k0 = kt * TK;
+  const int q_end = k0 < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(min(k0 + TK - 1, a.L - 1), m) + 1) * a.Lmax);
+  const int qb_lo = k0 / 64, qb_hi = (q_end + 63) / 64;
+  const int n_items = max(qb_hi - qb_lo, 0) * a.q_per_kv;
+  auto next = [&](int& i, int& hh, int& qb) {
+    for (; i < n_items; ++i) {
+      qb = qb_lo + i / a.q_per_kv;
+      hh = i % a.q_per_kv;
+      if (range_visible(qb * 64, 64, k0, TK, m)) return true;
+    }
+    return false;
+  };
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmQ64);
+    tma_prefetch_desc(&tmDO64);
+    tma_prefetch_desc(&tmLSE);
+    tma_prefetch_desc(&tmD);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < KV2_RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&ds_full[b], 256);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + KV2_OFF_K + c * CHUNK, &tmQKV, kv_full, a.k_col0 + kvh * HD + c * 64, k0);
+          tma_load_2d(smem + KV2_OFF_V + c * CHUNK, &tmQKV, kv_full, a.v_col0 + kvh * HD + c * 64, k0);
+        }
+        int slot = 0;
+        uint32_t ph = 0;
+        int hh, qb;
+        for (int i = 0; next(i, hh, qb); ++i) {
+          const int h = kvh * a.q_per_kv + hh;
+          mbar_wait(&r_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&r_full[slot], 2 * HALF + KV2_STAT);
+          uint8_t* st = smem + KV2_OFF_RING + slot * KV2_STAGE;
+          for (int c = 0; c < 2; ++c) {
+            tma_load_2d(st + c * H_CHUNK, &tmQ64, &r_full[slot], a.q_col0 + h * HD + c * 64, qb * 64);
+            tma_load_2d(st + HALF + c * H_CHUNK, &tmDO64, &r_full[slot], h * HD + c * 64, qb * 64);
+          }
+          tma_load_2d(st + 2 * HALF, &tmLSE, &r_full[slot], qb * 64, h);
+          tma_load_2d(st + 2 * HALF + 256, &tmD, &r_full[slot], qb * 64, h);
+          if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TK, 64);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TK, HD);
+      const uint32_t k_addr = smem_u32(smem + KV2_OFF_K), v_addr = smem_u32(smem + KV2_OFF_V);
+      const uint32_t ring = smem_u32(smem + KV2_OFF_RING);
+      mbar_wait(kv_full, 0);
+      auto issue_sdp = [&](int it, int slot) {
+        const uint32_t tb = tmem + (it & 1) * 128;
+        const uint32_t q_addr = ring + slot * KV2_STAGE, do_addr = q_addr + HALF;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tb, sdesc_sw128(k_addr + kmajor_off(kk)), sdesc_sw128(q_addr + half_kmajor_off(kk)),
+                        idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tb + 64, sdesc_sw128(v_addr + kmajor_off(kk)),
+                        sdesc_sw128(do_addr + half_kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(&s_full[it & 1]);
+        }
+        __syncwarp();
+      };
+      auto issue_acc = [&](int it, int slot) {
+        mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = ring + slot * KV2_STAGE, do_addr = q_addr + HALF;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 64 / 16; ++kk) {
+            const uint32_t acol = (it & 1) * 128 + (kk / 2) * 32 + (kk % 2) * 8;
+            mma_bf16_ts(tmem + 256, tmem + acol, sdesc_sw128_mn(do_addr + kk * 2048, H_CHUNK),
+                        idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16_ts(tmem + 384, tmem + 64 + acol, sdesc_sw128_mn(q_addr + kk * 2048, H_CHUNK),
+                        idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&r_empty[slot]);
+        }
+        __syncwarp();
+      };
+      int slot = 0, prev = -1, it = 0;
+      uint32_t ph = 0;
+      int hh, qb;
+      for (int i = 0; next(i, hh, qb); ++i, ++it) {
+        mbar_wait(&r_full[slot], ph);
+        tc_fence_after();
+        issue_sdp(it, slot);
+        if (it > 0) issue_acc(it - 1, prev);
+        prev = slot;
+        if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
+      }
+      if (it > 0) issue_acc(it - 1, prev);
+      if (elect_one()) mma_commit(acc_done);
+      __syncwarp();
+    }
+  } else {
+    reg_alloc<200>();
+    const int hf = (warp - 4) >> 2;
+    const int ew = (warp - 4) & 3;
+    const int r = ew * 32 + lane_id();
+    const int k = k0 + r;
+    const bool row_ok = k < a.L;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int q_vis_end = !row_ok ? 0 : k < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(k, m) + 1) * a.Lmax);
+    int slot = 0, it = 0;
+    uint32_t ph = 0;
+    int hh, qb;
+    for (int i = 0; next(i, hh, qb); ++i, ++it) {
+      mbar_wait(&r_full[slot], ph);
+      const float* st_lse = reinterpret_cast<const float*>(smem + KV2_OFF_RING + slot * KV2_STAGE + 2 * HALF);
+      const float* st_d = st_lse + 64;
+      const uint32_t tb = tmem + lane_off + (it & 1) * 128;
+      mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld32(tb + hf * 32, sv);
+      tmem_ld32(tb + 64 + hf * 32, dv);
+      tmem_ld_wait();
+      const int qbase = qb * 64 + hf * 32;
+      const uint32_t vis = lt_bits(q_vis_end, qbase) & ~lt_bits(k, qbase);
+      uint32_t wp[16], wd[16];
+#pragma unroll
+      for (int j2 = 0; j2 < 16; ++j2) {
+        float p[2], g[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * j2 + e, c = hf * 32 + j;
+          p[e] = ((vis >> j) & 1u) ? exp2_mufu(__uint_as_float(sv[j]) * sl2 - st_lse[c]) : 0.f;
+          g[e] = p[e] * (__uint_as_float(dv[j]) - st_d[c]);
+        }
+        wp[j2] = pack_bf16(p[0], p[1]);
+        wd[j2] = pack_bf16(g[0], g[1]);
+      }
+      tmem_st16(tb + hf * 32, wp);
+      tmem_st16(tb + 64 + hf * 32, wd);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&ds_full[it & 1]);
+      if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
+    }
+    const int col0 = (hf ? a.k_col0 : a.v_col0) + kvh * HD;
+    const float mul = hf ? a.scale : 1.0f;
+    __nv_bfloat16* out = a.dqkv + static_cast<size_t>(k) * a.ld_dqkv + col0;
+    if (it > 0) {
+      mbar_wait(acc_done, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+    } else if (row_ok) {
+      for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// dQ (v2): one CTA per (query tile, query head); items = 64-key half tiles.
+constexpr int DQ2_RING = 4;  // K half | V half per stage
+constexpr int DQ2_STAGE = 2 * HALF;
+constexpr int DQ2_OFF_Q = 0, DQ2_OFF_DO = TILE, DQ2_OFF_RING = 2 * TILE;
+constexpr int DQ2_OFF_BAR = DQ2_OFF_RING + DQ2_RING * DQ2_STAGE;
+constexpr size_t DQ2_SMEM = 1024 + DQ2_OFF_BAR + 256;
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dq2(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV64,
+                 const __grid_constant__ CUtensorMap tmDO, BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DQ2_OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* r_full = bars + 1;
+  uint64_t* r_empty = bars + 1 + DQ2_RING;
+  uint64_t* s_full = bars + 1 + 2 * DQ2_RING;  // [2]
+  uint64_t* ds_full = s_full + 2;              // [2]
+  uint64_t* dq_done = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+
+  const int warp = warp_id();
+  const MaskDev m = mask_of(a);
+  const int n_qt = (a.L + TQ - 1) / TQ;
+  const int per_kv = n_qt * a.q_per_kv;
+  const int kvh = blockIdx.x / per_kv;
+  const int rem = blockIdx.x - kvh * per_kv;
+  const int qt = n_qt - 1 - rem / a.q_per_kv;
+  const int h = kvh * a.q_per_kv + rem % a.q_per_kv;
+  const int q0 = qt * TQ;
+  const int kb_hi = min((a.L + 63) / 64, (q0 + TQ - 1) / 64 + 1);
+  auto next = [&](int& kb) {
+    for (; kb < kb_hi; ++kb)
+      if (range_visible(q0, TQ, kb * 64, 64, m)) return true;
+    return false;
+  };
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmKV64);
+    tma_prefetch_desc(&tmDO);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < DQ2_RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&ds_full[b], 256);
+    }
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(q_full, 2 * TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + DQ2_OFF_Q + c * CHUNK, &tmQKV, q_full, a.q_col0 + h * HD + c * 64, q0);
+          tma_load_2d(smem + DQ2_OFF_DO + c * CHUNK, &tmDO, q_full, h * HD + c * 64, q0);
+        }
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int kb = 0; next(kb); ++kb) {
+          mbar_wait(&r_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&r_full[slot], DQ2_STAGE);
+          uint8_t* st = smem + DQ2_OFF_RING + slot * DQ2_STAGE;
+          for (int c = 0; c < 2; ++c) {
+            tma_load_2d(st + c * H_CHUNK, &tmKV64, &r_full[slot], a.k_col0 + kvh * HD + c * 64, kb * 64);
+            tma_load_2d(st + HALF + c * H_CHUNK, &tmKV64, &r_full[slot], a.v_col0 + kvh * HD + c * 64, kb * 64);
+          }
+          if (++slot == DQ2_RING) { slot = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TQ, 64);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TQ, HD);
+      const uint32_t q_addr = smem_u32(smem + DQ2_OFF_Q), do_addr = smem_u32(smem + DQ2_OFF_DO);
+      const uint32_t ring = smem_u32(smem + DQ2_OFF_RING);
+      mbar_wait(q_full, 0);
+      auto issue_sdp = [&](int it, int slot) {
+        const uint32_t tb = tmem + (it & 1) * 128;
+        const uint32_t kh = ring + slot * DQ2_STAGE, vh = kh + HALF;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tb, sdesc_sw128(q_addr + kmajor_off(kk)), sdesc_sw128(kh + half_kmajor_off(kk)),
+                        idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tb + 64, sdesc_sw128(do_addr + kmajor_off(kk)), sdesc_sw128(vh + half_kmajor_off(kk)),
+                        idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(&s_full[it & 1]);
+        }
+        __syncwarp();
+      };
+      auto issue_acc = [&](int it, int slot) {
+        mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t kh = ring + slot * DQ2_STAGE;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 64 / 16; ++kk)
+            mma_bf16_ts(tmem + 256, tmem + (it & 1) * 128 + (kk / 2) * 32 + (kk % 2) * 8,
+                        sdesc_sw128_mn(kh + kk * 2048, H_CHUNK), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&r_empty[slot]);
+        }
+        __syncwarp();
+      };
+      int slot = 0, prev = -1, it = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; next(kb); ++kb, ++it) {
+        mbar_wait(&r_full[slot], ph);
+        tc_fence_after();
+        issue_sdp(it, slot);
+        if (it > 0) issue_acc(it - 1, prev);
+        prev = slot;
+        if (++slot == DQ2_RING) { slot = 0; ph ^= 1; }
+      }
+      if (it > 0) issue_acc(it - 1, prev);
+      if (elect_one()) mma_commit(dq_done);
+      __syncwarp();
+    }
+  } else {
+    reg_alloc<200>();
+    const int hf = (warp - 4) >> 2;
+    const int ew = (warp - 4) & 3;
+    const int r = ew * 32 + lane_id();
+    const int q = q0 + r;
+    const bool row_ok = q < a.L;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const float lse = row_ok ? a.lse[static_cast<size_t>(h) * a.ld_stat + q] : INFINITY;
+    const float Dq = row_ok ? a.D[static_cast<size_t>(h) * a.ld_stat + q] : 0.f;
+    const float sl2 = a.scale_log2;
+    const int k_end = min(q + 1, a.L), k_mid = a.Lp;
+    const int k_lo = q >= a.Lp ? a.Lp + seg_of(q, m) * a.Lmax : 0;
+    int it = 0;
+    for (int kb = 0; next(kb); ++kb, ++it) {
+      const uint32_t tb = tmem + lane_off + (it & 1) * 128;
+      mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld32(tb + hf * 32, sv);
+      tmem_ld32(tb + 64 + hf * 32, dv);
+      tmem_ld_wait();
+      const int kbase = kb * 64 + hf * 32;
+      const uint32_t vis = lt_bits(k_end, kbase) & (lt_bits(k_mid, kbase) | ~lt_bits(k_lo, kbase));
+      uint32_t w[16];
+#pragma unroll
+      for (int j2 = 0; j2 < 16; ++j2) {
+        float g[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * j2 + e;
+          const float p = ((vis >> j) & 1u) ? exp2_mufu(__uint_as_float(sv[j]) * sl2 - lse) : 0.f;
+          g[e] = p * (__uint_as_float(dv[j]) - Dq);
+        }
+        w[j2] = pack_bf16(g[0], g[1]);
+      }
+      tmem_st16(tb + hf * 32, w);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&ds_full[it & 1]);
+    }
+    __nv_bfloat16* out = a.dqkv + static_cast<size_t>(q) * a.ld_dqkv + a.q_col0 + h * HD + hf * 64;
+    if (it > 0) {
+      mbar_wait(dq_done, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + 256 + hf * 64 + c, o);
+        tmem_ld_wait();
+        if (row_ok) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * a.scale, __uint_as_float(o[2 * j + 1]) * a.scale);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+    } else if (row_ok) {
+      for (int c = 0; c < 64; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // D[h][q] = sum_c dO[q][128 h + c] * O[q][128 h + c] (fp32), one warp per (q, h).
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ dO, int ldo,
                                      const __nv_bfloat16* __restrict__ O, int ld_o, int L,
@@ -678,7 +1130,16 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
                                    static_cast<int>(DQ_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(DQ2_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(KV2_SMEM)));
     return true;
+  }();
+  // MRSP_ATTN_BWD=1: the single-buffered v1 kernels (kept for A/B)
+  static const int version = [] {
+    const char* v = std::getenv("MRSP_ATTN_BWD");
+    return v ? std::atoi(v) : 2;
   }();
   (void)attr;
   // D = rowsum(dO o O) into the workspace p.D
@@ -711,10 +1172,24 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   CUtensorMap tlse = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   CUtensorMap td = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   const int n_qt = (p.L + TQ - 1) / TQ, n_kt = (p.L + TK - 1) / TK;
-  attn_bwd_dq<<<n_qt * p.n_heads, THREADS, DQ_SMEM, stream>>>(tqkv, tdo, a);
+  if (version == 1) {
+    attn_bwd_dq<<<n_qt * p.n_heads, THREADS, DQ_SMEM, stream>>>(tqkv, tdo, a);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    attn_bwd_dkdv<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    return;
+  }
+  CUtensorMap t64 = make_tmap_bf16_2d(p.qkv, p.L, p.ld_qkv, p.ld_qkv, 64, 64);
+  CUtensorMap tdo64 = make_tmap_bf16_2d(p.dO, p.L, p.ld_do, p.ld_do, 64, 64);
+  CUtensorMap tlse64 = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
+  CUtensorMap td64 = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
+  attn_bwd_dq2<<<n_qt * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
-  attn_bwd_dkdv<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+  attn_bwd_dkdv2<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV2_SMEM, stream>>>(tqkv, t64, tdo64, tlse64,
+                                                                                  td64, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
