@@ -399,6 +399,14 @@ mrsp_status mrsp_engine_grpo_backward(mrsp_engine* e, const char* video_id,
                                       const float* old_logprobs, const float* advantages,
                                       double clip_eps, double kl_beta, int sampled_kl,
                                       double* stats4, float* logprob_policy);
+/* SFT loss and gradient (sft_loss_and_grad, grpo.cpp:208-223) of the policy
+ * LLM over the G teacher-forced rows of a group (the reference's single target
+ * row is G = 1): loss = mean over all row tokens of -log pi(y), written to
+ * loss_out (host); gradients of the loss kept like mrsp_engine_grpo_backward's;
+ * logprob_policy (host, may be NULL). */
+mrsp_status mrsp_engine_sft_backward(mrsp_engine* e, const char* video_id, const int32_t* question,
+                                     int n_q, const int32_t* resp, const int32_t* lengths, int G,
+                                     int Lmax, double* loss_out, float* logprob_policy);
 /* The last mrsp_engine_grpo_backward's gradients as F32 safetensors under the
  * policy's tensor names (model.layers.N.*, model.embed_tokens.weight, ...). */
 mrsp_status mrsp_engine_save_grads(mrsp_engine* e, const char* path);

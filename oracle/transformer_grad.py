@@ -210,3 +210,17 @@ def grpo_objective_grad(c: T.Cfg, policy_seed: int, ref_seed: int, frame_emb, qu
     J.backward()
     grads = {k: v.grad.detach().cpu().numpy() for k, v in P.items()}
     return stats, lp.detach().cpu().numpy(), grads
+
+
+def sft_loss_grad(c: T.Cfg, policy_seed: int, frame_emb, question, resp, lengths, dev="cpu",
+                  emulate_bf16_attn_bwd: bool = False):
+    """sft_loss_and_grad (grpo.cpp:208-223) over the G teacher-forced rows:
+    loss = mean over all row tokens of -log pi(y); (loss, log-probs, grads of the loss)."""
+    c = T.Cfg.from_any(c)
+    P = llm_params(c, policy_seed, "policy.", dev, grad=True)
+    xs, tg = final_hidden(c, P, frame_emb, question, resp, lengths, dev, emulate_bf16_attn_bwd)
+    lp = torch.log_softmax(xs @ P["lm_head.weight"].T, -1).gather(1, tg[:, None])[:, 0]
+    loss = -lp.mean()
+    loss.backward()
+    grads = {k: v.grad.detach().cpu().numpy() for k, v in P.items()}
+    return float(loss.detach()), lp.detach().cpu().numpy(), grads

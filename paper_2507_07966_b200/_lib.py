@@ -133,6 +133,7 @@ _sig("mrsp_op_lmhead_dual_dlogits", [_V, _V, _V, _V, _I, _I, _I, _V, _V, _F, _V,
 _sig("mrsp_engine_grpo_backward", [_V, ctypes.c_char_p, _V, _I, _V, _V, _I, _I, _V, _V,
                                    ctypes.c_double, ctypes.c_double, _I, _V, _V])
 _sig("mrsp_engine_save_grads", [_V, ctypes.c_char_p])
+_sig("mrsp_engine_sft_backward", [_V, ctypes.c_char_p, _V, _I, _V, _V, _I, _I, _V, _V])
 
 
 def lib() -> ctypes.CDLL:

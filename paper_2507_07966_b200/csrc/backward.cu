@@ -1077,6 +1077,20 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, int ld_in,
   *reinterpret_cast<__nv_bfloat162*>(out + r * ld_out + c) = __floats2bfloat162_rn(v.x, v.y);
 }
 
+__global__ void slot_sum_kernel(const float* __restrict__ slots, int n_slots, long stride, long n,
+                                float* __restrict__ out) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float v = slots[i];
+  for (int q = 1; q < n_slots; ++q) v += slots[q * stride + i];
+  out[i] = v;
+}
+
+__global__ void fill_f32_kernel(float* __restrict__ out, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+
 __global__ void negate_i32_kernel(const int* __restrict__ in, int* __restrict__ out, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = -in[i];
@@ -1244,6 +1258,21 @@ void cast_f32_bf16(const float* in, int ld_in, __nv_bfloat16* out, int ld_out, i
   if (n == 0) return;
   cast_f32_bf16_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(in, ld_in, out, ld_out,
                                                                              n_rows, n_cols);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void slot_sum_f32(const float* slots, int n_slots, long slot_stride, long n, float* out,
+                  cudaStream_t s) {
+  if (n <= 0) return;
+  slot_sum_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(slots, n_slots, slot_stride, n, out);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void fill_f32(float* out, int n, float v, cudaStream_t s) {
+  if (n <= 0) return;
+  fill_f32_kernel<<<(n + 255) / 256, 256, 0, s>>>(out, n, v);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

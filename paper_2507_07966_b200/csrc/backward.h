@@ -51,6 +51,10 @@ void colsum_bf16(const __nv_bfloat16* X, int ld, int n_rows, int n_cols, float* 
 void cast_f32_bf16(const float* in, int ld_in, __nv_bfloat16* out, int ld_out, int n_rows,
                    int n_cols, cudaStream_t s);
 void negate_i32(const int* in, int* out, int n, cudaStream_t s);
+void fill_f32(float* out, int n, float v, cudaStream_t s);
+// out[i] = sum over q = 0 .. n_slots-1 of slots[q * slot_stride + i] (in slot order)
+void slot_sum_f32(const float* slots, int n_slots, long slot_stride, long n, float* out,
+                  cudaStream_t s);
 
 // dE[tok] += sum of dh rows at the positions listed for tok (CSR: seg_tok[i] =
 // token id of segment i, seg_off[i] .. seg_off[i+1] its ascending positions).

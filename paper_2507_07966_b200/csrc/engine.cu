@@ -1506,6 +1506,9 @@ size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void
   caps.tok_row = tokens_per_frame() * cfg_.dim;
   caps.lm_rows = (max_scored + k_ - 1) / k_;
   caps.dim = cfg_.dim;
+  caps.cq_me = std::max(1, R.hs.nq()) * 128;
+  caps.cqkv = (cfg_.n_q_heads + 2 * cfg_.n_kv_heads) * 128;
+  caps.red_floats = kGradReduceChunk;
   if (blob) mesh_->export_blob(caps, blob);
   return PeerMesh::kBlobBytes;
 }
@@ -1798,6 +1801,19 @@ extern "C" mrsp_status mrsp_engine_grpo_backward(mrsp_engine* e, const char* vid
     auto entry = lookup(e, video_id);
     e->impl->grpo_backward(*entry, question, n_q, resp, lengths, G, Lmax, old_logprobs, advantages,
                            clip_eps, kl_beta, sampled_kl, stats4, logprob_policy);
+  });
+}
+
+extern "C" mrsp_status mrsp_engine_sft_backward(mrsp_engine* e, const char* video_id,
+                                                const int32_t* question, int n_q,
+                                                const int32_t* resp, const int32_t* lengths, int G,
+                                                int Lmax, double* loss_out, float* logprob_policy) {
+  return guard([&] {
+    MRSP_REQUIRE(e && video_id && resp && lengths && loss_out && (question || n_q == 0),
+                 MRSP_INVALID_ARGUMENT, "sft_loss_and_grad: null argument");
+    MRSP_REQUIRE(G >= 1, MRSP_INVALID_ARGUMENT, "sft_loss_and_grad: empty targets");
+    auto entry = lookup(e, video_id);
+    e->impl->sft_backward(*entry, question, n_q, resp, lengths, G, Lmax, loss_out, logprob_policy);
   });
 }
 

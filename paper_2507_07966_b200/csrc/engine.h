@@ -83,6 +83,10 @@ struct HeadSplit {
 
 HeadSplit head_split(int nq, int nkv, int k, int r, bool row_split = false);
 
+// fp32 elements per chunk of the cross-process weight-gradient sum (peer mesh
+// staging: one slot per rank, 16 MB each)
+constexpr long kGradReduceChunk = 4L << 20;
+
 // Column stride of one vision head in the engine's QKV / attention-output
 // storage: the real head dim (SigLIP 72: unpadded GEMMs; the attention's 3-D
 // TMA boxes zero-fill 72 -> 128 on chip) when its rows are 16-byte multiples,
@@ -181,6 +185,11 @@ class Engine {
                      const int32_t* resp, const int32_t* lengths, int G, int Lmax,
                      const float* old_lp, const float* adv, double clip_eps, double kl_beta,
                      int sampled_kl, double* stats4, float* lp_out);
+  // SFT loss and gradient (sft_loss_and_grad, grpo.cpp:208-223) of the policy
+  // over G teacher-forced rows: loss = mean over all row tokens of -log pi(y)
+  void sft_backward(const CacheEntry& emb, const int32_t* question, int n_q,
+                    const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                    double* loss_out, float* lp_out);
   // the last grpo_backward's gradients as an F32 safetensors file (policy
   // tensor names, csrc/weights_io.cpp)
   void save_grads(const std::string& path);
@@ -201,6 +210,10 @@ class Engine {
   void prepare_group(const CacheEntry& emb, const int32_t* question, int n_q,
                      const int32_t* resp, const int32_t* lengths, int G, int Lmax);
   void run_pass(const CacheEntry& emb, int model, int xs_slot);
+  void backward_pass(int mode, const CacheEntry& emb, const int32_t* question, int n_q,
+                     const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                     const float* old_lp, const float* adv, double clip_eps, double kl_beta,
+                     int sampled_kl, double* stats4, float* lp_out);
   // backward: per-layer input hidden states kept by run_pass (per local rank,
   // [layers][n][d] fp32; empty = off), the per-rank backward workspaces and
   // the fp32 gradients in the engine's weight layout

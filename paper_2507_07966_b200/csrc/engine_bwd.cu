@@ -58,19 +58,42 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
                            const int32_t* resp, const int32_t* lengths, int G, int Lmax,
                            const float* old_lp, const float* adv, double clip_eps, double kl_beta,
                            int sampled_kl, double* stats4, float* lp_out) {
+  MRSP_REQUIRE(old_lp && adv && stats4, MRSP_INVALID_ARGUMENT, "grpo_backward: null argument");
+  MRSP_REQUIRE(clip_eps >= 0.0, MRSP_INVALID_ARGUMENT, "grpo_backward: clip_eps < 0");
+  MRSP_REQUIRE(has_ref_ || kl_beta == 0.0, MRSP_INVALID_ARGUMENT,
+               "grpo_backward: the KL term needs a separate reference model");
+  backward_pass(0, emb, question, n_q, resp, lengths, G, Lmax, old_lp, adv, clip_eps, kl_beta,
+                sampled_kl, stats4, lp_out);
+}
+
+void Engine::sft_backward(const CacheEntry& emb, const int32_t* question, int n_q,
+                          const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                          double* loss_out, float* lp_out) {
+  MRSP_REQUIRE(loss_out, MRSP_INVALID_ARGUMENT, "sft_loss_and_grad: null argument");
+  double st[4] = {0, 0, 0, 0};
+  backward_pass(1, emb, question, n_q, resp, lengths, G, Lmax, nullptr, nullptr, 0.0, 0.0, 0, st,
+                lp_out);
+  *loss_out = st[0];
+}
+
+// mode 0: GRPO objective (gradient of J, ascent direction, as grpo_gradient);
+// mode 1: SFT loss = mean over the rows' tokens of -log pi(y) (gradient of the
+// loss, as sft_loss_and_grad, grpo.cpp:208-223; the reference pass is skipped).
+void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* question, int n_q,
+                           const int32_t* resp, const int32_t* lengths, int G, int Lmax,
+                           const float* old_lp, const float* adv, double clip_eps, double kl_beta,
+                           int sampled_kl, double* stats4, float* lp_out) {
   const auto& c = cfg_;
   const int d = c.dim, nq = c.n_q_heads, nkv = c.n_kv_heads, mlp = c.mlp, V = c.vocab;
   const int Cqkv = (nq + 2 * nkv) * 128, Cq = nq * 128, NL = c.layers;
-  MRSP_REQUIRE(!mesh_ && !nccl_, MRSP_INVALID_ARGUMENT,
-               "grpo_backward: built for one-process engines (SP ranks as virtual ranks); the "
-               "multi-process backward is not built");
+  MRSP_REQUIRE(!nccl_, MRSP_INVALID_ARGUMENT,
+               "grpo_backward: built on the peer-memory transport (one process with virtual SP "
+               "ranks, or one process per GPU over CUDA IPC), not on NCCL");
+  MRSP_REQUIRE(!mesh_ || mesh_->ready(), MRSP_INVALID_ARGUMENT,
+               "grpo_backward: p2p export / import first");
   MRSP_REQUIRE(k_ <= nkv, MRSP_INVALID_ARGUMENT,
                "grpo_backward: the SP degree must divide the kv heads (head-sharded attention "
                "backward; query-row splits are forward-only)");
-  MRSP_REQUIRE(has_ref_ || kl_beta == 0.0, MRSP_INVALID_ARGUMENT,
-               "grpo_backward: the KL term needs a separate reference model");
-  MRSP_REQUIRE(old_lp && adv && stats4, MRSP_INVALID_ARGUMENT, "grpo_backward: null argument");
-  MRSP_REQUIRE(clip_eps >= 0.0, MRSP_INVALID_ARGUMENT, "grpo_backward: clip_eps < 0");
   MRSP_REQUIRE(d % 8 == 0 && mlp % 128 == 0 && V % 8 == 0, MRSP_INVALID_ARGUMENT,
                "grpo_backward: unsupported model geometry");
   std::lock_guard<std::mutex> run(run_mu_);
@@ -80,7 +103,34 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
   const long Ltot = g.Ltot;
   const int S = static_cast<int>(g.total_scored);
   MRSP_REQUIRE(S >= 1, MRSP_INVALID_ARGUMENT, "grpo_backward: the group has no scored token");
-  const int K = k_;
+  const int K = k_;                                      // SP degree
+  const int NLOC = static_cast<int>(ranks_.size());      // SP ranks in this process
+  if (mesh_)
+    MRSP_REQUIRE(Ltot <= mesh_->caps().tokens && S <= mesh_->caps().scored, MRSP_INVALID_ARGUMENT,
+                 "p2p: group exceeds the exported capacities");
+  // every global rank's scored tokens [sc_lo, sc_lo + n_sc) and LM-head slice
+  // [lm_lo, lm_lo + lm_n) in group order (scored tokens are position-ordered)
+  std::vector<long> sc_lo(K, 0), n_sc(K, 0), lm_lo(K, 0), lm_n(K, 0);
+  {
+    for (int r = 0; r < G; ++r)
+      for (int j = 0; j < lengths[r]; ++j) {
+        const long pos = g.Lp + static_cast<long>(r) * Lmax + j;
+        int p = 0;
+        while (p + 1 < K && pos >= token_b_[p + 1]) ++p;
+        ++n_sc[p];
+      }
+    for (int p = 1; p < K; ++p) sc_lo[p] = sc_lo[p - 1] + n_sc[p - 1];
+    for (int p = 0; p < K; ++p) {
+      if (spread_lm()) {
+        const long b = S / K * p + std::min<long>(p, S % K);
+        lm_lo[p] = b;
+        lm_n[p] = S / K + (p < S % K ? 1 : 0);
+      } else {
+        lm_lo[p] = sc_lo[p];
+        lm_n[p] = n_sc[p];
+      }
+    }
+  }
 
   // ---- gradient storage: fp32 in the engine's weight layout, zeroed per call
   // (every SP rank adds its tokens' share, in rank order: deterministic) -----
@@ -139,15 +189,15 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
   // ---- per-rank workspaces --------------------------------------------------
   struct RW {
     float *hm, *dh, *dx, *dxs_own, *lp, *lpr, *kl, *lsep, *lser, *stat_lse, *stat_D, *dxs;
-    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh;
+    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh, *oh;
     int* negpos;
     void *ws, *dws;
     int ld_stat;
   };
-  std::vector<RW> rw(K);
-  stash_bufs_.resize(K);
-  bwd_ws_.resize(K);
-  for (int r = 0; r < K; ++r) {
+  std::vector<RW> rw(NLOC);
+  stash_bufs_.resize(NLOC);
+  bwd_ws_.resize(NLOC);
+  for (int r = 0; r < NLOC; ++r) {
     RankCtx& R = ranks_[r];
     const int n = static_cast<int>(R.e - R.b);
     const size_t nd = static_cast<size_t>(n) * d;
@@ -169,13 +219,14 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
       w.dact = cv.take<bf16>(static_cast<size_t>(n) * mlp);
       w.dgu = cv.take<bf16>(static_cast<size_t>(n) * 2 * mlp);
       w.dO = cv.take<bf16>(static_cast<size_t>(n) * Cq);
-      w.dqkv = cv.take<bf16>(static_cast<size_t>(n) * Cqkv);
+      // dq | dk | dv of the shard: a peer-mesh landing buffer across processes
+      w.dqkv = mesh_ ? static_cast<bf16*>(mesh_->dqkv(R.g)) : cv.take<bf16>(static_cast<size_t>(n) * Cqkv);
       w.stat_lse = cv.take<float>(static_cast<size_t>(std::max(nqr, 1)) * ld_stat);
       w.stat_D = cv.take<float>(static_cast<size_t>(std::max(nqr, 1)) * ld_stat);
       w.negpos = cv.take<int>(n);
       w.Gl = cv.take<bf16>(static_cast<size_t>(lm) * V);
       w.dxs = cv.take<float>(static_cast<size_t>(lm) * d);
-      w.dxs_own = cv.take<float>(static_cast<size_t>(own) * d);
+      w.dxs_own = mesh_ ? mesh_->dxs(R.g) : cv.take<float>(static_cast<size_t>(own) * d);
       w.lp = cv.take<float>(lm);
       w.lpr = cv.take<float>(lm);
       w.kl = cv.take<float>(lm);
@@ -183,8 +234,12 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
       w.lser = cv.take<float>(lm);
       w.ws = cv.take<uint8_t>(std::max(ws_norm, ws_col));
       w.dws = cv.take<uint8_t>(dual_ws);
-      w.doh = K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128) : nullptr;
+      w.doh = mesh_ ? static_cast<bf16*>(mesh_->doh(R.g))
+            : K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128) : nullptr;
       w.dqkvh = K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * Cr) : nullptr;
+      // the recomputed O of the head shard (virtual ranks: RankCtx::oh)
+      w.oh = mesh_ ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128)
+           : K > 1 ? R.oh.as<bf16>() : nullptr;
     };
     Carve sizing{nullptr};
     layout(sizing);
@@ -196,9 +251,9 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
   }
 
   // ---- forward: reference pass, then the policy pass keeping layer inputs --
-  run_pass(emb, 1, 1);  // xs2 = reference final-norm rows
-  stash_.resize(K);
-  for (int r = 0; r < K; ++r) stash_[r] = stash_bufs_[r].as<float>();
+  if (mode == 0) run_pass(emb, 1, 1);  // xs2 = reference final-norm rows
+  stash_.resize(NLOC);
+  for (int r = 0; r < NLOC; ++r) stash_[r] = stash_bufs_[r].as<float>();
   try {
     run_pass(emb, 0, 0);  // xs = policy final-norm rows; h = h_L of every shard
   } catch (...) {
@@ -206,33 +261,55 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
     throw;
   }
   stash_.clear();
-  lm_exchange(2);  // both models' rows to the LM-head slices (spread LM head)
+  lm_exchange(mode == 0 ? 2 : 1);  // the final-norm rows to the LM-head slices (spread LM head)
   const LlmW& W = llm_[0];
-  const LlmW& Wr = llm_[1];
+  // SFT has no reference model: the dual head runs the policy against itself
+  // (KL 0, the same log-partition twice)
+  const LlmW& Wr = llm_[mode == 0 ? 1 : 0];
+  const int ref_slot = mode == 0 ? 1 : 0;
   {
     Prof pl(*this, P_LMHEAD);
-    for (int r = 0; r < K; ++r) {
+    if (mesh_) {  // the group vectors live in every rank's landing buffer
+      const long stride = mesh_->caps().scored + 16;
+      lp_f = mesh_->lp(ranks_[0].g);
+      lpr_f = lp_f + stride;
+      kl_f = lp_f + 2 * stride;
+      mesh_->barrier(s);  // every rank has read the previous group's outputs
+    }
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       if (R.lm_n == 0) continue;
       RW& w = rw[r];
       const size_t dual_ws = lmhead_dual_workspace_bytes(R.lm_n, V);
-      lmhead_dual_logprob_kl_lse(lm_rows(R, 0), W.lm_head, lm_rows(R, 1), Wr.lm_head, R.lm_n, V, d,
+      lmhead_dual_logprob_kl_lse(lm_rows(R, 0), W.lm_head, lm_rows(R, ref_slot), Wr.lm_head, R.lm_n, V, d,
                                  R.lm_idx.as<int32_t>(), w.lp, w.lpr, w.kl, w.lsep, w.lser, w.dws,
                                  dual_ws, s);
-      // slices are contiguous in group order
-      const size_t off = static_cast<size_t>(R.lm_lo) * 4, bytes = static_cast<size_t>(R.lm_n) * 4;
-      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lp_f) + off, w.lp, bytes, cudaMemcpyDeviceToDevice, s));
-      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(lpr_f) + off, w.lpr, bytes, cudaMemcpyDeviceToDevice, s));
-      MRSP_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(kl_f) + off, w.kl, bytes, cudaMemcpyDeviceToDevice, s));
+      // slices are contiguous in group order; across processes, into every rank's copy
+      const size_t off = static_cast<size_t>(R.lm_lo), bytes = static_cast<size_t>(R.lm_n) * 4;
+      for (int p = 0; p < (mesh_ ? K : 1); ++p) {
+        float* base = mesh_ ? mesh_->lp(p) : lp_f;
+        const long stride = mesh_ ? mesh_->caps().scored + 16 : 0;
+        float* dst[3] = {base, mesh_ ? base + stride : lpr_f, mesh_ ? base + 2 * stride : kl_f};
+        const float* src[3] = {w.lp, w.lpr, w.kl};
+        for (int v = 0; v < 3; ++v)
+          MRSP_CUDA(cudaMemcpyAsync(dst[v] + off, src[v], bytes, cudaMemcpyDeviceToDevice, s));
+      }
     }
+    if (mesh_) mesh_->barrier(s);  // every slice has landed
   }
-  MRSP_CUDA(cudaMemcpyAsync(old_f, old_lp, static_cast<size_t>(S) * 4, cudaMemcpyHostToDevice, s));
-  MRSP_CUDA(cudaMemcpyAsync(adv_f, adv, static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
-  grpo_stats(lp_f, old_f, lpr_f, kl_f, adv_f, g.d_len, G, clip_eps, kl_beta, sampled_kl, d_stats, s);
+  if (mode == 0) {
+    MRSP_CUDA(cudaMemcpyAsync(old_f, old_lp, static_cast<size_t>(S) * 4, cudaMemcpyHostToDevice, s));
+    MRSP_CUDA(cudaMemcpyAsync(adv_f, adv, static_cast<size_t>(G) * 4, cudaMemcpyHostToDevice, s));
+    grpo_stats(lp_f, old_f, lpr_f, kl_f, adv_f, g.d_len, G, clip_eps, kl_beta, sampled_kl, d_stats, s);
+  }
   {
   Prof pb(*this, P_BACKWARD);
-  grpo_token_coeffs(lp_f, old_f, lpr_f, adv_f, g.d_len, G, S, clip_eps, kl_beta, sampled_kl, coef_f, s);
-  const float kw = (sampled_kl || kl_beta == 0.0) ? 0.f : static_cast<float>(-kl_beta / S);
+  if (mode == 0)
+    grpo_token_coeffs(lp_f, old_f, lpr_f, adv_f, g.d_len, G, S, clip_eps, kl_beta, sampled_kl,
+                      coef_f, s);
+  else  // d(-mean log pi(y))/dlogits = (pi - onehot(y)) / n  (grpo.cpp:217-219)
+    fill_f32(coef_f, S, -1.0f / static_cast<float>(S), s);
+  const float kw = (mode != 0 || sampled_kl || kl_beta == 0.0) ? 0.f : static_cast<float>(-kl_beta / S);
   auto gemm_mn = [&](const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                      int ldc, int M, int N, int Kd, int epi) {
     if (M <= 0 || N <= 0 || Kd <= 0) return;
@@ -249,28 +326,32 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
   const int ACC = GEMM_EPI_RESID_F32;
 
   // ---- LM head (each rank's slice) and final norm (each rank's tokens) ------
-  for (int r = 0; r < K; ++r) {
+  for (int r = 0; r < NLOC; ++r) {
     RankCtx& R = ranks_[r];
     if (R.lm_n == 0) continue;
     RW& w = rw[r];
-    lmhead_dual_dlogits(lm_rows(R, 0), W.lm_head, lm_rows(R, 1), Wr.lm_head, R.lm_n, V, d,
+    lmhead_dual_dlogits(lm_rows(R, 0), W.lm_head, lm_rows(R, ref_slot), Wr.lm_head, R.lm_n, V, d,
                         R.lm_idx.as<int32_t>(), coef_f + R.lm_lo, kw, kl_f + R.lm_lo, w.lsep,
                         w.lser, w.Gl, V, s);
     gemm_mn(w.Gl, V, 0, W.lm_head, d, 1, w.dxs, d, R.lm_n, d, V, GEMM_EPI_STORE_F32);
     gemm_mn(w.Gl, V, 1, lm_rows(R, 0), d, 1, grads_.lm_head, d, V, d, R.lm_n, ACC);
   }
-  for (int r = 0; r < K; ++r) {  // the slices' dX rows back to the ranks owning the tokens
-    RankCtx& R = ranks_[r];
+  // the slices' dX rows back to the ranks owning the tokens (owner p's rows
+  // land in its dxs buffer: a virtual rank's workspace or a peer's landing)
+  auto dxs_dst = [&](int p) -> float* { return mesh_ ? mesh_->dxs(p) : rw[p].dxs_own; };
+  if (mesh_) mesh_->barrier(s);  // every owner has consumed the previous group's rows
+  for (int r = 0; r < NLOC; ++r) {
+    const RankCtx& R = ranks_[r];
     for (int p = 0; p < K; ++p) {
-      const RankCtx& P = ranks_[p];
-      const long lo = std::max<long>(R.sc_lo, P.lm_lo);
-      const long hi = std::min<long>(R.sc_lo + R.n_scored, P.lm_lo + P.lm_n);
+      const long lo = std::max<long>(sc_lo[p], R.lm_lo);
+      const long hi = std::min<long>(sc_lo[p] + n_sc[p], R.lm_lo + R.lm_n);
       if (hi <= lo) continue;
-      MRSP_CUDA(cudaMemcpyAsync(rw[r].dxs_own + (lo - R.sc_lo) * d, rw[p].dxs + (lo - P.lm_lo) * d,
+      MRSP_CUDA(cudaMemcpyAsync(dxs_dst(p) + (lo - sc_lo[p]) * d, rw[r].dxs + (lo - R.lm_lo) * d,
                                 static_cast<size_t>(hi - lo) * d * 4, cudaMemcpyDeviceToDevice, s));
     }
   }
-  for (int r = 0; r < K; ++r) {
+  if (mesh_) mesh_->barrier(s);  // every owner's rows have landed
+  for (int r = 0; r < NLOC; ++r) {
     RankCtx& R = ranks_[r];
     RW& w = rw[r];
     const int n = static_cast<int>(R.e - R.b);
@@ -287,7 +368,7 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
     LlmLayerW& Lg = grads_.layers[l];
     // (1) recompute the layer's attention input: RMSNorm, QKV + RoPE routed to
     // the head shards (the forward's fused epilogue), attention with its lse
-    for (int r = 0; r < K; ++r) {
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
@@ -305,7 +386,8 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
       ga.row_blocks = static_cast<int>((Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
       gemm_bf16(ga, s);
     }
-    for (int r = 0; r < K; ++r) {
+    if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -318,39 +400,44 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
         attention_fwd(ap, s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
-        AttnParams ap{R.qh.p, Cr, 0, R.qh.p, Cr, nqr * 128, R.qh.p, Cr, (nqr + R.hs.nkv()) * 128,
-                      R.oh.p, nqr * 128, 0, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
+        void* qh = qh_dst(R.g);
+        AttnParams ap{qh, Cr, 0, qh, Cr, nqr * 128, qh, Cr, (nqr + R.hs.nkv()) * 128,
+                      rw[r].oh, nqr * 128, 0, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
                       ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0};
         ap.lse = rw[r].stat_lse;
         ap.lse_ld = rw[r].ld_stat;
         attention_fwd(ap, s);
       }
     }
-    if (K > 1)  // heads -> sequence: every head shard's O rows to the token owners
-      for (int p = 0; p < K; ++p) {
-        const HeadSplit& hp = ranks_[p].hs;
+    if (K > 1) {  // heads -> sequence: every head shard's O rows to the token owners
+      for (int r = 0; r < NLOC; ++r) {
+        const HeadSplit& hp = ranks_[r].hs;
         if (hp.nq() == 0) continue;
-        for (int r = 0; r < K; ++r) {
-          const RankCtx& R = ranks_[r];
-          if (R.e <= R.b) continue;
-          MRSP_CUDA(cudaMemcpy2DAsync(R.ol.as<bf16>() + hp.q_lo * 128, static_cast<size_t>(Cq) * 2,
-                                      ranks_[p].oh.as<bf16>() + static_cast<size_t>(R.b) * hp.nq() * 128,
+        for (int p = 0; p < K; ++p) {
+          const long b = token_b_[p], e = token_e_[p];
+          if (e <= b) continue;
+          MRSP_CUDA(cudaMemcpy2DAsync(static_cast<bf16*>(ol_dst(p)) + hp.q_lo * 128,
+                                      static_cast<size_t>(Cq) * 2,
+                                      rw[r].oh + static_cast<size_t>(b) * hp.nq() * 128,
                                       static_cast<size_t>(hp.nq()) * 128 * 2,
-                                      static_cast<size_t>(hp.nq()) * 128 * 2, R.e - R.b,
+                                      static_cast<size_t>(hp.nq()) * 128 * 2, e - b,
                                       cudaMemcpyDeviceToDevice, s));
         }
       }
+      if (mesh_) mesh_->barrier(s);
+    }
     // (2) per sequence shard: O projection, MLP recompute, MLP backward, the
     // post-attention RMSNorm backward, dO
-    for (int r = 0; r < K; ++r) {
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       RW& w = rw[r];
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
       const size_t nd = static_cast<size_t>(n) * d;
+      bf16* ol = static_cast<bf16*>(ol_dst(R.g));
       const float* h_in = stash_bufs_[r].as<float>() + static_cast<size_t>(l) * nd;
       MRSP_CUDA(cudaMemcpyAsync(w.hm, h_in, nd * 4, cudaMemcpyDeviceToDevice, s));
-      gemm_bf16({R.ol.p, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, w.hm, d}, s);
+      gemm_bf16({ol, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, w.hm, d}, s);
       rmsnorm(w.hm, d, Lw.mlp_norm, R.xn.as<bf16>(), d, n, d, c.rms_eps, nullptr, s);
       cast_f32_bf16(w.dh, d, w.dhb, d, n, d, s);
       gemm_mn(w.dhb, d, 0, Lw.wdown, mlp, 1, w.dact, mlp, n, mlp, d, GEMM_EPI_STORE_BF16);
@@ -370,23 +457,26 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
                   w.ws, s);
       cast_f32_bf16(w.dh, d, w.dhb, d, n, d, s);
       gemm_mn(w.dhb, d, 0, Lw.wo, Cq, 1, w.dO, Cq, n, Cq, d, GEMM_EPI_STORE_BF16);
-      gemm_mn(w.dhb, d, 1, R.ol.p, Cq, 1, Lg.wo, Cq, d, Cq, n, ACC);
+      gemm_mn(w.dhb, d, 1, ol, Cq, 1, Lg.wo, Cq, d, Cq, n, ACC);
     }
-    if (K > 1)  // sequence -> heads: every shard's dO columns to the head owners
-      for (int r = 0; r < K; ++r) {
+    if (K > 1) {  // sequence -> heads: every shard's dO columns to the head owners
+      for (int r = 0; r < NLOC; ++r) {
         const RankCtx& R = ranks_[r];
         if (R.e <= R.b) continue;
         for (int p = 0; p < K; ++p) {
-          const HeadSplit& hp = ranks_[p].hs;
+          const HeadSplit hp = split_of(p);
           if (hp.nq() == 0) continue;
-          MRSP_CUDA(cudaMemcpy2DAsync(rw[p].doh + static_cast<size_t>(R.b) * hp.nq() * 128,
+          bf16* doh = mesh_ ? static_cast<bf16*>(mesh_->doh(p)) : rw[p].doh;
+          MRSP_CUDA(cudaMemcpy2DAsync(doh + static_cast<size_t>(R.b) * hp.nq() * 128,
                                       static_cast<size_t>(hp.nq()) * 128 * 2, rw[r].dO + hp.q_lo * 128,
                                       static_cast<size_t>(Cq) * 2, static_cast<size_t>(hp.nq()) * 128 * 2,
                                       R.e - R.b, cudaMemcpyDeviceToDevice, s));
         }
       }
+      if (mesh_) mesh_->barrier(s);
+    }
     // (3) attention backward on the head shards
-    for (int r = 0; r < K; ++r) {
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -398,34 +488,37 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
         attention_bwd(bp, s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
-        AttnBwdParams bp{R.qh.p, Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, R.oh.p, nqr * 128,
+        AttnBwdParams bp{qh_dst(R.g), Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, rw[r].oh, nqr * 128,
                          rw[r].doh, nqr * 128, rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat,
                          rw[r].dqkvh, Cr, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
                          static_cast<int>(g.Lp), g.Lmax};
         attention_bwd(bp, s);
       }
     }
-    if (K > 1)  // heads -> sequence: dq | dk | dv rows to the token owners
-      for (int p = 0; p < K; ++p) {
-        const HeadSplit& hp = ranks_[p].hs;
+    if (K > 1) {  // heads -> sequence: dq | dk | dv rows to the token owners
+      for (int r = 0; r < NLOC; ++r) {
+        const HeadSplit& hp = ranks_[r].hs;
         if (hp.nq() == 0) continue;
         const int Cr = (hp.nq() + 2 * hp.nkv()) * 128;
         const int src_col[3] = {0, hp.nq() * 128, (hp.nq() + hp.nkv()) * 128};
         const int dst_col[3] = {hp.q_lo * 128, (nq + hp.kv_lo) * 128, (nq + nkv + hp.kv_lo) * 128};
         const int width[3] = {hp.nq() * 128, hp.nkv() * 128, hp.nkv() * 128};
-        for (int r = 0; r < K; ++r) {
-          const RankCtx& R = ranks_[r];
-          if (R.e <= R.b) continue;
-          for (int b = 0; b < 3; ++b)
-            MRSP_CUDA(cudaMemcpy2DAsync(rw[r].dqkv + dst_col[b], static_cast<size_t>(Cqkv) * 2,
-                                        rw[p].dqkvh + static_cast<size_t>(R.b) * Cr + src_col[b],
-                                        static_cast<size_t>(Cr) * 2, static_cast<size_t>(width[b]) * 2,
-                                        R.e - R.b, cudaMemcpyDeviceToDevice, s));
+        for (int p = 0; p < K; ++p) {
+          const long b = token_b_[p], e = token_e_[p];
+          if (e <= b) continue;
+          bf16* dst = mesh_ ? static_cast<bf16*>(mesh_->dqkv(p)) : rw[p].dqkv;
+          for (int bl = 0; bl < 3; ++bl)
+            MRSP_CUDA(cudaMemcpy2DAsync(dst + dst_col[bl], static_cast<size_t>(Cqkv) * 2,
+                                        rw[r].dqkvh + static_cast<size_t>(b) * Cr + src_col[bl],
+                                        static_cast<size_t>(Cr) * 2, static_cast<size_t>(width[bl]) * 2,
+                                        e - b, cudaMemcpyDeviceToDevice, s));
         }
       }
+      if (mesh_) mesh_->barrier(s);
+    }
     // (4) per sequence shard: RoPE backward, QKV bias / weight gradients, dX,
     // the input RMSNorm backward
-    for (int r = 0; r < K; ++r) {
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       RW& w = rw[r];
       const int n = static_cast<int>(R.e - R.b);
@@ -451,7 +544,7 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
       for (int j = 0; j < lengths[r]; ++j)
         tp.emplace_back(j == 0 ? 1 /* Vocab::kEos */ : resp[static_cast<size_t>(r) * Lmax + j - 1],
                         g.Lp + static_cast<long>(r) * Lmax + j);
-    for (int r = 0; r < K; ++r) {
+    for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       std::map<int, std::vector<int>> at;  // token -> ascending local rows
       for (const auto& t : tp)
@@ -474,9 +567,36 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
       MRSP_CUDA(cudaStreamSynchronize(s));  // the host blob goes out of scope
     }
   }
-  MRSP_CUDA(cudaMemcpyAsync(stats4, d_stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (lp_out) MRSP_CUDA(cudaMemcpyAsync(lp_out, lp_f, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
+  // ---- across processes: every rank's weight gradients summed in rank order
+  // (chunked through the peer mesh's staging slots; identical on every rank)
+  if (mesh_) {
+    float* gr = static_cast<float*>(grad_buf_.p);
+    const long total = static_cast<long>(grad_bytes / 4), chunk = mesh_->caps().red_floats;
+    const int me = ranks_[0].g;
+    for (long off = 0; off < total; off += chunk) {
+      const long n = std::min(chunk, total - off);
+      mesh_->barrier(s);  // every rank has summed the previous chunk's slots
+      for (int p = 0; p < K; ++p)
+        MRSP_CUDA(cudaMemcpyAsync(mesh_->red(p) + static_cast<size_t>(me) * chunk, gr + off,
+                                  static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, s));
+      mesh_->barrier(s);  // every rank's chunk has landed
+      slot_sum_f32(mesh_->red(me), K, chunk, n, gr + off, s);
+    }
+    mesh_->barrier(s);
+  }
+  std::vector<float> lp_host(S);
+  MRSP_CUDA(cudaMemcpyAsync(lp_host.data(), lp_f, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
+  if (mode == 0)
+    MRSP_CUDA(cudaMemcpyAsync(stats4, d_stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
   MRSP_CUDA(cudaStreamSynchronize(s));
+  if (mode == 1) {  // loss = mean -log pi(y), summed in group order in double
+    double loss = 0.0;
+    for (int i = 0; i < S; ++i) loss -= lp_host[i];
+    stats4[0] = loss / S;
+    stats4[1] = stats4[2] = 0.0;
+    stats4[3] = S;
+  }
+  if (lp_out) std::copy(lp_host.begin(), lp_host.end(), lp_out);
   prof_collect();
   have_grads_ = true;
 }

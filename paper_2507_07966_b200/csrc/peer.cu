@@ -63,6 +63,10 @@ void PeerMesh::export_blob(const PeerCaps& caps, void* blob) {
   bytes_[3] = static_cast<size_t>(4) * (caps.scored + 16) * 4;
   bytes_[4] = 64 * sizeof(uint32_t);
   bytes_[5] = static_cast<size_t>(2) * caps.lm_rows * caps.dim * 2;
+  bytes_[6] = static_cast<size_t>(caps.tokens) * caps.cq_me * 2;
+  bytes_[7] = static_cast<size_t>(caps.shard) * caps.cqkv * 2;
+  bytes_[8] = static_cast<size_t>(caps.scored) * caps.dim * 4;
+  bytes_[9] = static_cast<size_t>(n_) * caps.red_floats * 4;
   uint8_t* out = static_cast<uint8_t*>(blob);
   const int32_t hdr[2] = {me_, n_};
   std::memcpy(out, hdr, 8);

@@ -12,6 +12,11 @@
 //   flags [64] u32       barrier flags, slot p written by rank p
 //   xs   [2][lm_rows][d] this rank's slice of the scored tokens' final-norm rows
 //                        (both models) for the spread LM head
+// and for the backward (engine_bwd.cu):
+//   doh  [L_cap][Cq_me]  this rank's head shard of dO (sequence -> heads)
+//   dqkv [n_cap][Cqkv]   this rank's sequence shard of dq | dk | dv (heads -> sequence)
+//   dxs  [S_cap][d] f32  dX of this rank's scored tokens from the LM-head slices
+//   red  [n][chunk] f32  staging slots of the chunked weight-gradient sum
 // A device-side barrier (st.release.sys / ld.acquire.sys on the flags)
 // orders the remote stores of one phase before the reads of the next.
 #pragma once
@@ -34,11 +39,14 @@ struct PeerCaps {
   int tok_row = 0;      // tokens per frame * dim (elements per frame)
   long lm_rows = 0;     // max scored tokens per rank's LM-head slice
   int dim = 0;          // model dim
+  int cq_me = 0;        // this rank's query-head columns (n_q heads here * 128)
+  int cqkv = 0;         // (n_q + 2 n_kv) * 128
+  long red_floats = 0;  // staging floats per rank slot of the gradient sum
 };
 
 class PeerMesh {
  public:
-  static constexpr int kBuffers = 6;  // qh, ol, emb, lp, flags, xs
+  static constexpr int kBuffers = 10;  // qh, ol, emb, lp, flags, xs, doh, dqkv, dxs, red
   static constexpr size_t kBlobBytes = 8 + kBuffers * (64 + 8);
 
   PeerMesh(int nranks, int rank);
@@ -57,6 +65,10 @@ class PeerMesh {
   void* emb(int p) const { return ptr_[p][2]; }
   float* lp(int p) const { return static_cast<float*>(ptr_[p][3]); }
   void* xs(int p) const { return ptr_[p][5]; }
+  void* doh(int p) const { return ptr_[p][6]; }
+  void* dqkv(int p) const { return ptr_[p][7]; }
+  float* dxs(int p) const { return static_cast<float*>(ptr_[p][8]); }
+  float* red(int p) const { return static_cast<float*>(ptr_[p][9]); }
   const PeerCaps& caps() const { return caps_; }
   int nranks() const { return n_; }
   int rank() const { return me_; }

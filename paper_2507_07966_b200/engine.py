@@ -327,6 +327,18 @@ class Engine:
         return dict(zip(["objective", "mean_kl", "clip_fraction", "token_count"],
                         [float(x) for x in st])), lp
 
+    def sft_backward(self, vid: str, group: Group):
+        """sft_loss_and_grad (grpo.cpp:208-223) over the group's rows as
+        teacher-forced targets; returns (loss, policy log-probs); gradients of
+        the loss stay in the engine (save_grads)."""
+        q, resp, lens = _group_arrays(group)
+        lp = np.zeros(int(lens.sum()), dtype=np.float32)
+        loss = ctypes.c_double()
+        check(_lib.lib().mrsp_engine_sft_backward(
+            self._h, vid.encode(), _ptr(q), len(q), _ptr(resp), _ptr(lens), int(resp.shape[0]),
+            int(resp.shape[1]), ctypes.byref(loss), _ptr(lp, ctypes.c_float)))
+        return float(loss.value), lp
+
     def save_grads(self, path: str) -> None:
         check(_lib.lib().mrsp_engine_save_grads(self._h, str(path).encode()))
 

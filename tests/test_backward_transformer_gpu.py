@@ -367,3 +367,35 @@ def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
         worst = max(rel(got[k], base[k]) for k in base if np.linalg.norm(base[k]) > 0)
         print(wname, "sp", sp, "worst grad rel diff vs sp1", worst)
         assert worst < 1e-4, (sp, worst)
+
+
+def test_sft_backward_c1_vs_autograd(gpu):
+    """sft_loss_and_grad (grpo.cpp:208-223) through the transformer prefill."""
+    w = E.workloads()["c1"]
+    c = T.Cfg.from_any(w.cfg)
+    grp = E.make_group(w, seed=8)
+    pix = E.gen_video(1, w.frames, 3 * c.image_size ** 2)
+    eng = E.Engine(w.cfg, sp=1, vision_seed=2, policy_seed=3, ref_seed=4, with_ref=False)
+    vid = E.video_id(1, w.frames)
+    eng.encode(vid, pix)
+    loss, lp = eng.sft_backward(vid, grp)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "g.safetensors")
+        eng.save_grads(path)
+        got = E.read_safetensors(path)
+    emb = torch.tensor(eng.embeddings(vid), dtype=torch.float64)
+    eng.close()
+    want_loss, want_lp, want = TG.sft_loss_grad(w.cfg, 3, emb, grp.question, grp.resp, grp.lengths,
+                                                "cuda")
+    assert np.abs(lp - want_lp).max() < 5e-2
+    assert loss == pytest.approx(-float(np.mean(lp.astype(np.float64))), rel=1e-12)
+    assert loss == pytest.approx(want_loss, abs=5e-3)
+    errs = {}
+    for name, ref in want.items():
+        if np.linalg.norm(ref) == 0:
+            assert np.abs(got[name]).max() == 0, name
+            continue
+        errs[name] = rel(got[name], ref)
+        t = 5e-2 if name.endswith(".bias") else 3e-2
+        assert errs[name] <= t, (name, errs[name])
+    print("sft grad errors", max(errs.values()))
