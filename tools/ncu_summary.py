@@ -45,7 +45,10 @@ def main(path, top=25):
         a[0] += 1
         a[1] += t
         a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-        a[3] += m.get("sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active", 0.0) * t
+        tp = next((m[k] for k in ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                                  "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active")
+                   if k in m), 0.0)
+        a[3] += tp * t
         total += t
     print(f"total {total:.2f} ms over {len(launches)} launches")
     print(f"{'ms':>10} {'share':>6} {'n':>5} {'GB/launch':>10} {'tensor%':>8}  kernel")
