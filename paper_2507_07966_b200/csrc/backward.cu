@@ -57,7 +57,21 @@ struct BwdArgs {
   int ld_stat;
   __nv_bfloat16* dqkv;
   int ld_dqkv;
+  // query-row split (common.h attn_row_part): only the 256-row query blocks of
+  // part row_part of row_parts (dQ rows; the dK / dV are then partial sums)
+  int row_parts, row_part, n_blocks, n_local_blocks;
 };
+
+// Query tile of dQ-kernel CTA index `rem` (kv-head-major order handled by the
+// caller): heaviest tiles first; with a row split, the part's blocks in
+// attn_row_block order.
+__device__ __forceinline__ int dq_tile(int lt, const BwdArgs& a, int n_qt) {
+  if (a.row_parts <= 1) return n_qt - 1 - lt;
+  return attn_row_block(lt >> 1, a.row_part, a.n_blocks, a.row_parts) * 2 + (lt & 1);
+}
+__device__ __forceinline__ bool own_rows(int q, const BwdArgs& a) {
+  return a.row_parts <= 1 || attn_row_part(q / ATTN_ROW_BLOCK, a.n_blocks, a.row_parts) == a.row_part;
+}
 
 __device__ __forceinline__ MaskDev mask_of(const BwdArgs& a) {
   return MaskDev{ATTN_CAUSAL_PREFIX, a.L, a.Lp, a.Lmax, 1};
@@ -92,10 +106,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = warp_id();
   const MaskDev m = mask_of(a);
   const int n_qt = (a.L + TQ - 1) / TQ, n_kt = (a.L + TK - 1) / TK;
-  const int per_kv = n_qt * a.q_per_kv;
+  const int n_tiles = a.row_parts > 1 ? 2 * a.n_local_blocks : n_qt;
+  const int per_kv = n_tiles * a.q_per_kv;
   const int kvh = blockIdx.x / per_kv;
   const int rem = blockIdx.x - kvh * per_kv;
-  const int qt = n_qt - 1 - rem / a.q_per_kv;
+  const int qt = dq_tile(rem / a.q_per_kv, a, n_qt);
   const int h = kvh * a.q_per_kv + rem % a.q_per_kv;
   const int q0 = qt * TQ;
   const int kt_hi = min(n_kt, (q0 + TQ - 1) / TK + 1);
@@ -570,7 +585,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (; i < n_items; ++i) {
       qb = qb_lo + i / a.q_per_kv;
       hh = i % a.q_per_kv;
-      if (range_visible(qb * 64, 64, k0, TK, m)) return true;
+      if (own_rows(qb * 64, a) && range_visible(qb * 64, 64, k0, TK, m)) return true;
     }
     return false;
   };
@@ -781,10 +796,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = warp_id();
   const MaskDev m = mask_of(a);
   const int n_qt = (a.L + TQ - 1) / TQ;
-  const int per_kv = n_qt * a.q_per_kv;
+  const int n_tiles = a.row_parts > 1 ? 2 * a.n_local_blocks : n_qt;
+  const int per_kv = n_tiles * a.q_per_kv;
   const int kvh = blockIdx.x / per_kv;
   const int rem = blockIdx.x - kvh * per_kv;
-  const int qt = n_qt - 1 - rem / a.q_per_kv;
+  const int qt = dq_tile(rem / a.q_per_kv, a, n_qt);
   const int h = kvh * a.q_per_kv + rem % a.q_per_kv;
   const int q0 = qt * TQ;
   const int kb_hi = min((a.L + 63) / 64, (q0 + TQ - 1) / 64 + 1);
@@ -1130,11 +1146,85 @@ __global__ void grpo_coeff_kernel(const float* __restrict__ lp, const float* __r
   }
 }
 
+// seq -> heads: one CTA per sequence row of this rank.
+__global__ void route_seq_to_heads_kernel(RouteArgs ra, long b, const __nv_bfloat16* __restrict__ dO,
+                                          int ld_do, const float* __restrict__ Dseq, int ld_dseq) {
+  const int r = blockIdx.x;
+  const long q = b + r;
+  const int blk = static_cast<int>(q / ATTN_ROW_BLOCK);
+  for (int p = 0; p < ra.K; ++p) {
+    const RouteRank& P = ra.r[p];
+    const int nqp = P.q_hi - P.q_lo;
+    if (nqp <= 0) continue;
+    if (P.rparts > 1 && attn_row_part(blk, ra.n_blocks, P.rparts) != P.rpart) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(dO + static_cast<size_t>(r) * ld_do + P.q_lo * 128);
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(P.doh) + q * nqp * 128);
+    for (int i = threadIdx.x; i < nqp * 16; i += blockDim.x) dst[i] = src[i];
+    for (int h = threadIdx.x; h < nqp; h += blockDim.x)
+      P.Dh[static_cast<size_t>(h) * P.ld_stat + q] = Dseq[static_cast<size_t>(P.q_lo + h) * ld_dseq + r];
+  }
+}
+
+// heads -> seq: one CTA per sequence row (all L rows) of head rank p.
+__global__ void route_heads_to_seq_kernel(RouteArgs ra, int p, const __nv_bfloat16* __restrict__ dqkvh,
+                                          int ld_h) {
+  const long q = blockIdx.x;
+  const RouteRank& P = ra.r[p];
+  int o = 0;
+  while (o + 1 < ra.K && q >= ra.r[o + 1].b) ++o;
+  const RouteRank& Ow = ra.r[o];
+  const long row = q - Ow.b;
+  const int nqp = P.q_hi - P.q_lo, nkvp = P.kv_hi - P.kv_lo;
+  const int Cqkv = (ra.nq + 2 * ra.nkv) * 128;
+  const int m = ra.K / ra.nkv > 1 ? ra.K / ra.nkv : 1;  // ranks sharing a kv head
+  const uint4* src = reinterpret_cast<const uint4*>(dqkvh + q * ld_h);
+  __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(Ow.dqkv) + row * Cqkv;
+  const bool own = P.rparts <= 1 ||
+                   attn_row_part(static_cast<int>(q / ATTN_ROW_BLOCK), ra.n_blocks, P.rparts) == P.rpart;
+  if (own) {  // dq of this rank's query heads
+    uint4* dst = reinterpret_cast<uint4*>(drow + P.q_lo * 128);
+    for (int i = threadIdx.x; i < nqp * 16; i += blockDim.x) dst[i] = src[i];
+  }
+  const uint4* sk = src + nqp * 16;
+  const uint4* sv = src + (nqp + nkvp) * 16;
+  uint4 *dk, *dv;
+  if (m == 1) {
+    dk = reinterpret_cast<uint4*>(drow + (ra.nq + P.kv_lo) * 128);
+    dv = reinterpret_cast<uint4*>(drow + (ra.nq + ra.nkv + P.kv_lo) * 128);
+  } else {  // partial: this rank's slot of the owner's [m][n][2 n_kv 128] buffer
+    __nv_bfloat16* srow = static_cast<__nv_bfloat16*>(Ow.slots) +
+                          (static_cast<size_t>(P.slot) * (Ow.e - Ow.b) + row) * (2 * ra.nkv * 128);
+    dk = reinterpret_cast<uint4*>(srow + P.kv_lo * 128);
+    dv = reinterpret_cast<uint4*>(srow + (ra.nkv + P.kv_lo) * 128);
+  }
+  for (int i = threadIdx.x; i < nkvp * 16; i += blockDim.x) {
+    dk[i] = sk[i];
+    dv[i] = sv[i];
+  }
+}
+
+// dk | dv columns of dqkv = sum over the m slots in slot order (fp32, one
+// rounding to bf16).
+__global__ void kv_partial_sum_kernel(const __nv_bfloat16* __restrict__ slots, int m, long n, int nkv,
+                                      __nv_bfloat16* __restrict__ dqkv, int nq) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int w = 2 * nkv * 128;
+  if (i >= n * w) return;
+  const long row = i / w;
+  const int c = static_cast<int>(i % w);
+  float v = 0.f;
+  for (int j = 0; j < m; ++j) v += __bfloat162float(slots[(static_cast<size_t>(j) * n + row) * w + c]);
+  const int Cqkv = (nq + 2 * nkv) * 128;
+  dqkv[row * Cqkv + nq * 128 + c] = __float2bfloat16_rn(v);
+}
+
 }  // namespace
 
 void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   MRSP_REQUIRE(p.L > 0 && p.n_heads > 0 && p.q_per_kv > 0 && p.n_heads % p.q_per_kv == 0,
                MRSP_INVALID_ARGUMENT, "attention_bwd: empty problem");
+  MRSP_REQUIRE(p.row_parts >= 1 && p.row_part >= 0 && p.row_part < p.row_parts,
+               MRSP_INVALID_ARGUMENT, "attention_bwd: bad query-row split");
   MRSP_REQUIRE(p.ld_qkv % 8 == 0 && p.ld_do % 8 == 0 && p.ld_o % 8 == 0 && p.ld_dqkv % 8 == 0 &&
                    p.ld_stat % 4 == 0 && p.ld_stat >= p.L,
                MRSP_INVALID_ARGUMENT, "attention_bwd: leading dims");
@@ -1156,8 +1246,8 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
     return v ? std::atoi(v) : 2;
   }();
   (void)attr;
-  // D = rowsum(dO o O) into the workspace p.D
-  {
+  // D = rowsum(dO o O) into the workspace p.D (unless the caller provides it)
+  if (!p.d_given) {
     const long warps = static_cast<long>(p.L) * p.n_heads;
     attn_bwd_prep_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(p.dO), p.ld_do, static_cast<const __nv_bfloat16*>(p.O),
@@ -1181,12 +1271,21 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   a.ld_stat = p.ld_stat;
   a.dqkv = static_cast<__nv_bfloat16*>(p.dqkv);
   a.ld_dqkv = p.ld_dqkv;
+  a.row_parts = p.row_parts;
+  a.row_part = p.row_part;
+  a.n_blocks = (p.L + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK;
+  a.n_local_blocks = 0;
+  if (p.row_parts > 1)
+    while (attn_row_block(a.n_local_blocks, p.row_part, a.n_blocks, p.row_parts) >= 0) ++a.n_local_blocks;
   CUtensorMap tqkv = make_tmap_bf16_2d(p.qkv, p.L, p.ld_qkv, p.ld_qkv, 128, 64);
   CUtensorMap tdo = make_tmap_bf16_2d(p.dO, p.L, p.ld_do, p.ld_do, 128, 64);
   CUtensorMap tlse = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   CUtensorMap td = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   const int n_qt = (p.L + TQ - 1) / TQ, n_kt = (p.L + TK - 1) / TK;
+  const int n_tiles = p.row_parts > 1 ? 2 * a.n_local_blocks : n_qt;
   if (version == 1) {
+    MRSP_REQUIRE(p.row_parts == 1, MRSP_INVALID_ARGUMENT,
+                 "attention_bwd: the v1 kernels have no query-row split");
     attn_bwd_dq<<<n_qt * p.n_heads, THREADS, DQ_SMEM, stream>>>(tqkv, tdo, a);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
@@ -1199,9 +1298,11 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   CUtensorMap tdo64 = make_tmap_bf16_2d(p.dO, p.L, p.ld_do, p.ld_do, 64, 64);
   CUtensorMap tlse64 = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   CUtensorMap td64 = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
-  attn_bwd_dq2<<<n_qt * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
-  count_launch();
-  MRSP_CUDA(cudaGetLastError());
+  if (n_tiles > 0) {
+    attn_bwd_dq2<<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+  }
   attn_bwd_dkdv2<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV2_SMEM, stream>>>(tqkv, t64, tdo64, tlse64,
                                                                                   td64, a);
   count_launch();
@@ -1376,3 +1477,44 @@ extern "C" mrsp_status mrsp_op_lmhead_dual_dlogits(const void* X_policy, const v
                         lse_policy, lse_ref, G, ldg, static_cast<cudaStream_t>(stream));
   });
 }
+
+namespace mrsp {
+
+void attention_rowdot(const void* dO, int ld_do, const void* O, int ld_o, int n, int n_heads,
+                      float* D, int ld_d, cudaStream_t stream) {
+  if (n <= 0 || n_heads <= 0) return;
+  const long warps = static_cast<long>(n) * n_heads;
+  attn_bwd_prep_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(dO), ld_do, static_cast<const __nv_bfloat16*>(O), ld_o, n,
+      n_heads, D, ld_d);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void route_seq_to_heads(const RouteArgs& ra, long b, long e, const void* dO, int ld_do,
+                        const float* Dseq, int ld_dseq, cudaStream_t s) {
+  if (e <= b) return;
+  route_seq_to_heads_kernel<<<static_cast<unsigned>(e - b), 128, 0, s>>>(
+      ra, b, static_cast<const __nv_bfloat16*>(dO), ld_do, Dseq, ld_dseq);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void route_heads_to_seq(const RouteArgs& ra, int p, const void* dqkvh, int ld_h, cudaStream_t s) {
+  if (ra.L <= 0) return;
+  route_heads_to_seq_kernel<<<static_cast<unsigned>(ra.L), 128, 0, s>>>(
+      ra, p, static_cast<const __nv_bfloat16*>(dqkvh), ld_h);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+void kv_partial_sum(const void* slots, int m, long n, int nkv, void* dqkv, int nq, cudaStream_t s) {
+  const long total = n * 2 * nkv * 128;
+  if (total <= 0) return;
+  kv_partial_sum_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(slots), m, n, nkv, static_cast<__nv_bfloat16*>(dqkv), nq);
+  count_launch();
+  MRSP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mrsp

@@ -1509,6 +1509,8 @@ size_t Engine::p2p_export(int max_frames, long max_tokens, long max_scored, void
   caps.cq_me = std::max(1, R.hs.nq()) * 128;
   caps.cqkv = (cfg_.n_q_heads + 2 * cfg_.n_kv_heads) * 128;
   caps.red_floats = kGradReduceChunk;
+  caps.m_kv = k_ > cfg_.n_kv_heads ? k_ / cfg_.n_kv_heads : 1;
+  caps.nkv = cfg_.n_kv_heads;
   if (blob) mesh_->export_blob(caps, blob);
   return PeerMesh::kBlobBytes;
 }

@@ -91,9 +91,6 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
                "ranks, or one process per GPU over CUDA IPC), not on NCCL");
   MRSP_REQUIRE(!mesh_ || mesh_->ready(), MRSP_INVALID_ARGUMENT,
                "grpo_backward: p2p export / import first");
-  MRSP_REQUIRE(k_ <= nkv, MRSP_INVALID_ARGUMENT,
-               "grpo_backward: the SP degree must divide the kv heads (head-sharded attention "
-               "backward; query-row splits are forward-only)");
   MRSP_REQUIRE(d % 8 == 0 && mlp % 128 == 0 && V % 8 == 0, MRSP_INVALID_ARGUMENT,
                "grpo_backward: unsupported model geometry");
   std::lock_guard<std::mutex> run(run_mu_);
@@ -104,6 +101,7 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   const int S = static_cast<int>(g.total_scored);
   MRSP_REQUIRE(S >= 1, MRSP_INVALID_ARGUMENT, "grpo_backward: the group has no scored token");
   const int K = k_;                                      // SP degree
+  const int m_kv = K > nkv ? K / nkv : 1;                // ranks sharing one kv head
   const int NLOC = static_cast<int>(ranks_.size());      // SP ranks in this process
   if (mesh_)
     MRSP_REQUIRE(Ltot <= mesh_->caps().tokens && S <= mesh_->caps().scored, MRSP_INVALID_ARGUMENT,
@@ -189,7 +187,9 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   // ---- per-rank workspaces --------------------------------------------------
   struct RW {
     float *hm, *dh, *dx, *dxs_own, *lp, *lpr, *kl, *lsep, *lser, *stat_lse, *stat_D, *dxs;
-    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh, *oh;
+    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh, *slots;
+    float* dseq;  // [nq][ld_dseq] row dots of dO and O on the sequence side
+    int ld_dseq;
     int* negpos;
     void *ws, *dws;
     int ld_stat;
@@ -237,9 +237,14 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       w.doh = mesh_ ? static_cast<bf16*>(mesh_->doh(R.g))
             : K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128) : nullptr;
       w.dqkvh = K > 1 ? cv.take<bf16>(static_cast<size_t>(Ltot) * Cr) : nullptr;
-      // the recomputed O of the head shard (virtual ranks: RankCtx::oh)
-      w.oh = mesh_ ? cv.take<bf16>(static_cast<size_t>(Ltot) * std::max(nqr, 1) * 128)
-           : K > 1 ? R.oh.as<bf16>() : nullptr;
+      w.ld_dseq = (n + 3) / 4 * 4;
+      w.dseq = K > 1 ? cv.take<float>(static_cast<size_t>(nq) * w.ld_dseq) : nullptr;
+      // dk | dv partials of kv heads shared by m ranks, one slot per sharer
+      w.slots = (K > 1 && m_kv > 1)
+                    ? (mesh_ ? static_cast<bf16*>(mesh_->kv_slots(R.g))
+                             : cv.take<bf16>(static_cast<size_t>(m_kv) * n * 2 * nkv * 128))
+                    : nullptr;
+      if (mesh_) w.stat_D = mesh_->dh_stat(R.g);  // routed by every sequence rank
     };
     Carve sizing{nullptr};
     layout(sizing);
@@ -248,6 +253,49 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
     layout(cv);
     w.ld_stat = ld_stat;
     stash_bufs_[r].ensure(std::max<size_t>(static_cast<size_t>(NL) * nd * 4, 256));
+  }
+
+  // Ulysses routing of the backward (every global rank's buffers; across
+  // processes the peers' landing buffers)
+  RouteArgs ra{};
+  if (K > 1) {
+    MRSP_REQUIRE(K <= 8, MRSP_INVALID_ARGUMENT, "grpo_backward: at most 8 SP ranks");
+    ra.K = K;
+    ra.nq = nq;
+    ra.nkv = nkv;
+    ra.L = Ltot;
+    ra.n_blocks = static_cast<int>((Ltot + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK);
+    for (int p = 0; p < K; ++p) {
+      const HeadSplit hp = split_of(p);
+      RouteRank& q = ra.r[p];
+      q.q_lo = hp.q_lo;
+      q.q_hi = hp.q_hi;
+      q.kv_lo = hp.kv_lo;
+      q.kv_hi = hp.kv_hi;
+      q.rparts = hp.rparts;
+      q.rpart = hp.rpart;
+      q.slot = m_kv > 1 ? p % m_kv : 0;
+      q.b = token_b_[p];
+      q.e = token_e_[p];
+      q.ld_stat = static_cast<int>((Ltot + 3) / 4 * 4);
+      if (mesh_) {
+        q.doh = mesh_->doh(p);
+        q.Dh = mesh_->dh_stat(p);
+        q.dqkv = mesh_->dqkv(p);
+        q.slots = mesh_->kv_slots(p);
+      } else {
+        q.doh = rw[p].doh;
+        q.Dh = rw[p].stat_D;
+        q.dqkv = rw[p].dqkv;
+        q.slots = rw[p].slots;
+      }
+    }
+    // a kv head shared by m ranks must be shared as a query-row split or as a
+    // split of its query heads; either way each sharer owns one slot
+    for (int p = 0; p < K; ++p)
+      MRSP_REQUIRE(m_kv == 1 || (ra.r[p].kv_hi - ra.r[p].kv_lo == 1 && ra.r[p].kv_lo == p / m_kv &&
+                                 (ra.r[p].rparts == m_kv || ra.r[p].rparts == 1)),
+                   MRSP_INVALID_ARGUMENT, "grpo_backward: unsupported head split");
   }
 
   // ---- forward: reference pass, then the policy pass keeping layer inputs --
@@ -399,33 +447,29 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
         ap.lse_ld = rw[r].ld_stat;
         attention_fwd(ap, s);
       } else {
+        // the forward's attention: head shard in, each O row stored straight
+        // into its token owner's sequence shard (fused heads -> sequence)
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
         void* qh = qh_dst(R.g);
         AttnParams ap{qh, Cr, 0, qh, Cr, nqr * 128, qh, Cr, (nqr + R.hs.nkv()) * 128,
-                      rw[r].oh, nqr * 128, 0, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
+                      nullptr, nqr * 128, 0, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
                       ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0};
+        ap.n_dst = K;
+        for (int p = 0; p < K; ++p) {
+          ap.dst_bounds[p] = token_b_[p];
+          ap.dst_base[p] = ol_dst(p);
+        }
+        ap.dst_bounds[K] = token_e_[K - 1];
+        ap.dst_ld = Cq;
+        ap.dst_col0 = R.hs.q_lo * 128;
+        ap.row_parts = R.hs.rparts;
+        ap.row_part = R.hs.rpart;
         ap.lse = rw[r].stat_lse;
         ap.lse_ld = rw[r].ld_stat;
         attention_fwd(ap, s);
       }
     }
-    if (K > 1) {  // heads -> sequence: every head shard's O rows to the token owners
-      for (int r = 0; r < NLOC; ++r) {
-        const HeadSplit& hp = ranks_[r].hs;
-        if (hp.nq() == 0) continue;
-        for (int p = 0; p < K; ++p) {
-          const long b = token_b_[p], e = token_e_[p];
-          if (e <= b) continue;
-          MRSP_CUDA(cudaMemcpy2DAsync(static_cast<bf16*>(ol_dst(p)) + hp.q_lo * 128,
-                                      static_cast<size_t>(Cq) * 2,
-                                      rw[r].oh + static_cast<size_t>(b) * hp.nq() * 128,
-                                      static_cast<size_t>(hp.nq()) * 128 * 2,
-                                      static_cast<size_t>(hp.nq()) * 128 * 2, e - b,
-                                      cudaMemcpyDeviceToDevice, s));
-        }
-      }
-      if (mesh_) mesh_->barrier(s);
-    }
+    if (mesh_) mesh_->barrier(s);  // every rank's O rows have landed
     // (2) per sequence shard: O projection, MLP recompute, MLP backward, the
     // post-attention RMSNorm backward, dO
     for (int r = 0; r < NLOC; ++r) {
@@ -458,20 +502,12 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       cast_f32_bf16(w.dh, d, w.dhb, d, n, d, s);
       gemm_mn(w.dhb, d, 0, Lw.wo, Cq, 1, w.dO, Cq, n, Cq, d, GEMM_EPI_STORE_BF16);
       gemm_mn(w.dhb, d, 1, ol, Cq, 1, Lg.wo, Cq, d, Cq, n, ACC);
+      if (K > 1) attention_rowdot(w.dO, Cq, ol, Cq, n, nq, w.dseq, w.ld_dseq, s);
     }
-    if (K > 1) {  // sequence -> heads: every shard's dO columns to the head owners
+    if (K > 1) {  // sequence -> heads: dO columns and row dots to the head owners
       for (int r = 0; r < NLOC; ++r) {
         const RankCtx& R = ranks_[r];
-        if (R.e <= R.b) continue;
-        for (int p = 0; p < K; ++p) {
-          const HeadSplit hp = split_of(p);
-          if (hp.nq() == 0) continue;
-          bf16* doh = mesh_ ? static_cast<bf16*>(mesh_->doh(p)) : rw[p].doh;
-          MRSP_CUDA(cudaMemcpy2DAsync(doh + static_cast<size_t>(R.b) * hp.nq() * 128,
-                                      static_cast<size_t>(hp.nq()) * 128 * 2, rw[r].dO + hp.q_lo * 128,
-                                      static_cast<size_t>(Cq) * 2, static_cast<size_t>(hp.nq()) * 128 * 2,
-                                      R.e - R.b, cudaMemcpyDeviceToDevice, s));
-        }
+        route_seq_to_heads(ra, R.b, R.e, rw[r].dO, Cq, rw[r].dseq, rw[r].ld_dseq, s);
       }
       if (mesh_) mesh_->barrier(s);
     }
@@ -488,33 +524,28 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
         attention_bwd(bp, s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
-        AttnBwdParams bp{qh_dst(R.g), Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, rw[r].oh, nqr * 128,
+        AttnBwdParams bp{qh_dst(R.g), Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, nullptr, nqr * 128,
                          rw[r].doh, nqr * 128, rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat,
                          rw[r].dqkvh, Cr, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
                          static_cast<int>(g.Lp), g.Lmax};
+        bp.d_given = 1;
+        bp.row_parts = R.hs.rparts;
+        bp.row_part = R.hs.rpart;
         attention_bwd(bp, s);
       }
     }
-    if (K > 1) {  // heads -> sequence: dq | dk | dv rows to the token owners
+    if (K > 1) {  // heads -> sequence: dq rows, dk / dv rows (or partials) to the owners
       for (int r = 0; r < NLOC; ++r) {
-        const HeadSplit& hp = ranks_[r].hs;
-        if (hp.nq() == 0) continue;
-        const int Cr = (hp.nq() + 2 * hp.nkv()) * 128;
-        const int src_col[3] = {0, hp.nq() * 128, (hp.nq() + hp.nkv()) * 128};
-        const int dst_col[3] = {hp.q_lo * 128, (nq + hp.kv_lo) * 128, (nq + nkv + hp.kv_lo) * 128};
-        const int width[3] = {hp.nq() * 128, hp.nkv() * 128, hp.nkv() * 128};
-        for (int p = 0; p < K; ++p) {
-          const long b = token_b_[p], e = token_e_[p];
-          if (e <= b) continue;
-          bf16* dst = mesh_ ? static_cast<bf16*>(mesh_->dqkv(p)) : rw[p].dqkv;
-          for (int bl = 0; bl < 3; ++bl)
-            MRSP_CUDA(cudaMemcpy2DAsync(dst + dst_col[bl], static_cast<size_t>(Cqkv) * 2,
-                                        rw[r].dqkvh + static_cast<size_t>(b) * Cr + src_col[bl],
-                                        static_cast<size_t>(Cr) * 2, static_cast<size_t>(width[bl]) * 2,
-                                        e - b, cudaMemcpyDeviceToDevice, s));
-        }
+        const RankCtx& R = ranks_[r];
+        if (R.hs.nq() == 0) continue;
+        route_heads_to_seq(ra, R.g, rw[r].dqkvh, (R.hs.nq() + 2 * R.hs.nkv()) * 128, s);
       }
       if (mesh_) mesh_->barrier(s);
+      if (m_kv > 1)  // kv heads shared by m ranks: their partial dk / dv summed in slot order
+        for (int r = 0; r < NLOC; ++r) {
+          const RankCtx& R = ranks_[r];
+          kv_partial_sum(rw[r].slots, m_kv, R.e - R.b, nkv, rw[r].dqkv, nq, s);
+        }
     }
     // (4) per sequence shard: RoPE backward, QKV bias / weight gradients, dX,
     // the input RMSNorm backward

@@ -17,6 +17,8 @@
 //   dqkv [n_cap][Cqkv]   this rank's sequence shard of dq | dk | dv (heads -> sequence)
 //   dxs  [S_cap][d] f32  dX of this rank's scored tokens from the LM-head slices
 //   red  [n][chunk] f32  staging slots of the chunked weight-gradient sum
+//   dh   [nq_me][L_cap] f32  row dots of dO and O for this rank's query heads
+//   kvs  [m][n_cap][2 n_kv 128] bf16  dk | dv partials of kv heads shared by m ranks
 // A device-side barrier (st.release.sys / ld.acquire.sys on the flags)
 // orders the remote stores of one phase before the reads of the next.
 #pragma once
@@ -42,11 +44,13 @@ struct PeerCaps {
   int cq_me = 0;        // this rank's query-head columns (n_q heads here * 128)
   int cqkv = 0;         // (n_q + 2 n_kv) * 128
   long red_floats = 0;  // staging floats per rank slot of the gradient sum
+  int m_kv = 1;         // ranks sharing one kv head
+  int nkv = 0;          // kv heads
 };
 
 class PeerMesh {
  public:
-  static constexpr int kBuffers = 10;  // qh, ol, emb, lp, flags, xs, doh, dqkv, dxs, red
+  static constexpr int kBuffers = 12;  // qh, ol, emb, lp, flags, xs, doh, dqkv, dxs, red, dh, kvs
   static constexpr size_t kBlobBytes = 8 + kBuffers * (64 + 8);
 
   PeerMesh(int nranks, int rank);
@@ -69,6 +73,8 @@ class PeerMesh {
   void* dqkv(int p) const { return ptr_[p][7]; }
   float* dxs(int p) const { return static_cast<float*>(ptr_[p][8]); }
   float* red(int p) const { return static_cast<float*>(ptr_[p][9]); }
+  float* dh_stat(int p) const { return static_cast<float*>(ptr_[p][10]); }
+  void* kv_slots(int p) const { return ptr_[p][11]; }
   const PeerCaps& caps() const { return caps_; }
   int nranks() const { return n_; }
   int rank() const { return me_; }

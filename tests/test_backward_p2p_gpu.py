@@ -69,8 +69,10 @@ def _worker(rank, world, port, q, td):
         q.put((rank, None, None, repr(ex)))
 
 
-def test_grpo_backward_processes_match_virtual_ranks(gpu):
-    world = 2
+@pytest.mark.parametrize("world", [2, 4])
+def test_grpo_backward_processes_match_virtual_ranks(gpu, world):
+    """world 4 > 2 kv heads: the query-row split, each kv head's dK / dV
+    partials summed on the token owners."""
     pix, grp, old, adv = _inputs()
     with tempfile.TemporaryDirectory() as td:
         ref = {}

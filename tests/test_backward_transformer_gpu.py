@@ -306,17 +306,11 @@ def test_grpo_backward_gqa7_vs_autograd(gpu):
 
 
 def test_grpo_backward_rejects_unsupported(gpu):
-    """SP above the kv-head count (query-row split) and bad inputs are
-    invalid arguments, not crashes."""
+    """Bad inputs are invalid arguments, not crashes."""
     w = E.workloads()["c1"]
     pix = E.gen_video(1, w.frames, 3 * w.cfg.image_size ** 2)
     grp = E.make_group(w)
     n = grp.scored
-    eng = E.Engine(w.cfg, sp=4)
-    eng.encode("v", pix)
-    with pytest.raises(_lib.InvalidArgument):
-        eng.grpo_backward("v", grp, np.zeros(n), np.ones(w.G))
-    eng.close()
     eng = E.Engine(w.cfg, sp=1)
     eng.encode("v", pix)
     with pytest.raises(ValueError):
@@ -343,14 +337,16 @@ def _grads(cfg, frames, sp, grp, old, adv, sampled=False):
     return stats, lp, got
 
 
-@pytest.mark.parametrize("wname,sps", [("c1", (2,)), ("c2", (2, 4))])
+@pytest.mark.parametrize("wname,sps", [("c1", (2, 4)), ("c2", (2, 4, 8))])
 def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
     """Sequence-parallel backward (virtual ranks: head-sharded attention
-    backward, dO / dq dk dv exchanged between sequence and head shards, weight
+    backward, dO / dq dk dv routed between sequence and head shards, weight
     gradients summed over the ranks' token shards) vs SP = 1: every per-token
     quantity is computed by the same kernels on the same rows, so log-probs and
-    the group statistics are bit-identical; the weight gradients differ only by
-    the order of the per-shard token sums."""
+    the group statistics are bit-identical; the weight gradients differ by the
+    order of the per-shard token sums and, above the kv-head count (c1 SP 4,
+    c2 SP 8: the forward's query-row split, a kv head shared by 2 ranks), by
+    the bf16 rounding of the two dK / dV partials before their sum."""
     w = E.workloads()[wname]
     grp = E.make_group(w, seed=5)
     n = grp.scored
@@ -366,7 +362,8 @@ def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
         assert stats == base_stats, sp
         worst = max(rel(got[k], base[k]) for k in base if np.linalg.norm(base[k]) > 0)
         print(wname, "sp", sp, "worst grad rel diff vs sp1", worst)
-        assert worst < 1e-4, (sp, worst)
+        shared_kv = sp > w.cfg.n_kv_heads
+        assert worst < (1e-2 if shared_kv else 1e-4), (sp, worst)  # measured 4.6e-3 / 2.6e-3
 
 
 def test_sft_backward_c1_vs_autograd(gpu):
