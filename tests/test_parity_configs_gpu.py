@@ -117,3 +117,35 @@ def test_c4_end_to_end_vs_oracle(gpu):
     got = _engine(w, 1, pix, grp, E.video_id(1, w.frames))
     want_emb, want_p, want_r, timing = _oracle(w, pix, grp)
     _check("c4", w, got, (want_emb, want_p, want_r), timing)
+
+
+def test_c2_generation_vs_oracle(gpu):
+    """Rollout generation at c2 width (sample_rollout,
+    policy.cpp:121-157): the old log-probs recorded while decoding G rows after
+    the 16K-token prompt, against the float64 oracle's teacher-forced log-probs
+    of the sampled tokens (its own tower and weights), at the §8c log-prob
+    tolerance."""
+    from oracle import transformer_torch as TT
+    w = E.workloads()["c2"]
+    c = T.Cfg.from_any(w.cfg)
+    pix = E.gen_video(1, w.frames, 3 * c.image_size ** 2)
+    q = np.arange(10, 10 + w.n_question, dtype=np.int32)
+    eng = E.Engine(w.cfg, sp=1, vision_seed=VSEED, policy_seed=PSEED, ref_seed=RSEED, with_ref=False)
+    eng.encode("v", pix)
+    G, max_len = 8, 32
+    tok, lens, olp = eng.generate("v", q, G, max_len, temperature=1.0, seed=5)
+    eng.close()
+    resp = np.zeros((G, max_len), dtype=np.int32)
+    for g in range(G):
+        resp[g, :lens[g]] = tok[g, :lens[g]]
+    Wv = TT.vision_weights(c, VSEED, "cuda")
+    emb = TT.vision_forward(c, Wv, pix, "cuda")
+    del Wv
+    want, _ = TT.llm_logprobs(c, PSEED, "policy.", emb, q, resp, lens, "cuda")
+    torch.cuda.empty_cache()
+    got = np.concatenate([olp[g, :lens[g]] for g in range(G)]).astype(np.float64)
+    d = np.abs(got - want)
+    rec = {"lp_max": float(d.max()), "lp_mean": float(d.mean()), "tokens": int(lens.sum())}
+    _record("c2_generation", rec)
+    print("c2 generation vs oracle", rec)
+    assert d.max() <= LP_MAX and d.mean() <= LP_MEAN, rec
