@@ -60,6 +60,11 @@ struct BwdArgs {
   // query-row split (common.h attn_row_part): only the 256-row query blocks of
   // part row_part of row_parts (dQ rows; the dK / dV are then partial sums)
   int row_parts, row_part, n_blocks, n_local_blocks;
+  // optional fp32 dK | dV output [L][ld_dkv32] (dk of local kv head g at
+  // 128 g, dv at (n_kv + g) 128) instead of bf16 into dqkv: the partials of a
+  // kv head shared by several ranks, summed before their single rounding
+  float* dkv32;
+  int ld_dkv32;
 };
 
 // Query tile of dQ-kernel CTA index `rem` (kv-head-major order handled by the
@@ -743,7 +748,32 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int col0 = (hf ? a.k_col0 : a.v_col0) + kvh * HD;
     const float mul = hf ? a.scale : 1.0f;
     __nv_bfloat16* out = a.dqkv + static_cast<size_t>(k) * a.ld_dqkv + col0;
-    if (it > 0) {
+    if (a.dkv32 != nullptr) {  // fp32 partials (a kv head shared by several ranks)
+      const int n_kv_local = a.n_heads / a.q_per_kv;
+      float* o32 = a.dkv32 + static_cast<size_t>(k) * a.ld_dkv32 + ((hf ? 0 : n_kv_local) + kvh) * HD;
+      if (it > 0) {
+        mbar_wait(acc_done, 0);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        if (it > 0) {
+          tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = 0u;
+        }
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(o32 + c)[j] =
+                make_float4(__uint_as_float(o[4 * j]) * mul, __uint_as_float(o[4 * j + 1]) * mul,
+                            __uint_as_float(o[4 * j + 2]) * mul, __uint_as_float(o[4 * j + 3]) * mul);
+        }
+      }
+    } else if (it > 0) {
       mbar_wait(acc_done, 0);
       tc_fence_after();
 #pragma unroll 1
@@ -1167,7 +1197,7 @@ __global__ void route_seq_to_heads_kernel(RouteArgs ra, long b, const __nv_bfloa
 
 // heads -> seq: one CTA per sequence row (all L rows) of head rank p.
 __global__ void route_heads_to_seq_kernel(RouteArgs ra, int p, const __nv_bfloat16* __restrict__ dqkvh,
-                                          int ld_h) {
+                                          int ld_h, const float* __restrict__ dkv32, int ld32) {
   const long q = blockIdx.x;
   const RouteRank& P = ra.r[p];
   int o = 0;
@@ -1185,27 +1215,31 @@ __global__ void route_heads_to_seq_kernel(RouteArgs ra, int p, const __nv_bfloat
     uint4* dst = reinterpret_cast<uint4*>(drow + P.q_lo * 128);
     for (int i = threadIdx.x; i < nqp * 16; i += blockDim.x) dst[i] = src[i];
   }
-  const uint4* sk = src + nqp * 16;
-  const uint4* sv = src + (nqp + nkvp) * 16;
-  uint4 *dk, *dv;
   if (m == 1) {
-    dk = reinterpret_cast<uint4*>(drow + (ra.nq + P.kv_lo) * 128);
-    dv = reinterpret_cast<uint4*>(drow + (ra.nq + ra.nkv + P.kv_lo) * 128);
-  } else {  // partial: this rank's slot of the owner's [m][n][2 n_kv 128] buffer
-    __nv_bfloat16* srow = static_cast<__nv_bfloat16*>(Ow.slots) +
-                          (static_cast<size_t>(P.slot) * (Ow.e - Ow.b) + row) * (2 * ra.nkv * 128);
-    dk = reinterpret_cast<uint4*>(srow + P.kv_lo * 128);
-    dv = reinterpret_cast<uint4*>(srow + (ra.nkv + P.kv_lo) * 128);
-  }
-  for (int i = threadIdx.x; i < nkvp * 16; i += blockDim.x) {
-    dk[i] = sk[i];
-    dv[i] = sv[i];
+    const uint4* sk = src + nqp * 16;
+    const uint4* sv = src + (nqp + nkvp) * 16;
+    uint4* dk = reinterpret_cast<uint4*>(drow + (ra.nq + P.kv_lo) * 128);
+    uint4* dv = reinterpret_cast<uint4*>(drow + (ra.nq + ra.nkv + P.kv_lo) * 128);
+    for (int i = threadIdx.x; i < nkvp * 16; i += blockDim.x) {
+      dk[i] = sk[i];
+      dv[i] = sv[i];
+    }
+  } else {  // fp32 partial: this rank's slot of the owner's [m][n][2 n_kv 128] buffer
+    const float4* s32 = reinterpret_cast<const float4*>(dkv32 + q * ld32);
+    float* srow = static_cast<float*>(Ow.slots) +
+                  (static_cast<size_t>(P.slot) * (Ow.e - Ow.b) + row) * (2 * ra.nkv * 128);
+    float4* dk = reinterpret_cast<float4*>(srow + P.kv_lo * 128);
+    float4* dv = reinterpret_cast<float4*>(srow + (ra.nkv + P.kv_lo) * 128);
+    for (int i = threadIdx.x; i < nkvp * 32; i += blockDim.x) {
+      dk[i] = s32[i];
+      dv[i] = s32[nkvp * 32 + i];
+    }
   }
 }
 
 // dk | dv columns of dqkv = sum over the m slots in slot order (fp32, one
 // rounding to bf16).
-__global__ void kv_partial_sum_kernel(const __nv_bfloat16* __restrict__ slots, int m, long n, int nkv,
+__global__ void kv_partial_sum_kernel(const float* __restrict__ slots, int m, long n, int nkv,
                                       __nv_bfloat16* __restrict__ dqkv, int nq) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int w = 2 * nkv * 128;
@@ -1213,7 +1247,7 @@ __global__ void kv_partial_sum_kernel(const __nv_bfloat16* __restrict__ slots, i
   const long row = i / w;
   const int c = static_cast<int>(i % w);
   float v = 0.f;
-  for (int j = 0; j < m; ++j) v += __bfloat162float(slots[(static_cast<size_t>(j) * n + row) * w + c]);
+  for (int j = 0; j < m; ++j) v += slots[(static_cast<size_t>(j) * n + row) * w + c];
   const int Cqkv = (nq + 2 * nkv) * 128;
   dqkv[row * Cqkv + nq * 128 + c] = __float2bfloat16_rn(v);
 }
@@ -1273,6 +1307,8 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   a.ld_dqkv = p.ld_dqkv;
   a.row_parts = p.row_parts;
   a.row_part = p.row_part;
+  a.dkv32 = p.dkv32;
+  a.ld_dkv32 = p.ld_dkv32;
   a.n_blocks = (p.L + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK;
   a.n_local_blocks = 0;
   if (p.row_parts > 1)
@@ -1284,8 +1320,8 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   const int n_qt = (p.L + TQ - 1) / TQ, n_kt = (p.L + TK - 1) / TK;
   const int n_tiles = p.row_parts > 1 ? 2 * a.n_local_blocks : n_qt;
   if (version == 1) {
-    MRSP_REQUIRE(p.row_parts == 1, MRSP_INVALID_ARGUMENT,
-                 "attention_bwd: the v1 kernels have no query-row split");
+    MRSP_REQUIRE(p.row_parts == 1 && p.dkv32 == nullptr, MRSP_INVALID_ARGUMENT,
+                 "attention_bwd: the v1 kernels have no query-row split / fp32 partials");
     attn_bwd_dq<<<n_qt * p.n_heads, THREADS, DQ_SMEM, stream>>>(tqkv, tdo, a);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
@@ -1500,10 +1536,11 @@ void route_seq_to_heads(const RouteArgs& ra, long b, long e, const void* dO, int
   MRSP_CUDA(cudaGetLastError());
 }
 
-void route_heads_to_seq(const RouteArgs& ra, int p, const void* dqkvh, int ld_h, cudaStream_t s) {
+void route_heads_to_seq(const RouteArgs& ra, int p, const void* dqkvh, int ld_h, const float* dkv32,
+                        int ld32, cudaStream_t s) {
   if (ra.L <= 0) return;
   route_heads_to_seq_kernel<<<static_cast<unsigned>(ra.L), 128, 0, s>>>(
-      ra, p, static_cast<const __nv_bfloat16*>(dqkvh), ld_h);
+      ra, p, static_cast<const __nv_bfloat16*>(dqkvh), ld_h, dkv32, ld32);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
@@ -1512,7 +1549,7 @@ void kv_partial_sum(const void* slots, int m, long n, int nkv, void* dqkv, int n
   const long total = n * 2 * nkv * 128;
   if (total <= 0) return;
   kv_partial_sum_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(slots), m, n, nkv, static_cast<__nv_bfloat16*>(dqkv), nq);
+      static_cast<const float*>(slots), m, n, nkv, static_cast<__nv_bfloat16*>(dqkv), nq);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }

@@ -37,6 +37,10 @@ struct AttnBwdParams {
   // query-row split (the forward's SP > n_kv layout): only the 256-row query
   // blocks of part row_part of row_parts; dq for those rows, dk / dv partial
   int row_parts = 1, row_part = 0;
+  // non-null: dK | dV in fp32 here ([L][ld_dkv32], local kv head g's dk at
+  // 128 g, dv at (n_kv_local + g) 128) instead of bf16 into dqkv
+  float* dkv32 = nullptr;
+  int ld_dkv32 = 0;
 };
 void attention_bwd(const AttnBwdParams& p, cudaStream_t stream);
 // D[h * ld_d + q] = sum_c dO[q][128 h + c] O[q][128 h + c], q < n (the
@@ -49,8 +53,9 @@ void attention_rowdot(const void* dO, int ld_do, const void* O, int ld_o, int n,
 //   seq -> heads: dO columns of each rank's query heads and the row dots D,
 //     only for the rows whose 256-row block the rank owns under a row split;
 //   heads -> seq: dq rows (owned blocks) to dqkv; dk / dv of every row to
-//     dqkv, or, when a kv head is shared by m ranks, into slot `rpart` of the
-//     owner's [m][n][2 n_kv 128] partial buffer (summed by kv_partial_sum).
+//     dqkv, or, when a kv head is shared by m ranks, the fp32 partials into the
+//     rank's slot of the owner's [m][n][2 n_kv 128] fp32 buffer (summed in slot
+//     order and rounded once by kv_partial_sum).
 struct RouteRank {
   int q_lo, q_hi, kv_lo, kv_hi, rparts, rpart;
   int slot;   // index among the ranks sharing its kv head (partial dk / dv slot)
@@ -59,7 +64,7 @@ struct RouteRank {
   float* Dh;   // [nq_p][ld_stat_p]
   int ld_stat;
   void* dqkv;  // [n_p][Cqkv] bf16 sequence-shard dq | dk | dv
-  void* slots; // [m][n_p][2 n_kv 128] bf16 dk | dv partials (m > 1)
+  void* slots; // [m][n_p][2 n_kv 128] fp32 dk | dv partials (m > 1)
 };
 struct RouteArgs {
   int K, nq, nkv, n_blocks;
@@ -68,7 +73,8 @@ struct RouteArgs {
 };
 void route_seq_to_heads(const RouteArgs& ra, long b, long e, const void* dO, int ld_do,
                         const float* Dseq, int ld_dseq, cudaStream_t s);
-void route_heads_to_seq(const RouteArgs& ra, int p, const void* dqkvh, int ld_h, cudaStream_t s);
+void route_heads_to_seq(const RouteArgs& ra, int p, const void* dqkvh, int ld_h, const float* dkv32,
+                        int ld32, cudaStream_t s);
 void kv_partial_sum(const void* slots, int m, long n, int nkv, void* dqkv, int nq, cudaStream_t s);
 
 // RMSNorm backward, y = w o x r, r = (mean x^2 + eps)^-1/2:

@@ -187,7 +187,8 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   // ---- per-rank workspaces --------------------------------------------------
   struct RW {
     float *hm, *dh, *dx, *dxs_own, *lp, *lpr, *kl, *lsep, *lser, *stat_lse, *stat_D, *dxs;
-    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh, *slots;
+    bf16 *dhb, *xn1, *dact, *dgu, *dO, *dqkv, *Gl, *doh, *dqkvh;
+    float *slots, *dkv32;  // shared kv heads: fp32 dk | dv partials
     float* dseq;  // [nq][ld_dseq] row dots of dO and O on the sequence side
     int ld_dseq;
     int* negpos;
@@ -241,8 +242,11 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       w.dseq = K > 1 ? cv.take<float>(static_cast<size_t>(nq) * w.ld_dseq) : nullptr;
       // dk | dv partials of kv heads shared by m ranks, one slot per sharer
       w.slots = (K > 1 && m_kv > 1)
-                    ? (mesh_ ? static_cast<bf16*>(mesh_->kv_slots(R.g))
-                             : cv.take<bf16>(static_cast<size_t>(m_kv) * n * 2 * nkv * 128))
+                    ? (mesh_ ? static_cast<float*>(mesh_->kv_slots(R.g))
+                             : cv.take<float>(static_cast<size_t>(m_kv) * n * 2 * nkv * 128))
+                    : nullptr;
+      w.dkv32 = (K > 1 && m_kv > 1)
+                    ? cv.take<float>(static_cast<size_t>(Ltot) * 2 * std::max(R.hs.nkv(), 1) * 128)
                     : nullptr;
       if (mesh_) w.stat_D = mesh_->dh_stat(R.g);  // routed by every sequence rank
     };
@@ -531,6 +535,8 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
         bp.d_given = 1;
         bp.row_parts = R.hs.rparts;
         bp.row_part = R.hs.rpart;
+        bp.dkv32 = rw[r].dkv32;
+        bp.ld_dkv32 = 2 * R.hs.nkv() * 128;
         attention_bwd(bp, s);
       }
     }
@@ -538,7 +544,8 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       for (int r = 0; r < NLOC; ++r) {
         const RankCtx& R = ranks_[r];
         if (R.hs.nq() == 0) continue;
-        route_heads_to_seq(ra, R.g, rw[r].dqkvh, (R.hs.nq() + 2 * R.hs.nkv()) * 128, s);
+        route_heads_to_seq(ra, R.g, rw[r].dqkvh, (R.hs.nq() + 2 * R.hs.nkv()) * 128, rw[r].dkv32,
+                           2 * R.hs.nkv() * 128, s);
       }
       if (mesh_) mesh_->barrier(s);
       if (m_kv > 1)  // kv heads shared by m ranks: their partial dk / dv summed in slot order

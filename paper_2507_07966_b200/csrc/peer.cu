@@ -68,7 +68,7 @@ void PeerMesh::export_blob(const PeerCaps& caps, void* blob) {
   bytes_[8] = static_cast<size_t>(caps.scored) * caps.dim * 4;
   bytes_[9] = static_cast<size_t>(n_) * caps.red_floats * 4;
   bytes_[10] = static_cast<size_t>(caps.cq_me / 128) * ((caps.tokens + 3) / 4 * 4) * 4;
-  bytes_[11] = caps.m_kv > 1 ? static_cast<size_t>(caps.m_kv) * caps.shard * 2 * caps.nkv * 128 * 2 : 0;
+  bytes_[11] = caps.m_kv > 1 ? static_cast<size_t>(caps.m_kv) * caps.shard * 2 * caps.nkv * 128 * 4 : 0;
   uint8_t* out = static_cast<uint8_t*>(blob);
   const int32_t hdr[2] = {me_, n_};
   std::memcpy(out, hdr, 8);

@@ -18,7 +18,7 @@
 //   dxs  [S_cap][d] f32  dX of this rank's scored tokens from the LM-head slices
 //   red  [n][chunk] f32  staging slots of the chunked weight-gradient sum
 //   dh   [nq_me][L_cap] f32  row dots of dO and O for this rank's query heads
-//   kvs  [m][n_cap][2 n_kv 128] bf16  dk | dv partials of kv heads shared by m ranks
+//   kvs  [m][n_cap][2 n_kv 128] f32  dk | dv partials of kv heads shared by m ranks
 // A device-side barrier (st.release.sys / ld.acquire.sys on the flags)
 // orders the remote stores of one phase before the reads of the next.
 #pragma once

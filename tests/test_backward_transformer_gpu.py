@@ -346,7 +346,8 @@ def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
     the group statistics are bit-identical; the weight gradients differ by the
     order of the per-shard token sums and, above the kv-head count (c1 SP 4,
     c2 SP 8: the forward's query-row split, a kv head shared by 2 ranks), by
-    the bf16 rounding of the two dK / dV partials before their sum."""
+    the order of the fp32 dK / dV partial sums — which flips the bf16 rounding
+    of a few dK / dV elements, amplified in the k-bias column sums."""
     w = E.workloads()[wname]
     grp = E.make_group(w, seed=5)
     n = grp.scored
@@ -363,7 +364,7 @@ def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
         worst = max(rel(got[k], base[k]) for k in base if np.linalg.norm(base[k]) > 0)
         print(wname, "sp", sp, "worst grad rel diff vs sp1", worst)
         shared_kv = sp > w.cfg.n_kv_heads
-        assert worst < (1e-2 if shared_kv else 1e-4), (sp, worst)  # measured 4.6e-3 / 2.6e-3
+        assert worst < (5e-3 if shared_kv else 1e-4), (sp, worst)  # measured 4e-6 (c1 sp4) / 2.2e-3 (c2 sp8)
 
 
 def test_sft_backward_c1_vs_autograd(gpu):
