@@ -585,14 +585,28 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int k0 = kt * TK;
   const int q_end = k0 < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(min(k0 + TK - 1, a.L - 1), m) + 1) * a.Lmax);
   const int qb_lo = k0 / 64, qb_hi = (q_end + 63) / 64;
-  const int n_items = max(qb_hi - qb_lo, 0) * a.q_per_kv;
-  auto next = [&](int& i, int& hh, int& qb) {
-    for (; i < n_items; ++i) {
-      qb = qb_lo + i / a.q_per_kv;
-      hh = i % a.q_per_kv;
-      if (own_rows(qb * 64, a) && range_visible(qb * 64, 64, k0, TK, m)) return true;
+  // Items (64-row query block, query head of the group), head-minor. Every
+  // block in [qb_lo, qb_hi) sees the key tile (prefix keys: every later query;
+  // row keys: the queries of their rows' segments, contiguous up to q_end), so
+  // the walk only skips the blocks of other row parts — incrementally, no
+  // per-item divisions (every role of every thread repeats it).
+  struct Items {
+    int qb, hh;
+    __device__ void own(const BwdArgs& a, int hi) {
+      while (qb < hi && !own_rows(qb * 64, a)) ++qb;
     }
-    return false;
+  };
+  auto items_begin = [&]() {
+    Items t{qb_lo, 0};
+    t.own(a, qb_hi);
+    return t;
+  };
+  auto items_next = [&](Items& t) {
+    if (++t.hh == a.q_per_kv) {
+      t.hh = 0;
+      ++t.qb;
+      t.own(a, qb_hi);
+    }
   };
 
   if (warp == 0 && elect_one()) {
@@ -630,9 +644,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         int slot = 0;
         uint32_t ph = 0;
-        int hh, qb;
-        for (int i = 0; next(i, hh, qb); ++i) {
-          const int h = kvh * a.q_per_kv + hh;
+        for (Items t = items_begin(); t.qb < qb_hi; items_next(t)) {
+          const int qb = t.qb, h = kvh * a.q_per_kv + t.hh;
           mbar_wait(&r_empty[slot], ph ^ 1);
           mbar_arrive_expect_tx(&r_full[slot], 2 * HALF + KV2_STAT);
           uint8_t* st = smem + KV2_OFF_RING + slot * KV2_STAGE;
@@ -686,8 +699,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       int slot = 0, prev = -1, it = 0;
       uint32_t ph = 0;
-      int hh, qb;
-      for (int i = 0; next(i, hh, qb); ++i, ++it) {
+      for (Items t = items_begin(); t.qb < qb_hi; items_next(t), ++it) {
         mbar_wait(&r_full[slot], ph);
         tc_fence_after();
         issue_sdp(it, slot);
@@ -711,11 +723,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q_vis_end = !row_ok ? 0 : k < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(k, m) + 1) * a.Lmax);
     int slot = 0, it = 0;
     uint32_t ph = 0;
-    int hh, qb;
-    for (int i = 0; next(i, hh, qb); ++i, ++it) {
+    for (Items t = items_begin(); t.qb < qb_hi; items_next(t), ++it) {
+      const int qb = t.qb;
       mbar_wait(&r_full[slot], ph);
       const float* st_lse = reinterpret_cast<const float*>(smem + KV2_OFF_RING + slot * KV2_STAGE + 2 * HALF);
       const float* st_d = st_lse + 64;
+      // this half's 32 lse and D values (broadcast 16-byte shared loads)
+      float lse_r[32], d_r[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 x = reinterpret_cast<const float4*>(st_lse + hf * 32)[j];
+        const float4 y = reinterpret_cast<const float4*>(st_d + hf * 32)[j];
+        lse_r[4 * j] = x.x; lse_r[4 * j + 1] = x.y; lse_r[4 * j + 2] = x.z; lse_r[4 * j + 3] = x.w;
+        d_r[4 * j] = y.x; d_r[4 * j + 1] = y.y; d_r[4 * j + 2] = y.z; d_r[4 * j + 3] = y.w;
+      }
       const uint32_t tb = tmem + lane_off + (it & 1) * 128;
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
@@ -731,9 +752,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         float p[2], g[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int j = 2 * j2 + e, c = hf * 32 + j;
-          p[e] = ((vis >> j) & 1u) ? exp2_mufu(__uint_as_float(sv[j]) * sl2 - st_lse[c]) : 0.f;
-          g[e] = p[e] * (__uint_as_float(dv[j]) - st_d[c]);
+          const int j = 2 * j2 + e;
+          p[e] = ((vis >> j) & 1u) ? exp2_mufu(__uint_as_float(sv[j]) * sl2 - lse_r[j]) : 0.f;
+          g[e] = p[e] * (__uint_as_float(dv[j]) - d_r[j]);
         }
         wp[j2] = pack_bf16(p[0], p[1]);
         wd[j2] = pack_bf16(g[0], g[1]);
@@ -833,12 +854,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int qt = dq_tile(rem / a.q_per_kv, a, n_qt);
   const int h = kvh * a.q_per_kv + rem % a.q_per_kv;
   const int q0 = qt * TQ;
-  const int kb_hi = min((a.L + 63) / 64, (q0 + TQ - 1) / 64 + 1);
-  auto next = [&](int& kb) {
-    for (; kb < kb_hi; ++kb)
-      if (range_visible(q0, TQ, kb * 64, 64, m)) return true;
-    return false;
-  };
+  // Keys this query tile sees, as two contiguous 64-key block ranges: the
+  // prompt [0, min(Lp, q_last + 1)) and the rows' own segments
+  // [segment start of max(q0, Lp), q_last + 1) (empty for a prompt tile)
+  const int q_last = min(q0 + TQ - 1, a.L - 1);
+  const int r1_hi = (min(a.Lp, q_last + 1) + 63) / 64;
+  int r2_lo = r1_hi, r2_hi = r1_hi;
+  if (q_last >= a.Lp) {
+    const int seg_start = a.Lp + seg_of(max(q0, a.Lp), m) * a.Lmax;
+    r2_lo = max(r1_hi, seg_start / 64);
+    r2_hi = (q_last + 1 + 63) / 64;
+  }
+  auto kb_first = [&]() { return r1_hi > 0 ? 0 : r2_lo; };
+  auto kb_next = [&](int kb) { return kb + 1 == r1_hi ? r2_lo : kb + 1; };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmQKV);
@@ -873,7 +901,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         int slot = 0;
         uint32_t ph = 0;
-        for (int kb = 0; next(kb); ++kb) {
+        for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb)) {
           mbar_wait(&r_empty[slot], ph ^ 1);
           mbar_arrive_expect_tx(&r_full[slot], DQ2_STAGE);
           uint8_t* st = smem + DQ2_OFF_RING + slot * DQ2_STAGE;
@@ -921,7 +949,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       int slot = 0, prev = -1, it = 0;
       uint32_t ph = 0;
-      for (int kb = 0; next(kb); ++kb, ++it) {
+      for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb), ++it) {
         mbar_wait(&r_full[slot], ph);
         tc_fence_after();
         issue_sdp(it, slot);
@@ -947,7 +975,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int k_end = min(q + 1, a.L), k_mid = a.Lp;
     const int k_lo = q >= a.Lp ? a.Lp + seg_of(q, m) * a.Lmax : 0;
     int it = 0;
-    for (int kb = 0; next(kb); ++kb, ++it) {
+    for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb), ++it) {
       const uint32_t tb = tmem + lane_off + (it & 1) * 128;
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
       tc_fence_after();
