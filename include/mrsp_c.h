@@ -391,8 +391,10 @@ mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id, const int
  * decoder layer (recomputed from its kept input) into fp32 gradients held by
  * the engine (mrsp_engine_save_grads). old_logprobs: sum(lengths) host floats
  * (row-major), advantages: G host floats; stats4 (host) = {objective, mean_kl,
- * clip_fraction, token_count}; logprob_policy (host, may be NULL). SP = 1
- * engines; the vision tower and projector are frozen. */
+ * clip_fraction, token_count}; logprob_policy (host, may be NULL). Any SP
+ * degree (virtual ranks, or one process per GPU on the peer-memory transport,
+ * where every rank of the group makes the same call: it is collective); the
+ * vision tower and projector are frozen. */
 mrsp_status mrsp_engine_grpo_backward(mrsp_engine* e, const char* video_id,
                                       const int32_t* question, int n_q, const int32_t* resp,
                                       const int32_t* lengths, int G, int Lmax,
