@@ -203,7 +203,9 @@ __device__ __forceinline__ constexpr bool poly_pair(int i) {
 }
 
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (0 = all MUFU).
-template <int kPoly>
+// kPC: chunks P is handed to the P.V MMA in (2: 64-key halves; 4: 32-key
+// quarters, so the last chunk's MMA is shorter on the S -> P -> P.V chain).
+template <int kPoly, int kPC>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
@@ -216,9 +218,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* r_empty = bars + 6;   // [RING]
   uint64_t* s_full = bars + 11;   // [2] per query tile
   uint64_t* s_free = bars + 13;   // [2]
-  uint64_t* p_full = bars + 15;   // [2][2]: per query tile, per 64-key half of P
-  uint64_t* pv_done = bars + 19;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint64_t* p_full = bars + 15;   // [2][4]: per query tile, per chunk of P
+  uint64_t* pv_done = bars + 23;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   ATRACE_INIT;
   const int warp = warp_id();
@@ -242,8 +244,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&s_free[t], 128);
-      mbar_init(&p_full[2 * t], 128);
-      mbar_init(&p_full[2 * t + 1], 128);
+      for (int c = 0; c < 4; ++c) mbar_init(&p_full[4 * t + c], 128);
       mbar_init(&pv_done[t], 1);
     }
     fence_barrier_init();
@@ -320,23 +321,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         ++n_s[t];
       };
       auto issue_pv = [&](int t, uint32_t v_addr) {
-        // two halves of 64 keys: the first half's MMAs start while the softmax
-        // is still exponentiating the second half
+        // kPC chunks of keys: the first chunks' MMAs start while the softmax
+        // is still exponentiating the later ones
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          mbar_wait(&p_full[2 * t + half], n_pv[t] & 1);
-          ATRACE(14 + 2 * t + half, n_pv[t]);
+        for (int half = 0; half < kPC; ++half) {
+          mbar_wait(&p_full[4 * t + half], n_pv[t] & 1);
+          ATRACE(14 + 2 * t + (half * 2) / kPC, n_pv[t]);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
-              const int kk = half * 4 + k4;
+            for (int k4 = 0; k4 < 8 / kPC; ++k4) {
+              const int kk = half * (8 / kPC) + k4;
               // A = P from TMEM (packed bf16 pairs over S(t)'s first 64 columns)
               const uint64_t bd = sdesc_sw128_mn(v_addr + kk * 2048, CHUNK);
               mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o,
                           (n_pv[t] > 0 || kk > 0) ? 1u : 0u);
             }
-            if (half == 1) mma_commit(&pv_done[t]);
+            if (half == kPC - 1) mma_commit(&pv_done[t]);
           }
           __syncwarp();
         }
@@ -471,16 +472,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (need) m_run = mt;
       const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 4 packed partial sums
+      constexpr int kPairs = 64 / kPC;  // packed bf16 pairs (TMEM columns) per chunk
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t w[32];  // 64 keys as 32 packed bf16 pairs -> TMEM columns [32c, 32c + 32)
+      for (int c = 0; c < kPC; ++c) {
+        uint32_t w[kPairs];  // 128/kPC keys as packed bf16 pairs -> TMEM columns [kPairs c, +kPairs)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int j = c * 64 + 2 * i;
+        for (int i = 0; i < kPairs; ++i) {
+          const int j = c * 2 * kPairs + 2 * i;
           float x0, x1;
           ffma2(x0, x1, s[j], s[j + 1], sl2, sl2, neg_m, neg_m);
           float p0, p1;
-          if (poly_pair<kPoly>(i)) {
+          if (poly_pair<kPoly>((c * kPairs + i) & 31)) {
             exp2_poly2(x0, x1, p0, p1);
           } else {
             p0 = exp2_mufu(x0);
@@ -489,13 +491,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           fadd2(acc[2 * (i & 3)], acc[2 * (i & 3) + 1], p0, p1);
           w[i] = pack_bf16(p0, p1);
         }
-        ATRACE(6 + c, it);
-        tmem_st32(tS + c * 32, w);
+        ATRACE(6 + (c * 2) / kPC, it);
+        if constexpr (kPairs == 32) {
+          tmem_st32(tS + c * 32, w);
+        } else {
+          tmem_st16(tS + c * 16, w);
+        }
         tmem_st_wait();
-        ATRACE(8 + c, it);
+        ATRACE(8 + (c * 2) / kPC, it);
         tc_fence_before();
-        mbar_arrive(&p_full[2 * t + c]);  // this half of P is ready for the MMA
-        ATRACE(4 + c, it);
+        mbar_arrive(&p_full[4 * t + c]);  // this chunk of P is ready for the MMA
+        ATRACE(4 + (c * 2) / kPC, it);
       }
       l_run += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       ++it;
@@ -540,6 +546,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // FMA-pipe exp2 share: measured no gain at c4 with P in TMEM (1180 TFLOP/s at
 // kPoly 0 vs 1155 at 8, profiles/r1_attention_study.md), so MUFU only.
 constexpr int kDefaultPoly = 0;
+constexpr int kDefaultPChunks = 2;
 
 }  // namespace
 
@@ -556,13 +563,18 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   // (tools/attn_perf.py); every instantiation is parity-tested.
   const char* env_poly = std::getenv("MRSP_ATTN_POLY");
   const int poly = env_poly ? std::atoi(env_poly) : kDefaultPoly;
+  // MRSP_ATTN_PCHUNKS: 2 (64-key halves of P, default) or 4 (32-key quarters)
+  const char* env_pc = std::getenv("MRSP_ATTN_PCHUNKS");
+  const int pc = env_pc ? std::atoi(env_pc) : kDefaultPChunks;
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, AttnArgs);
-  const Kern kern = poly == 4 ? attn_fwd_tcgen05<4> : poly == 8 ? attn_fwd_tcgen05<8>
-                  : poly == 12 ? attn_fwd_tcgen05<12> : poly == 16 ? attn_fwd_tcgen05<16>
-                  : attn_fwd_tcgen05<0>;
+  const Kern kern = pc == 4 ? (poly == 8 ? attn_fwd_tcgen05<8, 4> : attn_fwd_tcgen05<0, 4>)
+                  : poly == 4 ? attn_fwd_tcgen05<4, 2> : poly == 8 ? attn_fwd_tcgen05<8, 2>
+                  : poly == 12 ? attn_fwd_tcgen05<12, 2> : poly == 16 ? attn_fwd_tcgen05<16, 2>
+                  : attn_fwd_tcgen05<0, 2>;
   static const bool attr = [] {
-    for (auto k : {attn_fwd_tcgen05<0>, attn_fwd_tcgen05<4>, attn_fwd_tcgen05<8>,
-                   attn_fwd_tcgen05<12>, attn_fwd_tcgen05<16>})
+    for (auto k : {attn_fwd_tcgen05<0, 2>, attn_fwd_tcgen05<4, 2>, attn_fwd_tcgen05<8, 2>,
+                   attn_fwd_tcgen05<12, 2>, attn_fwd_tcgen05<16, 2>, attn_fwd_tcgen05<0, 4>,
+                   attn_fwd_tcgen05<8, 4>})
       MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(SMEM_BYTES)));
     return true;
