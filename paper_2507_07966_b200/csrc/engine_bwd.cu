@@ -106,29 +106,17 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   if (mesh_)
     MRSP_REQUIRE(Ltot <= mesh_->caps().tokens && S <= mesh_->caps().scored, MRSP_INVALID_ARGUMENT,
                  "p2p: group exceeds the exported capacities");
-  // every global rank's scored tokens [sc_lo, sc_lo + n_sc) and LM-head slice
-  // [lm_lo, lm_lo + lm_n) in group order (scored tokens are position-ordered)
-  std::vector<long> sc_lo(K, 0), n_sc(K, 0), lm_lo(K, 0), lm_n(K, 0);
-  {
-    for (int r = 0; r < G; ++r)
-      for (int j = 0; j < lengths[r]; ++j) {
-        const long pos = g.Lp + static_cast<long>(r) * Lmax + j;
-        int p = 0;
-        while (p + 1 < K && pos >= token_b_[p + 1]) ++p;
-        ++n_sc[p];
-      }
-    for (int p = 1; p < K; ++p) sc_lo[p] = sc_lo[p - 1] + n_sc[p - 1];
-    for (int p = 0; p < K; ++p) {
-      if (spread_lm()) {
-        const long b = S / K * p + std::min<long>(p, S % K);
-        lm_lo[p] = b;
-        lm_n[p] = S / K + (p < S % K ? 1 : 0);
-      } else {
-        lm_lo[p] = sc_lo[p];
-        lm_n[p] = n_sc[p];
-      }
+  // every global rank's scored tokens [sc_lo, sc_lo + n_sc) in group order
+  // (scored tokens are position-ordered): where the LM-head slices' dX rows go
+  std::vector<long> sc_lo(K, 0), n_sc(K, 0);
+  for (int r = 0; r < G; ++r)
+    for (int j = 0; j < lengths[r]; ++j) {
+      const long pos = g.Lp + static_cast<long>(r) * Lmax + j;
+      int p = 0;
+      while (p + 1 < K && pos >= token_b_[p + 1]) ++p;
+      ++n_sc[p];
     }
-  }
+  for (int p = 1; p < K; ++p) sc_lo[p] = sc_lo[p - 1] + n_sc[p - 1];
 
   // ---- gradient storage: fp32 in the engine's weight layout, zeroed per call
   // (every SP rank adds its tokens' share, in rank order: deterministic) -----
