@@ -355,6 +355,10 @@ typedef struct mrsp_engine mrsp_engine;
  * sp <= n_kv heads split contiguously; for sp > n_kv each kv head is replicated
  * to sp/n_kv ranks that split its query-head group with plan_shards. */
 mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, int32_t* out14);
+/* The engine's head split of SP rank `rank` (row_split != 0: the peer-memory
+ * transports' query-row split when sp > n_kv): out7 = {q_lo, q_hi, kv_lo,
+ * kv_hi, q_per_kv, row_parts, row_part}. */
+mrsp_status mrsp_head_split(int n_q, int n_kv, int sp, int rank, int row_split, int32_t* out7);
 
 /* Query-row split used instead by the peer-memory / virtual-rank transports
  * when sp > n_kv (MRSP_ULYSSES_SPLIT=heads restores the head split above):

@@ -99,6 +99,7 @@ _sig("mrsp_op_pack_sequence", [_V, _I, _V, _I, _V, _V, _I, _V, _I, _I64, _I, _V,
 _sig("mrsp_nccl_unique_id", [_V])
 _sig("mrsp_ulysses_plan", [_I, _I, _I, _I, _V])
 _sig("mrsp_attn_row_part", [_I, _I, _I], ctypes.c_int)
+_sig("mrsp_head_split", [_I, _I, _I, _I, _I, _V])
 _sig("mrsp_engine_create", [_V, _I, _I, _I, _U64, _U64, _U64, _I, _V, _V])
 _sig("mrsp_engine_destroy", [_V])
 _sig("mrsp_engine_encode", [_V, ctypes.c_char_p, _V, _I, _I, _I, _V])

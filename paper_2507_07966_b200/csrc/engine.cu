@@ -1644,6 +1644,17 @@ extern "C" mrsp_status mrsp_ulysses_plan(int n_q, int n_kv, int sp, int rank, in
   });
 }
 
+extern "C" mrsp_status mrsp_head_split(int n_q, int n_kv, int sp, int rank, int row_split,
+                                       int32_t* out7) {
+  return guard([&] {
+    MRSP_REQUIRE(sp >= 1 && rank >= 0 && rank < sp && out7, MRSP_INVALID_ARGUMENT,
+                 "ulysses: bad rank");
+    const HeadSplit hs = head_split(n_q, n_kv, sp, rank, row_split != 0);
+    const int32_t v[7] = {hs.q_lo, hs.q_hi, hs.kv_lo, hs.kv_hi, hs.q_per_kv, hs.rparts, hs.rpart};
+    std::memcpy(out7, v, sizeof(v));
+  });
+}
+
 extern "C" int mrsp_attn_row_part(int block, int n_blocks, int m) {
   if (m < 1 || n_blocks < 1 || block < 0 || block >= n_blocks) return -1;
   return mrsp::attn_row_part(block, n_blocks, m);

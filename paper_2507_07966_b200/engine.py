@@ -132,6 +132,20 @@ def ulysses_plan(n_q: int, n_kv: int, sp: int, rank: int) -> dict:
             "blocks": [tuple(v[5 + 3 * i: 8 + 3 * i]) for i in range(3)]}
 
 
+def head_split(n_q: int, n_kv: int, sp: int, rank: int, row_split: bool = True) -> dict:
+    """The engine's head split of one SP rank (mrsp_head_split): query / kv head
+    ranges and, above the kv-head count, the query-row split part."""
+    out = (ctypes.c_int32 * 7)()
+    check(_lib.lib().mrsp_head_split(n_q, n_kv, sp, rank, int(row_split), out))
+    v = list(out)
+    return {"q": (v[0], v[1]), "kv": (v[2], v[3]), "q_per_kv": v[4], "row_parts": v[5],
+            "row_part": v[6]}
+
+
+def attn_row_part(block: int, n_blocks: int, m: int) -> int:
+    return int(_lib.lib().mrsp_attn_row_part(block, n_blocks, m))
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     check(_lib.lib().mrsp_nccl_unique_id(buf))
