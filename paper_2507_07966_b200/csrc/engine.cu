@@ -530,6 +530,34 @@ void Engine::encode_rank(RankCtx& R, const float* pixels, bool on_device, int F,
   encoder_invocations.fetch_add(static_cast<uint64_t>(nf), std::memory_order_relaxed);
 }
 
+// Device buffer for a cache entry's embeddings: an evicted entry's buffer of
+// the same size is reused once nothing references it (cudaMalloc / cudaFree of
+// a ~1 GB buffer per fresh video stalls the stream); MRSP_CACHE_POOL=0 turns
+// the recycling off. Called under run_mu_.
+std::shared_ptr<DevBuf> Engine::entry_buffer(size_t bytes) {
+  static const bool pool_on = [] {
+    const char* v = std::getenv("MRSP_CACHE_POOL");
+    return !(v && std::atoi(v) == 0);
+  }();
+  if (pool_on) {
+    for (auto& b : entry_pool_)
+      if (b.use_count() == 1 && b->bytes >= bytes && b->bytes <= bytes + (bytes >> 3)) return b;
+  }
+  auto b = std::make_shared<DevBuf>();
+  b->ensure(bytes);
+  if (pool_on) {
+    if (entry_pool_.size() >= 6) {  // drop a buffer nobody holds, else do not pool
+      for (auto it = entry_pool_.begin(); it != entry_pool_.end(); ++it)
+        if (it->use_count() == 1) {
+          entry_pool_.erase(it);
+          break;
+        }
+    }
+    if (entry_pool_.size() < 6) entry_pool_.push_back(b);
+  }
+  return b;
+}
+
 std::shared_ptr<CacheEntry> Engine::get_or_encode(const std::string& id, const float* pixels,
                                                   int F, bool on_device, bool use_cache,
                                                   bool* hit) {
@@ -571,9 +599,9 @@ std::shared_ptr<CacheEntry> Engine::get_or_encode(const std::string& id, const f
     std::lock_guard<std::mutex> run(run_mu_);
     const int T = tokens_per_frame(), d = cfg_.dim;
     const auto fplan = plan(F, k_);
-    auto emb = std::make_shared<DevBuf>();
     const size_t row_bytes = static_cast<size_t>(T) * d * 2;  // one frame's embeddings
-    bf16* full = static_cast<bf16*>(emb->ensure(static_cast<size_t>(F) * row_bytes));
+    auto emb = entry_buffer(static_cast<size_t>(F) * row_bytes);
+    bf16* full = static_cast<bf16*>(emb->p);
     if (mesh_) {
       // one process per GPU over peer memory: encode this rank's frames, then
       // copy-engine P2P writes of the slice into every rank's landing buffer

@@ -288,6 +288,8 @@ class Engine {
  private:
   std::mutex cache_mu_;
   std::map<std::string, std::shared_ptr<CacheEntry>> cache_;
+  std::vector<std::shared_ptr<DevBuf>> entry_pool_;  // recycled entry buffers (run_mu_)
+  std::shared_ptr<DevBuf> entry_buffer(size_t bytes);
   uint64_t cache_seq_ = 0;
   std::mutex run_mu_;  // one stage at a time per engine
   // profiling
