@@ -205,7 +205,9 @@ __device__ __forceinline__ constexpr bool poly_pair(int i) {
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (0 = all MUFU).
 // kPC: chunks P is handed to the P.V MMA in (2: 64-key halves; 4: 32-key
 // quarters, so the last chunk's MMA is shorter on the S -> P -> P.V chain).
-template <int kPoly, int kPC>
+// kSpec: the first chunk's exponentials are computed with the running max
+// while the tile max is formed (redone on the rare max growth).
+template <int kPoly, int kPC, int kSpec>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_fwd_tcgen05(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
@@ -437,8 +439,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (!((vis >> j) & 1u)) s[32 * q + j] = -INFINITY;
         }
       }
-      float mx;
-      {  // 8 independent max chains (FMNMX3) instead of one 128-deep chain
+      // 8 independent max chains (FMNMX3) instead of one 128-deep chain
+      auto tile_max = [&]() {
         float m8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) m8[i] = fmaxf(s[i], s[i + 8]);
@@ -446,36 +448,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 16; j < TK; j += 16)
 #pragma unroll
           for (int i = 0; i < 8; ++i) m8[i] = fmaxf(m8[i], fmaxf(s[j + i], s[j + i + 8]));
-        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      }
-      const float mt = mx * sl2;  // -inf stays -inf
-      ATRACE(3, it);
-      // P buffer and O are free once this tile's previous P.V has completed.
-      if (it > 0) mbar_wait(&pv_done[t], (it - 1) & 1);
-      tc_fence_after();
-      const bool need = mt > m_run + RESCALE_THRESHOLD;
-      if (__any_sync(0xffffffffu, need) && it > 0) {
-        const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
-        if (need) l_run *= alpha;
-#pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(tO + c, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + c, o);
-        }
-        tmem_st_wait();
-      }
-      if (need) m_run = mt;
-      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 4 packed partial sums
+        return fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                     fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      };
       constexpr int kPairs = 64 / kPC;  // packed bf16 pairs (TMEM columns) per chunk
-#pragma unroll
-      for (int c = 0; c < kPC; ++c) {
-        uint32_t w[kPairs];  // 128/kPC keys as packed bf16 pairs -> TMEM columns [kPairs c, +kPairs)
+      // p = 2^(s scale log2e - m) for chunk c of the tile, packed, row sums in acc
+      auto exp_chunk = [&](int c, float neg_m, uint32_t (&w)[kPairs], float (&acc)[8]) {
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
           const int j = c * 2 * kPairs + 2 * i;
@@ -491,6 +469,61 @@ __global__ void __launch_bounds__(THREADS, 1)
           fadd2(acc[2 * (i & 3)], acc[2 * (i & 3) + 1], p0, p1);
           w[i] = pack_bf16(p0, p1);
         }
+      };
+      // the lazy rescale: the running max moves only when the tile's max
+      // exceeds it by > 2^8; O and l are rescaled once the previous P.V is done
+      auto rescale = [&](float mt, bool need) {
+        if (it > 0) mbar_wait(&pv_done[t], (it - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need) && it > 0) {
+          const float alpha = (need && m_run != -INFINITY) ? exp2f(m_run - mt) : 1.0f;
+          if (need) l_run *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+            tmem_st32(tO + c, o);
+          }
+          tmem_st_wait();
+        }
+        if (need) m_run = mt;
+      };
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 4 packed partial sums
+      uint32_t w0[kPairs];
+      float neg_m;
+      if (kSpec && it > 0) {
+        // Speculative: chunk 0's exponentials with the running max while the
+        // tile max is formed alongside (MUFU and ALU pipes), so the max is off
+        // the S -> P chain. Only when the max grows by > 2^8 (rare after the
+        // first tiles) is chunk 0 redone after the rescale — the same results
+        // as max-first, bit for bit.
+        neg_m = m_run == -INFINITY ? 0.f : -m_run;
+        exp_chunk(0, neg_m, w0, acc);
+        const float mt = tile_max() * sl2;  // -inf stays -inf
+        const bool need = mt > m_run + RESCALE_THRESHOLD;
+        ATRACE(3, it);
+        if (__any_sync(0xffffffffu, need)) {
+          rescale(mt, need);
+          neg_m = m_run == -INFINITY ? 0.f : -m_run;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+          exp_chunk(0, neg_m, w0, acc);
+        }
+      } else {
+        const float mt = tile_max() * sl2;
+        ATRACE(3, it);
+        rescale(mt, mt > m_run + RESCALE_THRESHOLD);
+        neg_m = m_run == -INFINITY ? 0.f : -m_run;
+        exp_chunk(0, neg_m, w0, acc);
+      }
+#pragma unroll
+      for (int c = 0; c < kPC; ++c) {
+        uint32_t wc[kPairs];
+        if (c > 0) exp_chunk(c, neg_m, wc, acc);
+        const uint32_t (&w)[kPairs] = c == 0 ? w0 : wc;
         ATRACE(6 + (c * 2) / kPC, it);
         if constexpr (kPairs == 32) {
           tmem_st32(tS + c * 32, w);
@@ -547,6 +580,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // kPoly 0 vs 1155 at 8, profiles/r1_attention_study.md), so MUFU only.
 constexpr int kDefaultPoly = 0;
 constexpr int kDefaultPChunks = 2;
+constexpr int kDefaultSpec = 0;
 
 }  // namespace
 
@@ -567,14 +601,18 @@ void attention_fwd(const AttnParams& p, cudaStream_t stream) {
   const char* env_pc = std::getenv("MRSP_ATTN_PCHUNKS");
   const int pc = env_pc ? std::atoi(env_pc) : kDefaultPChunks;
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, AttnArgs);
-  const Kern kern = pc == 4 ? (poly == 8 ? attn_fwd_tcgen05<8, 4> : attn_fwd_tcgen05<0, 4>)
-                  : poly == 4 ? attn_fwd_tcgen05<4, 2> : poly == 8 ? attn_fwd_tcgen05<8, 2>
-                  : poly == 12 ? attn_fwd_tcgen05<12, 2> : poly == 16 ? attn_fwd_tcgen05<16, 2>
-                  : attn_fwd_tcgen05<0, 2>;
+  // MRSP_ATTN_SPEC: 1 speculative first-chunk exponentials (see kSpec), 0 max first
+  const char* env_spec = std::getenv("MRSP_ATTN_SPEC");
+  const int spec = env_spec ? std::atoi(env_spec) : kDefaultSpec;
+  const Kern kern = spec ? (pc == 4 ? attn_fwd_tcgen05<0, 4, 1> : attn_fwd_tcgen05<0, 2, 1>)
+                  : pc == 4 ? (poly == 8 ? attn_fwd_tcgen05<8, 4, 0> : attn_fwd_tcgen05<0, 4, 0>)
+                  : poly == 4 ? attn_fwd_tcgen05<4, 2, 0> : poly == 8 ? attn_fwd_tcgen05<8, 2, 0>
+                  : poly == 12 ? attn_fwd_tcgen05<12, 2, 0> : poly == 16 ? attn_fwd_tcgen05<16, 2, 0>
+                  : attn_fwd_tcgen05<0, 2, 0>;
   static const bool attr = [] {
-    for (auto k : {attn_fwd_tcgen05<0, 2>, attn_fwd_tcgen05<4, 2>, attn_fwd_tcgen05<8, 2>,
-                   attn_fwd_tcgen05<12, 2>, attn_fwd_tcgen05<16, 2>, attn_fwd_tcgen05<0, 4>,
-                   attn_fwd_tcgen05<8, 4>})
+    for (auto k : {attn_fwd_tcgen05<0, 2, 0>, attn_fwd_tcgen05<4, 2, 0>, attn_fwd_tcgen05<8, 2, 0>,
+                   attn_fwd_tcgen05<12, 2, 0>, attn_fwd_tcgen05<16, 2, 0>, attn_fwd_tcgen05<0, 4, 0>,
+                   attn_fwd_tcgen05<8, 4, 0>, attn_fwd_tcgen05<0, 2, 1>, attn_fwd_tcgen05<0, 4, 1>})
       MRSP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(SMEM_BYTES)));
     return true;
