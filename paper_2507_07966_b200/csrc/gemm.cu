@@ -120,6 +120,7 @@ __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __e
 // Fused epilogue of one accumulator tile row slice: TMEM row `t_row` (this
 // thread's lane, BN fp32 columns) -> the epilogue op -> global. Shared by the
 // single-CTA and the CTA-pair kernels.
+template <int kBN = BN>
 __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row, int row,
                                              bool row_ok, int nt, int n_tiles) {
   if (args.epi == GEMM_EPI_QKV_SCATTER) {
@@ -131,8 +132,8 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
     const float p = row_ok ? static_cast<float>(args.pos[row]) : 0.f;
     const long grow = args.row0 + row;
 #pragma unroll 1
-    for (int hl = 0; hl < BN / 128; ++hl) {
-      const int hb = nt * (BN / 128) + hl;
+    for (int hl = 0; hl < kBN / 128; ++hl) {
+      const int hb = nt * (kBN / 128) + hl;
       if (hb * 128 >= args.N) break;  // warp-uniform
       const bool rope = hb < args.n_rope_blocks;
       const int2 d0 = args.route[2 * hb], d1 = args.route[2 * hb + 1];
@@ -196,11 +197,11 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
     // Logits never leave TMEM/registers.
     const int tgt = row_ok ? args.targets[row] : -1;
     float m = -INFINITY, ssum = 0.f;
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < kBN; c += 32) {
       uint32_t r[32];
       tmem_ld32(t_row + c, r);
       tmem_ld_wait();
-      const int col = nt * BN + c;
+      const int col = nt * kBN + c;
       float cm = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 32; ++j)
@@ -222,12 +223,12 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
     //   dg = dA u silu'(g), du = dA silu(g)   -> C[:, nt*256 + j] | C[:, nt*256 + 128 + j]
     // and the forward output silu(g) u (bit-identical to GEMM_EPI_SWIGLU_BF16) -> aux_out
     __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
-    for (int c = 0; c < BN / 2; c += 32) {
+    for (int c = 0; c < kBN / 2; c += 32) {
       uint32_t g[32], u[32];
       tmem_ld32(t_row + c, g);
-      tmem_ld32(t_row + BN / 2 + c, u);
+      tmem_ld32(t_row + kBN / 2 + c, u);
       tmem_ld_wait();
-      const int col = nt * (BN / 2) + c;
+      const int col = nt * (kBN / 2) + c;
       if (row_ok) {
         const uint4* da4 = reinterpret_cast<const uint4*>(args.aux + static_cast<size_t>(row) * args.ld_aux + col);
         uint32_t dar[16];
@@ -255,8 +256,8 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
           ou[j] = pack_bf16(ru[0], ru[1]);
           oa[j] = pack_bf16(ra[0], ra[1]);
         }
-        uint4* dg = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * BN + c);
-        uint4* du = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * BN + BN / 2 + c);
+        uint4* dg = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * kBN + c);
+        uint4* du = reinterpret_cast<uint4*>(C + static_cast<size_t>(row) * args.ldc + nt * kBN + kBN / 2 + c);
         uint4* ac = reinterpret_cast<uint4*>(args.aux_out + static_cast<size_t>(row) * args.ld_aux_out + col);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -269,12 +270,12 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
   } else if (args.epi == GEMM_EPI_SWIGLU_BF16) {
     // columns [0,128) are gate, [128,256) the matching up projections
     __nv_bfloat16* C = static_cast<__nv_bfloat16*>(args.C);
-    for (int c = 0; c < BN / 2; c += 32) {
+    for (int c = 0; c < kBN / 2; c += 32) {
       uint32_t g[32], u[32];
       tmem_ld32(t_row + c, g);
-      tmem_ld32(t_row + BN / 2 + c, u);
+      tmem_ld32(t_row + kBN / 2 + c, u);
       tmem_ld_wait();
-      const int col = nt * (BN / 2) + c;
+      const int col = nt * (kBN / 2) + c;
       if (row_ok) {
         uint32_t o[16];
 #pragma unroll
@@ -296,11 +297,11 @@ __device__ __forceinline__ void epilogue_row(const EpiArgs& args, uint32_t t_row
       }
     }
   } else {
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < kBN; c += 32) {
       uint32_t r[32];
       tmem_ld32(t_row + c, r);
       tmem_ld_wait();
-      const int col = nt * BN + c;
+      const int col = nt * kBN + c;
       if (row_ok && col < args.N) {  // stores only; the TMEM load above is warp-wide
       float v[32];
 #pragma unroll
@@ -386,13 +387,14 @@ __device__ __forceinline__ void load_bias(const float* bias, int col, int N, flo
 // TMA reduce-add in L2, i.e. resid += v rounded once, as the load/add/store
 // path). Two boxes per warp: filling one overlaps the other's bulk copy.
 // Rows past M / columns past N are clipped by the TMA unit.
+template <int kBN = BN>
 __device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUtensorMap* tmC,
                                                 uint32_t t_row, int y, int nt, uint8_t* boxes,
                                                 uint32_t& buf) {
   const int lane = lane_id();
   const bool f32 = args.epi == GEMM_EPI_RESID_F32 || args.epi == GEMM_EPI_STORE_F32;
   const bool swiglu = args.epi == GEMM_EPI_SWIGLU_BF16;
-  const int out_cols = swiglu ? BN / 2 : BN;
+  const int out_cols = swiglu ? kBN / 2 : kBN;
   const int col0 = nt * out_cols;
   const int out_n = swiglu ? args.N / 2 : args.N;
 #pragma unroll 1
@@ -412,7 +414,7 @@ __device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUten
       for (int h = 0; h < 64; h += 32) {
         uint32_t g[32], u[32];
         tmem_ld32(t_row + c + h, g);
-        tmem_ld32(t_row + BN / 2 + c + h, u);
+        tmem_ld32(t_row + kBN / 2 + c + h, u);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j)
@@ -468,10 +470,11 @@ __device__ __forceinline__ void epilogue_staged(const EpiArgs& args, const CUten
 // 4; the M = 128 MMA still reads 128 A rows, rows 16..127 being whatever bytes
 // follow in the stage (the B tile) — they only produce accumulator rows >= 16,
 // which no epilogue stores. No staged-epilogue boxes (row epilogue only).
-template <int kStages, int kARows>
+template <int kStages, int kARows, int kBN = BN>
 struct GemmCfg {
   static constexpr int kABytes = kARows * BK * 2;
-  static constexpr int kStageBytes = kABytes + B_BYTES;
+  static constexpr int kBBytes = kBN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = kARows == BM ? OUT_BYTES : 0;
   static constexpr size_t kSmem = 1024 + kStages * kStageBytes + kOutBytes + 256;
   static_assert(kABytes % 1024 == 0, "A box = whole SW128 atoms");
@@ -486,14 +489,16 @@ struct GemmCfg {
 // (LBO = one 64-wide box, 8 KB); the instruction descriptor's transpose bits
 // tell the tensor core. kMajor 0 is the forward kernel, unchanged.
 constexpr int MN_BOX = 64 * 64 * 2;
-template <int kStages, int kARows, int kMajor = 0>
+// kBN: output-tile width (256; 192 for N = 1152 / 3456-shaped GEMMs, where
+// 256-wide tiles would leave a half-empty last tile).
+template <int kStages, int kARows, int kMajor = 0, int kBN = BN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmC, EpiArgs args) {
   constexpr bool kAMN = (kMajor & 1) != 0, kBMN = (kMajor & 2) != 0;
   static_assert(kMajor == 0 || kARows == BM, "MN-major operands: full tiles only");
-  using Cfg = GemmCfg<kStages, kARows>;
+  using Cfg = GemmCfg<kStages, kARows, kBN>;
   constexpr int STAGES = kStages;
   constexpr int STAGE_BYTES = Cfg::kStageBytes;
   constexpr int A_STAGE = Cfg::kABytes;
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = warp_id();
   const int m_tiles = (args.M + BM - 1) / BM;
-  const int n_tiles = (args.N + BN - 1) / BN;
+  const int n_tiles = (args.N + kBN - 1) / kBN;
   const int ks_n = args.k_splits;
   const int num_tiles = m_tiles * n_tiles * ks_n;
   const int k_blocks = (args.K + BK - 1) / BK;
@@ -558,9 +563,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   auto load_b = [&](uint8_t* dst, uint64_t* bar, int kb, int nt) {
     if constexpr (kBMN) {
 #pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tma_load_2d(dst + c * MN_BOX, &tmB, bar, nt * BN + c * 64, kb * BK);
+      for (int c = 0; c < kBN / 64; ++c) tma_load_2d(dst + c * MN_BOX, &tmB, bar, nt * kBN + c * 64, kb * BK);
     } else {
-      tma_load_2d(dst, &tmB, bar, kb * BK, nt * BN);
+      tma_load_2d(dst, &tmB, bar, kb * BK, nt * kBN);
     }
   };
   if (warp == 0) {
@@ -596,7 +601,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     const uint32_t idesc =
-        idesc_bf16_f32(BM, BN) | (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
+        idesc_bf16_f32(BM, kBN) | (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -606,7 +611,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       decode_tile(tile, mt, nt, kb0, kb1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * kBN;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -645,14 +650,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const int row = mt * BM + ew * 32 + lane_id();
       const bool row_ok = row < args.M;
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kBN;
       if (ks_n > 1) {  // fp32 partial of this K split (rows < M only)
         float* P = args.ws + (static_cast<size_t>(tile % ks_n) * args.M + row) * args.N;
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < kBN; c += 32) {
           uint32_t r[32];
           tmem_ld32(t_row + c, r);
           tmem_ld_wait();
-          const int col = nt * BN + c;
+          const int col = nt * kBN + c;
           if (row_ok && col < args.N) {
             if (col + 32 <= args.N && (args.N & 3) == 0) {
 #pragma unroll
@@ -668,9 +673,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       } else if (kARows == BM && args.staged)
-        epilogue_staged(args, &tmC, t_row, mt * BM + ew * 32, nt, boxes, buf);
+        epilogue_staged<kBN>(args, &tmC, t_row, mt * BM + ew * 32, nt, boxes, buf);
       else
-        epilogue_row(args, t_row, row, row_ok, nt, n_tiles);
+        epilogue_row<kBN>(args, t_row, row, row_ok, nt, n_tiles);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -1189,6 +1194,32 @@ bool gemm_bf16(const GemmArgs& g, cudaStream_t stream) {
       e.staged = 0;
       tiles *= splits;
     }
+  }
+  // MRSP_GEMM_BN192=1: 192-wide tiles when N is a multiple of 192 but not of
+  // 256 (SigLIP's 1152 / 3456: 6 / 18 full tiles instead of 4.5 / 13.5).
+  // Measured neutral on the c4 tower (164.0-164.2 vs 164.4-164.9 ms), so off.
+  static const bool bn192_env = [] {
+    const char* v = std::getenv("MRSP_GEMM_BN192");
+    return v && std::atoi(v) != 0;
+  }();
+  const bool bn192_epi = g.epi == GEMM_EPI_STORE_BF16 || g.epi == GEMM_EPI_BIAS_BF16 ||
+                         g.epi == GEMM_EPI_BIAS_GELU_BF16 || g.epi == GEMM_EPI_RESID_F32 ||
+                         g.epi == GEMM_EPI_STORE_F32;
+  if (bn192_env && !skinny && e.k_splits <= 1 && bn192_epi && g.N % BN != 0 && g.N % 192 == 0) {
+    static const bool attr192 = [] {
+      MRSP_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<STAGES, BM, 0, 192>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(GemmCfg<STAGES, BM, 192>::kSmem)));
+      return true;
+    }();
+    (void)attr192;
+    CUtensorMap tb192 = make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 192, BK);
+    const int tiles192 = ((g.M + BM - 1) / BM) * (g.N / 192);
+    launch_pdl(gemm_bf16_tcgen05<STAGES, BM, 0, 192>, dim3(std::min(tiles192, num_sms())),
+               dim3(THREADS), GemmCfg<STAGES, BM, 192>::kSmem, stream, ta, tb192, tc, e);
+    count_launch();
+    MRSP_CUDA(cudaGetLastError());
+    return false;
   }
   const int grid = std::min(tiles, num_sms());
   if (skinny) {

@@ -127,3 +127,49 @@ def test_gemm_skinny_matches_default(gpu, gemm_impl, M, N, K, monkeypatch):
         if x is not None:
             assert torch.equal(x, y)
     assert rel_err(out["1"][0], ref(A, B)) < 1e-5
+
+
+@pytest.mark.parametrize("N", [1152, 3456])
+def test_gemm_bn192_epilogues(gpu, gemm_impl, N):
+    """N a multiple of 192 but not of 256 (SigLIP's O / fc2 and QKV widths):
+    every plain epilogue, with the default tiles and (a subprocess with
+    MRSP_GEMM_BN192=1) the 192-wide-tile kernel."""
+    M, K = 1300, 1152
+    g = torch.Generator(device="cuda").manual_seed(N)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    r = ref(A, B)
+    assert rel_err(ops.gemm(A, B, ops.EPI_STORE_F32), r) < 1e-5
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_BF16, bias=bias), r + bias) < 5e-3
+    gelu = torch.nn.functional.gelu(r + bias, approximate="tanh")
+    assert rel_err(ops.gemm(A, B, ops.EPI_BIAS_GELU_BF16, bias=bias), gelu) < 5e-3
+    resid = torch.randn(M, N, device="cuda", generator=g)
+    want = resid + r + bias
+    ops.gemm(A, B, ops.EPI_RESID_F32, resid=resid, bias=bias)
+    assert rel_err(resid, want) < 1e-5
+
+
+def test_gemm_bn192_variant(gpu):
+    """The 192-wide-tile kernel (read once per process) in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = ("import torch, sys; sys.path.insert(0, '.');"
+            "from paper_2507_07966_b200 import ops;"
+            "g = torch.Generator(device='cuda').manual_seed(3);"
+            "A = torch.randn(1300, 1152, device='cuda', generator=g).bfloat16();"
+            "B = (torch.randn(3456, 1152, device='cuda', generator=g) / 34).bfloat16();"
+            "bias = torch.randn(3456, device='cuda', generator=g);"
+            "r = A.float() @ B.float().T + bias;"
+            "C = ops.gemm(A, B, ops.EPI_BIAS_BF16, bias=bias);"
+            "R = torch.randn(1300, 3456, device='cuda', generator=g); W = R + r;"
+            "ops.gemm(A, B, ops.EPI_RESID_F32, resid=R, bias=bias);"
+            "e1 = ((C.float() - r).norm() / r.norm()).item();"
+            "e2 = ((R - W).norm() / W.norm()).item();"
+            "assert e1 < 5e-3 and e2 < 1e-5, (e1, e2); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**os.environ, "MRSP_GEMM_BN192": "1", "MRSP_GEMM_IMPL": "1"},
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
