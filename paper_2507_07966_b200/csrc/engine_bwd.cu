@@ -58,8 +58,13 @@ void Engine::grpo_backward(const CacheEntry& emb, const int32_t* question, int n
                            const int32_t* resp, const int32_t* lengths, int G, int Lmax,
                            const float* old_lp, const float* adv, double clip_eps, double kl_beta,
                            int sampled_kl, double* stats4, float* lp_out) {
-  MRSP_REQUIRE(old_lp && adv && stats4, MRSP_INVALID_ARGUMENT, "grpo_backward: null argument");
+  MRSP_REQUIRE(old_lp && adv && stats4 && lengths, MRSP_INVALID_ARGUMENT,
+               "grpo_backward: null argument");
   MRSP_REQUIRE(clip_eps >= 0.0, MRSP_INVALID_ARGUMENT, "grpo_backward: clip_eps < 0");
+  // check_group (grpo.cpp:57-66): every rollout has tokens
+  MRSP_REQUIRE(G >= 1 && G <= 1024, MRSP_INVALID_ARGUMENT, "grpo: empty rollout group");
+  for (int r = 0; r < G; ++r)
+    MRSP_REQUIRE(lengths[r] >= 1, MRSP_INVALID_ARGUMENT, "grpo: empty rollout");
   MRSP_REQUIRE(has_ref_ || kl_beta == 0.0, MRSP_INVALID_ARGUMENT,
                "grpo_backward: the KL term needs a separate reference model");
   backward_pass(0, emb, question, n_q, resp, lengths, G, Lmax, old_lp, adv, clip_eps, kl_beta,

@@ -319,6 +319,12 @@ def test_grpo_backward_rejects_unsupported(gpu):
         eng.grpo_backward("v", grp, np.zeros(n), np.ones(w.G), clip_eps=-1.0)
     with pytest.raises(_lib.InvalidArgument):
         eng.save_grads("/tmp/none.safetensors")  # no gradients yet
+    # check_group (grpo.cpp:57-66): an empty rollout is an invalid argument
+    lens0 = grp.lengths.copy()
+    lens0[1] = 0
+    g0 = E.Group(grp.question, grp.resp, lens0)
+    with pytest.raises(_lib.InvalidArgument, match="empty rollout"):
+        eng.grpo_backward("v", g0, np.zeros(int(lens0.sum())), np.ones(w.G))
     eng.close()
 
 
