@@ -8,21 +8,23 @@
 // tcgen05 kernels so that every output is written once and the result is
 // deterministic (no atomics; SP = k stays bit-identical to SP = 1):
 //
-//   attn_bwd_dq    one CTA per (128-query tile, query head), sweeping the KV
-//                  tiles it sees:  S = Q K^T, dP = dO V^T (TMEM), then per
-//                  element P = 2^(S scale log2e - lse), dS = P (dP - D) packed
-//                  bf16 back into TMEM, and dQ += dS K (A operand from TMEM,
-//                  K read MN-major from the same smem tile). dQ = scale dQ.
-//   attn_bwd_dkdv  one CTA per (128-key tile, kv head), sweeping the q_per_kv
-//                  query heads x the query tiles that see it:  S^T = K Q^T,
+//   attn_bwd_dq2   one CTA per (128-query tile, query head), sweeping the KV
+//                  it sees in 64-key halves:  S = Q K^T, dP = dO V^T (TMEM,
+//                  two buffers so the tensor core runs ahead of the softmax),
+//                  then per element P = 2^(S scale log2e - lse), dS = P (dP - D)
+//                  packed bf16 back into TMEM, and dQ += dS K (A operand from
+//                  TMEM, K read MN-major from the same smem half). Q and dO,
+//                  constant over the CTA, sit in TMEM as the S / dP A operands.
+//   attn_bwd_dkdv2 one CTA per (128-key tile, kv head), sweeping the q_per_kv
+//                  query heads x the 64-query halves that see it:  S^T = K Q^T,
 //                  dP^T = V dO^T, P^T and dS^T packed into TMEM, then
 //                  dV += P^T dO and dK += dS^T Q (dO, Q read MN-major).
-//                  TMEM = S^T | dP^T | dV | dK (512 columns).
 //
-// lse is the forward kernel's per-row log-sum-exp (scaled log2 domain,
-// AttnParams::lse), D = rowsum(dO o O) (attn_bwd_prep). Roles as in the
-// forward kernel: warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator,
-// warps 4-11 two warpgroups that each take one 64-column half of the tile.
+// (attn_bwd_dq / attn_bwd_dkdv: the single-buffered 128-wide first version,
+// MRSP_ATTN_BWD=1.) lse is the forward kernel's per-row log-sum-exp (scaled
+// log2 domain, AttnParams::lse), D = rowsum(dO o O) (attn_bwd_prep). Roles as
+// in the forward kernel: warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warps 4-11 two warpgroups that each take one half of the tile's columns.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -65,6 +67,11 @@ struct BwdArgs {
   // kv head shared by several ranks, summed before their single rounding
   float* dkv32;
   int ld_dkv32;
+  // raw rows (the dQ kernel reads its constant A operands Q / dO into TMEM)
+  const __nv_bfloat16* qkv;
+  int ld_qkv;
+  const __nv_bfloat16* dO;
+  int ld_do;
 };
 
 // Query tile of dQ-kernel CTA index `rem` (kv-head-major order handled by the
@@ -552,6 +559,74 @@ __device__ __forceinline__ bool range_visible(int q0, int nq, int k0, int nk, co
   return sk1 >= qs0 && sk0 <= qs1;
 }
 
+// A 128 x 64 bf16 half row of a constant A operand (this thread's row) into
+// 32 packed TMEM columns (lane = row, column c = elements 2c, 2c + 1).
+__device__ __forceinline__ void operand_row_to_tmem(const __nv_bfloat16* row, bool ok, uint32_t taddr) {
+  const uint4* src = reinterpret_cast<const uint4*>(row);
+  uint32_t w[32];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 x = ok ? __ldg(src + j) : make_uint4(0, 0, 0, 0);
+    w[4 * j] = x.x; w[4 * j + 1] = x.y; w[4 * j + 2] = x.z; w[4 * j + 3] = x.w;
+  }
+  tmem_st32(taddr, w);
+}
+
+// dK / dV out of TMEM (dV at column 256, dK at 384; warpgroup hf = 0 writes dV,
+// 1 writes dK scaled): bf16 into dqkv, or the fp32 partials of a shared kv head.
+__device__ __forceinline__ void dkdv_epilogue(const BwdArgs& a, uint32_t tmem, uint32_t lane_off, int hf, int k,
+                                              bool row_ok, int kvh, int it, uint64_t* acc_done) {
+  const int col0 = (hf ? a.k_col0 : a.v_col0) + kvh * HD;
+  const float mul = hf ? a.scale : 1.0f;
+  __nv_bfloat16* out = a.dqkv + static_cast<size_t>(k) * a.ld_dqkv + col0;
+  if (a.dkv32 != nullptr) {  // fp32 partials (a kv head shared by several ranks)
+    const int n_kv_local = a.n_heads / a.q_per_kv;
+    float* o32 = a.dkv32 + static_cast<size_t>(k) * a.ld_dkv32 + ((hf ? 0 : n_kv_local) + kvh) * HD;
+    if (it > 0) {
+      mbar_wait(acc_done, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t o[32];
+      if (it > 0) {
+        tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<float4*>(o32 + c)[j] =
+              make_float4(__uint_as_float(o[4 * j]) * mul, __uint_as_float(o[4 * j + 1]) * mul,
+                          __uint_as_float(o[4 * j + 2]) * mul, __uint_as_float(o[4 * j + 3]) * mul);
+      }
+    }
+  } else if (it > 0) {
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
+      tmem_ld_wait();
+      if (row_ok) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      }
+    }
+  } else if (row_ok) {
+    for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // dK, dV (v2): one CTA per (key tile, kv head); items = (64-query half block,
 // query head of the group).
 constexpr int KV2_RING = 4;
@@ -766,55 +841,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_arrive(&ds_full[it & 1]);
       if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
     }
-    const int col0 = (hf ? a.k_col0 : a.v_col0) + kvh * HD;
-    const float mul = hf ? a.scale : 1.0f;
-    __nv_bfloat16* out = a.dqkv + static_cast<size_t>(k) * a.ld_dqkv + col0;
-    if (a.dkv32 != nullptr) {  // fp32 partials (a kv head shared by several ranks)
-      const int n_kv_local = a.n_heads / a.q_per_kv;
-      float* o32 = a.dkv32 + static_cast<size_t>(k) * a.ld_dkv32 + ((hf ? 0 : n_kv_local) + kvh) * HD;
-      if (it > 0) {
-        mbar_wait(acc_done, 0);
-        tc_fence_after();
-      }
-#pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t o[32];
-        if (it > 0) {
-          tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
-          tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = 0u;
-        }
-        if (row_ok) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            reinterpret_cast<float4*>(o32 + c)[j] =
-                make_float4(__uint_as_float(o[4 * j]) * mul, __uint_as_float(o[4 * j + 1]) * mul,
-                            __uint_as_float(o[4 * j + 2]) * mul, __uint_as_float(o[4 * j + 3]) * mul);
-        }
-      }
-    } else if (it > 0) {
-      mbar_wait(acc_done, 0);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + 256 + hf * 128 + c, o);
-        tmem_ld_wait();
-        if (row_ok) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            reinterpret_cast<uint4*>(out + c)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
-      }
-    } else if (row_ok) {
-      for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
-    }
+    dkdv_epilogue(a, tmem, lane_off, hf, k, row_ok, kvh, it, acc_done);
   }
   tc_fence_before();
   __syncthreads();
@@ -823,12 +850,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // dQ (v2): one CTA per (query tile, query head); items = 64-key half tiles.
+// kTmemA: Q and dO, the A operands of every S / dP MMA of the CTA, live in
+// TMEM (columns 384 | 448, packed bf16, written once by the softmax warps), so
+// the 64-wide S / dP MMAs read only B from shared memory and run at full rate
+// instead of the 2/3 of the smem-bound ss form. TMEM = [S_0|dP_0] [S_1|dP_1]
+// | dQ | Q | dO = 512 columns.
 constexpr int DQ2_RING = 4;  // K half | V half per stage
 constexpr int DQ2_STAGE = 2 * HALF;
 constexpr int DQ2_OFF_Q = 0, DQ2_OFF_DO = TILE, DQ2_OFF_RING = 2 * TILE;
 constexpr int DQ2_OFF_BAR = DQ2_OFF_RING + DQ2_RING * DQ2_STAGE;
 constexpr size_t DQ2_SMEM = 1024 + DQ2_OFF_BAR + 256;
 
+template <bool kTmemA>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dq2(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV64,
                  const __grid_constant__ CUtensorMap tmDO, BwdArgs a) {
@@ -872,7 +905,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tmQKV);
     tma_prefetch_desc(&tmKV64);
     tma_prefetch_desc(&tmDO);
-    mbar_init(q_full, 1);
+    mbar_init(q_full, kTmemA ? 256 : 1);
     for (int s = 0; s < DQ2_RING; ++s) {
       mbar_init(&r_full[s], 1);
       mbar_init(&r_empty[s], 1);
@@ -894,10 +927,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     reg_dealloc<56>();
     if (warp == 0) {
       if (elect_one()) {
-        mbar_arrive_expect_tx(q_full, 2 * TILE);
-        for (int c = 0; c < 2; ++c) {
-          tma_load_2d(smem + DQ2_OFF_Q + c * CHUNK, &tmQKV, q_full, a.q_col0 + h * HD + c * 64, q0);
-          tma_load_2d(smem + DQ2_OFF_DO + c * CHUNK, &tmDO, q_full, h * HD + c * 64, q0);
+        if (!kTmemA) {
+          mbar_arrive_expect_tx(q_full, 2 * TILE);
+          for (int c = 0; c < 2; ++c) {
+            tma_load_2d(smem + DQ2_OFF_Q + c * CHUNK, &tmQKV, q_full, a.q_col0 + h * HD + c * 64, q0);
+            tma_load_2d(smem + DQ2_OFF_DO + c * CHUNK, &tmDO, q_full, h * HD + c * 64, q0);
+          }
         }
         int slot = 0;
         uint32_t ph = 0;
@@ -918,18 +953,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t q_addr = smem_u32(smem + DQ2_OFF_Q), do_addr = smem_u32(smem + DQ2_OFF_DO);
       const uint32_t ring = smem_u32(smem + DQ2_OFF_RING);
       mbar_wait(q_full, 0);
+      tc_fence_after();
       auto issue_sdp = [&](int it, int slot) {
         const uint32_t tb = tmem + (it & 1) * 128;
         const uint32_t kh = ring + slot * DQ2_STAGE, vh = kh + HALF;
         if (elect_one()) {
+          if (kTmemA) {
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk)
-            mma_bf16_ss(tb, sdesc_sw128(q_addr + kmajor_off(kk)), sdesc_sw128(kh + half_kmajor_off(kk)),
-                        idesc_s, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < HD / 16; ++kk)
+              mma_bf16_ts(tb, tmem + 384 + kk * 8, sdesc_sw128(kh + half_kmajor_off(kk)), idesc_s,
+                          kk > 0 ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk)
-            mma_bf16_ss(tb + 64, sdesc_sw128(do_addr + kmajor_off(kk)), sdesc_sw128(vh + half_kmajor_off(kk)),
-                        idesc_s, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < HD / 16; ++kk)
+              mma_bf16_ts(tb + 64, tmem + 448 + kk * 8, sdesc_sw128(vh + half_kmajor_off(kk)), idesc_s,
+                          kk > 0 ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+              mma_bf16_ss(tb, sdesc_sw128(q_addr + kmajor_off(kk)), sdesc_sw128(kh + half_kmajor_off(kk)),
+                          idesc_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+              mma_bf16_ss(tb + 64, sdesc_sw128(do_addr + kmajor_off(kk)),
+                          sdesc_sw128(vh + half_kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+          }
           mma_commit(&s_full[it & 1]);
         }
         __syncwarp();
@@ -974,6 +1021,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = a.scale_log2;
     const int k_end = min(q + 1, a.L), k_mid = a.Lp;
     const int k_lo = q >= a.Lp ? a.Lp + seg_of(q, m) * a.Lmax : 0;
+    if (kTmemA) {  // this thread's Q / dO row half into the A-operand columns
+      const __nv_bfloat16* qrow = a.qkv + static_cast<size_t>(q) * a.ld_qkv + a.q_col0 + h * HD + hf * 64;
+      const __nv_bfloat16* drow = a.dO + static_cast<size_t>(q) * a.ld_do + h * HD + hf * 64;
+      operand_row_to_tmem(qrow, row_ok, tmem + lane_off + 384 + hf * 32);
+      operand_row_to_tmem(drow, row_ok, tmem + lane_off + 448 + hf * 32);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(q_full);
+    }
     int it = 0;
     for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb), ++it) {
       const uint32_t tb = tmem + lane_off + (it & 1) * 128;
@@ -1296,16 +1352,19 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
                                    static_cast<int>(DQ_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV_SMEM)));
-    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(DQ2_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(DQ2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV2_SMEM)));
     return true;
   }();
-  // MRSP_ATTN_BWD=1: the single-buffered v1 kernels (kept for A/B)
+  // MRSP_ATTN_BWD=1: the single-buffered v1 kernels; =2: v2 with the dQ
+  // kernel's Q / dO read from shared memory (both kept for A/B)
   static const int version = [] {
     const char* v = std::getenv("MRSP_ATTN_BWD");
-    return v ? std::atoi(v) : 2;
+    return v ? std::atoi(v) : 3;
   }();
   (void)attr;
   // D = rowsum(dO o O) into the workspace p.D (unless the caller provides it)
@@ -1337,6 +1396,10 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   a.row_part = p.row_part;
   a.dkv32 = p.dkv32;
   a.ld_dkv32 = p.ld_dkv32;
+  a.qkv = static_cast<const __nv_bfloat16*>(p.qkv);
+  a.ld_qkv = p.ld_qkv;
+  a.dO = static_cast<const __nv_bfloat16*>(p.dO);
+  a.ld_do = p.ld_do;
   a.n_blocks = (p.L + ATTN_ROW_BLOCK - 1) / ATTN_ROW_BLOCK;
   a.n_local_blocks = 0;
   if (p.row_parts > 1)
@@ -1363,7 +1426,10 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   CUtensorMap tlse64 = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   CUtensorMap td64 = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (n_tiles > 0) {
-    attn_bwd_dq2<<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
+    if (version >= 3)
+      attn_bwd_dq2<true><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
+    else
+      attn_bwd_dq2<false><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
