@@ -329,6 +329,11 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         if comm == "nccl":
+            if same_dev:  # NCCL refuses two ranks on one GPU of one host: a host id
+                # per rank puts them on its socket transport over loopback
+                os.environ["NCCL_HOSTID"] = f"mrsp-bench-{rank}"
+                os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+                os.environ.setdefault("NCCL_IB_DISABLE", "1")
             obj = [E.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             nccl_id = obj[0]

@@ -17,8 +17,11 @@ pytestmark = pytest.mark.gpu
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 
 
-def test_bench_self_launches_two_ranks(gpu):
-    env = {**os.environ, "MRSP_BENCH_SAME_DEVICE": "1"}
+@pytest.mark.parametrize("comm", ["p2p", "nccl"])
+def test_bench_self_launches_two_ranks(gpu, comm):
+    """comm "nccl": the NCCL transport (MRSP_COMM=nccl), the two ranks on
+    separate NCCL host ids (its socket transport; tests/test_nccl_gpu.py)."""
+    env = {**os.environ, "MRSP_BENCH_SAME_DEVICE": "1", "MRSP_COMM": comm}
     env.pop("WORLD_SIZE", None)
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--workload", "c1",
                           "--steps", "1", "--warmup", "3", "--no-cpu", "--no-gen"],
