@@ -1060,11 +1060,17 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
       Prof pa(*this, P_ATTN);
+      const size_t ri = static_cast<size_t>(&R - ranks_.data());
+      float* lse_keep = ri < stash_lse_.size()
+                            ? stash_lse_[ri] + static_cast<size_t>(layer) * nqr * stash_lse_ld_
+                            : nullptr;
       if (k_ == 1) {
-        attention_fwd({R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
-                       R.ol.p, Cq, 0, static_cast<int>(g.Ltot), nq, nq / nkv, scale,
-                       ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0},
-                      s);
+        AttnParams ap{R.qkv.p, Cqkv, 0, R.qkv.p, Cqkv, nq * 128, R.qkv.p, Cqkv, (nq + nkv) * 128,
+                      R.ol.p, Cq, 0, static_cast<int>(g.Ltot), nq, nq / nkv, scale,
+                      ATTN_CAUSAL_PREFIX, static_cast<int>(g.Lp), g.Lmax, 0};
+        ap.lse = lse_keep;
+        ap.lse_ld = stash_lse_ld_;
+        attention_fwd(ap, s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
         void* qh = fused_a2a() ? qh_dst(R.g) : R.qh.p;
@@ -1087,11 +1093,19 @@ void Engine::run_pass(const CacheEntry& emb, int model, int xs_slot) {
           ap.dst_ld = Cq;
           ap.dst_col0 = R.hs.q_lo * 128;
         }
+        ap.lse = lse_keep;
+        ap.lse_ld = stash_lse_ld_;
         attention_fwd(ap, s);
       }
     }
     if (k_ > 1 && !fused_a2a()) a2a_backward(static_cast<int>(g.Ltot));
     if (mesh_) mesh_->barrier(s);  // every rank's O rows have landed
+    for (size_t r = 0; r < stash_o_.size(); ++r) {  // backward: keep this layer's O
+      const size_t nc = static_cast<size_t>(ranks_[r].e - ranks_[r].b) * Cq;
+      if (nc)
+        MRSP_CUDA(cudaMemcpyAsync(stash_o_[r] + layer * nc, mesh_ ? ol_dst(ranks_[r].g) : ranks_[r].ol.p,
+                                  nc * 2, cudaMemcpyDeviceToDevice, s));
+    }
     for (auto& R : ranks_) {
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;

@@ -219,6 +219,14 @@ class Engine {
   // the fp32 gradients in the engine's weight layout
   std::vector<float*> stash_;
   std::vector<DevBuf> stash_bufs_, bwd_ws_;
+  // ... and, when they fit (bwd_stash_attention), each layer's attention
+  // output O ([layers][n][nq 128] bf16, sequence shard) and log-sum-exp
+  // ([layers][nq_r][stash_lse_ld_] fp32, head shard), so the backward skips
+  // the attention recompute
+  std::vector<bf16*> stash_o_;
+  std::vector<float*> stash_lse_;
+  std::vector<DevBuf> stash_attn_bufs_;
+  int stash_lse_ld_ = 0;
   DevBuf grad_buf_, bwd_group_ws_;
   LlmW grads_{};  // fp32 storage typed as the weight struct (see save_grads)
   bool have_grads_ = false;

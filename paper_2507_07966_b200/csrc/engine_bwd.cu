@@ -13,7 +13,8 @@
 //   final norm   RMSNorm backward at the scored positions
 //   layer l      recomputed from its kept input h_l (activation checkpointing:
 //                the forward keeps one fp32 [n][d] per layer): RMSNorm, QKV +
-//                RoPE, attention (with its log-sum-exp), O projection, RMSNorm;
+//                RoPE, attention (with its log-sum-exp — or, when they fit,
+//                the O and log-sum-exp the policy pass kept), O projection, RMSNorm;
 //                then  d act = dh W_down;  the gate/up GEMM again with the
 //                SwiGLU-backward epilogue (dgate | dup, and act);  wgrads of
 //                W_down, W_gate|up;  dx = dgu W_gu;  RMSNorm backward;  dO =
@@ -251,6 +252,46 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
     w.ld_stat = ld_stat;
     stash_bufs_[r].ensure(std::max<size_t>(static_cast<size_t>(NL) * nd * 4, 256));
   }
+  // The policy pass also keeps every layer's attention output O and its
+  // log-sum-exp when they fit, so the layer recompute below skips the
+  // attention (MRSP_BWD_STASH_ATTN=0 / 1: never / always; default: when the
+  // largest rank's share is at most a quarter of the device). The decision
+  // uses only global sizes, so every process of a mesh takes the same one.
+  const int ld_keep = static_cast<int>((Ltot + 3) / 4 * 4);
+  bool keep_attn = false;
+  std::vector<size_t> o_keep_bytes(NLOC, 0);
+  {
+    const char* env = std::getenv("MRSP_BWD_STASH_ATTN");
+    long n_max = 0;
+    int nq_max = 1;
+    for (int p = 0; p < K; ++p) {
+      n_max = std::max(n_max, token_e_[p] - token_b_[p]);
+      nq_max = std::max(nq_max, split_of(p).nq());
+    }
+    const size_t per_rank = static_cast<size_t>(NL) * n_max * Cq * 2 +
+                            static_cast<size_t>(NL) * nq_max * ld_keep * 4;
+    size_t free_b = 0, total_b = 0;
+    MRSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    keep_attn = env && std::string(env) == "1"
+                    ? true
+                    : !(env && std::string(env) == "0") && per_rank * NLOC <= total_b / 4;
+  }
+  stash_attn_bufs_.resize(NLOC);
+  if (keep_attn)
+    for (int r = 0; r < NLOC; ++r) {
+      const size_t n = static_cast<size_t>(ranks_[r].e - ranks_[r].b);
+      o_keep_bytes[r] = (static_cast<size_t>(NL) * n * Cq * 2 + 255) / 256 * 256;
+      stash_attn_bufs_[r].ensure(o_keep_bytes[r] + static_cast<size_t>(NL) *
+                                                       std::max(ranks_[r].hs.nq(), 1) * ld_keep * 4);
+    }
+  auto o_kept = [&](int r, int l) {
+    return static_cast<bf16*>(stash_attn_bufs_[r].p) +
+           static_cast<size_t>(l) * (ranks_[r].e - ranks_[r].b) * Cq;
+  };
+  auto lse_kept = [&](int r, int l) {
+    return reinterpret_cast<float*>(static_cast<uint8_t*>(stash_attn_bufs_[r].p) + o_keep_bytes[r]) +
+           static_cast<size_t>(l) * std::max(ranks_[r].hs.nq(), 1) * ld_keep;
+  };
 
   // Ulysses routing of the backward (every global rank's buffers; across
   // processes the peers' landing buffers)
@@ -299,13 +340,28 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   if (mode == 0) run_pass(emb, 1, 1);  // xs2 = reference final-norm rows
   stash_.resize(NLOC);
   for (int r = 0; r < NLOC; ++r) stash_[r] = stash_bufs_[r].as<float>();
+  if (keep_attn) {
+    stash_o_.resize(NLOC);
+    stash_lse_.resize(NLOC);
+    for (int r = 0; r < NLOC; ++r) {
+      stash_o_[r] = o_kept(r, 0);
+      stash_lse_[r] = lse_kept(r, 0);
+    }
+    stash_lse_ld_ = ld_keep;
+  }
+  auto unstash = [&] {
+    stash_.clear();
+    stash_o_.clear();
+    stash_lse_.clear();
+    stash_lse_ld_ = 0;
+  };
   try {
     run_pass(emb, 0, 0);  // xs = policy final-norm rows; h = h_L of every shard
   } catch (...) {
-    stash_.clear();
+    unstash();
     throw;
   }
-  stash_.clear();
+  unstash();
   lm_exchange(mode == 0 ? 2 : 1);  // the final-norm rows to the LM-head slices (spread LM head)
   const LlmW& W = llm_[0];
   // SFT has no reference model: the dual head runs the policy against itself
@@ -413,6 +469,7 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
     LlmLayerW& Lg = grads_.layers[l];
     // (1) recompute the layer's attention input: RMSNorm, QKV + RoPE routed to
     // the head shards (the forward's fused epilogue), attention with its lse
+    // (unless the policy pass kept O and lse)
     for (int r = 0; r < NLOC; ++r) {
       RankCtx& R = ranks_[r];
       const int n = static_cast<int>(R.e - R.b);
@@ -432,7 +489,7 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       gemm_bf16(ga, s);
     }
     if (mesh_) mesh_->barrier(s);  // every rank's head blocks have landed
-    for (int r = 0; r < NLOC; ++r) {
+    for (int r = 0; r < NLOC && !keep_attn; ++r) {
       RankCtx& R = ranks_[r];
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
@@ -475,7 +532,7 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       const int n = static_cast<int>(R.e - R.b);
       if (n <= 0) continue;
       const size_t nd = static_cast<size_t>(n) * d;
-      bf16* ol = static_cast<bf16*>(ol_dst(R.g));
+      bf16* ol = keep_attn ? o_kept(r, l) : static_cast<bf16*>(ol_dst(R.g));
       const float* h_in = stash_bufs_[r].as<float>() + static_cast<size_t>(l) * nd;
       MRSP_CUDA(cudaMemcpyAsync(w.hm, h_in, nd * 4, cudaMemcpyDeviceToDevice, s));
       gemm_bf16({ol, Lw.wo, nullptr, n, d, Cq, Cq, Cq, 0, GEMM_EPI_RESID_F32, nullptr, w.hm, d}, s);
@@ -514,15 +571,17 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
       const int nqr = R.hs.nq();
       if (nqr == 0) continue;
       Prof pa(*this, P_BWD_ATTN);
+      float* lse = keep_attn ? lse_kept(r, l) : rw[r].stat_lse;
       if (K == 1) {
-        AttnBwdParams bp{R.qkv.p, Cqkv, 0, nq * 128, (nq + nkv) * 128, R.ol.p, Cq, rw[r].dO, Cq,
-                         rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat, rw[r].dqkv, Cqkv,
+        AttnBwdParams bp{R.qkv.p, Cqkv, 0, nq * 128, (nq + nkv) * 128,
+                         keep_attn ? static_cast<void*>(o_kept(r, l)) : R.ol.p, Cq, rw[r].dO, Cq,
+                         lse, rw[r].stat_D, rw[r].ld_stat, rw[r].dqkv, Cqkv,
                          static_cast<int>(Ltot), nq, nq / nkv, scale, static_cast<int>(g.Lp), g.Lmax};
         attention_bwd(bp, s);
       } else {
         const int Cr = (nqr + 2 * R.hs.nkv()) * 128;
         AttnBwdParams bp{qh_dst(R.g), Cr, 0, nqr * 128, (nqr + R.hs.nkv()) * 128, nullptr, nqr * 128,
-                         rw[r].doh, nqr * 128, rw[r].stat_lse, rw[r].stat_D, rw[r].ld_stat,
+                         rw[r].doh, nqr * 128, lse, rw[r].stat_D, rw[r].ld_stat,
                          rw[r].dqkvh, Cr, static_cast<int>(Ltot), nqr, R.hs.q_per_kv, scale,
                          static_cast<int>(g.Lp), g.Lmax};
         bp.d_given = 1;

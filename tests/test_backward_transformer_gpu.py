@@ -373,6 +373,28 @@ def test_grpo_backward_sp_matches_sp1(gpu, wname, sps):
         assert worst < (5e-3 if shared_kv else 1e-4), (sp, worst)  # measured 4e-6 (c1 sp4) / 2.2e-3 (c2 sp8)
 
 
+@pytest.mark.parametrize("wname,sp", [("c1", 1), ("c1", 2), ("c2", 8)])
+def test_grpo_backward_kept_attention_bit_identical(gpu, wname, sp, monkeypatch):
+    """The policy pass keeping every layer's attention output and log-sum-exp
+    (MRSP_BWD_STASH_ATTN=1) instead of the backward recomputing them (=0): the
+    same kernels on the same inputs, so gradients, log-probs and statistics are
+    bit-identical (c2 SP 8: the query-row split, O rows from peers)."""
+    w = E.workloads()[wname]
+    grp = E.make_group(w, seed=5)
+    rng = np.random.default_rng(2)
+    old = rng.normal(-2, 0.3, size=grp.scored).astype(np.float32)
+    adv = rng.normal(size=w.G).astype(np.float32)
+    out = {}
+    for keep in ("0", "1"):
+        monkeypatch.setenv("MRSP_BWD_STASH_ATTN", keep)
+        out[keep] = _grads(w.cfg, w.frames, sp, grp, old, adv)
+    (st0, lp0, g0), (st1, lp1, g1) = out["0"], out["1"]
+    assert st0 == st1 and np.array_equal(lp0, lp1)
+    assert g0.keys() == g1.keys()
+    for k in g0:
+        assert np.array_equal(g0[k], g1[k]), k
+
+
 def test_sft_backward_c1_vs_autograd(gpu):
     """sft_loss_and_grad (grpo.cpp:208-223) through the transformer prefill."""
     w = E.workloads()["c1"]
