@@ -89,6 +89,31 @@ __device__ __forceinline__ MaskDev mask_of(const BwdArgs& a) {
   return MaskDev{ATTN_CAUSAL_PREFIX, a.L, a.Lp, a.Lmax, 1};
 }
 
+// Per-phase timeline of one dK / dV CTA (dev tool tools/ubench/bwd_trace.cu
+// builds this file with MRSP_BWD_TRACE): clock() stamps of lane 0 per warp.
+#ifdef MRSP_BWD_TRACE
+constexpr int kBTraceCap = 4096;
+__device__ uint64_t g_bwd_trace[12][kBTraceCap];
+__device__ int g_bwd_trace_n[12];
+__device__ int g_bwd_trace_cta;
+#define BTRACE_INIT int btrace_n = 0
+#define BTRACE(ev, it)                                                                            \
+  do {                                                                                            \
+    if (blockIdx.x == g_bwd_trace_cta && (threadIdx.x & 31) == 0 && btrace_n < kBTraceCap)        \
+      g_bwd_trace[threadIdx.x >> 5][btrace_n++] = (static_cast<uint64_t>(ev) << 56) |              \
+                                                  (static_cast<uint64_t>((it) & 0xffffff) << 32) | \
+                                                  static_cast<uint32_t>(clock());                 \
+  } while (0)
+#define BTRACE_FINISH \
+  if (blockIdx.x == g_bwd_trace_cta && (threadIdx.x & 31) == 0) g_bwd_trace_n[threadIdx.x >> 5] = btrace_n
+#else
+#define BTRACE_INIT
+#define BTRACE(ev, it) \
+  do {                 \
+  } while (0)
+#define BTRACE_FINISH
+#endif
+
 // K-major SW128 operand: 16-element K step kk of a 128 x 128 tile (two 64-col chunks)
 __device__ __forceinline__ uint32_t kmajor_off(int kk) { return (kk / 4) * CHUNK + (kk % 4) * 32; }
 
@@ -653,6 +678,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
   const int warp = warp_id();
+  BTRACE_INIT;
   const MaskDev m = mask_of(a);
   const int n_kt = (a.L + TK - 1) / TK;
   const int kvh = blockIdx.x / n_kt;
@@ -722,6 +748,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (Items t = items_begin(); t.qb < qb_hi; items_next(t)) {
           const int qb = t.qb, h = kvh * a.q_per_kv + t.hh;
           mbar_wait(&r_empty[slot], ph ^ 1);
+          BTRACE(20, qb);
           mbar_arrive_expect_tx(&r_full[slot], 2 * HALF + KV2_STAT);
           uint8_t* st = smem + KV2_OFF_RING + slot * KV2_STAGE;
           for (int c = 0; c < 2; ++c) {
@@ -757,6 +784,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       auto issue_acc = [&](int it, int slot) {
         mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+        BTRACE(12, it);
         tc_fence_after();
         const uint32_t q_addr = ring + slot * KV2_STAGE, do_addr = q_addr + HALF;
         if (elect_one()) {
@@ -776,9 +804,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       for (Items t = items_begin(); t.qb < qb_hi; items_next(t), ++it) {
         mbar_wait(&r_full[slot], ph);
+        BTRACE(10, it);
         tc_fence_after();
         issue_sdp(it, slot);
+        BTRACE(11, it);
         if (it > 0) issue_acc(it - 1, prev);
+        if (it > 0) BTRACE(13, it - 1);
         prev = slot;
         if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
       }
@@ -813,12 +844,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         d_r[4 * j] = y.x; d_r[4 * j + 1] = y.y; d_r[4 * j + 2] = y.z; d_r[4 * j + 3] = y.w;
       }
       const uint32_t tb = tmem + lane_off + (it & 1) * 128;
+      BTRACE(0, it);
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+      BTRACE(1, it);
       tc_fence_after();
       uint32_t sv[32], dv[32];
       tmem_ld32(tb + hf * 32, sv);
       tmem_ld32(tb + 64 + hf * 32, dv);
       tmem_ld_wait();
+      BTRACE(2, it);
       const int qbase = qb * 64 + hf * 32;
       const uint32_t vis = lt_bits(q_vis_end, qbase) & ~lt_bits(k, qbase);
       uint32_t wp[16], wd[16];
@@ -834,15 +868,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         wp[j2] = pack_bf16(p[0], p[1]);
         wd[j2] = pack_bf16(g[0], g[1]);
       }
+      BTRACE(3, it);
       tmem_st16(tb + hf * 32, wp);
       tmem_st16(tb + 64 + hf * 32, wd);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&ds_full[it & 1]);
+      BTRACE(4, it);
       if (++slot == KV2_RING) { slot = 0; ph ^= 1; }
     }
     dkdv_epilogue(a, tmem, lane_off, hf, k, row_ok, kvh, it, acc_done);
   }
+  BTRACE_FINISH;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
