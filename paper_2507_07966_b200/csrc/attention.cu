@@ -170,38 +170,6 @@ __device__ int g_attn_trace_cta;
 #define ATRACE_FINISH
 #endif
 
-// (2^x0, 2^x1) on the FMA pipe, packed: x = j + f with j = round(x) taken from
-// the low mantissa bits of x + 1.5*2^23, f in [-0.5, 0.5], degree-3 minimax
-// polynomial for 2^f (max rel. error 7.7e-5, far below bf16's 3.9e-3), then j
-// added to the exponent field (one LEA). 8 issue slots per pair instead of two
-// MUFU.EX2 (which is the softmax's binding pipe: 16 results/clk/SM, the same
-// rate the tensor core consumes P at). Inputs clamp at -126 (2^-126 ~ 1e-38,
-// i.e. zero after the P.V product and the row sum).
-__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& p0, float& p1) {
-  constexpr float kRound = 12582912.0f;  // 1.5 * 2^23
-  x0 = fmaxf(x0, -126.0f);
-  x1 = fmaxf(x1, -126.0f);
-  float r0 = x0, r1 = x1;
-  fadd2(r0, r1, kRound, kRound);
-  float t0, t1, f0, f1;
-  fsub2(t0, t1, r0, r1, kRound, kRound);
-  fsub2(f0, f1, x0, x1, t0, t1);
-  float q0, q1;
-  ffma2(q0, q1, f0, f1, 0.05508868396282196f, 0.05508868396282196f, 0.24260404706001282f,
-        0.24260404706001282f);
-  ffma2(q0, q1, f0, f1, q0, q1, 0.6932762265205383f, 0.6932762265205383f);
-  ffma2(q0, q1, f0, f1, q0, q1, 0.9999289512634277f, 0.9999289512634277f);
-  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(r0) << 23));
-  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(r1) << 23));
-}
-
-// Pair i (of 32 per 64-key half) takes the FMA-pipe exp2 when kPoly of every
-// 32 pairs are to be offloaded (spread evenly, Bresenham).
-template <int kPoly>
-__device__ __forceinline__ constexpr bool poly_pair(int i) {
-  return kPoly > 0 && ((i + 1) * kPoly) / 32 != (i * kPoly) / 32;
-}
-
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (0 = all MUFU).
 // kPC: chunks P is handed to the P.V MMA in (2: 64-key halves; 4: 32-key
 // quarters, so the last chunk's MMA is shorter on the S -> P -> P.V chain).

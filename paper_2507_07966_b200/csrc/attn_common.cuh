@@ -67,6 +67,46 @@ __device__ __forceinline__ void fsub2(float& d0, float& d1, float a0, float a1, 
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 
+__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// (2^x0, 2^x1) on the FMA pipe, packed: x = j + f with j = round(x) taken from
+// the low mantissa bits of x + 1.5*2^23, f in [-0.5, 0.5], degree-3 minimax
+// polynomial for 2^f (max rel. error 7.7e-5, far below bf16's 3.9e-3), then j
+// added to the exponent field (one LEA). 8 issue slots per pair instead of two
+// MUFU.EX2 (which is the softmax's binding pipe: 16 results/clk/SM, the same
+// rate the tensor core consumes P at). Inputs clamp at -126 (2^-126 ~ 1e-38,
+// i.e. zero after the P.V product and the row sum).
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& p0, float& p1) {
+  constexpr float kRound = 12582912.0f;  // 1.5 * 2^23
+  x0 = fmaxf(x0, -126.0f);
+  x1 = fmaxf(x1, -126.0f);
+  float r0 = x0, r1 = x1;
+  fadd2(r0, r1, kRound, kRound);
+  float t0, t1, f0, f1;
+  fsub2(t0, t1, r0, r1, kRound, kRound);
+  fsub2(f0, f1, x0, x1, t0, t1);
+  float q0, q1;
+  ffma2(q0, q1, f0, f1, 0.05508868396282196f, 0.05508868396282196f, 0.24260404706001282f,
+        0.24260404706001282f);
+  ffma2(q0, q1, f0, f1, q0, q1, 0.6932762265205383f, 0.6932762265205383f);
+  ffma2(q0, q1, f0, f1, q0, q1, 0.9999289512634277f, 0.9999289512634277f);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(r0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(r1) << 23));
+}
+
+// Pair i (of 32 per 64-key half) takes the FMA-pipe exp2 when kPoly of every
+// 32 pairs are to be offloaded (spread evenly, Bresenham).
+template <int kPoly>
+__device__ __forceinline__ constexpr bool poly_pair(int i) {
+  return kPoly > 0 && ((i + 1) * kPoly) / 32 != (i * kPoly) / 32;
+}
+
 // bit j set iff base + j < bound (j in [0, 32)).
 __device__ __forceinline__ uint32_t lt_bits(int bound, int base) {
   const int n = bound - base;

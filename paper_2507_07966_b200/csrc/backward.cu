@@ -15,10 +15,14 @@
 //                  packed bf16 back into TMEM, and dQ += dS K (A operand from
 //                  TMEM, K read MN-major from the same smem half). Q and dO,
 //                  constant over the CTA, sit in TMEM as the S / dP A operands.
-//   attn_bwd_dkdv2 one CTA per (128-key tile, kv head), sweeping the q_per_kv
-//                  query heads x the 64-query halves that see it:  S^T = K Q^T,
+//   attn_bwd_dkdv4 one CTA per (128-key tile, kv head), sweeping the q_per_kv
+//                  query heads x the 128-query tiles that see it:  S^T = K Q^T,
 //                  dP^T = V dO^T, P^T and dS^T packed into TMEM, then
-//                  dV += P^T dO and dK += dS^T Q (dO, Q read MN-major).
+//                  dV += P^T dO and dK += dS^T Q (dO, Q read MN-major), the
+//                  softmax handing P^T and dS^T over separately so that it
+//                  runs behind dK(i-1), dP^T(i) and dV(i), S^T(i+1).
+//                  (attn_bwd_dkdv2: 64-query halves over two S^T / dP^T
+//                  buffers, MRSP_ATTN_BWD=2 / 3.)
 //
 // (attn_bwd_dq / attn_bwd_dkdv: the single-buffered 128-wide first version,
 // MRSP_ATTN_BWD=1.) lse is the forward kernel's per-row log-sum-exp (scaled
@@ -886,6 +890,286 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// dK, dV (v4): 128-query items, ONE S^T / dP^T buffer pair, and the softmax
+// handing P^T and dS^T over separately. The tensor core runs, per item i,
+//   S^T(i) -> dK += dS^T(i-1) Q(i-1) -> dP^T(i) -> dV += P^T(i) dO(i)
+// so the softmax turns S^T(i) into P^T(i) behind dK(i-1) and dP^T(i), and
+// dP^T(i) into dS^T(i) behind dV(i) and S^T(i+1). The N = 128 S^T / dP^T MMAs
+// read K / V once per 128 queries at the full ss rate (v2's N = 64 halves
+// re-read the key tile for every 64 queries and are shared-memory bound,
+// profiles/r1_attention_study.md §7b). TMEM = S^T | dP^T | dV | dK (512
+// columns), like v1, which handed P^T and dS^T over together after both MMAs
+// and so serialised the softmax and the tensor core. Each ring stage has two
+// barriers: Q + lse (for S^T and P^T) and dO + D (for dP^T and dS^T).
+// kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (P^T is the
+// MUFU-bound step on the S^T -> P^T -> dV chain).
+template <int kPoly>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_dkdv4(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                   const __grid_constant__ CUtensorMap tmLSE, const __grid_constant__ CUtensorMap tmD,
+                   BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KV_OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* rq_full = bars + 1;               // [KV_RING] Q + lse landed
+  uint64_t* rd_full = bars + 1 + KV_RING;     // [KV_RING] dO + D landed
+  uint64_t* r_empty = bars + 1 + 2 * KV_RING;  // [KV_RING]
+  uint64_t* s_full = bars + 1 + 3 * KV_RING;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* p_ready = s_full + 2;
+  uint64_t* ds_ready = s_full + 3;
+  uint64_t* acc_done = s_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+
+  const int warp = warp_id();
+  BTRACE_INIT;
+  const MaskDev m = mask_of(a);
+  const int n_kt = (a.L + TK - 1) / TK;
+  const int kvh = blockIdx.x / n_kt;
+  const int kt = blockIdx.x - kvh * n_kt;
+  const int k0 = kt * TK;
+  const int q_end = k0 < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(min(k0 + TK - 1, a.L - 1), m) + 1) * a.Lmax);
+  const int qt_lo = k0 / TQ, qt_hi = (q_end + TQ - 1) / TQ;
+  struct Items {  // (128-row query tile, query head of the group), head-minor
+    int qt, hh;
+    __device__ void own(const BwdArgs& a, int hi) {
+      while (qt < hi && !own_rows(qt * TQ, a)) ++qt;
+    }
+  };
+  auto items_begin = [&]() {
+    Items t{qt_lo, 0};
+    t.own(a, qt_hi);
+    return t;
+  };
+  auto items_next = [&](Items& t) {
+    if (++t.hh == a.q_per_kv) {
+      t.hh = 0;
+      ++t.qt;
+      t.own(a, qt_hi);
+    }
+  };
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmDO);
+    tma_prefetch_desc(&tmLSE);
+    tma_prefetch_desc(&tmD);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < KV_RING; ++s) {
+      mbar_init(&rq_full[s], 1);
+      mbar_init(&rd_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_ready, 256);
+    mbar_init(ds_ready, 256);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
+
+  if (warp < 4) {
+    reg_dealloc<56>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_2d(smem + KV_OFF_K + c * CHUNK, &tmQKV, kv_full, a.k_col0 + kvh * HD + c * 64, k0);
+          tma_load_2d(smem + KV_OFF_V + c * CHUNK, &tmQKV, kv_full, a.v_col0 + kvh * HD + c * 64, k0);
+        }
+        int slot = 0;
+        uint32_t ph = 0;
+        for (Items t = items_begin(); t.qt < qt_hi; items_next(t)) {
+          const int qt = t.qt, h = kvh * a.q_per_kv + t.hh;
+          mbar_wait(&r_empty[slot], ph ^ 1);
+          BTRACE(20, qt);
+          uint8_t* st = smem + KV_OFF_RING + slot * KV_STAGE;
+          mbar_arrive_expect_tx(&rq_full[slot], TILE + 512);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(st + c * CHUNK, &tmQKV, &rq_full[slot], a.q_col0 + h * HD + c * 64, qt * TQ);
+          tma_load_2d(st + 2 * TILE, &tmLSE, &rq_full[slot], qt * TQ, h);
+          mbar_arrive_expect_tx(&rd_full[slot], TILE + 512);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(st + TILE + c * CHUNK, &tmDO, &rd_full[slot], h * HD + c * 64, qt * TQ);
+          tma_load_2d(st + 2 * TILE + 512, &tmD, &rd_full[slot], qt * TQ, h);
+          if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1) {
+      const uint32_t idesc_s = idesc_bf16_f32(TK, TQ);
+      const uint32_t idesc_o = idesc_bf16_f32_bmn(TK, HD);
+      const uint32_t k_addr = smem_u32(smem + KV_OFF_K), v_addr = smem_u32(smem + KV_OFF_V);
+      const uint32_t ring = smem_u32(smem + KV_OFF_RING);
+      mbar_wait(kv_full, 0);
+      // dK += dS^T(j) Q(j) (A: packed pairs in columns [128,160) + [192,224)),
+      // then the ring slot of item j is free
+      auto issue_dk = [&](int j, int jslot) {
+        mbar_wait(ds_ready, j & 1);
+        BTRACE(14, j);
+        tc_fence_after();
+        const uint32_t q_addr = ring + jslot * KV_STAGE;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < TQ / 16; ++kk)
+            mma_bf16_ts(tmem + 384, tmem + 128 + (kk / 4) * 64 + (kk % 4) * 8,
+                        sdesc_sw128_mn(q_addr + kk * 2048, CHUNK), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&r_empty[jslot]);
+        }
+        __syncwarp();
+      };
+      int slot = 0, prev = 0, it = 0;
+      uint32_t ph = 0;
+      for (Items t = items_begin(); t.qt < qt_hi; items_next(t), ++it) {
+        const uint32_t q_addr = ring + slot * KV_STAGE, do_addr = q_addr + TILE;
+        // S^T(i) overwrites P^T(i-1) and dP^T(i) overwrites dS^T(i-1): both
+        // read by MMAs issued earlier, and the tensor pipe runs in issue order
+        mbar_wait(&rq_full[slot], ph);
+        BTRACE(10, it);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem, sdesc_sw128(k_addr + kmajor_off(kk)), sdesc_sw128(q_addr + kmajor_off(kk)),
+                        idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(s_full);
+        }
+        __syncwarp();
+        if (it > 0) issue_dk(it - 1, prev);
+        mbar_wait(&rd_full[slot], ph);
+        BTRACE(11, it);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            mma_bf16_ss(tmem + 128, sdesc_sw128(v_addr + kmajor_off(kk)),
+                        sdesc_sw128(do_addr + kmajor_off(kk)), idesc_s, kk > 0 ? 1u : 0u);
+          mma_commit(dp_full);
+        }
+        __syncwarp();
+        // dV += P^T(i) dO(i) (A: packed pairs in columns [0,32) + [64,96))
+        mbar_wait(p_ready, it & 1);
+        BTRACE(12, it);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < TQ / 16; ++kk)
+            mma_bf16_ts(tmem + 256, tmem + (kk / 4) * 64 + (kk % 4) * 8,
+                        sdesc_sw128_mn(do_addr + kk * 2048, CHUNK), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+        BTRACE(13, it);
+        prev = slot;
+        if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+      }
+      if (it > 0) issue_dk(it - 1, prev);
+      if (elect_one()) mma_commit(acc_done);
+      __syncwarp();
+    }
+  } else {
+    reg_alloc<200>();
+    const int hf = (warp - 4) >> 2;  // query columns [64 hf, 64 hf + 64) of the item
+    const int ew = (warp - 4) & 3;
+    const int r = ew * 32 + lane_id();
+    const int k = k0 + r;
+    const bool row_ok = k < a.L;
+    const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
+    const float sl2 = a.scale_log2;
+    const int q_vis_end = !row_ok ? 0 : k < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(k, m) + 1) * a.Lmax);
+    const uint32_t tS = tmem + lane_off + hf * 64, tP = tmem + lane_off + 128 + hf * 64;
+    int slot = 0, it = 0;
+    uint32_t ph = 0;
+    for (Items t = items_begin(); t.qt < qt_hi; items_next(t), ++it) {
+      const int qbase = t.qt * TQ + hf * 64;
+      const float4* st_lse =
+          reinterpret_cast<const float4*>(smem + KV_OFF_RING + slot * KV_STAGE + 2 * TILE) + hf * 16;
+      const float4* st_d = st_lse + 32;
+      float p[64];
+      mbar_wait(&rq_full[slot], ph);
+      BTRACE(0, it);
+      mbar_wait(s_full, it & 1);
+      BTRACE(1, it);
+      tc_fence_after();
+      uint32_t w[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t sv[32];
+        tmem_ld32(tS + c * 32, sv);
+        tmem_ld_wait();
+        const uint32_t vis = lt_bits(q_vis_end, qbase + 32 * c) & ~lt_bits(k, qbase + 32 * c);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 l4 = st_lse[c * 8 + j4];
+          float x[4];
+          ffma2(x[0], x[1], __uint_as_float(sv[4 * j4]), __uint_as_float(sv[4 * j4 + 1]), sl2, sl2, -l4.x,
+                -l4.y);
+          ffma2(x[2], x[3], __uint_as_float(sv[4 * j4 + 2]), __uint_as_float(sv[4 * j4 + 3]), sl2, sl2, -l4.z,
+                -l4.w);
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const int j = 4 * j4 + e;
+            float y0, y1;
+            if (poly_pair<kPoly>(16 * c + j / 2)) {
+              exp2_poly2(x[e], x[e + 1], y0, y1);
+            } else {
+              y0 = exp2_mufu(x[e]);
+              y1 = exp2_mufu(x[e + 1]);
+            }
+            p[32 * c + j] = ((vis >> j) & 1u) ? y0 : 0.f;
+            p[32 * c + j + 1] = ((vis >> (j + 1)) & 1u) ? y1 : 0.f;
+          }
+          w[16 * c + 2 * j4] = pack_bf16(p[32 * c + 4 * j4], p[32 * c + 4 * j4 + 1]);
+          w[16 * c + 2 * j4 + 1] = pack_bf16(p[32 * c + 4 * j4 + 2], p[32 * c + 4 * j4 + 3]);
+        }
+      }
+      tmem_st32(tS, w);  // packed P^T over this half's first 32 columns
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_ready);
+      BTRACE(3, it);
+      mbar_wait(&rd_full[slot], ph);
+      mbar_wait(dp_full, it & 1);
+      BTRACE(4, it);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t dv[32];
+        tmem_ld32(tP + c * 32, dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 d4 = st_d[c * 8 + j4];
+          float g[4];
+          fsub2(g[0], g[1], __uint_as_float(dv[4 * j4]), __uint_as_float(dv[4 * j4 + 1]), d4.x, d4.y);
+          fsub2(g[2], g[3], __uint_as_float(dv[4 * j4 + 2]), __uint_as_float(dv[4 * j4 + 3]), d4.z, d4.w);
+          fmul2(g[0], g[1], p[32 * c + 4 * j4], p[32 * c + 4 * j4 + 1], g[0], g[1]);
+          fmul2(g[2], g[3], p[32 * c + 4 * j4 + 2], p[32 * c + 4 * j4 + 3], g[2], g[3]);
+          w[16 * c + 2 * j4] = pack_bf16(g[0], g[1]);
+          w[16 * c + 2 * j4 + 1] = pack_bf16(g[2], g[3]);
+        }
+      }
+      tmem_st32(tP, w);  // packed dS^T
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(ds_ready);
+      BTRACE(5, it);
+      if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+    }
+    dkdv_epilogue(a, tmem, lane_off, hf, k, row_ok, kvh, it, acc_done);
+  }
+  BTRACE_FINISH;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // dQ (v2): one CTA per (query tile, query head); items = 64-key half tiles.
 // kTmemA: Q and dO, the A operands of every S / dP MMA of the CTA, live in
 // TMEM (columns 384 | 448, packed bf16, written once by the softmax warps), so
@@ -1395,13 +1679,20 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
                                    static_cast<int>(DQ2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV2_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(KV_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(KV_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(KV_SMEM)));
     return true;
   }();
-  // MRSP_ATTN_BWD=1: the single-buffered v1 kernels; =2: v2 with the dQ
-  // kernel's Q / dO read from shared memory (both kept for A/B)
+  // MRSP_ATTN_BWD=1: the single-buffered v1 kernels; =2: v2 (dQ with Q / dO
+  // in shared memory, dK / dV in 64-query halves); =3: v2 with the TMEM-operand
+  // dQ kernel; default 4: that dQ kernel and the v4 dK / dV kernel
   static const int version = [] {
     const char* v = std::getenv("MRSP_ATTN_BWD");
-    return v ? std::atoi(v) : 3;
+    return v ? std::atoi(v) : 4;
   }();
   (void)attr;
   // D = rowsum(dO o O) into the workspace p.D (unless the caller provides it)
@@ -1470,8 +1761,20 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
-  attn_bwd_dkdv2<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV2_SMEM, stream>>>(tqkv, t64, tdo64, tlse64,
-                                                                                  td64, a);
+  static const int bwd_poly = [] {
+    const char* v = std::getenv("MRSP_ATTN_BWD_POLY");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int n_kv_ctas = n_kt * (p.n_heads / p.q_per_kv);
+  if (version >= 4 && bwd_poly >= 12)
+    attn_bwd_dkdv4<12><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+  else if (version >= 4 && bwd_poly >= 8)
+    attn_bwd_dkdv4<8><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+  else if (version >= 4)
+    attn_bwd_dkdv4<0><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+  else
+    attn_bwd_dkdv2<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV2_SMEM, stream>>>(tqkv, t64, tdo64, tlse64,
+                                                                                    td64, a);
   count_launch();
   MRSP_CUDA(cudaGetLastError());
 }
