@@ -530,8 +530,11 @@ def backward_side_line(w, peaks):
     fl = T.step_flops(c, wb.frames, len(grp.question), list(grp.lengths), passes=1)
     attn = fl["attn_prefix"] + fl["attn_resp"]
     bwd_ms, attn_ms = prof["backward"][0], prof["attention_backward"][0]
-    # recompute (1 forward pass of the layers) + dgrad + wgrad + attention backward
-    bwd_flops = 3 * fl["linear"] + attn + 2.5 * attn + 2 * fl["lm_head"]
+    # algorithmic: dgrad + wgrad of every linear layer, the attention backward
+    # (2.5x its forward) and the LM head's two products — the checkpointing
+    # recompute of the linear layers is not counted (the attention is not
+    # recomputed when the policy pass keeps its outputs, MRSP_BWD_STASH_ATTN)
+    bwd_flops = 2 * fl["linear"] + 2.5 * attn + 2 * fl["lm_head"]
     return {"workload": name, "tokens": fl["tokens"], "wall_ms": round(wall * 1e3, 1),
             "tokens_per_s": round(fl["tokens"] / wall, 1),
             "backward_kernels_ms": round(bwd_ms, 1),
@@ -542,7 +545,8 @@ def backward_side_line(w, peaks):
                                        + prof["lm_head"][0] + prof["misc"][0], 1),
             "objective": st["objective"],
             "note": "policy-LLM gradients of the GRPO objective (exact KL, beta 0.04, clip 0.2); "
-                    "vision tower frozen; parity in tests/test_backward_transformer_gpu.py"}
+                    "vision tower frozen; backward FLOPs exclude the checkpointing recompute; "
+                    "parity in tests/test_backward_transformer_gpu.py"}
 
 
 def generation_side_line(eng, w, group, peaks, pix):
