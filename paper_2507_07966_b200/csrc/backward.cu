@@ -899,8 +899,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 // re-read the key tile for every 64 queries and are shared-memory bound,
 // profiles/r1_attention_study.md §7b). TMEM = S^T | dP^T | dV | dK (512
 // columns), like v1, which handed P^T and dS^T over together after both MMAs
-// and so serialised the softmax and the tensor core. Each ring stage has two
-// barriers: Q + lse (for S^T and P^T) and dO + D (for dP^T and dS^T).
+// and so serialised the softmax and the tensor core. P^T goes over in two
+// 32-query chunks per warpgroup, so dV starts on the first while the second is
+// exponentiated. Each ring stage has two barriers: Q + lse (for S^T and P^T)
+// and dO + D (for dP^T and dS^T).
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (P^T is the
 // MUFU-bound step on the S^T -> P^T -> dV chain).
 template <int kPoly>
@@ -918,10 +920,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* r_empty = bars + 1 + 2 * KV_RING;  // [KV_RING]
   uint64_t* s_full = bars + 1 + 3 * KV_RING;
   uint64_t* dp_full = s_full + 1;
-  uint64_t* p_ready = s_full + 2;
-  uint64_t* ds_ready = s_full + 3;
-  uint64_t* acc_done = s_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+  uint64_t* p_ready = s_full + 2;  // [2]: query columns [32 c, 32 c + 32) of each half
+  uint64_t* ds_ready = s_full + 4;
+  uint64_t* acc_done = s_full + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
   const int warp = warp_id();
   BTRACE_INIT;
@@ -964,7 +966,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 256);
+    mbar_init(&p_ready[0], 256);
+    mbar_init(&p_ready[1], 256);
     mbar_init(ds_ready, 256);
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -1053,17 +1056,23 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_commit(dp_full);
         }
         __syncwarp();
-        // dV += P^T(i) dO(i) (A: packed pairs in columns [0,32) + [64,96))
-        mbar_wait(p_ready, it & 1);
-        BTRACE(12, it);
-        tc_fence_after();
-        if (elect_one()) {
+        // dV += P^T(i) dO(i) (A: packed pairs in columns [0,32) + [64,96)), in
+        // the two chunks the softmax hands over: K steps {0,1,4,5}, {2,3,6,7}
 #pragma unroll
-          for (int kk = 0; kk < TQ / 16; ++kk)
-            mma_bf16_ts(tmem + 256, tmem + (kk / 4) * 64 + (kk % 4) * 8,
-                        sdesc_sw128_mn(do_addr + kk * 2048, CHUNK), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+        for (int c = 0; c < 2; ++c) {
+          mbar_wait(&p_ready[c], it & 1);
+          if (c == 0) BTRACE(12, it);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int kk = (k4 >> 1) * 4 + c * 2 + (k4 & 1);
+              mma_bf16_ts(tmem + 256, tmem + (kk / 4) * 64 + (kk % 4) * 8,
+                          sdesc_sw128_mn(do_addr + kk * 2048, CHUNK), idesc_o, (it > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
         BTRACE(13, it);
         prev = slot;
         if (++slot == KV_RING) { slot = 0; ph ^= 1; }
@@ -1099,7 +1108,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t w[32];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t sv[32];
+        uint32_t sv[32], wc[16];
         tmem_ld32(tS + c * 32, sv);
         tmem_ld_wait();
         const uint32_t vis = lt_bits(q_vis_end, qbase + 32 * c) & ~lt_bits(k, qbase + 32 * c);
@@ -1124,14 +1133,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             p[32 * c + j] = ((vis >> j) & 1u) ? y0 : 0.f;
             p[32 * c + j + 1] = ((vis >> (j + 1)) & 1u) ? y1 : 0.f;
           }
-          w[16 * c + 2 * j4] = pack_bf16(p[32 * c + 4 * j4], p[32 * c + 4 * j4 + 1]);
-          w[16 * c + 2 * j4 + 1] = pack_bf16(p[32 * c + 4 * j4 + 2], p[32 * c + 4 * j4 + 3]);
+          wc[2 * j4] = pack_bf16(p[32 * c + 4 * j4], p[32 * c + 4 * j4 + 1]);
+          wc[2 * j4 + 1] = pack_bf16(p[32 * c + 4 * j4 + 2], p[32 * c + 4 * j4 + 3]);
         }
+        // packed P^T of these 32 queries over columns [16 c, 16 c + 16) of the
+        // half (S^T of chunk 0 is consumed; chunk 1's S^T lies in [32, 64))
+        tmem_st16(tS + 16 * c, wc);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_ready[c]);
       }
-      tmem_st32(tS, w);  // packed P^T over this half's first 32 columns
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(p_ready);
       BTRACE(3, it);
       mbar_wait(&rd_full[slot], ph);
       mbar_wait(dp_full, it & 1);
