@@ -393,7 +393,11 @@ mrsp_status mrsp_engine_generate(mrsp_engine* e, const char* video_id, const int
  * be encoded (mrsp_engine_encode / _step). Runs the reference and policy
  * passes, the fused dual LM head, then the backward of the LM head and every
  * decoder layer (recomputed from its kept input) into fp32 gradients held by
- * the engine (mrsp_engine_save_grads). old_logprobs: sum(lengths) host floats
+ * the engine (mrsp_engine_save_grads). Memory per rank: the fp32 layer inputs
+ * (layers x shard tokens x dim x 4 bytes) and, when the largest rank's share
+ * fits in a quarter of the device, each layer's attention output and
+ * log-sum-exp so the recompute skips the attention (env MRSP_BWD_STASH_ATTN =
+ * 0 / 1: never / always; the gradients are bit-identical either way). old_logprobs: sum(lengths) host floats
  * (row-major), advantages: G host floats; stats4 (host) = {objective, mean_kl,
  * clip_fraction, token_count}; logprob_policy (host, may be NULL). Any SP
  * degree (virtual ranks, or one process per GPU on the peer-memory transport,
