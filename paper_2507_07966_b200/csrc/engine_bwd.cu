@@ -256,7 +256,9 @@ void Engine::backward_pass(int mode, const CacheEntry& emb, const int32_t* quest
   // log-sum-exp when they fit, so the layer recompute below skips the
   // attention (MRSP_BWD_STASH_ATTN=0 / 1: never / always; default: when the
   // largest rank's share is at most a quarter of the device). The decision
-  // uses only global sizes, so every process of a mesh takes the same one.
+  // uses only global sizes and the device's total memory, so every process of
+  // a mesh of identical GPUs takes the same one (the peer mesh is one node's
+  // GPUs; a rank deciding differently would not send its O rows).
   const int ld_keep = static_cast<int>((Ltot + 3) / 4 * 4);
   bool keep_attn = false;
   std::vector<size_t> o_keep_bytes(NLOC, 0);
