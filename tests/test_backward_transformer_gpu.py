@@ -71,7 +71,10 @@ def _mask(L, Lp, Lmax):
 
 
 @pytest.mark.parametrize("nq,nkv,Lp,G,Lmax", [(4, 2, 300, 3, 150), (7, 1, 517, 2, 200),
-                                              (2, 2, 128, 1, 128)])
+                                              (2, 2, 128, 1, 128),
+                                              (2, 1, 40, 2, 30),      # L = 100: one partial tile
+                                              (4, 4, 70, 5, 77),      # rows straddling tiles
+                                              (7, 1, 1300, 4, 129)])  # ring wrap, many items per CTA
 def test_attention_lse_and_backward(gpu, nq, nkv, Lp, G, Lmax):
     L = Lp + G * Lmax
     C = (nq + 2 * nkv) * 128
