@@ -1772,9 +1772,11 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
     count_launch();
     MRSP_CUDA(cudaGetLastError());
   }
+  // dK / dV v4: pairs (of 32) whose exp2 runs on the FMA pipe (8 measured 2%
+  // faster at c3 than 0 or 12, profiles/r1_attention_study.md §7c)
   static const int bwd_poly = [] {
     const char* v = std::getenv("MRSP_ATTN_BWD_POLY");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : 8;
   }();
   const int n_kv_ctas = n_kt * (p.n_heads / p.q_per_kv);
   if (version >= 4 && bwd_poly >= 12)
