@@ -905,20 +905,33 @@ __global__ void __launch_bounds__(THREADS, 1)
 // and dO + D (for dP^T and dS^T).
 // kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe (P^T is the
 // MUFU-bound step on the S^T -> P^T -> dV chain).
+// v4 shared memory: K | V, then a 3-deep Q ring and a 2-deep dO ring (Q(i) is
+// read by S^T(i) and by dK(i), which runs after S^T(i+1), so three Q tiles
+// keep the next load ahead), their lse / D rows, and the barriers: 232,192
+// bytes, i.e. no room for the usual 1 KB alignment slack — the kernel traps if
+// the dynamic shared window is not 1024-aligned.
+constexpr int V4_QR = 3, V4_DR = 2;
+constexpr int V4_OFF_K = 0, V4_OFF_V = TILE, V4_OFF_Q = 2 * TILE, V4_OFF_DO = V4_OFF_Q + V4_QR * TILE;
+constexpr int V4_OFF_LSE = V4_OFF_DO + V4_DR * TILE, V4_OFF_D = V4_OFF_LSE + V4_QR * 512;
+constexpr int V4_OFF_BAR = V4_OFF_D + V4_DR * 512;
+constexpr size_t V4_SMEM = V4_OFF_BAR + 256;
+static_assert(V4_SMEM <= 232448, "v4 dK / dV shared memory");
+
 template <int kPoly>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dkdv4(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                    const __grid_constant__ CUtensorMap tmLSE, const __grid_constant__ CUtensorMap tmD,
                    BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KV_OFF_BAR);
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem) & 1023u) __trap();  // the layout has no alignment slack
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + V4_OFF_BAR);
   uint64_t* kv_full = bars;
-  uint64_t* rq_full = bars + 1;               // [KV_RING] Q + lse landed
-  uint64_t* rd_full = bars + 1 + KV_RING;     // [KV_RING] dO + D landed
-  uint64_t* r_empty = bars + 1 + 2 * KV_RING;  // [KV_RING]
-  uint64_t* s_full = bars + 1 + 3 * KV_RING;
+  uint64_t* rq_full = bars + 1;                    // [V4_QR] Q + lse landed
+  uint64_t* rq_empty = rq_full + V4_QR;            // [V4_QR] Q read by S^T and dK
+  uint64_t* rd_full = rq_empty + V4_QR;            // [V4_DR] dO + D landed
+  uint64_t* rd_empty = rd_full + V4_DR;            // [V4_DR] dO read by dP^T and dV
+  uint64_t* s_full = rd_empty + V4_DR;
   uint64_t* dp_full = s_full + 1;
   uint64_t* p_ready = s_full + 2;  // [2]: query columns [32 c, 32 c + 32) of each half
   uint64_t* ds_ready = s_full + 4;
@@ -959,10 +972,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tmLSE);
     tma_prefetch_desc(&tmD);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < KV_RING; ++s) {
+    for (int s = 0; s < V4_QR; ++s) {
       mbar_init(&rq_full[s], 1);
+      mbar_init(&rq_empty[s], 1);
+    }
+    for (int s = 0; s < V4_DR; ++s) {
       mbar_init(&rd_full[s], 1);
-      mbar_init(&r_empty[s], 1);
+      mbar_init(&rd_empty[s], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
@@ -984,32 +1000,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (elect_one()) {
         mbar_arrive_expect_tx(kv_full, 2 * TILE);
         for (int c = 0; c < 2; ++c) {
-          tma_load_2d(smem + KV_OFF_K + c * CHUNK, &tmQKV, kv_full, a.k_col0 + kvh * HD + c * 64, k0);
-          tma_load_2d(smem + KV_OFF_V + c * CHUNK, &tmQKV, kv_full, a.v_col0 + kvh * HD + c * 64, k0);
+          tma_load_2d(smem + V4_OFF_K + c * CHUNK, &tmQKV, kv_full, a.k_col0 + kvh * HD + c * 64, k0);
+          tma_load_2d(smem + V4_OFF_V + c * CHUNK, &tmQKV, kv_full, a.v_col0 + kvh * HD + c * 64, k0);
         }
-        int slot = 0;
-        uint32_t ph = 0;
+        int qs = 0, ds = 0;
+        uint32_t qph = 0, dph = 0;
         for (Items t = items_begin(); t.qt < qt_hi; items_next(t)) {
           const int qt = t.qt, h = kvh * a.q_per_kv + t.hh;
-          mbar_wait(&r_empty[slot], ph ^ 1);
+          mbar_wait(&rq_empty[qs], qph ^ 1);
           BTRACE(20, qt);
-          uint8_t* st = smem + KV_OFF_RING + slot * KV_STAGE;
-          mbar_arrive_expect_tx(&rq_full[slot], TILE + 512);
+          mbar_arrive_expect_tx(&rq_full[qs], TILE + 512);
           for (int c = 0; c < 2; ++c)
-            tma_load_2d(st + c * CHUNK, &tmQKV, &rq_full[slot], a.q_col0 + h * HD + c * 64, qt * TQ);
-          tma_load_2d(st + 2 * TILE, &tmLSE, &rq_full[slot], qt * TQ, h);
-          mbar_arrive_expect_tx(&rd_full[slot], TILE + 512);
+            tma_load_2d(smem + V4_OFF_Q + qs * TILE + c * CHUNK, &tmQKV, &rq_full[qs],
+                        a.q_col0 + h * HD + c * 64, qt * TQ);
+          tma_load_2d(smem + V4_OFF_LSE + qs * 512, &tmLSE, &rq_full[qs], qt * TQ, h);
+          mbar_wait(&rd_empty[ds], dph ^ 1);
+          mbar_arrive_expect_tx(&rd_full[ds], TILE + 512);
           for (int c = 0; c < 2; ++c)
-            tma_load_2d(st + TILE + c * CHUNK, &tmDO, &rd_full[slot], h * HD + c * 64, qt * TQ);
-          tma_load_2d(st + 2 * TILE + 512, &tmD, &rd_full[slot], qt * TQ, h);
-          if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+            tma_load_2d(smem + V4_OFF_DO + ds * TILE + c * CHUNK, &tmDO, &rd_full[ds], h * HD + c * 64,
+                        qt * TQ);
+          tma_load_2d(smem + V4_OFF_D + ds * 512, &tmD, &rd_full[ds], qt * TQ, h);
+          if (++qs == V4_QR) { qs = 0; qph ^= 1; }
+          if (++ds == V4_DR) { ds = 0; dph ^= 1; }
         }
       }
     } else if (warp == 1) {
       const uint32_t idesc_s = idesc_bf16_f32(TK, TQ);
       const uint32_t idesc_o = idesc_bf16_f32_bmn(TK, HD);
-      const uint32_t k_addr = smem_u32(smem + KV_OFF_K), v_addr = smem_u32(smem + KV_OFF_V);
-      const uint32_t ring = smem_u32(smem + KV_OFF_RING);
+      const uint32_t k_addr = smem_u32(smem + V4_OFF_K), v_addr = smem_u32(smem + V4_OFF_V);
+      const uint32_t qring = smem_u32(smem + V4_OFF_Q), dring = smem_u32(smem + V4_OFF_DO);
       mbar_wait(kv_full, 0);
       // dK += dS^T(j) Q(j) (A: packed pairs in columns [128,160) + [192,224)),
       // then the ring slot of item j is free
@@ -1017,23 +1036,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(ds_ready, j & 1);
         BTRACE(14, j);
         tc_fence_after();
-        const uint32_t q_addr = ring + jslot * KV_STAGE;
+        const uint32_t q_addr = qring + jslot * TILE;
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < TQ / 16; ++kk)
             mma_bf16_ts(tmem + 384, tmem + 128 + (kk / 4) * 64 + (kk % 4) * 8,
                         sdesc_sw128_mn(q_addr + kk * 2048, CHUNK), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&r_empty[jslot]);
+          mma_commit(&rq_empty[jslot]);
         }
         __syncwarp();
       };
-      int slot = 0, prev = 0, it = 0;
-      uint32_t ph = 0;
+      int qs = 0, ds = 0, prev = 0, it = 0;
+      uint32_t qph = 0, dph = 0;
       for (Items t = items_begin(); t.qt < qt_hi; items_next(t), ++it) {
-        const uint32_t q_addr = ring + slot * KV_STAGE, do_addr = q_addr + TILE;
+        const uint32_t q_addr = qring + qs * TILE, do_addr = dring + ds * TILE;
         // S^T(i) overwrites P^T(i-1) and dP^T(i) overwrites dS^T(i-1): both
         // read by MMAs issued earlier, and the tensor pipe runs in issue order
-        mbar_wait(&rq_full[slot], ph);
+        mbar_wait(&rq_full[qs], qph);
         BTRACE(10, it);
         tc_fence_after();
         if (elect_one()) {
@@ -1045,7 +1064,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         if (it > 0) issue_dk(it - 1, prev);
-        mbar_wait(&rd_full[slot], ph);
+        mbar_wait(&rd_full[ds], dph);
         BTRACE(11, it);
         tc_fence_after();
         if (elect_one()) {
@@ -1073,9 +1092,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           __syncwarp();
         }
+        if (elect_one()) mma_commit(&rd_empty[ds]);  // dO(i) read by dP^T(i) and dV(i)
+        __syncwarp();
         BTRACE(13, it);
-        prev = slot;
-        if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+        prev = qs;
+        if (++qs == V4_QR) { qs = 0; qph ^= 1; }
+        if (++ds == V4_DR) { ds = 0; dph ^= 1; }
       }
       if (it > 0) issue_dk(it - 1, prev);
       if (elect_one()) mma_commit(acc_done);
@@ -1092,15 +1114,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float sl2 = a.scale_log2;
     const int q_vis_end = !row_ok ? 0 : k < a.Lp ? a.L : min(a.L, a.Lp + (seg_of(k, m) + 1) * a.Lmax);
     const uint32_t tS = tmem + lane_off + hf * 64, tP = tmem + lane_off + 128 + hf * 64;
-    int slot = 0, it = 0;
-    uint32_t ph = 0;
+    int qs = 0, ds = 0, it = 0;
+    uint32_t qph = 0, dph = 0;
     for (Items t = items_begin(); t.qt < qt_hi; items_next(t), ++it) {
       const int qbase = t.qt * TQ + hf * 64;
-      const float4* st_lse =
-          reinterpret_cast<const float4*>(smem + KV_OFF_RING + slot * KV_STAGE + 2 * TILE) + hf * 16;
-      const float4* st_d = st_lse + 32;
+      const float4* st_lse = reinterpret_cast<const float4*>(smem + V4_OFF_LSE + qs * 512) + hf * 16;
+      const float4* st_d = reinterpret_cast<const float4*>(smem + V4_OFF_D + ds * 512) + hf * 16;
       float p[64];
-      mbar_wait(&rq_full[slot], ph);
+      mbar_wait(&rq_full[qs], qph);
       BTRACE(0, it);
       mbar_wait(s_full, it & 1);
       BTRACE(1, it);
@@ -1144,7 +1165,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive(&p_ready[c]);
       }
       BTRACE(3, it);
-      mbar_wait(&rd_full[slot], ph);
+      mbar_wait(&rd_full[ds], dph);
       mbar_wait(dp_full, it & 1);
       BTRACE(4, it);
       tc_fence_after();
@@ -1170,7 +1191,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       mbar_arrive(ds_ready);
       BTRACE(5, it);
-      if (++slot == KV_RING) { slot = 0; ph ^= 1; }
+      if (++qs == V4_QR) { qs = 0; qph ^= 1; }
+      if (++ds == V4_DR) { ds = 0; dph ^= 1; }
     }
     dkdv_epilogue(a, tmem, lane_off, hf, k, row_ok, kvh, it, acc_done);
   }
@@ -1691,11 +1713,11 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(KV_SMEM)));
+                                   static_cast<int>(V4_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(KV_SMEM)));
+                                   static_cast<int>(V4_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(KV_SMEM)));
+                                   static_cast<int>(V4_SMEM)));
     return true;
   }();
   // MRSP_ATTN_BWD=1: the single-buffered v1 kernels; =2: v2 (dQ with Q / dO
@@ -1780,11 +1802,11 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   }();
   const int n_kv_ctas = n_kt * (p.n_heads / p.q_per_kv);
   if (version >= 4 && bwd_poly >= 12)
-    attn_bwd_dkdv4<12><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+    attn_bwd_dkdv4<12><<<n_kv_ctas, THREADS, V4_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
   else if (version >= 4 && bwd_poly >= 8)
-    attn_bwd_dkdv4<8><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+    attn_bwd_dkdv4<8><<<n_kv_ctas, THREADS, V4_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
   else if (version >= 4)
-    attn_bwd_dkdv4<0><<<n_kv_ctas, THREADS, KV_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
+    attn_bwd_dkdv4<0><<<n_kv_ctas, THREADS, V4_SMEM, stream>>>(tqkv, tdo, tlse, td, a);
   else
     attn_bwd_dkdv2<<<n_kt * (p.n_heads / p.q_per_kv), THREADS, KV2_SMEM, stream>>>(tqkv, t64, tdo64, tlse64,
                                                                                     td64, a);
