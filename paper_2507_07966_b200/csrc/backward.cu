@@ -1215,7 +1215,8 @@ constexpr int DQ2_OFF_Q = 0, DQ2_OFF_DO = TILE, DQ2_OFF_RING = 2 * TILE;
 constexpr int DQ2_OFF_BAR = DQ2_OFF_RING + DQ2_RING * DQ2_STAGE;
 constexpr size_t DQ2_SMEM = 1024 + DQ2_OFF_BAR + 256;
 
-template <bool kTmemA>
+// kPoly: pairs (of every 32) whose exp2 runs on the FMA pipe.
+template <bool kTmemA, int kPoly = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_dq2(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmKV64,
                  const __grid_constant__ CUtensorMap tmDO, BwdArgs a) {
@@ -1398,14 +1399,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t w[16];
 #pragma unroll
       for (int j2 = 0; j2 < 16; ++j2) {
-        float g[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = 2 * j2 + e;
-          const float p = ((vis >> j) & 1u) ? exp2_mufu(__uint_as_float(sv[j]) * sl2 - lse) : 0.f;
-          g[e] = p * (__uint_as_float(dv[j]) - Dq);
+        const int j = 2 * j2;
+        float x0, x1, y0, y1;
+        ffma2(x0, x1, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]), sl2, sl2, -lse, -lse);
+        if (poly_pair<kPoly>(j2 + 16 * hf)) {
+          exp2_poly2(x0, x1, y0, y1);
+        } else {
+          y0 = exp2_mufu(x0);
+          y1 = exp2_mufu(x1);
         }
-        w[j2] = pack_bf16(g[0], g[1]);
+        const float p0 = ((vis >> j) & 1u) ? y0 : 0.f, p1 = ((vis >> (j + 1)) & 1u) ? y1 : 0.f;
+        float g0, g1;
+        fsub2(g0, g1, __uint_as_float(dv[j]), __uint_as_float(dv[j + 1]), Dq, Dq);
+        fmul2(g0, g1, p0, p1, g0, g1);
+        w[j2] = pack_bf16(g0, g1);
       }
       tmem_st16(tb + hf * 32, w);
       tmem_st_wait();
@@ -1710,6 +1717,10 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
                                    static_cast<int>(DQ2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(DQ2_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(DQ2_SMEM)));
+    MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dq2<true, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(DQ2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(KV2_SMEM)));
     MRSP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv4<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1787,7 +1798,15 @@ void attention_bwd(const AttnBwdParams& p, cudaStream_t stream) {
   CUtensorMap tlse64 = make_tmap_f32_2d(p.lse, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   CUtensorMap td64 = make_tmap_f32_2d(p.D, p.n_heads, p.L, p.ld_stat, 1, 64, CU_TENSOR_MAP_SWIZZLE_NONE);
   if (n_tiles > 0) {
-    if (version >= 3)
+    static const int dq_poly = [] {
+      const char* v = std::getenv("MRSP_ATTN_BWD_DQ_POLY");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (version >= 3 && dq_poly >= 12)
+      attn_bwd_dq2<true, 12><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
+    else if (version >= 3 && dq_poly >= 8)
+      attn_bwd_dq2<true, 8><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
+    else if (version >= 3)
       attn_bwd_dq2<true><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
     else
       attn_bwd_dq2<false><<<n_tiles * p.n_heads, THREADS, DQ2_SMEM, stream>>>(tqkv, t64, tdo, a);
