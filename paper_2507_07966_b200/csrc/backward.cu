@@ -100,18 +100,21 @@ constexpr int kBTraceCap = 4096;
 __device__ uint64_t g_bwd_trace[12][kBTraceCap];
 __device__ int g_bwd_trace_n[12];
 __device__ int g_bwd_trace_cta;
-#define BTRACE_INIT int btrace_n = 0
+__device__ int g_bwd_trace_kernel;  // 0: dK / dV, 1: dQ
+#define BTRACE_INIT(kid) \
+  const bool btrace_on = blockIdx.x == g_bwd_trace_cta && g_bwd_trace_kernel == (kid); \
+  int btrace_n = 0
 #define BTRACE(ev, it)                                                                            \
   do {                                                                                            \
-    if (blockIdx.x == g_bwd_trace_cta && (threadIdx.x & 31) == 0 && btrace_n < kBTraceCap)        \
+    if (btrace_on && (threadIdx.x & 31) == 0 && btrace_n < kBTraceCap)                            \
       g_bwd_trace[threadIdx.x >> 5][btrace_n++] = (static_cast<uint64_t>(ev) << 56) |              \
                                                   (static_cast<uint64_t>((it) & 0xffffff) << 32) | \
                                                   static_cast<uint32_t>(clock());                 \
   } while (0)
 #define BTRACE_FINISH \
-  if (blockIdx.x == g_bwd_trace_cta && (threadIdx.x & 31) == 0) g_bwd_trace_n[threadIdx.x >> 5] = btrace_n
+  if (btrace_on && (threadIdx.x & 31) == 0) g_bwd_trace_n[threadIdx.x >> 5] = btrace_n
 #else
-#define BTRACE_INIT
+#define BTRACE_INIT(kid)
 #define BTRACE(ev, it) \
   do {                 \
   } while (0)
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
   const int warp = warp_id();
-  BTRACE_INIT;
+  BTRACE_INIT(0);
   const MaskDev m = mask_of(a);
   const int n_kt = (a.L + TK - 1) / TK;
   const int kvh = blockIdx.x / n_kt;
@@ -939,7 +942,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
   const int warp = warp_id();
-  BTRACE_INIT;
+  BTRACE_INIT(0);
   const MaskDev m = mask_of(a);
   const int n_kt = (a.L + TK - 1) / TK;
   const int kvh = blockIdx.x / n_kt;
@@ -1233,6 +1236,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
   const int warp = warp_id();
+  BTRACE_INIT(1);
   const MaskDev m = mask_of(a);
   const int n_qt = (a.L + TQ - 1) / TQ;
   const int n_tiles = a.row_parts > 1 ? 2 * a.n_local_blocks : n_qt;
@@ -1338,6 +1342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       auto issue_acc = [&](int it, int slot) {
         mbar_wait(&ds_full[it & 1], (it >> 1) & 1);
+        BTRACE(12, it);
         tc_fence_after();
         const uint32_t kh = ring + slot * DQ2_STAGE;
         if (elect_one()) {
@@ -1353,9 +1358,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb), ++it) {
         mbar_wait(&r_full[slot], ph);
+        BTRACE(10, it);
         tc_fence_after();
         issue_sdp(it, slot);
+        BTRACE(11, it);
         if (it > 0) issue_acc(it - 1, prev);
+        if (it > 0) BTRACE(13, it - 1);
         prev = slot;
         if (++slot == DQ2_RING) { slot = 0; ph ^= 1; }
       }
@@ -1388,7 +1396,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0;
     for (int kb = kb_first(); kb < r2_hi; kb = kb_next(kb), ++it) {
       const uint32_t tb = tmem + lane_off + (it & 1) * 128;
+      BTRACE(0, it);
       mbar_wait(&s_full[it & 1], (it >> 1) & 1);
+      BTRACE(1, it);
       tc_fence_after();
       uint32_t sv[32], dv[32];
       tmem_ld32(tb + hf * 32, sv);
@@ -1414,10 +1424,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         fmul2(g0, g1, p0, p1, g0, g1);
         w[j2] = pack_bf16(g0, g1);
       }
+      BTRACE(3, it);
       tmem_st16(tb + hf * 32, w);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&ds_full[it & 1]);
+      BTRACE(4, it);
     }
     __nv_bfloat16* out = a.dqkv + static_cast<size_t>(q) * a.ld_dqkv + a.q_col0 + h * HD + hf * 64;
     if (it > 0) {
@@ -1442,6 +1454,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < 64; c += 8) *reinterpret_cast<uint4*>(out + c) = make_uint4(0, 0, 0, 0);
     }
   }
+  BTRACE_FINISH;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

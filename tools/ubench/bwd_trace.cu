@@ -2,7 +2,7 @@
 // Builds csrc/backward.cu with MRSP_BWD_TRACE, runs the forward (from the
 // library, for a real log-sum-exp) and the backward on a c2-shaped layer, and
 // prints per event the clock() stamps of lane 0 of each warp of CTA `cta`.
-//   bwd_trace [L Lp Lmax cta]
+//   bwd_trace [L Lp Lmax cta kernel]   (kernel 0: dK / dV, 1: dQ)
 // Events: TMA warp 20 (ring slot free); MMA warp 10 (stage landed), 11 (S / dP
 // issued), 12 (dS of the previous item ready), 13 (its dV / dK issued);
 // softmax warps 0 (wait S), 1 (S / dP ready), 2 (loaded), 3 (P / dS computed),
@@ -19,6 +19,7 @@ int main(int argc, char** argv) {
   const int Lp = argc > 2 ? atoi(argv[2]) : 16421;
   const int Lmax = argc > 3 ? atoi(argv[3]) : 1024;
   const int cta = argc > 4 ? atoi(argv[4]) : 8;
+  const int kernel = argc > 5 ? atoi(argv[5]) : 0;  // 0: dK / dV, 1: dQ
   const int nq = 28, nkv = 4, C = (nq + 2 * nkv) * 128, Cq = nq * 128;
   std::vector<__nv_bfloat16> h(static_cast<size_t>(L) * C), hd(static_cast<size_t>(L) * Cq);
   uint32_t x = 12345;
@@ -47,6 +48,7 @@ int main(int argc, char** argv) {
   fp.lse_ld = ld;
   mrsp::attention_fwd(fp, 0);
   cudaMemcpyToSymbol(mrsp::g_bwd_trace_cta, &cta, sizeof(int));
+  cudaMemcpyToSymbol(mrsp::g_bwd_trace_kernel, &kernel, sizeof(int));
   mrsp::AttnBwdParams bp{qkv, C, 0, nq * 128, (nq + nkv) * 128, o, Cq, dO, Cq, lse, D, ld, dqkv, C,
                          L, nq, nq / nkv, 0.08838834764831845f, Lp, Lmax};
   for (int rep = 0; rep < 3; ++rep) {
