@@ -499,14 +499,14 @@ def backward_side_line(w, peaks):
     prefill (mrsp_engine_grpo_backward: reference + policy passes keeping the
     layer inputs, fused dual LM head, then the backward of the LM head and of
     every decoder layer recomputed from its kept input), on the same workload
-    when its SP = 1 working set fits next to the gradients (c1-c3), else on c3
-    (28 layers, 65K-token prompt). Wall time of the call, device time of the
+    when its SP = 1 working set fits next to the gradients (c1-c4), else on c4
+    (c5's 108 GB of fp32 layer inputs need SP > 1 across GPUs). Wall time of the call, device time of the
     backward kernels, and the attention-backward kernels' algorithmic TFLOP/s
     (2.5x the forward attention FLOPs: S, dP, dQ, dK, dV)."""
     import numpy as np
     from oracle import transformer as T
     from paper_2507_07966_b200 import engine as E
-    name = w.name if w.name in ("c1", "c2", "c3") else "c3"
+    name = w.name if w.name in ("c1", "c2", "c3", "c4") else "c4"
     wb = E.workloads()[name]
     c = T.Cfg.from_any(wb.cfg)
     eng = E.Engine(wb.cfg, sp=1)
